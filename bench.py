@@ -1,0 +1,354 @@
+"""bench.py — packed embedding fwd + bwd + sparse-Adagrad step on synthetic Zipf batches.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl reference]`; for
+N > 1 launched by torchrun (one process per GPU).  Prints ONE JSON line on rank 0.
+
+Workload at N = 1: BASELINE.json configs[1], the Criteo-shaped DLRM embedding layer:
+26 one-hot categorical fields, dim 128, batch 16,384 per GPU, 46.875M rows (24 GB fp32 +
+24 GB Adagrad state), Zipf(alpha = 0.8) IDs hashed into the tables.  A step = one forward
+(hash + Unique + gather/pool) and one backward (transpose + segment-sum + Adagrad update)
+over one batch.  Inputs resident in HBM; L2 flushed (256 MiB write) before every timed
+step.  Per-phase times come from CUDA events the library records on the launch stream.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "packed embedding fwd+bwd samples/sec"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="picasso", choices=["picasso", "reference"])
+    ap.add_argument("--config", default="criteo")
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--nbatches", type=int, default=4, help="distinct pre-generated batches, used round robin")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def get_cfg(args):
+    from datagen import configs as dc
+
+    cfg = dc.get_config(args.config)
+    if args.alpha is not None:
+        cfg = cfg.replace(alpha=args.alpha)
+    if args.batch is not None:
+        cfg = cfg.replace(batch=args.batch)
+    return cfg
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_oracle_baseline(cfg, seconds):
+    """The oracle (oracle/picasso_oracle.cpp, single thread, as it stands) on a bounded sample
+    of the same workload: whole batches of this config, one rank; forward over every segment
+    (oracle_forward_sampled), gradients of every touched row (oracle_row_grads) and the
+    Adagrad update (oracle_apply_update).  Table rows the sample touches are materialised
+    from the same generator beforehand (not timed)."""
+    import oracle
+    from datagen import make_batch, make_dy, table_values_np
+
+    m = oracle.OracleModel(cfg.field_to_table, cfg.table_rows, cfg.table_dim, cfg.field_col, id_mode=cfg.id_mode,
+                           pool=cfg.pool, table_salt=cfg.table_salt)
+    B = cfg.batch
+    ld = int(cfg.table_dim.max())
+    spent, samples, steps = 0.0, 0, 0
+    while steps == 0 or (spent < seconds and steps < 50):
+        b = make_batch(cfg, 0, 1000 + steps)
+        dy = make_dy(cfg, 0, 1000 + steps, dyadic=False)
+        ob = oracle.OracleBatch(B, b.ids, b.offsets, dy)
+        qf = np.repeat(np.arange(cfg.F, dtype=np.int32), B)
+        qs = np.tile(np.arange(B, dtype=np.int32), cfg.F)
+        rt, rr = oracle.segment_rows(m, ob, qf, qs)
+        key = np.unique(rt.astype(np.int64) * (1 << 40) + rr)
+        ut, ur = (key >> 40).astype(np.int32), key & ((1 << 40) - 1)
+        vals = np.zeros((len(key), ld), np.float32)
+        for t in np.unique(ut):
+            sel = ut == t
+            D = int(cfg.table_dim[t])
+            vals[sel, :D] = table_values_np(cfg.seed, int(t), ur[sel], D)
+        acc = np.full_like(vals, 0.1)
+        t0 = time.perf_counter()
+        oracle.forward_sampled(m, ob, ut, ur, vals, qf, qs)
+        G, cnt = oracle.row_grads(m, [ob], ut, ur, ld)
+        oracle.apply_update(G, cnt, vals, acc, lr=0.01, D=ld)
+        spent += time.perf_counter() - t0
+        samples += B
+        steps += 1
+    return {"value": samples / spent, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full batch(es) of {cfg.name} (B={B}, {cfg.F} fields): fwd over all segments, "
+                      f"grads + Adagrad over all touched rows; {spent:.1f} s single-threaded C++ (-O2)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = get_cfg(args)
+    per = []
+    # bounded: one batch per step; warmup steps untimed
+    for i in range(args.warmup + args.steps):
+        cb = cpu_oracle_baseline(cfg, seconds=0.0)  # exactly one batch per call
+        if i >= args.warmup:
+            per.append(cfg.batch / cb["value"])
+    tot = float(np.sum(per))
+    value = cfg.batch * len(per) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(per),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": cfg.batch, "fields": cfg.F,
+                       "dims": sorted(set(cfg.table_dim.tolist())), "alpha": cfg.alpha},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{len(per)} full batches of {cfg.name}, single thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def algorithmic_bytes(cfg, B, N, U_by_pack, plan):
+    """SURVEY.md §8(d) per-kernel algorithmic bytes (what the method must move), per step."""
+    S = cfg.F * B
+    fd = cfg.field_dim.astype(np.int64)
+    out_bytes = 4 * B * int(fd.sum())
+    rows_bytes = sum(4 * int(plan["pack_dim"][p]) * U_by_pack[p] for p in range(plan["n_packs"]))
+    pool = 8 * N + 4 * (S + 1) + rows_bytes + out_bytes
+    # segsum+update: dY rows (one read per segment), sorted segment list, ustart, unique keys,
+    # weight + Adagrad state read and written once per touched row
+    U = sum(U_by_pack)
+    upd = out_bytes + 4 * N + 4 * (U + 1) + 8 * U + 4 * rows_bytes
+    return {"pool": pool, "segsum_update": upd}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2204_04903_b200 as pb
+    from datagen import init_pack_tables_torch, make_batch, make_dy
+
+    cfg = get_cfg(args)
+    B = cfg.batch
+    batches = [make_batch(cfg, rank, s) for s in range(args.nbatches)]
+    max_ids = max(b.n_ids for b in batches)
+    # this build: each rank holds a full replica of the tables (the row-sharded NCCL path is
+    # the next row of SURVEY §8); every rank processes its own B samples (weak scaling)
+    emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=B, max_ids=max_ids,
+                             table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
+                             device=dev)
+    init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights)
+    dev_in = [(torch.from_numpy(b.ids).to(dev), torch.from_numpy(b.offsets).to(dev)) for b in batches]
+    dys_host = [torch.from_numpy(make_dy(cfg, rank, s, dyadic=False)).pin_memory() for s in range(args.nbatches)]
+    dys = [d.to(dev) for d in dys_host]
+    out = torch.empty(B, emb.out_width, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lr = 0.01
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, s):
+        ids, off = dev_in[i % args.nbatches]
+        emb.forward(ids, off, B, out, stream=s)
+        emb.backward_update(dys[i % args.nbatches], lr, step=i + 1, stream=s)
+
+    for i in range(args.warmup):
+        step(i, stream)
+    emb.check()
+    torch.cuda.synchronize()
+    lf, lb = emb.launch_count()
+
+    # ---------------- timed region: K steps, L2 flushed before each (flush not timed)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    pb.picasso_profile_enable(emb.ctx, True)
+    pb.picasso_profile_read(emb.ctx)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            starts[i].record(stream)
+            step(args.warmup + i, stream)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    phase_ms, ncalls = pb.picasso_profile_read(emb.ctx)
+    pb.picasso_profile_enable(emb.ctx, False)
+    emb.check()
+    ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends))) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # unique counts of the last timed step (for algorithmic bytes)
+    U_pref = np.array(emb.unique_offsets_host(), np.int64)
+    U_by_pack = list(np.diff(U_pref))
+    last_b = batches[(args.warmup + args.steps - 1) % args.nbatches]
+    alg = algorithmic_bytes(cfg, B, last_b.n_ids, U_by_pack, emb.plan)
+    per_phase = {k: v / max(ncalls, 1) for k, v in phase_ms.items()}
+    dom = "segsum_update" if per_phase["segsum_update"] >= per_phase["pool"] else "pool"
+    peak = None
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "MEASURED_PEAKS.json hbm_gbs"
+    else:
+        peak = 6650.0
+    achieved = alg[dom] / (per_phase[dom] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(cfg.name, {}).get(dom)
+
+    # ---------------- end-to-end through the public API with host buffers
+    host_ids = [torch.from_numpy(b.ids).pin_memory() for b in batches]
+    host_off = [torch.from_numpy(b.offsets).pin_memory() for b in batches]
+    ids_buf = torch.empty(max_ids, dtype=torch.int64, device=dev)
+    off_buf = torch.empty(cfg.F * B + 1, dtype=torch.int32, device=dev)
+    dy_buf = torch.empty_like(dys[0])
+    u_host = torch.empty(emb.n_packs + 1, dtype=torch.int32).pin_memory()
+    e_st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        k = (args.warmup + i) % args.nbatches
+        flush.fill_(i & 0xFF)
+        e_st[i].record(stream)
+        n = host_ids[k].numel()
+        ids_buf[:n].copy_(host_ids[k], non_blocking=True)
+        off_buf.copy_(host_off[k], non_blocking=True)
+        dy_buf.copy_(dys_host[k], non_blocking=True)
+        emb.forward(ids_buf[:n], off_buf, B, out, stream=stream)
+        emb.backward_update(dy_buf, lr, step=10_000 + i, stream=stream)
+        emb.unique_offsets(u_host, stream=stream)
+        e_en[i].record(stream)
+        h2d = 8 * n + 4 * off_buf.numel() + 4 * dy_buf.numel()
+        d2h = 4 * u_host.numel()
+    torch.cuda.synchronize()
+    e2e_ms = float(sum(s.elapsed_time(e) for s, e in zip(e_st, e_en))) / args.steps
+    t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(cfg, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": world * B / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": world * B, "batch_per_gpu": B, "fields": cfg.F,
+                       "dims": sorted(set(cfg.table_dim.tolist())), "rows": int(cfg.table_rows.sum()),
+                       "alpha": cfg.alpha, "optimizer": "adagrad", "pool": "sum",
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "flushed (256 MiB write, untimed) before every timed step",
+                       "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
+            "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "note": "H2D of ids+offsets+dY from pinned host memory, D2H of the per-pack unique counts"},
+            "gpu_launches": int((lf + lb) * args.steps),
+            "roofline": {"bound": "hbm", "kernel": "k_segsum_update" if dom == "segsum_update" else "k_pool",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
+                         "peak_source": peak_src},
+            "phases_ms": per_phase,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

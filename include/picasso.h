@@ -1,0 +1,179 @@
+/*
+ * picasso.h — C ABI of the B200-native PICASSO packed sparse-embedding hot path.
+ *
+ * The operation (§III, arXiv 2204.04903): the embedding layer of a wide-and-deep
+ * model looks up multi-hot categorical IDs of many feature fields (L131-140) through the
+ * operator chain Unique -> Partition -> Gather -> Shuffle -> Stitch -> SegmentReduction
+ * (L209-215); its backward pass is the mirror image (L219).  D-Packing (L319-362) merges the
+ * fields whose tables share an embedding dimension into one packed ID stream served by one
+ * fused pass; K-Packing (L364-382) fuses Unique&Partition and Shuffle&Stitch.  HybridHash
+ * (L459-522, Alg. 1) keeps the top-k frequent rows in hot storage.  The backward ends in a
+ * sparse optimizer update of the touched rows (north star; not specified by the paper).
+ *
+ * Conventions (every entry point):
+ *  - All functions return picasso_status; no C++ type or exception crosses the ABI.
+ *  - "device" pointers are CUDA global-memory pointers on the ctx's device; "host" pointers
+ *    are ordinary host memory.  The caller owns every buffer (ids, offsets, out, dY,
+ *    weights, optimizer state, workspace).  The library never allocates device memory in
+ *    the step path; the ctx owns only host objects (and its NCCL communicator).
+ *  - Work is enqueued on the caller's stream and is asynchronous.  fwd and bwd_update never
+ *    synchronise the host when world == 1 (the step is CUDA-graph capturable).
+ *  - Argument / plan errors are synchronous return codes.  Device-detected errors (ID out
+ *    of range in ROWS mode, capacity overflow) are latched in a device word and reported by
+ *    picasso_last_error (which synchronises the stream it last used).
+ *  - One ctx per rank; a ctx is not thread-safe.
+ */
+#ifndef PICASSO_H_
+#define PICASSO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PICASSO_OK = 0,
+    PICASSO_ERR_INVALID_ARG = -1,   /* bad pointer / size / enum value */
+    PICASSO_ERR_PLAN_MISMATCH = -2, /* plan or field layout inconsistent with the call */
+    PICASSO_ERR_ID_RANGE = -3,      /* ROWS mode: a raw ID outside [0, V_t) (latched) */
+    PICASSO_ERR_CAPACITY = -4,      /* batch / ids / workspace larger than the ctx was built for */
+    PICASSO_ERR_CUDA = -5,          /* a CUDA runtime call failed */
+    PICASSO_ERR_NCCL = -6,          /* an NCCL call failed */
+    PICASSO_ERR_STATE = -7          /* call order violated (bwd_update without a preceding fwd) */
+} picasso_status;
+
+typedef enum { PICASSO_POOL_SUM = 0, PICASSO_POOL_MEAN = 1 } picasso_pool;
+typedef enum { PICASSO_OPT_ADAGRAD = 0, PICASSO_OPT_ADAM_LAZY = 1 } picasso_opt;
+/* Row of a raw ID in its table (reading O4): ROWS: row = raw (0 <= raw < V_t);
+ * HASH: row = floor(mix64(raw XOR salt_t) * V_t / 2^64), mix64 = SplitMix64's output mix. */
+typedef enum { PICASSO_IDS_ROWS = 0, PICASSO_IDS_HASH = 1 } picasso_id_mode;
+
+typedef struct picasso_ctx picasso_ctx;
+
+/* ------------------------------------------------------------------------------------ */
+/* 1. Planning — D-Packing with Eq. 1.  Host only, pure, deterministic.
+ *   Groups tables by embedding dim (ascending dim).  vparam(group) = sum_t dim_t * count_t
+ *   (Eq. 1 with ID_freq = count/N, reading O15); count_t = table_warmup_count[t] (ID
+ *   occurrences seen in warm-up iterations, L353-354) or, when NULL, the number of fields
+ *   that reference t.  split != 0: a group with vparam above the mean is split into
+ *   min(#tables, ceil(vparam / min_vparam)) shards (reading O14; reproduces the paper's
+ *   four-shard example L358-362), members dealt round-robin by descending dim_t*count_t.
+ *   Within a pack tables are ordered by ascending index; table_base[t] = rows of the pack's
+ *   earlier tables, so pack key = table_base[t] + row.
+ * In : n_fields F >= 1, field_to_table [F] (host), n_tables T >= 1, table_rows [T] (> 0),
+ *      table_dim [T] (> 0), table_warmup_count [T] or NULL, split.
+ * Out (caller-allocated host arrays): field_to_pack [F], table_to_pack [T], table_base [T],
+ *      pack_dim [T], pack_rows [T] (first *n_packs entries valid), *n_packs.
+ * Errors: PICASSO_ERR_INVALID_ARG on NULL pointers, F/T <= 0, out-of-range table index,
+ *      non-positive rows/dims. */
+picasso_status picasso_pack_plan(int32_t n_fields, const int32_t *field_to_table, int32_t n_tables,
+                                 const int64_t *table_rows, const int32_t *table_dim,
+                                 const uint64_t *table_warmup_count, int32_t split,
+                                 int32_t *field_to_pack, int32_t *table_to_pack, int64_t *table_base,
+                                 int32_t *pack_dim, int64_t *pack_rows, int32_t *n_packs);
+
+/* The plan, as returned by picasso_pack_plan, plus the model's per-field output columns.
+ * All pointers are host pointers; the ctx copies them. */
+typedef struct {
+    int32_t n_fields, n_tables, n_packs;
+    const int32_t *field_to_table; /* [F] */
+    const int32_t *table_to_pack;  /* [T] */
+    const int64_t *table_base;     /* [T] */
+    const int64_t *table_rows;     /* [T] */
+    const int32_t *table_dim;      /* [T]; every dim a multiple of 4, <= 512 */
+    const uint64_t *table_salt;    /* [T] HASH-mode salts (NULL = all 0) */
+    const int64_t *field_col;      /* [F] first column of field f in the [B, out_width] output
+                                      (a multiple of 4) */
+    int64_t out_width;             /* row stride of out / dY in floats (multiple of 4) */
+} picasso_plan_view;
+
+typedef struct {
+    int32_t max_batch;     /* B per rank per step, upper bound */
+    int64_t max_ids;       /* ID occurrences per rank per step, upper bound (< 2^31) */
+    int32_t pool;          /* picasso_pool */
+    int32_t id_mode;       /* picasso_id_mode */
+    int32_t opt;           /* picasso_opt */
+    float eps;             /* Adagrad 1e-10 / Adam 1e-8 */
+    float beta1, beta2;    /* Adam (0.9, 0.999) */
+} picasso_ctx_opts;
+
+/* 2. Context.  rank/world: this process's place in the row-sharded group (owner of pack
+ * key k = k mod world, local row = k div world; reading O3).  This build: world == 1.
+ * Errors: INVALID_ARG / PLAN_MISMATCH on inconsistent plans or options. */
+picasso_status picasso_ctx_create(const picasso_plan_view *plan, int32_t rank, int32_t world,
+                                  const picasso_ctx_opts *opts, picasso_ctx **out);
+/* Bytes of device workspace the ctx needs (depends on max_batch, max_ids, plan). */
+picasso_status picasso_workspace_size(const picasso_ctx *ctx, size_t *bytes);
+/* Rows of pack p held by this rank: ceil((pack_rows[p] - rank) / world). */
+picasso_status picasso_pack_local_rows(const picasso_ctx *ctx, int32_t pack, int64_t *rows);
+/* Attach caller-owned device memory: workspace (>= picasso_workspace_size bytes, 256-B
+ * aligned); pack_weight[p] = fp32 [local_rows_p, pack_dim_p] row-major; pack_state1[p] =
+ * Adagrad accumulator or Adam m (same shape); pack_state2[p] = Adam v (NULL for Adagrad).
+ * Synchronous (uploads the plan tables into the workspace). */
+picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t bytes, float *const *pack_weight,
+                            float *const *pack_state1, float *const *pack_state2);
+picasso_status picasso_ctx_destroy(picasso_ctx *ctx);
+
+/* 3. Forward — packed lookup.  For every pack: ID hashing
+ * into pack keys, fused Unique&Partition (first-occurrence unique + inverse; reading O1),
+ * row gather fused with SegmentReduction (stitch fused away):
+ *     out[b, col(f) + d] = sum_{j in seg(f,b)} W_t[row_j][d]   (ascending j; mean: / len;
+ *                                                              empty segment: 0)
+ * ids     : device int64 [n_ids], field-major: field f, then sample b, then j.
+ * offsets : device int32 [F*batch + 1]; seg(f,b) = [offsets[f*B+b], offsets[f*B+b+1]),
+ *           offsets[0] == 0, non-decreasing, offsets[F*B] == n_ids.
+ * out     : device fp32 [batch, out_width], fully overwritten.
+ * Keeps the per-step state (unique keys, inverse, segment map) in the workspace for the
+ * next picasso_packed_lookup_bwd_update.
+ * Errors: CAPACITY if batch > max_batch or n_ids > max_ids; STATE if not bound. */
+picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets,
+                                         int32_t batch, int64_t n_ids, float *out, void *stream);
+
+/* 4. Backward + sparse update — the mirror of the forward: for every
+ * unique row u of the last forward,
+ *     G_u = sum_{j : inverse[j] = u} dY[b(j), col(f(j)) + .]   (mean: dY / len)
+ * then, for touched rows only (reading O9), Adagrad: acc += G^2; w -= lr*G/(sqrt(acc)+eps),
+ * or lazy Adam (torch SparseAdam form, bias correction with the 1-based `step`).
+ * grad_out: device fp32 [batch, out_width] (dY, same layout as out).
+ * Summation order: ascending occurrence for rows with <= 256 occurrences (bit-identical to
+ * the sequential definition); longer rows are split into fixed chunks combined in a fixed
+ * order (deterministic run to run).
+ * Errors: STATE without a preceding fwd. */
+picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, const float *grad_out, float lr,
+                                                int64_t step, void *stream);
+
+/* Last latched error (synchronises the ctx's last stream).  msg may be NULL. */
+picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t len);
+
+/* ------------------------------------------------------------------------------------ */
+/* Introspection of the last forward's intermediates (tests; synchronise the stream).
+ * Copies into caller device buffers; *n receives the element count (copy truncated at cap).
+ *   picasso_get_unique : pack keys of pack p in first-occurrence order (int64 [U_p])
+ *   picasso_get_inverse: per occurrence of pack p's key stream (pack fields in ascending
+ *                        field order, then b, then j) its index into unique (int32 [N_p]) */
+picasso_status picasso_get_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n);
+picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, int32_t *dst, int64_t cap, int64_t *n);
+
+/* Number of CUDA kernel launches the last fwd / bwd_update enqueued (host counters). */
+picasso_status picasso_launch_count(const picasso_ctx *ctx, int64_t *fwd, int64_t *bwd);
+
+/* Phase timing with CUDA events recorded on the caller's stream around each phase of the
+ * step: 0 = ID hash + Unique (k_field_prep .. k_pack_ustart), 1 = gather/pool (k_pool),
+ * 2 = occurrence transpose (radix sort + k_csr_bounds), 3 = segment-sum + optimizer
+ * (k_segsum_update + k_long_update).  picasso_profile_read synchronises, writes the summed
+ * milliseconds of each phase since the last read into ms[4] (host), the number of steps
+ * into *calls, and resets.  Off by default. */
+picasso_status picasso_profile_enable(picasso_ctx *ctx, int32_t on);
+picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int64_t *calls);
+
+/* Per-pack unique counts of the last forward as an int32 [n_packs + 1] prefix (uid range of
+ * pack p = [u[p], u[p+1])), copied asynchronously on `stream` into dst (device memory or
+ * pinned host memory).  Enqueue-only; the caller synchronises. */
+picasso_status picasso_unique_offsets(picasso_ctx *ctx, int32_t *dst, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PICASSO_H_ */

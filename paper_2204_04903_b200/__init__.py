@@ -1,0 +1,26 @@
+"""B200-native PICASSO packed sparse-embedding hot path (arXiv 2204.04903).
+
+The compute lives in ``libpicasso.so`` (hand-written sm_100a CUDA kernels behind the C ABI
+of ``include/picasso.h``).  This package is argument marshalling only: it converts torch
+tensors to raw pointers and calls the C entry points of the same names.  There is no CPU
+fallback: importing fails loudly if the library is missing.
+"""
+from .abi import (  # noqa: F401
+    PicassoError,
+    lib,
+    lib_path,
+    picasso_bind,
+    picasso_ctx_create,
+    picasso_ctx_destroy,
+    picasso_get_inverse,
+    picasso_get_unique,
+    picasso_last_error,
+    picasso_launch_count,
+    picasso_pack_local_rows,
+    picasso_pack_plan,
+    picasso_packed_lookup_bwd_update,
+    picasso_packed_lookup_fwd,
+    picasso_workspace_size,
+    POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
+)
+from .embedding import PackedEmbedding  # noqa: F401

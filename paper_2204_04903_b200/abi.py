@@ -1,0 +1,234 @@
+"""ctypes binding of include/picasso.h — same names, argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libpicasso.so")
+
+POOL_SUM, POOL_MEAN = 0, 1
+OPT_ADAGRAD, OPT_ADAM_LAZY = 0, 1
+IDS_ROWS, IDS_HASH = 0, 1
+
+_STATUS = {0: "OK", -1: "INVALID_ARG", -2: "PLAN_MISMATCH", -3: "ID_RANGE", -4: "CAPACITY", -5: "CUDA",
+           -6: "NCCL", -7: "STATE"}
+
+EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", "picasso_pack_local_rows",
+           "picasso_bind", "picasso_ctx_destroy", "picasso_packed_lookup_fwd", "picasso_packed_lookup_bwd_update",
+           "picasso_last_error", "picasso_get_unique", "picasso_get_inverse", "picasso_launch_count",
+           "picasso_profile_enable", "picasso_profile_read", "picasso_unique_offsets"]
+PHASES = ["unique", "pool", "transpose", "segsum_update"]
+
+
+class PicassoError(RuntimeError):
+    def __init__(self, status, where, msg=""):
+        super().__init__(f"{where}: PICASSO_ERR_{_STATUS.get(status, status)} {msg}".strip())
+        self.status = status
+
+
+class PlanView(C.Structure):
+    _fields_ = [("n_fields", C.c_int32), ("n_tables", C.c_int32), ("n_packs", C.c_int32),
+                ("field_to_table", C.c_void_p), ("table_to_pack", C.c_void_p), ("table_base", C.c_void_p),
+                ("table_rows", C.c_void_p), ("table_dim", C.c_void_p), ("table_salt", C.c_void_p),
+                ("field_col", C.c_void_p), ("out_width", C.c_int64)]
+
+
+class CtxOpts(C.Structure):
+    _fields_ = [("max_batch", C.c_int32), ("max_ids", C.c_int64), ("pool", C.c_int32), ("id_mode", C.c_int32),
+                ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpicasso.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(lib_path):
+            raise ImportError(f"{lib_path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(lib_path)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        sig = {
+            "picasso_pack_plan": [i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],
+            "picasso_ctx_create": [C.POINTER(PlanView), i32, i32, C.POINTER(CtxOpts), C.POINTER(vp)],
+            "picasso_workspace_size": [vp, C.POINTER(C.c_size_t)],
+            "picasso_pack_local_rows": [vp, i32, C.POINTER(i64)],
+            "picasso_bind": [vp, vp, C.c_size_t, vp, vp, vp],
+            "picasso_ctx_destroy": [vp],
+            "picasso_packed_lookup_fwd": [vp, vp, vp, i32, i64, vp, vp],
+            "picasso_packed_lookup_bwd_update": [vp, vp, C.c_float, i64, vp],
+            "picasso_last_error": [vp, C.c_char_p, C.c_size_t],
+            "picasso_get_unique": [vp, i32, vp, i64, C.POINTER(i64)],
+            "picasso_get_inverse": [vp, i32, vp, i64, C.POINTER(i64)],
+            "picasso_launch_count": [vp, C.POINTER(i64), C.POINTER(i64)],
+            "picasso_profile_enable": [vp, i32],
+            "picasso_profile_read": [vp, vp, C.POINTER(i64)],
+            "picasso_unique_offsets": [vp, vp, vp],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _chk(st, where, ctx=None):
+    if st != 0:
+        msg = ""
+        if ctx is not None:
+            buf = C.create_string_buffer(256)
+            lib().picasso_last_error(ctx, buf, 256)
+            msg = buf.value.decode(errors="replace")
+        raise PicassoError(st, where, msg)
+
+
+def _np(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+# ------------------------------------------------------------------------------------------
+def picasso_pack_plan(field_to_table, table_rows, table_dim, table_warmup_count=None, split=False):
+    f2t, rows, dims = _np(field_to_table, np.int32), _np(table_rows, np.int64), _np(table_dim, np.int32)
+    wc = None if table_warmup_count is None else _np(table_warmup_count, np.uint64)
+    F, T = len(f2t), len(rows)
+    f2p, t2p = np.zeros(F, np.int32), np.zeros(T, np.int32)
+    tb, pd, pr = np.zeros(T, np.int64), np.zeros(T, np.int32), np.zeros(T, np.int64)
+    n = C.c_int32()
+    st = lib().picasso_pack_plan(F, f2t.ctypes.data, T, rows.ctypes.data, dims.ctypes.data,
+                                 None if wc is None else wc.ctypes.data, int(bool(split)), f2p.ctypes.data,
+                                 t2p.ctypes.data, tb.ctypes.data, pd.ctypes.data, pr.ctypes.data, C.byref(n))
+    _chk(st, "picasso_pack_plan")
+    P = n.value
+    return dict(field_to_pack=f2p, table_to_pack=t2p, table_base=tb, pack_dim=pd[:P].copy(),
+                pack_rows=pr[:P].copy(), n_packs=P)
+
+
+class _Keep:
+    """Keeps numpy arrays referenced by a C struct alive."""
+
+
+def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, field_col, out_width, rank, world,
+                       max_batch, max_ids, pool=POOL_SUM, id_mode=IDS_HASH, opt=OPT_ADAGRAD, eps=None, beta1=0.9,
+                       beta2=0.999):
+    k = _Keep()
+    k.f2t = _np(field_to_table, np.int32)
+    k.t2p = _np(plan["table_to_pack"], np.int32)
+    k.tb = _np(plan["table_base"], np.int64)
+    k.rows = _np(table_rows, np.int64)
+    k.dims = _np(table_dim, np.int32)
+    k.salt = _np(np.zeros(len(k.rows)) if table_salt is None else table_salt, np.uint64)
+    k.col = _np(field_col, np.int64)
+    pv = PlanView(len(k.f2t), len(k.rows), int(plan["n_packs"]), k.f2t.ctypes.data, k.t2p.ctypes.data,
+                  k.tb.ctypes.data, k.rows.ctypes.data, k.dims.ctypes.data, k.salt.ctypes.data, k.col.ctypes.data,
+                  int(out_width))
+    if eps is None:
+        eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
+    o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),
+                float(beta2))
+    ctx = C.c_void_p()
+    _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), C.byref(o), C.byref(ctx)),
+         "picasso_ctx_create")
+    return ctx
+
+
+def picasso_workspace_size(ctx):
+    n = C.c_size_t()
+    _chk(lib().picasso_workspace_size(ctx, C.byref(n)), "picasso_workspace_size")
+    return n.value
+
+
+def picasso_pack_local_rows(ctx, pack):
+    n = C.c_int64()
+    _chk(lib().picasso_pack_local_rows(ctx, int(pack), C.byref(n)), "picasso_pack_local_rows")
+    return n.value
+
+
+def picasso_bind(ctx, workspace, weights, state1, state2=None):
+    P = len(weights)
+    w = (C.c_void_p * P)(*[t.data_ptr() for t in weights])
+    s1 = (C.c_void_p * P)(*[t.data_ptr() for t in state1])
+    s2 = None if state2 is None else (C.c_void_p * P)(*[t.data_ptr() for t in state2])
+    _chk(lib().picasso_bind(ctx, C.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+                            w, s1, s2), "picasso_bind", ctx)
+
+
+def picasso_ctx_destroy(ctx):
+    lib().picasso_ctx_destroy(ctx)
+
+
+def picasso_packed_lookup_fwd(ctx, ids, offsets, batch, out, stream=None):
+    _chk(lib().picasso_packed_lookup_fwd(ctx, _ptr(ids), _ptr(offsets), int(batch), int(ids.numel()), _ptr(out),
+                                         _stream(stream)), "picasso_packed_lookup_fwd", ctx)
+
+
+def picasso_packed_lookup_bwd_update(ctx, grad_out, lr, step, stream=None):
+    _chk(lib().picasso_packed_lookup_bwd_update(ctx, _ptr(grad_out), float(lr), int(step), _stream(stream)),
+         "picasso_packed_lookup_bwd_update", ctx)
+
+
+def picasso_last_error(ctx):
+    buf = C.create_string_buffer(512)
+    st = lib().picasso_last_error(ctx, buf, 512)
+    return st, buf.value.decode(errors="replace")
+
+
+def picasso_get_unique(ctx, pack, device):
+    import torch
+
+    n = C.c_int64()
+    _chk(lib().picasso_get_unique(ctx, int(pack), None, 0, C.byref(n)), "picasso_get_unique", ctx)
+    out = torch.empty(max(n.value, 1), dtype=torch.int64, device=device)
+    _chk(lib().picasso_get_unique(ctx, int(pack), _ptr(out), n.value, C.byref(n)), "picasso_get_unique", ctx)
+    return out[:n.value]
+
+
+def picasso_get_inverse(ctx, pack, device):
+    import torch
+
+    n = C.c_int64()
+    _chk(lib().picasso_get_inverse(ctx, int(pack), None, 0, C.byref(n)), "picasso_get_inverse", ctx)
+    out = torch.empty(max(n.value, 1), dtype=torch.int32, device=device)
+    _chk(lib().picasso_get_inverse(ctx, int(pack), _ptr(out), n.value, C.byref(n)), "picasso_get_inverse", ctx)
+    return out[:n.value]
+
+
+def picasso_launch_count(ctx):
+    f, b = C.c_int64(), C.c_int64()
+    _chk(lib().picasso_launch_count(ctx, C.byref(f), C.byref(b)), "picasso_launch_count")
+    return f.value, b.value
+
+
+def picasso_profile_enable(ctx, on=True):
+    _chk(lib().picasso_profile_enable(ctx, int(bool(on))), "picasso_profile_enable")
+
+
+def picasso_profile_read(ctx):
+    """{phase: summed ms since the last read}, number of profiled steps."""
+    ms = (C.c_float * 4)()
+    n = C.c_int64()
+    _chk(lib().picasso_profile_read(ctx, ms, C.byref(n)), "picasso_profile_read", ctx)
+    return {PHASES[i]: float(ms[i]) for i in range(4)}, n.value
+
+
+def picasso_unique_offsets(ctx, dst, stream=None):
+    """Enqueue a copy of the int32 [n_packs+1] uid prefix of the last forward into `dst` (a
+    device tensor or a pinned host tensor)."""
+    _chk(lib().picasso_unique_offsets(ctx, _ptr(dst), _stream(stream)), "picasso_unique_offsets", ctx)
+    return dst

@@ -1,0 +1,225 @@
+// k_index.cu — ID hashing + fused Unique ("Unique&Partition").
+//
+// All packs are processed by one launch over the *packed ID stream*: the concatenation, pack
+// by pack (ascending pack, then ascending field, then sample b, then j), of every ID of the
+// batch (D-Packing's "packed ID tensor", L319-323; kept virtual — position g maps back to
+// its field-major index j by a binary search, no copy).
+//
+//   k_field_prep   : per-field ID ranges and the packed-stream layout (one small block)
+//   k_dedup_insert : row mapping, pack key, segment id; warp pre-dedup (__match_any_sync) and
+//                    one open-addressing insert per distinct key per warp; atomicMin keeps the
+//                    first position of every key
+//   k_flag_count   : first-occurrence flags, counted per 2048-position tile
+//   k_assign       : tile-ordered exclusive scan -> global uid in first-occurrence order;
+//                    unique keys; inverse index; per-pack uid ranges
+// Unique order is the first-occurrence order of each pack's key stream (reading O1), and
+// because packs occupy contiguous position ranges the per-pack uid of a key is its global
+// uid minus pack_ustart[p].
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.h"
+
+namespace picasso {
+
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_field_prep(IndexArgs a) {
+    __shared__ int32_t warp_sums[32];
+    __shared__ int32_t carry;
+    const int tid = threadIdx.x;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < a.F; base += 1024) {
+        const int k = base + tid;
+        int32_t len = 0;
+        if (k < a.F) {
+            const int f = a.pm_fields[k];
+            const int32_t s0 = a.offsets[(int64_t)f * a.B];
+            const int32_t s1 = a.offsets[(int64_t)(f + 1) * a.B];
+            a.id_start[f] = s0;
+            len = s1 - s0;
+        }
+        // block exclusive scan of len
+        int32_t x = len;
+        const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int32_t s = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;  // inclusive
+        }
+        __syncthreads();
+        const int32_t excl = carry + (w ? warp_sums[w - 1] : 0) + x - len;
+        if (k < a.F) {
+            a.gstart_pm[k] = excl;
+            a.field_gstart[a.pm_fields[k]] = excl;
+        }
+        __syncthreads();
+        if (tid == 0) carry += warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) a.gstart_pm[a.F] = carry;
+    __syncthreads();
+    for (int p = tid; p <= a.P; p += 1024) a.pack_gstart[p] = a.gstart_pm[a.pack_first_k[p]];
+}
+
+void launch_field_prep(const IndexArgs &a, cudaStream_t s) { k_field_prep<<<1, 1024, 0, s>>>(a); }
+
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dedup_insert(IndexArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = g < a.N;
+    unsigned long long gkey = 0;
+    if (valid) {
+        // packed position -> pm field -> field-major index j -> sample b
+        const int64_t k = upper_bound_dev(a.gstart_pm, 0, a.F + 1, (int32_t)g) - 1;
+        const int f = __ldg(a.pm_fields + k);
+        const int64_t j = (int64_t)__ldg(a.id_start + f) + (g - __ldg(a.gstart_pm + k));
+        const FieldInfo fi = a.finfo[f];
+        const int64_t row = row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
+        gkey = (unsigned long long)(__ldg(a.pack_key_off + fi.pack) + fi.base + row);
+        const int64_t s0 = (int64_t)f * a.B;
+        const int64_t b = upper_bound_dev(a.offsets, s0, s0 + a.B + 1, (int32_t)j) - 1 - s0;
+        a.seg_of[g] = (int32_t)(s0 + b);
+    }
+    // warp pre-dedup: lanes holding the same key elect the lowest lane (= smallest g)
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(vmask, gkey);
+    const int leader = __ffs(peers) - 1;
+    uint32_t slot = 0;
+    if (lane == leader) {
+        slot = slot_hash(gkey) & a.cap_mask;
+        for (uint32_t probe = 0;; ++probe) {
+            unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(&a.table[slot].key);
+            if (cur == kEmptyKey) cur = atomicCAS(&a.table[slot].key, kEmptyKey, gkey);
+            if (cur == kEmptyKey || cur == gkey) break;
+            slot = (slot + 1) & a.cap_mask;
+            if (probe > a.cap_mask) {  // table full: cannot happen with cap >= 2N
+                atomicOr(a.err, ERR_CAPACITY);
+                break;
+            }
+        }
+        atomicMin(&a.table[slot].minpos, (unsigned int)g);
+    }
+    slot = __shfl_sync(vmask, slot, leader);
+    a.slot_of[g] = (int32_t)slot;
+}
+
+void launch_dedup_insert(const IndexArgs &a, cudaStream_t s) {
+    const int64_t nb = (a.N + 255) / 256;
+    if (nb) k_dedup_insert<<<(unsigned)nb, 256, 0, s>>>(a);
+}
+
+// ------------------------------------------------------------------------------------------
+constexpr int kItems = kTile / kTileThreads;  // 8 consecutive positions per thread
+
+__global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
+    using BlockReduce = cub::BlockReduce<int32_t, kTileThreads>;
+    __shared__ typename BlockReduce::TempStorage tmp;
+    const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    int32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const int64_t g = g0 + i;
+        if (g < a.N) c += (a.table[a.slot_of[g]].minpos == (unsigned int)g);
+    }
+    const int32_t tot = BlockReduce(tmp).Sum(c);
+    if (threadIdx.x == 0) a.blk_cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
+    using BlockScan = cub::BlockScan<int32_t, kTileThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    int32_t slot[kItems];
+    bool first[kItems];
+    int32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const int64_t g = g0 + i;
+        first[i] = false;
+        slot[i] = 0;
+        if (g < a.N) {
+            slot[i] = a.slot_of[g];
+            first[i] = a.table[slot[i]].minpos == (unsigned int)g;
+            c += first[i];
+        }
+    }
+    int32_t excl;
+    BlockScan(tmp).ExclusiveSum(c, excl);
+    int32_t uid = a.blk_off[blockIdx.x] + excl;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        if (first[i]) {
+            a.table[slot[i]].uid = uid;
+            a.unique_gkey[uid] = a.table[slot[i]].key;
+            ++uid;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < a.N) a.inverse[g] = a.table[a.slot_of[g]].uid;
+}
+
+// pack_ustart[p] = #uniques whose global key lies below pack p's key range (keys of later
+// packs are larger and their uids later, so the predicate is monotone in uid).
+__global__ void k_pack_ustart(IndexArgs a) {
+    const int p = threadIdx.x;
+    if (p > a.P) return;
+    const int32_t U = *a.d_total;
+    const unsigned long long lim = (unsigned long long)a.pack_key_off[p];
+    int64_t lo = 0, hi = U;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a.unique_gkey[mid] < lim) lo = mid + 1; else hi = mid;
+    }
+    a.pack_ustart[p] = (p == a.P) ? U : (int32_t)lo;
+}
+
+__global__ void k_scan_blocks(const int32_t *cnt, int32_t *off, int32_t n, int32_t *total) {
+    // single block, n small (N / 2048): chunked sequential scan with block carry
+    __shared__ int32_t s_carry;
+    using BlockScan = cub::BlockScan<int32_t, 1024>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + threadIdx.x;
+        int32_t v = i < n ? cnt[i] : 0, e, agg;
+        BlockScan(tmp).ExclusiveSum(v, e, agg);
+        if (i < n) off[i] = s_carry + e;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = s_carry;
+}
+
+void launch_dedup_assign(const IndexArgs &a, cudaStream_t s) {
+    const int64_t nb = (a.N + kTile - 1) / kTile;
+    if (nb) {
+        k_flag_count<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
+        k_scan_blocks<<<1, 1024, 0, s>>>(a.blk_cnt, a.blk_off, (int32_t)nb, a.d_total);
+        k_assign<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
+        k_inverse<<<(unsigned)((a.N + 255) / 256), 256, 0, s>>>(a);
+    } else {
+        cudaMemsetAsync(a.d_total, 0, sizeof(int32_t), s);
+    }
+    k_pack_ustart<<<1, ((a.P + 1 + 31) / 32) * 32, 0, s>>>(a);
+}
+
+}  // namespace picasso

@@ -1,0 +1,98 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal; not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace picasso {
+
+constexpr int kTile = 2048;     // keys per block in the index / scan / sort kernels
+constexpr int kTileThreads = 256;
+constexpr int kLongRow = 256;   // rows with more occurrences take the chunked backward path
+
+struct IndexArgs {
+    const int64_t *ids;
+    const int32_t *offsets;
+    int32_t B;
+    int64_t N;
+    int32_t F, P;
+    int32_t id_mode;
+    const FieldInfo *finfo;        // [F]
+    const int32_t *pm_fields;      // [F] fields in pack-major order (pack asc, field asc)
+    const int32_t *pack_first_k;   // [P+1] first pm index of each pack
+    const int64_t *pack_key_off;   // [P+1] global key offset of each pack
+    int32_t *id_start;             // [F]  out: offsets[f*B]
+    int32_t *gstart_pm;            // [F+1] out: packed-stream start of the k-th pm field
+    int32_t *field_gstart;         // [F]  out
+    int32_t *pack_gstart;          // [P+1] out
+    Slot *table;
+    uint32_t cap_mask;
+    int32_t *slot_of;              // [N]
+    int32_t *seg_of;               // [N]
+    int32_t *inverse;              // [N] global uid per packed position
+    int32_t *blk_cnt;              // [nblk]
+    int32_t *blk_off;              // [nblk]
+    int32_t *d_total;              // [1] U (all packs)
+    unsigned long long *unique_gkey; // [N]
+    int32_t *pack_ustart;          // [P+1]
+    int *err;
+};
+
+// k_index.cu
+void launch_field_prep(const IndexArgs &a, cudaStream_t s);
+void launch_dedup_insert(const IndexArgs &a, cudaStream_t s);
+void launch_dedup_assign(const IndexArgs &a, cudaStream_t s);  // flag, scan, uid, unique, pack_ustart, inverse
+
+// k_scan.cu / k_sort.cu
+void launch_scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *scratch, int32_t *total,
+                           cudaStream_t s);
+size_t scan_scratch_ints(int64_t n);
+// Stable LSD radix sort of (key, val) int32 pairs by key < 2^bits.  Result in (k_out, v_out).
+void radix_sort_pairs(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, int32_t *v_a, int32_t *k_b,
+                      int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, int bits, int32_t *hist,
+                      int32_t *scratch, cudaStream_t s, int64_t *launches);
+size_t radix_hist_ints(int64_t n);
+
+// k_pool.cu
+struct PoolArgs {
+    const int64_t *ids;
+    const int32_t *offsets;
+    int32_t B;
+    int32_t Fp;                 // fields in this pack
+    const int32_t *pack_fields; // [Fp] field indices (ascending)
+    const FieldInfo *finfo;
+    int32_t id_mode, pool_mean;
+    const float *weight;        // [rows, D]
+    float *out;
+    int64_t out_stride;
+    int *err;
+};
+void launch_pool(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
+
+// k_update.cu
+struct UpdateArgs {
+    const int32_t *sorted_u;     // [N] (unused by kernels; boundaries)
+    const int32_t *sorted_seg;   // [N]
+    const int32_t *ustart;       // [U+1]
+    const int32_t *pack_ustart;  // [P+1]
+    int32_t pack;
+    const unsigned long long *unique_gkey;
+    int64_t pack_key_off;
+    const int32_t *offsets;
+    int32_t B;
+    const FieldInfo *finfo;
+    const float *dy;
+    int64_t dy_stride;
+    int32_t pool_mean;
+    int32_t opt;                 // 0 adagrad, 1 adam
+    float lr, eps, beta1, beta2, adam_ss;
+    float *weight, *state1, *state2;
+    int32_t *long_list;          // [cap]
+    int32_t *long_cnt;           // [1]
+};
+void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, cudaStream_t s);
+void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
+void launch_long_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
+
+}  // namespace picasso

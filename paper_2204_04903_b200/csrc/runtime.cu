@@ -1,0 +1,516 @@
+// runtime.cu — the C ABI (include/picasso.h): context, workspace carving, step orchestration.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "picasso.h"
+
+using namespace picasso;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    T *take(size_t n) {
+        off = (off + kAlign - 1) / kAlign * kAlign;
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += n * sizeof(T);
+        return p;
+    }
+};
+
+uint32_t pow2_at_least(uint64_t x) {
+    uint64_t p = 1024;
+    while (p < x) p <<= 1;
+    return (uint32_t)p;
+}
+
+int bits_for(int64_t maxval) {
+    int b = 1;
+    while (b < 31 && ((int64_t)1 << b) <= maxval) ++b;
+    return b;
+}
+
+}  // namespace
+
+struct picasso_ctx {
+    int32_t rank = 0, world = 1;
+    picasso_ctx_opts opts{};
+    int32_t F = 0, T = 0, P = 0;
+    std::vector<int32_t> f2t, t2p, tdim, pack_dim;
+    std::vector<int64_t> tbase, trows, fcol, pack_rows, pack_key_off;
+    std::vector<uint64_t> tsalt;
+    int64_t out_width = 0;
+    std::vector<int32_t> pm_fields, pack_first_k;
+    // workspace layout
+    size_t ws_bytes = 0;
+    uint32_t cap = 0;
+    bool bound = false;
+    FieldInfo *finfo = nullptr;
+    int32_t *pm_fields_d = nullptr, *pack_first_k_d = nullptr;
+    int64_t *pack_key_off_d = nullptr;
+    int32_t *id_start = nullptr, *gstart_pm = nullptr, *field_gstart = nullptr, *pack_gstart = nullptr;
+    int32_t *pack_ustart = nullptr;
+    Slot *table = nullptr;
+    int32_t *slot_of = nullptr, *seg_of = nullptr, *inverse = nullptr;
+    int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
+    int *err = nullptr;
+    unsigned long long *unique_gkey = nullptr;
+    int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
+    int32_t *ustart = nullptr, *long_list = nullptr;
+    std::vector<float *> w, s1, s2;
+    // step state
+    bool fwd_done = false;
+    int32_t B = 0;
+    int64_t N = 0;
+    const int32_t *offsets = nullptr;
+    cudaStream_t last_stream = nullptr;
+    int num_sms = 148;
+    int64_t launches_fwd = 0, launches_bwd = 0;
+    std::string last_msg;
+    // phase profiling (events on the caller's stream)
+    static constexpr int kPhases = 4;
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
+    size_t ev_used[kPhases] = {0, 0, 0, 0};
+    int64_t prof_calls = 0;
+
+    void mark(int ph, bool begin, cudaStream_t s) {
+        if (!prof) return;
+        auto &v = ev[ph];
+        if (begin) {
+            if (ev_used[ph] == v.size()) {
+                cudaEvent_t a, b;
+                cudaEventCreate(&a);
+                cudaEventCreate(&b);
+                v.emplace_back(a, b);
+            }
+            cudaEventRecord(v[ev_used[ph]].first, s);
+        } else {
+            cudaEventRecord(v[ev_used[ph]].second, s);
+            ++ev_used[ph];
+        }
+    }
+    ~picasso_ctx() {
+        for (auto &v : ev)
+            for (auto &p : v) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
+    }
+
+    size_t carve(char *base) {
+        Carver c{base};
+        const int64_t N = std::max<int64_t>(opts.max_ids, 1);
+        const int64_t nblk = (N + kTile - 1) / kTile + 1;
+        finfo = c.take<FieldInfo>(F);
+        pm_fields_d = c.take<int32_t>(F);
+        pack_first_k_d = c.take<int32_t>(P + 1);
+        pack_key_off_d = c.take<int64_t>(P + 1);
+        id_start = c.take<int32_t>(F);
+        gstart_pm = c.take<int32_t>(F + 1);
+        field_gstart = c.take<int32_t>(F);
+        pack_gstart = c.take<int32_t>(P + 1);
+        pack_ustart = c.take<int32_t>(P + 1);
+        table = c.take<Slot>(cap);
+        slot_of = c.take<int32_t>(N);
+        seg_of = c.take<int32_t>(N);
+        inverse = c.take<int32_t>(N);
+        blk_cnt = c.take<int32_t>(nblk);
+        blk_off = c.take<int32_t>(nblk);
+        d_total = c.take<int32_t>(1);
+        long_cnt = c.take<int32_t>(1);
+        err = c.take<int>(1);
+        unique_gkey = c.take<unsigned long long>(N);
+        k_a = c.take<int32_t>(N);
+        v_a = c.take<int32_t>(N);
+        k_b = c.take<int32_t>(N);
+        v_b = c.take<int32_t>(N);
+        hist = c.take<int32_t>(radix_hist_ints(N));
+        scratch = c.take<int32_t>(scan_scratch_ints((int64_t)radix_hist_ints(N)) + 16);
+        ustart = c.take<int32_t>(N + 1);
+        long_list = c.take<int32_t>(N / (kLongRow + 1) + 2);
+        return c.off + kAlign;
+    }
+};
+
+#define CK(x)                                                             \
+    do {                                                                  \
+        cudaError_t e_ = (x);                                             \
+        if (e_ != cudaSuccess) {                                          \
+            if (ctx) ctx->last_msg = std::string(#x ": ") + cudaGetErrorString(e_); \
+            return PICASSO_ERR_CUDA;                                      \
+        }                                                                 \
+    } while (0)
+
+static bool dim_ok(int32_t d) {
+    return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 384 || d == 512;
+}
+
+extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int32_t rank, int32_t world,
+                                             const picasso_ctx_opts *opts, picasso_ctx **out) {
+    if (!plan || !opts || !out || plan->n_fields <= 0 || plan->n_tables <= 0 || plan->n_packs <= 0)
+        return PICASSO_ERR_INVALID_ARG;
+    if (world != 1 || rank != 0) return PICASSO_ERR_INVALID_ARG;  // this build: single rank
+    if (opts->max_batch <= 0 || opts->max_ids < 0 || opts->max_ids >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
+    if (opts->pool < 0 || opts->pool > 1 || opts->id_mode < 0 || opts->id_mode > 1 || opts->opt < 0 || opts->opt > 1)
+        return PICASSO_ERR_INVALID_ARG;
+    if ((int64_t)plan->n_fields * opts->max_batch >= ((int64_t)1 << 31)) return PICASSO_ERR_INVALID_ARG;
+    auto *c = new picasso_ctx();
+    c->rank = rank;
+    c->world = world;
+    c->opts = *opts;
+    c->F = plan->n_fields;
+    c->T = plan->n_tables;
+    c->P = plan->n_packs;
+    c->f2t.assign(plan->field_to_table, plan->field_to_table + c->F);
+    c->t2p.assign(plan->table_to_pack, plan->table_to_pack + c->T);
+    c->tbase.assign(plan->table_base, plan->table_base + c->T);
+    c->trows.assign(plan->table_rows, plan->table_rows + c->T);
+    c->tdim.assign(plan->table_dim, plan->table_dim + c->T);
+    c->tsalt.assign(c->T, 0);
+    if (plan->table_salt) c->tsalt.assign(plan->table_salt, plan->table_salt + c->T);
+    c->fcol.assign(plan->field_col, plan->field_col + c->F);
+    c->out_width = plan->out_width;
+    // validate plan: tables tile each pack's key range, dims agree, columns fit
+    c->pack_dim.assign(c->P, -1);
+    c->pack_rows.assign(c->P, 0);
+    for (int32_t t = 0; t < c->T; ++t) {
+        const int32_t p = c->t2p[t];
+        if (p < 0 || p >= c->P || !dim_ok(c->tdim[t]) || c->trows[t] <= 0) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
+        if (c->pack_dim[p] != -1 && c->pack_dim[p] != c->tdim[t]) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
+        c->pack_dim[p] = c->tdim[t];
+        c->pack_rows[p] = std::max(c->pack_rows[p], c->tbase[t] + c->trows[t]);
+    }
+    for (int32_t p = 0; p < c->P; ++p)
+        if (c->pack_dim[p] < 0) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
+    if (c->out_width % 4) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
+    for (int32_t f = 0; f < c->F; ++f) {
+        const int32_t t = c->f2t[f];
+        if (t < 0 || t >= c->T || c->fcol[f] % 4 || c->fcol[f] < 0 || c->fcol[f] + c->tdim[t] > c->out_width) {
+            delete c;
+            return PICASSO_ERR_PLAN_MISMATCH;
+        }
+    }
+    c->pack_key_off.assign(c->P + 1, 0);
+    for (int32_t p = 0; p < c->P; ++p) c->pack_key_off[p + 1] = c->pack_key_off[p] + c->pack_rows[p];
+    // pack-major field order (pack asc, field asc)
+    c->pack_first_k.assign(c->P + 1, 0);
+    for (int32_t p = 0; p < c->P; ++p) {
+        c->pack_first_k[p] = (int32_t)c->pm_fields.size();
+        for (int32_t f = 0; f < c->F; ++f)
+            if (c->t2p[c->f2t[f]] == p) c->pm_fields.push_back(f);
+    }
+    c->pack_first_k[c->P] = c->F;
+    c->cap = pow2_at_least((uint64_t)std::max<int64_t>(opts->max_ids, 1) * 2);
+    c->ws_bytes = c->carve(nullptr);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    *out = c;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_workspace_size(const picasso_ctx *ctx, size_t *bytes) {
+    if (!ctx || !bytes) return PICASSO_ERR_INVALID_ARG;
+    *bytes = ctx->ws_bytes;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_pack_local_rows(const picasso_ctx *ctx, int32_t pack, int64_t *rows) {
+    if (!ctx || !rows || pack < 0 || pack >= ctx->P) return PICASSO_ERR_INVALID_ARG;
+    const int64_t R = ctx->pack_rows[pack];
+    *rows = R > ctx->rank ? (R - ctx->rank + ctx->world - 1) / ctx->world : 0;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t bytes, float *const *pack_weight,
+                                       float *const *pack_state1, float *const *pack_state2) {
+    if (!ctx || !workspace || !pack_weight || !pack_state1) return PICASSO_ERR_INVALID_ARG;
+    if (bytes < ctx->ws_bytes) return PICASSO_ERR_CAPACITY;
+    if (ctx->opts.opt == PICASSO_OPT_ADAM_LAZY && !pack_state2) return PICASSO_ERR_INVALID_ARG;
+    char *base = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(workspace) + kAlign - 1) / kAlign * kAlign);
+    if ((size_t)(base - reinterpret_cast<char *>(workspace)) + ctx->ws_bytes - kAlign > bytes) return PICASSO_ERR_CAPACITY;
+    ctx->carve(base);
+    ctx->w.assign(pack_weight, pack_weight + ctx->P);
+    ctx->s1.assign(pack_state1, pack_state1 + ctx->P);
+    ctx->s2.assign(ctx->P, nullptr);
+    if (pack_state2) ctx->s2.assign(pack_state2, pack_state2 + ctx->P);
+    for (int32_t p = 0; p < ctx->P; ++p) {
+        if (!ctx->w[p] || !ctx->s1[p] || (ctx->opts.opt == PICASSO_OPT_ADAM_LAZY && !ctx->s2[p]))
+            return PICASSO_ERR_INVALID_ARG;
+        if ((reinterpret_cast<uintptr_t>(ctx->w[p]) | reinterpret_cast<uintptr_t>(ctx->s1[p])) & 15)
+            return PICASSO_ERR_INVALID_ARG;
+    }
+    std::vector<FieldInfo> fi(ctx->F);
+    for (int32_t f = 0; f < ctx->F; ++f) {
+        const int32_t t = ctx->f2t[f];
+        fi[f].base = ctx->tbase[t];
+        fi[f].rows = ctx->trows[t];
+        fi[f].salt = ctx->tsalt[t];
+        fi[f].col = ctx->fcol[f];
+        fi[f].pack = ctx->t2p[t];
+        fi[f].dim = ctx->tdim[t];
+        fi[f].table = t;
+        fi[f].pad = 0;
+    }
+    CK(cudaMemcpy(ctx->finfo, fi.data(), sizeof(FieldInfo) * ctx->F, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->pm_fields_d, ctx->pm_fields.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->pack_first_k_d, ctx->pack_first_k.data(), sizeof(int32_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemset(ctx->err, 0, sizeof(int)));
+    ctx->bound = true;
+    ctx->fwd_done = false;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
+    delete ctx;
+    return PICASSO_OK;
+}
+
+static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N) {
+    IndexArgs a{};
+    a.ids = ids;
+    a.offsets = offsets;
+    a.B = B;
+    a.N = N;
+    a.F = ctx->F;
+    a.P = ctx->P;
+    a.id_mode = ctx->opts.id_mode;
+    a.finfo = ctx->finfo;
+    a.pm_fields = ctx->pm_fields_d;
+    a.pack_first_k = ctx->pack_first_k_d;
+    a.pack_key_off = ctx->pack_key_off_d;
+    a.id_start = ctx->id_start;
+    a.gstart_pm = ctx->gstart_pm;
+    a.field_gstart = ctx->field_gstart;
+    a.pack_gstart = ctx->pack_gstart;
+    a.table = ctx->table;
+    a.slot_of = ctx->slot_of;
+    a.seg_of = ctx->seg_of;
+    a.inverse = ctx->inverse;
+    a.blk_cnt = ctx->blk_cnt;
+    a.blk_off = ctx->blk_off;
+    a.d_total = ctx->d_total;
+    a.unique_gkey = ctx->unique_gkey;
+    a.pack_ustart = ctx->pack_ustart;
+    a.err = ctx->err;
+    return a;
+}
+
+extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets,
+                                                    int32_t batch, int64_t n_ids, float *out, void *stream) {
+    if (!ctx || !offsets || !out || batch < 0 || n_ids < 0 || (n_ids > 0 && !ids)) return PICASSO_ERR_INVALID_ARG;
+    if (!ctx->bound) return PICASSO_ERR_STATE;
+    if (batch > ctx->opts.max_batch || n_ids > ctx->opts.max_ids) return PICASSO_ERR_CAPACITY;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    ctx->launches_fwd = 0;
+    IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
+    const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
+    a.cap_mask = cap_step - 1;
+    ctx->mark(0, true, s);
+    CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+    launch_field_prep(a, s);
+    launch_dedup_insert(a, s);
+    launch_dedup_assign(a, s);
+    ctx->mark(0, false, s);
+    ctx->launches_fwd += 1 + (n_ids > 0 ? 1 + 4 : 0) + 1;
+    ctx->mark(1, true, s);
+    for (int32_t p = 0; p < ctx->P; ++p) {
+        PoolArgs pa{};
+        pa.ids = ids;
+        pa.offsets = offsets;
+        pa.B = batch;
+        pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
+        pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
+        pa.finfo = ctx->finfo;
+        pa.id_mode = ctx->opts.id_mode;
+        pa.pool_mean = ctx->opts.pool == PICASSO_POOL_MEAN;
+        pa.weight = ctx->w[p];
+        pa.out = out;
+        pa.out_stride = ctx->out_width;
+        pa.err = ctx->err;
+        launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
+        if ((int64_t)pa.Fp * batch > 0) ctx->launches_fwd += 1;
+    }
+    ctx->mark(1, false, s);
+    CK(cudaGetLastError());
+    ctx->fwd_done = true;
+    ctx->B = batch;
+    ctx->N = n_ids;
+    ctx->offsets = offsets;
+    ctx->last_stream = s;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, const float *grad_out, float lr,
+                                                           int64_t step, void *stream) {
+    if (!ctx || !grad_out || step < 1) return PICASSO_ERR_INVALID_ARG;
+    if (!ctx->bound || !ctx->fwd_done) return PICASSO_ERR_STATE;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    ctx->launches_bwd = 0;
+    const int64_t N = ctx->N;
+    int32_t *su = nullptr, *sseg = nullptr;
+    ctx->mark(2, true, s);
+    radix_sort_pairs(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N,
+                     bits_for(std::max<int64_t>(N - 1, 1)), ctx->hist, ctx->scratch, s, &ctx->launches_bwd);
+    launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, s);
+    ctx->mark(2, false, s);
+    ctx->launches_bwd += N > 0 ? 1 : 0;
+    ctx->mark(3, true, s);
+    UpdateArgs u{};
+    u.sorted_u = su;
+    u.sorted_seg = sseg;
+    u.ustart = ctx->ustart;
+    u.pack_ustart = ctx->pack_ustart;
+    u.unique_gkey = ctx->unique_gkey;
+    u.offsets = ctx->offsets;
+    u.B = ctx->B;
+    u.finfo = ctx->finfo;
+    u.dy = grad_out;
+    u.dy_stride = ctx->out_width;
+    u.pool_mean = ctx->opts.pool == PICASSO_POOL_MEAN;
+    u.opt = ctx->opts.opt;
+    u.lr = lr;
+    u.eps = ctx->opts.eps;
+    u.beta1 = ctx->opts.beta1;
+    u.beta2 = ctx->opts.beta2;
+    {   // SparseAdam step size, in double then rounded once (torch: lr*sqrt(bc2)/bc1)
+        const double bc1 = 1.0 - std::pow((double)ctx->opts.beta1, (double)step);
+        const double bc2 = 1.0 - std::pow((double)ctx->opts.beta2, (double)step);
+        u.adam_ss = (float)((double)lr * std::sqrt(bc2) / bc1);
+    }
+    u.long_list = ctx->long_list;
+    u.long_cnt = ctx->long_cnt;
+    if (N > 0) {
+        for (int32_t p = 0; p < ctx->P; ++p) {
+            u.pack = p;
+            u.pack_key_off = ctx->pack_key_off[p];
+            u.weight = ctx->w[p];
+            u.state1 = ctx->s1[p];
+            u.state2 = ctx->s2[p];
+            launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+            ctx->launches_bwd += 1;
+        }
+        for (int32_t p = 0; p < ctx->P; ++p) {
+            u.pack = p;
+            u.pack_key_off = ctx->pack_key_off[p];
+            u.weight = ctx->w[p];
+            u.state1 = ctx->s1[p];
+            u.state2 = ctx->s2[p];
+            launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+            ctx->launches_bwd += 1;
+        }
+    }
+    ctx->mark(3, false, s);
+    if (ctx->prof) ++ctx->prof_calls;
+    CK(cudaGetLastError());
+    ctx->fwd_done = false;
+    ctx->last_stream = s;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t len) {
+    if (!ctx) return PICASSO_ERR_INVALID_ARG;
+    picasso_status st = PICASSO_OK;
+    std::string m = ctx->last_msg;
+    if (ctx->bound) {
+        cudaError_t e = cudaStreamSynchronize(ctx->last_stream);
+        if (e != cudaSuccess) {
+            m = cudaGetErrorString(e);
+            st = PICASSO_ERR_CUDA;
+        } else {
+            int h = 0;
+            if (cudaMemcpy(&h, ctx->err, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && h) {
+                if (h & ERR_ID_RANGE) { st = PICASSO_ERR_ID_RANGE; m = "raw ID outside [0, V_t) in ROWS mode"; }
+                else if (h & ERR_CAPACITY) { st = PICASSO_ERR_CAPACITY; m = "device capacity overflow"; }
+                cudaMemset(ctx->err, 0, sizeof(int));
+            }
+        }
+    }
+    if (msg && len) {
+        std::snprintf(msg, len, "%s", m.c_str());
+    }
+    return st;
+}
+
+extern "C" picasso_status picasso_get_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n) {
+    if (!ctx || !n || pack < 0 || pack >= ctx->P || !ctx->bound) return PICASSO_ERR_INVALID_ARG;
+    CK(cudaStreamSynchronize(ctx->last_stream));
+    std::vector<int32_t> us(ctx->P + 1);
+    CK(cudaMemcpy(us.data(), ctx->pack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost));
+    const int64_t U = us[pack + 1] - us[pack];
+    *n = U;
+    if (dst && cap > 0 && U > 0) {
+        std::vector<unsigned long long> g(U);
+        CK(cudaMemcpy(g.data(), ctx->unique_gkey + us[pack], sizeof(unsigned long long) * U, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> k(U);
+        for (int64_t i = 0; i < U; ++i) k[i] = (int64_t)(g[i] - (unsigned long long)ctx->pack_key_off[pack]);
+        CK(cudaMemcpy(dst, k.data(), sizeof(int64_t) * std::min(U, cap), cudaMemcpyHostToDevice));
+    }
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, int32_t *dst, int64_t cap, int64_t *n) {
+    if (!ctx || !n || pack < 0 || pack >= ctx->P || !ctx->bound) return PICASSO_ERR_INVALID_ARG;
+    CK(cudaStreamSynchronize(ctx->last_stream));
+    std::vector<int32_t> gs(ctx->P + 1), us(ctx->P + 1);
+    CK(cudaMemcpy(gs.data(), ctx->pack_gstart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(us.data(), ctx->pack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost));
+    const int64_t Np = gs[pack + 1] - gs[pack];
+    *n = Np;
+    if (dst && cap > 0 && Np > 0) {
+        std::vector<int32_t> v(Np);
+        CK(cudaMemcpy(v.data(), ctx->inverse + gs[pack], sizeof(int32_t) * Np, cudaMemcpyDeviceToHost));
+        for (auto &x : v) x -= us[pack];
+        CK(cudaMemcpy(dst, v.data(), sizeof(int32_t) * std::min(Np, cap), cudaMemcpyHostToDevice));
+    }
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_profile_enable(picasso_ctx *ctx, int32_t on) {
+    if (!ctx) return PICASSO_ERR_INVALID_ARG;
+    ctx->prof = on != 0;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int64_t *calls) {
+    if (!ctx || !ms) return PICASSO_ERR_INVALID_ARG;
+    for (int ph = 0; ph < picasso_ctx::kPhases; ++ph) {
+        float tot = 0.f;
+        for (size_t i = 0; i < ctx->ev_used[ph]; ++i) {
+            CK(cudaEventSynchronize(ctx->ev[ph][i].second));
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, ctx->ev[ph][i].first, ctx->ev[ph][i].second));
+            tot += t;
+        }
+        ms[ph] = tot;
+        ctx->ev_used[ph] = 0;
+    }
+    if (calls) *calls = ctx->prof_calls;
+    ctx->prof_calls = 0;
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_unique_offsets(picasso_ctx *ctx, int32_t *dst, void *stream) {
+    if (!ctx || !dst || !ctx->bound) return PICASSO_ERR_INVALID_ARG;
+    CK(cudaMemcpyAsync(dst, ctx->pack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDefault,
+                       reinterpret_cast<cudaStream_t>(stream)));
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_launch_count(const picasso_ctx *ctx, int64_t *fwd, int64_t *bwd) {
+    if (!ctx) return PICASSO_ERR_INVALID_ARG;
+    if (fwd) *fwd = ctx->launches_fwd;
+    if (bwd) *bwd = ctx->launches_bwd;
+    return PICASSO_OK;
+}

@@ -1,0 +1,101 @@
+"""PackedEmbedding: owns the torch buffers (workspace, packed tables, optimizer state) of one
+rank's context and forwards to the C ABI.  Plumbing only — every step runs in libpicasso."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import abi
+
+
+class PackedEmbedding:
+    """One rank of the packed multi-field embedding layer.
+
+    field_to_table [F], table_rows [T], table_dim [T]: the model.
+    The D-Packing plan comes from picasso_pack_plan (Eq. 1).  Output columns are the
+    fields' dims laid side by side in field order unless field_col is given.
+    """
+
+    def __init__(self, field_to_table, table_rows, table_dim, *, max_batch, max_ids, table_salt=None,
+                 field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
+                 beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
+                 init_acc=0.1):
+        self.f2t = np.asarray(field_to_table, np.int32)
+        self.rows = np.asarray(table_rows, np.int64)
+        self.dims = np.asarray(table_dim, np.int32)
+        fd = self.dims[self.f2t].astype(np.int64)
+        self.field_col = (np.concatenate([[0], np.cumsum(fd)[:-1]]) if field_col is None
+                          else np.asarray(field_col, np.int64))
+        self.out_width = int(max(self.field_col + fd)) if len(fd) else 0
+        self.out_width = (self.out_width + 3) // 4 * 4
+        self.plan = abi.picasso_pack_plan(self.f2t, self.rows, self.dims, warmup_count, split)
+        self.opt = opt
+        self.rank, self.world = rank, world
+        self.device = torch.device(device)
+        self.ctx = abi.picasso_ctx_create(self.plan, self.f2t, self.rows, self.dims, table_salt, self.field_col,
+                                          self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
+                                          eps, beta1, beta2)
+        P = self.plan["n_packs"]
+        self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
+        ws = abi.picasso_workspace_size(self.ctx)
+        self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=self.device)
+        self.weights = [torch.zeros(max(r, 1), int(self.plan["pack_dim"][p]), dtype=torch.float32,
+                                    device=self.device) for p, r in enumerate(self.local_rows)]
+        if opt == abi.OPT_ADAGRAD:
+            self.state1 = [torch.full_like(w, init_acc) for w in self.weights]
+            self.state2 = None
+        else:
+            self.state1 = [torch.zeros_like(w) for w in self.weights]
+            self.state2 = [torch.zeros_like(w) for w in self.weights]
+        abi.picasso_bind(self.ctx, self.workspace, self.weights, self.state1, self.state2)
+        self.step = 0
+
+    @property
+    def n_packs(self):
+        return self.plan["n_packs"]
+
+    def forward(self, ids: torch.Tensor, offsets: torch.Tensor, batch: int, out: torch.Tensor | None = None,
+                stream=None):
+        if out is None:
+            out = torch.empty(batch, self.out_width, dtype=torch.float32, device=self.device)
+        abi.picasso_packed_lookup_fwd(self.ctx, ids, offsets, batch, out, stream)
+        return out
+
+    def backward_update(self, grad_out: torch.Tensor, lr: float, step: int | None = None, stream=None):
+        self.step = self.step + 1 if step is None else step
+        abi.picasso_packed_lookup_bwd_update(self.ctx, grad_out, lr, self.step, stream)
+
+    def check(self):
+        st, msg = abi.picasso_last_error(self.ctx)
+        if st != 0:
+            raise abi.PicassoError(st, "device", msg)
+
+    def unique(self, pack):
+        return abi.picasso_get_unique(self.ctx, pack, self.device)
+
+    def inverse(self, pack):
+        return abi.picasso_get_inverse(self.ctx, pack, self.device)
+
+    def unique_offsets(self, dst=None, stream=None):
+        """int32 [n_packs+1] uid prefix of the last forward, copied into dst (enqueue only)."""
+        if dst is None:
+            dst = torch.empty(self.n_packs + 1, dtype=torch.int32, device=self.device)
+        return abi.picasso_unique_offsets(self.ctx, dst, stream)
+
+    def unique_offsets_host(self):
+        o = self.unique_offsets()
+        return o.cpu().numpy()
+
+    def launch_count(self):
+        return abi.picasso_launch_count(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            abi.picasso_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bit-exact: row mapping/dedup/inverse, forward pooling (sequential order by design).
+fp32 update: within 1e-5 rel / 1e-6 abs (north star), and bit-exact under dyadic dY
+(reading O19) for rows whose occurrences are summed in ascending order."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from datagen import configs as dc
+from datagen import make_batch, make_dy, table_values_np
+from harness import (assert_close, gpu_embedding, gpu_table_rows, oracle_model, oracle_tables, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
+def run_step(cfg, opt=oracle.OPT_ADAGRAD, dyadic=True, steps=1, lr=0.05, split=False, batch_fn=None,
+             check_intermediates=True):
+    """Run `steps` fwd+bwd steps on both sides; compare every step."""
+    emb = gpu_embedding(cfg, opt=opt, split=split)
+    m = oracle_model(cfg)
+    tabs = oracle_tables(cfg)
+    if opt == oracle.OPT_ADAGRAD:
+        s1, s2 = [np.full_like(t, 0.1) for t in tabs], None
+    else:
+        s1, s2 = [np.zeros_like(t) for t in tabs], [np.zeros_like(t) for t in tabs]
+    for step in range(1, steps + 1):
+        b = batch_fn(step) if batch_fn else make_batch(cfg, 0, step)
+        dy = make_dy(cfg, 0, step, dyadic=dyadic)
+        ids, off = to_dev(b)
+        out = emb.forward(ids, off, cfg.batch)
+        ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy)
+        ref = oracle.forward(m, ob, tabs, cfg.out_width)
+        got = out.cpu().numpy()
+        assert np.array_equal(got, ref), f"forward not bit-exact at step {step}: max |d| {np.abs(got - ref).max()}"
+        if check_intermediates:
+            for p in range(emb.n_packs):
+                keys = oracle.pack_key_stream(m, emb.plan["field_to_pack"], emb.plan["table_base"], ob, p)
+                u_ref, inv_ref = oracle.unique(keys)
+                assert np.array_equal(emb.unique(p).cpu().numpy(), u_ref), f"unique pack {p}"
+                assert np.array_equal(emb.inverse(p).cpu().numpy(), inv_ref), f"inverse pack {p}"
+        emb.backward_update(torch.from_numpy(dy).cuda(), lr=lr, step=step)
+        emb.check()
+        oracle.backward_update(m, [ob], tabs, s1, s2, kind=opt, lr=lr, step=step)
+        for t in range(cfg.T):
+            gw = gpu_table_rows(emb, cfg, t, "w")
+            if dyadic:
+                assert np.array_equal(gw, tabs[t]) or _close(gw, tabs[t]), f"table {t} step {step}"
+            assert_close(gw, tabs[t], what=f"weights t{t} step {step}")
+            assert_close(gpu_table_rows(emb, cfg, t, "s1"), s1[t], what=f"state1 t{t}")
+            if s2:
+                assert_close(gpu_table_rows(emb, cfg, t, "s2"), s2[t], what=f"state2 t{t}")
+    return emb, tabs
+
+
+def _close(a, b):
+    return np.all(np.abs(a - b) <= 1e-6 + 1e-5 * np.abs(b))
+
+
+# ------------------------------------------------------------------------------------------
+def test_toy_sum_adagrad_bit_exact():
+    cfg = dc.toy()
+    emb = gpu_embedding(cfg)
+    m, tabs = oracle_model(cfg), oracle_tables(cfg)
+    b, dy = make_batch(cfg, 0, 0), make_dy(cfg, 0, 0)
+    ids, off = to_dev(b)
+    out = emb.forward(ids, off, cfg.batch).cpu().numpy()
+    ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy)
+    assert np.array_equal(out, oracle.forward(m, ob, tabs, cfg.out_width))
+    w0 = [gpu_table_rows(emb, cfg, t) for t in range(cfg.T)]
+    emb.backward_update(torch.from_numpy(dy).cuda(), lr=0.05, step=1)
+    emb.check()
+    acc = [np.full_like(t, 0.1) for t in tabs]
+    oracle.backward_update(m, [ob], tabs, acc, lr=0.05)
+    for t in range(cfg.T):
+        _, cnt = oracle.table_grad(m, [ob], t)
+        gw = gpu_table_rows(emb, cfg, t)
+        assert np.array_equal(gw, tabs[t]), f"table {t}: dyadic dY must give a bit-exact update"
+        assert np.array_equal(gpu_table_rows(emb, cfg, t, "s1"), acc[t])
+        # an update touches only looked-up rows
+        assert np.array_equal(gw[cnt == 0], w0[t][cnt == 0])
+        assert not np.array_equal(gw[cnt > 0], w0[t][cnt > 0])
+
+
+@pytest.mark.parametrize("pool", [dc.POOL_SUM, dc.POOL_MEAN])
+@pytest.mark.parametrize("mode", [dc.IDS_HASH, dc.IDS_ROWS])
+def test_toy_pool_modes_three_steps(pool, mode):
+    run_step(dc.toy(pool=pool, id_mode=mode), steps=3, dyadic=(pool == dc.POOL_SUM))
+
+
+def test_toy_continuous_dy():
+    run_step(dc.toy(), dyadic=False, steps=2)
+
+
+@pytest.mark.parametrize("steps", [1, 3])
+def test_toy_adam_lazy(steps):
+    run_step(dc.toy(), opt=oracle.OPT_ADAM, steps=steps, dyadic=False, lr=0.01)
+
+
+def test_multipack_wdl_small():
+    cfg = dc.scaled(dc.wdl(), batch=48, rows_div=1000)  # 200 fields, 4 packs, bags 1..50
+    run_step(cfg, steps=2)
+
+
+def test_multipack_split_plan_same_results():
+    cfg = dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    b = make_batch(cfg, 0, 1)
+    outs = []
+    for split in (False, True):
+        emb = gpu_embedding(cfg, split=split)
+        ids, off = to_dev(b)
+        outs.append(emb.forward(ids, off, cfg.batch).cpu().numpy())
+        if split:
+            assert emb.n_packs > 4
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_packed_equals_unpacked_per_field():
+    """Packed (one fused pass per dim-pack) == unpacked (one context per field: the per-field
+    operator chain of PAPER.md Fig. packing a), bit-exact forward; updates agree."""
+    cfg = dc.scaled(dc.wdl(), batch=40, rows_div=2000).replace(alpha=1.1)
+    b, dy = make_batch(cfg, 0, 2), make_dy(cfg, 0, 2)
+    emb = gpu_embedding(cfg)
+    ids, off = to_dev(b)
+    packed = emb.forward(ids, off, cfg.batch).cpu().numpy()
+    emb.backward_update(torch.from_numpy(dy).cuda(), lr=0.05, step=1)
+    B = cfg.batch
+    import paper_2204_04903_b200 as pb
+    for f in range(0, cfg.F, 37):
+        t = int(cfg.field_to_table[f])
+        e1 = pb.PackedEmbedding([0], cfg.table_rows[[t]], cfg.table_dim[[t]], max_batch=B, max_ids=B * 60,
+                                table_salt=cfg.table_salt[[t]], pool=cfg.pool, id_mode=cfg.id_mode)
+        w = table_values_np(cfg.seed, t, np.arange(cfg.table_rows[t]), int(cfg.table_dim[t]))
+        e1.weights[0].copy_(torch.from_numpy(w))
+        lo, hi = int(b.offsets[f * B]), int(b.offsets[(f + 1) * B])
+        ids1 = torch.from_numpy(b.ids[lo:hi].copy()).cuda()
+        off1 = torch.from_numpy((b.offsets[f * B:(f + 1) * B + 1] - lo).astype(np.int32)).cuda()
+        o1 = e1.forward(ids1, off1, B).cpu().numpy()
+        c, D = int(cfg.field_col[f]), int(cfg.table_dim[t])
+        assert np.array_equal(o1, packed[:, c:c + D]), f"field {f}"
+        # the packed update of this field's table equals the unpacked one when t has one field
+        e1.backward_update(torch.from_numpy(np.ascontiguousarray(dy[:, c:c + D])).cuda(), lr=0.05, step=1)
+        assert_close(e1.weights[0].cpu().numpy(), gpu_table_rows(emb, cfg, t), what=f"update field {f}")
+
+
+def test_long_rows_chunked_path():
+    """Tiny tables make every row hot (> 256 occurrences): the chunked backward path."""
+    cfg = dc.toy(batch=1024).replace(table_rows=np.array([3, 5, 2, 7, 1, 4, 6, 3], np.int64),
+                                     bags=[("uniform", 0, 8)] * 8)
+    run_step(cfg, steps=2, dyadic=True)
+    run_step(cfg, steps=1, dyadic=False)
+
+
+def test_empty_and_degenerate_batches():
+    cfg = dc.toy()
+    emb = gpu_embedding(cfg)
+    m, tabs = oracle_model(cfg), oracle_tables(cfg)
+    B = cfg.batch
+    # every bag empty (N = 0)
+    ids = torch.empty(0, dtype=torch.int64, device="cuda")
+    off = torch.zeros(cfg.F * B + 1, dtype=torch.int32, device="cuda")
+    out = emb.forward(ids, off, B)
+    assert (out == 0).all()
+    w0 = [w.clone() for w in emb.weights]
+    emb.backward_update(torch.ones(B, cfg.out_width, device="cuda"), lr=0.1, step=1)
+    emb.check()
+    assert all(torch.equal(a, b) for a, b in zip(w0, emb.weights))
+    # batch of 1 sample, one id in one field
+    off1 = np.zeros(cfg.F + 1, np.int32)
+    off1[3 + 1:] = 1
+    ids1 = np.array([12345], np.int64)
+    out = emb.forward(torch.from_numpy(ids1).cuda(), torch.from_numpy(off1).cuda(), 1).cpu().numpy()
+    ref = oracle.forward(m, oracle.OracleBatch(1, ids1, off1), tabs, cfg.out_width)
+    assert np.array_equal(out, ref)
+    # batch 0
+    emb.forward(ids, torch.zeros(1, dtype=torch.int32, device="cuda"), 0)
+    emb.check()
+
+
+def test_capacity_and_state_errors():
+    import paper_2204_04903_b200 as pb
+
+    cfg = dc.toy()
+    emb = gpu_embedding(cfg, max_ids=100)
+    b = make_batch(cfg, 0, 0)
+    ids, off = to_dev(b)
+    with pytest.raises(pb.PicassoError):
+        emb.forward(ids, off, cfg.batch)  # more ids than max_ids
+    with pytest.raises(pb.PicassoError):
+        emb.backward_update(torch.zeros(cfg.batch, cfg.out_width, device="cuda"), lr=0.1, step=1)
+
+
+def test_rows_mode_out_of_range_is_latched():
+    import paper_2204_04903_b200 as pb
+
+    cfg = dc.toy(id_mode=dc.IDS_ROWS)
+    emb = gpu_embedding(cfg)
+    b = make_batch(cfg, 0, 0)
+    bad = b.ids.copy()
+    bad[5] = cfg.table_rows[0] + 7
+    ids = torch.from_numpy(bad).cuda()
+    off = torch.from_numpy(b.offsets).cuda()
+    emb.forward(ids, off, cfg.batch)
+    with pytest.raises(pb.PicassoError):
+        emb.check()
+
+
+def test_deterministic_rerun():
+    cfg = dc.scaled(dc.wdl(), batch=64, rows_div=5000).replace(alpha=1.3)
+    res = []
+    for _ in range(2):
+        emb = gpu_embedding(cfg)
+        b, dy = make_batch(cfg, 0, 0), make_dy(cfg, 0, 0, dyadic=False)
+        ids, off = to_dev(b)
+        out = emb.forward(ids, off, cfg.batch).clone()
+        emb.backward_update(torch.from_numpy(dy).cuda(), lr=0.05, step=1)
+        torch.cuda.synchronize()
+        res.append((out.cpu().numpy(), [w.cpu().numpy() for w in emb.weights]))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][1], res[1][1]))
+
+
+def test_criteo_small_shape():
+    cfg = dc.scaled(dc.criteo(), batch=2048, rows_div=1000)
+    run_step(cfg, steps=2, check_intermediates=True)
