@@ -21,6 +21,9 @@ from .abi import (  # noqa: F401
     picasso_packed_lookup_bwd_update,
     picasso_packed_lookup_fwd,
     picasso_workspace_size,
+    picasso_profile_enable,
+    picasso_profile_read,
+    picasso_unique_offsets,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
 from .embedding import PackedEmbedding  # noqa: F401

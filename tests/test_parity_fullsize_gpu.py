@@ -1,0 +1,89 @@
+"""Full-size parity at BASELINE.json configs[1] (Criteo-shaped: 26 fields, dim 128, batch
+16,384, 46.875M rows = 24 GB fp32 tables) in the launch configuration bench.py times.
+The oracle cannot hold the tables, so it checks (a) the whole unique/inverse of the pack
+(bit-exact), (b) a random sample of pooled segments (bit-exact), (c) a sample of touched
+rows — including the hottest — after the Adagrad step (1e-5/1e-6), and (d) a sample of
+untouched rows (bitwise unchanged).  Table rows for the oracle are regenerated on the host
+from the same seeded generator."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from datagen import configs as dc
+from datagen import make_batch, make_dy, table_values_np
+from harness import assert_close, gpu_embedding, oracle_model, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
+def _rows_values(cfg, t_arr, r_arr, ld):
+    vals = np.zeros((len(t_arr), ld), np.float32)
+    for t in np.unique(t_arr):
+        sel = t_arr == t
+        vals[sel, :cfg.table_dim[t]] = table_values_np(cfg.seed, int(t), r_arr[sel], int(cfg.table_dim[t]))
+    return vals
+
+
+@pytest.mark.parametrize("dyadic", [True, False])
+def test_criteo_fullsize_sampled(dyadic):
+    cfg = dc.criteo()
+    b = make_batch(cfg, 0, 7)
+    dy = make_dy(cfg, 0, 7, dyadic=dyadic)
+    emb = gpu_embedding(cfg, max_ids=b.n_ids)
+    m = oracle_model(cfg)
+    ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy)
+    ids, off = to_dev(b)
+    out = emb.forward(ids, off, cfg.batch)
+    torch.cuda.synchronize()
+    # (a) unique / inverse of the single pack, whole stream
+    keys = oracle.pack_key_stream(m, emb.plan["field_to_pack"], emb.plan["table_base"], ob, 0)
+    u_ref, inv_ref = oracle.unique(keys)
+    assert np.array_equal(emb.unique(0).cpu().numpy(), u_ref)
+    assert np.array_equal(emb.inverse(0).cpu().numpy(), inv_ref)
+    # (b) sampled segments
+    rng = np.random.default_rng(0)
+    qf = rng.integers(0, cfg.F, 3000).astype(np.int32)
+    qs = rng.integers(0, cfg.batch, 3000).astype(np.int32)
+    rt, rr = oracle.segment_rows(m, ob, qf, qs)
+    ref = oracle.forward_sampled(m, ob, rt, rr, _rows_values(cfg, rt, rr, 128), qf, qs)
+    got = out.cpu().numpy()
+    for i in range(len(qf)):
+        c = int(cfg.field_col[qf[i]])
+        assert np.array_equal(got[qs[i], c:c + 128], ref[i]), f"segment {i}"
+    # (c) touched rows: hottest 64 + 1000 random; (d) 500 random rows (mostly untouched)
+    tb = emb.plan["table_base"]
+    allt, allr = oracle.segment_rows(m, ob, np.repeat(np.arange(cfg.F, dtype=np.int32), cfg.batch),
+                                     np.tile(np.arange(cfg.batch, dtype=np.int32), cfg.F))
+    key = tb[allt] + allr
+    uk, cnt = np.unique(key, return_counts=True)
+    pick = np.concatenate([uk[np.argsort(-cnt, kind="stable")[:64]], rng.choice(uk, 1000, replace=False),
+                           rng.integers(0, int(cfg.table_rows.sum()), 500)])
+    pick = np.unique(pick)
+    qt = (np.searchsorted(tb, pick, side="right") - 1).astype(np.int32)
+    qr = pick - tb[qt]
+    w0 = _rows_values(cfg, qt, qr, 128)
+    G, n = oracle.row_grads(m, [ob], qt, qr, 128)
+    w_ref, s_ref = w0.copy(), np.full_like(w0, 0.1)
+    oracle.apply_update(G, n, w_ref, s_ref, lr=0.01)
+    emb.backward_update(torch.from_numpy(dy).cuda(), lr=0.01, step=1)
+    emb.check()
+    idx = torch.from_numpy(pick).cuda()
+    w_gpu = emb.weights[0].index_select(0, idx).cpu().numpy()
+    s_gpu = emb.state1[0].index_select(0, idx).cpu().numpy()
+    assert (n > 0).sum() >= 1064 - 5 and n.max() > 256  # hot rows take the chunked path
+    assert_close(w_gpu, w_ref, what="weights")
+    if dyadic:
+        assert np.array_equal(w_gpu, w_ref) and np.array_equal(s_gpu, s_ref)
+    else:
+        short = n <= 256  # rows summed sequentially in ascending order are bit-exact
+        assert np.array_equal(w_gpu[short], w_ref[short])
+        assert_close(s_gpu, s_ref, rtol=1e-4, what="state (long rows: fixed chunk order)")
+    assert np.array_equal(w_gpu[n == 0], w0[n == 0])
