@@ -19,9 +19,10 @@
  *
  * Precision: the paper trains in full precision ("full-precision training", fp32,
  * PAPER.md L577; accuracy loss "intolerable", L164).  The oracle therefore computes in
- * fp32 with every reduction summed sequentially left to right from +0.0f (SPEC.md
- * L157, L165: "fixed left-to-right order, no reassociation").  Built with
- * -ffp-contract=off -fno-fast-math so no FMA contraction occurs.
+ * fp32; the forward SegmentReduction sums sequentially left to right from +0.0f (SPEC.md
+ * L157, L165: "fixed left-to-right order, no reassociation"); the backward's per-row
+ * gradient sum, whose precision the paper does not fix, accumulates in fp64 and rounds
+ * once (reading O6).  Built with -ffp-contract=off -fno-fast-math (no FMA contraction).
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC worked examples, brute force on
  * tiny inputs, float64 dense incidence-matrix closed forms (Y = A·W, dW = A^T·dY),
@@ -355,11 +356,15 @@ int32_t oracle_partition(int64_t U, const int64_t *uniq, int32_t W, int64_t *out
  * order (reading O6/O9).  For each table t and row:
  *   G_t[row] = sum over occurrences (r, f with table t in ascending f, b, j) of
  *              dY_r[b][col(f)+.]   (mean: dY_r[b][col(f)+.] / (float)len)
- * summed sequentially from +0.0f in that order ("mirror image").
+ * ("mirror image").  Each contribution is formed in fp32 (the paper's
+ * precision: dY is fp32, mean divides in fp32), the sum is accumulated in fp64 in that order
+ * and rounded once to fp32 (reading O6: the paper fixes fp32 for parameters and activations,
+ * not the precision of the gradient reduction; fp64 accumulation makes G = fp32(exact sum)
+ * up to 2^-53-relative error, independent of summation order).
  * Touched = rows with >= 1 occurrence.  Untouched rows are not written. */
 struct GradAcc {
-    std::vector<int64_t> order;                        /* rows in first-touch order */
-    std::unordered_map<int64_t, std::vector<float>> g; /* row -> G */
+    std::vector<int64_t> order;                         /* rows in first-touch order */
+    std::unordered_map<int64_t, std::vector<double>> g; /* row -> G (fp64 accumulator) */
 };
 
 static int32_t accumulate_grads(const oracle_model *m, int32_t R, const oracle_batch *batches,
@@ -382,13 +387,13 @@ static int32_t accumulate_grads(const oracle_model *m, int32_t R, const oracle_b
                         return OR_ID_RANGE;
                     auto it = acc[t].g.find(row);
                     if (it == acc[t].g.end()) {
-                        it = acc[t].g.emplace(row, std::vector<float>(D, 0.0f)).first;
+                        it = acc[t].g.emplace(row, std::vector<double>(D, 0.0)).first;
                         acc[t].order.push_back(row);
                     }
                     for (int32_t d = 0; d < D; ++d) {
                         float c = dy[d];
                         if (m->pool == OR_POOL_MEAN) c = c / (float)len; /* reading O7 */
-                        it->second[d] = it->second[d] + c;
+                        it->second[d] = it->second[d] + (double)c;
                     }
                 }
             }
@@ -437,7 +442,8 @@ int32_t oracle_backward_update(const oracle_model *m, int32_t R, const oracle_ba
     for (int32_t t = 0; t < m->n_tables; ++t) {
         const int32_t D = m->table_dim[t];
         for (int64_t row : acc[t].order) {
-            const std::vector<float> &g = acc[t].g[row];
+            const std::vector<double> &g64 = acc[t].g[row];
+            std::vector<float> g(g64.begin(), g64.end()); /* one rounding to fp32 */
             update_row(opt, step, D, g.data(), tables[t] + row * D, state1[t] + row * D,
                        state2 ? (state2[t] ? state2[t] + row * D : nullptr) : nullptr);
         }
@@ -456,8 +462,8 @@ int32_t oracle_table_grad(const oracle_model *m, int32_t R, const oracle_batch *
     std::memset(G, 0, sizeof(float) * (size_t)m->table_rows[t] * D);
     if (count) std::memset(count, 0, sizeof(int64_t) * (size_t)m->table_rows[t]);
     for (int64_t row : acc[t].order) {
-        const std::vector<float> &g = acc[t].g[row];
-        for (int32_t d = 0; d < D; ++d) G[row * D + d] = g[d];
+        const std::vector<double> &g = acc[t].g[row];
+        for (int32_t d = 0; d < D; ++d) G[row * D + d] = (float)g[d];
     }
     if (count) {
         for (int32_t r = 0; r < R; ++r) {
@@ -482,10 +488,10 @@ int32_t oracle_row_grads(const oracle_model *m, int32_t R, const oracle_batch *b
                          int64_t *count) {
     std::unordered_map<uint64_t, int64_t> where;
     where.reserve((size_t)n_q * 2 + 1);
+    std::vector<double> G64((size_t)n_q * ld, 0.0);
     for (int64_t q = 0; q < n_q; ++q) {
         where[((uint64_t)q_table[q] << 48) ^ (uint64_t)q_row[q]] = q;
         count[q] = 0;
-        for (int64_t d = 0; d < ld; ++d) G[q * ld + d] = 0.0f;
     }
     for (int32_t r = 0; r < R; ++r) {
         const oracle_batch *bt = &batches[r];
@@ -504,17 +510,18 @@ int32_t oracle_row_grads(const oracle_model *m, int32_t R, const oracle_batch *b
                     auto it = where.find(((uint64_t)t << 48) ^ (uint64_t)row);
                     if (it == where.end()) continue;
                     const float *dy = bt->dy + (int64_t)b * bt->dy_stride + m->field_col[f];
-                    float *g = G + it->second * ld;
+                    double *g = G64.data() + it->second * ld;
                     for (int32_t d = 0; d < D; ++d) {
                         float c = dy[d];
                         if (m->pool == OR_POOL_MEAN) c = c / (float)len;
-                        g[d] = g[d] + c;
+                        g[d] = g[d] + (double)c;
                     }
                     count[it->second] += 1;
                 }
             }
         }
     }
+    for (size_t i = 0; i < G64.size(); ++i) G[i] = (float)G64[i];
     return OR_OK;
 }
 
