@@ -265,7 +265,7 @@ def main():
 
     # unique counts of the last timed step (for algorithmic bytes)
     U_pref = np.array(emb.unique_offsets_host(), np.int64)
-    U_by_pack = list(np.diff(U_pref))
+    U_by_pack = [int(x) for x in np.diff(U_pref)]
     last_b = batches[(args.warmup + args.steps - 1) % args.nbatches]
     alg = algorithmic_bytes(cfg, B, last_b.n_ids, U_by_pack, emb.plan)
     per_phase = {k: v / max(ncalls, 1) for k, v in phase_ms.items()}

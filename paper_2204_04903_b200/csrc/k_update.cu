@@ -8,10 +8,13 @@
 //   lazy Adam m += (G-m)(1-b1); v += (G*G-v)(1-b2); w -= ss * (m / (sqrt(v) + eps))
 // Fusing the two keeps G in registers: per touched row the kernel reads dY rows once and
 // the weight/state rows once, writes weight/state once (no G round trip through HBM).
+// Each contribution is formed in fp32 (dY, dY/len) and accumulated in fp64, then rounded
+// once to fp32 (reading O6): the result is fp32(exact sum) whatever the summation order, so
+// the chunked hot-row path and the oracle agree even when G nearly cancels.
 //
 //   k_csr_bounds     : row boundaries in the uid-sorted occurrence list (ustart)
 //   k_segsum_update  : one sub-warp per unique row with <= kLongRow occurrences; sums in
-//                      ascending position (bit-identical to the sequential definition)
+//                      ascending position
 //   k_long_update    : one block per hot row (Zipf heads reach 1e4-1e6 occurrences): the
 //                      block's sub-warps sum fixed strided chunks, combined in sub-warp order
 //                      (deterministic), then one update
@@ -40,9 +43,25 @@ struct Geo {
     static constexpr int VPL = V4 / LANES;
 };
 
+struct dbl4 {
+    double x, y, z, w;
+};
+__device__ __forceinline__ dbl4 zero4d() { return dbl4{0.0, 0.0, 0.0, 0.0}; }
+__device__ __forceinline__ dbl4 add4d(dbl4 a, float4 b) {
+    return dbl4{__dadd_rn(a.x, (double)b.x), __dadd_rn(a.y, (double)b.y), __dadd_rn(a.z, (double)b.z),
+                __dadd_rn(a.w, (double)b.w)};
+}
+__device__ __forceinline__ dbl4 add4d(dbl4 a, dbl4 b) {
+    return dbl4{__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y), __dadd_rn(a.z, b.z), __dadd_rn(a.w, b.w)};
+}
+__device__ __forceinline__ float4 round4(dbl4 a) {
+    return make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(a.z),
+                       __double2float_rn(a.w));
+}
+
 template <int VPL>
 __device__ __forceinline__ void accumulate_one(const UpdateArgs &a, int32_t seg, const float *dyl, int LANES,
-                                               float4 *g) {
+                                               dbl4 *g) {
     const int32_t f = seg / a.B;
     const int32_t b = seg - f * a.B;
     const float *p = dyl + (int64_t)b * a.dy_stride + a.finfo[f].col;
@@ -55,12 +74,12 @@ __device__ __forceinline__ void accumulate_one(const UpdateArgs &a, int32_t seg,
         for (int q = 0; q < VPL; ++q) c[q] = div4(c[q], len);
     }
 #pragma unroll
-    for (int q = 0; q < VPL; ++q) g[q] = add4(g[q], c[q]);
+    for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], c[q]);
 }
 
 template <int D>
 __device__ __forceinline__ void accumulate_range(const UpdateArgs &a, int32_t i0, int32_t i1, int32_t step,
-                                                 int li, float4 *g) {
+                                                 int li, dbl4 *g) {
     constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
     const float *dyl = a.dy + li * 4;
     int32_t i = i0;
@@ -86,7 +105,7 @@ __device__ __forceinline__ void accumulate_range(const UpdateArgs &a, int32_t i0
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int q = 0; q < VPL; ++q) g[q] = add4(g[q], c[u][q]);
+            for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], c[u][q]);
     }
     for (; i < i1; i += step) accumulate_one<VPL>(a, __ldg(a.sorted_seg + i), dyl, LANES, g);
 }
@@ -147,12 +166,15 @@ __global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
             if (li == 0) a.long_list[atomicAdd(a.long_cnt, 1)] = (int32_t)u;
             continue;
         }
-        float4 g[VPL];
+        dbl4 g[VPL];
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) g[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < VPL; ++q) g[q] = zero4d();
         accumulate_range<D>(a, i0, i1, 1, li, g);
+        float4 g32[VPL];
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) g32[q] = round4(g[q]);
         const int64_t row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
-        apply_update<D>(a, row, li, g);
+        apply_update<D>(a, row, li, g32);
     }
 }
 
@@ -160,7 +182,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_long_update(UpdateArgs a) {
     constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
     constexpr int G = 256 / LANES;
-    __shared__ float4 part[G][LANES * VPL];
+    __shared__ dbl4 part[G][LANES * VPL];
     const int li = threadIdx.x % LANES;
     const int gi = threadIdx.x / LANES;
     const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
@@ -169,22 +191,25 @@ __global__ void __launch_bounds__(256) k_long_update(UpdateArgs a) {
         const int32_t u = a.long_list[e];
         if (u < u0 || u >= u1) continue;  // block-uniform
         const int32_t i0 = __ldg(a.ustart + u), i1 = __ldg(a.ustart + u + 1);
-        float4 g[VPL];
+        dbl4 g[VPL];
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) g[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < VPL; ++q) g[q] = zero4d();
         accumulate_range<D>(a, i0 + gi, i1, G, li, g);
 #pragma unroll
         for (int q = 0; q < VPL; ++q) part[gi][q * LANES + li] = g[q];
         __syncthreads();
         if (gi == 0) {
-            float4 t[VPL];
+            dbl4 t[VPL];
 #pragma unroll
             for (int q = 0; q < VPL; ++q) t[q] = part[0][q * LANES + li];
             for (int x = 1; x < G; ++x)
 #pragma unroll
-                for (int q = 0; q < VPL; ++q) t[q] = add4(t[q], part[x][q * LANES + li]);
+                for (int q = 0; q < VPL; ++q) t[q] = add4d(t[q], part[x][q * LANES + li]);
+            float4 g32[VPL];
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) g32[q] = round4(t[q]);
             const int64_t row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
-            apply_update<D>(a, row, li, t);
+            apply_update<D>(a, row, li, g32);
         }
         __syncthreads();
     }

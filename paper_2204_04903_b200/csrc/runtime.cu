@@ -309,7 +309,8 @@ static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t 
 
 extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets,
                                                     int32_t batch, int64_t n_ids, float *out, void *stream) {
-    if (!ctx || !offsets || !out || batch < 0 || n_ids < 0 || (n_ids > 0 && !ids)) return PICASSO_ERR_INVALID_ARG;
+    if (!ctx || !offsets || (!out && batch > 0) || batch < 0 || n_ids < 0 || (n_ids > 0 && !ids))
+        return PICASSO_ERR_INVALID_ARG;
     if (!ctx->bound) return PICASSO_ERR_STATE;
     if (batch > ctx->opts.max_batch || n_ids > ctx->opts.max_ids) return PICASSO_ERR_CAPACITY;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -83,7 +83,7 @@ def test_criteo_fullsize_sampled(dyadic):
     if dyadic:
         assert np.array_equal(w_gpu, w_ref) and np.array_equal(s_gpu, s_ref)
     else:
-        short = n <= 256  # rows summed sequentially in ascending order are bit-exact
-        assert np.array_equal(w_gpu[short], w_ref[short])
-        assert_close(s_gpu, s_ref, rtol=1e-4, what="state (long rows: fixed chunk order)")
+        # fp64 accumulation on both sides: G = fp32(exact sum) except at rounding ties
+        assert_close(s_gpu, s_ref, what="state")
+        assert (w_gpu == w_ref).all(axis=1).mean() > 0.99
     assert np.array_equal(w_gpu[n == 0], w0[n == 0])
