@@ -26,6 +26,11 @@ struct Slot {
 
 enum ErrBits : int { ERR_ID_RANGE = 1, ERR_CAPACITY = 2 };
 
+// fp64 accumulator of four columns (gradient sums, reading O6)
+struct alignas(16) dbl4 {
+    double x, y, z, w;
+};
+
 constexpr unsigned long long kEmptyKey = ~0ull;
 
 // SplitMix64 output mix (reading O4 of DESIGN.md).

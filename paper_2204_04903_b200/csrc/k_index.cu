@@ -6,17 +6,20 @@
 // its field-major index j by a binary search, no copy).
 //
 //   k_field_prep   : per-field ID ranges and the packed-stream layout (one small block)
-//   k_dedup_insert : row mapping, pack key, segment id; warp pre-dedup (__match_any_sync) and
+//   k_dedup_insert : row mapping, pack key; warp pre-dedup (__match_any_sync) and
 //                    one open-addressing insert per distinct key per warp; atomicMin keeps the
 //                    first position of every key
 //   k_flag_count   : first-occurrence flags, counted per 2048-position tile
 //   k_assign       : tile-ordered exclusive scan -> global uid in first-occurrence order;
-//                    unique keys; inverse index; per-pack uid ranges
+//                    unique keys; per-pack uid ranges
+//   k_inverse      : inverse index (global uid per packed position)
 // Unique order is the first-occurrence order of each pack's key stream (reading O1), and
 // because packs occupy contiguous position ranges the per-pack uid of a key is its global
 // uid minus pack_ustart[p].
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+
+#include <algorithm>
 
 #include "kernels.h"
 
@@ -81,16 +84,14 @@ __global__ void __launch_bounds__(256) k_dedup_insert(IndexArgs a) {
     const bool valid = g < a.N;
     unsigned long long gkey = 0;
     if (valid) {
-        // packed position -> pm field -> field-major index j -> sample b
+        // packed position -> pm field -> field-major index j (segment ids are written by the
+        // pool kernel, which walks segments anyway)
         const int64_t k = upper_bound_dev(a.gstart_pm, 0, a.F + 1, (int32_t)g) - 1;
         const int f = __ldg(a.pm_fields + k);
         const int64_t j = (int64_t)__ldg(a.id_start + f) + (g - __ldg(a.gstart_pm + k));
         const FieldInfo fi = a.finfo[f];
         const int64_t row = row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
         gkey = (unsigned long long)(__ldg(a.pack_key_off + fi.pack) + fi.base + row);
-        const int64_t s0 = (int64_t)f * a.B;
-        const int64_t b = upper_bound_dev(a.offsets, s0, s0 + a.B + 1, (int32_t)j) - 1 - s0;
-        a.seg_of[g] = (int32_t)(s0 + b);
     }
     // warp pre-dedup: lanes holding the same key elect the lowest lane (= smallest g)
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
@@ -165,6 +166,10 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
         if (first[i]) {
             a.table[slot[i]].uid = uid;
             a.unique_gkey[uid] = a.table[slot[i]].key;
+            // the first position of a non-empty pack is always a first occurrence
+            const int64_t g = g0 + i;
+            const int64_t p = upper_bound_dev(a.pack_gstart, 0, a.P + 1, (int32_t)g) - 1;
+            if (p < a.P && __ldg(a.pack_gstart + p) == (int32_t)g) a.pack_ustart[p] = uid;
             ++uid;
         }
     }
@@ -173,21 +178,14 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
 __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g < a.N) a.inverse[g] = a.table[a.slot_of[g]].uid;
-}
-
-// pack_ustart[p] = #uniques whose global key lies below pack p's key range (keys of later
-// packs are larger and their uids later, so the predicate is monotone in uid).
-__global__ void k_pack_ustart(IndexArgs a) {
-    const int p = threadIdx.x;
-    if (p > a.P) return;
-    const int32_t U = *a.d_total;
-    const unsigned long long lim = (unsigned long long)a.pack_key_off[p];
-    int64_t lo = 0, hi = U;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (a.unique_gkey[mid] < lim) lo = mid + 1; else hi = mid;
+    if (g == 0) {  // uid ranges of empty packs (and the end) — k_assign filled the others
+        int32_t next = *a.d_total;
+        a.pack_ustart[a.P] = next;
+        for (int p = a.P - 1; p >= 0; --p) {
+            if (a.pack_gstart[p] == a.pack_gstart[p + 1]) a.pack_ustart[p] = next;
+            next = a.pack_ustart[p];
+        }
     }
-    a.pack_ustart[p] = (p == a.P) ? U : (int32_t)lo;
 }
 
 __global__ void k_scan_blocks(const int32_t *cnt, int32_t *off, int32_t n, int32_t *total) {
@@ -215,11 +213,10 @@ void launch_dedup_assign(const IndexArgs &a, cudaStream_t s) {
         k_flag_count<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
         k_scan_blocks<<<1, 1024, 0, s>>>(a.blk_cnt, a.blk_off, (int32_t)nb, a.d_total);
         k_assign<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
-        k_inverse<<<(unsigned)((a.N + 255) / 256), 256, 0, s>>>(a);
     } else {
         cudaMemsetAsync(a.d_total, 0, sizeof(int32_t), s);
     }
-    k_pack_ustart<<<1, ((a.P + 1 + 31) / 32) * 32, 0, s>>>(a);
+    k_inverse<<<(unsigned)std::max<int64_t>(1, (a.N + 255) / 256), 256, 0, s>>>(a);
 }
 
 }  // namespace picasso

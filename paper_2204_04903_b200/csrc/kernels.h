@@ -62,6 +62,9 @@ struct PoolArgs {
     int32_t Fp;                 // fields in this pack
     const int32_t *pack_fields; // [Fp] field indices (ascending)
     const FieldInfo *finfo;
+    const int32_t *field_gstart; // [F] packed-stream start of each field
+    const int32_t *id_start;     // [F] offsets[f*B]
+    int32_t *seg_of;             // [N] out: global segment f*B+b of each packed position
     int32_t id_mode, pool_mean;
     const float *weight;        // [rows, D]
     float *out;
@@ -88,11 +91,15 @@ struct UpdateArgs {
     int32_t opt;                 // 0 adagrad, 1 adam
     float lr, eps, beta1, beta2, adam_ss;
     float *weight, *state1, *state2;
-    int32_t *long_list;          // [cap]
-    int32_t *long_cnt;           // [1]
+    int32_t *long_list;          // [cap] rows deferred to the chunked path (this pack)
+    int32_t *long_cnt;           // [1]   this pack's counter
+    int32_t *chunk_off;          // [cap+1]
+    dbl4 *partial;               // [chunks, D/4] fp64 chunk partial sums
 };
-void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, cudaStream_t s);
+void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, int32_t n_cnt,
+                       cudaStream_t s);
 void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
-void launch_long_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
+int launch_long_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);  // returns #launches
+size_t long_partial_doubles(int64_t N, int maxD);
 
 }  // namespace picasso

@@ -65,7 +65,8 @@ struct picasso_ctx {
     int *err = nullptr;
     unsigned long long *unique_gkey = nullptr;
     int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
-    int32_t *ustart = nullptr, *long_list = nullptr;
+    int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr;
+    dbl4 *partial = nullptr;
     std::vector<float *> w, s1, s2;
     // step state
     bool fwd_done = false;
@@ -127,7 +128,7 @@ struct picasso_ctx {
         blk_cnt = c.take<int32_t>(nblk);
         blk_off = c.take<int32_t>(nblk);
         d_total = c.take<int32_t>(1);
-        long_cnt = c.take<int32_t>(1);
+        long_cnt = c.take<int32_t>(P);
         err = c.take<int>(1);
         unique_gkey = c.take<unsigned long long>(N);
         k_a = c.take<int32_t>(N);
@@ -138,6 +139,10 @@ struct picasso_ctx {
         scratch = c.take<int32_t>(scan_scratch_ints((int64_t)radix_hist_ints(N)) + 16);
         ustart = c.take<int32_t>(N + 1);
         long_list = c.take<int32_t>(N / (kLongRow + 1) + 2);
+        chunk_off = c.take<int32_t>(N / (kLongRow + 1) + 3);
+        int maxD = 4;
+        for (int32_t d : pack_dim) maxD = std::max(maxD, d);
+        partial = reinterpret_cast<dbl4 *>(c.take<double>(long_partial_doubles(N, maxD)));
         return c.off + kAlign;
     }
 };
@@ -324,7 +329,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     launch_dedup_insert(a, s);
     launch_dedup_assign(a, s);
     ctx->mark(0, false, s);
-    ctx->launches_fwd += 1 + (n_ids > 0 ? 1 + 4 : 0) + 1;
+    ctx->launches_fwd += 1 + (n_ids > 0 ? 4 : 0) + 1;  // prep, insert+flag+scan+assign, inverse
     ctx->mark(1, true, s);
     for (int32_t p = 0; p < ctx->P; ++p) {
         PoolArgs pa{};
@@ -334,6 +339,9 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
         pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
         pa.finfo = ctx->finfo;
+        pa.field_gstart = ctx->field_gstart;
+        pa.id_start = ctx->id_start;
+        pa.seg_of = ctx->seg_of;
         pa.id_mode = ctx->opts.id_mode;
         pa.pool_mean = ctx->opts.pool == PICASSO_POOL_MEAN;
         pa.weight = ctx->w[p];
@@ -364,7 +372,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     ctx->mark(2, true, s);
     radix_sort_pairs(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N,
                      bits_for(std::max<int64_t>(N - 1, 1)), ctx->hist, ctx->scratch, s, &ctx->launches_bwd);
-    launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, s);
+    launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
     ctx->mark(2, false, s);
     ctx->launches_bwd += N > 0 ? 1 : 0;
     ctx->mark(3, true, s);
@@ -391,25 +399,18 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
         u.adam_ss = (float)((double)lr * std::sqrt(bc2) / bc1);
     }
     u.long_list = ctx->long_list;
-    u.long_cnt = ctx->long_cnt;
+    u.chunk_off = ctx->chunk_off;
+    u.partial = ctx->partial;
     if (N > 0) {
-        for (int32_t p = 0; p < ctx->P; ++p) {
+        for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
             u.pack = p;
+            u.long_cnt = ctx->long_cnt + p;
             u.pack_key_off = ctx->pack_key_off[p];
             u.weight = ctx->w[p];
             u.state1 = ctx->s1[p];
             u.state2 = ctx->s2[p];
             launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-            ctx->launches_bwd += 1;
-        }
-        for (int32_t p = 0; p < ctx->P; ++p) {
-            u.pack = p;
-            u.pack_key_off = ctx->pack_key_off[p];
-            u.weight = ctx->w[p];
-            u.state1 = ctx->s1[p];
-            u.state2 = ctx->s2[p];
-            launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-            ctx->launches_bwd += 1;
+            ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
         }
     }
     ctx->mark(3, false, s);
