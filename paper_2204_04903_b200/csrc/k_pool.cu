@@ -5,17 +5,19 @@
 //                                                          empty segment: 0)
 //
 // Work decomposition (memory-level parallelism independent of the bag-length mix):
-//  - a warp owns a tile of 32 consecutive segments of the pack in field-major order (k, b), so
-//    the tile's offsets are one coalesced load and its IDs one contiguous range;
-//  - the warp splits into R = 32 / LANES row groups (LANES = D/4 lanes, each lane owns float4
-//    columns: a D = 128 row is one coalesced 512-B request);
-//  - each group walks the flattened (segment, j) stream of its 32/R segments and issues U row
-//    loads at a time (8 at D = 128: 4 KB in flight per warp) regardless of where segment
-//    boundaries fall — one-hot and 50-hot bags keep the same number of loads in flight;
-//  - rows are then added strictly in ascending j per segment (bit-identical to the
-//    sequential definition); a finished segment is written straight into its column block of
-//    the stitched [B, out_width] output with streaming 128-bit stores.
-// The same walk records seg_of[g] (segment of every packed-stream position) for the backward.
+//  - a warp owns a tile of 32 consecutive segments of the pack in field-major order (k, b): the
+//    tile's offsets are one coalesced load and its IDs one contiguous range;
+//  - the warp splits into R = 32 / LANES row groups (LANES = D/4 lanes; each lane owns float4
+//    columns, so a D = 128 row is one coalesced 512-B request); group g takes SPG = 32/R
+//    consecutive segments of the tile;
+//  - the group's (segment, j) pairs form one flattened stream; each lane resolves a different
+//    pair (segment by a 5-step search over the tile's length prefix, raw ID, row hash, row
+//    address), so the scalar work is spread over the lanes instead of repeated by all of them;
+//  - addresses are broadcast with width-LANES shuffles and U rows are loaded at once (8 x 512 B
+//    per warp at D = 128), then added strictly in ascending j per segment (bit-identical to the
+//    sequential definition); a finished segment is written into its column block of the
+//    stitched [B, out_width] output with streaming 128-bit stores.
+// The walk also records seg_of[g] (segment of every packed-stream position) for the backward.
 #include "kernels.h"
 
 namespace picasso {
@@ -25,127 +27,146 @@ struct PoolGeo {
     static constexpr int V4 = D / 4;
     static constexpr int LANES = V4 < 32 ? V4 : 32;
     static constexpr int VPL = V4 / LANES;
-    static constexpr int R = 32 / LANES;    // row groups per warp
-    static constexpr int SPG = 32 / R;      // segments per group per tile
-    static constexpr int U = D >= 64 ? 8 : 4;  // rows in flight per group
+    static constexpr int R = 32 / LANES;               // row groups per warp
+    static constexpr int SPG = 32 / R;                 // segments per group per tile
+    static constexpr int U = 8;                        // rows in flight per group
+    static constexpr int PPL = U > LANES ? U / LANES : 1;  // pairs resolved per lane per round
+    static constexpr int RND = LANES * PPL;            // pairs resolved per round (>= U)
 };
+
+struct SegTile {
+    int32_t cum[8][64];   // per warp: per group, exclusive prefix of its SPG segment lengths
+    int32_t o0[8][32];
+    int32_t sg[8][32];
+    int32_t gb[8][32];    // packed position = j + gb
+    int64_t out[8][32];   // out offset of the segment's column block
+    int64_t base[8][32];  // table base of the segment's field
+    int64_t rows[8][32];
+    uint64_t salt[8][32];
+};
+
+template <int D>
+__device__ __forceinline__ void flush_seg(const PoolArgs &a, float4 *acc, int64_t out_off, int32_t len, int li) {
+    constexpr int LANES = PoolGeo<D>::LANES, VPL = PoolGeo<D>::VPL;
+    float *o = a.out + out_off + li * 4;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+        if (a.pool_mean && len > 0) acc[q] = div4(acc[q], (float)len);
+        stcs_f4(o + q * LANES * 4, acc[q]);
+        acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
 
 template <int D>
 __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
     using Gm = PoolGeo<D>;
-    constexpr int LANES = Gm::LANES, VPL = Gm::VPL, SPG = Gm::SPG, U = Gm::U;
-    __shared__ int32_t s_o0[8][32], s_o1[8][32], s_gb[8][32], s_sg[8][32], s_f[8][32];
-    __shared__ int64_t s_out[8][32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    constexpr int LANES = Gm::LANES, VPL = Gm::VPL, SPG = Gm::SPG, U = Gm::U, PPL = Gm::PPL, RND = Gm::RND;
+    __shared__ SegTile st;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int li = lane % LANES, grp = lane / LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
     const int64_t S = (int64_t)a.Fp * a.B;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * 32; t0 < S; t0 += nwarps * 32) {
+    for (int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32; t0 < S; t0 += nwarps * 32) {
         // ---- tile descriptors: lane i <- segment t0 + i
+        int32_t len = 0;
         {
             const int64_t s = t0 + lane;
-            int32_t o0 = 0, o1 = 0, gb = 0, sg = 0, f = 0;
-            int64_t ob = 0;
             if (s < S) {
                 const int32_t k = (int32_t)(s / a.B);
                 const int32_t b = (int32_t)(s - (int64_t)k * a.B);
-                f = __ldg(a.pack_fields + k);
-                sg = f * a.B + b;
-                o0 = __ldg(a.offsets + sg);
-                o1 = __ldg(a.offsets + sg + 1);
-                gb = __ldg(a.field_gstart + f) - __ldg(a.id_start + f);  // g = j + gb
-                ob = (int64_t)b * a.out_stride + a.finfo[f].col;
+                const int32_t f = __ldg(a.pack_fields + k);
+                const int32_t sg = f * a.B + b;
+                const int32_t o0 = __ldg(a.offsets + sg);
+                len = __ldg(a.offsets + sg + 1) - o0;
+                const FieldInfo fi = a.finfo[f];
+                st.o0[w][lane] = o0;
+                st.sg[w][lane] = sg;
+                st.gb[w][lane] = __ldg(a.field_gstart + f) - __ldg(a.id_start + f);
+                st.out[w][lane] = (int64_t)b * a.out_stride + fi.col;
+                st.base[w][lane] = fi.base;
+                st.rows[w][lane] = fi.rows;
+                st.salt[w][lane] = fi.salt;
             }
-            s_o0[wib][lane] = o0;
-            s_o1[wib][lane] = o1;
-            s_gb[wib][lane] = gb;
-            s_sg[wib][lane] = sg;
-            s_f[wib][lane] = f;
-            s_out[wib][lane] = ob;
+            // group-local inclusive scan of the lengths -> exclusive prefix in cum
+            int32_t x = len;
+#pragma unroll
+            for (int o = 1; o < SPG; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, x, o, SPG);
+                if ((lane % SPG) >= o) x += y;
+            }
+            st.cum[w][lane + (lane / SPG) + 1] = x;  // group g's prefix lives at [g*(SPG+1) ...]
+            if (lane % SPG == 0) st.cum[w][lane + lane / SPG] = 0;
         }
         __syncwarp();
         const int nseg = (int)((S - t0) < 32 ? (S - t0) : 32);
         const int c_lo = grp * SPG, c_hi = min(nseg, c_lo + SPG);
-        // field info of the group's first segment; refreshed when the field changes
-        int cur = c_lo;
-        int32_t j = cur < c_hi ? s_o0[wib][cur] : 0, e = cur < c_hi ? s_o1[wib][cur] : 0;
+        const int32_t *cum = &st.cum[w][grp * (SPG + 1)];  // cum[c - c_lo]
+        const int32_t total = c_hi > c_lo ? cum[c_hi - c_lo] : 0;
         float4 acc[VPL];
 #pragma unroll
         for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int cur = c_lo;
         const float *wb = a.weight + (int64_t)li * 4;
-        while (cur < c_hi) {
-            // ---- collect up to U (segment, j) pairs of the flattened stream
-            int bseg[U];
-            int32_t bj[U];
-            int n = 0;
-            {
-                int c2 = cur;
-                int32_t j2 = j, e2 = e;
+        for (int32_t q0 = 0; q0 < total; q0 += RND) {
+            // ---- each lane resolves PPL pairs of the group's flattened stream
+            int64_t myrow[PPL];
+            int32_t myseg[PPL];
+#pragma unroll
+            for (int p = 0; p < PPL; ++p) {
+                const int32_t q = q0 + p * LANES + li;
+                myseg[p] = c_hi;
+                myrow[p] = 0;
+                if (q < total) {
+                    int lo = 0, hi = c_hi - c_lo;  // last c with cum[c] <= q
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (cum[mid] <= q) lo = mid; else hi = mid;
+                    }
+                    const int c = c_lo + lo;
+                    const int32_t j = st.o0[w][c] + (q - cum[lo]);
+                    FieldInfo fi;
+                    fi.base = st.base[w][c];
+                    fi.rows = st.rows[w][c];
+                    fi.salt = st.salt[w][c];
+                    myrow[p] = fi.base + row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
+                    myseg[p] = c;
+                    a.seg_of[j + st.gb[w][c]] = st.sg[w][c];
+                }
+            }
+            // ---- U rows at a time: broadcast addresses, load, add in ascending order
+            const int32_t nround = min(RND, total - q0);
+#pragma unroll
+            for (int k0 = 0; k0 < RND; k0 += U) {
+                if (k0 >= nround) break;
+                float4 v[U][VPL];
+                int sk[U];
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
-                    while (j2 >= e2 && c2 < c_hi) {
-                        ++c2;
-                        if (c2 < c_hi) {
-                            j2 = s_o0[wib][c2];
-                            e2 = s_o1[wib][c2];
+                    const int src = (k0 + k) % LANES, slot = (k0 + k) / LANES;
+                    const int64_t r = __shfl_sync(gmask, myrow[slot], src, LANES);
+                    sk[k] = __shfl_sync(gmask, myseg[slot], src, LANES);
+                    if (k0 + k < nround) {
+#pragma unroll
+                        for (int qq = 0; qq < VPL; ++qq) v[k][qq] = ldg_f4(wb + r * D + qq * LANES * 4);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    if (k0 + k < nround) {
+                        while (cur < sk[k]) {
+                            flush_seg<D>(a, acc, st.out[w][cur], cum[cur - c_lo + 1] - cum[cur - c_lo], li);
+                            ++cur;
                         }
-                    }
-                    bseg[k] = c2;
-                    bj[k] = j2;
-                    if (c2 < c_hi) {
-                        ++n;
-                        ++j2;
+#pragma unroll
+                        for (int qq = 0; qq < VPL; ++qq) acc[qq] = add4(acc[qq], v[k][qq]);
                     }
                 }
             }
-            // ---- issue the row loads (keys recomputed from the raw IDs)
-            float4 v[U][VPL];
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                if (k < n) {
-                    const FieldInfo fi = a.finfo[s_f[wib][bseg[k]]];
-                    const int64_t r = fi.base + row_of(a.id_mode, __ldg(a.ids + bj[k]), fi, a.err);
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) v[k][q] = ldg_f4(wb + r * D + q * LANES * 4);
-                    if (li == 0) a.seg_of[bj[k] + s_gb[wib][bseg[k]]] = s_sg[wib][bseg[k]];
-                }
-            }
-            // ---- accumulate in ascending j; flush finished (and empty) segments
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                if (k < n) {
-                    while (cur < bseg[k]) {
-                        const int32_t len = s_o1[wib][cur] - s_o0[wib][cur];
-                        float *o = a.out + s_out[wib][cur] + li * 4;
-#pragma unroll
-                        for (int q = 0; q < VPL; ++q) {
-                            if (a.pool_mean && len > 0) acc[q] = div4(acc[q], (float)len);
-                            stcs_f4(o + q * LANES * 4, acc[q]);
-                            acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-                        ++cur;
-                    }
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) acc[q] = add4(acc[q], v[k][q]);
-                }
-            }
-            if (n < U) {  // stream exhausted: flush the rest
-                while (cur < c_hi) {
-                    const int32_t len = s_o1[wib][cur] - s_o0[wib][cur];
-                    float *o = a.out + s_out[wib][cur] + li * 4;
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) {
-                        if (a.pool_mean && len > 0) acc[q] = div4(acc[q], (float)len);
-                        stcs_f4(o + q * LANES * 4, acc[q]);
-                        acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                    ++cur;
-                }
-            } else {
-                cur = bseg[U - 1];
-                j = bj[U - 1] + 1;
-                e = s_o1[wib][cur];
-            }
+        }
+        while (cur < c_hi) {  // the last segment and trailing empty ones
+            flush_seg<D>(a, acc, st.out[w][cur], cum[cur - c_lo + 1] - cum[cur - c_lo], li);
+            ++cur;
         }
         __syncwarp();
     }

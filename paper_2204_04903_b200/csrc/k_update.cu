@@ -13,11 +13,13 @@
 // path and the oracle agree even when G nearly cancels.
 //
 //   k_csr_bounds     : row boundaries in the uid-sorted occurrence list (ustart)
-//   k_segsum_update  : a warp owns 32 consecutive unique rows, split into LANES-wide row
-//                      groups; each group walks the flattened occurrence stream of its rows
-//                      with U dY-row loads in flight, prefetches the weight/state row of the
-//                      row it is summing, and updates it when the row's occurrences end.
-//                      Rows with > kLongRow occurrences are deferred to the chunked path.
+//   k_segsum_update  : a warp owns the rows that start in its tile of kPosTile occurrence
+//                      positions (balanced under Zipf skew); rows go 32 at a time to LANES-wide
+//                      row groups; each group's occurrences form one flattened stream whose
+//                      dY addresses are resolved one per lane and broadcast, U dY rows in
+//                      flight; the weight/state row being summed is prefetched and updated
+//                      when its occurrences end.  Rows with > kLongRow occurrences are
+//                      deferred to the chunked path.
 //   k_long_plan      : chunk counts (kChunk occurrences per chunk) of the deferred rows + scan
 //   k_long_partial   : one row group per chunk -> fp64 partial sums (all chunks in parallel:
 //                      a Zipf head with 1e5 occurrences is spread over the whole GPU)
@@ -143,103 +145,148 @@ __device__ __forceinline__ void update_row(const UpdateArgs &a, int64_t row, int
 }
 
 // ------------------------------------------------------------------------------------------
+constexpr int kPosTile = 512;  // occurrence positions per warp tile (load balance under Zipf skew)
+
+template <int D>
+__device__ __forceinline__ void finish_row(const UpdateArgs &a, int64_t row, int li, RowRegs<Geo<D>::VPL> &rr,
+                                           dbl4 *g) {
+    if (row >= 0) update_row<D>(a, row, li, rr, g);
+#pragma unroll
+    for (int q = 0; q < Geo<D>::VPL; ++q) g[q] = zero4d();
+}
+
+// first row that starts at or after position p (p in [P0, P1); rows partition the positions)
+__device__ __forceinline__ int32_t row_at_or_after(const int32_t *su, int32_t p, int32_t P0) {
+    const int32_t u = __ldg(su + p);
+    return (p == P0 || __ldg(su + p - 1) != u) ? u : u + 1;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
     using Gm = Geo<D>;
     constexpr int LANES = Gm::LANES, VPL = Gm::VPL, SPG = Gm::SPG, U = Gm::U;
-    __shared__ int32_t s_i0[8][32], s_i1[8][32];
+    constexpr int PPL = U > LANES ? U / LANES : 1, RND = LANES * PPL;
+    __shared__ int32_t s_i0[8][32], s_cum[8][64];
     __shared__ int64_t s_row[8][32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int li = lane % LANES, grp = lane / LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
     const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
-    const int64_t nU = (int64_t)u1 - u0;
+    if (u1 <= u0) return;
+    const int32_t P0 = __ldg(a.ustart + u0), P1 = __ldg(a.ustart + u1);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * 32; t0 < nU; t0 += nwarps * 32) {
-        {
-            const int64_t u = u0 + t0 + lane;
-            int32_t i0 = 0, i1 = 0;
-            int64_t row = -1;
-            if (u < u1) {
-                i0 = __ldg(a.ustart + u);
-                i1 = __ldg(a.ustart + u + 1);
-                if (i1 - i0 > kLongRow) {  // Zipf head: chunked path
-                    a.long_list[atomicAdd(a.long_cnt, 1)] = (int32_t)u;
-                    i1 = i0;
-                } else {
-                    row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
-                }
-            }
-            s_i0[wib][lane] = i0;
-            s_i1[wib][lane] = i1;
-            s_row[wib][lane] = row;
-        }
-        __syncwarp();
-        const int nrow = (int)((nU - t0) < 32 ? (nU - t0) : 32);
-        const int c_lo = grp * SPG, c_hi = min(nrow, c_lo + SPG);
-        int cur = c_lo;
-        int32_t i = cur < c_hi ? s_i0[wib][cur] : 0, e = cur < c_hi ? s_i1[wib][cur] : 0;
-        dbl4 g[VPL];
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-        RowRegs<VPL> rr;
-        if (cur < c_hi && s_row[wib][cur] >= 0) load_row<D>(a, s_row[wib][cur], li, rr);
-        while (cur < c_hi) {
-            int bcur[U];
-            int32_t bpos[U];
-            int n = 0;
+    // a warp owns the rows that START inside its tile of kPosTile occurrence positions; rows
+    // have <= kLongRow occurrences here, so every warp sums about the same number of dY rows
+    for (int64_t pa = P0 + ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * kPosTile; pa < P1;
+         pa += nwarps * kPosTile) {
+        const int64_t pb = pa + kPosTile < P1 ? pa + kPosTile : P1;
+        const int32_t ua = row_at_or_after(a.sorted_u, (int32_t)pa, P0);
+        const int32_t ub = pb == P1 ? u1 : row_at_or_after(a.sorted_u, (int32_t)pb, P0);
+        for (int32_t t0 = ua; t0 < ub; t0 += 32) {
+            // ---- 32 rows: ranges (long rows -> empty, deferred), group-local length prefix
             {
-                int c2 = cur;
-                int32_t i2 = i, e2 = e;
+                const int32_t u = t0 + lane;
+                int32_t i0 = 0, n = 0;
+                int64_t row = -1;
+                if (u < ub) {
+                    i0 = __ldg(a.ustart + u);
+                    n = __ldg(a.ustart + u + 1) - i0;
+                    if (n > kLongRow) {  // Zipf head: chunked path
+                        a.long_list[atomicAdd(a.long_cnt, 1)] = u;
+                        n = 0;
+                    } else {
+                        row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
+                    }
+                }
+                s_i0[w][lane] = i0;
+                s_row[w][lane] = row;
+                int32_t x = n;
 #pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    while (i2 >= e2 && c2 < c_hi) {
-                        ++c2;
-                        if (c2 < c_hi) {
-                            i2 = s_i0[wib][c2];
-                            e2 = s_i1[wib][c2];
+                for (int o = 1; o < SPG; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(0xffffffffu, x, o, SPG);
+                    if ((lane % SPG) >= o) x += y;
+                }
+                s_cum[w][lane + lane / SPG + 1] = x;
+                if (lane % SPG == 0) s_cum[w][lane + lane / SPG] = 0;
+            }
+            __syncwarp();
+            const int nrow = (ub - t0) < 32 ? (ub - t0) : 32;
+            const int c_lo = grp * SPG, c_hi = min(nrow, c_lo + SPG);
+            const int32_t *cum = &s_cum[w][grp * (SPG + 1)];
+            const int32_t total = c_hi > c_lo ? cum[c_hi - c_lo] : 0;
+            dbl4 g[VPL];
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) g[q] = zero4d();
+            RowRegs<VPL> rr;
+            int cur = c_lo;
+            if (cur < c_hi && s_row[w][cur] >= 0) load_row<D>(a, s_row[w][cur], li, rr);
+            for (int32_t q0 = 0; q0 < total; q0 += RND) {
+                // ---- each lane resolves PPL occurrences: dY row address (+ mean length)
+                int64_t myoff[PPL];
+                int32_t myc[PPL], mylen[PPL];
+#pragma unroll
+                for (int p = 0; p < PPL; ++p) {
+                    const int32_t q = q0 + p * LANES + li;
+                    myc[p] = c_hi;
+                    myoff[p] = 0;
+                    mylen[p] = 0;
+                    if (q < total) {
+                        int lo = 0, hi = c_hi - c_lo;
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (cum[mid] <= q) lo = mid; else hi = mid;
+                        }
+                        const int c = c_lo + lo;
+                        const int32_t seg = __ldg(a.sorted_seg + s_i0[w][c] + (q - cum[lo]));
+                        const int32_t f = seg / a.B;
+                        myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
+                        if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
+                        myc[p] = c;
+                    }
+                }
+                const int32_t nround = min(RND, total - q0);
+#pragma unroll
+                for (int k0 = 0; k0 < RND; k0 += U) {
+                    if (k0 >= nround) break;
+                    float4 c4[U][VPL];
+                    int ck[U];
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        const int src = (k0 + k) % LANES, slot = (k0 + k) / LANES;
+                        const int64_t off = __shfl_sync(gmask, myoff[slot], src, LANES);
+                        const int32_t len = __shfl_sync(gmask, mylen[slot], src, LANES);
+                        ck[k] = __shfl_sync(gmask, myc[slot], src, LANES);
+                        if (k0 + k < nround) {
+                            const float *p = a.dy + off + li * 4;
+#pragma unroll
+                            for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = ldg_f4(p + qq * LANES * 4);
+                            if (a.pool_mean) {
+#pragma unroll
+                                for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = div4(c4[k][qq], (float)len);
+                            }
                         }
                     }
-                    bcur[k] = c2;
-                    bpos[k] = i2;
-                    if (c2 < c_hi) {
-                        ++n;
-                        ++i2;
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        if (k0 + k < nround) {
+                            while (cur < ck[k]) {  // row `cur` complete: update, prefetch the next
+                                finish_row<D>(a, s_row[w][cur], li, rr, g);
+                                ++cur;
+                                if (s_row[w][cur] >= 0) load_row<D>(a, s_row[w][cur], li, rr);
+                            }
+#pragma unroll
+                            for (int qq = 0; qq < VPL; ++qq) g[qq] = add4d(g[qq], c4[k][qq]);
+                        }
                     }
                 }
             }
-            float4 c[U][VPL];
-#pragma unroll
-            for (int k = 0; k < U; ++k)
-                if (k < n) load_contrib<D>(a, __ldg(a.sorted_seg + bpos[k]), li, c[k]);
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                if (k < n) {
-                    while (cur < bcur[k]) {  // row `cur` complete: update, prefetch the next
-                        if (s_row[wib][cur] >= 0) update_row<D>(a, s_row[wib][cur], li, rr, g);
-#pragma unroll
-                        for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-                        ++cur;
-                        if (s_row[wib][cur] >= 0) load_row<D>(a, s_row[wib][cur], li, rr);
-                    }
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], c[k][q]);
-                }
+            while (cur < c_hi) {
+                finish_row<D>(a, s_row[w][cur], li, rr, g);
+                ++cur;
+                if (cur < c_hi && s_row[w][cur] >= 0) load_row<D>(a, s_row[w][cur], li, rr);
             }
-            if (n < U) {
-                while (cur < c_hi) {
-                    if (s_row[wib][cur] >= 0) update_row<D>(a, s_row[wib][cur], li, rr, g);
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-                    ++cur;
-                    if (cur < c_hi && s_row[wib][cur] >= 0) load_row<D>(a, s_row[wib][cur], li, rr);
-                }
-            } else {
-                cur = bcur[U - 1];
-                i = bpos[U - 1] + 1;
-                e = s_i1[wib][cur];
-            }
+            __syncwarp();
         }
-        __syncwarp();
     }
 }
 
