@@ -13,13 +13,13 @@
 // path and the oracle agree even when G nearly cancels.
 //
 //   k_csr_bounds     : row boundaries in the uid-sorted occurrence list (ustart)
-//   k_segsum_update  : a warp owns the rows that start in its tile of kPosTile occurrence
-//                      positions (balanced under Zipf skew); rows go 32 at a time to LANES-wide
-//                      row groups; each group's occurrences form one flattened stream whose
-//                      dY addresses are resolved one per lane and broadcast, U dY rows in
-//                      flight; the weight/state row being summed is prefetched and updated
-//                      when its occurrences end.  Rows with > kLongRow occurrences are
-//                      deferred to the chunked path.
+//   k_segsum_update  : a warp owns the rows that start in its tile of occurrence positions
+//                      (one tile per warp: balanced under Zipf skew); each LANES-wide row group
+//                      takes RT rows at a time: phase 1 walks their occurrences as one
+//                      flattened stream (dY addresses resolved one per lane and broadcast, U dY
+//                      rows in flight) and stages the rounded G in shared memory; phase 2 loads
+//                      UB rows' weight/state at once and applies the optimizer.  Rows with
+//                      > kLongRow occurrences are deferred to the chunked path.
 //   k_long_plan      : chunk counts (kChunk occurrences per chunk) of the deferred rows + scan
 //   k_long_partial   : one row group per chunk -> fp64 partial sums (all chunks in parallel:
 //                      a Zipf head with 1e5 occurrences is spread over the whole GPU)
@@ -105,13 +105,13 @@ __device__ __forceinline__ void load_row(const UpdateArgs &a, int64_t row, int l
 }
 
 template <int D>
-__device__ __forceinline__ void update_row(const UpdateArgs &a, int64_t row, int li, RowRegs<Geo<D>::VPL> &r,
-                                           const dbl4 *g64) {
+__device__ __forceinline__ void update_row32(const UpdateArgs &a, int64_t row, int li, RowRegs<Geo<D>::VPL> &r,
+                                             const float4 *g32) {
     constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
     const int64_t o = row * D + li * 4;
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
-        const float4 g4 = round4(g64[q]);
+        const float4 g4 = g32[q];
         const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
         float ww[4] = {r.w[q].x, r.w[q].y, r.w[q].z, r.w[q].w};
         float ss[4] = {r.s1[q].x, r.s1[q].y, r.s1[q].z, r.s1[q].w};
@@ -144,17 +144,16 @@ __device__ __forceinline__ void update_row(const UpdateArgs &a, int64_t row, int
     }
 }
 
-// ------------------------------------------------------------------------------------------
-constexpr int kPosTile = 512;  // occurrence positions per warp tile (load balance under Zipf skew)
-
 template <int D>
-__device__ __forceinline__ void finish_row(const UpdateArgs &a, int64_t row, int li, RowRegs<Geo<D>::VPL> &rr,
-                                           dbl4 *g) {
-    if (row >= 0) update_row<D>(a, row, li, rr, g);
+__device__ __forceinline__ void update_row(const UpdateArgs &a, int64_t row, int li, RowRegs<Geo<D>::VPL> &r,
+                                           const dbl4 *g64) {
+    float4 g32[Geo<D>::VPL];
 #pragma unroll
-    for (int q = 0; q < Geo<D>::VPL; ++q) g[q] = zero4d();
+    for (int q = 0; q < Geo<D>::VPL; ++q) g32[q] = round4(g64[q]);
+    update_row32<D>(a, row, li, r, g32);
 }
 
+// ------------------------------------------------------------------------------------------
 // first row that starts at or after position p (p in [P0, P1); rows partition the positions)
 __device__ __forceinline__ int32_t row_at_or_after(const int32_t *su, int32_t p, int32_t P0) {
     const int32_t u = __ldg(su + p);
@@ -162,12 +161,21 @@ __device__ __forceinline__ int32_t row_at_or_after(const int32_t *su, int32_t p,
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
+struct SegGeo {
+    static constexpr int RT = D <= 32 ? 4 : (D <= 128 ? 8 : 2);  // rows per group per sub-tile
+    static constexpr int ROWS = Geo<D>::R * RT;                  // rows per warp sub-tile
+    static constexpr int UB = D <= 32 ? 2 : (D <= 128 ? 4 : 1);  // rows per update batch
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
     using Gm = Geo<D>;
-    constexpr int LANES = Gm::LANES, VPL = Gm::VPL, SPG = Gm::SPG, U = Gm::U;
+    constexpr int LANES = Gm::LANES, VPL = Gm::VPL, R = Gm::R, U = Gm::U;
+    constexpr int RT = SegGeo<D>::RT, ROWS = SegGeo<D>::ROWS, UB = SegGeo<D>::UB;
     constexpr int PPL = U > LANES ? U / LANES : 1, RND = LANES * PPL;
-    __shared__ int32_t s_i0[8][32], s_cum[8][64];
-    __shared__ int64_t s_row[8][32];
+    __shared__ int32_t s_i0[8][ROWS], s_n[8][ROWS], s_cum[8][R][RT + 1];
+    __shared__ int64_t s_row[8][ROWS];
+    __shared__ float4 s_g[8][R][RT][D / 4];  // rounded G of the sub-tile's rows
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int li = lane % LANES, grp = lane / LANES;
     const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
@@ -175,17 +183,18 @@ __global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
     if (u1 <= u0) return;
     const int32_t P0 = __ldg(a.ustart + u0), P1 = __ldg(a.ustart + u1);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    // a warp owns the rows that START inside its tile of kPosTile occurrence positions; rows
-    // have <= kLongRow occurrences here, so every warp sums about the same number of dY rows
-    for (int64_t pa = P0 + ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * kPosTile; pa < P1;
-         pa += nwarps * kPosTile) {
-        const int64_t pb = pa + kPosTile < P1 ? pa + kPosTile : P1;
+    // a warp owns the rows that START inside its tile of occurrence positions (tiles sized so
+    // every warp gets one); rows have <= kLongRow occurrences here, so the work is balanced
+    int64_t tile = ((int64_t)(P1 - P0) + nwarps - 1) / nwarps;
+    tile = tile < 128 ? 128 : tile;
+    for (int64_t pa = P0 + ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * tile; pa < P1; pa += nwarps * tile) {
+        const int64_t pb = pa + tile < P1 ? pa + tile : P1;
         const int32_t ua = row_at_or_after(a.sorted_u, (int32_t)pa, P0);
         const int32_t ub = pb == P1 ? u1 : row_at_or_after(a.sorted_u, (int32_t)pb, P0);
-        for (int32_t t0 = ua; t0 < ub; t0 += 32) {
-            // ---- 32 rows: ranges (long rows -> empty, deferred), group-local length prefix
-            {
-                const int32_t u = t0 + lane;
+        for (int32_t t0 = ua; t0 < ub; t0 += ROWS) {
+            // ---- sub-tile rows: ranges (long rows -> empty, deferred), group-local prefix
+            for (int x = lane; x < ROWS; x += 32) {
+                const int32_t u = t0 + x;
                 int32_t i0 = 0, n = 0;
                 int64_t row = -1;
                 if (u < ub) {
@@ -198,50 +207,47 @@ __global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
                         row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
                     }
                 }
-                s_i0[w][lane] = i0;
-                s_row[w][lane] = row;
-                int32_t x = n;
-#pragma unroll
-                for (int o = 1; o < SPG; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(0xffffffffu, x, o, SPG);
-                    if ((lane % SPG) >= o) x += y;
-                }
-                s_cum[w][lane + lane / SPG + 1] = x;
-                if (lane % SPG == 0) s_cum[w][lane + lane / SPG] = 0;
+                s_i0[w][x] = i0;
+                s_n[w][x] = n;
+                s_row[w][x] = row;
             }
             __syncwarp();
-            const int nrow = (ub - t0) < 32 ? (ub - t0) : 32;
-            const int c_lo = grp * SPG, c_hi = min(nrow, c_lo + SPG);
-            const int32_t *cum = &s_cum[w][grp * (SPG + 1)];
-            const int32_t total = c_hi > c_lo ? cum[c_hi - c_lo] : 0;
+            if (li == 0) {
+                int32_t c = 0;
+                s_cum[w][grp][0] = 0;
+#pragma unroll
+                for (int r = 0; r < RT; ++r) {
+                    c += s_n[w][grp * RT + r];
+                    s_cum[w][grp][r + 1] = c;
+                }
+            }
+            __syncwarp();
+            const int32_t *cum = s_cum[w][grp];
+            const int rbase = grp * RT;
+            const int32_t total = cum[RT];
+            // ---- phase 1: G of the group's RT rows (fp64 accumulation, U dY rows in flight)
             dbl4 g[VPL];
 #pragma unroll
             for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-            RowRegs<VPL> rr;
-            int cur = c_lo;
-            if (cur < c_hi && s_row[w][cur] >= 0) load_row<D>(a, s_row[w][cur], li, rr);
+            int cur = 0;
             for (int32_t q0 = 0; q0 < total; q0 += RND) {
-                // ---- each lane resolves PPL occurrences: dY row address (+ mean length)
                 int64_t myoff[PPL];
                 int32_t myc[PPL], mylen[PPL];
 #pragma unroll
                 for (int p = 0; p < PPL; ++p) {
                     const int32_t q = q0 + p * LANES + li;
-                    myc[p] = c_hi;
+                    myc[p] = RT;
                     myoff[p] = 0;
                     mylen[p] = 0;
                     if (q < total) {
-                        int lo = 0, hi = c_hi - c_lo;
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (cum[mid] <= q) lo = mid; else hi = mid;
-                        }
-                        const int c = c_lo + lo;
-                        const int32_t seg = __ldg(a.sorted_seg + s_i0[w][c] + (q - cum[lo]));
+                        int lo = 0;
+#pragma unroll
+                        for (int r = 1; r < RT; ++r) lo += (cum[r] <= q);
+                        const int32_t seg = __ldg(a.sorted_seg + s_i0[w][rbase + lo] + (q - cum[lo]));
                         const int32_t f = seg / a.B;
                         myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
                         if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
-                        myc[p] = c;
+                        myc[p] = lo;
                     }
                 }
                 const int32_t nround = min(RND, total - q0);
@@ -269,10 +275,13 @@ __global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
 #pragma unroll
                     for (int k = 0; k < U; ++k) {
                         if (k0 + k < nround) {
-                            while (cur < ck[k]) {  // row `cur` complete: update, prefetch the next
-                                finish_row<D>(a, s_row[w][cur], li, rr, g);
+                            while (cur < ck[k]) {  // row `cur` complete
+#pragma unroll
+                                for (int qq = 0; qq < VPL; ++qq) {
+                                    s_g[w][grp][cur][qq * LANES + li] = round4(g[qq]);
+                                    g[qq] = zero4d();
+                                }
                                 ++cur;
-                                if (s_row[w][cur] >= 0) load_row<D>(a, s_row[w][cur], li, rr);
                             }
 #pragma unroll
                             for (int qq = 0; qq < VPL; ++qq) g[qq] = add4d(g[qq], c4[k][qq]);
@@ -280,10 +289,33 @@ __global__ void __launch_bounds__(256) k_segsum_update(UpdateArgs a) {
                     }
                 }
             }
-            while (cur < c_hi) {
-                finish_row<D>(a, s_row[w][cur], li, rr, g);
-                ++cur;
-                if (cur < c_hi && s_row[w][cur] >= 0) load_row<D>(a, s_row[w][cur], li, rr);
+            for (; cur < RT; ++cur) {
+#pragma unroll
+                for (int qq = 0; qq < VPL; ++qq) {
+                    s_g[w][grp][cur][qq * LANES + li] = round4(g[qq]);
+                    g[qq] = zero4d();
+                }
+            }
+            // ---- phase 2: optimizer on the RT rows, UB rows' weight/state loads in flight.
+            // (each lane reads back only the columns it wrote: no synchronisation needed)
+#pragma unroll
+            for (int r0 = 0; r0 < RT; r0 += UB) {
+                RowRegs<VPL> rr[UB];
+#pragma unroll
+                for (int r = 0; r < UB; ++r) {
+                    const int64_t row = s_row[w][rbase + r0 + r];
+                    if (row >= 0) load_row<D>(a, row, li, rr[r]);
+                }
+#pragma unroll
+                for (int r = 0; r < UB; ++r) {
+                    const int64_t row = s_row[w][rbase + r0 + r];
+                    if (row >= 0) {
+                        float4 g32[VPL];
+#pragma unroll
+                        for (int qq = 0; qq < VPL; ++qq) g32[qq] = s_g[w][grp][r0 + r][qq * LANES + li];
+                        update_row32<D>(a, row, li, rr[r], g32);
+                    }
+                }
             }
             __syncwarp();
         }
