@@ -15,11 +15,12 @@
 //   k_csr_bounds     : row boundaries in the uid-sorted occurrence list (ustart)
 //   k_segsum_update  : a warp owns the rows that start in its tile of occurrence positions
 //                      (one tile per warp: balanced under Zipf skew); each LANES-wide row group
-//                      takes RT rows at a time: phase 1 walks their occurrences as one
+//                      takes RT rows at a time: their weight/state rows are staged in shared
+//                      memory with cp.async while the group walks their occurrences as one
 //                      flattened stream (dY addresses resolved one per lane and broadcast, U dY
-//                      rows in flight) and stages the rounded G in shared memory; phase 2 loads
-//                      UB rows' weight/state at once and applies the optimizer.  Rows with
-//                      > kLongRow occurrences are deferred to the chunked path.
+//                      rows in flight); a row's optimizer step runs from shared memory the
+//                      moment its occurrences end.  Rows with > kLongRow occurrences are
+//                      deferred to the chunked path.
 //   k_long_plan      : chunk counts (kChunk occurrences per chunk) of the deferred rows + scan
 //   k_long_partial   : one row group per chunk -> fp64 partial sums (all chunks in parallel:
 //                      a Zipf head with 1e5 occurrences is spread over the whole GPU)
@@ -164,25 +165,36 @@ template <int D>
 struct SegGeo {
     static constexpr int RT = D <= 32 ? 4 : (D <= 128 ? 8 : 2);  // rows per group per sub-tile
     static constexpr int ROWS = Geo<D>::R * RT;                  // rows per warp sub-tile
-    static constexpr int UB = D <= 32 ? 2 : (D <= 128 ? 4 : 1);  // rows per update batch
+    static constexpr int NST = 3;                                // staged arrays: w, s1, s2
+    // shared bytes per warp: descriptors + staged weight/state rows of one sub-tile
+    static constexpr int STAGE_F4 = ROWS * NST * (D / 4);
 };
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <int D>
 __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
     using Gm = Geo<D>;
     constexpr int LANES = Gm::LANES, VPL = Gm::VPL, R = Gm::R, U = Gm::U;
-    constexpr int RT = SegGeo<D>::RT, ROWS = SegGeo<D>::ROWS, UB = SegGeo<D>::UB;
+    constexpr int RT = SegGeo<D>::RT, ROWS = SegGeo<D>::ROWS, V4 = D / 4;
     constexpr int PPL = U > LANES ? U / LANES : 1, RND = LANES * PPL;
     __shared__ int32_t s_i0[8][ROWS], s_n[8][ROWS], s_cum[8][R][RT + 1];
     __shared__ int64_t s_row[8][ROWS];
-    __shared__ float4 s_g[8][R][RT][D / 4];  // rounded G of the sub-tile's rows
+    extern __shared__ float4 s_stage[];  // [8 warps][ROWS][3][V4]: staged w, s1, s2 rows
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int li = lane % LANES, grp = lane / LANES;
     const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
+    float4 *stage = s_stage + (size_t)w * SegGeo<D>::STAGE_F4;
     const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
     if (u1 <= u0) return;
     const int32_t P0 = __ldg(a.ustart + u0), P1 = __ldg(a.ustart + u1);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int nst = a.opt == 1 ? 3 : 2;
     // a warp owns the rows that START inside its tile of occurrence positions (tiles sized so
     // every warp gets one); rows have <= kLongRow occurrences here, so the work is balanced
     int64_t tile = ((int64_t)(P1 - P0) + nwarps - 1) / nwarps;
@@ -212,24 +224,63 @@ __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
                 s_row[w][x] = row;
             }
             __syncwarp();
+            const int rbase = grp * RT;
+            // ---- stage the group's RT weight/state rows in shared memory (cp.async, 16 B per
+            // lane per row per array; each lane copies exactly the columns it will update, so it
+            // only waits for its own copies) — overlaps with the dY walk below
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                const int64_t row = s_row[w][rbase + r];
+                if (row >= 0) {
+                    const int64_t o = row * D + li * 4;
+                    float4 *st = stage + (size_t)(rbase + r) * 3 * V4 + li;
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) {
+                        cp_async16(st + q * LANES, a.weight + o + q * LANES * 4);
+                        cp_async16(st + V4 + q * LANES, a.state1 + o + q * LANES * 4);
+                        if (nst == 3) cp_async16(st + 2 * V4 + q * LANES, a.state2 + o + q * LANES * 4);
+                    }
+                }
+            }
+            cp_async_commit();
             if (li == 0) {
                 int32_t c = 0;
                 s_cum[w][grp][0] = 0;
 #pragma unroll
                 for (int r = 0; r < RT; ++r) {
-                    c += s_n[w][grp * RT + r];
+                    c += s_n[w][rbase + r];
                     s_cum[w][grp][r + 1] = c;
                 }
             }
             __syncwarp();
             const int32_t *cum = s_cum[w][grp];
-            const int rbase = grp * RT;
             const int32_t total = cum[RT];
-            // ---- phase 1: G of the group's RT rows (fp64 accumulation, U dY rows in flight)
+            bool staged = false;
             dbl4 g[VPL];
 #pragma unroll
             for (int q = 0; q < VPL; ++q) g[q] = zero4d();
             int cur = 0;
+            // row `cur` complete: optimizer on the staged row, results straight to global
+            auto finish = [&](int r) {
+                const int64_t row = s_row[w][rbase + r];
+                if (row >= 0) {
+                    if (!staged) {
+                        cp_async_wait_all();
+                        staged = true;
+                    }
+                    const float4 *st = stage + (size_t)(rbase + r) * 3 * V4 + li;
+                    RowRegs<VPL> rr;
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) {
+                        rr.w[q] = st[q * LANES];
+                        rr.s1[q] = st[V4 + q * LANES];
+                        if (nst == 3) rr.s2[q] = st[2 * V4 + q * LANES];
+                    }
+                    update_row<D>(a, row, li, rr, g);
+                }
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) g[q] = zero4d();
+            };
             for (int32_t q0 = 0; q0 < total; q0 += RND) {
                 int64_t myoff[PPL];
                 int32_t myc[PPL], mylen[PPL];
@@ -275,50 +326,26 @@ __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
 #pragma unroll
                     for (int k = 0; k < U; ++k) {
                         if (k0 + k < nround) {
-                            while (cur < ck[k]) {  // row `cur` complete
-#pragma unroll
-                                for (int qq = 0; qq < VPL; ++qq) {
-                                    s_g[w][grp][cur][qq * LANES + li] = round4(g[qq]);
-                                    g[qq] = zero4d();
-                                }
-                                ++cur;
-                            }
+                            while (cur < ck[k]) finish(cur++);
 #pragma unroll
                             for (int qq = 0; qq < VPL; ++qq) g[qq] = add4d(g[qq], c4[k][qq]);
                         }
                     }
                 }
             }
-            for (; cur < RT; ++cur) {
-#pragma unroll
-                for (int qq = 0; qq < VPL; ++qq) {
-                    s_g[w][grp][cur][qq * LANES + li] = round4(g[qq]);
-                    g[qq] = zero4d();
-                }
-            }
-            // ---- phase 2: optimizer on the RT rows, UB rows' weight/state loads in flight.
-            // (each lane reads back only the columns it wrote: no synchronisation needed)
-#pragma unroll
-            for (int r0 = 0; r0 < RT; r0 += UB) {
-                RowRegs<VPL> rr[UB];
-#pragma unroll
-                for (int r = 0; r < UB; ++r) {
-                    const int64_t row = s_row[w][rbase + r0 + r];
-                    if (row >= 0) load_row<D>(a, row, li, rr[r]);
-                }
-#pragma unroll
-                for (int r = 0; r < UB; ++r) {
-                    const int64_t row = s_row[w][rbase + r0 + r];
-                    if (row >= 0) {
-                        float4 g32[VPL];
-#pragma unroll
-                        for (int qq = 0; qq < VPL; ++qq) g32[qq] = s_g[w][grp][r0 + r][qq * LANES + li];
-                        update_row32<D>(a, row, li, rr[r], g32);
-                    }
-                }
-            }
+            while (cur < RT) finish(cur++);
+            cp_async_wait_all();  // no copy may still target the stage when it is reused
             __syncwarp();
         }
+    }
+}
+
+size_t segsum_smem_bytes(int D) {
+    switch (D) {
+#define SB(DD) case DD: return (size_t)8 * SegGeo<DD>::STAGE_F4 * sizeof(float4);
+        SB(4) SB(8) SB(16) SB(32) SB(64) SB(128) SB(256) SB(384) SB(512)
+#undef SB
+        default: return 0;
     }
 }
 
@@ -421,8 +448,17 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
     }
 
 void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
-    const unsigned blocks = (unsigned)num_sms * 8;
-#define CALL(DD) k_segsum_update<DD><<<blocks, 256, 0, s>>>(a)
+    const unsigned blocks = (unsigned)num_sms * 2;  // one resident wave (2 blocks / SM)
+    const size_t smem = segsum_smem_bytes(D);
+#define CALL(DD)                                                                                        \
+    {                                                                                                   \
+        static bool attr = false;                                                                       \
+        if (!attr) {                                                                                    \
+            cudaFuncSetAttribute(k_segsum_update<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            attr = true;                                                                                \
+        }                                                                                               \
+        k_segsum_update<DD><<<blocks, 256, smem, s>>>(a);                                               \
+    }
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
 }
