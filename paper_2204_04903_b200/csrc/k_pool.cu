@@ -136,14 +136,14 @@ __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
             }
             // ---- U rows at a time: broadcast addresses, load, add in ascending order
             const int32_t nround = min(RND, total - q0);
-#pragma unroll
-            for (int k0 = 0; k0 < RND; k0 += U) {
-                if (k0 >= nround) break;
+#pragma unroll 1
+            for (int k0 = 0; k0 < nround; k0 += U) {
                 float4 v[U][VPL];
                 int sk[U];
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
-                    const int src = (k0 + k) % LANES, slot = (k0 + k) / LANES;
+                    // PPL > 1 only when RND == U (k0 == 0): the slot index stays static
+                    const int src = (k0 + k) % LANES, slot = PPL > 1 ? k / LANES : 0;
                     const int64_t r = __shfl_sync(gmask, myrow[slot], src, LANES);
                     sk[k] = __shfl_sync(gmask, myseg[slot], src, LANES);
                     if (k0 + k < nround) {

@@ -163,9 +163,9 @@ __device__ __forceinline__ int32_t row_at_or_after(const int32_t *su, int32_t p,
 
 template <int D>
 struct SegGeo {
-    static constexpr int RT = D <= 32 ? 4 : (D <= 128 ? 8 : 2);  // rows per group per sub-tile
+    static constexpr int RT = D <= 128 ? 4 : 2;                  // rows per group per sub-tile
     static constexpr int ROWS = Geo<D>::R * RT;                  // rows per warp sub-tile
-    static constexpr int NST = 3;                                // staged arrays: w, s1, s2
+    static constexpr int NST = 4;                                // staged: w, s1, s2, G
     // shared bytes per warp: descriptors + staged weight/state rows of one sub-tile
     static constexpr int STAGE_F4 = ROWS * NST * (D / 4);
 };
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
                 const int64_t row = s_row[w][rbase + r];
                 if (row >= 0) {
                     const int64_t o = row * D + li * 4;
-                    float4 *st = stage + (size_t)(rbase + r) * 3 * V4 + li;
+                    float4 *st = stage + (size_t)(rbase + r) * SegGeo<D>::NST * V4 + li;
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) {
                         cp_async16(st + q * LANES, a.weight + o + q * LANES * 4);
@@ -255,32 +255,20 @@ __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
             __syncwarp();
             const int32_t *cum = s_cum[w][grp];
             const int32_t total = cum[RT];
-            bool staged = false;
             dbl4 g[VPL];
 #pragma unroll
             for (int q = 0; q < VPL; ++q) g[q] = zero4d();
             int cur = 0;
-            // row `cur` complete: optimizer on the staged row, results straight to global
+            // row `cur` complete: its rounded G goes to the row's 4th staging slot
             auto finish = [&](int r) {
-                const int64_t row = s_row[w][rbase + r];
-                if (row >= 0) {
-                    if (!staged) {
-                        cp_async_wait_all();
-                        staged = true;
-                    }
-                    const float4 *st = stage + (size_t)(rbase + r) * 3 * V4 + li;
-                    RowRegs<VPL> rr;
+                float4 *st = stage + (size_t)(rbase + r) * SegGeo<D>::NST * V4 + 3 * V4 + li;
 #pragma unroll
-                    for (int q = 0; q < VPL; ++q) {
-                        rr.w[q] = st[q * LANES];
-                        rr.s1[q] = st[V4 + q * LANES];
-                        if (nst == 3) rr.s2[q] = st[2 * V4 + q * LANES];
-                    }
-                    update_row<D>(a, row, li, rr, g);
+                for (int q = 0; q < VPL; ++q) {
+                    st[q * LANES] = round4(g[q]);
+                    g[q] = zero4d();
                 }
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) g[q] = zero4d();
             };
+#pragma unroll 1
             for (int32_t q0 = 0; q0 < total; q0 += RND) {
                 int64_t myoff[PPL];
                 int32_t myc[PPL], mylen[PPL];
@@ -302,14 +290,14 @@ __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
                     }
                 }
                 const int32_t nround = min(RND, total - q0);
-#pragma unroll
-                for (int k0 = 0; k0 < RND; k0 += U) {
-                    if (k0 >= nround) break;
+#pragma unroll 1
+                for (int k0 = 0; k0 < nround; k0 += U) {
                     float4 c4[U][VPL];
                     int ck[U];
 #pragma unroll
                     for (int k = 0; k < U; ++k) {
-                        const int src = (k0 + k) % LANES, slot = (k0 + k) / LANES;
+                        // PPL > 1 only when RND == U (k0 == 0): the slot index stays static
+                        const int src = (k0 + k) % LANES, slot = PPL > 1 ? k / LANES : 0;
                         const int64_t off = __shfl_sync(gmask, myoff[slot], src, LANES);
                         const int32_t len = __shfl_sync(gmask, mylen[slot], src, LANES);
                         ck[k] = __shfl_sync(gmask, myc[slot], src, LANES);
@@ -334,7 +322,25 @@ __global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
                 }
             }
             while (cur < RT) finish(cur++);
-            cp_async_wait_all();  // no copy may still target the stage when it is reused
+            // ---- optimizer on the group's RT rows from shared memory, results to global (one
+            // copy of the update code: keeps the kernel inside the instruction cache)
+            cp_async_wait_all();
+#pragma unroll 1
+            for (int r = 0; r < RT; ++r) {
+                const int64_t row = s_row[w][rbase + r];
+                if (row < 0) continue;
+                const float4 *st = stage + (size_t)(rbase + r) * SegGeo<D>::NST * V4 + li;
+                RowRegs<VPL> rr;
+                float4 g32[VPL];
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
+                    rr.w[q] = st[q * LANES];
+                    rr.s1[q] = st[V4 + q * LANES];
+                    if (nst == 3) rr.s2[q] = st[2 * V4 + q * LANES];
+                    g32[q] = st[3 * V4 + q * LANES];
+                }
+                update_row32<D>(a, row, li, rr, g32);
+            }
             __syncwarp();
         }
     }
