@@ -185,6 +185,12 @@ __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
             if (a.pack_gstart[p] == a.pack_gstart[p + 1]) a.pack_ustart[p] = next;
             next = a.pack_ustart[p];
         }
+        int64_t gb = 0;  // G-buffer layout of the split backward
+        for (int p = 0; p < a.P; ++p) {
+            a.pack_gbase[p] = gb;
+            gb += (int64_t)(a.pack_ustart[p + 1] - a.pack_ustart[p]) * a.pack_dim[p];
+        }
+        a.pack_gbase[a.P] = gb;
     }
 }
 

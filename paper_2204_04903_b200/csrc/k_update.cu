@@ -356,6 +356,166 @@ size_t segsum_smem_bytes(int D) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Split backward (PICASSO_BWD=split, the default): k_segsum writes the rounded G of every
+// unique row of the pack into a G buffer (rows in uid order: coalesced), k_update_rows then
+// applies the optimizer row by row with two rows' weight/state loads in flight per group.
+// Costs one extra G write + read (4·D bytes per unique row each way) but both kernels are
+// short, register-light and run at high occupancy; the fused kernel above is kept as an
+// alternative (PICASSO_BWD=fused).
+template <int D>
+__global__ void __launch_bounds__(256) k_segsum(UpdateArgs a) {
+    using Gm = Geo<D>;
+    constexpr int LANES = Gm::LANES, VPL = Gm::VPL, R = Gm::R, SPG = Gm::SPG, U = Gm::U;
+    constexpr int PPL = U > LANES ? U / LANES : 1, RND = LANES * PPL;
+    __shared__ int32_t s_i0[8][32], s_cum[8][R][SPG + 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int li = lane % LANES, grp = lane / LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
+    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
+    if (u1 <= u0) return;
+    float *gp = a.gbuf + a.pack_gbase[a.pack];
+    const int32_t P0 = __ldg(a.ustart + u0), P1 = __ldg(a.ustart + u1);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t tile = ((int64_t)(P1 - P0) + nwarps - 1) / nwarps;
+    tile = tile < 64 ? 64 : tile;
+    for (int64_t pa = P0 + ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * tile; pa < P1; pa += nwarps * tile) {
+        const int64_t pb = pa + tile < P1 ? pa + tile : P1;
+        const int32_t ua = row_at_or_after(a.sorted_u, (int32_t)pa, P0);
+        const int32_t ub = pb == P1 ? u1 : row_at_or_after(a.sorted_u, (int32_t)pb, P0);
+#pragma unroll 1
+        for (int32_t t0 = ua; t0 < ub; t0 += 32) {
+            {
+                const int32_t u = t0 + lane;
+                int32_t i0 = 0, n = 0;
+                if (u < ub) {
+                    i0 = __ldg(a.ustart + u);
+                    n = __ldg(a.ustart + u + 1) - i0;
+                    if (n > kLongRow) {  // Zipf head: chunked path
+                        a.long_list[atomicAdd(a.long_cnt, 1)] = u;
+                        n = 0;
+                    }
+                }
+                s_i0[w][lane] = i0;
+                int32_t x = n;
+#pragma unroll
+                for (int o = 1; o < SPG; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(0xffffffffu, x, o, SPG);
+                    if ((lane % SPG) >= o) x += y;
+                }
+                s_cum[w][lane / SPG][lane % SPG + 1] = x;
+                if (lane % SPG == 0) s_cum[w][lane / SPG][0] = 0;
+            }
+            __syncwarp();
+            const int nrow = (ub - t0) < 32 ? (ub - t0) : 32;
+            const int c_lo = grp * SPG, c_hi = min(nrow, c_lo + SPG);
+            const int32_t *cum = s_cum[w][grp];
+            const int32_t total = c_hi > c_lo ? cum[c_hi - c_lo] : 0;
+            dbl4 g[VPL];
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) g[q] = zero4d();
+            int cur = c_lo;
+            auto finish = [&](int c) {  // rows deferred to the chunked path write nothing here
+                if (cum[c - c_lo + 1] > cum[c - c_lo]) {
+                    float *o = gp + (int64_t)(t0 + c - u0) * D + li * 4;
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) *reinterpret_cast<float4 *>(o + q * LANES * 4) = round4(g[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) g[q] = zero4d();
+            };
+#pragma unroll 1
+            for (int32_t q0 = 0; q0 < total; q0 += RND) {
+                int64_t myoff[PPL];
+                int32_t myc[PPL], mylen[PPL];
+#pragma unroll
+                for (int p = 0; p < PPL; ++p) {
+                    const int32_t q = q0 + p * LANES + li;
+                    myc[p] = c_hi;
+                    myoff[p] = 0;
+                    mylen[p] = 0;
+                    if (q < total) {
+                        int lo = 0, hi = c_hi - c_lo;
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (cum[mid] <= q) lo = mid; else hi = mid;
+                        }
+                        const int32_t seg = __ldg(a.sorted_seg + s_i0[w][c_lo + lo] + (q - cum[lo]));
+                        const int32_t f = seg / a.B;
+                        myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
+                        if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
+                        myc[p] = c_lo + lo;
+                    }
+                }
+                const int32_t nround = min(RND, total - q0);
+#pragma unroll 1
+                for (int k0 = 0; k0 < nround; k0 += U) {
+                    float4 c4[U][VPL];
+                    int ck[U];
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        const int src = (k0 + k) % LANES, slot = PPL > 1 ? k / LANES : 0;
+                        const int64_t off = __shfl_sync(gmask, myoff[slot], src, LANES);
+                        const int32_t len = __shfl_sync(gmask, mylen[slot], src, LANES);
+                        ck[k] = __shfl_sync(gmask, myc[slot], src, LANES);
+                        if (k0 + k < nround) {
+                            const float *p = a.dy + off + li * 4;
+#pragma unroll
+                            for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = ldg_f4(p + qq * LANES * 4);
+                            if (a.pool_mean) {
+#pragma unroll
+                                for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = div4(c4[k][qq], (float)len);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        if (k0 + k < nround) {
+                            while (cur < ck[k]) finish(cur++);
+#pragma unroll
+                            for (int qq = 0; qq < VPL; ++qq) g[qq] = add4d(g[qq], c4[k][qq]);
+                        }
+                    }
+                }
+            }
+            while (cur < c_hi) finish(cur++);
+            __syncwarp();
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_update_rows(UpdateArgs a) {
+    constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
+    constexpr int RB = 2;  // rows per group iteration (their loads are issued together)
+    const int li = threadIdx.x % LANES;
+    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
+    const float *gp = a.gbuf + a.pack_gbase[a.pack];
+    const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / LANES;
+#pragma unroll 1
+    for (int64_t ub = u0 + grp * RB; ub < u1; ub += ngrp * RB) {
+        RowRegs<VPL> rr[RB];
+        float4 g32[RB][VPL];
+        int64_t row[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            const int64_t u = ub + r;
+            row[r] = -1;
+            if (u < u1) {
+                row[r] = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
+                const float *gr = gp + (u - u0) * D + li * 4;
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) g32[r][q] = ldg_f4(gr + q * LANES * 4);
+                load_row<D>(a, row[r], li, rr[r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+            if (row[r] >= 0) update_row32<D>(a, row[r], li, rr[r], g32[r]);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_long_plan(UpdateArgs a) {
     using BlockScan = cub::BlockScan<int32_t, 1024>;
     __shared__ typename BlockScan::TempStorage tmp;
@@ -426,7 +586,7 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
         const int32_t u = a.long_list[e];
         const int64_t row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
         RowRegs<VPL> rr;
-        load_row<D>(a, row, li, rr);
+        if (!a.gbuf) load_row<D>(a, row, li, rr);
         dbl4 g[VPL];
 #pragma unroll
         for (int q = 0; q < VPL; ++q) g[q] = zero4d();
@@ -435,7 +595,13 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
 #pragma unroll
             for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], pp[q * LANES]);
         }
-        update_row<D>(a, row, li, rr, g);
+        if (a.gbuf) {  // split backward: the update kernel applies the optimizer
+            float *o = a.gbuf + a.pack_gbase[a.pack] + (int64_t)(u - a.pack_ustart[a.pack]) * D + li * 4;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) *reinterpret_cast<float4 *>(o + q * LANES * 4) = round4(g[q]);
+        } else {
+            update_row<D>(a, row, li, rr, g);
+        }
     }
 }
 
@@ -465,6 +631,20 @@ void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t 
         }                                                                                               \
         k_segsum_update<DD><<<blocks, 256, smem, s>>>(a);                                               \
     }
+    PICASSO_DISPATCH_D(D, CALL)
+#undef CALL
+}
+
+void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    const unsigned blocks = (unsigned)num_sms * 4;
+#define CALL(DD) k_segsum<DD><<<blocks, 256, 0, s>>>(a)
+    PICASSO_DISPATCH_D(D, CALL)
+#undef CALL
+}
+
+void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    const unsigned blocks = (unsigned)num_sms * 8;
+#define CALL(DD) k_update_rows<DD><<<blocks, 256, 0, s>>>(a)
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
 }

@@ -36,6 +36,8 @@ struct IndexArgs {
     int32_t *d_total;              // [1] U (all packs)
     unsigned long long *unique_gkey; // [N]
     int32_t *pack_ustart;          // [P+1]
+    const int32_t *pack_dim;       // [P]
+    int64_t *pack_gbase;           // [P+1] out: float offset of each pack's G rows (sum U_p * D_p)
     int *err;
 };
 
@@ -95,7 +97,11 @@ struct UpdateArgs {
     int32_t *long_cnt;           // [1]   this pack's counter
     int32_t *chunk_off;          // [cap+1]
     dbl4 *partial;               // [chunks, D/4] fp64 chunk partial sums
+    float *gbuf;                 // split backward: G rows of all packs (nullptr: fused)
+    const int64_t *pack_gbase;   // [P+1] float offset of each pack's G rows in gbuf
 };
+void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
+void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, int32_t n_cnt,
                        cudaStream_t s);
 void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -67,6 +68,10 @@ struct picasso_ctx {
     int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
     int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr;
     dbl4 *partial = nullptr;
+    float *gbuf = nullptr;
+    int64_t *pack_gbase = nullptr;
+    int32_t *pack_dim_d = nullptr;
+    bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
     std::vector<float *> w, s1, s2;
     // step state
     bool fwd_done = false;
@@ -143,6 +148,9 @@ struct picasso_ctx {
         int maxD = 4;
         for (int32_t d : pack_dim) maxD = std::max(maxD, d);
         partial = reinterpret_cast<dbl4 *>(c.take<double>(long_partial_doubles(N, maxD)));
+        pack_gbase = c.take<int64_t>(P + 1);
+        pack_dim_d = c.take<int32_t>(P);
+        gbuf = split_bwd ? c.take<float>((size_t)N * maxD) : nullptr;
         return c.off + kAlign;
     }
 };
@@ -216,6 +224,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     }
     c->pack_first_k[c->P] = c->F;
     c->cap = pow2_at_least((uint64_t)std::max<int64_t>(opts->max_ids, 1) * 2);
+    if (const char *e = std::getenv("PICASSO_BWD")) c->split_bwd = std::strcmp(e, "fused") != 0;
     c->ws_bytes = c->carve(nullptr);
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -271,6 +280,7 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemcpy(ctx->pm_fields_d, ctx->pm_fields.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_first_k_d, ctx->pack_first_k.data(), sizeof(int32_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->pack_dim_d, ctx->pack_dim.data(), sizeof(int32_t) * ctx->P, cudaMemcpyHostToDevice));
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
     ctx->bound = true;
     ctx->fwd_done = false;
@@ -308,6 +318,8 @@ static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t 
     a.d_total = ctx->d_total;
     a.unique_gkey = ctx->unique_gkey;
     a.pack_ustart = ctx->pack_ustart;
+    a.pack_dim = ctx->pack_dim_d;
+    a.pack_gbase = ctx->pack_gbase;
     a.err = ctx->err;
     return a;
 }
@@ -401,6 +413,8 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     u.long_list = ctx->long_list;
     u.chunk_off = ctx->chunk_off;
     u.partial = ctx->partial;
+    u.gbuf = ctx->split_bwd ? ctx->gbuf : nullptr;
+    u.pack_gbase = ctx->pack_gbase;
     if (N > 0) {
         for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
             u.pack = p;
@@ -409,8 +423,14 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
             u.weight = ctx->w[p];
             u.state1 = ctx->s1[p];
             u.state2 = ctx->s2[p];
-            launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-            ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+            if (ctx->split_bwd) {
+                launch_segsum(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->launches_bwd += 2 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+                launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
+            } else {
+                launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+            }
         }
     }
     ctx->mark(3, false, s);
