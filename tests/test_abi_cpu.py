@@ -70,7 +70,8 @@ def test_ctx_create_and_workspace(pb):
                                 cfg.field_col, cfg.out_width, 0, 1, cfg.batch, cfg.batch * cfg.F)
     try:
         ws = pb.picasso_workspace_size(ctx)
-        assert 16 * cfg.batch * cfg.F < ws < 200 * cfg.batch * cfg.F
+        # index scratch (~100 B / id) + the split backward's G buffer (4 * maxD B / id)
+        assert 16 * cfg.batch * cfg.F < ws < (200 + 4 * 128) * cfg.batch * cfg.F
         assert pb.picasso_pack_local_rows(ctx, 0) == int(cfg.table_rows.sum())
         with pytest.raises(pb.PicassoError):
             pb.picasso_pack_local_rows(ctx, 1)
