@@ -146,15 +146,21 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
     int32_t slot[kItems];
     bool first[kItems];
+    unsigned long long key[kItems];
     int32_t c = 0;
+    // all table reads before any table write: stores to table[] would otherwise order every
+    // later load behind them (possible aliasing) and serialise the round trips
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;
         first[i] = false;
         slot[i] = 0;
+        key[i] = 0;
         if (g < a.N) {
             slot[i] = a.slot_of[g];
-            first[i] = a.table[slot[i]].minpos == (unsigned int)g;
+            const ulonglong2 sv = *reinterpret_cast<const ulonglong2 *>(&a.table[slot[i]]);  // key | minpos,uid
+            key[i] = sv.x;
+            first[i] = (unsigned int)(sv.y & 0xffffffffull) == (unsigned int)g;
             c += first[i];
         }
     }
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
     for (int i = 0; i < kItems; ++i) {
         if (first[i]) {
             a.table[slot[i]].uid = uid;
-            a.unique_gkey[uid] = a.table[slot[i]].key;
+            a.unique_gkey[uid] = key[i];
             // the first position of a non-empty pack is always a first occurrence
             const int64_t g = g0 + i;
             const int64_t p = upper_bound_dev(a.pack_gstart, 0, a.P + 1, (int32_t)g) - 1;

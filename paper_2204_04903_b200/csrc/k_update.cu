@@ -532,7 +532,10 @@ __global__ void __launch_bounds__(1024) k_long_plan(UpdateArgs a) {
         }
         int32_t ex, agg;
         BlockScan(tmp).ExclusiveSum(n, ex, agg);
-        if (e < K) a.chunk_off[e] = carry + ex;
+        if (e < K) {
+            a.chunk_off[e] = carry + ex;
+            for (int32_t i = 0; i < n; ++i) a.chunk_row[carry + ex + i] = e;  // chunk -> row
+        }
         __syncthreads();
         if (threadIdx.x == 0) carry += agg;
         __syncthreads();
@@ -546,28 +549,64 @@ __global__ void __launch_bounds__(256) k_long_partial(UpdateArgs a) {
     const int li = threadIdx.x % LANES;
     const int32_t K = *a.long_cnt;
     if (K == 0) return;
+    constexpr int PPL = U > LANES ? U / LANES : 1, RND = LANES * PPL;
+    const int grp_in_warp = (threadIdx.x & 31) / LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp_in_warp * LANES));
     const int32_t total = a.chunk_off[K];
     const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / LANES;
+#pragma unroll 1
     for (int64_t c = grp; c < total; c += ngrp) {
-        const int64_t e = upper_bound_dev(a.chunk_off, 0, K + 1, (int32_t)c) - 1;
+        const int32_t e = a.chunk_row[c];
         const int32_t u = a.long_list[e];
         const int32_t ci = (int32_t)(c - a.chunk_off[e]);
         const int32_t p0 = __ldg(a.ustart + u) + ci * kChunk;
-        const int32_t p1 = min(p0 + kChunk, __ldg(a.ustart + u + 1));
+        const int32_t n = min(kChunk, __ldg(a.ustart + u + 1) - p0);
         dbl4 g[VPL];
 #pragma unroll
         for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-        for (int32_t p = p0; p < p1; p += U) {
-            float4 cc[U][VPL];
+#pragma unroll 1
+        for (int32_t q0 = 0; q0 < n; q0 += RND) {
+            // each lane resolves PPL occurrences; addresses broadcast, U dY rows in flight
+            int64_t myoff[PPL];
+            int32_t mylen[PPL];
 #pragma unroll
-            for (int k = 0; k < U; ++k)
-                if (p + k < p1) load_contrib<D>(a, __ldg(a.sorted_seg + p + k), li, cc[k]);
+            for (int p = 0; p < PPL; ++p) {
+                const int32_t q = q0 + p * LANES + li;
+                myoff[p] = 0;
+                mylen[p] = 0;
+                if (q < n) {
+                    const int32_t seg = __ldg(a.sorted_seg + p0 + q);
+                    const int32_t f = seg / a.B;
+                    myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
+                    if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
+                }
+            }
+            const int32_t nround = min(RND, n - q0);
+#pragma unroll 1
+            for (int k0 = 0; k0 < nround; k0 += U) {
+                float4 c4[U][VPL];
 #pragma unroll
-            for (int k = 0; k < U; ++k)
-                if (p + k < p1)
+                for (int k = 0; k < U; ++k) {
+                    const int src = (k0 + k) % LANES, slot = PPL > 1 ? k / LANES : 0;
+                    const int64_t off = __shfl_sync(gmask, myoff[slot], src, LANES);
+                    const int32_t len = __shfl_sync(gmask, mylen[slot], src, LANES);
+                    if (k0 + k < nround) {
+                        const float *p = a.dy + off + li * 4;
 #pragma unroll
-                    for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], cc[k][q]);
+                        for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = ldg_f4(p + qq * LANES * 4);
+                        if (a.pool_mean) {
+#pragma unroll
+                            for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = div4(c4[k][qq], (float)len);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+                    if (k0 + k < nround)
+#pragma unroll
+                        for (int qq = 0; qq < VPL; ++qq) g[qq] = add4d(g[qq], c4[k][qq]);
+            }
         }
         dbl4 *out = a.partial + c * (D / 4) + li;
 #pragma unroll
@@ -590,10 +629,22 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
         dbl4 g[VPL];
 #pragma unroll
         for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-        for (int32_t c = a.chunk_off[e]; c < a.chunk_off[e + 1]; ++c) {  // chunk order
-            const dbl4 *pp = a.partial + (int64_t)c * (D / 4) + li;
+        const int32_t c0 = a.chunk_off[e], c1 = a.chunk_off[e + 1];
+#pragma unroll 1
+        for (int32_t c = c0; c < c1; c += 8) {  // chunk order; 8 partial loads in flight
+            dbl4 pv[8][VPL];
 #pragma unroll
-            for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], pp[q * LANES]);
+            for (int k = 0; k < 8; ++k)
+                if (c + k < c1) {
+                    const dbl4 *pp = a.partial + (int64_t)(c + k) * (D / 4) + li;
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) pv[k][q] = pp[q * LANES];
+                }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (c + k < c1)
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], pv[k][q]);
         }
         if (a.gbuf) {  // split backward: the update kernel applies the optimizer
             float *o = a.gbuf + a.pack_gbase[a.pack] + (int64_t)(u - a.pack_ustart[a.pack]) * D + li * 4;

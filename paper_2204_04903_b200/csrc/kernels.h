@@ -96,6 +96,7 @@ struct UpdateArgs {
     int32_t *long_list;          // [cap] rows deferred to the chunked path (this pack)
     int32_t *long_cnt;           // [1]   this pack's counter
     int32_t *chunk_off;          // [cap+1]
+    int32_t *chunk_row;          // [chunks] deferred-row index of each chunk
     dbl4 *partial;               // [chunks, D/4] fp64 chunk partial sums
     float *gbuf;                 // split backward: G rows of all packs (nullptr: fused)
     const int64_t *pack_gbase;   // [P+1] float offset of each pack's G rows in gbuf

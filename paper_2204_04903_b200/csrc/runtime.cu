@@ -66,7 +66,7 @@ struct picasso_ctx {
     int *err = nullptr;
     unsigned long long *unique_gkey = nullptr;
     int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
-    int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr;
+    int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr, *chunk_row = nullptr;
     dbl4 *partial = nullptr;
     float *gbuf = nullptr;
     int64_t *pack_gbase = nullptr;
@@ -148,6 +148,7 @@ struct picasso_ctx {
         int maxD = 4;
         for (int32_t d : pack_dim) maxD = std::max(maxD, d);
         partial = reinterpret_cast<dbl4 *>(c.take<double>(long_partial_doubles(N, maxD)));
+        chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
         pack_gbase = c.take<int64_t>(P + 1);
         pack_dim_d = c.take<int32_t>(P);
         gbuf = split_bwd ? c.take<float>((size_t)N * maxD) : nullptr;
@@ -413,6 +414,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     u.long_list = ctx->long_list;
     u.chunk_off = ctx->chunk_off;
     u.partial = ctx->partial;
+    u.chunk_row = ctx->chunk_row;
     u.gbuf = ctx->split_bwd ? ctx->gbuf : nullptr;
     u.pack_gbase = ctx->pack_gbase;
     if (N > 0) {
