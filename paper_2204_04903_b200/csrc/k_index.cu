@@ -181,10 +181,36 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
     }
 }
 
+// inverse[g] = uid; also the digit histogram of the backward's first radix pass over this
+// 2048-position tile (digit-major, so the sort starts with its scan: one pass over N saved)
 __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < a.N) a.inverse[g] = a.table[a.slot_of[g]].uid;
-    if (g == 0) {  // uid ranges of empty packs (and the end) — k_assign filled the others
+    __shared__ int32_t h[kMaxRadix];
+    const int radix = 1 << a.sort_bits0;
+    for (int d = threadIdx.x; d < radix; d += kTileThreads) h[d] = 0;
+    __syncthreads();
+    const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const int64_t g = g0 + i;
+        const bool valid = g < a.N;
+        int32_t uid = 0;
+        if (valid) {
+            uid = a.table[a.slot_of[g]].uid;
+            a.inverse[g] = uid;
+        }
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const int d = uid & (radix - 1);
+            const unsigned peers = __match_any_sync(vm, d);
+            if (lane == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    const int64_t nblk = (a.N + kTile - 1) / kTile;
+    if (a.N > 0)
+        for (int d = threadIdx.x; d < radix; d += kTileThreads) a.sort_hist0[(int64_t)d * nblk + blockIdx.x] = h[d];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // uid ranges of empty packs (and the end)
         int32_t next = *a.d_total;
         a.pack_ustart[a.P] = next;
         for (int p = a.P - 1; p >= 0; --p) {
@@ -228,7 +254,7 @@ void launch_dedup_assign(const IndexArgs &a, cudaStream_t s) {
     } else {
         cudaMemsetAsync(a.d_total, 0, sizeof(int32_t), s);
     }
-    k_inverse<<<(unsigned)std::max<int64_t>(1, (a.N + 255) / 256), 256, 0, s>>>(a);
+    k_inverse<<<(unsigned)std::max<int64_t>(1, nb), kTileThreads, 0, s>>>(a);
 }
 
 }  // namespace picasso

@@ -1,0 +1,177 @@
+// k_sort2.cu — the backward's transpose: stable LSD radix sort of (uid, segment) pairs with
+// passes of up to 10 bits and two launches per pass.
+//
+// The backward needs, per unique row, its occurrences in ascending packed
+// position: a stable sort of the forward's inverse index by uid.  Per pass:
+//   k_scan_rows    : one block per digit scans its row of the digit-major per-tile histogram
+//                    (exclusive, in place), writes the digit total, and zeroes the same row of
+//                    the other histogram buffer for the next pass;
+//   k_scatter2     : every block scans the digit totals (<= 1024) in shared memory, ranks its
+//                    2048 keys stably (each warp takes 256 contiguous keys in 8 rounds of
+//                    __match_any_sync), scatters them, and — when another pass follows — adds
+//                    each key's next digit to the next pass's histogram of the tile it lands in.
+// The first pass's histogram comes from k_inverse, so a 2-pass sort is 4 launches.
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.h"
+
+namespace picasso {
+
+SortPlan make_sort_plan(int64_t n) {
+    int bits = 1;
+    while (bits < 31 && ((int64_t)1 << bits) < n) ++bits;  // keys (uids) < U <= n
+    SortPlan p{};
+    p.passes = (bits + kMaxRadixBits - 1) / kMaxRadixBits;
+    int shift = 0;
+    for (int i = 0; i < p.passes; ++i) {
+        const int b = (bits - shift + (p.passes - i) - 1) / (p.passes - i);
+        p.bits[i] = b;
+        p.shift[i] = shift;
+        shift += b;
+    }
+    return p;
+}
+
+size_t radix_hist2_ints(int64_t n) { return (size_t)kMaxRadix * (size_t)((n + kTile - 1) / kTile) + 1; }
+
+__global__ void __launch_bounds__(1024) k_scan_rows(int32_t *hist, int64_t nblk, int32_t *rowtot, int32_t *zero_next,
+                                                    int next_radix) {
+    using BlockScan = cub::BlockScan<int32_t, 1024>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ int32_t carry;
+    const int d = blockIdx.x;
+    int32_t *row = hist + (int64_t)d * nblk;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nblk; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        int32_t v = i < nblk ? row[i] : 0, e, agg;
+        BlockScan(tmp).ExclusiveSum(v, e, agg);
+        if (i < nblk) row[i] = carry + e;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) rowtot[d] = carry;
+    if (zero_next) {  // the next pass's histogram rows owned by this block
+        for (int dd = d; dd < next_radix; dd += gridDim.x)
+            for (int64_t i = threadIdx.x; i < nblk; i += 1024) zero_next[(int64_t)dd * nblk + i] = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_scatter2(const int32_t *kin, const int32_t *vin, int32_t *kout,
+                                                           int32_t *vout, int64_t n, int shift, int bits,
+                                                           const int32_t *hist_off, const int32_t *rowtot,
+                                                           int64_t nblk, int32_t *hist_next, int next_shift,
+                                                           int next_bits) {
+    constexpr int kWarps = kTileThreads / 32;
+    constexpr int kRounds = kTile / kTileThreads;  // 8 rounds of 32 keys per warp
+    __shared__ int32_t wc[kWarps][kMaxRadix];
+    __shared__ int32_t dbase[kMaxRadix];
+    using BlockScan = cub::BlockScan<int32_t, kTileThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    const int radix = 1 << bits;
+    const unsigned dmask = (unsigned)radix - 1u;
+    for (int i = threadIdx.x; i < kWarps * kMaxRadix; i += kTileThreads) (&wc[0][0])[i] = 0;
+    {   // digit bases: exclusive scan of the digit totals (radix <= 1024 = 4 per thread)
+        constexpr int PER = kMaxRadix / kTileThreads;
+        int32_t v[PER], s = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int d = threadIdx.x * PER + i;
+            v[i] = d < radix ? rowtot[d] : 0;
+            s += v[i];
+        }
+        int32_t e;
+        BlockScan(tmp).ExclusiveSum(s, e);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            dbase[threadIdx.x * PER + i] = e;
+            e += v[i];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)w * (32 * kRounds);
+    int32_t key[kRounds], val[kRounds], rk[kRounds];
+    int dg[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t g = base + r * 32 + lane;
+        const bool valid = g < n;
+        key[r] = valid ? kin[g] : 0;
+        val[r] = valid ? vin[g] : 0;
+        dg[r] = valid ? (int)(((unsigned)key[r] >> shift) & dmask) : (kMaxRadix + lane);
+        const unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
+        int32_t before = 0;
+        if (valid) before = wc[w][dg[r]];
+        rk[r] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wc[w][dg[r]] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < radix; d += kTileThreads) {  // prefix across warps + global offset
+        int32_t run = dbase[d] + hist_off[(int64_t)d * nblk + blockIdx.x];
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ++ww) {
+            const int32_t t = wc[ww][d];
+            wc[ww][d] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    const unsigned nmask = (1u << next_bits) - 1u;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t g = base + r * 32 + lane;
+        const bool valid = g < n;
+        int32_t pos = 0;
+        if (valid) {
+            pos = wc[w][dg[r]] + rk[r];
+            kout[pos] = key[r];
+            vout[pos] = val[r];
+        }
+        if (hist_next) {  // next pass: digit of this key in the tile it lands in
+            const unsigned vm = __ballot_sync(0xffffffffu, valid);
+            if (valid) {
+                const int64_t slot = (int64_t)(((unsigned)key[r] >> next_shift) & nmask) * nblk + pos / kTile;
+                const unsigned peers = __match_any_sync(vm, (unsigned long long)slot);
+                if (lane == __ffs(peers) - 1) atomicAdd(hist_next + slot, (int32_t)__popc(peers));
+            }
+        }
+    }
+}
+
+void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, int32_t *v_a, int32_t *k_b,
+                       int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
+                       int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches) {
+    const int64_t nblk = (n + kTile - 1) / kTile;
+    const int32_t *ck = k_in, *cv = v_in;
+    int32_t *bufk[2] = {k_a, k_b}, *bufv[2] = {v_a, v_b};
+    int32_t *hist[2] = {hist0, hist1};
+    if (nblk == 0) {
+        *k_out = const_cast<int32_t *>(ck);
+        *v_out = const_cast<int32_t *>(cv);
+        return;
+    }
+    for (int p = 0; p < plan.passes; ++p) {
+        const bool more = p + 1 < plan.passes;
+        const int radix = 1 << plan.bits[p];
+        const int next_radix = more ? 1 << plan.bits[p + 1] : 0;
+        k_scan_rows<<<radix, 1024, 0, s>>>(hist[p & 1], nblk, rowtot, more ? hist[(p + 1) & 1] : nullptr,
+                                           next_radix);
+        k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
+                                                          plan.bits[p], hist[p & 1], rowtot, nblk,
+                                                          more ? hist[(p + 1) & 1] : nullptr,
+                                                          more ? plan.shift[p + 1] : 0, more ? plan.bits[p + 1] : 0);
+        *launches += 2;
+        ck = bufk[p & 1];
+        cv = bufv[p & 1];
+    }
+    *k_out = const_cast<int32_t *>(ck);
+    *v_out = const_cast<int32_t *>(cv);
+}
+
+}  // namespace picasso

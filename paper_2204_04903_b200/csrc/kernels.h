@@ -38,8 +38,26 @@ struct IndexArgs {
     int32_t *pack_ustart;          // [P+1]
     const int32_t *pack_dim;       // [P]
     int64_t *pack_gbase;           // [P+1] out: float offset of each pack's G rows (sum U_p * D_p)
+    int32_t sort_bits0;            // digit width of the backward's first radix pass
+    int32_t *sort_hist0;           // [radix0, nblk] out: digit-major histogram of that pass
     int *err;
 };
+
+// Radix sort plan of the backward's transpose: keys (uids) < 2^bits, passes of <= 10 bits.
+constexpr int kMaxRadixBits = 10;
+constexpr int kMaxRadix = 1 << kMaxRadixBits;
+struct SortPlan {
+    int passes;
+    int bits[4];
+    int shift[4];
+};
+SortPlan make_sort_plan(int64_t n);
+// Stable LSD radix sort of (key, val) int32 pairs; hist0 = digit-major histogram of pass 0
+// (from k_inverse).  hist1: scratch of the same size; rowtot: [kMaxRadix].
+void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, int32_t *v_a, int32_t *k_b,
+                       int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
+                       int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches);
+size_t radix_hist2_ints(int64_t n);
 
 // k_index.cu
 void launch_field_prep(const IndexArgs &a, cudaStream_t s);

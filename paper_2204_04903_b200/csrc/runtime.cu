@@ -66,6 +66,8 @@ struct picasso_ctx {
     int *err = nullptr;
     unsigned long long *unique_gkey = nullptr;
     int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
+    int32_t *hist0 = nullptr, *hist1 = nullptr, *rowtot = nullptr;
+    SortPlan splan{};
     int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr, *chunk_row = nullptr;
     dbl4 *partial = nullptr;
     float *gbuf = nullptr;
@@ -140,8 +142,9 @@ struct picasso_ctx {
         v_a = c.take<int32_t>(N);
         k_b = c.take<int32_t>(N);
         v_b = c.take<int32_t>(N);
-        hist = c.take<int32_t>(radix_hist_ints(N));
-        scratch = c.take<int32_t>(scan_scratch_ints((int64_t)radix_hist_ints(N)) + 16);
+        hist0 = c.take<int32_t>(radix_hist2_ints(N));
+        hist1 = c.take<int32_t>(radix_hist2_ints(N));
+        rowtot = c.take<int32_t>(kMaxRadix);
         ustart = c.take<int32_t>(N + 1);
         long_list = c.take<int32_t>(N / (kLongRow + 1) + 2);
         chunk_off = c.take<int32_t>(N / (kLongRow + 1) + 3);
@@ -321,6 +324,9 @@ static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t 
     a.pack_ustart = ctx->pack_ustart;
     a.pack_dim = ctx->pack_dim_d;
     a.pack_gbase = ctx->pack_gbase;
+    ctx->splan = make_sort_plan(std::max<int64_t>(N, 1));
+    a.sort_bits0 = ctx->splan.bits[0];
+    a.sort_hist0 = ctx->hist0;
     a.err = ctx->err;
     return a;
 }
@@ -383,8 +389,8 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     const int64_t N = ctx->N;
     int32_t *su = nullptr, *sseg = nullptr;
     ctx->mark(2, true, s);
-    radix_sort_pairs(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N,
-                     bits_for(std::max<int64_t>(N - 1, 1)), ctx->hist, ctx->scratch, s, &ctx->launches_bwd);
+    radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N, ctx->splan,
+                      ctx->hist0, ctx->hist1, ctx->rowtot, s, &ctx->launches_bwd);
     launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
     ctx->mark(2, false, s);
     ctx->launches_bwd += N > 0 ? 1 : 0;
