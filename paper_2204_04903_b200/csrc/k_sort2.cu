@@ -34,29 +34,31 @@ SortPlan make_sort_plan(int64_t n) {
 
 size_t radix_hist2_ints(int64_t n) { return (size_t)kMaxRadix * (size_t)((n + kTile - 1) / kTile) + 1; }
 
-__global__ void __launch_bounds__(1024) k_scan_rows(int32_t *hist, int64_t nblk, int32_t *rowtot, int32_t *zero_next,
-                                                    int next_radix) {
-    using BlockScan = cub::BlockScan<int32_t, 1024>;
-    __shared__ typename BlockScan::TempStorage tmp;
-    __shared__ int32_t carry;
-    const int d = blockIdx.x;
-    int32_t *row = hist + (int64_t)d * nblk;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < nblk; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        int32_t v = i < nblk ? row[i] : 0, e, agg;
-        BlockScan(tmp).ExclusiveSum(v, e, agg);
-        if (i < nblk) row[i] = carry + e;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
+// one warp per digit row: rows are short (nblk = N / 2048 tiles), so a warp-level scan with a
+// running carry keeps 8 rows per 256-thread block busy instead of idling 1024 threads per row
+__global__ void __launch_bounds__(256) k_scan_rows(int32_t *hist, int64_t nblk, int32_t *rowtot, int32_t *zero_next,
+                                                   int radix, int next_radix) {
+    const int lane = threadIdx.x & 31;
+    const int d = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (d < radix) {
+        int32_t *row = hist + (int64_t)d * nblk;
+        int32_t carry = 0;
+        for (int64_t base = 0; base < nblk; base += 32) {
+            const int64_t i = base + lane;
+            const int32_t v = i < nblk ? row[i] : 0;
+            int32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (i < nblk) row[i] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) rowtot[d] = carry;
     }
-    if (threadIdx.x == 0) rowtot[d] = carry;
-    if (zero_next) {  // the next pass's histogram rows owned by this block
-        for (int dd = d; dd < next_radix; dd += gridDim.x)
-            for (int64_t i = threadIdx.x; i < nblk; i += 1024) zero_next[(int64_t)dd * nblk + i] = 0;
-    }
+    if (zero_next && d < next_radix)  // the next pass's histogram row of the same index
+        for (int64_t i = lane; i < nblk; i += 32) zero_next[(int64_t)d * nblk + i] = 0;
 }
 
 __global__ void __launch_bounds__(kTileThreads) k_scatter2(const int32_t *kin, const int32_t *vin, int32_t *kout,
@@ -160,8 +162,9 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
         const bool more = p + 1 < plan.passes;
         const int radix = 1 << plan.bits[p];
         const int next_radix = more ? 1 << plan.bits[p + 1] : 0;
-        k_scan_rows<<<radix, 1024, 0, s>>>(hist[p & 1], nblk, rowtot, more ? hist[(p + 1) & 1] : nullptr,
-                                           next_radix);
+        const int rows = radix > next_radix ? radix : next_radix;
+        k_scan_rows<<<(rows + 7) / 8, 256, 0, s>>>(hist[p & 1], nblk, rowtot, more ? hist[(p + 1) & 1] : nullptr,
+                                                   radix, next_radix);
         k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
                                                           plan.bits[p], hist[p & 1], rowtot, nblk,
                                                           more ? hist[(p + 1) & 1] : nullptr,

@@ -32,7 +32,7 @@
 
 namespace picasso {
 
-constexpr int kChunk = 128;
+constexpr int kChunk = 64;  // occurrences per hot-row chunk (latency per chunk vs partials to combine)
 
 __global__ void k_csr_bounds(const int32_t *su, int64_t N, int32_t *ustart) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
