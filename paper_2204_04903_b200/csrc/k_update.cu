@@ -32,7 +32,8 @@
 
 namespace picasso {
 
-constexpr int kChunk = 64;  // occurrences per hot-row chunk (latency per chunk vs partials to combine)
+constexpr int kChunk = 64;      // occurrences per hot-row chunk (latency per chunk vs partials to combine)
+constexpr int kMaxChunks = 64;  // chunks per hot row at most (bounds the final combine)
 
 __global__ void k_csr_bounds(const int32_t *su, int64_t N, int32_t *ustart) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(1024) k_long_plan(UpdateArgs a) {
         int32_t n = 0;
         if (e < K) {
             const int32_t u = a.long_list[e];
-            n = (__ldg(a.ustart + u + 1) - __ldg(a.ustart + u) + kChunk - 1) / kChunk;
+            n = min((__ldg(a.ustart + u + 1) - __ldg(a.ustart + u) + kChunk - 1) / kChunk, kMaxChunks);
         }
         int32_t ex, agg;
         BlockScan(tmp).ExclusiveSum(n, ex, agg);
@@ -560,8 +561,11 @@ __global__ void __launch_bounds__(256) k_long_partial(UpdateArgs a) {
         const int32_t e = a.chunk_row[c];
         const int32_t u = a.long_list[e];
         const int32_t ci = (int32_t)(c - a.chunk_off[e]);
-        const int32_t p0 = __ldg(a.ustart + u) + ci * kChunk;
-        const int32_t n = min(kChunk, __ldg(a.ustart + u + 1) - p0);
+        // a row of len occurrences is cut into nc = min(ceil(len/kChunk), kMaxChunks) equal chunks
+        const int32_t r0 = __ldg(a.ustart + u), len = __ldg(a.ustart + u + 1) - r0;
+        const int32_t nc = a.chunk_off[e + 1] - a.chunk_off[e], clen = (len + nc - 1) / nc;
+        const int32_t p0 = r0 + ci * clen;
+        const int32_t n = min(clen, r0 + len - p0);
         dbl4 g[VPL];
 #pragma unroll
         for (int q = 0; q < VPL; ++q) g[q] = zero4d();
@@ -631,17 +635,17 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
         for (int q = 0; q < VPL; ++q) g[q] = zero4d();
         const int32_t c0 = a.chunk_off[e], c1 = a.chunk_off[e + 1];
 #pragma unroll 1
-        for (int32_t c = c0; c < c1; c += 8) {  // chunk order; 8 partial loads in flight
-            dbl4 pv[8][VPL];
+        for (int32_t c = c0; c < c1; c += 16) {  // chunk order; 16 partial loads in flight
+            dbl4 pv[16][VPL];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < 16; ++k)
                 if (c + k < c1) {
                     const dbl4 *pp = a.partial + (int64_t)(c + k) * (D / 4) + li;
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) pv[k][q] = pp[q * LANES];
                 }
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < 16; ++k)
                 if (c + k < c1)
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], pv[k][q]);
