@@ -97,13 +97,23 @@ typedef struct {
     int32_t opt;           /* picasso_opt */
     float eps;             /* Adagrad 1e-10 / Adam 1e-8 */
     float beta1, beta2;    /* Adam (0.9, 0.999) */
+    int64_t max_recv;      /* world > 1: keys this rank may receive per step as an owner
+                              (0 = 2 * max_ids); exceeding it fails the step with CAPACITY */
 } picasso_ctx_opts;
 
-/* 2. Context.  rank/world: this process's place in the row-sharded group (owner of pack
- * key k = k mod world, local row = k div world; reading O3).  This build: world == 1.
+/* NCCL unique id (128 bytes, host) for picasso_ctx_create; rank 0 calls it and broadcasts
+ * the bytes to the other ranks (e.g. over torch.distributed). */
+picasso_status picasso_nccl_unique_id(uint8_t *out);
+
+/* 2. Context.  rank/world (1 <= world <= 8): this rank's place in the row-sharded group —
+ * owner of pack key k is rank k mod world, at local row k div world (reading O3; PAPER.md
+ * L192-195 model parallelism).  nccl_uid: world > 1 with one process per GPU — the 128-byte
+ * NCCL id; the communicator is created in picasso_bind (a collective over the world).
+ * nccl_uid == NULL with world > 1: "loopback" — all ranks live in this process on one device
+ * and are driven together through picasso_group_* (tests of W up to 8 without 8 GPUs).
  * Errors: INVALID_ARG / PLAN_MISMATCH on inconsistent plans or options. */
 picasso_status picasso_ctx_create(const picasso_plan_view *plan, int32_t rank, int32_t world,
-                                  const picasso_ctx_opts *opts, picasso_ctx **out);
+                                  const uint8_t *nccl_uid, const picasso_ctx_opts *opts, picasso_ctx **out);
 /* Bytes of device workspace the ctx needs (depends on max_batch, max_ids, plan). */
 picasso_status picasso_workspace_size(const picasso_ctx *ctx, size_t *bytes);
 /* Rows of pack p held by this rank: ceil((pack_rows[p] - rank) / world). */
@@ -160,11 +170,12 @@ picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, int32_t *dst,
 picasso_status picasso_launch_count(const picasso_ctx *ctx, int64_t *fwd, int64_t *bwd);
 
 /* Phase timing with CUDA events recorded on the caller's stream around each phase of the
- * step: 0 = ID hash + Unique (k_field_prep .. k_pack_ustart), 1 = gather/pool (k_pool),
- * 2 = occurrence transpose (radix sort + k_csr_bounds), 3 = segment-sum + optimizer
- * (k_segsum_update + k_long_update).  picasso_profile_read synchronises, writes the summed
- * milliseconds of each phase since the last read into ms[4] (host), the number of steps
- * into *calls, and resets.  Off by default. */
+ * step: 0 = ID hash + Unique (+ Partition at world > 1), 1 = gather/pool (k_pool),
+ * 2 = occurrence transpose (radix sort + k_csr_bounds), 3 = segment-sum (+ optimizer at
+ * world == 1), 4 = owner dedup + gather (world > 1), 5 = owner reduce + optimizer (world > 1).
+ * The exchanges themselves are outside every phase.  picasso_profile_read synchronises,
+ * writes the summed milliseconds of each phase since the last read into ms[6] (host), the
+ * number of steps into *calls, and resets.  Off by default. */
 picasso_status picasso_profile_enable(picasso_ctx *ctx, int32_t on);
 picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int64_t *calls);
 
@@ -172,6 +183,30 @@ picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int64_t *calls)
  * pack p = [u[p], u[p+1])), copied asynchronously on `stream` into dst (device memory or
  * pinned host memory).  Enqueue-only; the caller synchronises. */
 picasso_status picasso_unique_offsets(picasso_ctx *ctx, int32_t *dst, void *stream);
+
+/* ------------------------------------------------------------------------------------ */
+/* 5. Row-sharded step at world > 1 (PAPER.md L192-195 MP strategy, L209-215 operators).
+ * With NCCL (one process per GPU) the ordinary picasso_packed_lookup_fwd / _bwd_update run
+ * the sharded step: Unique & Partition -> counts exchange (one host synchronisation: NCCL
+ * needs host-side sizes) -> IDs AllToAllv -> owner dedup + Gather -> rows AllToAllv ->
+ * pooling from the received rows (Stitch fused) ; backward: segment-sum into the send
+ * layout -> gradients AllToAllv -> owner reduce over <= world contributions (source rank
+ * ascending, fp64) + optimizer.  Per-requester gradient partials travel as fp32 (reading O6).
+ * The loopback group runs the same phases for all ranks of one process, with device copies
+ * for the exchanges; its arguments are per-rank arrays of what fwd/bwd_update take. */
+typedef struct picasso_group picasso_group;
+picasso_status picasso_group_create(picasso_ctx *const *ctxs, int32_t world, picasso_group **out);
+picasso_status picasso_group_destroy(picasso_group *group);
+picasso_status picasso_group_fwd(picasso_group *group, const int64_t *const *ids, const int32_t *const *offsets,
+                                 const int32_t *batch, const int64_t *n_ids, float *const *out, void *stream);
+picasso_status picasso_group_bwd_update(picasso_group *group, const float *const *grad_out, float lr, int64_t step,
+                                        void *stream);
+/* Owner-side intermediate of the last forward (world > 1; tests, synchronises): the owner's
+ * unique local rows of pack p in first-occurrence order of the received lists concatenated by
+ * source rank (int64, copied to dst), and the per-peer key counts this rank sent (int64 [world],
+ * host). */
+picasso_status picasso_get_owner_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n);
+picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts);
 
 #ifdef __cplusplus
 }

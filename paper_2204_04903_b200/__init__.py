@@ -24,6 +24,13 @@ from .abi import (  # noqa: F401
     picasso_profile_enable,
     picasso_profile_read,
     picasso_unique_offsets,
+    picasso_nccl_unique_id,
+    picasso_group_create,
+    picasso_group_destroy,
+    picasso_group_fwd,
+    picasso_group_bwd_update,
+    picasso_get_owner_unique,
+    picasso_get_send_counts,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
-from .embedding import PackedEmbedding  # noqa: F401
+from .embedding import LoopbackGroup, PackedEmbedding  # noqa: F401

@@ -19,8 +19,10 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "PLAN_MISMATCH", -3: "ID_RANGE", -4: 
 EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", "picasso_pack_local_rows",
            "picasso_bind", "picasso_ctx_destroy", "picasso_packed_lookup_fwd", "picasso_packed_lookup_bwd_update",
            "picasso_last_error", "picasso_get_unique", "picasso_get_inverse", "picasso_launch_count",
-           "picasso_profile_enable", "picasso_profile_read", "picasso_unique_offsets"]
-PHASES = ["unique", "pool", "transpose", "segsum_update"]
+           "picasso_profile_enable", "picasso_profile_read", "picasso_unique_offsets", "picasso_nccl_unique_id",
+           "picasso_group_create", "picasso_group_destroy", "picasso_group_fwd", "picasso_group_bwd_update",
+           "picasso_get_owner_unique", "picasso_get_send_counts"]
+PHASES = ["unique", "pool", "transpose", "segsum_update", "owner_gather", "owner_update"]
 
 
 class PicassoError(RuntimeError):
@@ -38,7 +40,8 @@ class PlanView(C.Structure):
 
 class CtxOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_ids", C.c_int64), ("pool", C.c_int32), ("id_mode", C.c_int32),
-                ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float)]
+                ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("max_recv", C.c_int64)]
 
 
 _lib = None
@@ -54,7 +57,14 @@ def lib():
         vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         sig = {
             "picasso_pack_plan": [i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],
-            "picasso_ctx_create": [C.POINTER(PlanView), i32, i32, C.POINTER(CtxOpts), C.POINTER(vp)],
+            "picasso_ctx_create": [C.POINTER(PlanView), i32, i32, vp, C.POINTER(CtxOpts), C.POINTER(vp)],
+            "picasso_nccl_unique_id": [vp],
+            "picasso_group_create": [vp, i32, C.POINTER(vp)],
+            "picasso_group_destroy": [vp],
+            "picasso_group_fwd": [vp, vp, vp, vp, vp, vp, vp],
+            "picasso_group_bwd_update": [vp, vp, C.c_float, i64, vp],
+            "picasso_get_owner_unique": [vp, i32, vp, i64, C.POINTER(i64)],
+            "picasso_get_send_counts": [vp, vp],
             "picasso_workspace_size": [vp, C.POINTER(C.c_size_t)],
             "picasso_pack_local_rows": [vp, i32, C.POINTER(i64)],
             "picasso_bind": [vp, vp, C.c_size_t, vp, vp, vp],
@@ -124,9 +134,15 @@ class _Keep:
     """Keeps numpy arrays referenced by a C struct alive."""
 
 
+def picasso_nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    _chk(lib().picasso_nccl_unique_id(buf), "picasso_nccl_unique_id")
+    return bytes(buf)
+
+
 def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, field_col, out_width, rank, world,
                        max_batch, max_ids, pool=POOL_SUM, id_mode=IDS_HASH, opt=OPT_ADAGRAD, eps=None, beta1=0.9,
-                       beta2=0.999):
+                       beta2=0.999, nccl_uid=None, max_recv=0):
     k = _Keep()
     k.f2t = _np(field_to_table, np.int32)
     k.t2p = _np(plan["table_to_pack"], np.int32)
@@ -141,9 +157,10 @@ def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, 
     if eps is None:
         eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
     o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),
-                float(beta2))
+                float(beta2), int(max_recv))
     ctx = C.c_void_p()
-    _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), C.byref(o), C.byref(ctx)),
+    uid = None if nccl_uid is None else (C.c_uint8 * 128)(*nccl_uid)
+    _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), uid, C.byref(o), C.byref(ctx)),
          "picasso_ctx_create")
     return ctx
 
@@ -221,10 +238,56 @@ def picasso_profile_enable(ctx, on=True):
 
 def picasso_profile_read(ctx):
     """{phase: summed ms since the last read}, number of profiled steps."""
-    ms = (C.c_float * 4)()
+    ms = (C.c_float * len(PHASES))()
     n = C.c_int64()
     _chk(lib().picasso_profile_read(ctx, ms, C.byref(n)), "picasso_profile_read", ctx)
-    return {PHASES[i]: float(ms[i]) for i in range(4)}, n.value
+    return {PHASES[i]: float(ms[i]) for i in range(len(PHASES))}, n.value
+
+
+# ---- world > 1 ---------------------------------------------------------------------------
+def picasso_group_create(ctxs):
+    arr = (C.c_void_p * len(ctxs))(*[c.value for c in ctxs])
+    g = C.c_void_p()
+    _chk(lib().picasso_group_create(arr, len(ctxs), C.byref(g)), "picasso_group_create")
+    return g
+
+
+def picasso_group_destroy(group):
+    lib().picasso_group_destroy(group)
+
+
+def _ptrs(ts):
+    return (C.c_void_p * len(ts))(*[t.data_ptr() if t.numel() else None for t in ts])
+
+
+def picasso_group_fwd(group, ids, offsets, batch, out, stream=None):
+    W = len(ids)
+    b = (C.c_int32 * W)(*[int(x) for x in batch])
+    n = (C.c_int64 * W)(*[int(t.numel()) for t in ids])
+    _chk(lib().picasso_group_fwd(group, _ptrs(ids), _ptrs(offsets), b, n, _ptrs(out), _stream(stream)),
+         "picasso_group_fwd")
+
+
+def picasso_group_bwd_update(group, grad_out, lr, step, stream=None):
+    _chk(lib().picasso_group_bwd_update(group, _ptrs(grad_out), float(lr), int(step), _stream(stream)),
+         "picasso_group_bwd_update")
+
+
+def picasso_get_owner_unique(ctx, pack, device):
+    import torch
+
+    n = C.c_int64()
+    _chk(lib().picasso_get_owner_unique(ctx, int(pack), None, 0, C.byref(n)), "picasso_get_owner_unique", ctx)
+    out = torch.empty(max(n.value, 1), dtype=torch.int64, device=device)
+    _chk(lib().picasso_get_owner_unique(ctx, int(pack), _ptr(out), n.value, C.byref(n)), "picasso_get_owner_unique",
+         ctx)
+    return out[:n.value]
+
+
+def picasso_get_send_counts(ctx, world):
+    arr = (C.c_int64 * world)()
+    _chk(lib().picasso_get_send_counts(ctx, arr), "picasso_get_send_counts", ctx)
+    return list(arr)
 
 
 def picasso_unique_offsets(ctx, dst, stream=None):

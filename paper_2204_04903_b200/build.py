@@ -14,8 +14,22 @@ OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpicasso.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+
+def _nccl_dir():
+    """NCCL 2.28 from the nvidia-nccl wheel torch loads (never the system 2.27 copy)."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia-nccl wheel not found")
+    return list(spec.submodule_search_locations)[0]
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include")]
 
 
 def _needs(obj, src, deps):
@@ -52,7 +66,9 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
             if verbose and err:
                 print(err)
     if cmds or not os.path.exists(LIB):
-        link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-fPIC"]
+        nlib = os.path.join(NCCL, "lib")
+        link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-fPIC", "-L", nlib,
+                "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib]
         run(link)
         os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -1,0 +1,239 @@
+// ctx.h — the context object behind the C ABI (internal).
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "kernels.h"
+#include "multi.h"
+#include "picasso.h"
+
+using namespace picasso;
+
+namespace ctxutil {
+
+constexpr size_t kAlign = 256;
+
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    T *take(size_t n) {
+        off = (off + kAlign - 1) / kAlign * kAlign;
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += n * sizeof(T);
+        return p;
+    }
+};
+
+inline uint32_t pow2_at_least(uint64_t x) {
+    uint64_t p = 1024;
+    while (p < x) p <<= 1;
+    return (uint32_t)p;
+}
+
+inline int bits_for(int64_t maxval) {
+    int b = 1;
+    while (b < 31 && ((int64_t)1 << b) <= maxval) ++b;
+    return b;
+}
+
+}  // namespace ctxutil
+using namespace ctxutil;
+
+struct picasso_group;
+
+// Per-rank state of the row-sharded step (world > 1), host side.
+struct MultiState {
+    ncclComm_t comm = nullptr;       // NCCL mode
+    picasso_group *group = nullptr;  // loopback mode (all ranks in one process)
+    int64_t max_recv = 0;
+    // device
+    int32_t *bkey = nullptr, *bval = nullptr, *bsorted = nullptr, *send_uid = nullptr, *bhist = nullptr,
+            *bcount = nullptr;
+    int64_t *bstart = nullptr, *sroff = nullptr;
+    int32_t *send_pos = nullptr, *send_keys = nullptr;
+    int64_t *row_off = nullptr;
+    int32_t *cnt_recv_d = nullptr;   // [W*P] counts this rank receives, (source, pack)
+    int32_t *recv_keys = nullptr, *opos_map = nullptr, *oslot = nullptr, *oinv = nullptr;
+    unsigned long long *ouid_key = nullptr;
+    int32_t *opack_gstart = nullptr, *opack_ustart = nullptr, *od_total = nullptr, *oblk_cnt = nullptr,
+            *oblk_off = nullptr;
+    int64_t *opack_ostart_d = nullptr, *ogbase_scratch = nullptr;
+    OwnerBlock *oblk_d = nullptr;
+    int32_t *contrib = nullptr;
+    int64_t *rsend_off = nullptr;
+    float *rows_send = nullptr;
+    // host (pinned staging for the counts / block tables)
+    int32_t *cnt_send_h = nullptr, *cnt_recv_h = nullptr;
+    OwnerBlock *oblk_h = nullptr;
+    int32_t *og_h = nullptr;
+    uint8_t uid[128] = {0};
+    bool has_uid = false;
+    int64_t *ostart_h = nullptr;
+    std::vector<int64_t> skoff, sk, rkoff, rk, srow_off, srow_n, rrow_off, rrow_n;  // per peer
+    int64_t R = 0, U_send = 0;
+    std::vector<int64_t> opack_ostart;  // [P+1]
+};
+
+struct picasso_ctx {
+    int32_t rank = 0, world = 1;
+    MultiState mp;
+    picasso_ctx_opts opts{};
+    int32_t F = 0, T = 0, P = 0;
+    std::vector<int32_t> f2t, t2p, tdim, pack_dim;
+    std::vector<int64_t> tbase, trows, fcol, pack_rows, pack_key_off;
+    std::vector<uint64_t> tsalt;
+    int64_t out_width = 0;
+    std::vector<int32_t> pm_fields, pack_first_k;
+    // workspace layout
+    size_t ws_bytes = 0;
+    uint32_t cap = 0;
+    bool bound = false;
+    FieldInfo *finfo = nullptr;
+    int32_t *pm_fields_d = nullptr, *pack_first_k_d = nullptr;
+    int64_t *pack_key_off_d = nullptr;
+    int32_t *id_start = nullptr, *gstart_pm = nullptr, *field_gstart = nullptr, *pack_gstart = nullptr;
+    int32_t *pack_ustart = nullptr;
+    Slot *table = nullptr;
+    int32_t *slot_of = nullptr, *seg_of = nullptr, *inverse = nullptr;
+    int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
+    int *err = nullptr;
+    unsigned long long *unique_gkey = nullptr;
+    int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
+    int32_t *hist0 = nullptr, *hist1 = nullptr, *rowtot = nullptr;
+    SortPlan splan{};
+    int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr, *chunk_row = nullptr;
+    dbl4 *partial = nullptr;
+    float *gbuf = nullptr;
+    int64_t *pack_gbase = nullptr;
+    int32_t *pack_dim_d = nullptr;
+    bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
+    std::vector<float *> w, s1, s2;
+    // step state
+    bool fwd_done = false;
+    int32_t B = 0;
+    int64_t N = 0;
+    const int32_t *offsets = nullptr;
+    cudaStream_t last_stream = nullptr;
+    int num_sms = 148;
+    int64_t launches_fwd = 0, launches_bwd = 0;
+    std::string last_msg;
+    // phase profiling (events on the caller's stream)
+    // 0 unique(+partition) 1 pool 2 transpose 3 segsum(+update at W=1) 4 owner dedup+gather 5 owner update
+    static constexpr int kPhases = 6;
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
+    size_t ev_used[kPhases] = {0, 0, 0, 0, 0, 0};
+    int64_t prof_calls = 0;
+
+    void mark(int ph, bool begin, cudaStream_t s) {
+        if (!prof) return;
+        auto &v = ev[ph];
+        if (begin) {
+            if (ev_used[ph] == v.size()) {
+                cudaEvent_t a, b;
+                cudaEventCreate(&a);
+                cudaEventCreate(&b);
+                v.emplace_back(a, b);
+            }
+            cudaEventRecord(v[ev_used[ph]].first, s);
+        } else {
+            cudaEventRecord(v[ev_used[ph]].second, s);
+            ++ev_used[ph];
+        }
+    }
+    ~picasso_ctx() {
+        for (auto &v : ev)
+            for (auto &p : v) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
+    }
+
+    int32_t *osort_hist = nullptr;  // k_inverse's pass-0 histogram output when run on the owner stream
+
+    size_t carve(char *base) {
+        Carver c{base};
+        const int64_t N = std::max<int64_t>(opts.max_ids, 1);
+        const int64_t NR = std::max<int64_t>(N, mp.max_recv);  // index work of both stream kinds
+        const int64_t nblk = (NR + kTile - 1) / kTile + 1;
+        finfo = c.take<FieldInfo>(F);
+        pm_fields_d = c.take<int32_t>(F);
+        pack_first_k_d = c.take<int32_t>(P + 1);
+        pack_key_off_d = c.take<int64_t>(P + 1);
+        id_start = c.take<int32_t>(F);
+        gstart_pm = c.take<int32_t>(F + 1);
+        field_gstart = c.take<int32_t>(F);
+        pack_gstart = c.take<int32_t>(P + 1);
+        pack_ustart = c.take<int32_t>(P + 1);
+        table = c.take<Slot>(cap);
+        slot_of = c.take<int32_t>(N);
+        seg_of = c.take<int32_t>(N);
+        inverse = c.take<int32_t>(N);
+        blk_cnt = c.take<int32_t>(nblk);
+        blk_off = c.take<int32_t>(nblk);
+        d_total = c.take<int32_t>(1);
+        long_cnt = c.take<int32_t>(P);
+        err = c.take<int>(1);
+        unique_gkey = c.take<unsigned long long>(N);
+        k_a = c.take<int32_t>(N);
+        v_a = c.take<int32_t>(N);
+        k_b = c.take<int32_t>(N);
+        v_b = c.take<int32_t>(N);
+        hist0 = c.take<int32_t>(radix_hist2_ints(N));
+        hist1 = c.take<int32_t>(radix_hist2_ints(N));
+        rowtot = c.take<int32_t>(kMaxRadix);
+        ustart = c.take<int32_t>(N + 1);
+        long_list = c.take<int32_t>(N / (kLongRow + 1) + 2);
+        chunk_off = c.take<int32_t>(N / (kLongRow + 1) + 3);
+        int maxD = 4;
+        for (int32_t d : pack_dim) maxD = std::max(maxD, d);
+        partial = reinterpret_cast<dbl4 *>(c.take<double>(long_partial_doubles(N, maxD)));
+        chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
+        pack_gbase = c.take<int64_t>(P + 1);
+        pack_dim_d = c.take<int32_t>(P);
+        gbuf = (split_bwd || world > 1) ? c.take<float>((size_t)N * maxD) : nullptr;
+        if (world > 1) {
+            const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
+            const int WP = world * P;
+            int bb = 1;
+            while ((1 << bb) < WP) ++bb;
+            mp.bkey = c.take<int32_t>(N);
+            mp.bval = c.take<int32_t>(N);
+            mp.bsorted = c.take<int32_t>(N);
+            mp.send_uid = c.take<int32_t>(N);
+            mp.bhist = c.take<int32_t>((size_t)(1 << bb) * ((N + kTile - 1) / kTile) + 1);
+            mp.bcount = c.take<int32_t>(kMaxRadix);
+            mp.bstart = c.take<int64_t>(WP + 1);
+            mp.sroff = c.take<int64_t>(WP + 1);
+            mp.send_pos = c.take<int32_t>(N);
+            mp.send_keys = c.take<int32_t>(N);
+            mp.row_off = c.take<int64_t>(N);
+            mp.cnt_recv_d = c.take<int32_t>(WP);
+            mp.recv_keys = c.take<int32_t>(RM);
+            mp.opos_map = c.take<int32_t>(RM);
+            mp.oslot = c.take<int32_t>(RM);
+            mp.oinv = c.take<int32_t>(RM);
+            mp.ouid_key = c.take<unsigned long long>(RM);
+            mp.opack_gstart = c.take<int32_t>(P + 1);
+            mp.opack_ustart = c.take<int32_t>(P + 1);
+            mp.od_total = c.take<int32_t>(1);
+            mp.opack_ostart_d = c.take<int64_t>(P + 1);
+            mp.ogbase_scratch = c.take<int64_t>(P + 1);
+            mp.oblk_d = c.take<OwnerBlock>(WP);
+            mp.contrib = c.take<int32_t>((size_t)RM * world);
+            mp.rsend_off = c.take<int64_t>(RM);
+            mp.rows_send = c.take<float>((size_t)RM * maxD);
+            osort_hist = c.take<int32_t>(2 * ((RM + kTile - 1) / kTile) + 2);
+        }
+        return c.off + kAlign;
+    }
+};
+

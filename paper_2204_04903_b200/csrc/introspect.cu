@@ -1,0 +1,31 @@
+// introspect.cu — test-facing getters of the multi-GPU intermediates (synchronising).
+#include "ctx.h"
+
+extern "C" picasso_status picasso_get_owner_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap,
+                                                   int64_t *n) {
+    if (!ctx || !n || pack < 0 || pack >= ctx->P || !ctx->bound || ctx->world < 2) return PICASSO_ERR_INVALID_ARG;
+    if (cudaStreamSynchronize(ctx->last_stream) != cudaSuccess) return PICASSO_ERR_CUDA;
+    std::vector<int32_t> us(ctx->P + 1);
+    if (cudaMemcpy(us.data(), ctx->mp.opack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return PICASSO_ERR_CUDA;
+    const int64_t U = us[pack + 1] - us[pack];
+    *n = U;
+    if (dst && cap > 0 && U > 0) {
+        std::vector<unsigned long long> g(U);
+        if (cudaMemcpy(g.data(), ctx->mp.ouid_key + us[pack], sizeof(unsigned long long) * U, cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+            return PICASSO_ERR_CUDA;
+        std::vector<int64_t> k(U);
+        for (int64_t i = 0; i < U; ++i) k[i] = (int64_t)(g[i] - (unsigned long long)ctx->pack_key_off[pack]);
+        if (cudaMemcpy(dst, k.data(), sizeof(int64_t) * std::min(U, cap), cudaMemcpyHostToDevice) != cudaSuccess)
+            return PICASSO_ERR_CUDA;
+    }
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts) {
+    if (!ctx || !host_counts || ctx->world < 2 || ctx->mp.sk.empty()) return PICASSO_ERR_INVALID_ARG;
+    for (int r = 0; r < ctx->world; ++r) host_counts[r] = ctx->mp.sk[r];
+    return PICASSO_OK;
+}

@@ -129,7 +129,10 @@ __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
                     fi.base = st.base[w][c];
                     fi.rows = st.rows[w][c];
                     fi.salt = st.salt[w][c];
-                    myrow[p] = fi.base + row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
+                    // float offset of the row: the local table (W = 1), or the row received for
+                    // the position's unique key (W > 1: the stitched Shuffle output)
+                    myrow[p] = a.row_off ? a.row_off[__ldg(a.inverse + j + st.gb[w][c])]
+                                         : (fi.base + row_of(a.id_mode, __ldg(a.ids + j), fi, a.err)) * D;
                     myseg[p] = c;
                     a.seg_of[j + st.gb[w][c]] = st.sg[w][c];
                 }
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
                     sk[k] = __shfl_sync(gmask, myseg[slot], src, LANES);
                     if (k0 + k < nround) {
 #pragma unroll
-                        for (int qq = 0; qq < VPL; ++qq) v[k][qq] = ldg_f4(wb + r * D + qq * LANES * 4);
+                        for (int qq = 0; qq < VPL; ++qq) v[k][qq] = ldg_f4(wb + r + qq * LANES * 4);
                     }
                 }
 #pragma unroll

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter2(const int32_t *kin, c
                                                            int32_t *vout, int64_t n, int shift, int bits,
                                                            const int32_t *hist_off, const int32_t *rowtot,
                                                            int64_t nblk, int32_t *hist_next, int next_shift,
-                                                           int next_bits) {
+                                                           int next_bits, const int32_t *n_dev) {
+    if (n_dev) n = *n_dev;  // device-side element count (tiles past it are empty)
     constexpr int kWarps = kTileThreads / 32;
     constexpr int kRounds = kTile / kTileThreads;  // 8 rounds of 32 keys per warp
     __shared__ int32_t wc[kWarps][kMaxRadix];
@@ -168,13 +169,26 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
         k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
                                                           plan.bits[p], hist[p & 1], rowtot, nblk,
                                                           more ? hist[(p + 1) & 1] : nullptr,
-                                                          more ? plan.shift[p + 1] : 0, more ? plan.bits[p + 1] : 0);
+                                                          more ? plan.shift[p + 1] : 0, more ? plan.bits[p + 1] : 0,
+                                                          nullptr);
         *launches += 2;
         ck = bufk[p & 1];
         cv = bufv[p & 1];
     }
     *k_out = const_cast<int32_t *>(ck);
     *v_out = const_cast<int32_t *>(cv);
+}
+
+// One stable pass by a small key (the multi-GPU partition by (owner, pack)); bhist was filled
+// by k_bucket; rowtot receives the bucket counts.
+void bucket_sort_pass(const int32_t *k_in, const int32_t *v_in, int32_t *k_out, int32_t *v_out, int64_t n_max,
+                      const int32_t *n_dev, int bits, int32_t *bhist, int32_t *rowtot, cudaStream_t s) {
+    const int64_t nblk = (n_max + kTile - 1) / kTile;
+    if (nblk == 0) return;
+    const int radix = 1 << bits;
+    k_scan_rows<<<(radix + 7) / 8, 256, 0, s>>>(bhist, nblk, rowtot, nullptr, radix, 0);
+    k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(k_in, v_in, k_out, v_out, n_max, 0, bits, bhist, rowtot, nblk,
+                                                      nullptr, 0, 0, n_dev);
 }
 
 }  // namespace picasso

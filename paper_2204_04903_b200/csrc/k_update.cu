@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256) k_segsum(UpdateArgs a) {
             int cur = c_lo;
             auto finish = [&](int c) {  // rows deferred to the chunked path write nothing here
                 if (cum[c - c_lo + 1] > cum[c - c_lo]) {
-                    float *o = gp + (int64_t)(t0 + c - u0) * D + li * 4;
+                    float *o = (a.row_off ? a.gbuf + a.row_off[t0 + c] : gp + (int64_t)(t0 + c - u0) * D) + li * 4;
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) *reinterpret_cast<float4 *>(o + q * LANES * 4) = round4(g[q]);
                 }
@@ -651,7 +651,8 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
                     for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], pv[k][q]);
         }
         if (a.gbuf) {  // split backward: the update kernel applies the optimizer
-            float *o = a.gbuf + a.pack_gbase[a.pack] + (int64_t)(u - a.pack_ustart[a.pack]) * D + li * 4;
+            float *o = (a.row_off ? a.gbuf + a.row_off[u]
+                                  : a.gbuf + a.pack_gbase[a.pack] + (int64_t)(u - a.pack_ustart[a.pack]) * D) + li * 4;
 #pragma unroll
             for (int q = 0; q < VPL; ++q) *reinterpret_cast<float4 *>(o + q * LANES * 4) = round4(g[q]);
         } else {

@@ -58,6 +58,8 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
                        int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
                        int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches);
 size_t radix_hist2_ints(int64_t n);
+void bucket_sort_pass(const int32_t *k_in, const int32_t *v_in, int32_t *k_out, int32_t *v_out, int64_t n_max,
+                      const int32_t *n_dev, int bits, int32_t *bhist, int32_t *rowtot, cudaStream_t s);
 
 // k_index.cu
 void launch_field_prep(const IndexArgs &a, cudaStream_t s);
@@ -85,6 +87,8 @@ struct PoolArgs {
     const int32_t *field_gstart; // [F] packed-stream start of each field
     const int32_t *id_start;     // [F] offsets[f*B]
     int32_t *seg_of;             // [N] out: global segment f*B+b of each packed position
+    const int64_t *row_off;      // W > 1: [U] float offset of each unique row in `weight` (the
+    const int32_t *inverse;      //        received rows); inverse [N] maps positions to uids
     int32_t id_mode, pool_mean;
     const float *weight;        // [rows, D]
     float *out;
@@ -117,6 +121,7 @@ struct UpdateArgs {
     int32_t *chunk_row;          // [chunks] deferred-row index of each chunk
     dbl4 *partial;               // [chunks, D/4] fp64 chunk partial sums
     float *gbuf;                 // split backward: G rows of all packs (nullptr: fused)
+    const int64_t *row_off;      // W > 1: [U] float offset of each unique row's G in gbuf
     const int64_t *pack_gbase;   // [P+1] float offset of each pack's G rows in gbuf
 };
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);

@@ -7,157 +7,7 @@
 #include <string>
 #include <vector>
 
-#include "kernels.h"
-#include "picasso.h"
-
-using namespace picasso;
-
-namespace {
-
-constexpr size_t kAlign = 256;
-
-struct Carver {
-    char *base;
-    size_t off = 0;
-    template <typename T>
-    T *take(size_t n) {
-        off = (off + kAlign - 1) / kAlign * kAlign;
-        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
-        off += n * sizeof(T);
-        return p;
-    }
-};
-
-uint32_t pow2_at_least(uint64_t x) {
-    uint64_t p = 1024;
-    while (p < x) p <<= 1;
-    return (uint32_t)p;
-}
-
-int bits_for(int64_t maxval) {
-    int b = 1;
-    while (b < 31 && ((int64_t)1 << b) <= maxval) ++b;
-    return b;
-}
-
-}  // namespace
-
-struct picasso_ctx {
-    int32_t rank = 0, world = 1;
-    picasso_ctx_opts opts{};
-    int32_t F = 0, T = 0, P = 0;
-    std::vector<int32_t> f2t, t2p, tdim, pack_dim;
-    std::vector<int64_t> tbase, trows, fcol, pack_rows, pack_key_off;
-    std::vector<uint64_t> tsalt;
-    int64_t out_width = 0;
-    std::vector<int32_t> pm_fields, pack_first_k;
-    // workspace layout
-    size_t ws_bytes = 0;
-    uint32_t cap = 0;
-    bool bound = false;
-    FieldInfo *finfo = nullptr;
-    int32_t *pm_fields_d = nullptr, *pack_first_k_d = nullptr;
-    int64_t *pack_key_off_d = nullptr;
-    int32_t *id_start = nullptr, *gstart_pm = nullptr, *field_gstart = nullptr, *pack_gstart = nullptr;
-    int32_t *pack_ustart = nullptr;
-    Slot *table = nullptr;
-    int32_t *slot_of = nullptr, *seg_of = nullptr, *inverse = nullptr;
-    int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
-    int *err = nullptr;
-    unsigned long long *unique_gkey = nullptr;
-    int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
-    int32_t *hist0 = nullptr, *hist1 = nullptr, *rowtot = nullptr;
-    SortPlan splan{};
-    int32_t *ustart = nullptr, *long_list = nullptr, *chunk_off = nullptr, *chunk_row = nullptr;
-    dbl4 *partial = nullptr;
-    float *gbuf = nullptr;
-    int64_t *pack_gbase = nullptr;
-    int32_t *pack_dim_d = nullptr;
-    bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
-    std::vector<float *> w, s1, s2;
-    // step state
-    bool fwd_done = false;
-    int32_t B = 0;
-    int64_t N = 0;
-    const int32_t *offsets = nullptr;
-    cudaStream_t last_stream = nullptr;
-    int num_sms = 148;
-    int64_t launches_fwd = 0, launches_bwd = 0;
-    std::string last_msg;
-    // phase profiling (events on the caller's stream)
-    static constexpr int kPhases = 4;
-    bool prof = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
-    size_t ev_used[kPhases] = {0, 0, 0, 0};
-    int64_t prof_calls = 0;
-
-    void mark(int ph, bool begin, cudaStream_t s) {
-        if (!prof) return;
-        auto &v = ev[ph];
-        if (begin) {
-            if (ev_used[ph] == v.size()) {
-                cudaEvent_t a, b;
-                cudaEventCreate(&a);
-                cudaEventCreate(&b);
-                v.emplace_back(a, b);
-            }
-            cudaEventRecord(v[ev_used[ph]].first, s);
-        } else {
-            cudaEventRecord(v[ev_used[ph]].second, s);
-            ++ev_used[ph];
-        }
-    }
-    ~picasso_ctx() {
-        for (auto &v : ev)
-            for (auto &p : v) {
-                cudaEventDestroy(p.first);
-                cudaEventDestroy(p.second);
-            }
-    }
-
-    size_t carve(char *base) {
-        Carver c{base};
-        const int64_t N = std::max<int64_t>(opts.max_ids, 1);
-        const int64_t nblk = (N + kTile - 1) / kTile + 1;
-        finfo = c.take<FieldInfo>(F);
-        pm_fields_d = c.take<int32_t>(F);
-        pack_first_k_d = c.take<int32_t>(P + 1);
-        pack_key_off_d = c.take<int64_t>(P + 1);
-        id_start = c.take<int32_t>(F);
-        gstart_pm = c.take<int32_t>(F + 1);
-        field_gstart = c.take<int32_t>(F);
-        pack_gstart = c.take<int32_t>(P + 1);
-        pack_ustart = c.take<int32_t>(P + 1);
-        table = c.take<Slot>(cap);
-        slot_of = c.take<int32_t>(N);
-        seg_of = c.take<int32_t>(N);
-        inverse = c.take<int32_t>(N);
-        blk_cnt = c.take<int32_t>(nblk);
-        blk_off = c.take<int32_t>(nblk);
-        d_total = c.take<int32_t>(1);
-        long_cnt = c.take<int32_t>(P);
-        err = c.take<int>(1);
-        unique_gkey = c.take<unsigned long long>(N);
-        k_a = c.take<int32_t>(N);
-        v_a = c.take<int32_t>(N);
-        k_b = c.take<int32_t>(N);
-        v_b = c.take<int32_t>(N);
-        hist0 = c.take<int32_t>(radix_hist2_ints(N));
-        hist1 = c.take<int32_t>(radix_hist2_ints(N));
-        rowtot = c.take<int32_t>(kMaxRadix);
-        ustart = c.take<int32_t>(N + 1);
-        long_list = c.take<int32_t>(N / (kLongRow + 1) + 2);
-        chunk_off = c.take<int32_t>(N / (kLongRow + 1) + 3);
-        int maxD = 4;
-        for (int32_t d : pack_dim) maxD = std::max(maxD, d);
-        partial = reinterpret_cast<dbl4 *>(c.take<double>(long_partial_doubles(N, maxD)));
-        chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
-        pack_gbase = c.take<int64_t>(P + 1);
-        pack_dim_d = c.take<int32_t>(P);
-        gbuf = split_bwd ? c.take<float>((size_t)N * maxD) : nullptr;
-        return c.off + kAlign;
-    }
-};
+#include "ctx.h"
 
 #define CK(x)                                                             \
     do {                                                                  \
@@ -172,16 +22,35 @@ static bool dim_ok(int32_t d) {
     return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 384 || d == 512;
 }
 
+extern "C" picasso_status picasso_nccl_unique_id(uint8_t *out) {
+    if (!out) return PICASSO_ERR_INVALID_ARG;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return PICASSO_ERR_NCCL;
+    std::memcpy(out, &id, 128);
+    return PICASSO_OK;
+}
+
 extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int32_t rank, int32_t world,
-                                             const picasso_ctx_opts *opts, picasso_ctx **out) {
+                                             const uint8_t *nccl_uid, const picasso_ctx_opts *opts,
+                                             picasso_ctx **out) {
     if (!plan || !opts || !out || plan->n_fields <= 0 || plan->n_tables <= 0 || plan->n_packs <= 0)
         return PICASSO_ERR_INVALID_ARG;
-    if (world != 1 || rank != 0) return PICASSO_ERR_INVALID_ARG;  // this build: single rank
+    if (world < 1 || world > 8 || rank < 0 || rank >= world) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_batch <= 0 || opts->max_ids < 0 || opts->max_ids >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
+    if (opts->max_recv < 0 || opts->max_recv >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
     if (opts->pool < 0 || opts->pool > 1 || opts->id_mode < 0 || opts->id_mode > 1 || opts->opt < 0 || opts->opt > 1)
         return PICASSO_ERR_INVALID_ARG;
     if ((int64_t)plan->n_fields * opts->max_batch >= ((int64_t)1 << 31)) return PICASSO_ERR_INVALID_ARG;
+    if ((int64_t)world * plan->n_packs > kMaxOwnerBlocks) return PICASSO_ERR_INVALID_ARG;
     auto *c = new picasso_ctx();
+    if (world > 1) {
+        c->mp.max_recv = opts->max_recv > 0 ? opts->max_recv : std::max<int64_t>(2 * opts->max_ids, 1024);
+        if (nccl_uid) {
+            std::memcpy(c->mp.uid, nccl_uid, 128);
+            c->mp.has_uid = true;
+        }
+    }
     c->rank = rank;
     c->world = world;
     c->opts = *opts;
@@ -227,7 +96,14 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
             if (c->t2p[c->f2t[f]] == p) c->pm_fields.push_back(f);
     }
     c->pack_first_k[c->P] = c->F;
-    c->cap = pow2_at_least((uint64_t)std::max<int64_t>(opts->max_ids, 1) * 2);
+    c->cap = pow2_at_least((uint64_t)std::max<int64_t>(std::max<int64_t>(opts->max_ids, c->mp.max_recv), 1) * 2);
+    if (world > 1) {  // local rows must fit int32 (received keys are int32 local rows)
+        for (int32_t p = 0; p < c->P; ++p)
+            if (c->pack_rows[p] / world >= ((int64_t)1 << 31)) {
+                delete c;
+                return PICASSO_ERR_PLAN_MISMATCH;
+            }
+    }
     if (const char *e = std::getenv("PICASSO_BWD")) c->split_bwd = std::strcmp(e, "fused") != 0;
     c->ws_bytes = c->carve(nullptr);
     int dev = 0;
@@ -286,17 +162,55 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_dim_d, ctx->pack_dim.data(), sizeof(int32_t) * ctx->P, cudaMemcpyHostToDevice));
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
+    if (ctx->world > 1 && !ctx->mp.cnt_send_h) {
+        const int WP = ctx->world * ctx->P;
+        CK(cudaMallocHost(&ctx->mp.cnt_send_h, sizeof(int32_t) * WP));
+        CK(cudaMallocHost(&ctx->mp.cnt_recv_h, sizeof(int32_t) * WP));
+        CK(cudaMallocHost(&ctx->mp.oblk_h, sizeof(OwnerBlock) * WP));
+        CK(cudaMallocHost(&ctx->mp.ostart_h, sizeof(int64_t) * (ctx->P + 1)));
+        CK(cudaMallocHost(&ctx->mp.og_h, sizeof(int32_t) * (ctx->P + 1)));
+    }
+    if (ctx->world > 1 && ctx->mp.has_uid && !ctx->mp.comm) {  // one rank per process: NCCL
+        ncclUniqueId id;
+        std::memcpy(&id, ctx->mp.uid, 128);
+        if (ncclCommInitRank(&ctx->mp.comm, ctx->world, id, ctx->rank) != ncclSuccess) {
+            ctx->last_msg = "ncclCommInitRank failed";
+            return PICASSO_ERR_NCCL;
+        }
+    }
     ctx->bound = true;
     ctx->fwd_done = false;
     return PICASSO_OK;
 }
 
 extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
+    if (!ctx) return PICASSO_OK;
+    if (ctx->mp.comm) ncclCommDestroy(ctx->mp.comm);
+    if (ctx->mp.cnt_send_h) {
+        cudaFreeHost(ctx->mp.cnt_send_h);
+        cudaFreeHost(ctx->mp.cnt_recv_h);
+        cudaFreeHost(ctx->mp.oblk_h);
+        cudaFreeHost(ctx->mp.ostart_h);
+        cudaFreeHost(ctx->mp.og_h);
+    }
     delete ctx;
     return PICASSO_OK;
 }
 
+namespace picasso {
+IndexArgs make_index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N);
+UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, const int32_t *su,
+                            const int32_t *sseg);
+}
+picasso_status multi_fwd_nccl(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
+                              float *out, cudaStream_t s);
+picasso_status multi_bwd_nccl(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
+
 static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N) {
+    return picasso::make_index_args(ctx, ids, offsets, B, N);
+}
+
+IndexArgs picasso::make_index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N) {
     IndexArgs a{};
     a.ids = ids;
     a.offsets = offsets;
@@ -339,6 +253,10 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     if (batch > ctx->opts.max_batch || n_ids > ctx->opts.max_ids) return PICASSO_ERR_CAPACITY;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ctx->launches_fwd = 0;
+    if (ctx->world > 1) {
+        if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_fwd
+        return multi_fwd_nccl(ctx, ids, offsets, batch, n_ids, out, s);
+    }
     IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
     const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
     a.cap_mask = cap_step - 1;
@@ -386,6 +304,10 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     if (!ctx->bound || !ctx->fwd_done) return PICASSO_ERR_STATE;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ctx->launches_bwd = 0;
+    if (ctx->world > 1) {
+        if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_bwd_update
+        return multi_bwd_nccl(ctx, grad_out, lr, step, s);
+    }
     const int64_t N = ctx->N;
     int32_t *su = nullptr, *sseg = nullptr;
     ctx->mark(2, true, s);
@@ -395,6 +317,35 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     ctx->mark(2, false, s);
     ctx->launches_bwd += N > 0 ? 1 : 0;
     ctx->mark(3, true, s);
+    UpdateArgs u = picasso::make_update_args(ctx, grad_out, lr, step, su, sseg);
+    if (N > 0) {
+        for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
+            u.pack = p;
+            u.long_cnt = ctx->long_cnt + p;
+            u.pack_key_off = ctx->pack_key_off[p];
+            u.weight = ctx->w[p];
+            u.state1 = ctx->s1[p];
+            u.state2 = ctx->s2[p];
+            if (ctx->split_bwd) {
+                launch_segsum(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->launches_bwd += 2 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+                launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
+            } else {
+                launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+            }
+        }
+    }
+    ctx->mark(3, false, s);
+    if (ctx->prof) ++ctx->prof_calls;
+    CK(cudaGetLastError());
+    ctx->fwd_done = false;
+    ctx->last_stream = s;
+    return PICASSO_OK;
+}
+
+UpdateArgs picasso::make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step,
+                                     const int32_t *su, const int32_t *sseg) {
     UpdateArgs u{};
     u.sorted_u = su;
     u.sorted_seg = sseg;
@@ -423,30 +374,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     u.chunk_row = ctx->chunk_row;
     u.gbuf = ctx->split_bwd ? ctx->gbuf : nullptr;
     u.pack_gbase = ctx->pack_gbase;
-    if (N > 0) {
-        for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
-            u.pack = p;
-            u.long_cnt = ctx->long_cnt + p;
-            u.pack_key_off = ctx->pack_key_off[p];
-            u.weight = ctx->w[p];
-            u.state1 = ctx->s1[p];
-            u.state2 = ctx->s2[p];
-            if (ctx->split_bwd) {
-                launch_segsum(ctx->pack_dim[p], u, ctx->num_sms, s);
-                ctx->launches_bwd += 2 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-                launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
-            } else {
-                launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-                ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-            }
-        }
-    }
-    ctx->mark(3, false, s);
-    if (ctx->prof) ++ctx->prof_calls;
-    CK(cudaGetLastError());
-    ctx->fwd_done = false;
-    ctx->last_stream = s;
-    return PICASSO_OK;
+    return u;
 }
 
 extern "C" picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t len) {

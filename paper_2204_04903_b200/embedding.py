@@ -19,7 +19,7 @@ class PackedEmbedding:
     def __init__(self, field_to_table, table_rows, table_dim, *, max_batch, max_ids, table_salt=None,
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
-                 init_acc=0.1):
+                 init_acc=0.1, nccl_uid=None, max_recv=0):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -34,7 +34,7 @@ class PackedEmbedding:
         self.device = torch.device(device)
         self.ctx = abi.picasso_ctx_create(self.plan, self.f2t, self.rows, self.dims, table_salt, self.field_col,
                                           self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
-                                          eps, beta1, beta2)
+                                          eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv)
         P = self.plan["n_packs"]
         self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
         ws = abi.picasso_workspace_size(self.ctx)
@@ -89,10 +89,50 @@ class PackedEmbedding:
     def launch_count(self):
         return abi.picasso_launch_count(self.ctx)
 
+    def owner_unique(self, pack):
+        return abi.picasso_get_owner_unique(self.ctx, pack, self.device)
+
+    def send_counts(self):
+        return abi.picasso_get_send_counts(self.ctx, self.world)
+
     def close(self):
         if self.ctx:
             abi.picasso_ctx_destroy(self.ctx)
             self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LoopbackGroup:
+    """W ranks of the row-sharded layer in ONE process on one device (nccl_uid = None): the
+    exchanges of the step are device copies between the ranks' buffers.  Used to test the
+    sharded path at W up to 8 with a single GPU; the arithmetic is the same kernels as NCCL mode."""
+
+    def __init__(self, world, field_to_table, table_rows, table_dim, **kw):
+        self.world = world
+        self.ranks = [PackedEmbedding(field_to_table, table_rows, table_dim, rank=r, world=world, **kw)
+                      for r in range(world)]
+        self.group = abi.picasso_group_create([e.ctx for e in self.ranks])
+
+    def forward(self, ids, offsets, batch, outs=None, stream=None):
+        if outs is None:
+            outs = [torch.empty(b, e.out_width, dtype=torch.float32, device=e.device) for b, e in zip(batch, self.ranks)]
+        abi.picasso_group_fwd(self.group, ids, offsets, batch, outs, stream)
+        return outs
+
+    def backward_update(self, grad_outs, lr, step, stream=None):
+        abi.picasso_group_bwd_update(self.group, grad_outs, lr, step, stream)
+
+    def close(self):
+        if self.group:
+            abi.picasso_group_destroy(self.group)
+            self.group = None
+        for e in self.ranks:
+            e.close()
 
     def __del__(self):
         try:

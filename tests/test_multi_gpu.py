@@ -1,0 +1,134 @@
+"""Row-sharded path (world W > 1) against the oracle, W = 2, 4, 8 ranks driven in one process on
+one GPU through the loopback group (the exchanges are device copies; every kernel is the one the
+NCCL path runs).  Checked per rank: forward bit-exact; unique keys, per-owner send counts and the
+owner-side unique rows (first occurrence over the received lists concatenated by source rank)
+bit-exact; after the backward, every rank's table shard equals the oracle's global-batch update
+(bit-exact under dyadic dY, 1e-5 / 1e-6 otherwise)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from datagen import configs as dc
+from datagen import init_pack_tables_torch, make_batch, make_dy
+from harness import assert_close, oracle_model, oracle_tables
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
+def make_group(cfg, W, opt=0, max_ids=None):
+    import paper_2204_04903_b200 as pb
+
+    mi = max_ids or cfg.batch * cfg.F * 60
+    g = pb.LoopbackGroup(W, cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=cfg.batch, max_ids=mi,
+                         table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
+                         opt=opt, max_recv=W * mi)
+    for r, e in enumerate(g.ranks):
+        init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights, rank=r,
+                               world=W)
+    torch.cuda.synchronize()
+    return g
+
+
+def shard_expected(e, cfg, tabs, which, W, r):
+    """Expected contents of rank r's pack shards from per-table oracle arrays."""
+    out = []
+    tb, t2p = e.plan["table_base"], e.plan["table_to_pack"]
+    for p in range(e.n_packs):
+        tabs_p = np.nonzero(t2p == p)[0]
+        tabs_p = tabs_p[np.argsort(tb[tabs_p], kind="stable")]
+        bases = tb[tabs_p]
+        lr = np.arange(e.local_rows[p])
+        key = lr * W + r
+        ti = np.searchsorted(bases, key, side="right") - 1
+        D = int(e.plan["pack_dim"][p])
+        exp = np.zeros((len(lr), D), np.float32)
+        for k, t in enumerate(tabs_p):
+            sel = ti == k
+            exp[sel] = tabs[t][key[sel] - bases[k]]
+        out.append(exp)
+    return out
+
+
+def run(cfg, W, steps=1, opt=0, dyadic=True, lr=0.05):
+    g = make_group(cfg, W, opt)
+    m = oracle_model(cfg)
+    tabs = oracle_tables(cfg)
+    if opt == 0:
+        s1, s2 = [np.full_like(t, 0.1) for t in tabs], None
+    else:
+        s1, s2 = [np.zeros_like(t) for t in tabs], [np.zeros_like(t) for t in tabs]
+    e0 = g.ranks[0]
+    for step in range(1, steps + 1):
+        bs = [make_batch(cfg, r, step) for r in range(W)]
+        dys = [make_dy(cfg, r, step, dyadic=dyadic) for r in range(W)]
+        ids = [torch.from_numpy(b.ids).cuda() for b in bs]
+        offs = [torch.from_numpy(b.offsets).cuda() for b in bs]
+        outs = g.forward(ids, offs, [cfg.batch] * W)
+        obs = [oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy) for b, dy in zip(bs, dys)]
+        for r in range(W):
+            ref = oracle.forward(m, obs[r], tabs, cfg.out_width)
+            assert np.array_equal(outs[r].cpu().numpy(), ref), f"forward rank {r} step {step}"
+        if step == 1:  # intermediates: unique, partition, owner unique
+            plan = e0.plan
+            recv = {}  # (owner, pack) -> list of per-source local-row lists
+            for r in range(W):
+                sent = np.zeros(W, np.int64)
+                for p in range(e0.n_packs):
+                    keys = oracle.pack_key_stream(m, plan["field_to_pack"], plan["table_base"], obs[r], p)
+                    u_ref, _ = oracle.unique(keys)
+                    assert np.array_equal(g.ranks[r].unique(p).cpu().numpy(), u_ref), f"unique r{r} p{p}"
+                    pk, plr, cnt = oracle.partition(u_ref, W)
+                    sent += cnt
+                    s = 0
+                    for o in range(W):
+                        recv.setdefault((o, p), []).append(plr[s:s + cnt[o]])
+                        s += cnt[o]
+                assert g.ranks[r].send_counts() == sent.tolist(), f"send counts r{r}"
+            for (o, p), lists in recv.items():
+                ou_ref, _ = oracle.unique(np.concatenate(lists) if lists else np.zeros(0, np.int64))
+                assert np.array_equal(g.ranks[o].owner_unique(p).cpu().numpy(), ou_ref), f"owner unique o{o} p{p}"
+        g.backward_update([torch.from_numpy(d).cuda() for d in dys], lr=lr, step=step)
+        for e in g.ranks:
+            e.check()
+        oracle.backward_update(m, obs, tabs, s1, s2, kind=opt, lr=lr, step=step)
+        for r, e in enumerate(g.ranks):
+            for p, exp in enumerate(shard_expected(e, cfg, tabs, "w", W, r)):
+                got = e.weights[p][:len(exp)].cpu().numpy()
+                if dyadic and opt == 0:
+                    assert np.array_equal(got, exp), f"weights r{r} p{p} step {step}"
+                assert_close(got, exp, what=f"weights r{r} p{p} step {step}")
+            for p, exp in enumerate(shard_expected(e, cfg, s1, "s1", W, r)):
+                assert_close(e.state1[p][:len(exp)].cpu().numpy(), exp, what=f"state1 r{r} p{p}")
+    g.close()
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_toy_sharded(W):
+    run(dc.toy(), W, steps=2)
+
+
+@pytest.mark.parametrize("W", [2, 8])
+def test_multipack_sharded(W):
+    run(dc.scaled(dc.wdl(), batch=24, rows_div=2000), W, steps=1)
+
+
+def test_criteo_small_sharded_continuous_dy():
+    run(dc.scaled(dc.criteo(), batch=512, rows_div=1000), 4, steps=2, dyadic=False)
+
+
+def test_sharded_adam_mean():
+    run(dc.toy(pool=dc.POOL_MEAN), 4, steps=2, opt=1, dyadic=False, lr=0.01)
+
+
+def test_sharded_hot_rows():
+    cfg = dc.toy(batch=1024).replace(table_rows=np.array([3, 5, 2, 7, 1, 4, 6, 3], np.int64),
+                                     bags=[("uniform", 0, 8)] * 8)
+    run(cfg, 4, steps=1)
