@@ -175,18 +175,25 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------------
-def algorithmic_bytes(cfg, B, N, U_by_pack, plan):
-    """SURVEY.md §8(d) per-kernel algorithmic bytes (what the method must move), per step."""
+def algorithmic_bytes(cfg, B, N, U_by_pack, plan, world=1):
+    """Per-kernel algorithmic bytes per step (SURVEY.md §8(d) per-unit figures x
+    the units one launch processes): what each kernel must move, index scratch not credited.
+    N ids, S = F*B segments, U unique rows (per pack), Adagrad (1 state array)."""
     S = cfg.F * B
     fd = cfg.field_dim.astype(np.int64)
-    out_bytes = 4 * B * int(fd.sum())
-    rows_bytes = sum(4 * int(plan["pack_dim"][p]) * U_by_pack[p] for p in range(plan["n_packs"]))
-    pool = 8 * N + 4 * (S + 1) + rows_bytes + out_bytes
-    # segsum+update: dY rows (one read per segment), sorted segment list, ustart, unique keys,
-    # weight + Adagrad state read and written once per touched row
+    out_bytes = 4 * B * int(fd.sum())                      # pooled output / dY, [B, sum D]
+    rows_bytes = sum(4 * int(plan["pack_dim"][p]) * U_by_pack[p] for p in range(plan["n_packs"]))  # 4*D*U
     U = sum(U_by_pack)
-    upd = out_bytes + 4 * N + 4 * (U + 1) + 8 * U + 4 * rows_bytes
-    return {"pool": pool, "segsum_update": upd}
+    return {
+        # ids + offsets + distinct rows + pooled output
+        "pool": 8 * N + 4 * (S + 1) + rows_bytes + out_bytes,
+        # dY rows + sorted segment list + row bounds + G rows out
+        "segsum": out_bytes + 4 * N + 4 * (U + 1) + rows_bytes,
+        # G rows in + row keys + weight and accumulator read + written (W = 1: this rank's uniques)
+        "update": rows_bytes + 8 * U + 4 * rows_bytes if world == 1 else None,
+        # whole step, fused definition of SURVEY §8(d) (fwd + bwd + Adagrad)
+        "step": 8 * N + 4 * (S + 1) + 4 * N + 8 * U + rows_bytes + out_bytes + out_bytes + 4 * N + 4 * rows_bytes,
+    }
 
 
 def main():
@@ -214,12 +221,18 @@ def main():
     B = cfg.batch
     batches = [make_batch(cfg, rank, s) for s in range(args.nbatches)]
     max_ids = max(b.n_ids for b in batches)
-    # this build: each rank holds a full replica of the tables (the row-sharded NCCL path is
-    # the next row of SURVEY §8); every rank processes its own B samples (weak scaling)
+    # every rank processes its own B samples (weak scaling, data parallel over samples); at
+    # world > 1 the tables are row-sharded over the ranks (key mod W) and exchanged with NCCL
+    uid = None
+    if world > 1:
+        obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
     emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=B, max_ids=max_ids,
                              table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
-                             device=dev)
-    init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights)
+                             device=dev, rank=rank, world=world, nccl_uid=uid, max_recv=2 * max_ids)
+    init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights,
+                           rank=rank, world=world)
     dev_in = [(torch.from_numpy(b.ids).to(dev), torch.from_numpy(b.offsets).to(dev)) for b in batches]
     dys_host = [torch.from_numpy(make_dy(cfg, rank, s, dyadic=False)).pin_memory() for s in range(args.nbatches)]
     dys = [d.to(dev) for d in dys_host]
@@ -269,9 +282,12 @@ def main():
     U_pref = np.array(emb.unique_offsets_host(), np.int64)
     U_by_pack = [int(x) for x in np.diff(U_pref)]
     last_b = batches[(args.warmup + args.steps - 1) % args.nbatches]
-    alg = algorithmic_bytes(cfg, B, last_b.n_ids, U_by_pack, emb.plan)
+    alg = algorithmic_bytes(cfg, B, last_b.n_ids, U_by_pack, emb.plan, world)
+    alg = {k: v for k, v in alg.items() if v is not None}
     per_phase = {k: v / max(ncalls, 1) for k, v in phase_ms.items()}
-    dom = "segsum_update" if per_phase["segsum_update"] >= per_phase["pool"] else "pool"
+    per_phase = {k: v for k, v in per_phase.items() if v > 0}
+    cand = [k for k in ("pool", "segsum", "update") if k in per_phase and k in alg]
+    dom = max(cand, key=lambda k: per_phase[k])
     peak = None
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
@@ -332,18 +348,22 @@ def main():
             "config": {"workload": cfg.name, "global_batch": world * B, "batch_per_gpu": B, "fields": cfg.F,
                        "dims": sorted(set(cfg.table_dim.tolist())), "rows": int(cfg.table_rows.sum()),
                        "alpha": cfg.alpha, "optimizer": "adagrad", "pool": "sum",
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"dp{world}+rowshard{world}" if world > 1 else "single",
                        "l2": "flushed (256 MiB write, untimed) before every timed step",
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "note": "H2D of ids+offsets+dY from pinned host memory, D2H of the per-pack unique counts"},
             "gpu_launches": int((lf + lb) * args.steps),
-            "roofline": {"bound": "hbm", "kernel": "k_segsum_update" if dom == "segsum_update" else "k_pool",
+            "roofline": {"bound": "hbm", "kernel": {"pool": "k_pool", "segsum": "k_segsum (+ hot-row chunks)",
+                                                     "update": "k_update_rows"}[dom],
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
                          "peak_source": peak_src},
             "phases_ms": per_phase,
+            "outside_phases_ms": ms - sum(per_phase.values()),  # exchanges + host sync (W > 1), launch gaps
+            "step_algorithmic_bytes": alg["step"],
+            "step_roofline_frac": alg["step"] / (ms_max * 1e-3) / 1e9 / peak,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

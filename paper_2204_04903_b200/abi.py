@@ -22,7 +22,7 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_profile_enable", "picasso_profile_read", "picasso_unique_offsets", "picasso_nccl_unique_id",
            "picasso_group_create", "picasso_group_destroy", "picasso_group_fwd", "picasso_group_bwd_update",
            "picasso_get_owner_unique", "picasso_get_send_counts"]
-PHASES = ["unique", "pool", "transpose", "segsum_update", "owner_gather", "owner_update"]
+PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
 class PicassoError(RuntimeError):

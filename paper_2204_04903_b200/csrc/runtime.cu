@@ -329,7 +329,11 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
             if (ctx->split_bwd) {
                 launch_segsum(ctx->pack_dim[p], u, ctx->num_sms, s);
                 ctx->launches_bwd += 2 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->mark(3, false, s);
+                ctx->mark(5, true, s);
                 launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->mark(5, false, s);
+                ctx->mark(3, true, s);
             } else {
                 launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
                 ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);

@@ -1,0 +1,67 @@
+"""One rank of the NCCL row-sharded parity check (launched by tests/test_nccl_gpu.py under
+torchrun, one process per GPU).  Every rank regenerates all ranks' seeded batches, runs the
+oracle on the global batch itself, and checks its own outputs and table shard."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import oracle
+    import paper_2204_04903_b200 as pb
+    from datagen import configs as dc
+    from datagen import init_pack_tables_torch, make_batch, make_dy
+    from harness import assert_close, oracle_model, oracle_tables
+    from test_multi_gpu import shard_expected
+
+    name = sys.argv[1] if len(sys.argv) > 1 else "toy"
+    cfg = dc.toy() if name == "toy" else dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    mi = cfg.batch * cfg.F * 60
+    e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=cfg.batch, max_ids=mi,
+                           table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
+                           rank=rank, world=world, nccl_uid=obj[0], max_recv=world * mi,
+                           device=torch.device("cuda", local))
+    init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights, rank=rank,
+                           world=world)
+    m, tabs = oracle_model(cfg), oracle_tables(cfg)
+    acc = [np.full_like(t, 0.1) for t in tabs]
+    report = {"rank": rank, "world": world, "ok": False}
+    for step in (1, 2):
+        bs = [make_batch(cfg, r, step) for r in range(world)]
+        dys = [make_dy(cfg, r, step) for r in range(world)]
+        out = e.forward(torch.from_numpy(bs[rank].ids).cuda(), torch.from_numpy(bs[rank].offsets).cuda(), cfg.batch)
+        obs = [oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy) for b, dy in zip(bs, dys)]
+        ref = oracle.forward(m, obs[rank], tabs, cfg.out_width)
+        assert np.array_equal(out.cpu().numpy(), ref), f"forward step {step}"
+        e.backward_update(torch.from_numpy(dys[rank]).cuda(), lr=0.05, step=step)
+        e.check()
+        oracle.backward_update(m, obs, tabs, acc, lr=0.05, step=step)
+        for p, exp in enumerate(shard_expected(e, cfg, tabs, "w", world, rank)):
+            got = e.weights[p][:len(exp)].cpu().numpy()
+            assert np.array_equal(got, exp), f"weights p{p} step {step} (dyadic dY: exact)"
+        for p, exp in enumerate(shard_expected(e, cfg, acc, "s1", world, rank)):
+            assert_close(e.state1[p][:len(exp)].cpu().numpy(), exp, what=f"state p{p}")
+    report["ok"] = True
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"nccl_{name}_rank{rank}.json"), "w") as f:
+        json.dump(report, f)
+    e.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -75,7 +75,10 @@ def run(cfg, W, steps=1, opt=0, dyadic=True, lr=0.05):
         obs = [oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy) for b, dy in zip(bs, dys)]
         for r in range(W):
             ref = oracle.forward(m, obs[r], tabs, cfg.out_width)
-            assert np.array_equal(outs[r].cpu().numpy(), ref), f"forward rank {r} step {step}"
+            if step == 1 or (dyadic and opt == 0):  # identical tables: bit-exact by construction
+                assert np.array_equal(outs[r].cpu().numpy(), ref), f"forward rank {r} step {step}"
+            else:  # tables already differ by the fp32 partial rounding of earlier steps (O6)
+                assert_close(outs[r].cpu().numpy(), ref, what=f"forward rank {r} step {step}")
         if step == 1:  # intermediates: unique, partition, owner unique
             plan = e0.plan
             recv = {}  # (owner, pack) -> list of per-source local-row lists
