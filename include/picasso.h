@@ -99,6 +99,8 @@ typedef struct {
     float beta1, beta2;    /* Adam (0.9, 0.999) */
     int64_t max_recv;      /* world > 1: keys this rank may receive per step as an owner
                               (0 = 2 * max_ids); exceeding it fails the step with CAPACITY */
+    int64_t cache_max_bytes; /* world > 1: largest hot-storage capacity picasso_hot_cache_refresh
+                              will be asked for (0 = no HybridHash: no FCounter, no hot rows) */
 } picasso_ctx_opts;
 
 /* NCCL unique id (128 bytes, host) for picasso_ctx_create; rank 0 calls it and broadcasts
@@ -195,6 +197,36 @@ picasso_status picasso_unique_offsets(picasso_ctx *ctx, int32_t *dst, void *stre
  * The loopback group runs the same phases for all ranks of one process, with device copies
  * for the exchanges; its arguments are per-rank arrays of what fwd/bwd_update take. */
 typedef struct picasso_group picasso_group;
+
+/* 6. HybridHash hot storage (Alg. 1), world > 1 and cache_max_bytes > 0.
+ * FCounter counts every key once per rank-step in which it is in that rank's unique set
+ * (reading O11; owners count received keys, ranks count their hot hits).  The caller applies
+ * Alg. 1's schedule: after picasso_packed_lookup_bwd_update of iteration itr, call
+ * picasso_hot_cache_refresh when itr >= warmup_iters and itr % flush_iters == 0 (reading O13;
+ * the paper warms up 100 steps, L795).  The refresh writes the replicas back to the owners,
+ * selects the longest prefix of all keys sorted by (count desc, pack asc, key asc) whose rows
+ * (weights + optimizer state, 4*D*(1+n_state) bytes each) fit capacity_bytes (<= the ctx's
+ * cache_max_bytes), and replicates those rows on every rank.  From then on hot keys are served
+ * by the local replica, skip the AllToAllv, and their gradients are summed over the ranks
+ * (AllReduce) so every replica applies the same update.  Results equal the uncached step
+ * (tier transparency) up to the fp32 cross-rank sum of hot gradients.  capacity_bytes = 0:
+ * write back and drop (e.g. before a checkpoint).  world == 1: no-op (the table itself is the
+ * hot storage; reading O18).  Collective: every rank calls it (NCCL mode).  stats (host, may
+ * be NULL) describe the new hot set and the last forward's hit ratio over unique keys
+ * (P:L796). */
+typedef struct {
+    int64_t k;                /* hot rows */
+    int64_t bytes;            /* bytes of hot storage in use (weights + optimizer state) */
+    int64_t hot_uniques;      /* last forward: unique keys served by the replica ... */
+    int64_t uniques;          /* ... out of this many unique keys of the rank */
+    double hit_ratio_unique;  /* hot_uniques / uniques */
+} picasso_cache_stats;
+picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t capacity_bytes, void *stream,
+                                         picasso_cache_stats *stats);
+picasso_status picasso_group_hot_cache_refresh(picasso_group *group, size_t capacity_bytes, void *stream,
+                                               picasso_cache_stats *stats /* [world] or NULL */);
+/* Current hot keys (tests): pack and pack key of each hot slot, slot order (host arrays). */
+picasso_status picasso_get_hot_keys(picasso_ctx *ctx, int32_t *pack, int64_t *key, int64_t cap, int64_t *n);
 picasso_status picasso_group_create(picasso_ctx *const *ctxs, int32_t world, picasso_group **out);
 picasso_status picasso_group_destroy(picasso_group *group);
 picasso_status picasso_group_fwd(picasso_group *group, const int64_t *const *ids, const int32_t *const *offsets,

@@ -31,6 +31,9 @@ from .abi import (  # noqa: F401
     picasso_group_bwd_update,
     picasso_get_owner_unique,
     picasso_get_send_counts,
+    picasso_hot_cache_refresh,
+    picasso_group_hot_cache_refresh,
+    picasso_get_hot_keys,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
 from .embedding import LoopbackGroup, PackedEmbedding  # noqa: F401

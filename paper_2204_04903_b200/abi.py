@@ -21,7 +21,8 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_last_error", "picasso_get_unique", "picasso_get_inverse", "picasso_launch_count",
            "picasso_profile_enable", "picasso_profile_read", "picasso_unique_offsets", "picasso_nccl_unique_id",
            "picasso_group_create", "picasso_group_destroy", "picasso_group_fwd", "picasso_group_bwd_update",
-           "picasso_get_owner_unique", "picasso_get_send_counts"]
+           "picasso_get_owner_unique", "picasso_get_send_counts", "picasso_hot_cache_refresh",
+           "picasso_group_hot_cache_refresh", "picasso_get_hot_keys"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -41,7 +42,15 @@ class PlanView(C.Structure):
 class CtxOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_ids", C.c_int64), ("pool", C.c_int32), ("id_mode", C.c_int32),
                 ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
-                ("max_recv", C.c_int64)]
+                ("max_recv", C.c_int64), ("cache_max_bytes", C.c_int64)]
+
+
+class CacheStats(C.Structure):
+    _fields_ = [("k", C.c_int64), ("bytes", C.c_int64), ("hot_uniques", C.c_int64), ("uniques", C.c_int64),
+                ("hit_ratio_unique", C.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
 
 
 _lib = None
@@ -65,6 +74,9 @@ def lib():
             "picasso_group_bwd_update": [vp, vp, C.c_float, i64, vp],
             "picasso_get_owner_unique": [vp, i32, vp, i64, C.POINTER(i64)],
             "picasso_get_send_counts": [vp, vp],
+            "picasso_hot_cache_refresh": [vp, C.c_size_t, vp, vp],
+            "picasso_group_hot_cache_refresh": [vp, C.c_size_t, vp, vp],
+            "picasso_get_hot_keys": [vp, vp, vp, i64, C.POINTER(i64)],
             "picasso_workspace_size": [vp, C.POINTER(C.c_size_t)],
             "picasso_pack_local_rows": [vp, i32, C.POINTER(i64)],
             "picasso_bind": [vp, vp, C.c_size_t, vp, vp, vp],
@@ -142,7 +154,7 @@ def picasso_nccl_unique_id():
 
 def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, field_col, out_width, rank, world,
                        max_batch, max_ids, pool=POOL_SUM, id_mode=IDS_HASH, opt=OPT_ADAGRAD, eps=None, beta1=0.9,
-                       beta2=0.999, nccl_uid=None, max_recv=0):
+                       beta2=0.999, nccl_uid=None, max_recv=0, cache_max_bytes=0):
     k = _Keep()
     k.f2t = _np(field_to_table, np.int32)
     k.t2p = _np(plan["table_to_pack"], np.int32)
@@ -157,7 +169,7 @@ def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, 
     if eps is None:
         eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
     o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),
-                float(beta2), int(max_recv))
+                float(beta2), int(max_recv), int(cache_max_bytes))
     ctx = C.c_void_p()
     uid = None if nccl_uid is None else (C.c_uint8 * 128)(*nccl_uid)
     _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), uid, C.byref(o), C.byref(ctx)),
@@ -295,3 +307,28 @@ def picasso_unique_offsets(ctx, dst, stream=None):
     device tensor or a pinned host tensor)."""
     _chk(lib().picasso_unique_offsets(ctx, _ptr(dst), _stream(stream)), "picasso_unique_offsets", ctx)
     return dst
+
+
+# ---- HybridHash ---------------------------------------------------------------------------
+def picasso_hot_cache_refresh(ctx, capacity_bytes, stream=None):
+    st = CacheStats()
+    _chk(lib().picasso_hot_cache_refresh(ctx, int(capacity_bytes), _stream(stream), C.byref(st)),
+         "picasso_hot_cache_refresh", ctx)
+    return st.as_dict()
+
+
+def picasso_group_hot_cache_refresh(group, world, capacity_bytes, stream=None):
+    st = (CacheStats * world)()
+    _chk(lib().picasso_group_hot_cache_refresh(group, int(capacity_bytes), _stream(stream), st),
+         "picasso_group_hot_cache_refresh")
+    return [s.as_dict() for s in st]
+
+
+def picasso_get_hot_keys(ctx):
+    n = C.c_int64()
+    _chk(lib().picasso_get_hot_keys(ctx, None, None, 0, C.byref(n)), "picasso_get_hot_keys", ctx)
+    pk = np.zeros(max(n.value, 1), np.int32)
+    ky = np.zeros(max(n.value, 1), np.int64)
+    _chk(lib().picasso_get_hot_keys(ctx, pk.ctypes.data, ky.ctypes.data, n.value, C.byref(n)), "picasso_get_hot_keys",
+         ctx)
+    return pk[:n.value], ky[:n.value]

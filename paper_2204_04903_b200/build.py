@@ -68,7 +68,7 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     if cmds or not os.path.exists(LIB):
         nlib = os.path.join(NCCL, "lib")
         link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-fPIC", "-L", nlib,
-                "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib]
+                "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib, "-Xlinker", "--no-undefined"]
         run(link)
         os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -80,6 +80,28 @@ struct MultiState {
     std::vector<int64_t> skoff, sk, rkoff, rk, srow_off, srow_n, rrow_off, rrow_n;  // per peer
     int64_t R = 0, U_send = 0;
     std::vector<int64_t> opack_ostart;  // [P+1]
+    // ---- HybridHash (cache.cu / cache_host.cu)
+    int64_t k_max = 0;                  // hot rows the workspace can hold
+    int32_t hot_k = 0;                  // current hot rows (0 = off)
+    uint32_t hot_mask = 0;
+    Slot *hot_index = nullptr;
+    int32_t *hslot = nullptr;
+    unsigned long long *hot_keys = nullptr;
+    float *hot_arena = nullptr, *hot_g = nullptr, *hot_gsum = nullptr, *hot_touch = nullptr, *stage = nullptr;
+    uint32_t *hot_cnt = nullptr, *cnt_sum = nullptr, *fcnt = nullptr, *cnt_hist = nullptr;
+    int32_t *hot_pslot_d = nullptr, *stage_idx = nullptr, *tie_cnt = nullptr, *cand_n = nullptr;
+    int64_t *hot_off_d = nullptr;       // [4P]: w, s1, s2, g offsets
+    int64_t *fcnt_off_d = nullptr, *row_key_d = nullptr;
+    unsigned long long *cand_key = nullptr;
+    uint32_t *cand_cnt = nullptr;
+    int64_t rows_total = 0;
+    std::vector<int64_t> fcnt_off;      // [P+1]
+    std::vector<int32_t> hot_pslot;     // [P+1]
+    std::vector<int64_t> hot_off;       // [4P]
+    int64_t hot_g_floats = 0;
+    int64_t last_hot_uniques = 0, last_uniques = 0;
+    std::vector<int64_t> stage_blk;     // [W+1] owner blocks of the refresh staging (floats)
+    int32_t new_k = 0;
 };
 
 struct picasso_ctx {
@@ -158,6 +180,7 @@ struct picasso_ctx {
     }
 
     int32_t *osort_hist = nullptr;  // k_inverse's pass-0 histogram output when run on the owner stream
+    int32_t *hot_scan_scratch = nullptr;
 
     size_t carve(char *base) {
         Carver c{base};
@@ -232,8 +255,39 @@ struct picasso_ctx {
             mp.rsend_off = c.take<int64_t>(RM);
             mp.rows_send = c.take<float>((size_t)RM * maxD);
             osort_hist = c.take<int32_t>(2 * ((RM + kTile - 1) / kTile) + 2);
+            if (opts.cache_max_bytes > 0) {  // HybridHash
+                const int64_t K = std::max<int64_t>(mp.k_max, 1);
+                const int64_t arena = opts.cache_max_bytes / 4 + 4 * P;
+                mp.hot_index = c.take<Slot>((size_t)mp.hot_mask + 1);
+                mp.hslot = c.take<int32_t>(N);
+                mp.hot_keys = c.take<unsigned long long>(K);
+                mp.hot_arena = c.take<float>(arena);
+                mp.hot_g = c.take<float>(arena / 2 + 4);
+                mp.hot_gsum = c.take<float>(arena / 2 + 4);
+                mp.hot_touch = c.take<float>(2 * K);
+                mp.stage = c.take<float>(arena);
+                mp.hot_cnt = c.take<uint32_t>(K);
+                mp.cnt_sum = c.take<uint32_t>(2 * K);
+                mp.fcnt = c.take<uint32_t>(std::max<int64_t>(mp.rows_total, 1));
+                mp.cnt_hist = c.take<uint32_t>(1 << 16);
+                mp.hot_pslot_d = c.take<int32_t>(P + 1);
+                mp.stage_idx = c.take<int32_t>(K);
+                mp.tie_cnt = c.take<int32_t>((mp.rows_total + kTile - 1) / kTile + 2);
+                mp.cand_n = c.take<int32_t>(2);
+                mp.hot_off_d = c.take<int64_t>(4 * P);
+                mp.fcnt_off_d = c.take<int64_t>(P + 1);
+                mp.row_key_d = c.take<int64_t>(2 * P);
+                mp.cand_key = c.take<unsigned long long>((size_t)K * world);
+                mp.cand_cnt = c.take<uint32_t>((size_t)K * world);
+                hot_scan_scratch = c.take<int32_t>((mp.rows_total + kTile - 1) / kTile / kTile + 64);
+            }
         }
         return c.off + kAlign;
     }
+};
+
+// Loopback group: all ranks of a row-sharded step in one process (multi_host.cu, cache_host.cu).
+struct picasso_group {
+    std::vector<picasso_ctx *> ctx;
 };
 

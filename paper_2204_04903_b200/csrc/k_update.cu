@@ -72,6 +72,22 @@ __device__ __forceinline__ float4 round4(dbl4 a) {
                        __double2float_rn(a.w));
 }
 
+// Where the G row of unique u goes: the hot-gradient buffer for a HybridHash hot row (and its
+// occurrence count into hot_touch), else the rows/G buffer (send layout at W > 1, pack layout
+// at W = 1).
+template <int D>
+__device__ __forceinline__ float *g_row_ptr(const UpdateArgs &a, int64_t u, int32_t u0, float *gp, int li,
+                                            float nocc) {
+    if (a.hslot) {
+        const int32_t hs = a.hslot[u];
+        if (hs >= 0) {
+            if (li == 0) a.hot_touch[hs] = nocc;
+            return a.hot_g + a.hot_g_off[a.pack] + (int64_t)(hs - a.hot_pslot[a.pack]) * D;
+        }
+    }
+    return a.row_off ? a.gbuf + a.row_off[u] : gp + (u - u0) * D;
+}
+
 // One dY contribution (fp32, mean: dY / len) of the occurrence in segment `seg`.
 template <int D>
 __device__ __forceinline__ void load_contrib(const UpdateArgs &a, int32_t seg, int li, float4 *c) {
@@ -416,8 +432,9 @@ __global__ void __launch_bounds__(256) k_segsum(UpdateArgs a) {
             for (int q = 0; q < VPL; ++q) g[q] = zero4d();
             int cur = c_lo;
             auto finish = [&](int c) {  // rows deferred to the chunked path write nothing here
-                if (cum[c - c_lo + 1] > cum[c - c_lo]) {
-                    float *o = (a.row_off ? a.gbuf + a.row_off[t0 + c] : gp + (int64_t)(t0 + c - u0) * D) + li * 4;
+                const int32_t nocc = cum[c - c_lo + 1] - cum[c - c_lo];
+                if (nocc > 0) {
+                    float *o = g_row_ptr<D>(a, t0 + c, u0, gp, li, (float)nocc) + li * 4;
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) *reinterpret_cast<float4 *>(o + q * LANES * 4) = round4(g[q]);
                 }
@@ -651,8 +668,9 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
                     for (int q = 0; q < VPL; ++q) g[q] = add4d(g[q], pv[k][q]);
         }
         if (a.gbuf) {  // split backward: the update kernel applies the optimizer
-            float *o = (a.row_off ? a.gbuf + a.row_off[u]
-                                  : a.gbuf + a.pack_gbase[a.pack] + (int64_t)(u - a.pack_ustart[a.pack]) * D) + li * 4;
+            const int32_t u0 = a.pack_ustart[a.pack];
+            float *o = g_row_ptr<D>(a, u, u0, a.gbuf + a.pack_gbase[a.pack], li,
+                                    (float)(__ldg(a.ustart + u + 1) - __ldg(a.ustart + u))) + li * 4;
 #pragma unroll
             for (int q = 0; q < VPL; ++q) *reinterpret_cast<float4 *>(o + q * LANES * 4) = round4(g[q]);
         } else {

@@ -123,6 +123,11 @@ struct UpdateArgs {
     float *gbuf;                 // split backward: G rows of all packs (nullptr: fused)
     const int64_t *row_off;      // W > 1: [U] float offset of each unique row's G in gbuf
     const int64_t *pack_gbase;   // [P+1] float offset of each pack's G rows in gbuf
+    const int32_t *hslot;        // HybridHash: [U] hot slot or -1 (nullptr: no hot rows)
+    float *hot_g;                // hot-slot gradient rows (pack p at hot_g_off[p])
+    const int64_t *hot_g_off;    // [P]
+    const int32_t *hot_pslot;    // [P+1]
+    float *hot_touch;            // [k] occurrences of the hot slot this step
 };
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(kTileThreads) k_bucket(MultiArgs m) {
             const int64_t p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
             const uint64_t key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
             b = (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
+            if (m.hot_k > 0 && m.hslot[u] >= 0) b = m.W * m.P;  // hot: served by the replica, not sent
             m.bkey[u] = b;
             m.bval[u] = (int32_t)u;
         }
@@ -72,8 +73,14 @@ __global__ void k_send_prep(MultiArgs m) {
         const int32_t u = m.send_uid[i];
         const int64_t p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, u) - 1;
         const uint64_t key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
-        const int32_t b = (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
         m.send_pos[u] = (int32_t)i;
+        const int32_t hs = m.hot_k > 0 ? m.hslot[u] : -1;
+        if (hs >= 0) {  // row of the local replica (offset relative to the rows buffer)
+            m.row_off[u] = (int64_t)((m.hot_arena + m.hot_w_off[p] + (int64_t)(hs - m.hot_pslot[p]) * m.pack_dim[p]) -
+                                     m.gbuf_base);
+            continue;
+        }
+        const int32_t b = (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
         m.send_keys[i] = (int32_t)(key / (uint64_t)m.W);
         m.row_off[u] = m.sroff[b] + (i - m.bstart[b]) * m.pack_dim[p];
     }
@@ -103,6 +110,8 @@ __global__ void __launch_bounds__(256) k_owner_insert(MultiArgs m, Slot *table, 
         const int64_t i = sb[k].rstart + (opos - sb[k].ostart);
         m.opos_map[opos] = (int32_t)i;
         key = (unsigned long long)(m.pack_key_off[sb[k].pack] + (int64_t)m.recv_keys[i]);
+        // FCounter (Alg. 1 L501/L511): one count per requesting rank (its keys are unique)
+        if (m.fcnt) atomicAdd(m.fcnt + m.fcnt_off[sb[k].pack] + m.recv_keys[i], 1u);
     }
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
     if (!valid) return;

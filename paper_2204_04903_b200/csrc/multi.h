@@ -6,6 +6,10 @@ namespace picasso {
 
 constexpr int kMaxOwnerBlocks = 1024;  // W * P blocks of the owner stream (W <= 8, P <= 128)
 
+struct RankPtrs {  // the W ranks' buffers of a loopback group, passed to a kernel by value
+    const void *p[8];
+};
+
 // One (pack, source) block of the owner stream (pack-major: pack, then source rank).
 struct OwnerBlock {
     int64_t ostart;  // first owner-stream position of the block
@@ -46,6 +50,22 @@ struct MultiArgs {
     int32_t *contrib;                // [U_o, W] receive index of each source's request, or -1
     int64_t *rsend_off;              // [R] float offset of receive index i's row in rows_send
     float *rows_send;                // owner rows out (fwd) / gradient rows in (bwd)
+    // HybridHash hot storage: replicated top-k rows on every rank
+    int32_t hot_k;                   // hot rows (all packs); 0 = cache off
+    const Slot *hot_index;           // key -> slot (minpos field holds the slot), replicated
+    uint32_t hot_mask;               // hot index capacity - 1
+    int32_t *hslot;                  // [U] hot slot of each unique, or -1
+    const int32_t *hot_pslot;        // [P+1] slot range of each pack (slots grouped by pack)
+    const int64_t *hot_w_off;        // [P] float offset of pack p's replica rows in the arena
+    float *hot_arena;                // replicas: per pack [k_p, D] weights, then states
+    const int64_t *hot_s1_off, *hot_s2_off;  // [P] offsets of the replicated optimizer state
+    float *hot_g;                    // [k rows of D_p] gradient rows of the hot slots (summed over ranks)
+    float *hot_touch;                // [k] occurrences of each hot slot this step (summed over ranks)
+    uint32_t *hot_cnt;               // [k] FCounter of hot keys (this rank's post-unique hits)
+    const int64_t *hot_g_off;        // [P] float offset of pack p's hot G rows in hot_g
+    const float *gbuf_base;          // rows/G buffer base (row_off of a hot unique is relative to it)
+    uint32_t *fcnt;                  // FCounter of owned rows: [sum_p local_rows_p]
+    const int64_t *fcnt_off;         // [P] offset of pack p's counters
 };
 
 void launch_bucket(const MultiArgs &m, cudaStream_t s);

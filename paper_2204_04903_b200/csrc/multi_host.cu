@@ -71,8 +71,34 @@ static MultiArgs multi_args(picasso_ctx *ctx) {
     m.contrib = mp.contrib;
     m.rsend_off = mp.rsend_off;
     m.rows_send = mp.rows_send;
+    while ((1 << m.bucket_bits) < ctx->world * ctx->P + 1) ++m.bucket_bits;  // + the hot bucket
+    m.hot_k = mp.hot_k;
+    m.hot_index = mp.hot_index;
+    m.hot_mask = mp.hot_mask;
+    m.hslot = mp.hslot;
+    m.hot_pslot = mp.hot_pslot_d;
+    m.hot_w_off = mp.hot_off_d;
+    m.hot_s1_off = mp.hot_off_d + ctx->P;
+    m.hot_s2_off = mp.hot_off_d + 2 * ctx->P;
+    m.hot_g_off = mp.hot_off_d + 3 * ctx->P;
+    m.hot_arena = mp.hot_arena;
+    m.hot_g = mp.hot_g;
+    m.hot_touch = mp.hot_touch;
+    m.hot_cnt = mp.hot_cnt;
+    m.gbuf_base = ctx->gbuf;
+    m.fcnt = mp.fcnt;
+    m.fcnt_off = mp.fcnt_off_d;
     return m;
 }
+
+MultiArgs picasso_multi_args(picasso_ctx *ctx) { return multi_args(ctx); }
+
+namespace picasso {
+void launch_hot_probe(const MultiArgs &m, int num_sms, cudaStream_t s);
+void launch_hot_update(int D, const MultiArgs &m, int pack, int opt, float lr, float eps, float b1, float b2, float ss,
+                       int num_sms, cudaStream_t s);
+void launch_sum_ranks(const RankPtrs &src, int W, float *dst, int64_t n, cudaStream_t s);
+}  // namespace picasso
 
 // ---- phase A: dedup (as at W = 1) + Partition into the owner-major send layout -------------
 picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
@@ -90,12 +116,15 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
     launch_dedup_insert(a, s);
     launch_dedup_assign(a, s);
     MultiArgs m = multi_args(ctx);
+    if (mp.hot_k > 0) launch_hot_probe(m, ctx->num_sms, s);  // hot keys skip the exchange
     launch_bucket(m, s);
     bucket_sort_pass(mp.bkey, mp.bval, mp.bsorted, mp.send_uid, std::max<int64_t>(N, 1), ctx->d_total,
                      m.bucket_bits, mp.bhist, mp.bcount, s);
     launch_bucket_prefix(m, s);
     launch_send_prep(m, ctx->num_sms, s);
-    MCK(cudaMemcpyAsync(mp.cnt_send_h, mp.bcount, sizeof(int32_t) * ctx->world * ctx->P, cudaMemcpyDeviceToHost, s));
+    // bucket counts (+ the hot bucket: the hit statistic of HybridHash)
+    MCK(cudaMemcpyAsync(mp.cnt_send_h, mp.bcount, sizeof(int32_t) * (ctx->world * ctx->P + 1), cudaMemcpyDeviceToHost,
+                        s));
     ctx->mark(0, false, s);
     ctx->launches_fwd += 1 + (N > 0 ? 4 : 0) + 1 + 5;
     return PICASSO_OK;
@@ -129,6 +158,8 @@ picasso_status mfwd_b(picasso_ctx *ctx, cudaStream_t s) {
         mp.rrow_off[r + 1] = mp.rrow_off[r] + mp.rrow_n[r];
     }
     mp.R = mp.rkoff[W];
+    mp.last_hot_uniques = mp.hot_k > 0 ? mp.cnt_send_h[W * P] : 0;
+    mp.last_uniques = mp.skoff[W] + mp.last_hot_uniques;
     mp.U_send = mp.skoff[W];
     if (mp.R > mp.max_recv) {
         ctx->last_msg = "received keys exceed max_recv";
@@ -246,6 +277,16 @@ picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
     ctx->launches_bwd += N > 0 ? 1 : 0;
     ctx->mark(3, true, s);
     UpdateArgs u = make_update_args(ctx, grad_out, lr, step, su, sseg);
+    MultiState &mp = ctx->mp;
+    if (mp.hot_k > 0) {  // this rank's hot-row gradients and occurrence counts (AllReduced next)
+        MCK(cudaMemsetAsync(mp.hot_g, 0, sizeof(float) * mp.hot_g_floats, s));
+        MCK(cudaMemsetAsync(mp.hot_touch, 0, sizeof(float) * mp.hot_k, s));
+        u.hslot = mp.hslot;
+        u.hot_g = mp.hot_g;
+        u.hot_g_off = mp.hot_off_d + 3 * ctx->P;
+        u.hot_pslot = mp.hot_pslot_d;
+        u.hot_touch = mp.hot_touch;
+    }
     u.gbuf = ctx->gbuf;
     u.row_off = ctx->mp.row_off;
     if (N > 0) {
@@ -272,6 +313,11 @@ picasso_status mbwd_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) 
         launch_owner_update(ctx->pack_dim[p], m, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr,
                             ctx->opts.eps, ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s);
         ctx->launches_bwd += 1;
+        if (ctx->mp.hot_k > 0 && ctx->mp.hot_pslot[p + 1] > ctx->mp.hot_pslot[p]) {  // replicas, same on every rank
+            launch_hot_update(ctx->pack_dim[p], m, p, ctx->opts.opt, lr, ctx->opts.eps, ctx->opts.beta1,
+                              ctx->opts.beta2, ss, ctx->num_sms, s);
+            ctx->launches_bwd += 1;
+        }
     }
     ctx->mark(5, false, s);
     if (ctx->prof) ++ctx->prof_calls;
@@ -320,14 +366,38 @@ picasso_status multi_bwd_nccl(picasso_ctx *ctx, const float *grad_out, float lr,
     if ((st = a2av_nccl(ctx, ctx->gbuf, mp.srow_off, mp.srow_n, mp.rows_send, mp.rrow_off, mp.rrow_n, ncclFloat32, 4,
                         s)))
         return st;
+    if (mp.hot_k > 0) {  // HybridHash: hot-row gradients and occurrence counts summed over ranks
+        NCK(ncclGroupStart());
+        NCK(ncclAllReduce(mp.hot_g, mp.hot_g, mp.hot_g_floats, ncclFloat32, ncclSum, mp.comm, s));
+        NCK(ncclAllReduce(mp.hot_touch, mp.hot_touch, mp.hot_k, ncclFloat32, ncclSum, mp.comm, s));
+        NCK(ncclGroupEnd());
+    }
     return mbwd_f(ctx, lr, step, s);
+}
+
+// loopback AllReduce of the hot-row gradients / occurrence counts: rank-order sum into rank 0's
+// scratch, then a copy to every rank (all replicas then apply identical arithmetic)
+static picasso_status hot_allreduce_loop(std::vector<picasso_ctx *> &cs, cudaStream_t s) {
+    picasso_ctx *ctx = cs[0];
+    const int W = (int)cs.size();
+    MultiState &m0 = ctx->mp;
+    if (m0.hot_k == 0) return PICASSO_OK;
+    RankPtrs pg{}, pt{};
+    for (int r = 0; r < W; ++r) {
+        pg.p[r] = cs[r]->mp.hot_g;
+        pt.p[r] = cs[r]->mp.hot_touch;
+    }
+    launch_sum_ranks(pg, W, m0.hot_gsum, m0.hot_g_floats, s);
+    launch_sum_ranks(pt, W, m0.stage, m0.hot_k, s);
+    for (int r = 0; r < W; ++r) {
+        MCK(cudaMemcpyAsync(cs[r]->mp.hot_g, m0.hot_gsum, sizeof(float) * m0.hot_g_floats, cudaMemcpyDeviceToDevice, s));
+        MCK(cudaMemcpyAsync(cs[r]->mp.hot_touch, m0.stage, sizeof(float) * m0.hot_k, cudaMemcpyDeviceToDevice, s));
+    }
+    return PICASSO_OK;
 }
 
 // ------------------------------------------------------------------------------------------
 // Loopback driver: all W ranks in this process, on one device; exchanges are device copies.
-struct picasso_group {
-    std::vector<picasso_ctx *> ctx;
-};
 
 static picasso_status a2av_loop(picasso_group *g, int which, cudaStream_t s) {
     const int W = (int)g->ctx.size();
@@ -422,6 +492,7 @@ extern "C" picasso_status picasso_group_bwd_update(picasso_group *g, const float
         if ((st = mbwd_e(c, grad_out[r], lr, step, s))) return st;
     }
     if ((st = a2av_loop(g, 3, s))) return st;
+    if ((st = hot_allreduce_loop(g->ctx, s))) return st;
     for (int r = 0; r < W; ++r)
         if ((st = mbwd_f(g->ctx[r], lr, step, s))) return st;
     return PICASSO_OK;

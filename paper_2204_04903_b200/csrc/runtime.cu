@@ -103,6 +103,19 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
                 delete c;
                 return PICASSO_ERR_PLAN_MISMATCH;
             }
+        if (opts->cache_max_bytes > 0) {  // HybridHash sizing: FCounter over owned rows, hot rows
+            c->mp.fcnt_off.assign(c->P + 1, 0);
+            int minD = 1 << 30;
+            for (int32_t p = 0; p < c->P; ++p) {
+                const int64_t R = c->pack_rows[p];
+                c->mp.fcnt_off[p + 1] = c->mp.fcnt_off[p] + (R > rank ? (R - rank + world - 1) / world : 0);
+                minD = std::min(minD, c->pack_dim[p]);
+            }
+            c->mp.rows_total = c->mp.fcnt_off[c->P];
+            const int nst = opts->opt == PICASSO_OPT_ADAM_LAZY ? 2 : 1;
+            c->mp.k_max = opts->cache_max_bytes / ((int64_t)4 * minD * (1 + nst));
+            c->mp.hot_mask = pow2_at_least((uint64_t)std::max<int64_t>(c->mp.k_max, 1) * 2) - 1;
+        }
     }
     if (const char *e = std::getenv("PICASSO_BWD")) c->split_bwd = std::strcmp(e, "fused") != 0;
     c->ws_bytes = c->carve(nullptr);
@@ -164,11 +177,21 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
     if (ctx->world > 1 && !ctx->mp.cnt_send_h) {
         const int WP = ctx->world * ctx->P;
-        CK(cudaMallocHost(&ctx->mp.cnt_send_h, sizeof(int32_t) * WP));
+        CK(cudaMallocHost(&ctx->mp.cnt_send_h, sizeof(int32_t) * (WP + 1)));
         CK(cudaMallocHost(&ctx->mp.cnt_recv_h, sizeof(int32_t) * WP));
         CK(cudaMallocHost(&ctx->mp.oblk_h, sizeof(OwnerBlock) * WP));
         CK(cudaMallocHost(&ctx->mp.ostart_h, sizeof(int64_t) * (ctx->P + 1)));
         CK(cudaMallocHost(&ctx->mp.og_h, sizeof(int32_t) * (ctx->P + 1)));
+    }
+    if (ctx->world > 1 && ctx->opts.cache_max_bytes > 0) {  // HybridHash: FCounter, empty hot set
+        MultiState &mp = ctx->mp;
+        CK(cudaMemcpy(mp.fcnt_off_d, mp.fcnt_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
+        CK(cudaMemset(mp.fcnt, 0, sizeof(uint32_t) * std::max<int64_t>(mp.rows_total, 1)));
+        CK(cudaMemset(mp.hot_cnt, 0, sizeof(uint32_t) * std::max<int64_t>(mp.k_max, 1)));
+        CK(cudaMemset(mp.hot_index, 0xFF, sizeof(Slot) * ((size_t)mp.hot_mask + 1)));
+        CK(cudaMemset(mp.hot_pslot_d, 0, sizeof(int32_t) * (ctx->P + 1)));
+        CK(cudaMemset(mp.hot_off_d, 0, sizeof(int64_t) * 4 * ctx->P));
+        mp.hot_k = 0;
     }
     if (ctx->world > 1 && ctx->mp.has_uid && !ctx->mp.comm) {  // one rank per process: NCCL
         ncclUniqueId id;

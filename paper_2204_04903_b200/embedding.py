@@ -19,7 +19,7 @@ class PackedEmbedding:
     def __init__(self, field_to_table, table_rows, table_dim, *, max_batch, max_ids, table_salt=None,
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
-                 init_acc=0.1, nccl_uid=None, max_recv=0):
+                 init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -34,7 +34,8 @@ class PackedEmbedding:
         self.device = torch.device(device)
         self.ctx = abi.picasso_ctx_create(self.plan, self.f2t, self.rows, self.dims, table_salt, self.field_col,
                                           self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
-                                          eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv)
+                                          eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv,
+                                          cache_max_bytes=cache_max_bytes)
         P = self.plan["n_packs"]
         self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
         ws = abi.picasso_workspace_size(self.ctx)
@@ -92,6 +93,13 @@ class PackedEmbedding:
     def owner_unique(self, pack):
         return abi.picasso_get_owner_unique(self.ctx, pack, self.device)
 
+    def hot_cache_refresh(self, capacity_bytes, stream=None):
+        """Alg. 1 L514-517 (collective over the ranks in NCCL mode); returns the cache stats."""
+        return abi.picasso_hot_cache_refresh(self.ctx, capacity_bytes, stream)
+
+    def hot_keys(self):
+        return abi.picasso_get_hot_keys(self.ctx)
+
     def send_counts(self):
         return abi.picasso_get_send_counts(self.ctx, self.world)
 
@@ -126,6 +134,9 @@ class LoopbackGroup:
 
     def backward_update(self, grad_outs, lr, step, stream=None):
         abi.picasso_group_bwd_update(self.group, grad_outs, lr, step, stream)
+
+    def hot_cache_refresh(self, capacity_bytes, stream=None):
+        return abi.picasso_group_hot_cache_refresh(self.group, self.world, capacity_bytes, stream)
 
     def close(self):
         if self.group:
