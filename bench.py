@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--nbatches", type=int, default=4, help="distinct pre-generated batches, used round robin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cache-bytes", type=int, default=0, help="HybridHash hot storage per GPU (N > 1)")
+    ap.add_argument("--cache-warmup", type=int, default=3, help="Alg. 1 warmup_iters")
+    ap.add_argument("--cache-flush", type=int, default=10, help="Alg. 1 flush_iters")
     return ap.parse_args()
 
 
@@ -230,7 +233,8 @@ def main():
         uid = obj[0]
     emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=B, max_ids=max_ids,
                              table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
-                             device=dev, rank=rank, world=world, nccl_uid=uid, max_recv=2 * max_ids)
+                             device=dev, rank=rank, world=world, nccl_uid=uid, max_recv=2 * max_ids,
+                             cache_max_bytes=args.cache_bytes if world > 1 else 0)
     init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights,
                            rank=rank, world=world)
     dev_in = [(torch.from_numpy(b.ids).to(dev), torch.from_numpy(b.offsets).to(dev)) for b in batches]
@@ -241,10 +245,15 @@ def main():
     lr = 0.01
     stream = torch.cuda.current_stream(dev)
 
+    cache_stats = {}
+
     def step(i, s):
         ids, off = dev_in[i % args.nbatches]
         emb.forward(ids, off, B, out, stream=s)
         emb.backward_update(dys[i % args.nbatches], lr, step=i + 1, stream=s)
+        itr = i + 1  # Alg. 1 schedule (reading O13): refresh after bwd when itr >= warmup, itr % flush == 0
+        if world > 1 and args.cache_bytes > 0 and itr >= args.cache_warmup and itr % args.cache_flush == 0:
+            cache_stats.update(emb.hot_cache_refresh(args.cache_bytes, stream=s))
 
     for i in range(args.warmup):
         step(i, stream)
@@ -361,6 +370,8 @@ def main():
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
                          "peak_source": peak_src},
             "phases_ms": per_phase,
+            "cache": ({"bytes_per_gpu": args.cache_bytes, "warmup_iters": args.cache_warmup,
+                       "flush_iters": args.cache_flush, **cache_stats} if args.cache_bytes and world > 1 else None),
             "outside_phases_ms": ms - sum(per_phase.values()),  # exchanges + host sync (W > 1), launch gaps
             "step_algorithmic_bytes": alg["step"],
             "step_roofline_frac": alg["step"] / (ms_max * 1e-3) / 1e9 / peak,

@@ -27,20 +27,22 @@ def main():
     from test_multi_gpu import shard_expected
 
     name = sys.argv[1] if len(sys.argv) > 1 else "toy"
-    cfg = dc.toy() if name == "toy" else dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    cache = name.endswith("_cache")  # HybridHash on: refresh after step 1 (warm-up 1, flush 1)
+    base = name[:-6] if cache else name
+    cfg = dc.toy(alpha=1.2) if base == "toy" else dc.scaled(dc.wdl(), batch=32, rows_div=2000)
     obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     mi = cfg.batch * cfg.F * 60
     e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=cfg.batch, max_ids=mi,
                            table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
                            rank=rank, world=world, nccl_uid=obj[0], max_recv=world * mi,
-                           device=torch.device("cuda", local))
+                           device=torch.device("cuda", local), cache_max_bytes=(1 << 20) if cache else 0)
     init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights, rank=rank,
                            world=world)
     m, tabs = oracle_model(cfg), oracle_tables(cfg)
     acc = [np.full_like(t, 0.1) for t in tabs]
     report = {"rank": rank, "world": world, "ok": False}
-    for step in (1, 2):
+    for step in (1, 2, 3):
         bs = [make_batch(cfg, r, step) for r in range(world)]
         dys = [make_dy(cfg, r, step) for r in range(world)]
         out = e.forward(torch.from_numpy(bs[rank].ids).cuda(), torch.from_numpy(bs[rank].offsets).cuda(), cfg.batch)
@@ -50,6 +52,11 @@ def main():
         e.backward_update(torch.from_numpy(dys[rank]).cuda(), lr=0.05, step=step)
         e.check()
         oracle.backward_update(m, obs, tabs, acc, lr=0.05, step=step)
+        if cache:  # the shards are authoritative only after a write-back: refresh every step
+            stats = e.hot_cache_refresh(8 * 1024 if step < 3 else 0)
+            report[f"stats{step}"] = stats
+            if step == 2:
+                assert stats["hot_uniques"] > 0 and stats["k"] > 0, stats
         for p, exp in enumerate(shard_expected(e, cfg, tabs, "w", world, rank)):
             got = e.weights[p][:len(exp)].cpu().numpy()
             assert np.array_equal(got, exp), f"weights p{p} step {step} (dyadic dY: exact)"

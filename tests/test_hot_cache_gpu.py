@@ -87,8 +87,7 @@ def test_hybridhash_transparency_and_topk(cfg_name):
                 pk, ky = e.hot_keys()
                 assert np.array_equal(pk, exp_pack[order]) and np.array_equal(ky, (exp - pko[exp_pack])[order])
             assert stats[0]["k"] == len(exp) > 0 and stats[0]["bytes"] <= capacity
-        if itr > warmup:
-            st = g.hot_cache_refresh(capacity) if False else None  # (refresh only on the schedule)
+        if itr > warmup:  # hot keys left the exchange
             assert sent < sent_before or cfg_name == "wdl", "hot keys must leave the exchange"
     g.hot_cache_refresh(0)  # write back + drop: the shards are the authoritative copy again
     for r, e in enumerate(g.ranks):

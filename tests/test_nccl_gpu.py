@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("name", ["toy", "wdl"])
+@pytest.mark.parametrize("name", ["toy", "wdl", "toy_cache", "wdl_cache"])
 def test_nccl_sharded_parity(name):
     n = torch.cuda.device_count()
     if n < 2:
