@@ -220,6 +220,8 @@ typedef struct {
     int64_t hot_uniques;      /* last forward: unique keys served by the replica ... */
     int64_t uniques;          /* ... out of this many unique keys of the rank */
     double hit_ratio_unique;  /* hot_uniques / uniques */
+    double refresh_ms;        /* host wall time of this refresh (all phases, synchronised) */
+    double propose_ms, select_ms;  /* of which: local top-k proposals; gather + merge + pack */
 } picasso_cache_stats;
 picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t capacity_bytes, void *stream,
                                          picasso_cache_stats *stats);

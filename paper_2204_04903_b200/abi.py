@@ -47,7 +47,8 @@ class CtxOpts(C.Structure):
 
 class CacheStats(C.Structure):
     _fields_ = [("k", C.c_int64), ("bytes", C.c_int64), ("hot_uniques", C.c_int64), ("uniques", C.c_int64),
-                ("hit_ratio_unique", C.c_double)]
+                ("hit_ratio_unique", C.c_double), ("refresh_ms", C.c_double), ("propose_ms", C.c_double),
+                ("select_ms", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -11,6 +11,8 @@
 //   4. owners pack their new hot rows, every rank receives every owner's block (broadcasts),
 //      places the rows into its replica arena and rebuilds the key -> slot index.
 // capacity_bytes = 0 writes back and drops the hot set (checkpoint / disable).
+#include <chrono>
+
 #include "ctx.h"
 
 #define HCK(x)                                                                    \
@@ -260,6 +262,9 @@ extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t cap
     }
     if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;
     MultiState &mp = ctx->mp;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    auto t1 = t0, t2 = t0;
     if (mp.hot_k > 0)
         HNK(ncclAllReduce(mp.hot_cnt, mp.cnt_sum, mp.hot_k, ncclUint32, ncclSum, mp.comm, s));
     if ((st = refresh_writeback(ctx, s))) return st;
@@ -267,6 +272,7 @@ extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t cap
         const int64_t kc = kc_for(ctx, capacity_bytes);
         std::vector<Cand> mine;
         if ((st = refresh_propose(ctx, kc, mine, s))) return st;
+        t1 = clk::now();
         // gather the proposals: fixed kc records per rank (count 0 = padding)
         const int W = ctx->world;
         std::vector<unsigned long long> kk(kc, 0ull);
@@ -292,6 +298,7 @@ extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t cap
         for (size_t i = 0; i < ak.size(); ++i)
             if (ac[i] > 0) all.push_back({ac[i], ak[i]});
         if ((st = refresh_select(ctx, all, capacity_bytes, s))) return st;
+        t2 = clk::now();
         HNK(ncclGroupStart());
         for (int o = 0; o < W; ++o) {
             const int64_t n = mp.stage_blk[o + 1] - mp.stage_blk[o];
@@ -301,7 +308,14 @@ extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t cap
         HNK(ncclGroupEnd());
         if ((st = refresh_place(ctx, s))) return st;
     }
+    HCK(cudaStreamSynchronize(s));
     fill_stats(ctx, stats);
+    if (stats) {
+        const auto t3 = clk::now();
+        stats->refresh_ms = std::chrono::duration<double, std::milli>(t3 - t0).count();
+        stats->propose_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        stats->select_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    }
     return PICASSO_OK;
 }
 
