@@ -255,6 +255,8 @@ def main():
         if world > 1 and args.cache_bytes > 0 and itr >= args.cache_warmup and itr % args.cache_flush == 0:
             cache_stats.update(emb.hot_cache_refresh(args.cache_bytes, stream=s))
 
+    if world > 1 and args.cache_bytes > 0:  # the first refresh and a hot step happen before timing
+        args.warmup = max(args.warmup, max(args.cache_flush, args.cache_warmup) + 1)
     for i in range(args.warmup):
         step(i, stream)
     emb.check()

@@ -200,6 +200,12 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
             ctx->last_msg = "ncclCommInitRank failed";
             return PICASSO_ERR_NCCL;
         }
+        if (ctx->opts.cache_max_bytes > 0) {  // set up the AllReduce path now, not in the first hot step
+            if (ncclAllReduce(ctx->mp.hot_touch, ctx->mp.hot_touch, 1, ncclFloat32, ncclSum, ctx->mp.comm, 0) !=
+                ncclSuccess)
+                return PICASSO_ERR_NCCL;
+            CK(cudaStreamSynchronize(0));
+        }
     }
     ctx->bound = true;
     ctx->fwd_done = false;
