@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--cache-bytes", type=int, default=0, help="HybridHash hot storage per GPU (N > 1)")
     ap.add_argument("--cache-warmup", type=int, default=3, help="Alg. 1 warmup_iters")
     ap.add_argument("--cache-flush", type=int, default=10, help="Alg. 1 flush_iters")
+    ap.add_argument("--eager", action="store_true", help="N = 1: launch every step eagerly instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -266,8 +267,29 @@ def main():
     # ---------------- timed region: K steps, L2 flushed before each (flush not timed)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    pb.picasso_profile_enable(emb.ctx, True)
-    pb.picasso_profile_read(emb.ctx)
+    # world == 1: the whole step (no host synchronisation inside) is one CUDA graph; its phase
+    # events are graph nodes, read after every replay.  world > 1 runs eagerly (the NCCL sizes
+    # need one host sync per step).
+    use_graph = world == 1 and not args.eager
+    graph = None
+    if use_graph:
+        ids0, off0 = dev_in[0]
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        pb.picasso_profile_enable(emb.ctx, 2)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            emb.forward(ids0, off0, B, out, stream=cap)
+            emb.backward_update(dys[0], lr, step=args.warmup + 1, stream=cap)
+        stream.wait_stream(cap)
+        for _ in range(2):  # warm replays
+            graph.replay()
+        torch.cuda.synchronize()
+    else:
+        pb.picasso_profile_enable(emb.ctx, True)
+        pb.picasso_profile_read(emb.ctx)
+    phase_ms = {}
+    ncalls = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -275,12 +297,20 @@ def main():
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             starts[i].record(stream)
-            step(args.warmup + i, stream)
+            if use_graph:
+                graph.replay()
+            else:
+                step(args.warmup + i, stream)
             ends[i].record(stream)
+            if use_graph:  # this replay's phase times (the sync is outside the start/end events)
+                ph, _ = pb.picasso_profile_read(emb.ctx)
+                phase_ms = {k: phase_ms.get(k, 0.0) + v for k, v in ph.items()}
+                ncalls += 1
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    phase_ms, ncalls = pb.picasso_profile_read(emb.ctx)
+    if not use_graph:
+        phase_ms, ncalls = pb.picasso_profile_read(emb.ctx)
     pb.picasso_profile_enable(emb.ctx, False)
     emb.check()
     ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends))) / args.steps
@@ -361,6 +391,7 @@ def main():
                        "alpha": cfg.alpha, "optimizer": "adagrad", "pool": "sum",
                        "parallelism": f"dp{world}+rowshard{world}" if world > 1 else "single",
                        "l2": "flushed (256 MiB write, untimed) before every timed step",
+                       "launch": "cuda_graph (one captured step, replayed)" if use_graph else "eager",
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

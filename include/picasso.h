@@ -178,6 +178,9 @@ picasso_status picasso_launch_count(const picasso_ctx *ctx, int64_t *fwd, int64_
  * The exchanges themselves are outside every phase.  picasso_profile_read synchronises,
  * writes the summed milliseconds of each phase since the last read into ms[6] (host), the
  * number of steps into *calls, and resets.  Off by default. */
+/* on: 0 off, 1 on, 2 on for a step about to be captured into a CUDA graph (world == 1): the
+ * recorded events become graph nodes, so picasso_profile_read after each replay returns that
+ * replay's phase times without resetting the event list. */
 picasso_status picasso_profile_enable(picasso_ctx *ctx, int32_t on);
 picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int64_t *calls);
 

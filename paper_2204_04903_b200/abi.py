@@ -246,7 +246,9 @@ def picasso_launch_count(ctx):
 
 
 def picasso_profile_enable(ctx, on=True):
-    _chk(lib().picasso_profile_enable(ctx, int(bool(on))), "picasso_profile_enable")
+    """on: False/True, or 2 before capturing the step into a CUDA graph."""
+    _chk(lib().picasso_profile_enable(ctx, 2 if on == 2 and not isinstance(on, bool) else int(bool(on))),
+         "picasso_profile_enable")
 
 
 def picasso_profile_read(ctx):

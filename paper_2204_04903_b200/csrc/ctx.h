@@ -151,6 +151,7 @@ struct picasso_ctx {
     // 0 unique(+partition) 1 pool 2 transpose 3 segsum(+update at W=1) 4 owner dedup+gather 5 owner update
     static constexpr int kPhases = 6;
     bool prof = false;
+    bool prof_graph = false;  // events were captured into a CUDA graph: reads do not reset them
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
     size_t ev_used[kPhases] = {0, 0, 0, 0, 0, 0};
     int64_t prof_calls = 0;

@@ -470,7 +470,12 @@ extern "C" picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, in
 
 extern "C" picasso_status picasso_profile_enable(picasso_ctx *ctx, int32_t on) {
     if (!ctx) return PICASSO_ERR_INVALID_ARG;
+    if (on == 2 && !ctx->prof_graph) {  // start of a graph capture: fresh event list, kept afterwards
+        for (int ph = 0; ph < picasso_ctx::kPhases; ++ph) ctx->ev_used[ph] = 0;
+        ctx->prof_calls = 0;
+    }
     ctx->prof = on != 0;
+    ctx->prof_graph = on == 2;
     return PICASSO_OK;
 }
 
@@ -485,10 +490,10 @@ extern "C" picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int6
             tot += t;
         }
         ms[ph] = tot;
-        ctx->ev_used[ph] = 0;
+        if (!ctx->prof_graph) ctx->ev_used[ph] = 0;  // graph mode: the replayed nodes re-record them
     }
-    if (calls) *calls = ctx->prof_calls;
-    ctx->prof_calls = 0;
+    if (calls) *calls = ctx->prof_graph ? 1 : ctx->prof_calls;
+    if (!ctx->prof_graph) ctx->prof_calls = 0;
     return PICASSO_OK;
 }
 
