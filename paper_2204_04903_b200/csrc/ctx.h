@@ -136,6 +136,11 @@ struct picasso_ctx {
     float *gbuf = nullptr;
     int64_t *pack_gbase = nullptr;
     int32_t *pack_dim_d = nullptr;
+    bool bulk_segsum = true;  // PICASSO_SEGSUM=legacy selects the register-staged segsum + hot-row path
+    int seg_cfg = 0;          // PICASSO_SEGSUM_CFG (warps x stages of the pipelined segsum)
+    int32_t seg_nt = 0;       // its tiles per pack
+    int32_t *tile_start = nullptr;
+    int4 *split = nullptr;
     bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
     std::vector<float *> w, s1, s2;
     // step state
@@ -156,6 +161,11 @@ struct picasso_ctx {
     size_t ev_used[kPhases] = {0, 0, 0, 0, 0, 0};
     int64_t prof_calls = 0;
 
+    // inside a capture, an external record becomes a graph node that re-records on every replay
+    void record(cudaEvent_t e, cudaStream_t s) const {
+        if (prof_graph) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+        else cudaEventRecord(e, s);
+    }
     void mark(int ph, bool begin, cudaStream_t s) {
         if (!prof) return;
         auto &v = ev[ph];
@@ -166,9 +176,9 @@ struct picasso_ctx {
                 cudaEventCreate(&b);
                 v.emplace_back(a, b);
             }
-            cudaEventRecord(v[ev_used[ph]].first, s);
+            record(v[ev_used[ph]].first, s);
         } else {
-            cudaEventRecord(v[ev_used[ph]].second, s);
+            record(v[ev_used[ph]].second, s);
             ++ev_used[ph];
         }
     }
@@ -219,7 +229,10 @@ struct picasso_ctx {
         chunk_off = c.take<int32_t>(N / (kLongRow + 1) + 3);
         int maxD = 4;
         for (int32_t d : pack_dim) maxD = std::max(maxD, d);
-        partial = reinterpret_cast<dbl4 *>(c.take<double>(long_partial_doubles(N, maxD)));
+        partial = reinterpret_cast<dbl4 *>(
+            c.take<double>(std::max(long_partial_doubles(N, maxD), segsum_bulk_partial_doubles(maxD, num_sms))));
+        tile_start = c.take<int32_t>(segsum_tile_ints(P, num_sms));
+        split = c.take<int4>(segsum_split_entries(num_sms));
         chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
         pack_gbase = c.take<int64_t>(P + 1);
         pack_dim_d = c.take<int32_t>(P);

@@ -1,0 +1,436 @@
+// k_segsum_bulk.cu — backward segment-sum (Unique^T) as a copy pipeline.
+//
+// After the transpose, the occurrences of the pack sit in uid order (sorted_u / sorted_seg) and
+//   G_u = sum_{p in [ustart[u], ustart[u+1])} dY[seg(p)] * s(p)      (s = 1, or 1/len for mean)
+// The work is a gather of one dY row per occurrence (random rows of the [B, sum D] gradient), a
+// segmented reduction, and one G row written per unique row: HBM-bound.
+//
+//   k_csr_tiles    : row starts (ustart) and, per pack, nt tiles of equal cost, cost(p) =
+//                    occurrences + rows before p (one dY row read per occurrence, one G row
+//                    written per row), so head tiles (few long rows) and tail tiles (many
+//                    one-occurrence rows) take the same time; tiles cut rows anywhere.
+//   k_segsum_pipe  : one warp per tile.  Its lanes resolve 32 positions at a time (sorted_seg ->
+//                    dY row address, one round ahead); per ring stage (~4 KB of rows) each lane
+//                    issues the asynchronous 16-byte copies (LDGSTS) of its own slice of every
+//                    row into a per-warp shared-memory ring, so each SM keeps ~190 KB of dY
+//                    in flight without register staging.  (1-D bulk copies through the TMA unit
+//                    were measured first: no faster at 512-byte rows.)  Landed rows are reduced
+//                    in fp64 (reading O6); each finished row's G is rounded and written.  A row
+//                    cut by a tile edge leaves fp64 partials (head piece: slot 2t, tail piece:
+//                    slot 2t+1) and the tile where it starts lists it.
+//   k_segsum_fix   : per listed row, its pieces summed in tile order, rounded, written.
+#include <cstdlib>
+#include <cstring>
+
+#include "kernels.h"
+
+namespace picasso {
+namespace {
+
+__device__ __forceinline__ void ldgsts(void *smem, const void *gmem, int bytes) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void ldgsts_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ldgsts_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int kStageBytes = 4096;  // target bytes per ring stage
+constexpr int kMaxNW = 16;         // warps per CTA at most (sizes the tile arrays)
+
+template <int D, int NW, int S>
+struct BG {
+    static constexpr int ROWB = D * 4;
+    static constexpr int RS = ROWB >= kStageBytes ? 1 : kStageBytes / ROWB;  // rows per stage (divides 32)
+    static constexpr int SB = RS * ROWB;
+    static constexpr int EPL = D / 32;                                      // floats per lane
+    static constexpr int META = NW * S * 8 * RS;                            // uid + len per staged row
+    static constexpr int RING_OFF = (META + 127) / 128 * 128;
+    static constexpr int SMEM = RING_OFF + NW * S * SB;
+    static_assert(32 % RS == 0, "a stage must lie inside one 32-position round");
+    static_assert(EPL == 2 || EPL % 4 == 0, "lane layout: float2 or float4 chunks");
+    static_assert(NW <= kMaxNW, "tile arrays are sized for kMaxNW warps per SM");
+};
+
+// Where the rounded G row of unique u goes (hot-gradient buffer, send layout, or pack layout).
+template <int D>
+__device__ __forceinline__ float *g_dst(const UpdateArgs &a, int32_t u, int32_t u0, float *gp, int lane,
+                                        float nocc) {
+    if (a.hslot) {
+        const int32_t hs = a.hslot[u];
+        if (hs >= 0) {
+            if (lane == 0) a.hot_touch[hs] = nocc;
+            return a.hot_g + a.hot_g_off[a.pack] + (int64_t)(hs - a.hot_pslot[a.pack]) * D;
+        }
+    }
+    return a.row_off ? a.gbuf + a.row_off[u] : gp + (int64_t)(u - u0) * D;
+}
+
+// A lane's elements of a row: D = 64 -> floats [2*lane, 2*lane+2); D >= 128 -> float4 chunks q
+// at floats 128*q + 4*lane (consecutive lanes, consecutive 16 bytes: conflict-free).
+template <int D>
+__device__ __forceinline__ void lane_load(const float *row, int lane, float *v) {
+    constexpr int EPL = D / 32;
+    if constexpr (EPL == 2) {
+        const float2 x = reinterpret_cast<const float2 *>(row)[lane];
+        v[0] = x.x;
+        v[1] = x.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q) {
+            const float4 x = reinterpret_cast<const float4 *>(row)[q * 32 + lane];
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+    }
+}
+template <int D>
+__device__ __forceinline__ void lane_store_f32(float *row, int lane, const double *acc) {
+    constexpr int EPL = D / 32;
+    if constexpr (EPL == 2) {
+        reinterpret_cast<float2 *>(row)[lane] = make_float2(__double2float_rn(acc[0]), __double2float_rn(acc[1]));
+    } else {
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q)
+            reinterpret_cast<float4 *>(row)[q * 32 + lane] =
+                make_float4(__double2float_rn(acc[4 * q]), __double2float_rn(acc[4 * q + 1]),
+                            __double2float_rn(acc[4 * q + 2]), __double2float_rn(acc[4 * q + 3]));
+    }
+}
+template <int D>
+__device__ __forceinline__ void lane_store_f64(double *row, int lane, const double *acc) {
+    constexpr int EPL = D / 32;
+    if constexpr (EPL == 2) {
+        reinterpret_cast<double2 *>(row)[lane] = make_double2(acc[0], acc[1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q) {
+            double2 *o = reinterpret_cast<double2 *>(row + q * 128 + lane * 4);
+            o[0] = make_double2(acc[4 * q], acc[4 * q + 1]);
+            o[1] = make_double2(acc[4 * q + 2], acc[4 * q + 3]);
+        }
+    }
+}
+template <int D>
+__device__ __forceinline__ void lane_load_f64(const double *row, int lane, double *v) {
+    constexpr int EPL = D / 32;
+    if constexpr (EPL == 2) {
+        const double2 x = reinterpret_cast<const double2 *>(row)[lane];
+        v[0] = x.x;
+        v[1] = x.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q) {
+            const double2 *o = reinterpret_cast<const double2 *>(row + q * 128 + lane * 4);
+            const double2 x = o[0], y = o[1];
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = y.x;
+            v[4 * q + 3] = y.y;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Row starts + equal-cost tiles.  Pack p holds sorted positions [G0, G1) = [pack_gstart[p],
+// pack_gstart[p+1]) (uids are pack-major) and rows [U0, U1).  cost(i) = (i - G0) + (su[i] - U0)
+// rises by 1 inside a row and by 2 at a row start; with C = (G1 - G0) + (U1 - U0) and
+// nte = min(nt, C), position i belongs to tile floor(cost(i) * nte / C): tiles never come out
+// empty inside a row, and tiles >= nte are empty at the pack's end.
+__global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const int32_t *pack_gstart,
+                            const int32_t *pack_ustart, int32_t P, int32_t nt, int32_t *tile_start) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int32_t u = su[i];
+    const bool row_start = i == 0 || su[i - 1] != u;
+    if (row_start) ustart[u] = (int32_t)i;
+    if (i == N - 1) ustart[u + 1] = (int32_t)N;
+    int lo = 0, hi = P;  // pack: the last p with pack_ustart[p] <= u
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(pack_ustart + mid) <= u) lo = mid; else hi = mid;
+    }
+    const int64_t G0 = __ldg(pack_gstart + lo), G1 = __ldg(pack_gstart + lo + 1);
+    const int64_t U0 = __ldg(pack_ustart + lo), U1 = __ldg(pack_ustart + lo + 1);
+    const int64_t C = (G1 - G0) + (U1 - U0);
+    const int64_t nte = nt < C ? nt : C;
+    const int64_t cost = (i - G0) + (u - U0);
+    const int64_t k = cost * nte / C;
+    int64_t kprev = -1;
+    if (i > G0) kprev = (cost - (row_start ? 2 : 1)) * nte / C;
+    int32_t *ts = tile_start + (int64_t)lo * (nt + 1);
+    for (int64_t kk = kprev + 1; kk <= k; ++kk) ts[kk] = (int32_t)i;
+    if (i == G1 - 1)
+        for (int64_t kk = k + 1; kk <= nt; ++kk) ts[kk] = (int32_t)G1;
+}
+
+template <int D, int NW, int S>
+__global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
+    using G = BG<D, NW, S>;
+    constexpr int RS = G::RS, SB = G::SB, ROWB = G::ROWB, EPL = G::EPL;
+    extern __shared__ __align__(128) unsigned char smem[];
+    int32_t *s_uid = reinterpret_cast<int32_t *>(smem);
+    int32_t *s_len = s_uid + NW * S * RS;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
+    if (u1 <= u0) return;
+    const int32_t *ts = a.tile_start + (int64_t)a.pack * (a.nt + 1);
+    const int32_t t = blockIdx.x * NW + w;
+    const int32_t pa = __ldg(ts + t), pb = __ldg(ts + t + 1);
+    if (pa >= pb) return;
+
+    int32_t *wu = s_uid + w * S * RS, *wl = s_len + w * S * RS;
+    unsigned char *wr = smem + G::RING_OFF + (size_t)w * S * SB;
+    float *gp = a.gbuf + a.pack_gbase[a.pack];
+    const float4 *dy4 = reinterpret_cast<const float4 *>(a.dy);
+
+    // rows cut by the tile edges leave fp64 partials instead of G
+    const int32_t u_first = __ldg(a.sorted_u + pa), u_last = __ldg(a.sorted_u + pb - 1);
+    const int32_t last_end = __ldg(a.ustart + u_last + 1);
+    const int32_t hp = __ldg(a.ustart + u_first) < pa ? u_first : -1;  // piece -> slot 2t
+    const int32_t tp = (last_end > pb && u_last != hp) ? u_last : -1;   // piece -> slot 2t+1
+    if (lane == 0 && tp >= 0)                                            // the split row starts here
+        a.split[atomicAdd(a.long_cnt, 1)] = make_int4(t, tp, __ldg(a.ustart + tp), last_end);
+    const int32_t nst = (pb - pa + RS - 1) / RS;
+
+    // lane l holds position base + l of a 32-position round: dY row (float4 units), uid, bag length
+    uint32_t off_c, off_n;
+    int32_t uid_c, uid_n, len_c, len_n;
+    auto resolve = [&](int32_t base, uint32_t &off, int32_t &uid, int32_t &len) {
+        const int32_t p = base + lane;
+        off = 0;
+        uid = -1;
+        len = 1;
+        if (p < pb) {
+            const int32_t seg = __ldg(a.sorted_seg + p);
+            uid = __ldg(a.sorted_u + p);
+            const int32_t f = seg / a.B;
+            off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col) >> 2);
+            if (a.pool_mean) len = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
+        }
+    };
+    resolve(pa, off_c, uid_c, len_c);
+    resolve(pa + 32, off_n, uid_n, len_n);
+    int32_t round_c = 0;
+    auto issue = [&](int32_t k) {  // stage k -> ring slot k % S
+        const int slot = k % S;
+        const int32_t r = (k * RS) >> 5;
+        if (r != round_c) {  // stages are issued in order: r == round_c + 1
+            off_c = off_n;
+            uid_c = uid_n;
+            len_c = len_n;
+            round_c = r;
+            resolve(pa + (r + 1) * 32, off_n, uid_n, len_n);
+        }
+        const int32_t p0 = pa + k * RS;
+        const int nrows = pb - p0 < RS ? pb - p0 : RS;
+        const int l0 = (k * RS) & 31;
+        unsigned char *dst = wr + slot * SB;
+#pragma unroll
+        for (int i = 0; i < RS; ++i) {
+            const uint32_t off = __shfl_sync(0xffffffffu, off_c, l0 + i);
+            if (i < nrows) {
+                const float4 *src = dy4 + off;
+                if constexpr (EPL == 2) {
+                    ldgsts(dst + i * ROWB + lane * 8, reinterpret_cast<const float *>(src) + lane * 2, 8);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < EPL / 4; ++q)
+                        ldgsts(dst + i * ROWB + q * 512 + lane * 16, src + q * 32 + lane, 16);
+                }
+            }
+        }
+        const int i = lane - l0;
+        if (i >= 0 && i < nrows) {
+            wu[slot * RS + i] = uid_c;
+            wl[slot * RS + i] = len_c;
+        }
+    };
+
+    double acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.0;
+    int32_t cur = -1, ncur = 0;  // current row, its occurrences in this tile (= all of them if unsplit)
+    auto flush = [&](int32_t u) {
+        double *part = reinterpret_cast<double *>(a.partial);
+        if (u == hp) {
+            lane_store_f64<D>(part + (int64_t)(2 * t) * D, lane, acc);
+        } else if (u == tp) {
+            lane_store_f64<D>(part + (int64_t)(2 * t + 1) * D, lane, acc);
+        } else {
+            lane_store_f32<D>(g_dst<D>(a, u, u0, gp, lane, (float)ncur), lane, acc);
+        }
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = 0.0;
+    };
+
+    // one commit group per stage (empty past the end), so stage k is complete at wait_group(S - 1)
+    for (int32_t k = 0; k < S; ++k) {
+        if (k < nst) issue(k);
+        ldgsts_commit();
+    }
+#pragma unroll 1
+    for (int32_t k = 0; k < nst; ++k) {
+        const int slot = k % S;
+        ldgsts_wait<S - 1>();
+        __syncwarp();  // uid / len of the stage were written by other lanes
+        const int32_t p0 = pa + k * RS;
+        const int nrows = pb - p0 < RS ? pb - p0 : RS;
+        const float *rows = reinterpret_cast<const float *>(wr + slot * SB);
+        float v[RS][EPL];
+#pragma unroll
+        for (int i = 0; i < RS; ++i)
+            if (i < nrows) lane_load<D>(rows + i * D, lane, v[i]);
+#pragma unroll
+        for (int i = 0; i < RS; ++i) {
+            if (i < nrows) {
+                const int32_t uid = wu[slot * RS + i];
+                if (uid != cur) {
+                    if (cur >= 0) flush(cur);
+                    cur = uid;
+                    ncur = 0;
+                }
+                ++ncur;
+                if (a.pool_mean) {
+                    const float len = (float)wl[slot * RS + i];
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) v[i][e] = __fdiv_rn(v[i][e], len);
+                }
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) acc[e] = __dadd_rn(acc[e], (double)v[i][e]);
+            }
+        }
+        __syncwarp();  // the slot's uid / len are rewritten by the next issue
+        if (k + S < nst) issue(k + S);
+        ldgsts_commit();
+    }
+    if (cur >= 0) flush(cur);
+}
+
+// One CTA per listed split row: its pieces (j = 0: slot 2t+1 of its first tile t; j >= 1: slot
+// 2(t+j)) summed in tile order — warp w takes j = w mod 4, the warps combined in order.
+template <int D>
+__global__ void __launch_bounds__(128) k_segsum_fix(UpdateArgs a) {
+    constexpr int EPL = D / 32, NWF = 4;
+    __shared__ double s_acc[NWF][D];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if ((int32_t)blockIdx.x >= *a.long_cnt) return;
+    const int4 e = a.split[blockIdx.x];
+    const int32_t t = e.x, u = e.y, rs = e.z, re = e.w;
+    const int32_t *ts = a.tile_start + (int64_t)a.pack * (a.nt + 1);
+    // the last piece is in the last tile starting before re
+    int32_t tl = t;
+    for (int32_t base = t + 1; base <= a.nt; base += 32) {
+        const int32_t k = base + lane;
+        const bool inside = k <= a.nt && __ldg(ts + k) < re;
+        const unsigned m = __ballot_sync(0xffffffffu, inside);
+        tl = base - 1 + __popc(m);  // tile starts are non-decreasing: the set bits are a prefix
+        if (m != 0xffffffffu) break;
+    }
+    const int32_t npieces = tl - t + 1;
+    const double *part = reinterpret_cast<const double *>(a.partial);
+    double acc[EPL];
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) acc[k] = 0.0;
+#pragma unroll 1
+    for (int32_t j0 = w; j0 < npieces; j0 += NWF * 4) {
+        double v[4][EPL];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t j = j0 + NWF * k;
+            if (j < npieces) lane_load_f64<D>(part + (int64_t)(j == 0 ? 2 * t + 1 : 2 * (t + j)) * D, lane, v[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (j0 + NWF * k < npieces)
+#pragma unroll
+                for (int q = 0; q < EPL; ++q) acc[q] = __dadd_rn(acc[q], v[k][q]);
+    }
+    lane_store_f64<D>(s_acc[w], lane, acc);
+    __syncthreads();
+    if (w == 0) {
+        lane_load_f64<D>(s_acc[0], lane, acc);
+        for (int k = 1; k < NWF; ++k) {
+            double v[EPL];
+            lane_load_f64<D>(s_acc[k], lane, v);
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) acc[q] = __dadd_rn(acc[q], v[q]);
+        }
+        const int32_t u0 = a.pack_ustart[a.pack];
+        float *gp = a.gbuf + a.pack_gbase[a.pack];
+        lane_store_f32<D>(g_dst<D>(a, u, u0, gp, lane, (float)(re - rs)), lane, acc);
+    }
+}
+
+template <int D, int NW, int S>
+void launch_pipe(const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    using G = BG<D, NW, S>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_segsum_pipe<D, NW, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        attr = true;
+    }
+    k_segsum_pipe<D, NW, S><<<(unsigned)num_sms, NW * 32, G::SMEM, s>>>(a);
+    k_segsum_fix<D><<<(unsigned)a.nt, 128, 0, s>>>(a);
+}
+
+template <int D>
+void launch_cfg(int cfg, const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    switch (cfg) {
+        case 1: launch_pipe<D, 12, 4>(a, num_sms, s); break;
+        case 2: launch_pipe<D, 8, 6>(a, num_sms, s); break;
+        case 3: launch_pipe<D, 16, 2>(a, num_sms, s); break;
+        default: launch_pipe<D, 16, 3>(a, num_sms, s); break;
+    }
+}
+
+}  // namespace
+
+// PICASSO_SEGSUM_CFG = 16x3 (default) | 12x4 | 8x6 | 16x2: warps per CTA x ring stages
+int segsum_pipe_cfg() {
+    const char *e = std::getenv("PICASSO_SEGSUM_CFG");
+    if (!e) return 0;
+    if (!std::strcmp(e, "12x4")) return 1;
+    if (!std::strcmp(e, "8x6")) return 2;
+    if (!std::strcmp(e, "16x2")) return 3;
+    return 0;
+}
+int segsum_pipe_warps(int cfg) { return cfg == 1 ? 12 : cfg == 2 ? 8 : 16; }
+
+bool segsum_bulk_supported(int D, const UpdateArgs &a) {
+    const bool dim_ok = D == 64 || D == 128 || D == 256 || D == 384 || D == 512;
+    return dim_ok && a.gbuf && a.tile_start && ((uintptr_t)a.dy & 15) == 0 && (a.dy_stride & 3) == 0;
+}
+
+int launch_segsum_bulk(int cfg, int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    switch (D) {
+        case 64: launch_cfg<64>(cfg, a, num_sms, s); break;
+        case 128: launch_cfg<128>(cfg, a, num_sms, s); break;
+        case 256: launch_cfg<256>(cfg, a, num_sms, s); break;
+        case 384: launch_cfg<384>(cfg, a, num_sms, s); break;
+        case 512: launch_cfg<512>(cfg, a, num_sms, s); break;
+        default: return 0;
+    }
+    return 2;
+}
+
+void launch_csr_tiles(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt,
+                      const int32_t *pack_gstart, const int32_t *pack_ustart, int32_t P, int32_t nt,
+                      int32_t *tile_start, cudaStream_t s) {
+    cudaMemsetAsync(long_cnt, 0, sizeof(int32_t) * P, s);
+    if (N > 0)
+        k_csr_tiles<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(sorted_u, N, ustart, pack_gstart, pack_ustart, P,
+                                                                nt, tile_start);
+}
+
+size_t segsum_bulk_partial_doubles(int maxD, int num_sms) { return (size_t)2 * num_sms * kMaxNW * maxD; }
+size_t segsum_tile_ints(int P, int num_sms) { return (size_t)P * (num_sms * kMaxNW + 1); }
+size_t segsum_split_entries(int num_sms) { return (size_t)num_sms * kMaxNW; }
+
+}  // namespace picasso

@@ -128,6 +128,9 @@ struct UpdateArgs {
     const int64_t *hot_g_off;    // [P]
     const int32_t *hot_pslot;    // [P+1]
     float *hot_touch;            // [k] occurrences of the hot slot this step
+    const int32_t *tile_start;   // pipelined segsum: [P, nt+1] equal-cost tile starts (nullptr: legacy)
+    int32_t nt;                  //   tiles per pack (= SMs x warps per CTA)
+    int4 *split;                 //   [nt] rows cut by tile edges: {first tile, uid, start, end}
 };
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
@@ -136,5 +139,16 @@ void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int3
 void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 int launch_long_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);  // returns #launches
 size_t long_partial_doubles(int64_t N, int maxD);
+// k_segsum_bulk.cu: bulk-copy pipelined segsum (+ split-row fix-up); returns #launches
+int segsum_pipe_cfg();            // PICASSO_SEGSUM_CFG
+int segsum_pipe_warps(int cfg);    // warps per CTA of that configuration
+bool segsum_bulk_supported(int D, const UpdateArgs &a);
+int launch_segsum_bulk(int cfg, int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
+void launch_csr_tiles(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt,
+                      const int32_t *pack_gstart, const int32_t *pack_ustart, int32_t P, int32_t nt,
+                      int32_t *tile_start, cudaStream_t s);
+size_t segsum_bulk_partial_doubles(int maxD, int num_sms);
+size_t segsum_tile_ints(int P, int num_sms);
+size_t segsum_split_entries(int num_sms);
 
 }  // namespace picasso

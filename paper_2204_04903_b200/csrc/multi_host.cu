@@ -33,6 +33,8 @@ namespace picasso {
 IndexArgs make_index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N);
 UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, const int32_t *su,
                             const int32_t *sseg);
+int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
+void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
 }
 
 static MultiArgs multi_args(picasso_ctx *ctx) {
@@ -272,7 +274,7 @@ picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
     ctx->mark(2, true, s);
     radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N, ctx->splan,
                       ctx->hist0, ctx->hist1, ctx->rowtot, s, &ctx->launches_bwd);
-    launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
+    launch_csr_any(ctx, su, N, s);
     ctx->mark(2, false, s);
     ctx->launches_bwd += N > 0 ? 1 : 0;
     ctx->mark(3, true, s);
@@ -294,8 +296,7 @@ picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
             u.pack = p;
             u.long_cnt = ctx->long_cnt + p;
             u.pack_key_off = ctx->pack_key_off[p];
-            launch_segsum(ctx->pack_dim[p], u, ctx->num_sms, s);
-            ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+            ctx->launches_bwd += launch_segsum_any(ctx, ctx->pack_dim[p], u, s);
         }
     }
     ctx->mark(3, false, s);

@@ -118,10 +118,13 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
         }
     }
     if (const char *e = std::getenv("PICASSO_BWD")) c->split_bwd = std::strcmp(e, "fused") != 0;
-    c->ws_bytes = c->carve(nullptr);
+    if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
+    c->seg_cfg = segsum_pipe_cfg();
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
+    c->seg_nt = c->num_sms * segsum_pipe_warps(c->seg_cfg);
+    c->ws_bytes = c->carve(nullptr);
     *out = c;
     return PICASSO_OK;
 }
@@ -230,6 +233,8 @@ namespace picasso {
 IndexArgs make_index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N);
 UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, const int32_t *su,
                             const int32_t *sseg);
+int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
+void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
 }
 picasso_status multi_fwd_nccl(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
                               float *out, cudaStream_t s);
@@ -342,7 +347,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     ctx->mark(2, true, s);
     radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N, ctx->splan,
                       ctx->hist0, ctx->hist1, ctx->rowtot, s, &ctx->launches_bwd);
-    launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
+    launch_csr_any(ctx, su, N, s);
     ctx->mark(2, false, s);
     ctx->launches_bwd += N > 0 ? 1 : 0;
     ctx->mark(3, true, s);
@@ -356,8 +361,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
             u.state1 = ctx->s1[p];
             u.state2 = ctx->s2[p];
             if (ctx->split_bwd) {
-                launch_segsum(ctx->pack_dim[p], u, ctx->num_sms, s);
-                ctx->launches_bwd += 2 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
+                ctx->launches_bwd += 1 + launch_segsum_any(ctx, ctx->pack_dim[p], u, s);
                 ctx->mark(3, false, s);
                 ctx->mark(5, true, s);
                 launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
@@ -375,6 +379,21 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     ctx->fwd_done = false;
     ctx->last_stream = s;
     return PICASSO_OK;
+}
+
+void picasso::launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s) {
+    if (ctx->bulk_segsum)
+        launch_csr_tiles(su, N, ctx->ustart, ctx->long_cnt, ctx->pack_gstart, ctx->pack_ustart, ctx->P, ctx->seg_nt,
+                         ctx->tile_start, s);
+    else
+        launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
+}
+
+int picasso::launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s) {
+    if (ctx->bulk_segsum && segsum_bulk_supported(D, u))
+        return launch_segsum_bulk(ctx->seg_cfg, D, u, ctx->num_sms, s);
+    launch_segsum(D, u, ctx->num_sms, s);
+    return 1 + launch_long_update(D, u, ctx->num_sms, s);
 }
 
 UpdateArgs picasso::make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step,
@@ -407,6 +426,9 @@ UpdateArgs picasso::make_update_args(picasso_ctx *ctx, const float *grad_out, fl
     u.chunk_row = ctx->chunk_row;
     u.gbuf = ctx->split_bwd ? ctx->gbuf : nullptr;
     u.pack_gbase = ctx->pack_gbase;
+    u.tile_start = ctx->bulk_segsum ? ctx->tile_start : nullptr;
+    u.nt = ctx->seg_nt;
+    u.split = ctx->split;
     return u;
 }
 
