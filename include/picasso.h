@@ -245,6 +245,29 @@ picasso_status picasso_group_bwd_update(picasso_group *group, const float *const
 picasso_status picasso_get_owner_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n);
 picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts);
 
+/* 7. Exchange over NVLink peer memory (kernel-initiated Shuffle&Stitch).
+ * Replaces the NCCL AllToAllv of section 5 with one shared window per rank (barrier flags,
+ * bucket counts, send list, rows / G buffer; cudaMalloc'ed by the library, freed at destroy):
+ * owners read the requested keys from the requesters' send lists, store the gathered rows
+ * straight into the requesters' rows buffers (Gather + Shuffle + Stitch in one kernel), and in
+ * the backward pull the requesters' G rows into the reduce + optimizer kernel.  Sizes stay on
+ * the device (no host synchronisation inside a step: a step can be captured in a CUDA graph);
+ * ranks meet at three device-side barriers per step (system-scope release/acquire flags; a
+ * peer missing for 20 s latches PICASSO_ERR_CUDA "peer timeout" instead of hanging).  Results are
+ * bit-identical to section 5 (same layouts, same source-ordered sums).  HybridHash hot rows
+ * keep their NCCL AllReduce.  Requirements: every rank built with the same plan and max_ids,
+ * one GPU per rank, peer access between the GPUs (NVLink / NVSwitch).
+ *   picasso_p2p_handle : after picasso_bind: allocates this rank's window and writes its CUDA
+ *                        IPC handle (64 bytes) into handle_out (host).
+ *   picasso_p2p_open   : handles = the world ranks' 64-byte handles, rank order (host; own
+ *                        entry ignored); maps the peers' windows.  Collective in effect: every
+ *                        rank must open before any rank steps.
+ *   picasso_group_p2p  : loopback group: the same path with the ranks' windows as plain
+ *                        pointers on one device (no barriers: the host orders the phases). */
+picasso_status picasso_p2p_handle(picasso_ctx *ctx, void *handle_out);
+picasso_status picasso_p2p_open(picasso_ctx *ctx, const void *handles);
+picasso_status picasso_group_p2p(picasso_group *group);
+
 #ifdef __cplusplus
 }
 #endif

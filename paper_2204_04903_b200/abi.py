@@ -22,7 +22,8 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_profile_enable", "picasso_profile_read", "picasso_unique_offsets", "picasso_nccl_unique_id",
            "picasso_group_create", "picasso_group_destroy", "picasso_group_fwd", "picasso_group_bwd_update",
            "picasso_get_owner_unique", "picasso_get_send_counts", "picasso_hot_cache_refresh",
-           "picasso_group_hot_cache_refresh", "picasso_get_hot_keys"]
+           "picasso_group_hot_cache_refresh", "picasso_get_hot_keys", "picasso_p2p_handle", "picasso_p2p_open",
+           "picasso_group_p2p"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -260,6 +261,22 @@ def picasso_profile_read(ctx):
 
 
 # ---- world > 1 ---------------------------------------------------------------------------
+def picasso_p2p_handle(ctx):
+    buf = (C.c_uint8 * 64)()
+    _chk(lib().picasso_p2p_handle(ctx, buf), "picasso_p2p_handle", ctx)
+    return bytes(buf)
+
+
+def picasso_p2p_open(ctx, handles):
+    blob = b"".join(handles)
+    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+    _chk(lib().picasso_p2p_open(ctx, buf), "picasso_p2p_open", ctx)
+
+
+def picasso_group_p2p(group):
+    _chk(lib().picasso_group_p2p(group), "picasso_group_p2p")
+
+
 def picasso_group_create(ctxs):
     arr = (C.c_void_p * len(ctxs))(*[c.value for c in ctxs])
     g = C.c_void_p()

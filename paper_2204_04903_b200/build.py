@@ -65,7 +65,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
         for err in ex.map(run, cmds):
             if verbose and err:
                 print(err)
-    if cmds or not os.path.exists(LIB):
+    stale = not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)
+    if cmds or stale:
         nlib = os.path.join(NCCL, "lib")
         link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-fPIC", "-L", nlib,
                 "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib, "-Xlinker", "--no-undefined"]

@@ -15,6 +15,8 @@
 
 #include "ctx.h"
 
+void p2p_host_counts(picasso_ctx *ctx);  // p2p_host.cu
+
 #define HCK(x)                                                                    \
     do {                                                                          \
         cudaError_t e_ = (x);                                                     \
@@ -223,6 +225,7 @@ picasso_status refresh_place(picasso_ctx *ctx, cudaStream_t s) {
 
 void fill_stats(picasso_ctx *ctx, picasso_cache_stats *st) {
     if (!st) return;
+    p2p_host_counts(ctx);
     MultiState &mp = ctx->mp;
     st->k = mp.hot_k;
     int64_t bytes = 0;

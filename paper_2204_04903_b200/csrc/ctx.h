@@ -12,6 +12,7 @@
 
 #include "kernels.h"
 #include "multi.h"
+#include "p2p.h"
 #include "picasso.h"
 
 using namespace picasso;
@@ -102,6 +103,15 @@ struct MultiState {
     int64_t last_hot_uniques = 0, last_uniques = 0;
     std::vector<int64_t> stage_blk;     // [W+1] owner blocks of the refresh staging (floats)
     int32_t new_k = 0;
+    // ---- NVLink peer-memory exchange (p2p.cu / p2p_host.cu)
+    bool p2p = false;                   // exchanges go through the peers' windows (no NCCL a2av)
+    bool p2p_loop = false;              // loopback group: the host sequences the phases, no barriers
+    char *win = nullptr;                // this rank's IPC window (cudaMalloc)
+    size_t win_bytes = 0, win_bcount = 0, win_keys = 0, win_gbuf = 0;
+    P2PPeers peers{};
+    void *peer_base[kP2PMaxW] = {};     // opened IPC mappings (closed at destroy)
+    uint32_t *epoch_d = nullptr;        // [kP2PPhases]
+    int32_t *R_d = nullptr;             // [1] received keys (device)
 };
 
 struct picasso_ctx {
@@ -120,6 +130,8 @@ struct picasso_ctx {
     bool bound = false;
     FieldInfo *finfo = nullptr;
     int32_t *pm_fields_d = nullptr, *pack_first_k_d = nullptr;
+    int32_t *field_k_d = nullptr;  // [F] index of each field within its pack
+    bool pipe_pool = true;         // PICASSO_POOL=legacy selects the register-staged pool for every D
     int64_t *pack_key_off_d = nullptr;
     int32_t *id_start = nullptr, *gstart_pm = nullptr, *field_gstart = nullptr, *pack_gstart = nullptr;
     int32_t *pack_ustart = nullptr;
@@ -200,6 +212,7 @@ struct picasso_ctx {
         const int64_t nblk = (NR + kTile - 1) / kTile + 1;
         finfo = c.take<FieldInfo>(F);
         pm_fields_d = c.take<int32_t>(F);
+        field_k_d = c.take<int32_t>(F);
         pack_first_k_d = c.take<int32_t>(P + 1);
         pack_key_off_d = c.take<int64_t>(P + 1);
         id_start = c.take<int32_t>(F);
@@ -269,6 +282,8 @@ struct picasso_ctx {
             mp.rsend_off = c.take<int64_t>(RM);
             mp.rows_send = c.take<float>((size_t)RM * maxD);
             osort_hist = c.take<int32_t>(2 * ((RM + kTile - 1) / kTile) + 2);
+            mp.epoch_d = c.take<uint32_t>(kP2PPhases);
+            mp.R_d = c.take<int32_t>(1);
             if (opts.cache_max_bytes > 0) {  // HybridHash
                 const int64_t K = std::max<int64_t>(mp.k_max, 1);
                 const int64_t arena = opts.cache_max_bytes / 4 + 4 * P;

@@ -24,7 +24,10 @@ extern "C" picasso_status picasso_get_owner_unique(picasso_ctx *ctx, int32_t pac
     return PICASSO_OK;
 }
 
+void p2p_host_counts(picasso_ctx *ctx);
+
 extern "C" picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts) {
+    if (ctx && ctx->mp.p2p) p2p_host_counts(ctx);
     if (!ctx || !host_counts || ctx->world < 2 || ctx->mp.sk.empty()) return PICASSO_ERR_INVALID_ARG;
     for (int r = 0; r < ctx->world; ++r) host_counts[r] = ctx->mp.sk[r];
     return PICASSO_OK;

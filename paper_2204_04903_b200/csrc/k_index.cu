@@ -129,12 +129,13 @@ constexpr int kItems = kTile / kTileThreads;  // 8 consecutive positions per thr
 __global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
     using BlockReduce = cub::BlockReduce<int32_t, kTileThreads>;
     __shared__ typename BlockReduce::TempStorage tmp;
+    const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
     int32_t c = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;
-        if (g < a.N) c += (a.table[a.slot_of[g]].minpos == (unsigned int)g);
+        if (g < N) c += (a.table[a.slot_of[g]].minpos == (unsigned int)g);
     }
     const int32_t tot = BlockReduce(tmp).Sum(c);
     if (threadIdx.x == 0) a.blk_cnt[blockIdx.x] = tot;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
 __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
     using BlockScan = cub::BlockScan<int32_t, kTileThreads>;
     __shared__ typename BlockScan::TempStorage tmp;
+    const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
     int32_t slot[kItems];
     bool first[kItems];
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
         first[i] = false;
         slot[i] = 0;
         key[i] = 0;
-        if (g < a.N) {
+        if (g < N) {
             slot[i] = a.slot_of[g];
             const ulonglong2 sv = *reinterpret_cast<const ulonglong2 *>(&a.table[slot[i]]);  // key | minpos,uid
             key[i] = sv.x;
@@ -188,12 +190,13 @@ __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
     const int radix = 1 << a.sort_bits0;
     for (int d = threadIdx.x; d < radix; d += kTileThreads) h[d] = 0;
     __syncthreads();
+    const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;
-        const bool valid = g < a.N;
+        const bool valid = g < N;
         int32_t uid = 0;
         if (valid) {
             uid = a.table[a.slot_of[g]].uid;
@@ -207,8 +210,8 @@ __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
         }
     }
     __syncthreads();
-    const int64_t nblk = (a.N + kTile - 1) / kTile;
-    if (a.N > 0)
+    const int64_t nblk = (N + kTile - 1) / kTile;
+    if (N > 0 && blockIdx.x < nblk)
         for (int d = threadIdx.x; d < radix; d += kTileThreads) a.sort_hist0[(int64_t)d * nblk + blockIdx.x] = h[d];
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // uid ranges of empty packs (and the end)
         int32_t next = *a.d_total;
@@ -226,8 +229,9 @@ __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
     }
 }
 
-__global__ void k_scan_blocks(const int32_t *cnt, int32_t *off, int32_t n, int32_t *total) {
+__global__ void k_scan_blocks(const int32_t *cnt, int32_t *off, int32_t n, int32_t *total, const int32_t *n_dev) {
     // single block, n small (N / 2048): chunked sequential scan with block carry
+    if (n_dev) n = (*n_dev + kTile - 1) / kTile;
     __shared__ int32_t s_carry;
     using BlockScan = cub::BlockScan<int32_t, 1024>;
     __shared__ typename BlockScan::TempStorage tmp;
@@ -249,7 +253,7 @@ void launch_dedup_assign(const IndexArgs &a, cudaStream_t s) {
     const int64_t nb = (a.N + kTile - 1) / kTile;
     if (nb) {
         k_flag_count<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
-        k_scan_blocks<<<1, 1024, 0, s>>>(a.blk_cnt, a.blk_off, (int32_t)nb, a.d_total);
+        k_scan_blocks<<<1, 1024, 0, s>>>(a.blk_cnt, a.blk_off, (int32_t)nb, a.d_total, a.n_dev);
         k_assign<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
     } else {
         cudaMemsetAsync(a.d_total, 0, sizeof(int32_t), s);

@@ -38,6 +38,7 @@ struct IndexArgs {
     int32_t *pack_ustart;          // [P+1]
     const int32_t *pack_dim;       // [P]
     int64_t *pack_gbase;           // [P+1] out: float offset of each pack's G rows (sum U_p * D_p)
+    const int32_t *n_dev;          // if set: the position count lives on the device (N = capacity)
     int32_t sort_bits0;            // digit width of the backward's first radix pass
     int32_t *sort_hist0;           // [radix0, nblk] out: digit-major histogram of that pass
     int *err;
@@ -94,8 +95,16 @@ struct PoolArgs {
     float *out;
     int64_t out_stride;
     int *err;
+    int32_t pack;                // pipelined pool: this pack,
+    const int32_t *pack_gstart;  //   [P+1] its packed positions,
+    const int32_t *field_k;      //   [F] index of each field within its pack
 };
 void launch_pool(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
+// k_pool_pipe.cu: pipelined pool for D >= 64 (needs seg_of from launch_seg_of); returns #launches
+bool pool_pipe_supported(int D, const PoolArgs &a);
+int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
+void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
+                   int32_t *seg_of, cudaStream_t s);
 
 // k_update.cu
 struct UpdateArgs {

@@ -35,7 +35,13 @@ UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, i
                             const int32_t *sseg);
 int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
+int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
 }
+picasso_status hot_update_all(picasso_ctx *ctx, float lr, float ss, cudaStream_t s);
+picasso_status group_fwd_p2p(picasso_group *g, const int64_t *const *ids, const int32_t *const *offsets,
+                             const int32_t *batch, const int64_t *n_ids, float *const *out, cudaStream_t s);
+picasso_status group_bwd_p2p(picasso_group *g, const float *const *grad_out, float lr, int64_t step,
+                             cudaStream_t s);
 
 static MultiArgs multi_args(picasso_ctx *ctx) {
     MultiState &mp = ctx->mp;
@@ -238,27 +244,14 @@ picasso_status mfwd_c(picasso_ctx *ctx, cudaStream_t s) {
 picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s) {
     MultiState &mp = ctx->mp;
     ctx->mark(1, true, s);
-    for (int32_t p = 0; p < ctx->P; ++p) {
+    {
         PoolArgs pa{};
         pa.ids = nullptr;
         pa.offsets = ctx->offsets;
         pa.B = ctx->B;
-        pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
-        pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
-        pa.finfo = ctx->finfo;
-        pa.field_gstart = ctx->field_gstart;
-        pa.id_start = ctx->id_start;
-        pa.seg_of = ctx->seg_of;
         pa.row_off = mp.row_off;
         pa.inverse = ctx->inverse;
-        pa.id_mode = ctx->opts.id_mode;
-        pa.pool_mean = ctx->opts.pool == PICASSO_POOL_MEAN;
-        pa.weight = ctx->gbuf;
-        pa.out = out;
-        pa.out_stride = ctx->out_width;
-        pa.err = ctx->err;
-        launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
-        if ((int64_t)pa.Fp * ctx->B > 0) ctx->launches_fwd += 1;
+        ctx->launches_fwd += launch_pool_all(ctx, pa, out, s);
     }
     ctx->mark(1, false, s);
     MCK(cudaGetLastError());
@@ -303,6 +296,20 @@ picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
     return PICASSO_OK;
 }
 
+// HybridHash replicas: the same update on every rank (after the hot-gradient AllReduce)
+picasso_status hot_update_all(picasso_ctx *ctx, float lr, float ss, cudaStream_t s) {
+    if (ctx->mp.hot_k == 0) return PICASSO_OK;
+    MultiArgs m = multi_args(ctx);
+    for (int32_t p = 0; p < ctx->P; ++p)
+        if (ctx->mp.hot_pslot[p + 1] > ctx->mp.hot_pslot[p]) {
+            launch_hot_update(ctx->pack_dim[p], m, p, ctx->opts.opt, lr, ctx->opts.eps, ctx->opts.beta1,
+                              ctx->opts.beta2, ss, ctx->num_sms, s);
+            ctx->launches_bwd += 1;
+        }
+    MCK(cudaGetLastError());
+    return PICASSO_OK;
+}
+
 // ---- phase F: owner reduce (source order) + optimizer ----------------------------------------
 picasso_status mbwd_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) {
     MultiArgs m = multi_args(ctx);
@@ -314,12 +321,9 @@ picasso_status mbwd_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) 
         launch_owner_update(ctx->pack_dim[p], m, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr,
                             ctx->opts.eps, ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s);
         ctx->launches_bwd += 1;
-        if (ctx->mp.hot_k > 0 && ctx->mp.hot_pslot[p + 1] > ctx->mp.hot_pslot[p]) {  // replicas, same on every rank
-            launch_hot_update(ctx->pack_dim[p], m, p, ctx->opts.opt, lr, ctx->opts.eps, ctx->opts.beta1,
-                              ctx->opts.beta2, ss, ctx->num_sms, s);
-            ctx->launches_bwd += 1;
-        }
     }
+    picasso_status st = hot_update_all(ctx, lr, ss, s);
+    if (st) return st;
     ctx->mark(5, false, s);
     if (ctx->prof) ++ctx->prof_calls;
     MCK(cudaGetLastError());
@@ -397,6 +401,8 @@ static picasso_status hot_allreduce_loop(std::vector<picasso_ctx *> &cs, cudaStr
     return PICASSO_OK;
 }
 
+picasso_status hot_allreduce_group(std::vector<picasso_ctx *> &cs, cudaStream_t s) { return hot_allreduce_loop(cs, s); }
+
 // ------------------------------------------------------------------------------------------
 // Loopback driver: all W ranks in this process, on one device; exchanges are device copies.
 
@@ -466,8 +472,10 @@ extern "C" picasso_status picasso_group_fwd(picasso_group *g, const int64_t *con
         picasso_ctx *c = g->ctx[r];
         if (batch[r] > c->opts.max_batch || n_ids[r] > c->opts.max_ids) return PICASSO_ERR_CAPACITY;
         c->launches_fwd = 0;
+        if (c->mp.p2p) continue;
         if ((st = mfwd_a(c, ids[r], offsets[r], batch[r], n_ids[r], s))) return st;
     }
+    if (g->ctx[0]->mp.p2p) return group_fwd_p2p(g, ids, offsets, batch, n_ids, out, s);
     if ((st = a2av_loop(g, 0, s))) return st;
     for (int r = 0; r < W; ++r)
         if ((st = mfwd_b(g->ctx[r], s))) return st;
@@ -490,8 +498,10 @@ extern "C" picasso_status picasso_group_bwd_update(picasso_group *g, const float
         picasso_ctx *c = g->ctx[r];
         if (!c->fwd_done) return PICASSO_ERR_STATE;
         c->launches_bwd = 0;
+        if (c->mp.p2p) continue;
         if ((st = mbwd_e(c, grad_out[r], lr, step, s))) return st;
     }
+    if (g->ctx[0]->mp.p2p) return group_bwd_p2p(g, grad_out, lr, step, s);
     if ((st = a2av_loop(g, 3, s))) return st;
     if ((st = hot_allreduce_loop(g->ctx, s))) return st;
     for (int r = 0; r < W; ++r)

@@ -1,0 +1,56 @@
+// p2p.h — device-side arguments of the NVLink peer-memory exchange (internal; p2p.cu).
+#pragma once
+#include "kernels.h"
+#include "multi.h"
+
+namespace picasso {
+
+constexpr int kP2PMaxW = 8;                                 // ranks per node at most
+constexpr int kP2PPhases = 4;                               // barrier phases per step
+constexpr unsigned long long kP2PTimeoutNs = 20000000000ull;  // a peer missing for 20 s latches an error
+enum P2PErrBits : int { ERR_PEER_TIMEOUT = 4 };
+
+// One rank's IPC window, seen by everyone (index = rank; own pointers at [rank]).
+struct P2PPeers {
+    uint32_t *flags[kP2PMaxW];     // [kP2PPhases][kP2PMaxW] epoch written by each source rank
+    int32_t *bcount[kP2PMaxW];     // [W*P+1] bucket counts (owner-major, pack), hot bucket last
+    int32_t *send_keys[kP2PMaxW];  // [max_ids] requested local rows, owner-major send layout
+    float *gbuf[kP2PMaxW];         // [max_ids * maxD] rows (fwd) / G rows (bwd), send layout
+};
+
+struct P2PArgs {
+    int32_t W, P, rank;
+    int64_t max_recv;
+    P2PPeers peer;
+    uint32_t *epoch;               // [kP2PPhases] this rank's barrier epochs (device)
+    int *err;
+    const int32_t *pack_dim;       // [P]
+    const int64_t *pack_key_off;   // [P+1]
+    OwnerBlock *oblk;              // [W*P] pack-major (p, src): ostart, rstart = key index in src's
+                                   //   send list, rroff = float offset of the row slot in src's gbuf
+    int64_t *pack_ostart;          // [P+1] owner-stream start of each pack
+    int32_t *opack_gstart;         // [P+1] same, int32, for the index kernels
+    int32_t *R;                    // [1] received keys
+    int32_t *cnt_recv;             // [W*P] received counts (source, pack), introspection
+    int32_t *lrow;                 // [max_recv] local row per owner position
+    int32_t *osrc;                 // [max_recv] source rank per owner position
+    int64_t *roff;                 // [max_recv] float offset of the row slot in the source's gbuf
+    int32_t *oslot;                // [max_recv]
+    const int32_t *oinv;           // [max_recv] owner-unique index per owner position
+    int32_t *contrib;              // [max_recv * W] owner position of each (owner-unique, source)
+    const unsigned long long *ouid_key;
+    const int32_t *opack_ustart;   // [P+1]
+    uint32_t *fcnt;                // HybridHash FCounter of owned rows (nullptr: off)
+    const int64_t *fcnt_off;
+};
+
+void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s);
+void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s);
+void launch_p2p_blocks(const P2PArgs &a, cudaStream_t s);
+void launch_p2p_insert(const P2PArgs &a, Slot *table, uint32_t cap_mask, cudaStream_t s);
+void launch_p2p_contrib(const P2PArgs &a, int num_sms, cudaStream_t s);
+void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s);
+void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
+                       float b1, float b2, float ss, int num_sms, cudaStream_t s);
+
+}  // namespace picasso

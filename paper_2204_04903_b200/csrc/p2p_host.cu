@@ -1,0 +1,314 @@
+// p2p_host.cu — host orchestration of the row-sharded step over NVLink peer memory.
+//
+//   fwd:  A  dedup + Partition (multi_host.cu)                 -> barrier 0 (send lists ready)
+//         C' owner: block table from the peers' counts, keys read from the requesters' send
+//            lists, dedup, rows stored into the requesters' rows buffers -> barrier 1
+//         D  pool from the local rows buffer (multi_host.cu)
+//   bwd:  E  transpose + segment-sum, G rows into the local rows buffer -> barrier 2
+//         (HybridHash hot rows: AllReduce as in the NCCL driver)
+//         F' owner: G rows pulled from the requesters, reduced in source order, optimizer
+// No host synchronisation inside the step (sizes live on the device), so a step can be captured
+// in a CUDA graph.  Barrier 0 also orders every owner's F' pulls of the previous step before
+// any rank's buffers are rewritten (a rank signals it only after its own F').  Windows are
+// exchanged with CUDA IPC handles (one process per GPU) or, for the loopback group, are plain
+// pointers on one device (the host then runs each phase for every rank before the next one,
+// which is the barrier).
+#include "ctx.h"
+
+#define PCK(x)                                                                    \
+    do {                                                                          \
+        cudaError_t e_ = (x);                                                     \
+        if (e_ != cudaSuccess) {                                                  \
+            ctx->last_msg = std::string(#x ": ") + cudaGetErrorString(e_);        \
+            return PICASSO_ERR_CUDA;                                              \
+        }                                                                         \
+    } while (0)
+#define PNCK(x)                                                                   \
+    do {                                                                          \
+        ncclResult_t r_ = (x);                                                    \
+        if (r_ != ncclSuccess) {                                                  \
+            ctx->last_msg = std::string(#x ": ") + ncclGetErrorString(r_);        \
+            return PICASSO_ERR_NCCL;                                              \
+        }                                                                         \
+    } while (0)
+
+// phases shared with the NCCL driver (multi_host.cu)
+picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
+                      cudaStream_t s);
+picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s);
+picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
+picasso_status hot_allreduce_group(std::vector<picasso_ctx *> &cs, cudaStream_t s);
+picasso_status hot_update_all(picasso_ctx *ctx, float lr, float ss, cudaStream_t s);
+
+namespace {
+
+int max_dim(const picasso_ctx *ctx) {
+    int maxD = 4;
+    for (int32_t d : ctx->pack_dim) maxD = std::max(maxD, d);
+    return maxD;
+}
+
+constexpr size_t kFlagBytes = sizeof(uint32_t) * kP2PPhases * kP2PMaxW;
+
+// window: [flags | bcount | send_keys | gbuf], the same layout on every rank (same plan, max_ids)
+void window_layout(picasso_ctx *ctx) {
+    MultiState &mp = ctx->mp;
+    const int64_t N = std::max<int64_t>(ctx->opts.max_ids, 1);
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    size_t o = up(kFlagBytes);
+    mp.win_bcount = o;
+    o = up(o + sizeof(int32_t) * kMaxRadix);
+    mp.win_keys = o;
+    o = up(o + sizeof(int32_t) * N);
+    mp.win_gbuf = o;
+    o = up(o + sizeof(float) * (size_t)N * max_dim(ctx));
+    mp.win_bytes = o;
+}
+
+void set_peer(picasso_ctx *ctx, int q, char *base) {
+    MultiState &mp = ctx->mp;
+    mp.peers.flags[q] = reinterpret_cast<uint32_t *>(base);
+    mp.peers.bcount[q] = reinterpret_cast<int32_t *>(base + mp.win_bcount);
+    mp.peers.send_keys[q] = reinterpret_cast<int32_t *>(base + mp.win_keys);
+    mp.peers.gbuf[q] = reinterpret_cast<float *>(base + mp.win_gbuf);
+}
+
+// allocate this rank's window and move the shared buffers (bucket counts, send list, rows / G
+// buffer) into it
+picasso_status window_alloc(picasso_ctx *ctx) {
+    MultiState &mp = ctx->mp;
+    if (mp.win) return PICASSO_OK;
+    window_layout(ctx);
+    PCK(cudaMalloc(&mp.win, mp.win_bytes));
+    PCK(cudaMemset(mp.win, 0, mp.win_bcount));
+    set_peer(ctx, ctx->rank, mp.win);
+    mp.bcount = mp.peers.bcount[ctx->rank];
+    mp.send_keys = mp.peers.send_keys[ctx->rank];
+    ctx->gbuf = mp.peers.gbuf[ctx->rank];
+    PCK(cudaMemset(mp.epoch_d, 0, sizeof(uint32_t) * kP2PPhases));
+    return PICASSO_OK;
+}
+
+P2PArgs make_p2p_args(picasso_ctx *ctx) {
+    MultiState &mp = ctx->mp;
+    P2PArgs a{};
+    a.W = ctx->world;
+    a.P = ctx->P;
+    a.rank = ctx->rank;
+    a.max_recv = mp.max_recv;
+    a.peer = mp.peers;
+    a.epoch = mp.epoch_d;
+    a.err = ctx->err;
+    a.pack_dim = ctx->pack_dim_d;
+    a.pack_key_off = ctx->pack_key_off_d;
+    a.oblk = mp.oblk_d;
+    a.pack_ostart = mp.opack_ostart_d;
+    a.opack_gstart = mp.opack_gstart;
+    a.R = mp.R_d;
+    a.cnt_recv = mp.cnt_recv_d;
+    a.lrow = mp.recv_keys;
+    a.osrc = mp.opos_map;
+    a.roff = mp.rsend_off;
+    a.oslot = mp.oslot;
+    a.oinv = mp.oinv;
+    a.contrib = mp.contrib;
+    a.ouid_key = mp.ouid_key;
+    a.opack_ustart = mp.opack_ustart;
+    a.fcnt = ctx->opts.cache_max_bytes > 0 ? mp.fcnt : nullptr;
+    a.fcnt_off = mp.fcnt_off_d;
+    return a;
+}
+
+void barrier(picasso_ctx *ctx, int phase, cudaStream_t s) {
+    if (ctx->mp.p2p_loop) return;
+    const P2PArgs a = make_p2p_args(ctx);
+    launch_p2p_signal(a, phase, s);
+    launch_p2p_wait(a, phase, s);
+    ctx->launches_fwd += 2;
+}
+
+// ---- C': owner side --------------------------------------------------------------------------
+picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
+    MultiState &mp = ctx->mp;
+    const int P = ctx->P;
+    const P2PArgs a = make_p2p_args(ctx);
+    const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
+    ctx->mark(4, true, s);
+    launch_p2p_blocks(a, s);
+    const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)RM * 2));
+    PCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+    launch_p2p_insert(a, ctx->table, cap_step - 1, s);
+    IndexArgs ia{};  // owner dedup: the index kernels on the owner stream, sizes on the device
+    ia.N = RM;
+    ia.n_dev = mp.R_d;
+    ia.P = P;
+    ia.table = ctx->table;
+    ia.slot_of = mp.oslot;
+    ia.blk_cnt = ctx->blk_cnt;
+    ia.blk_off = ctx->blk_off;
+    ia.d_total = mp.od_total;
+    ia.unique_gkey = mp.ouid_key;
+    ia.pack_gstart = mp.opack_gstart;
+    ia.pack_ustart = mp.opack_ustart;
+    ia.inverse = mp.oinv;
+    ia.pack_dim = ctx->pack_dim_d;
+    ia.pack_gbase = mp.ogbase_scratch;
+    ia.sort_bits0 = 1;
+    ia.sort_hist0 = ctx->osort_hist;
+    ia.err = ctx->err;
+    launch_dedup_assign(ia, s);
+    PCK(cudaMemsetAsync(mp.contrib, 0xFF, sizeof(int32_t) * RM * ctx->world, s));
+    launch_p2p_contrib(a, ctx->num_sms, s);
+    for (int p = 0; p < P; ++p) launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
+    ctx->mark(4, false, s);
+    ctx->launches_fwd += 2 + 4 + 1 + P;
+    PCK(cudaGetLastError());
+    return PICASSO_OK;
+}
+
+// ---- F': owner reduce (pulled G rows, source order) + optimizer -------------------------------
+picasso_status p2p_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) {
+    const P2PArgs a = make_p2p_args(ctx);
+    const double bc1 = 1.0 - std::pow((double)ctx->opts.beta1, (double)step);
+    const double bc2 = 1.0 - std::pow((double)ctx->opts.beta2, (double)step);
+    const float ss = (float)((double)lr * std::sqrt(bc2) / bc1);
+    ctx->mark(5, true, s);
+    for (int32_t p = 0; p < ctx->P; ++p) {
+        launch_p2p_update(ctx->pack_dim[p], a, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr,
+                          ctx->opts.eps, ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s);
+        ctx->launches_bwd += 1;
+    }
+    picasso_status st = hot_update_all(ctx, lr, ss, s);
+    if (st) return st;
+    ctx->mark(5, false, s);
+    if (ctx->prof) ++ctx->prof_calls;
+    PCK(cudaGetLastError());
+    ctx->fwd_done = false;
+    ctx->last_stream = s;
+    return PICASSO_OK;
+}
+
+}  // namespace
+
+// ---- drivers ---------------------------------------------------------------------------------
+picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
+                             float *out, cudaStream_t s) {
+    picasso_status st;
+    if ((st = mfwd_a(ctx, ids, offsets, B, N, s))) return st;
+    barrier(ctx, 0, s);
+    if ((st = p2p_c(ctx, s))) return st;
+    barrier(ctx, 1, s);
+    return mfwd_d(ctx, out, s);
+}
+
+picasso_status multi_bwd_p2p(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s) {
+    picasso_status st;
+    MultiState &mp = ctx->mp;
+    if ((st = mbwd_e(ctx, grad_out, lr, step, s))) return st;
+    barrier(ctx, 2, s);
+    if (mp.hot_k > 0) {  // HybridHash: hot-row gradients and occurrence counts summed over ranks
+        PNCK(ncclGroupStart());
+        PNCK(ncclAllReduce(mp.hot_g, mp.hot_g, mp.hot_g_floats, ncclFloat32, ncclSum, mp.comm, s));
+        PNCK(ncclAllReduce(mp.hot_touch, mp.hot_touch, mp.hot_k, ncclFloat32, ncclSum, mp.comm, s));
+        PNCK(ncclGroupEnd());
+    }
+    return p2p_f(ctx, lr, step, s);
+}
+
+picasso_status group_fwd_p2p(picasso_group *g, const int64_t *const *ids, const int32_t *const *offsets,
+                             const int32_t *batch, const int64_t *n_ids, float *const *out, cudaStream_t s) {
+    const int W = (int)g->ctx.size();
+    picasso_status st;
+    for (int r = 0; r < W; ++r)
+        if ((st = mfwd_a(g->ctx[r], ids[r], offsets[r], batch[r], n_ids[r], s))) return st;
+    for (int r = 0; r < W; ++r)
+        if ((st = p2p_c(g->ctx[r], s))) return st;
+    for (int r = 0; r < W; ++r)
+        if ((st = mfwd_d(g->ctx[r], out[r], s))) return st;
+    return PICASSO_OK;
+}
+
+picasso_status group_bwd_p2p(picasso_group *g, const float *const *grad_out, float lr, int64_t step,
+                             cudaStream_t s) {
+    const int W = (int)g->ctx.size();
+    picasso_status st;
+    for (int r = 0; r < W; ++r)
+        if ((st = mbwd_e(g->ctx[r], grad_out[r], lr, step, s))) return st;
+    if ((st = hot_allreduce_group(g->ctx, s))) return st;
+    for (int r = 0; r < W; ++r)
+        if ((st = p2p_f(g->ctx[r], lr, step, s))) return st;
+    return PICASSO_OK;
+}
+
+// ---- C ABI: window exchange ------------------------------------------------------------------
+extern "C" picasso_status picasso_p2p_handle(picasso_ctx *ctx, void *handle_out) {
+    if (!ctx || !handle_out || ctx->world < 2 || !ctx->bound || ctx->mp.group) return PICASSO_ERR_INVALID_ARG;
+    picasso_status st = window_alloc(ctx);
+    if (st) return st;
+    cudaIpcMemHandle_t h;
+    PCK(cudaIpcGetMemHandle(&h, ctx->mp.win));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_p2p_open(picasso_ctx *ctx, const void *handles) {
+    if (!ctx || !handles || ctx->world < 2 || !ctx->mp.win || ctx->mp.p2p) return PICASSO_ERR_INVALID_ARG;
+    MultiState &mp = ctx->mp;
+    for (int q = 0; q < ctx->world; ++q) {
+        if (q == ctx->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char *>(handles) + (size_t)q * sizeof(h), sizeof(h));
+        void *base = nullptr;
+        PCK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        mp.peer_base[q] = base;
+        set_peer(ctx, q, static_cast<char *>(base));
+    }
+    mp.p2p = true;
+    mp.p2p_loop = false;
+    PCK(cudaDeviceSynchronize());
+    return PICASSO_OK;
+}
+
+extern "C" picasso_status picasso_group_p2p(picasso_group *g) {
+    if (!g || g->ctx.empty()) return PICASSO_ERR_INVALID_ARG;
+    for (auto *ctx : g->ctx) {
+        picasso_status st = window_alloc(ctx);
+        if (st) return st;
+    }
+    for (auto *ctx : g->ctx) {
+        for (auto *peer : g->ctx) set_peer(ctx, peer->rank, peer->mp.win);
+        ctx->mp.p2p = true;
+        ctx->mp.p2p_loop = true;
+    }
+    return PICASSO_OK;
+}
+
+void p2p_release(picasso_ctx *ctx) {
+    MultiState &mp = ctx->mp;
+    for (int q = 0; q < kP2PMaxW; ++q)
+        if (mp.peer_base[q]) {
+            cudaIpcCloseMemHandle(mp.peer_base[q]);
+            mp.peer_base[q] = nullptr;
+        }
+    if (mp.win) cudaFree(mp.win);
+    mp.win = nullptr;
+    mp.p2p = false;
+}
+
+// host view of this step's send counts (the P2P step never synchronises for them)
+void p2p_host_counts(picasso_ctx *ctx) {
+    MultiState &mp = ctx->mp;
+    if (!mp.p2p || !mp.cnt_send_h) return;
+    cudaStreamSynchronize(ctx->last_stream);
+    const int W = ctx->world, P = ctx->P;
+    mp.sk.assign(W, 0);
+    int64_t tot = 0;
+    for (int r = 0; r < W; ++r)
+        for (int p = 0; p < P; ++p) {
+            mp.sk[r] += mp.cnt_send_h[r * P + p];
+            tot += mp.cnt_send_h[r * P + p];
+        }
+    mp.last_hot_uniques = mp.hot_k > 0 ? mp.cnt_send_h[W * P] : 0;
+    mp.last_uniques = tot + mp.last_hot_uniques;
+    mp.U_send = tot;
+}

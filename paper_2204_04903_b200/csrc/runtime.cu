@@ -9,6 +9,8 @@
 
 #include "ctx.h"
 
+void p2p_release(picasso_ctx *ctx);  // p2p_host.cu
+
 #define CK(x)                                                             \
     do {                                                                  \
         cudaError_t e_ = (x);                                             \
@@ -120,6 +122,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_BWD")) c->split_bwd = std::strcmp(e, "fused") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     c->seg_cfg = segsum_pipe_cfg();
+    if (const char *e = std::getenv("PICASSO_POOL")) c->pipe_pool = std::strcmp(e, "legacy") != 0;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
@@ -175,6 +178,13 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemcpy(ctx->finfo, fi.data(), sizeof(FieldInfo) * ctx->F, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pm_fields_d, ctx->pm_fields.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_first_k_d, ctx->pack_first_k.data(), sizeof(int32_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
+    {
+        std::vector<int32_t> fk(ctx->F);
+        for (int32_t p = 0; p < ctx->P; ++p)
+            for (int32_t k = ctx->pack_first_k[p]; k < ctx->pack_first_k[p + 1]; ++k)
+                fk[ctx->pm_fields[k]] = k - ctx->pack_first_k[p];
+        CK(cudaMemcpy(ctx->field_k_d, fk.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_dim_d, ctx->pack_dim.data(), sizeof(int32_t) * ctx->P, cudaMemcpyHostToDevice));
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
@@ -217,6 +227,7 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
 
 extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
     if (!ctx) return PICASSO_OK;
+    p2p_release(ctx);
     if (ctx->mp.comm) ncclCommDestroy(ctx->mp.comm);
     if (ctx->mp.cnt_send_h) {
         cudaFreeHost(ctx->mp.cnt_send_h);
@@ -235,10 +246,14 @@ UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, i
                             const int32_t *sseg);
 int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
+int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
 }
 picasso_status multi_fwd_nccl(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
                               float *out, cudaStream_t s);
 picasso_status multi_bwd_nccl(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
+picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
+                             float *out, cudaStream_t s);
+picasso_status multi_bwd_p2p(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
 
 static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N) {
     return picasso::make_index_args(ctx, ids, offsets, B, N);
@@ -289,7 +304,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     ctx->launches_fwd = 0;
     if (ctx->world > 1) {
         if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_fwd
-        return multi_fwd_nccl(ctx, ids, offsets, batch, n_ids, out, s);
+        return ctx->mp.p2p ? multi_fwd_p2p(ctx, ids, offsets, batch, n_ids, out, s)
+                           : multi_fwd_nccl(ctx, ids, offsets, batch, n_ids, out, s);
     }
     IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
     const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
@@ -302,25 +318,12 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     ctx->mark(0, false, s);
     ctx->launches_fwd += 1 + (n_ids > 0 ? 4 : 0) + 1;  // prep, insert+flag+scan+assign, inverse
     ctx->mark(1, true, s);
-    for (int32_t p = 0; p < ctx->P; ++p) {
+    {
         PoolArgs pa{};
         pa.ids = ids;
         pa.offsets = offsets;
         pa.B = batch;
-        pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
-        pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
-        pa.finfo = ctx->finfo;
-        pa.field_gstart = ctx->field_gstart;
-        pa.id_start = ctx->id_start;
-        pa.seg_of = ctx->seg_of;
-        pa.id_mode = ctx->opts.id_mode;
-        pa.pool_mean = ctx->opts.pool == PICASSO_POOL_MEAN;
-        pa.weight = ctx->w[p];
-        pa.out = out;
-        pa.out_stride = ctx->out_width;
-        pa.err = ctx->err;
-        launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
-        if ((int64_t)pa.Fp * batch > 0) ctx->launches_fwd += 1;
+        ctx->launches_fwd += launch_pool_all(ctx, pa, out, s);
     }
     ctx->mark(1, false, s);
     CK(cudaGetLastError());
@@ -340,7 +343,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     ctx->launches_bwd = 0;
     if (ctx->world > 1) {
         if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_bwd_update
-        return multi_bwd_nccl(ctx, grad_out, lr, step, s);
+        return ctx->mp.p2p ? multi_bwd_p2p(ctx, grad_out, lr, step, s) : multi_bwd_nccl(ctx, grad_out, lr, step, s);
     }
     const int64_t N = ctx->N;
     int32_t *su = nullptr, *sseg = nullptr;
@@ -387,6 +390,43 @@ void picasso::launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cud
                          ctx->tile_start, s);
     else
         launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
+}
+
+// Gather + Stitch + pool of every pack (base: ids / offsets / B, plus row_off / inverse at W > 1,
+// where the rows come from the received-rows buffer instead of the local tables).
+int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s) {
+    int n = 0;
+    pa.finfo = ctx->finfo;
+    pa.field_gstart = ctx->field_gstart;
+    pa.id_start = ctx->id_start;
+    pa.seg_of = ctx->seg_of;
+    pa.id_mode = ctx->opts.id_mode;
+    pa.pool_mean = ctx->opts.pool == PICASSO_POOL_MEAN;
+    pa.out = out;
+    pa.out_stride = ctx->out_width;
+    pa.err = ctx->err;
+    pa.pack_gstart = ctx->pack_gstart;
+    pa.field_k = ctx->pipe_pool ? ctx->field_k_d : nullptr;
+    bool seg_done = false;
+    for (int32_t p = 0; p < ctx->P; ++p) {
+        pa.pack = p;
+        pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
+        pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
+        pa.weight = pa.row_off ? ctx->gbuf : ctx->w[p];
+        if ((int64_t)pa.Fp * pa.B == 0) continue;
+        if (pool_pipe_supported(ctx->pack_dim[p], pa)) {
+            if (!seg_done) {
+                launch_seg_of(pa.offsets, pa.B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
+                seg_done = true;
+                ++n;
+            }
+            n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->num_sms, s);
+        } else {
+            launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
+            ++n;
+        }
+    }
+    return n;
 }
 
 int picasso::launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s) {

@@ -8,6 +8,13 @@ import torch
 from . import abi
 
 
+def default_exchange():
+    """PICASSO_EXCHANGE = p2p (default) | nccl: how a row-sharded step exchanges keys / rows / G."""
+    import os
+
+    return os.environ.get("PICASSO_EXCHANGE", "p2p")
+
+
 class PackedEmbedding:
     """One rank of the packed multi-field embedding layer.
 
@@ -19,7 +26,7 @@ class PackedEmbedding:
     def __init__(self, field_to_table, table_rows, table_dim, *, max_batch, max_ids, table_salt=None,
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
-                 init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0):
+                 init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange=None, all_gather=None):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -50,6 +57,20 @@ class PackedEmbedding:
             self.state2 = [torch.zeros_like(w) for w in self.weights]
         abi.picasso_bind(self.ctx, self.workspace, self.weights, self.state1, self.state2)
         self.step = 0
+        # world > 1, one process per GPU: the exchange runs over NVLink peer memory ("p2p", the
+        # default) or NCCL AllToAllv ("nccl").  all_gather(bytes) -> [bytes] * world shares the
+        # windows' IPC handles (default: torch.distributed.all_gather_object).
+        self.exchange = exchange or default_exchange()
+        if world > 1 and nccl_uid is not None and self.exchange == "p2p":
+            h = abi.picasso_p2p_handle(self.ctx)
+            if all_gather is None:
+                import torch.distributed as dist
+
+                def all_gather(x):
+                    out = [None] * world
+                    dist.all_gather_object(out, x)
+                    return out
+            abi.picasso_p2p_open(self.ctx, all_gather(h))
 
     @property
     def n_packs(self):
@@ -116,15 +137,19 @@ class PackedEmbedding:
 
 
 class LoopbackGroup:
-    """W ranks of the row-sharded layer in ONE process on one device (nccl_uid = None): the
-    exchanges of the step are device copies between the ranks' buffers.  Used to test the
-    sharded path at W up to 8 with a single GPU; the arithmetic is the same kernels as NCCL mode."""
+    """W ranks of the row-sharded layer in ONE process on one device (nccl_uid = None).  With
+    exchange="p2p" the step runs the peer-memory kernels on the ranks' windows (plain pointers,
+    the host ordering the phases); with "nccl" the exchanges are device copies between the ranks'
+    buffers.  Used to test the sharded path at W up to 8 with a single GPU."""
 
-    def __init__(self, world, field_to_table, table_rows, table_dim, **kw):
+    def __init__(self, world, field_to_table, table_rows, table_dim, exchange=None, **kw):
         self.world = world
         self.ranks = [PackedEmbedding(field_to_table, table_rows, table_dim, rank=r, world=world, **kw)
                       for r in range(world)]
         self.group = abi.picasso_group_create([e.ctx for e in self.ranks])
+        self.exchange = exchange or default_exchange()
+        if self.exchange == "p2p":  # the peer-memory kernels, windows as plain pointers
+            abi.picasso_group_p2p(self.group)
 
     def forward(self, ids, offsets, batch, outs=None, stream=None):
         if outs is None:

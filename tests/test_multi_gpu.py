@@ -1,6 +1,7 @@
 """Row-sharded path (world W > 1) against the oracle, W = 2, 4, 8 ranks driven in one process on
-one GPU through the loopback group (the exchanges are device copies; every kernel is the one the
-NCCL path runs).  Checked per rank: forward bit-exact; unique keys, per-owner send counts and the
+one GPU through the loopback group, with both exchanges: the peer-memory kernels (the ranks'
+windows as plain pointers) and the staged AllToAllv (device copies; every other kernel is the one
+the NCCL path runs).  Checked per rank: forward bit-exact; unique keys, per-owner send counts and the
 owner-side unique rows (first occurrence over the received lists concatenated by source rank)
 bit-exact; after the backward, every rank's table shard equals the oracle's global-batch update
 (bit-exact under dyadic dY, 1e-5 / 1e-6 otherwise)."""
@@ -21,6 +22,14 @@ def _build():
     import __graft_entry__
 
     __graft_entry__.build()
+
+
+@pytest.fixture(params=["p2p", "nccl"], autouse=True)
+def exchange(request, monkeypatch):
+    """Both exchange implementations: the peer-memory kernels (windows as plain pointers) and the
+    staged AllToAllv (device copies in loopback)."""
+    monkeypatch.setenv("PICASSO_EXCHANGE", request.param)
+    return request.param
 
 
 def make_group(cfg, W, opt=0, max_ids=None):

@@ -1,5 +1,5 @@
-"""NCCL row-sharded parity: one process per GPU (torchrun), real grouped send/recv over
-NVLink.  Needs >= 2 GPUs (skipped otherwise; the loopback tests cover W up to 8 on one GPU)."""
+"""Row-sharded parity with one process per GPU (torchrun): the NVLink peer-memory exchange
+(CUDA IPC windows) and the NCCL grouped send/recv.  Needs >= 2 GPUs (skipped otherwise; the loopback tests cover W up to 8 on one GPU)."""
 import os
 import subprocess
 import sys
@@ -11,8 +11,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("name", ["toy", "wdl", "toy_cache", "wdl_cache"])
-def test_nccl_sharded_parity(name):
+def test_nccl_sharded_parity(name, exchange):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -22,5 +23,6 @@ def test_nccl_sharded_parity(name):
     W = 4 if n >= 4 else 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "nccl_worker.py"), name]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = {**os.environ, "PICASSO_EXCHANGE": exchange}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

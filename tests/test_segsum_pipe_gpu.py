@@ -12,7 +12,7 @@ import torch
 import oracle
 from datagen import configs as dc
 from datagen import make_batch, make_dy
-from harness import assert_close, gpu_embedding, gpu_table_rows, to_dev
+from harness import assert_close, gpu_embedding, gpu_table_rows, oracle_model, oracle_tables, to_dev
 from test_parity_gpu import run_step
 
 pytestmark = pytest.mark.gpu
@@ -90,3 +90,47 @@ def test_pipe_equals_legacy(dyadic):
             assert np.array_equal(res[0][t], res[1][t]), f"table {t}"
         else:
             assert_close(res[1][t], res[0][t], what=f"table {t}")
+
+
+# ---- pipelined pool (csrc/k_pool_pipe.cu) -------------------------------------------------------
+def _fwd(cfg, env=None, step=1):
+    if env:
+        os.environ.update(env)
+    try:
+        emb = gpu_embedding(cfg)
+    finally:
+        for k in env or {}:
+            os.environ.pop(k, None)
+    b = make_batch(cfg, 0, step)
+    ids, off = to_dev(b)
+    return emb.forward(ids, off, cfg.batch).cpu().numpy(), b
+
+
+@pytest.mark.parametrize("name", ["wdl", "criteo", "mixed"])
+def test_pool_pipe_equals_legacy_and_oracle(name):
+    """Pipelined pool == legacy pool == oracle, bit-exact (sequential fp32 per segment)."""
+    if name == "wdl":
+        cfg = dc.scaled(dc.wdl(), batch=96, rows_div=1000)
+    elif name == "criteo":
+        cfg = dc.scaled(dc.criteo(), batch=512, rows_div=100)
+    else:  # D = 64 / 128 / 256 packs, one field of all-empty bags, bags 0..50 elsewhere
+        cfg = dc.toy(batch=300).replace(
+            table_rows=np.array([50, 7, 900, 3, 20], np.int64), table_dim=np.array([64, 128, 256, 128, 64], np.int32),
+            field_to_table=np.arange(5, dtype=np.int32),
+            bags=[("uniform", 0, 50), ("fixed", 0), ("uniform", 1, 3), ("fixed", 1), ("uniform", 0, 2)])
+    got, b = _fwd(cfg)
+    leg, _ = _fwd(cfg, {"PICASSO_POOL": "legacy"})
+    assert np.array_equal(got, leg)
+    m, tabs = oracle_model(cfg), oracle_tables(cfg)
+    ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, None)
+    assert np.array_equal(got, oracle.forward(m, ob, tabs, cfg.out_width))
+
+
+def test_pool_pipe_mean_and_all_empty_pack():
+    cfg = dc.toy(batch=200, pool=dc.POOL_MEAN).replace(
+        table_rows=np.array([10, 10, 500], np.int64), table_dim=np.array([128, 256, 128], np.int32),
+        field_to_table=np.arange(3, dtype=np.int32), bags=[("uniform", 0, 9), ("fixed", 0), ("uniform", 0, 1)])
+    got, b = _fwd(cfg)
+    m, tabs = oracle_model(cfg), oracle_tables(cfg)
+    ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, None)
+    assert np.array_equal(got, oracle.forward(m, ob, tabs, cfg.out_width))
