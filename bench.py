@@ -226,7 +226,8 @@ def main():
     batches = [make_batch(cfg, rank, s) for s in range(args.nbatches)]
     max_ids = max(b.n_ids for b in batches)
     # every rank processes its own B samples (weak scaling, data parallel over samples); at
-    # world > 1 the tables are row-sharded over the ranks (key mod W) and exchanged with NCCL
+    # world > 1 the tables are row-sharded over the ranks (key mod W); keys / rows / gradients are
+    # exchanged over NVLink peer memory (PICASSO_EXCHANGE=p2p, default) or NCCL AllToAllv
     uid = None
     if world > 1:
         obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
@@ -267,10 +268,11 @@ def main():
     # ---------------- timed region: K steps, L2 flushed before each (flush not timed)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    # world == 1: the whole step (no host synchronisation inside) is one CUDA graph; its phase
-    # events are graph nodes, read after every replay.  world > 1 runs eagerly (the NCCL sizes
-    # need one host sync per step).
-    use_graph = world == 1 and not args.eager
+    # The whole step is one CUDA graph when it has no host synchronisation inside: world == 1,
+    # and world > 1 with the peer-memory exchange (device-side sizes) and no HybridHash refresh
+    # schedule.  Its phase events are graph nodes, read after every replay.  The NCCL exchange
+    # needs one host sync per step (host-side sizes) and runs eagerly.
+    use_graph = not args.eager and (world == 1 or (emb.exchange == "p2p" and not args.cache_bytes))
     graph = None
     if use_graph:
         ids0, off0 = dev_in[0]
@@ -390,6 +392,7 @@ def main():
                        "dims": sorted(set(cfg.table_dim.tolist())), "rows": int(cfg.table_rows.sum()),
                        "alpha": cfg.alpha, "optimizer": "adagrad", "pool": "sum",
                        "parallelism": f"dp{world}+rowshard{world}" if world > 1 else "single",
+                       "exchange": emb.exchange if world > 1 else None,
                        "l2": "flushed (256 MiB write, untimed) before every timed step",
                        "launch": "cuda_graph (one captured step, replayed)" if use_graph else "eager",
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
@@ -397,7 +400,8 @@ def main():
                     "d2h_bytes_per_step": int(d2h),
                     "note": "H2D of ids+offsets+dY from pinned host memory, D2H of the per-pack unique counts"},
             "gpu_launches": int((lf + lb) * args.steps),
-            "roofline": {"bound": "hbm", "kernel": {"pool": "k_pool", "segsum": "k_segsum (+ hot-row chunks)",
+            "roofline": {"bound": "hbm", "kernel": {"pool": "k_pool_pipe (+ k_seg_of)",
+                                                     "segsum": "k_segsum_pipe (+ k_segsum_fix)",
                                                      "update": "k_update_rows"}[dom],
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],

@@ -112,6 +112,12 @@ struct MultiState {
     void *peer_base[kP2PMaxW] = {};     // opened IPC mappings (closed at destroy)
     uint32_t *epoch_d = nullptr;        // [kP2PPhases]
     int32_t *R_d = nullptr;             // [1] received keys (device)
+    int64_t *gsrc = nullptr;            // [max_recv * W] G-row offsets per (owner-unique, source)
+    int64_t *pack_fbase_d = nullptr, *dbase_d = nullptr, *dst_off = nullptr, *row_base_d = nullptr;
+    std::vector<int64_t> row_base;      // [P+1] owned rows per pack, prefix
+    int32_t *dtab = nullptr;            // [rows_total * W] owner position of (owned row, source), or -1
+    int32_t *dst_rank = nullptr;
+    size_t win_ogbuf = 0;
 };
 
 struct picasso_ctx {
@@ -274,11 +280,17 @@ struct picasso_ctx {
             mp.ouid_key = c.take<unsigned long long>(RM);
             mp.opack_gstart = c.take<int32_t>(P + 1);
             mp.opack_ustart = c.take<int32_t>(P + 1);
-            mp.od_total = c.take<int32_t>(1);
+            mp.od_total = c.take<int32_t>(P + 1);  // NCCL driver: owner unique count; p2p: per-pack row counts
             mp.opack_ostart_d = c.take<int64_t>(P + 1);
             mp.ogbase_scratch = c.take<int64_t>(P + 1);
             mp.oblk_d = c.take<OwnerBlock>(WP);
             mp.contrib = c.take<int32_t>((size_t)RM * world);
+            mp.gsrc = c.take<int64_t>((size_t)RM * world);
+            mp.pack_fbase_d = c.take<int64_t>(P + 1);
+            mp.row_base_d = c.take<int64_t>(P + 1);
+            mp.dbase_d = c.take<int64_t>(WP);
+            mp.dst_rank = c.take<int32_t>(N);
+            mp.dst_off = c.take<int64_t>(N);
             mp.rsend_off = c.take<int64_t>(RM);
             mp.rows_send = c.take<float>((size_t)RM * maxD);
             osort_hist = c.take<int32_t>(2 * ((RM + kTile - 1) / kTile) + 2);

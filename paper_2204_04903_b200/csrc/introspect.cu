@@ -4,6 +4,7 @@
 extern "C" picasso_status picasso_get_owner_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap,
                                                    int64_t *n) {
     if (!ctx || !n || pack < 0 || pack >= ctx->P || !ctx->bound || ctx->world < 2) return PICASSO_ERR_INVALID_ARG;
+    if (ctx->mp.p2p) return PICASSO_ERR_STATE;  // the peer-memory owner keeps a direct table, no unique list
     if (cudaStreamSynchronize(ctx->last_stream) != cudaSuccess) return PICASSO_ERR_CUDA;
     std::vector<int32_t> us(ctx->P + 1);
     if (cudaMemcpy(us.data(), ctx->mp.opack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost) !=

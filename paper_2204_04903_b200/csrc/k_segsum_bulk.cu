@@ -66,6 +66,7 @@ __device__ __forceinline__ float *g_dst(const UpdateArgs &a, int32_t u, int32_t 
             return a.hot_g + a.hot_g_off[a.pack] + (int64_t)(hs - a.hot_pslot[a.pack]) * D;
         }
     }
+    if (a.dst_off) return a.dst_buf[a.dst_rank[u]] + a.dst_off[u];
     return a.row_off ? a.gbuf + a.row_off[u] : gp + (int64_t)(u - u0) * D;
 }
 

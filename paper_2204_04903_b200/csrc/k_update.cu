@@ -85,6 +85,7 @@ __device__ __forceinline__ float *g_row_ptr(const UpdateArgs &a, int64_t u, int3
             return a.hot_g + a.hot_g_off[a.pack] + (int64_t)(hs - a.hot_pslot[a.pack]) * D;
         }
     }
+    if (a.dst_off) return a.dst_buf[a.dst_rank[u]] + a.dst_off[u];
     return a.row_off ? a.gbuf + a.row_off[u] : gp + (u - u0) * D;
 }
 

@@ -140,6 +140,10 @@ struct UpdateArgs {
     const int32_t *tile_start;   // pipelined segsum: [P, nt+1] equal-cost tile starts (nullptr: legacy)
     int32_t nt;                  //   tiles per pack (= SMs x warps per CTA)
     int4 *split;                 //   [nt] rows cut by tile edges: {first tile, uid, start, end}
+    // W > 1 over peer memory: G rows go straight to their owner's receive buffer
+    const int32_t *dst_rank;     //   [U] owner of each unique row (nullptr: G stays local)
+    const int64_t *dst_off;      //   [U] float offset of its G row in the owner's receive buffer
+    float *dst_buf[8];           //   the ranks' receive buffers (NVLink peer pointers)
 };
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);

@@ -284,6 +284,11 @@ picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
     }
     u.gbuf = ctx->gbuf;
     u.row_off = ctx->mp.row_off;
+    if (mp.p2p) {  // G rows straight into the owners' receive buffers (p2p.cu)
+        u.dst_rank = mp.dst_rank;
+        u.dst_off = mp.dst_off;
+        for (int q = 0; q < ctx->world; ++q) u.dst_buf[q] = mp.peers.ogbuf[q];
+    }
     if (N > 0) {
         for (int32_t p = 0; p < ctx->P; ++p) {
             u.pack = p;

@@ -10,8 +10,11 @@
 //   k_p2p_gather : gathers the owner's rows and stores them straight into each requester's rows
 //                  buffer at the slot its send layout reserved (NVLink stores): Gather + Shuffle
 //                  + Stitch in one kernel, the transfer overlapping the gather row by row
-//   k_p2p_update : pulls each owner-unique row's <= W gradient rows from the requesters' G
-//                  buffers (source rank ascending, fp64, reading O6') and applies the optimizer
+//   k_p2p_dst    : requester side: the owner receive-buffer slot of each unique row's G, so the
+//                  segment-sum kernels store G straight into the owner's memory (NVLink stores:
+//                  segment-sum + gradient Shuffle in one kernel)
+//   k_p2p_update : per owner-unique row, the <= W pushed G rows summed in source-rank order
+//                  (fp64, reading O6') and the optimizer applied
 //   k_p2p_signal / k_p2p_wait : epoch flags in the peers' windows (system-scope release /
 //                  acquire), with a timeout that latches an error instead of hanging
 #include "kernels.h"
@@ -124,6 +127,46 @@ __global__ void __launch_bounds__(1024) k_p2p_blocks(P2PArgs a) {
         *a.R = (int32_t)(over ? 0 : total);
         if (over) atomicOr(a.err, ERR_CAPACITY);
     }
+    __syncthreads();
+    if (t < a.P) a.ocount[t] = 0;
+    if (t == 0) {  // float layout of the received G rows: pack-major, D_p floats per position
+        int64_t f = 0;
+        for (int q = 0; q < a.P; ++q) {
+            a.pack_fbase[q] = f;
+            f += (a.pack_ostart[q + 1] - a.pack_ostart[q]) * __ldg(a.pack_dim + q);
+        }
+        a.pack_fbase[a.P] = f;
+    }
+}
+
+// Requester side: where each of my unique rows' G goes.  Owner r holds my requests of pack p
+// at owner positions pack_ostart_r(p) + sum_{s < me} count_s(r, p) + j, j = my slot index in
+// bucket (r, p); its G rows are pack-major with D_p floats each.  dbase[(r, p)] = float offset
+// of my block in r's receive buffer (from every rank's bucket counts).  One block.
+__global__ void __launch_bounds__(1024) k_p2p_dst_base(P2PArgs a) {
+    const int t = threadIdx.x;
+    if (t >= a.W * a.P) return;
+    const int r = t / a.P, p = t - (t / a.P) * a.P;
+    int64_t f = 0;
+    for (int q = 0; q < p; ++q) {  // packs before p at owner r, all sources
+        int64_t n = 0;
+        for (int s = 0; s < a.W; ++s) n += __ldcv(a.peer.bcount[s] + r * a.P + q);
+        f += n * __ldg(a.pack_dim + q);
+    }
+    int64_t before = 0;  // sources before me, same pack
+    for (int s = 0; s < a.rank; ++s) before += __ldcv(a.peer.bcount[s] + r * a.P + p);
+    a.dbase[t] = f + before * __ldg(a.pack_dim + p);
+}
+
+__global__ void k_p2p_dst(P2PArgs a) {
+    const int32_t U = *a.d_total;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = a.bkey[u];  // bucket (owner, pack) from the Partition pass
+        if (b >= a.W * a.P) continue;  // hot: G goes to the replicated hot buffer
+        const int p = b % a.P;
+        a.dst_rank[u] = b / a.P;
+        a.dst_off[u] = a.dbase[b] + (a.send_pos[u] - a.bstart[b]) * __ldg(a.pack_dim + p);
+    }
 }
 
 __device__ __forceinline__ int owner_block_p(const OwnerBlock *blk, int nb, int64_t opos) {
@@ -135,57 +178,70 @@ __device__ __forceinline__ int owner_block_p(const OwnerBlock *blk, int nb, int6
     return lo;
 }
 
-// requested key -> owner hash; per owner position: local row, source, float offset of the
-// requester's row slot
-__global__ void __launch_bounds__(256) k_p2p_insert(P2PArgs a, Slot *table, uint32_t cap_mask) {
+// Requested key -> owner tables, per owner position: local row, source, float offset of the
+// requester's row slot; dtab[(row_base[p] + row) * W + src] = the position (each requester
+// asks for a key at most once, so (row, src) is unique: a direct table replaces the owner hash).
+__global__ void __launch_bounds__(256) k_p2p_insert(P2PArgs a) {
     __shared__ OwnerBlock sb[kMaxOwnerBlocks];
     const int nb = a.W * a.P;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sb[i] = a.oblk[i];
     __syncthreads();
     const int64_t R = *a.R;
-    const int64_t opos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = opos < R;
-    unsigned long long key = 0;
-    if (valid) {
+    for (int64_t opos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; opos < R;
+         opos += (int64_t)gridDim.x * blockDim.x) {
         const int k = owner_block_p(sb, nb, opos);
         const int64_t j = opos - sb[k].ostart;
-        const int32_t lr = __ldcv(a.peer.send_keys[sb[k].src] + sb[k].rstart + j);
+        const int p = sb[k].pack, src = sb[k].src;
+        const int32_t lr = __ldcv(a.peer.send_keys[src] + sb[k].rstart + j);
         a.lrow[opos] = lr;
-        a.osrc[opos] = sb[k].src;
-        a.roff[opos] = sb[k].rroff + j * __ldg(a.pack_dim + sb[k].pack);
-        key = (unsigned long long)(a.pack_key_off[sb[k].pack] + (int64_t)lr);
-        if (a.fcnt) atomicAdd(a.fcnt + a.fcnt_off[sb[k].pack] + lr, 1u);  // FCounter (Alg. 1)
+        a.osrc[opos] = src;
+        a.roff[opos] = sb[k].rroff + j * __ldg(a.pack_dim + p);
+        a.dtab[(a.row_base[p] + lr) * a.W + src] = (int32_t)opos;
+        if (a.fcnt) atomicAdd(a.fcnt + a.fcnt_off[p] + lr, 1u);  // FCounter (Alg. 1)
     }
-    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-    if (!valid) return;
-    const int lane = threadIdx.x & 31;
-    const unsigned peers = __match_any_sync(vmask, key);
-    const int leader = __ffs(peers) - 1;
-    uint32_t slot = 0;
-    if (lane == leader) {
-        slot = slot_hash(key) & cap_mask;
-        for (uint32_t probe = 0;; ++probe) {
-            unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(&table[slot].key);
-            if (cur == kEmptyKey) cur = atomicCAS(&table[slot].key, kEmptyKey, key);
-            if (cur == kEmptyKey || cur == key) break;
-            slot = (slot + 1) & cap_mask;
-            if (probe > cap_mask) {
-                atomicOr(a.err, ERR_CAPACITY);
-                break;
-            }
-        }
-        atomicMin(&table[slot].minpos, (unsigned int)opos);
-    }
-    slot = __shfl_sync(vmask, slot, leader);
-    a.oslot[opos] = (int32_t)slot;
 }
 
-// contrib[ou * W + src] = owner position of source src's request for owner-unique row ou
-__global__ void k_p2p_contrib(P2PArgs a) {
+// rows requested this step, listed once each (by the lowest requesting source), per pack:
+// olist[pack_ostart[p] + i], i < ocount[p] (order irrelevant: each row's update is independent)
+__global__ void k_p2p_leaders(P2PArgs a) {
+    const int64_t R = *a.R;
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count; one atomic per (warp, pack) instead of one per row
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < R;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t opos = base + lane;
+        int p = 0;
+        int32_t row = 0;
+        bool leader = false;
+        if (opos < R) {
+            while (p + 1 < a.P && a.pack_ostart[p + 1] <= opos) ++p;
+            row = a.lrow[opos];
+            const int32_t src = a.osrc[opos];
+            const int32_t *dt = a.dtab + (a.row_base[p] + row) * a.W;
+            leader = true;
+            for (int s = 0; s < src; ++s) leader = leader && dt[s] < 0;
+        }
+        const unsigned lm = __ballot_sync(0xffffffffu, leader);
+        if (leader) {
+            const unsigned peers = __match_any_sync(lm, p);
+            const int first = __ffs(peers) - 1;
+            int32_t b = 0;
+            if (lane == first) b = atomicAdd(a.ocount + p, __popc(peers));
+            b = __shfl_sync(peers, b, first);
+            a.olist[a.pack_ostart[p] + b + __popc(peers & ((1u << lane) - 1u))] = row;
+        }
+    }
+}
+
+// clears the previous step's direct-table entries (positions of the last forward)
+__global__ void k_p2p_reset(P2PArgs a) {
     const int64_t R = *a.R;
     for (int64_t opos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; opos < R;
-         opos += (int64_t)gridDim.x * blockDim.x)
-        a.contrib[(int64_t)a.oinv[opos] * a.W + a.osrc[opos]] = (int32_t)opos;
+         opos += (int64_t)gridDim.x * blockDim.x) {
+        int p = 0;
+        while (p + 1 < a.P && a.pack_ostart[p + 1] <= opos) ++p;
+        a.dtab[(a.row_base[p] + a.lrow[opos]) * a.W + a.osrc[opos]] = -1;
+    }
 }
 
 // owner rows -> the requesters' rows buffers (peer stores)
@@ -218,80 +274,113 @@ __global__ void __launch_bounds__(256) k_p2p_gather(P2PArgs a, const float *weig
     }
 }
 
-// per owner-unique row: its <= W gradient rows pulled from the requesters (source ascending),
-// summed in fp64, rounded once, Adagrad / lazy Adam
-template <int D>
-__global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *weight, float *state1, float *state2,
-                                                    int opt, float lr, float eps, float beta1, float beta2,
-                                                    float adam_ss) {
+// Per owned row requested this step (olist), the <= W pushed G rows (in this owner's receive
+// buffer) summed in source-rank order in fp64 (reading O6'), rounded once, Adagrad / lazy Adam.
+// RB rows per lane group at a time, all loads of a batch in flight together.
+template <int D, int NFW>
+__global__ void __launch_bounds__(256, 2) k_p2p_update(P2PArgs a, int pack, float *weight, float *state1,
+                                                       float *state2, int opt, float lr, float eps, float beta1,
+                                                       float beta2, float adam_ss) {
     constexpr int V4 = D / 4, LANES = V4 < 32 ? V4 : 32, VPL = V4 / LANES;
+    constexpr int RB = VPL == 1 ? 2 : 1;    // owner positions per group iteration
+    constexpr int NF = VPL == 1 ? NFW : 2;  // sources per load batch (NFW >= W when it fits)
     const int li = threadIdx.x % LANES;
-    const int32_t u0 = a.opack_ustart[pack], u1 = a.opack_ustart[pack + 1];
+    const int64_t o0 = a.pack_ostart[pack], o1 = o0 + a.ocount[pack];
+    const int64_t rb = a.row_base[pack], fb = a.pack_fbase[pack];
+    const float *gin = a.peer.ogbuf[a.rank] + fb + li * 4;
     const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / LANES;
-    for (int64_t ou = u0 + grp; ou < u1; ou += ngrp) {
-        const int64_t row = (int64_t)(a.ouid_key[ou] - (unsigned long long)a.pack_key_off[pack]);
-        const int64_t o = row * D + li * 4;
-        float4 w[VPL], s1[VPL], s2[VPL];
+#pragma unroll 1
+    for (int64_t ob = o0 + grp * RB; ob < o1; ob += ngrp * RB) {
+        int64_t o[RB];
+        const int32_t *dt[RB];
+        float4 w[RB][VPL], s1[RB][VPL], s2[RB][VPL];
+        double g[RB][VPL][4];
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-            w[q] = *reinterpret_cast<const float4 *>(weight + o + q * LANES * 4);
-            s1[q] = *reinterpret_cast<const float4 *>(state1 + o + q * LANES * 4);
-            if (opt == 1) s2[q] = *reinterpret_cast<const float4 *>(state2 + o + q * LANES * 4);
-        }
-        double g[VPL][4];
+        for (int r = 0; r < RB; ++r) {
+            o[r] = -1;
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) g[q][0] = g[q][1] = g[q][2] = g[q][3] = 0.0;
-        constexpr int NF = VPL == 1 ? kP2PMaxW : 2;  // contributions in flight at once
-        for (int s0 = 0; s0 < a.W; s0 += NF) {
-            float4 c[NF][VPL];
-            int32_t ci[NF];
-#pragma unroll
-            for (int k = 0; k < NF; ++k) {
-                ci[k] = s0 + k < a.W ? a.contrib[ou * a.W + s0 + k] : -1;
-                if (ci[k] >= 0) {
-                    const float *gr = a.peer.gbuf[s0 + k] + a.roff[ci[k]] + li * 4;
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) c[k][q] = __ldcv(reinterpret_cast<const float4 *>(gr + q * LANES * 4));
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < NF; ++k)  // source rank ascending
-                if (ci[k] >= 0)
+            for (int q = 0; q < VPL; ++q) g[r][q][0] = g[r][q][1] = g[r][q][2] = g[r][q][3] = 0.0;
+            if (ob + r < o1) {
+                const int32_t row = a.olist[ob + r];
+                dt[r] = a.dtab + (rb + row) * a.W;
+                {
+                    o[r] = (int64_t)row * D + li * 4;
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) {
-                        g[q][0] = __dadd_rn(g[q][0], (double)c[k][q].x);
-                        g[q][1] = __dadd_rn(g[q][1], (double)c[k][q].y);
-                        g[q][2] = __dadd_rn(g[q][2], (double)c[k][q].z);
-                        g[q][3] = __dadd_rn(g[q][3], (double)c[k][q].w);
+                        w[r][q] = *reinterpret_cast<const float4 *>(weight + o[r] + q * LANES * 4);
+                        s1[r][q] = *reinterpret_cast<const float4 *>(state1 + o[r] + q * LANES * 4);
+                        if (opt == 1) s2[r][q] = *reinterpret_cast<const float4 *>(state2 + o[r] + q * LANES * 4);
                     }
-        }
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-            float ww[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
-            float ss[4] = {s1[q].x, s1[q].y, s1[q].z, s1[q].w};
-            float v2[4] = {s2[q].x, s2[q].y, s2[q].z, s2[q].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float gg = __double2float_rn(g[q][e]);
-                if (opt == 0) {
-                    const float acc = __fadd_rn(ss[e], __fmul_rn(gg, gg));
-                    ss[e] = acc;
-                    ww[e] = __fsub_rn(ww[e], __fmul_rn(lr, __fdiv_rn(gg, __fadd_rn(__fsqrt_rn(acc), eps))));
-                } else {
-                    const float mo = ss[e], vo = v2[e];
-                    const float mu = __fmul_rn(__fsub_rn(gg, mo), __fsub_rn(1.0f, beta1));
-                    const float vu = __fmul_rn(__fsub_rn(__fmul_rn(gg, gg), vo), __fsub_rn(1.0f, beta2));
-                    const float mn = __fadd_rn(mu, mo), vn = __fadd_rn(vu, vo);
-                    ss[e] = mn;
-                    v2[e] = vn;
-                    ww[e] = __fsub_rn(ww[e], __fmul_rn(adam_ss, __fdiv_rn(mn, __fadd_rn(__fsqrt_rn(vn), eps))));
                 }
             }
-            *reinterpret_cast<float4 *>(weight + o + q * LANES * 4) = make_float4(ww[0], ww[1], ww[2], ww[3]);
-            *reinterpret_cast<float4 *>(state1 + o + q * LANES * 4) = make_float4(ss[0], ss[1], ss[2], ss[3]);
-            if (opt == 1)
-                *reinterpret_cast<float4 *>(state2 + o + q * LANES * 4) = make_float4(v2[0], v2[1], v2[2], v2[3]);
+        }
+#pragma unroll 1
+        for (int s0 = 0; s0 < a.W; s0 += NF) {
+            float4 c[RB][NF][VPL];
+            int32_t op[RB][NF];
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int k = 0; k < NF; ++k) {
+                    op[r][k] = (o[r] >= 0 && s0 + k < a.W) ? dt[r][s0 + k] : -1;
+                    if (op[r][k] >= 0) {
+                        const float *gr = gin + (op[r][k] - o0) * D;
+#pragma unroll
+                        for (int q = 0; q < VPL; ++q)
+                            c[r][k][q] = __ldcg(reinterpret_cast<const float4 *>(gr + q * LANES * 4));
+                    }
+                }
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int k = 0; k < NF; ++k)  // source rank ascending
+                    if (op[r][k] >= 0)
+#pragma unroll
+                        for (int q = 0; q < VPL; ++q) {
+                            g[r][q][0] = __dadd_rn(g[r][q][0], (double)c[r][k][q].x);
+                            g[r][q][1] = __dadd_rn(g[r][q][1], (double)c[r][k][q].y);
+                            g[r][q][2] = __dadd_rn(g[r][q][2], (double)c[r][k][q].z);
+                            g[r][q][3] = __dadd_rn(g[r][q][3], (double)c[r][k][q].w);
+                        }
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            if (o[r] < 0) continue;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) {
+                float ww[4] = {w[r][q].x, w[r][q].y, w[r][q].z, w[r][q].w};
+                float ss[4] = {s1[r][q].x, s1[r][q].y, s1[r][q].z, s1[r][q].w};
+                float v2[4] = {0.f, 0.f, 0.f, 0.f};
+                if (opt == 1) {
+                    v2[0] = s2[r][q].x;
+                    v2[1] = s2[r][q].y;
+                    v2[2] = s2[r][q].z;
+                    v2[3] = s2[r][q].w;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float gg = __double2float_rn(g[r][q][e]);
+                    if (opt == 0) {
+                        const float acc = __fadd_rn(ss[e], __fmul_rn(gg, gg));
+                        ss[e] = acc;
+                        ww[e] = __fsub_rn(ww[e], __fmul_rn(lr, __fdiv_rn(gg, __fadd_rn(__fsqrt_rn(acc), eps))));
+                    } else {
+                        const float mo = ss[e], vo = v2[e];
+                        const float mu = __fmul_rn(__fsub_rn(gg, mo), __fsub_rn(1.0f, beta1));
+                        const float vu = __fmul_rn(__fsub_rn(__fmul_rn(gg, gg), vo), __fsub_rn(1.0f, beta2));
+                        const float mn = __fadd_rn(mu, mo), vn = __fadd_rn(vu, vo);
+                        ss[e] = mn;
+                        v2[e] = vn;
+                        ww[e] = __fsub_rn(ww[e], __fmul_rn(adam_ss, __fdiv_rn(mn, __fadd_rn(__fsqrt_rn(vn), eps))));
+                    }
+                }
+                *reinterpret_cast<float4 *>(weight + o[r] + q * LANES * 4) = make_float4(ww[0], ww[1], ww[2], ww[3]);
+                *reinterpret_cast<float4 *>(state1 + o[r] + q * LANES * 4) = make_float4(ss[0], ss[1], ss[2], ss[3]);
+                if (opt == 1)
+                    *reinterpret_cast<float4 *>(state2 + o[r] + q * LANES * 4) =
+                        make_float4(v2[0], v2[1], v2[2], v2[3]);
+            }
         }
     }
 }
@@ -314,11 +403,18 @@ __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *
 void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s) { k_p2p_signal<<<1, 32, 0, s>>>(a, phase); }
 void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s) { k_p2p_wait<<<1, 32, 0, s>>>(a, phase); }
 void launch_p2p_blocks(const P2PArgs &a, cudaStream_t s) { k_p2p_blocks<<<1, 1024, 0, s>>>(a); }
-void launch_p2p_insert(const P2PArgs &a, Slot *table, uint32_t cap_mask, cudaStream_t s) {
-    if (a.max_recv > 0) k_p2p_insert<<<(unsigned)((a.max_recv + 255) / 256), 256, 0, s>>>(a, table, cap_mask);
+void launch_p2p_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
+    k_p2p_insert<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
-void launch_p2p_contrib(const P2PArgs &a, int num_sms, cudaStream_t s) {
-    k_p2p_contrib<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
+void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s) {
+    k_p2p_leaders<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
+}
+void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s) {
+    k_p2p_reset<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
+}
+void launch_p2p_dst(const P2PArgs &a, int num_sms, cudaStream_t s) {
+    k_p2p_dst_base<<<1, 1024, 0, s>>>(a);
+    k_p2p_dst<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s) {
 #define CALL(DD) k_p2p_gather<DD><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, weight, pack)
@@ -327,9 +423,19 @@ void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, i
 }
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
                        float b1, float b2, float ss, int num_sms, cudaStream_t s) {
-#define CALL(DD) k_p2p_update<DD><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
-    PICASSO_DISPATCH_D(D, CALL)
+    if (a.W <= 2) {
+#define CALL(DD) k_p2p_update<DD, 2><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+        PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
+    } else if (a.W <= 4) {
+#define CALL(DD) k_p2p_update<DD, 4><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+        PICASSO_DISPATCH_D(D, CALL)
+#undef CALL
+    } else {
+#define CALL(DD) k_p2p_update<DD, 8><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+        PICASSO_DISPATCH_D(D, CALL)
+#undef CALL
+    }
 }
 
 }  // namespace picasso

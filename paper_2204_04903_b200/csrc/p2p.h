@@ -15,7 +15,9 @@ struct P2PPeers {
     uint32_t *flags[kP2PMaxW];     // [kP2PPhases][kP2PMaxW] epoch written by each source rank
     int32_t *bcount[kP2PMaxW];     // [W*P+1] bucket counts (owner-major, pack), hot bucket last
     int32_t *send_keys[kP2PMaxW];  // [max_ids] requested local rows, owner-major send layout
-    float *gbuf[kP2PMaxW];         // [max_ids * maxD] rows (fwd) / G rows (bwd), send layout
+    float *gbuf[kP2PMaxW];         // [max_ids * maxD] rows received (fwd), send layout
+    float *ogbuf[kP2PMaxW];        // [max_recv * maxD] G rows received by the owner (bwd), owner-
+                                   //   stream layout: pack p's rows from pack_fbase[p], D_p floats each
 };
 
 struct P2PArgs {
@@ -35,11 +37,19 @@ struct P2PArgs {
     int32_t *lrow;                 // [max_recv] local row per owner position
     int32_t *osrc;                 // [max_recv] source rank per owner position
     int64_t *roff;                 // [max_recv] float offset of the row slot in the source's gbuf
-    int32_t *oslot;                // [max_recv]
-    const int32_t *oinv;           // [max_recv] owner-unique index per owner position
-    int32_t *contrib;              // [max_recv * W] owner position of each (owner-unique, source)
-    const unsigned long long *ouid_key;
-    const int32_t *opack_ustart;   // [P+1]
+    int32_t *dtab;                 // [rows_total * W] owner position of (owned row, source), or -1
+    const int64_t *row_base;       // [P+1] owned rows per pack, prefix
+    int32_t *olist;                // [max_recv] rows requested this step, once each, per pack block
+    int32_t *ocount;               // [P] rows listed per pack
+    int64_t *pack_fbase;           // [P+1] float offset of pack p's G rows in this rank's ogbuf
+    // requester side (push destinations of its G rows)
+    const int32_t *d_total;        // [1] U
+    const int32_t *bkey;           // [U] bucket (owner * P + pack; W * P = hot) of each unique
+    const int32_t *send_pos;       // [U] send slot of each unique
+    const int64_t *bstart;         // [W*P+1] first send slot of each bucket
+    int64_t *dbase;                // [W*P] float offset of my block of bucket (r, p) in r's ogbuf
+    int32_t *dst_rank;             // [U]
+    int64_t *dst_off;              // [U]
     uint32_t *fcnt;                // HybridHash FCounter of owned rows (nullptr: off)
     const int64_t *fcnt_off;
 };
@@ -47,9 +57,11 @@ struct P2PArgs {
 void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s);
 void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s);
 void launch_p2p_blocks(const P2PArgs &a, cudaStream_t s);
-void launch_p2p_insert(const P2PArgs &a, Slot *table, uint32_t cap_mask, cudaStream_t s);
-void launch_p2p_contrib(const P2PArgs &a, int num_sms, cudaStream_t s);
+void launch_p2p_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
+void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s);
+void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s);
+void launch_p2p_dst(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
                        float b1, float b2, float ss, int num_sms, cudaStream_t s);
 

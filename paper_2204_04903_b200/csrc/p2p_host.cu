@@ -2,11 +2,12 @@
 //
 //   fwd:  A  dedup + Partition (multi_host.cu)                 -> barrier 0 (send lists ready)
 //         C' owner: block table from the peers' counts, keys read from the requesters' send
-//            lists, dedup, rows stored into the requesters' rows buffers -> barrier 1
+//            lists into a direct (row, source) table, rows stored into the requesters' rows
+//            buffers -> barrier 1
 //         D  pool from the local rows buffer (multi_host.cu)
-//   bwd:  E  transpose + segment-sum, G rows into the local rows buffer -> barrier 2
+//   bwd:  E  transpose + segment-sum, G rows stored into the owners' receive buffers -> barrier 2
 //         (HybridHash hot rows: AllReduce as in the NCCL driver)
-//         F' owner: G rows pulled from the requesters, reduced in source order, optimizer
+//         F' owner: per requested row, the pushed G rows reduced in source order, optimizer
 // No host synchronisation inside the step (sizes live on the device), so a step can be captured
 // in a CUDA graph.  Barrier 0 also orders every owner's F' pulls of the previous step before
 // any rank's buffers are rewritten (a rank signals it only after its own F').  Windows are
@@ -50,7 +51,8 @@ int max_dim(const picasso_ctx *ctx) {
 
 constexpr size_t kFlagBytes = sizeof(uint32_t) * kP2PPhases * kP2PMaxW;
 
-// window: [flags | bcount | send_keys | gbuf], the same layout on every rank (same plan, max_ids)
+// window: [flags | bcount | send_keys | gbuf | ogbuf], the same layout on every rank (same plan,
+// max_ids, max_recv)
 void window_layout(picasso_ctx *ctx) {
     MultiState &mp = ctx->mp;
     const int64_t N = std::max<int64_t>(ctx->opts.max_ids, 1);
@@ -62,6 +64,8 @@ void window_layout(picasso_ctx *ctx) {
     o = up(o + sizeof(int32_t) * N);
     mp.win_gbuf = o;
     o = up(o + sizeof(float) * (size_t)N * max_dim(ctx));
+    mp.win_ogbuf = o;
+    o = up(o + sizeof(float) * (size_t)std::max<int64_t>(mp.max_recv, 1) * max_dim(ctx));
     mp.win_bytes = o;
 }
 
@@ -71,6 +75,7 @@ void set_peer(picasso_ctx *ctx, int q, char *base) {
     mp.peers.bcount[q] = reinterpret_cast<int32_t *>(base + mp.win_bcount);
     mp.peers.send_keys[q] = reinterpret_cast<int32_t *>(base + mp.win_keys);
     mp.peers.gbuf[q] = reinterpret_cast<float *>(base + mp.win_gbuf);
+    mp.peers.ogbuf[q] = reinterpret_cast<float *>(base + mp.win_ogbuf);
 }
 
 // allocate this rank's window and move the shared buffers (bucket counts, send list, rows / G
@@ -80,6 +85,9 @@ picasso_status window_alloc(picasso_ctx *ctx) {
     if (mp.win) return PICASSO_OK;
     window_layout(ctx);
     PCK(cudaMalloc(&mp.win, mp.win_bytes));
+    PCK(cudaMalloc(&mp.dtab, sizeof(int32_t) * (size_t)std::max<int64_t>(mp.rows_total, 1) * ctx->world));
+    PCK(cudaMemset(mp.dtab, 0xFF, sizeof(int32_t) * (size_t)std::max<int64_t>(mp.rows_total, 1) * ctx->world));
+    PCK(cudaMemset(mp.R_d, 0, sizeof(int32_t)));
     PCK(cudaMemset(mp.win, 0, mp.win_bcount));
     set_peer(ctx, ctx->rank, mp.win);
     mp.bcount = mp.peers.bcount[ctx->rank];
@@ -109,11 +117,18 @@ P2PArgs make_p2p_args(picasso_ctx *ctx) {
     a.lrow = mp.recv_keys;
     a.osrc = mp.opos_map;
     a.roff = mp.rsend_off;
-    a.oslot = mp.oslot;
-    a.oinv = mp.oinv;
-    a.contrib = mp.contrib;
-    a.ouid_key = mp.ouid_key;
-    a.opack_ustart = mp.opack_ustart;
+    a.dtab = mp.dtab;
+    a.olist = mp.oslot;     // the hash-dedup scratch of the NCCL driver, unused here
+    a.ocount = mp.od_total;
+    a.row_base = mp.row_base_d;
+    a.pack_fbase = mp.pack_fbase_d;
+    a.d_total = ctx->d_total;
+    a.bkey = mp.bkey;
+    a.send_pos = mp.send_pos;
+    a.bstart = mp.bstart;
+    a.dbase = mp.dbase_d;
+    a.dst_rank = mp.dst_rank;
+    a.dst_off = mp.dst_off;
     a.fcnt = ctx->opts.cache_max_bytes > 0 ? mp.fcnt : nullptr;
     a.fcnt_off = mp.fcnt_off_d;
     return a;
@@ -127,6 +142,14 @@ void barrier(picasso_ctx *ctx, int phase, cudaStream_t s) {
     ctx->launches_fwd += 2;
 }
 
+// ---- requester side: owner receive slots of this rank's G rows (after barrier 0) ------------
+picasso_status p2p_dst(picasso_ctx *ctx, cudaStream_t s) {
+    launch_p2p_dst(make_p2p_args(ctx), ctx->num_sms, s);
+    ctx->launches_fwd += 2;
+    PCK(cudaGetLastError());
+    return PICASSO_OK;
+}
+
 // ---- C': owner side --------------------------------------------------------------------------
 picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
     MultiState &mp = ctx->mp;
@@ -134,34 +157,13 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
     const P2PArgs a = make_p2p_args(ctx);
     const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
     ctx->mark(4, true, s);
+    launch_p2p_reset(a, ctx->num_sms, s);  // the previous forward's direct-table entries
     launch_p2p_blocks(a, s);
-    const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)RM * 2));
-    PCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
-    launch_p2p_insert(a, ctx->table, cap_step - 1, s);
-    IndexArgs ia{};  // owner dedup: the index kernels on the owner stream, sizes on the device
-    ia.N = RM;
-    ia.n_dev = mp.R_d;
-    ia.P = P;
-    ia.table = ctx->table;
-    ia.slot_of = mp.oslot;
-    ia.blk_cnt = ctx->blk_cnt;
-    ia.blk_off = ctx->blk_off;
-    ia.d_total = mp.od_total;
-    ia.unique_gkey = mp.ouid_key;
-    ia.pack_gstart = mp.opack_gstart;
-    ia.pack_ustart = mp.opack_ustart;
-    ia.inverse = mp.oinv;
-    ia.pack_dim = ctx->pack_dim_d;
-    ia.pack_gbase = mp.ogbase_scratch;
-    ia.sort_bits0 = 1;
-    ia.sort_hist0 = ctx->osort_hist;
-    ia.err = ctx->err;
-    launch_dedup_assign(ia, s);
-    PCK(cudaMemsetAsync(mp.contrib, 0xFF, sizeof(int32_t) * RM * ctx->world, s));
-    launch_p2p_contrib(a, ctx->num_sms, s);
+    launch_p2p_insert(a, ctx->num_sms, s);
+    launch_p2p_leaders(a, ctx->num_sms, s);
     for (int p = 0; p < P; ++p) launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
     ctx->mark(4, false, s);
-    ctx->launches_fwd += 2 + 4 + 1 + P;
+    ctx->launches_fwd += 4 + P;
     PCK(cudaGetLastError());
     return PICASSO_OK;
 }
@@ -196,6 +198,7 @@ picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t
     picasso_status st;
     if ((st = mfwd_a(ctx, ids, offsets, B, N, s))) return st;
     barrier(ctx, 0, s);
+    if ((st = p2p_dst(ctx, s))) return st;
     if ((st = p2p_c(ctx, s))) return st;
     barrier(ctx, 1, s);
     return mfwd_d(ctx, out, s);
@@ -221,6 +224,8 @@ picasso_status group_fwd_p2p(picasso_group *g, const int64_t *const *ids, const 
     picasso_status st;
     for (int r = 0; r < W; ++r)
         if ((st = mfwd_a(g->ctx[r], ids[r], offsets[r], batch[r], n_ids[r], s))) return st;
+    for (int r = 0; r < W; ++r)
+        if ((st = p2p_dst(g->ctx[r], s))) return st;
     for (int r = 0; r < W; ++r)
         if ((st = p2p_c(g->ctx[r], s))) return st;
     for (int r = 0; r < W; ++r)
@@ -291,7 +296,9 @@ void p2p_release(picasso_ctx *ctx) {
             mp.peer_base[q] = nullptr;
         }
     if (mp.win) cudaFree(mp.win);
+    if (mp.dtab) cudaFree(mp.dtab);
     mp.win = nullptr;
+    mp.dtab = nullptr;
     mp.p2p = false;
 }
 

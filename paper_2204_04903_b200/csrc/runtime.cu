@@ -105,15 +105,16 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
                 delete c;
                 return PICASSO_ERR_PLAN_MISMATCH;
             }
+        c->mp.row_base.assign(c->P + 1, 0);  // owned rows per pack, prefix (owner-row tables)
+        for (int32_t p = 0; p < c->P; ++p) {
+            const int64_t R = c->pack_rows[p];
+            c->mp.row_base[p + 1] = c->mp.row_base[p] + (R > rank ? (R - rank + world - 1) / world : 0);
+        }
+        c->mp.rows_total = c->mp.row_base[c->P];
         if (opts->cache_max_bytes > 0) {  // HybridHash sizing: FCounter over owned rows, hot rows
-            c->mp.fcnt_off.assign(c->P + 1, 0);
+            c->mp.fcnt_off = c->mp.row_base;
             int minD = 1 << 30;
-            for (int32_t p = 0; p < c->P; ++p) {
-                const int64_t R = c->pack_rows[p];
-                c->mp.fcnt_off[p + 1] = c->mp.fcnt_off[p] + (R > rank ? (R - rank + world - 1) / world : 0);
-                minD = std::min(minD, c->pack_dim[p]);
-            }
-            c->mp.rows_total = c->mp.fcnt_off[c->P];
+            for (int32_t p = 0; p < c->P; ++p) minD = std::min(minD, c->pack_dim[p]);
             const int nst = opts->opt == PICASSO_OPT_ADAM_LAZY ? 2 : 1;
             c->mp.k_max = opts->cache_max_bytes / ((int64_t)4 * minD * (1 + nst));
             c->mp.hot_mask = pow2_at_least((uint64_t)std::max<int64_t>(c->mp.k_max, 1) * 2) - 1;
@@ -196,6 +197,9 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
         CK(cudaMallocHost(&ctx->mp.ostart_h, sizeof(int64_t) * (ctx->P + 1)));
         CK(cudaMallocHost(&ctx->mp.og_h, sizeof(int32_t) * (ctx->P + 1)));
     }
+    if (ctx->world > 1)
+        CK(cudaMemcpy(ctx->mp.row_base_d, ctx->mp.row_base.data(), sizeof(int64_t) * (ctx->P + 1),
+                      cudaMemcpyHostToDevice));
     if (ctx->world > 1 && ctx->opts.cache_max_bytes > 0) {  // HybridHash: FCounter, empty hot set
         MultiState &mp = ctx->mp;
         CK(cudaMemcpy(mp.fcnt_off_d, mp.fcnt_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
