@@ -160,6 +160,10 @@ struct picasso_ctx {
     int32_t *tile_start = nullptr;
     int4 *split = nullptr;
     bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
+    bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int32_t *su = nullptr, *sseg = nullptr;  // the last forward's transpose (uid-sorted occurrences)
     std::vector<float *> w, s1, s2;
     // step state
     bool fwd_done = false;

@@ -193,15 +193,17 @@ __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
     const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
     const int lane = threadIdx.x & 31;
+    int32_t uids[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) uids[i] = g0 + i < N ? __ldg(a.slot_of + g0 + i) : 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) uids[i] = g0 + i < N ? a.table[uids[i]].uid : 0;  // all lookups in flight
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;
         const bool valid = g < N;
-        int32_t uid = 0;
-        if (valid) {
-            uid = a.table[a.slot_of[g]].uid;
-            a.inverse[g] = uid;
-        }
+        const int32_t uid = uids[i];
+        if (valid) a.inverse[g] = uid;
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
         if (valid) {
             const int d = uid & (radix - 1);

@@ -17,7 +17,7 @@
 //    per warp at D = 128), then added strictly in ascending j per segment (bit-identical to the
 //    sequential definition); a finished segment is written into its column block of the
 //    stitched [B, out_width] output with streaming 128-bit stores.
-// The walk also records seg_of[g] (segment of every packed-stream position) for the backward.
+// (seg_of, the segment of every packed-stream position, is written by k_seg_of beforehand.)
 #include "kernels.h"
 
 namespace picasso {
@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
                     myrow[p] = a.row_off ? a.row_off[__ldg(a.inverse + j + st.gb[w][c])]
                                          : (fi.base + row_of(a.id_mode, __ldg(a.ids + j), fi, a.err)) * D;
                     myseg[p] = c;
-                    a.seg_of[j + st.gb[w][c]] = st.sg[w][c];
                 }
             }
             // ---- U rows at a time: broadcast addresses, load, add in ascending order

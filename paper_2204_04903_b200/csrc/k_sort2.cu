@@ -100,11 +100,15 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter2(const int32_t *kin, c
     int32_t key[kRounds], val[kRounds], rk[kRounds];
     int dg[kRounds];
 #pragma unroll
+    for (int r = 0; r < kRounds; ++r) {  // all loads first: 16 independent requests in flight
+        const int64_t g = base + r * 32 + lane;
+        key[r] = g < n ? __ldg(kin + g) : 0;
+        val[r] = g < n ? __ldg(vin + g) : 0;
+    }
+#pragma unroll
     for (int r = 0; r < kRounds; ++r) {
         const int64_t g = base + r * 32 + lane;
         const bool valid = g < n;
-        key[r] = valid ? kin[g] : 0;
-        val[r] = valid ? vin[g] : 0;
         dg[r] = valid ? (int)(((unsigned)key[r] >> shift) & dmask) : (kMaxRadix + lane);
         const unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
         int32_t before = 0;

@@ -36,6 +36,8 @@ UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, i
 int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
 int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
+void transpose_fork(picasso_ctx *ctx, cudaStream_t s);
+void transpose_join(picasso_ctx *ctx, cudaStream_t s);
 }
 picasso_status hot_update_all(picasso_ctx *ctx, float lr, float ss, cudaStream_t s);
 picasso_status group_fwd_p2p(picasso_group *g, const int64_t *const *ids, const int32_t *const *offsets,
@@ -135,6 +137,7 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
                         s));
     ctx->mark(0, false, s);
     ctx->launches_fwd += 1 + (N > 0 ? 4 : 0) + 1 + 5;
+    transpose_fork(ctx, s);
     return PICASSO_OK;
 }
 
@@ -254,6 +257,7 @@ picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s) {
         ctx->launches_fwd += launch_pool_all(ctx, pa, out, s);
     }
     ctx->mark(1, false, s);
+    transpose_join(ctx, s);
     MCK(cudaGetLastError());
     ctx->fwd_done = true;
     ctx->last_stream = s;
@@ -263,15 +267,8 @@ picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s) {
 // ---- phase E: transpose + segment-sum into the send layout -----------------------------------
 picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s) {
     const int64_t N = ctx->N;
-    int32_t *su = nullptr, *sseg = nullptr;
-    ctx->mark(2, true, s);
-    radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N, ctx->splan,
-                      ctx->hist0, ctx->hist1, ctx->rowtot, s, &ctx->launches_bwd);
-    launch_csr_any(ctx, su, N, s);
-    ctx->mark(2, false, s);
-    ctx->launches_bwd += N > 0 ? 1 : 0;
-    ctx->mark(3, true, s);
-    UpdateArgs u = make_update_args(ctx, grad_out, lr, step, su, sseg);
+    ctx->mark(3, true, s);  // the transpose ran in the forward (transpose_fork)
+    UpdateArgs u = make_update_args(ctx, grad_out, lr, step, ctx->su, ctx->sseg);
     MultiState &mp = ctx->mp;
     if (mp.hot_k > 0) {  // this rank's hot-row gradients and occurrence counts (AllReduced next)
         MCK(cudaMemsetAsync(mp.hot_g, 0, sizeof(float) * mp.hot_g_floats, s));

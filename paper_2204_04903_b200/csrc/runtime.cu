@@ -124,6 +124,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     c->seg_cfg = segsum_pipe_cfg();
     if (const char *e = std::getenv("PICASSO_POOL")) c->pipe_pool = std::strcmp(e, "legacy") != 0;
+    if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap = std::strcmp(e, "0") != 0;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
@@ -224,6 +225,11 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
             CK(cudaStreamSynchronize(0));
         }
     }
+    if (!ctx->side) {  // internal stream of the forward's overlapped transpose
+        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
     ctx->bound = true;
     ctx->fwd_done = false;
     return PICASSO_OK;
@@ -232,6 +238,11 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
 extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
     if (!ctx) return PICASSO_OK;
     p2p_release(ctx);
+    if (ctx->side) {
+        cudaStreamDestroy(ctx->side);
+        cudaEventDestroy(ctx->ev_fork);
+        cudaEventDestroy(ctx->ev_join);
+    }
     if (ctx->mp.comm) ncclCommDestroy(ctx->mp.comm);
     if (ctx->mp.cnt_send_h) {
         cudaFreeHost(ctx->mp.cnt_send_h);
@@ -251,6 +262,8 @@ UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, i
 int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
 int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
+void transpose_fork(picasso_ctx *ctx, cudaStream_t s);
+void transpose_join(picasso_ctx *ctx, cudaStream_t s);
 }
 picasso_status multi_fwd_nccl(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
                               float *out, cudaStream_t s);
@@ -321,6 +334,10 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     launch_dedup_assign(a, s);
     ctx->mark(0, false, s);
     ctx->launches_fwd += 1 + (n_ids > 0 ? 4 : 0) + 1;  // prep, insert+flag+scan+assign, inverse
+    ctx->B = batch;
+    ctx->N = n_ids;
+    ctx->offsets = offsets;
+    picasso::transpose_fork(ctx, s);
     ctx->mark(1, true, s);
     {
         PoolArgs pa{};
@@ -330,11 +347,9 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         ctx->launches_fwd += launch_pool_all(ctx, pa, out, s);
     }
     ctx->mark(1, false, s);
+    picasso::transpose_join(ctx, s);
     CK(cudaGetLastError());
     ctx->fwd_done = true;
-    ctx->B = batch;
-    ctx->N = n_ids;
-    ctx->offsets = offsets;
     ctx->last_stream = s;
     return PICASSO_OK;
 }
@@ -350,15 +365,8 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
         return ctx->mp.p2p ? multi_bwd_p2p(ctx, grad_out, lr, step, s) : multi_bwd_nccl(ctx, grad_out, lr, step, s);
     }
     const int64_t N = ctx->N;
-    int32_t *su = nullptr, *sseg = nullptr;
-    ctx->mark(2, true, s);
-    radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, N, ctx->splan,
-                      ctx->hist0, ctx->hist1, ctx->rowtot, s, &ctx->launches_bwd);
-    launch_csr_any(ctx, su, N, s);
-    ctx->mark(2, false, s);
-    ctx->launches_bwd += N > 0 ? 1 : 0;
-    ctx->mark(3, true, s);
-    UpdateArgs u = picasso::make_update_args(ctx, grad_out, lr, step, su, sseg);
+    ctx->mark(3, true, s);  // the transpose ran in the forward (transpose_fork)
+    UpdateArgs u = picasso::make_update_args(ctx, grad_out, lr, step, ctx->su, ctx->sseg);
     if (N > 0) {
         for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
             u.pack = p;
@@ -388,6 +396,36 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     return PICASSO_OK;
 }
 
+// The backward's transpose (stable sort of the inverse index by uid, row starts, tiles) depends
+// only on the forward's index phase: the forward launches it right after that phase, on an
+// internal stream, so it overlaps the Gather / exchange / pool; the forward joins it before it
+// returns (a forward stays self-contained, e.g. inside a CUDA graph capture).  k_seg_of first:
+// segment of every packed position, for the sort and the pool.
+void picasso::transpose_fork(picasso_ctx *ctx, cudaStream_t s) {
+    launch_seg_of(ctx->offsets, ctx->B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
+    ctx->launches_fwd += (int64_t)ctx->F * ctx->B > 0 ? 1 : 0;
+    cudaStream_t t = s;
+    if (ctx->overlap && ctx->side) {
+        cudaEventRecord(ctx->ev_fork, s);
+        cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+        t = ctx->side;
+    }
+    ctx->mark(2, true, t);
+    int32_t *su = nullptr, *sseg = nullptr;
+    radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, ctx->N,
+                      ctx->splan, ctx->hist0, ctx->hist1, ctx->rowtot, t, &ctx->launches_fwd);
+    launch_csr_any(ctx, su, ctx->N, t);
+    ctx->launches_fwd += ctx->N > 0 ? 1 : 0;
+    ctx->mark(2, false, t);
+    ctx->su = su;
+    ctx->sseg = sseg;
+    if (t != s) cudaEventRecord(ctx->ev_join, t);
+}
+
+void picasso::transpose_join(picasso_ctx *ctx, cudaStream_t s) {
+    if (ctx->overlap && ctx->side) cudaStreamWaitEvent(s, ctx->ev_join, 0);
+}
+
 void picasso::launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s) {
     if (ctx->bulk_segsum)
         launch_csr_tiles(su, N, ctx->ustart, ctx->long_cnt, ctx->pack_gstart, ctx->pack_ustart, ctx->P, ctx->seg_nt,
@@ -411,19 +449,13 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
     pa.err = ctx->err;
     pa.pack_gstart = ctx->pack_gstart;
     pa.field_k = ctx->pipe_pool ? ctx->field_k_d : nullptr;
-    bool seg_done = false;
-    for (int32_t p = 0; p < ctx->P; ++p) {
+    for (int32_t p = 0; p < ctx->P; ++p) {  // seg_of: written by transpose_fork (k_seg_of)
         pa.pack = p;
         pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
         pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
         pa.weight = pa.row_off ? ctx->gbuf : ctx->w[p];
         if ((int64_t)pa.Fp * pa.B == 0) continue;
         if (pool_pipe_supported(ctx->pack_dim[p], pa)) {
-            if (!seg_done) {
-                launch_seg_of(pa.offsets, pa.B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
-                seg_done = true;
-                ++n;
-            }
             n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else {
             launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
