@@ -15,9 +15,12 @@
  *  - "device" pointers are CUDA global-memory pointers on the ctx's device; "host" pointers
  *    are ordinary host memory.  The caller owns every buffer (ids, offsets, out, dY,
  *    weights, optimizer state, workspace).  The library never allocates device memory in
- *    the step path; the ctx owns only host objects (and its NCCL communicator).
+ *    the step path; the ctx owns host objects, its NCCL communicator, one internal stream
+ *    (the forward's overlapped transpose, joined before the forward returns) and, with the
+ *    peer-memory exchange (section 7), its IPC window and owner table (allocated once).
  *  - Work is enqueued on the caller's stream and is asynchronous.  fwd and bwd_update never
- *    synchronise the host when world == 1 (the step is CUDA-graph capturable).
+ *    synchronise the host when world == 1 or with the peer-memory exchange at world > 1
+ *    (the step is CUDA-graph capturable).
  *  - Argument / plan errors are synchronous return codes.  Device-detected errors (ID out
  *    of range in ROWS mode, capacity overflow) are latched in a device word and reported by
  *    picasso_last_error (which synchronises the stream it last used).
@@ -148,11 +151,12 @@ picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, c
  *     G_u = sum_{j : inverse[j] = u} dY[b(j), col(f(j)) + .]   (mean: dY / len)
  * then, for touched rows only (reading O9), Adagrad: acc += G^2; w -= lr*G/(sqrt(acc)+eps),
  * or lazy Adam (torch SparseAdam form, bias correction with the 1-based `step`).
- * grad_out: device fp32 [batch, out_width] (dY, same layout as out).
- * Summation order: ascending occurrence for rows with <= 256 occurrences (bit-identical to
- * the sequential definition); longer rows are split into fixed chunks combined in a fixed
- * order (deterministic run to run).
- * Errors: STATE without a preceding fwd. */
+ * grad_out: device fp32 [batch, out_width] (dY, same layout as out); may be NULL when the
+ * forward's batch was 0 (at world > 1 such a rank still takes part in the step).
+ * Summation: each contribution formed in fp32, accumulated in fp64, rounded once (reading O6);
+ * the order is fixed (ascending occurrence within equal-cost tiles, tile pieces combined in
+ * tile order), so results are bitwise deterministic run to run.
+ * Errors: STATE without a preceding fwd; INVALID_ARG for a NULL grad_out with batch > 0. */
 picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, const float *grad_out, float lr,
                                                 int64_t step, void *stream);
 

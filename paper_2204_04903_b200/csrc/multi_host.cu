@@ -132,9 +132,11 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
                      m.bucket_bits, mp.bhist, mp.bcount, s);
     launch_bucket_prefix(m, s);
     launch_send_prep(m, ctx->num_sms, s);
-    // bucket counts (+ the hot bucket: the hit statistic of HybridHash)
-    MCK(cudaMemcpyAsync(mp.cnt_send_h, mp.bcount, sizeof(int32_t) * (ctx->world * ctx->P + 1), cudaMemcpyDeviceToHost,
-                        s));
+    // bucket counts (+ the hot bucket: the hit statistic of HybridHash); the peer-memory driver
+    // never needs them on the host inside a step (p2p_host_counts copies them on request)
+    if (!mp.p2p)
+        MCK(cudaMemcpyAsync(mp.cnt_send_h, mp.bcount, sizeof(int32_t) * (ctx->world * ctx->P + 1),
+                            cudaMemcpyDeviceToHost, s));
     ctx->mark(0, false, s);
     ctx->launches_fwd += 1 + (N > 0 ? 4 : 0) + 1 + 5;
     transpose_fork(ctx, s);

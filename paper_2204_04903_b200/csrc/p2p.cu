@@ -244,144 +244,82 @@ __global__ void k_p2p_reset(P2PArgs a) {
     }
 }
 
-// owner rows -> the requesters' rows buffers (peer stores)
+// owner rows -> the requesters' rows buffers (peer stores).  One thread per 16-B chunk of a row
+// (grid-stride): the most independent requests in flight per SM for this random-row pattern
+// (tools/gather_bench.cu).
 template <int D>
 __global__ void __launch_bounds__(256) k_p2p_gather(P2PArgs a, const float *weight, int pack) {
-    constexpr int V4 = D / 4, LANES = V4 < 32 ? V4 : 32, VPL = V4 / LANES, RB = 4;
-    const int li = threadIdx.x % LANES;
+    constexpr int V4 = D / 4;
     const int64_t o0 = a.pack_ostart[pack], o1 = a.pack_ostart[pack + 1];
-    const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / LANES;
-    for (int64_t ob = o0 + grp * RB; ob < o1; ob += ngrp * RB) {
-        float4 v[RB][VPL];
-        float *dst[RB];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            const int64_t opos = ob + r;
-            dst[r] = nullptr;
-            if (opos < o1) {
-                dst[r] = a.peer.gbuf[a.osrc[opos]] + a.roff[opos] + li * 4;
-                const float *src = weight + (int64_t)a.lrow[opos] * D + li * 4;
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) v[r][q] = ldg_f4(src + q * LANES * 4);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RB; ++r)
-            if (dst[r])
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) __stcg(reinterpret_cast<float4 *>(dst[r] + q * LANES * 4), v[r][q]);
+    const int64_t n = (o1 - o0) * V4;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t opos = o0 + e / V4;
+        const int c = (int)(e % V4);
+        const float4 v = ldg_f4(weight + (int64_t)__ldg(a.lrow + opos) * D + c * 4);
+        __stcg(reinterpret_cast<float4 *>(a.peer.gbuf[__ldg(a.osrc + opos)] + __ldg(a.roff + opos) + c * 4), v);
     }
 }
 
 // Per owned row requested this step (olist), the <= W pushed G rows (in this owner's receive
 // buffer) summed in source-rank order in fp64 (reading O6'), rounded once, Adagrad / lazy Adam.
-// RB rows per lane group at a time, all loads of a batch in flight together.
+// One thread per 16-B chunk of a row; the <= NFW contributions of a chunk are loaded together.
 template <int D, int NFW>
-__global__ void __launch_bounds__(256, 2) k_p2p_update(P2PArgs a, int pack, float *weight, float *state1,
-                                                       float *state2, int opt, float lr, float eps, float beta1,
-                                                       float beta2, float adam_ss) {
-    constexpr int V4 = D / 4, LANES = V4 < 32 ? V4 : 32, VPL = V4 / LANES;
-    constexpr int RB = VPL == 1 ? 2 : 1;    // owner positions per group iteration
-    constexpr int NF = VPL == 1 ? NFW : 2;  // sources per load batch (NFW >= W when it fits)
-    const int li = threadIdx.x % LANES;
-    const int64_t o0 = a.pack_ostart[pack], o1 = o0 + a.ocount[pack];
-    const int64_t rb = a.row_base[pack], fb = a.pack_fbase[pack];
-    const float *gin = a.peer.ogbuf[a.rank] + fb + li * 4;
-    const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / LANES;
-#pragma unroll 1
-    for (int64_t ob = o0 + grp * RB; ob < o1; ob += ngrp * RB) {
-        int64_t o[RB];
-        const int32_t *dt[RB];
-        float4 w[RB][VPL], s1[RB][VPL], s2[RB][VPL];
-        double g[RB][VPL][4];
+__global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *weight, float *state1,
+                                                    float *state2, int opt, float lr, float eps, float beta1,
+                                                    float beta2, float adam_ss) {
+    constexpr int V4 = D / 4;
+    const int64_t o0 = a.pack_ostart[pack];
+    const int64_t n = (int64_t)a.ocount[pack] * V4;
+    const int64_t rb = a.row_base[pack];
+    const float *gin = a.peer.ogbuf[a.rank] + a.pack_fbase[pack];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t row = __ldg(a.olist + o0 + e / V4);
+        const int c = (int)(e % V4);
+        const int32_t *dt = a.dtab + (rb + row) * a.W;
+        const int64_t o = (int64_t)row * D + c * 4;
+        float4 x[NFW];
+        int32_t op[NFW];
 #pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            o[r] = -1;
+        for (int s = 0; s < NFW; ++s) {
+            op[s] = s < a.W ? __ldg(dt + s) : -1;
+            if (op[s] >= 0) x[s] = __ldcg(reinterpret_cast<const float4 *>(gin + (op[s] - o0) * D + c * 4));
+        }
+        const float4 w4 = *reinterpret_cast<const float4 *>(weight + o);
+        const float4 a4 = *reinterpret_cast<const float4 *>(state1 + o);
+        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (opt == 1) v4 = *reinterpret_cast<const float4 *>(state2 + o);
+        double g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int q = 0; q < VPL; ++q) g[r][q][0] = g[r][q][1] = g[r][q][2] = g[r][q][3] = 0.0;
-            if (ob + r < o1) {
-                const int32_t row = a.olist[ob + r];
-                dt[r] = a.dtab + (rb + row) * a.W;
-                {
-                    o[r] = (int64_t)row * D + li * 4;
+        for (int s = 0; s < NFW; ++s)  // source rank ascending
+            if (op[s] >= 0) {
+                g[0] = __dadd_rn(g[0], (double)x[s].x);
+                g[1] = __dadd_rn(g[1], (double)x[s].y);
+                g[2] = __dadd_rn(g[2], (double)x[s].z);
+                g[3] = __dadd_rn(g[3], (double)x[s].w);
+            }
+        float ww[4] = {w4.x, w4.y, w4.z, w4.w};
+        float ss[4] = {a4.x, a4.y, a4.z, a4.w};
+        float v2[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-                    for (int q = 0; q < VPL; ++q) {
-                        w[r][q] = *reinterpret_cast<const float4 *>(weight + o[r] + q * LANES * 4);
-                        s1[r][q] = *reinterpret_cast<const float4 *>(state1 + o[r] + q * LANES * 4);
-                        if (opt == 1) s2[r][q] = *reinterpret_cast<const float4 *>(state2 + o[r] + q * LANES * 4);
-                    }
-                }
+        for (int k = 0; k < 4; ++k) {
+            const float gg = __double2float_rn(g[k]);
+            if (opt == 0) {
+                const float acc = __fadd_rn(ss[k], __fmul_rn(gg, gg));
+                ss[k] = acc;
+                ww[k] = __fsub_rn(ww[k], __fmul_rn(lr, __fdiv_rn(gg, __fadd_rn(__fsqrt_rn(acc), eps))));
+            } else {
+                const float mo = ss[k], vo = v2[k];
+                const float mu = __fmul_rn(__fsub_rn(gg, mo), __fsub_rn(1.0f, beta1));
+                const float vu = __fmul_rn(__fsub_rn(__fmul_rn(gg, gg), vo), __fsub_rn(1.0f, beta2));
+                const float mn = __fadd_rn(mu, mo), vn = __fadd_rn(vu, vo);
+                ss[k] = mn;
+                v2[k] = vn;
+                ww[k] = __fsub_rn(ww[k], __fmul_rn(adam_ss, __fdiv_rn(mn, __fadd_rn(__fsqrt_rn(vn), eps))));
             }
         }
-#pragma unroll 1
-        for (int s0 = 0; s0 < a.W; s0 += NF) {
-            float4 c[RB][NF][VPL];
-            int32_t op[RB][NF];
-#pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int k = 0; k < NF; ++k) {
-                    op[r][k] = (o[r] >= 0 && s0 + k < a.W) ? dt[r][s0 + k] : -1;
-                    if (op[r][k] >= 0) {
-                        const float *gr = gin + (op[r][k] - o0) * D;
-#pragma unroll
-                        for (int q = 0; q < VPL; ++q)
-                            c[r][k][q] = __ldcg(reinterpret_cast<const float4 *>(gr + q * LANES * 4));
-                    }
-                }
-#pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int k = 0; k < NF; ++k)  // source rank ascending
-                    if (op[r][k] >= 0)
-#pragma unroll
-                        for (int q = 0; q < VPL; ++q) {
-                            g[r][q][0] = __dadd_rn(g[r][q][0], (double)c[r][k][q].x);
-                            g[r][q][1] = __dadd_rn(g[r][q][1], (double)c[r][k][q].y);
-                            g[r][q][2] = __dadd_rn(g[r][q][2], (double)c[r][k][q].z);
-                            g[r][q][3] = __dadd_rn(g[r][q][3], (double)c[r][k][q].w);
-                        }
-        }
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            if (o[r] < 0) continue;
-#pragma unroll
-            for (int q = 0; q < VPL; ++q) {
-                float ww[4] = {w[r][q].x, w[r][q].y, w[r][q].z, w[r][q].w};
-                float ss[4] = {s1[r][q].x, s1[r][q].y, s1[r][q].z, s1[r][q].w};
-                float v2[4] = {0.f, 0.f, 0.f, 0.f};
-                if (opt == 1) {
-                    v2[0] = s2[r][q].x;
-                    v2[1] = s2[r][q].y;
-                    v2[2] = s2[r][q].z;
-                    v2[3] = s2[r][q].w;
-                }
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float gg = __double2float_rn(g[r][q][e]);
-                    if (opt == 0) {
-                        const float acc = __fadd_rn(ss[e], __fmul_rn(gg, gg));
-                        ss[e] = acc;
-                        ww[e] = __fsub_rn(ww[e], __fmul_rn(lr, __fdiv_rn(gg, __fadd_rn(__fsqrt_rn(acc), eps))));
-                    } else {
-                        const float mo = ss[e], vo = v2[e];
-                        const float mu = __fmul_rn(__fsub_rn(gg, mo), __fsub_rn(1.0f, beta1));
-                        const float vu = __fmul_rn(__fsub_rn(__fmul_rn(gg, gg), vo), __fsub_rn(1.0f, beta2));
-                        const float mn = __fadd_rn(mu, mo), vn = __fadd_rn(vu, vo);
-                        ss[e] = mn;
-                        v2[e] = vn;
-                        ww[e] = __fsub_rn(ww[e], __fmul_rn(adam_ss, __fdiv_rn(mn, __fadd_rn(__fsqrt_rn(vn), eps))));
-                    }
-                }
-                *reinterpret_cast<float4 *>(weight + o[r] + q * LANES * 4) = make_float4(ww[0], ww[1], ww[2], ww[3]);
-                *reinterpret_cast<float4 *>(state1 + o[r] + q * LANES * 4) = make_float4(ss[0], ss[1], ss[2], ss[3]);
-                if (opt == 1)
-                    *reinterpret_cast<float4 *>(state2 + o[r] + q * LANES * 4) =
-                        make_float4(v2[0], v2[1], v2[2], v2[3]);
-            }
-        }
+        *reinterpret_cast<float4 *>(weight + o) = make_float4(ww[0], ww[1], ww[2], ww[3]);
+        *reinterpret_cast<float4 *>(state1 + o) = make_float4(ss[0], ss[1], ss[2], ss[3]);
+        if (opt == 1) *reinterpret_cast<float4 *>(state2 + o) = make_float4(v2[0], v2[1], v2[2], v2[3]);
     }
 }
 
@@ -417,22 +355,22 @@ void launch_p2p_dst(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_dst<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s) {
-#define CALL(DD) k_p2p_gather<DD><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, weight, pack)
+#define CALL(DD) k_p2p_gather<DD><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack)
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
 }
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
                        float b1, float b2, float ss, int num_sms, cudaStream_t s) {
     if (a.W <= 2) {
-#define CALL(DD) k_p2p_update<DD, 2><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update<DD, 2><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
         PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
     } else if (a.W <= 4) {
-#define CALL(DD) k_p2p_update<DD, 4><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update<DD, 4><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
         PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
     } else {
-#define CALL(DD) k_p2p_update<DD, 8><<<(unsigned)num_sms * 8, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update<DD, 8><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
         PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
     }

@@ -161,8 +161,10 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
     launch_p2p_blocks(a, s);
     launch_p2p_insert(a, ctx->num_sms, s);
     launch_p2p_leaders(a, ctx->num_sms, s);
+    static const bool split = std::getenv("PICASSO_PROF_SPLIT") != nullptr;  // measurement aid
+    if (split) ctx->mark(4, false, s);
     for (int p = 0; p < P; ++p) launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
-    ctx->mark(4, false, s);
+    if (!split) ctx->mark(4, false, s);
     ctx->launches_fwd += 4 + P;
     PCK(cudaGetLastError());
     return PICASSO_OK;
@@ -307,6 +309,7 @@ void p2p_host_counts(picasso_ctx *ctx) {
     MultiState &mp = ctx->mp;
     if (!mp.p2p || !mp.cnt_send_h) return;
     cudaStreamSynchronize(ctx->last_stream);
+    cudaMemcpy(mp.cnt_send_h, mp.bcount, sizeof(int32_t) * (ctx->world * ctx->P + 1), cudaMemcpyDeviceToHost);
     const int W = ctx->world, P = ctx->P;
     mp.sk.assign(W, 0);
     int64_t tot = 0;

@@ -356,8 +356,9 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
 
 extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, const float *grad_out, float lr,
                                                            int64_t step, void *stream) {
-    if (!ctx || !grad_out || step < 1) return PICASSO_ERR_INVALID_ARG;
+    if (!ctx || step < 1) return PICASSO_ERR_INVALID_ARG;
     if (!ctx->bound || !ctx->fwd_done) return PICASSO_ERR_STATE;
+    if (!grad_out && ctx->B > 0) return PICASSO_ERR_INVALID_ARG;  // an empty batch has no dY
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ctx->launches_bwd = 0;
     if (ctx->world > 1) {

@@ -28,12 +28,25 @@ def main():
 
     name = sys.argv[1] if len(sys.argv) > 1 else "toy"
     cache = name.endswith("_cache")  # HybridHash on: refresh after step 1 (warm-up 1, flush 1)
-    base = name[:-6] if cache else name
-    cfg = dc.toy(alpha=1.2) if base == "toy" else dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    graph = name.endswith("_graph")  # one captured step (fixed batch) replayed 3 times
+    base = name[:-6] if (cache or graph) else name
+    if base == "toy":
+        cfg = dc.toy(alpha=1.2)
+    elif base == "criteo":  # D = 128: pipelined kernels, rows spanning tiles, P2P pushes
+        cfg = dc.scaled(dc.criteo(), batch=2048, rows_div=20000)
+    elif base == "uneven":  # per-rank batch sizes differ; the last rank has an empty batch
+        cfg = dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    else:
+        cfg = dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    bsz = [cfg.batch] * world
+    if base == "uneven":
+        bsz = [max(cfg.batch - 11 * r, 1) for r in range(world)]
+        bsz[-1] = 0
+    cfgs = [cfg.replace(batch=b) for b in bsz]
     obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     mi = cfg.batch * cfg.F * 60
-    e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=cfg.batch, max_ids=mi,
+    e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=max(cfg.batch, 1), max_ids=mi,
                            table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
                            rank=rank, world=world, nccl_uid=obj[0], max_recv=world * mi,
                            device=torch.device("cuda", local), cache_max_bytes=(1 << 20) if cache else 0)
@@ -42,16 +55,39 @@ def main():
     m, tabs = oracle_model(cfg), oracle_tables(cfg)
     acc = [np.full_like(t, 0.1) for t in tabs]
     report = {"rank": rank, "world": world, "ok": False}
+    gr = None
     for step in (1, 2, 3):
-        bs = [make_batch(cfg, r, step) for r in range(world)]
-        dys = [make_dy(cfg, r, step) for r in range(world)]
-        out = e.forward(torch.from_numpy(bs[rank].ids).cuda(), torch.from_numpy(bs[rank].offsets).cuda(), cfg.batch)
-        obs = [oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy) for b, dy in zip(bs, dys)]
+        bstep = 1 if graph else step
+        bs = [make_batch(cfgs[r], r, bstep) for r in range(world)]
+        dys = [make_dy(cfgs[r], r, bstep) for r in range(world)]
+        obs = [oracle.OracleBatch(cfgs[r].batch, b.ids, b.offsets, dy) for r, (b, dy) in enumerate(zip(bs, dys))]
         ref = oracle.forward(m, obs[rank], tabs, cfg.out_width)
-        assert np.array_equal(out.cpu().numpy(), ref), f"forward step {step}"
-        e.backward_update(torch.from_numpy(dys[rank]).cuda(), lr=0.05, step=step)
+        if graph:  # static buffers, captured once; every replay is a full row-sharded step
+            if gr is None:
+                ids_s = torch.from_numpy(bs[rank].ids).cuda()
+                off_s = torch.from_numpy(bs[rank].offsets).cuda()
+                dy_s = torch.from_numpy(dys[rank]).cuda()
+                out = torch.empty(bsz[rank], e.out_width, device="cuda")
+                e.forward(ids_s, off_s, bsz[rank], out)  # warm-up outside the capture (step 1 itself)
+                e.backward_update(dy_s, lr=0.05, step=1)
+                torch.cuda.synchronize()
+                gr = torch.cuda.CUDAGraph()
+                cap = torch.cuda.Stream()
+                with torch.cuda.graph(gr, stream=cap):
+                    e.forward(ids_s, off_s, bsz[rank], out, stream=cap)
+                    e.backward_update(dy_s, lr=0.05, step=1, stream=cap)
+            else:
+                gr.replay()
+            torch.cuda.synchronize()
+        else:
+            out = e.forward(torch.from_numpy(bs[rank].ids).cuda(), torch.from_numpy(bs[rank].offsets).cuda(),
+                            bsz[rank])
+        if not graph or step == 1:
+            assert np.array_equal(out.cpu().numpy(), ref), f"forward step {step}"
+        if not graph:
+            e.backward_update(torch.from_numpy(dys[rank]).cuda(), lr=0.05, step=step)
         e.check()
-        oracle.backward_update(m, obs, tabs, acc, lr=0.05, step=step)
+        oracle.backward_update(m, obs, tabs, acc, lr=0.05, step=1 if graph else step)
         if cache:  # the shards are authoritative only after a write-back: refresh every step
             stats = e.hot_cache_refresh(8 * 1024 if step < 3 else 0)
             report[f"stats{step}"] = stats

@@ -12,11 +12,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
-@pytest.mark.parametrize("name", ["toy", "wdl", "toy_cache", "wdl_cache"])
+@pytest.mark.parametrize("name", ["toy", "wdl", "toy_cache", "wdl_cache", "criteo", "uneven", "toy_graph",
+                                  "criteo_graph"])
 def test_nccl_sharded_parity(name, exchange):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
+    if name.endswith("_graph") and exchange == "nccl":
+        pytest.skip("the NCCL exchange synchronises with the host inside a step: not capturable")
     import __graft_entry__
 
     __graft_entry__.build()
