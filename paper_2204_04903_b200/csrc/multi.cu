@@ -87,6 +87,101 @@ __global__ void k_send_prep(MultiArgs m) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Partition for the peer-memory exchange.  There the owner reads a requester's bucket (r, p)
+// by slot index and sums contributions in source order, so the order of the slots inside a
+// bucket is free: counts with warp-aggregated atomics, then placement with per-bucket cursors
+// (two passes over the uniques, no sort).  Results do not depend on the slot order.
+__device__ __forceinline__ int32_t bucket_of(const MultiArgs &m, int64_t u, int64_t &p, uint64_t &key) {
+    p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
+    key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
+    if (m.hot_k > 0 && m.hslot[u] >= 0) return m.W * m.P;  // hot: served by the replica
+    return (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
+}
+
+// one atomic per (warp, bucket); returns this lane's rank among the lanes of its bucket
+__device__ __forceinline__ int32_t warp_agg_add(int32_t *ctr, int32_t b, bool active) {
+    const unsigned am = __ballot_sync(0xffffffffu, active);
+    int32_t r = 0;
+    if (active) {
+        const int lane = threadIdx.x & 31;
+        const unsigned peers = __match_any_sync(am, b);
+        const int first = __ffs(peers) - 1;
+        int32_t base = 0;
+        if (lane == first) base = atomicAdd(ctr + b, __popc(peers));
+        base = __shfl_sync(peers, base, first);
+        r = base + __popc(peers & ((1u << lane) - 1u));
+    }
+    return r;
+}
+
+__global__ void k_part_count(MultiArgs m) {
+    const int32_t U = *m.d_total;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < U;
+         b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = b0 + (threadIdx.x & 31);
+        int32_t b = 0;
+        if (u < U) {
+            int64_t p;
+            uint64_t key;
+            b = bucket_of(m, u, p, key);
+            m.bkey[u] = b;
+        }
+        warp_agg_add(m.bcount, b, u < U);
+    }
+}
+
+__global__ void k_part_place(MultiArgs m) {
+    __shared__ int64_t s_start[kMaxOwnerBlocks + 1], s_foff[kMaxOwnerBlocks + 1];
+    const int nb = m.W * m.P;
+    if (threadIdx.x == 0) {  // bucket starts (slots) and float offsets (rows buffer), every block
+        int64_t e = 0, f = 0;
+        for (int b = 0; b < nb; ++b) {
+            s_start[b] = e;
+            s_foff[b] = f;
+            const int32_t c = m.bcount[b];
+            e += c;
+            f += (int64_t)c * m.pack_dim[b % m.P];
+        }
+        s_start[nb] = e;
+        s_foff[nb] = f;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+            m.bstart[b] = s_start[b];
+            m.sroff[b] = s_foff[b];
+        }
+    const int32_t U = *m.d_total;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < U;
+         b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = b0 + (threadIdx.x & 31);
+        const bool valid = u < U;
+        int32_t b = nb;
+        int64_t p = 0;
+        uint64_t key = 0;
+        if (valid) {
+            b = m.bkey[u];
+            p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
+            key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
+        }
+        const bool cold = valid && b < nb;
+        const int32_t j = warp_agg_add(m.cursor, b, cold);
+        if (!valid) continue;
+        if (!cold) {  // hot: row of the local replica (offset relative to the rows buffer)
+            const int32_t hs = m.hslot[u];
+            m.send_pos[u] = -1;
+            m.row_off[u] = (int64_t)((m.hot_arena + m.hot_w_off[p] + (int64_t)(hs - m.hot_pslot[p]) * m.pack_dim[p]) -
+                                     m.gbuf_base);
+            continue;
+        }
+        const int64_t i = s_start[b] + j;
+        m.send_pos[u] = (int32_t)i;
+        m.send_keys[i] = (int32_t)(key / (uint64_t)m.W);
+        m.row_off[u] = s_foff[b] + (int64_t)j * m.pack_dim[p];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // owner stream position -> block (pack-major (p, src)) by a search over the block table
 __device__ __forceinline__ int owner_block(const OwnerBlock *blk, int nb, int64_t opos) {
     int lo = 0, hi = nb;
@@ -276,6 +371,12 @@ void launch_bucket(const MultiArgs &m, cudaStream_t s) {
 void launch_bucket_prefix(const MultiArgs &m, cudaStream_t s) { k_bucket_prefix<<<1, 32, 0, s>>>(m); }
 void launch_send_prep(const MultiArgs &m, int num_sms, cudaStream_t s) {
     k_send_prep<<<(unsigned)num_sms * 4, 256, 0, s>>>(m);
+}
+void launch_partition_p2p(const MultiArgs &m, int num_sms, cudaStream_t s) {
+    cudaMemsetAsync(m.bcount, 0, sizeof(int32_t) * (m.W * m.P + 1), s);
+    cudaMemsetAsync(m.cursor, 0, sizeof(int32_t) * (m.W * m.P + 1), s);
+    k_part_count<<<(unsigned)num_sms * 4, 256, 0, s>>>(m);
+    k_part_place<<<(unsigned)num_sms * 4, 256, 0, s>>>(m);
 }
 void launch_owner_insert(const MultiArgs &m, Slot *table, uint32_t cap_mask, int *err, cudaStream_t s) {
     if (m.R > 0) k_owner_insert<<<(unsigned)((m.R + 255) / 256), 256, 0, s>>>(m, table, cap_mask, err);

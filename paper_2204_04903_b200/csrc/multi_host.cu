@@ -63,6 +63,7 @@ static MultiArgs multi_args(picasso_ctx *ctx) {
     m.bval = mp.bval;
     m.bhist = mp.bhist;
     m.bcount = mp.bcount;
+    m.cursor = mp.bhist;  // scratch: the peer-memory partition does not use the bucket histogram
     m.bstart = mp.bstart;
     m.sroff = mp.sroff;
     m.send_uid = mp.send_uid;
@@ -127,11 +128,15 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
     launch_dedup_assign(a, s);
     MultiArgs m = multi_args(ctx);
     if (mp.hot_k > 0) launch_hot_probe(m, ctx->num_sms, s);  // hot keys skip the exchange
-    launch_bucket(m, s);
-    bucket_sort_pass(mp.bkey, mp.bval, mp.bsorted, mp.send_uid, std::max<int64_t>(N, 1), ctx->d_total,
-                     m.bucket_bits, mp.bhist, mp.bcount, s);
-    launch_bucket_prefix(m, s);
-    launch_send_prep(m, ctx->num_sms, s);
+    if (mp.p2p) {  // slot order inside a bucket is free: counts + placement, no sort
+        launch_partition_p2p(m, ctx->num_sms, s);
+    } else {       // first-occurrence order inside a bucket (the owner dedup's order, reading O2)
+        launch_bucket(m, s);
+        bucket_sort_pass(mp.bkey, mp.bval, mp.bsorted, mp.send_uid, std::max<int64_t>(N, 1), ctx->d_total,
+                         m.bucket_bits, mp.bhist, mp.bcount, s);
+        launch_bucket_prefix(m, s);
+        launch_send_prep(m, ctx->num_sms, s);
+    }
     // bucket counts (+ the hot bucket: the hit statistic of HybridHash); the peer-memory driver
     // never needs them on the host inside a step (p2p_host_counts copies them on request)
     if (!mp.p2p)

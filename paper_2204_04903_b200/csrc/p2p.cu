@@ -3,15 +3,15 @@
 // Every rank exposes one IPC-shared window: barrier flags, its bucket counts, its send list
 // (requested local rows, owner-major), and its rows/G buffer in the send layout.  The owner
 // side then needs no staged all-to-all (SURVEY §8(f) "kernel-initiated Shuffle&Stitch"):
-//   k_p2p_blocks : owner block table from the peers' bucket counts (device-side sizes: no host
-//                  synchronisation, so the whole step can be captured in a CUDA graph)
-//   k_p2p_insert : reads each requested key straight from the requester's send list (NVLink
-//                  loads) and inserts it in the owner hash (first occurrence, as k_owner_insert)
+//   k_p2p_tables : owner block table and G-slot bases from every rank's bucket counts (device-
+//                  side sizes: no host synchronisation, so a step can be captured in a CUDA graph)
+//   k_p2p_dst_insert : requester side, each unique row's G slot at its owner; owner side, each
+//                  requested key read straight from the requester's send list (NVLink loads)
+//                  into a direct (row, source) table (k_p2p_leaders lists each row once)
 //   k_p2p_gather : gathers the owner's rows and stores them straight into each requester's rows
 //                  buffer at the slot its send layout reserved (NVLink stores): Gather + Shuffle
 //                  + Stitch in one kernel, the transfer overlapping the gather row by row
-//   k_p2p_dst    : requester side: the owner receive-buffer slot of each unique row's G, so the
-//                  segment-sum kernels store G straight into the owner's memory (NVLink stores:
+//   (segment-sum) : stores each G row at its slot in the owner's memory (NVLink stores:
 //                  segment-sum + gradient Shuffle in one kernel)
 //   k_p2p_update : per owner-unique row, the <= W pushed G rows summed in source-rank order
 //                  (fp64, reading O6') and the optimizer applied
@@ -63,29 +63,47 @@ __global__ void k_p2p_wait(P2PArgs a, int phase) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Owner block table, pack-major (pack p, source s): ostart (owner-stream position), rstart =
-// index of the block's first key in s's send list, rroff = float offset of its first row in s's
-// rows buffer.  One block of W*P <= 1024 threads.
-__global__ void __launch_bounds__(1024) k_p2p_blocks(P2PArgs a) {
+// Both sides' tables from every rank's bucket counts, staged once in shared memory (one NVLink
+// round trip for the whole W x (W*P) count matrix).  One block of 1024 threads.
+//  owner side, pack-major blocks (pack p, source s): ostart (owner-stream position), rstart =
+//    index of the block's first key in s's send list, rroff = float offset of its first row in
+//    s's rows buffer; pack starts, received count R, float layout of the received G rows;
+//  requester side: dbase[(r, p)] = float offset of my requests' G block in owner r's receive
+//    buffer (owner r holds pack p's requests pack-major, then by source rank).
+__global__ void __launch_bounds__(1024) k_p2p_tables(P2PArgs a) {
+    __shared__ int32_t cm[kP2PMaxW][kMaxOwnerBlocks];  // cm[s][b]: source s's count of bucket b
     __shared__ int32_t wsum[32];
     __shared__ int64_t s_total;
     const int t = threadIdx.x, nb = a.W * a.P;
+    for (int e = t; e < a.W * nb; e += blockDim.x) cm[e / nb][e % nb] = __ldcv(a.peer.bcount[e / nb] + e % nb);
+    __syncthreads();
+    // requester side
+    if (t < nb) {
+        const int r = t / a.P, p = t - (t / a.P) * a.P;
+        int64_t f = 0;
+        for (int q = 0; q < p; ++q) {  // packs before p at owner r, all sources
+            int64_t n = 0;
+            for (int s = 0; s < a.W; ++s) n += cm[s][r * a.P + q];
+            f += n * __ldg(a.pack_dim + q);
+        }
+        int64_t before = 0;  // sources before me, same pack
+        for (int s = 0; s < a.rank; ++s) before += cm[s][t];
+        a.dbase[t] = f + before * __ldg(a.pack_dim + p);
+    }
+    // owner side
     const int p = t / a.W, s = t - (t / a.W) * a.W;
     int32_t c = 0;
     int64_t ks = 0, gs = 0;
     if (t < nb) {
-        const int32_t *bc = a.peer.bcount[s];
         const int me = a.rank * a.P + p;
         for (int b = 0; b < me; ++b) {  // s's buckets before (rank, p): owner-major, then pack
-            const int32_t x = __ldcv(bc + b);
-            ks += x;
-            gs += (int64_t)x * __ldg(a.pack_dim + (b % a.P));
+            ks += cm[s][b];
+            gs += (int64_t)cm[s][b] * __ldg(a.pack_dim + (b % a.P));
         }
-        c = __ldcv(bc + me);
+        c = cm[s][me];
         a.cnt_recv[s * a.P + p] = c;
     }
-    // block exclusive scan of c in t order
-    const int lane = t & 31, w = t >> 5;
+    const int lane = t & 31, w = t >> 5;  // block exclusive scan of c in t order
     int32_t x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -139,36 +157,6 @@ __global__ void __launch_bounds__(1024) k_p2p_blocks(P2PArgs a) {
     }
 }
 
-// Requester side: where each of my unique rows' G goes.  Owner r holds my requests of pack p
-// at owner positions pack_ostart_r(p) + sum_{s < me} count_s(r, p) + j, j = my slot index in
-// bucket (r, p); its G rows are pack-major with D_p floats each.  dbase[(r, p)] = float offset
-// of my block in r's receive buffer (from every rank's bucket counts).  One block.
-__global__ void __launch_bounds__(1024) k_p2p_dst_base(P2PArgs a) {
-    const int t = threadIdx.x;
-    if (t >= a.W * a.P) return;
-    const int r = t / a.P, p = t - (t / a.P) * a.P;
-    int64_t f = 0;
-    for (int q = 0; q < p; ++q) {  // packs before p at owner r, all sources
-        int64_t n = 0;
-        for (int s = 0; s < a.W; ++s) n += __ldcv(a.peer.bcount[s] + r * a.P + q);
-        f += n * __ldg(a.pack_dim + q);
-    }
-    int64_t before = 0;  // sources before me, same pack
-    for (int s = 0; s < a.rank; ++s) before += __ldcv(a.peer.bcount[s] + r * a.P + p);
-    a.dbase[t] = f + before * __ldg(a.pack_dim + p);
-}
-
-__global__ void k_p2p_dst(P2PArgs a) {
-    const int32_t U = *a.d_total;
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = a.bkey[u];  // bucket (owner, pack) from the Partition pass
-        if (b >= a.W * a.P) continue;  // hot: G goes to the replicated hot buffer
-        const int p = b % a.P;
-        a.dst_rank[u] = b / a.P;
-        a.dst_off[u] = a.dbase[b] + (a.send_pos[u] - a.bstart[b]) * __ldg(a.pack_dim + p);
-    }
-}
-
 __device__ __forceinline__ int owner_block_p(const OwnerBlock *blk, int nb, int64_t opos) {
     int lo = 0, hi = nb;
     while (hi - lo > 1) {
@@ -178,17 +166,27 @@ __device__ __forceinline__ int owner_block_p(const OwnerBlock *blk, int nb, int6
     return lo;
 }
 
-// Requested key -> owner tables, per owner position: local row, source, float offset of the
-// requester's row slot; dtab[(row_base[p] + row) * W + src] = the position (each requester
-// asks for a key at most once, so (row, src) is unique: a direct table replaces the owner hash).
-__global__ void __launch_bounds__(256) k_p2p_insert(P2PArgs a) {
+// One launch, two index ranges.  e < U (requester side): the owner receive-buffer slot of my
+// unique row e's G (k_segsum_pipe stores it there).  e >= U (owner side, opos = e - U): the
+// requested key read from the requester's send list (NVLink load); per owner position: local
+// row, source, float offset of the requester's row slot; dtab[(row_base[p] + row) * W + src] =
+// opos (each requester asks for a key at most once, so (row, src) is unique: a direct table
+// replaces the owner hash).
+__global__ void __launch_bounds__(256) k_p2p_dst_insert(P2PArgs a) {
     __shared__ OwnerBlock sb[kMaxOwnerBlocks];
     const int nb = a.W * a.P;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sb[i] = a.oblk[i];
     __syncthreads();
-    const int64_t R = *a.R;
-    for (int64_t opos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; opos < R;
-         opos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t U = *a.d_total, R = *a.R;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < U + R; e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < U) {
+            const int32_t b = a.bkey[e];  // bucket (owner, pack) from the Partition pass
+            if (b >= nb) continue;        // hot: G goes to the replicated hot buffer
+            a.dst_rank[e] = b / a.P;
+            a.dst_off[e] = a.dbase[b] + (a.send_pos[e] - a.bstart[b]) * __ldg(a.pack_dim + (b % a.P));
+            continue;
+        }
+        const int64_t opos = e - U;
         const int k = owner_block_p(sb, nb, opos);
         const int64_t j = opos - sb[k].ostart;
         const int p = sb[k].pack, src = sb[k].src;
@@ -340,19 +338,15 @@ __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *
 
 void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s) { k_p2p_signal<<<1, 32, 0, s>>>(a, phase); }
 void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s) { k_p2p_wait<<<1, 32, 0, s>>>(a, phase); }
-void launch_p2p_blocks(const P2PArgs &a, cudaStream_t s) { k_p2p_blocks<<<1, 1024, 0, s>>>(a); }
-void launch_p2p_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
-    k_p2p_insert<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
+void launch_p2p_tables(const P2PArgs &a, cudaStream_t s) { k_p2p_tables<<<1, 1024, 0, s>>>(a); }
+void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
+    k_p2p_dst_insert<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
 void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_leaders<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_reset<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
-}
-void launch_p2p_dst(const P2PArgs &a, int num_sms, cudaStream_t s) {
-    k_p2p_dst_base<<<1, 1024, 0, s>>>(a);
-    k_p2p_dst<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s) {
 #define CALL(DD) k_p2p_gather<DD><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack)

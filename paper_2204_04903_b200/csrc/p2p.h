@@ -56,12 +56,11 @@ struct P2PArgs {
 
 void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s);
 void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s);
-void launch_p2p_blocks(const P2PArgs &a, cudaStream_t s);
-void launch_p2p_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
+void launch_p2p_tables(const P2PArgs &a, cudaStream_t s);
+void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s);
-void launch_p2p_dst(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
                        float b1, float b2, float ss, int num_sms, cudaStream_t s);
 

@@ -142,14 +142,6 @@ void barrier(picasso_ctx *ctx, int phase, cudaStream_t s) {
     ctx->launches_fwd += 2;
 }
 
-// ---- requester side: owner receive slots of this rank's G rows (after barrier 0) ------------
-picasso_status p2p_dst(picasso_ctx *ctx, cudaStream_t s) {
-    launch_p2p_dst(make_p2p_args(ctx), ctx->num_sms, s);
-    ctx->launches_fwd += 2;
-    PCK(cudaGetLastError());
-    return PICASSO_OK;
-}
-
 // ---- C': owner side --------------------------------------------------------------------------
 picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
     MultiState &mp = ctx->mp;
@@ -158,8 +150,8 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
     const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
     ctx->mark(4, true, s);
     launch_p2p_reset(a, ctx->num_sms, s);  // the previous forward's direct-table entries
-    launch_p2p_blocks(a, s);
-    launch_p2p_insert(a, ctx->num_sms, s);
+    launch_p2p_tables(a, s);
+    launch_p2p_dst_insert(a, ctx->num_sms, s);
     launch_p2p_leaders(a, ctx->num_sms, s);
     static const bool split = std::getenv("PICASSO_PROF_SPLIT") != nullptr;  // measurement aid
     if (split) ctx->mark(4, false, s);
@@ -200,7 +192,6 @@ picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t
     picasso_status st;
     if ((st = mfwd_a(ctx, ids, offsets, B, N, s))) return st;
     barrier(ctx, 0, s);
-    if ((st = p2p_dst(ctx, s))) return st;
     if ((st = p2p_c(ctx, s))) return st;
     barrier(ctx, 1, s);
     return mfwd_d(ctx, out, s);
@@ -226,8 +217,6 @@ picasso_status group_fwd_p2p(picasso_group *g, const int64_t *const *ids, const 
     picasso_status st;
     for (int r = 0; r < W; ++r)
         if ((st = mfwd_a(g->ctx[r], ids[r], offsets[r], batch[r], n_ids[r], s))) return st;
-    for (int r = 0; r < W; ++r)
-        if ((st = p2p_dst(g->ctx[r], s))) return st;
     for (int r = 0; r < W; ++r)
         if ((st = p2p_c(g->ctx[r], s))) return st;
     for (int r = 0; r < W; ++r)
