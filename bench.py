@@ -235,7 +235,7 @@ def main():
         uid = obj[0]
     emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=B, max_ids=max_ids,
                              table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
-                             device=dev, rank=rank, world=world, nccl_uid=uid, max_recv=2 * max_ids,
+                             device=dev, rank=rank, world=world, nccl_uid=uid, max_recv=max_ids,
                              cache_max_bytes=args.cache_bytes if world > 1 else 0)
     init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights,
                            rank=rank, world=world)
@@ -345,6 +345,25 @@ def main():
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(cfg.name, {}).get(dom)
 
+    # ---------------- NVLink traffic of the exchange (W > 1): bytes this rank pushed per step
+    nvlink = None
+    if world > 1:
+        sent = emb.send_counts()  # keys this rank requested from each owner, last step
+        allsent = [None] * world
+        dist.all_gather_object(allsent, sent)
+        dims = sorted(set(int(d) for d in emb.plan["pack_dim"]))
+        row_b = 4 * dims[0] if len(dims) == 1 else None  # bytes per row (single-dim workloads)
+        if row_b:
+            rows_out = sum(allsent[q][rank] for q in range(world) if q != rank) * row_b  # owner -> requesters
+            g_out = sum(sent[q] for q in range(world) if q != rank) * row_b              # requester -> owners
+            tg = per_phase.get("owner_gather", 0.0) * 1e-3
+            ts = per_phase.get("segsum", 0.0) * 1e-3
+            nvlink = {"rows_push_bytes": int(rows_out), "rows_push_gbs": rows_out / tg / 1e9 if tg else None,
+                      "g_push_bytes": int(g_out), "g_push_gbs": g_out / ts / 1e9 if ts else None,
+                      "peak_gbs_per_direction": 900.0,
+                      "note": "rank 0, last step; GB/s over the phase that issues the peer stores "
+                              "(owner gather / segment-sum), so a lower bound on link use"}
+
     # ---------------- end-to-end through the public API with host buffers
     host_ids = [torch.from_numpy(b.ids).pin_memory() for b in batches]
     host_off = [torch.from_numpy(b.offsets).pin_memory() for b in batches]
@@ -407,6 +426,7 @@ def main():
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
                          "peak_source": peak_src},
             "phases_ms": per_phase,
+            "nvlink": nvlink,
             "cache": ({"bytes_per_gpu": args.cache_bytes, "warmup_iters": args.cache_warmup,
                        "flush_iters": args.cache_flush, **cache_stats} if args.cache_bytes and world > 1 else None),
             "outside_phases_ms": ms - sum(per_phase.values()),  # exchanges + host sync (W > 1), launch gaps

@@ -104,6 +104,9 @@ typedef struct {
                               (0 = 2 * max_ids); exceeding it fails the step with CAPACITY */
     int64_t cache_max_bytes; /* world > 1: largest hot-storage capacity picasso_hot_cache_refresh
                               will be asked for (0 = no HybridHash: no FCounter, no hot rows) */
+    int32_t exchange;        /* world > 1: 0 = NVLink peer memory (section 7; the rows / G buffers
+                              live in the IPC window, not the workspace), 1 = NCCL AllToAllv
+                              (section 5; loopback: device copies) */
 } picasso_ctx_opts;
 
 /* NCCL unique id (128 bytes, host) for picasso_ctx_create; rank 0 calls it and broadcasts

@@ -43,7 +43,7 @@ class PlanView(C.Structure):
 class CtxOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_ids", C.c_int64), ("pool", C.c_int32), ("id_mode", C.c_int32),
                 ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
-                ("max_recv", C.c_int64), ("cache_max_bytes", C.c_int64)]
+                ("max_recv", C.c_int64), ("cache_max_bytes", C.c_int64), ("exchange", C.c_int32)]
 
 
 class CacheStats(C.Structure):
@@ -156,7 +156,7 @@ def picasso_nccl_unique_id():
 
 def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, field_col, out_width, rank, world,
                        max_batch, max_ids, pool=POOL_SUM, id_mode=IDS_HASH, opt=OPT_ADAGRAD, eps=None, beta1=0.9,
-                       beta2=0.999, nccl_uid=None, max_recv=0, cache_max_bytes=0):
+                       beta2=0.999, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange="p2p"):
     k = _Keep()
     k.f2t = _np(field_to_table, np.int32)
     k.t2p = _np(plan["table_to_pack"], np.int32)
@@ -171,7 +171,7 @@ def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, 
     if eps is None:
         eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
     o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),
-                float(beta2), int(max_recv), int(cache_max_bytes))
+                float(beta2), int(max_recv), int(cache_max_bytes), 0 if exchange == "p2p" else 1)
     ctx = C.c_void_p()
     uid = None if nccl_uid is None else (C.c_uint8 * 128)(*nccl_uid)
     _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), uid, C.byref(o), C.byref(ctx)),

@@ -259,7 +259,9 @@ struct picasso_ctx {
         chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
         pack_gbase = c.take<int64_t>(P + 1);
         pack_dim_d = c.take<int32_t>(P);
-        gbuf = (split_bwd || world > 1) ? c.take<float>((size_t)N * maxD) : nullptr;
+        // rows / G buffer: the IPC window holds it with the peer-memory exchange
+        const bool p2p_ex = world > 1 && opts.exchange == 0;
+        gbuf = ((split_bwd && world == 1) || (world > 1 && !p2p_ex)) ? c.take<float>((size_t)N * maxD) : nullptr;
         if (world > 1) {
             const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
             const int WP = world * P;
@@ -296,7 +298,7 @@ struct picasso_ctx {
             mp.dst_rank = c.take<int32_t>(N);
             mp.dst_off = c.take<int64_t>(N);
             mp.rsend_off = c.take<int64_t>(RM);
-            mp.rows_send = c.take<float>((size_t)RM * maxD);
+            mp.rows_send = p2p_ex ? nullptr : c.take<float>((size_t)RM * maxD);  // NCCL staging only
             osort_hist = c.take<int32_t>(2 * ((RM + kTile - 1) / kTile) + 2);
             mp.epoch_d = c.take<uint32_t>(kP2PPhases);
             mp.R_d = c.take<int32_t>(1);

@@ -482,6 +482,7 @@ extern "C" picasso_status picasso_group_fwd(picasso_group *g, const int64_t *con
         if (batch[r] > c->opts.max_batch || n_ids[r] > c->opts.max_ids) return PICASSO_ERR_CAPACITY;
         c->launches_fwd = 0;
         if (c->mp.p2p) continue;
+        if (c->opts.exchange == 0) return PICASSO_ERR_STATE;  // picasso_group_p2p not called
         if ((st = mfwd_a(c, ids[r], offsets[r], batch[r], n_ids[r], s))) return st;
     }
     if (g->ctx[0]->mp.p2p) return group_fwd_p2p(g, ids, offsets, batch, n_ids, out, s);

@@ -238,7 +238,8 @@ picasso_status group_bwd_p2p(picasso_group *g, const float *const *grad_out, flo
 
 // ---- C ABI: window exchange ------------------------------------------------------------------
 extern "C" picasso_status picasso_p2p_handle(picasso_ctx *ctx, void *handle_out) {
-    if (!ctx || !handle_out || ctx->world < 2 || !ctx->bound || ctx->mp.group) return PICASSO_ERR_INVALID_ARG;
+    if (!ctx || !handle_out || ctx->world < 2 || !ctx->bound || ctx->mp.group || ctx->opts.exchange != 0)
+        return PICASSO_ERR_INVALID_ARG;
     picasso_status st = window_alloc(ctx);
     if (st) return st;
     cudaIpcMemHandle_t h;
@@ -267,6 +268,8 @@ extern "C" picasso_status picasso_p2p_open(picasso_ctx *ctx, const void *handles
 
 extern "C" picasso_status picasso_group_p2p(picasso_group *g) {
     if (!g || g->ctx.empty()) return PICASSO_ERR_INVALID_ARG;
+    for (auto *ctx : g->ctx)
+        if (ctx->opts.exchange != 0) return PICASSO_ERR_INVALID_ARG;
     for (auto *ctx : g->ctx) {
         picasso_status st = window_alloc(ctx);
         if (st) return st;

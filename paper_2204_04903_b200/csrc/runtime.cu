@@ -41,7 +41,8 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (world < 1 || world > 8 || rank < 0 || rank >= world) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_batch <= 0 || opts->max_ids < 0 || opts->max_ids >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_recv < 0 || opts->max_recv >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
-    if (opts->pool < 0 || opts->pool > 1 || opts->id_mode < 0 || opts->id_mode > 1 || opts->opt < 0 || opts->opt > 1)
+    if (opts->pool < 0 || opts->pool > 1 || opts->id_mode < 0 || opts->id_mode > 1 || opts->opt < 0 || opts->opt > 1 ||
+        opts->exchange < 0 || opts->exchange > 1)
         return PICASSO_ERR_INVALID_ARG;
     if ((int64_t)plan->n_fields * opts->max_batch >= ((int64_t)1 << 31)) return PICASSO_ERR_INVALID_ARG;
     if ((int64_t)world * plan->n_packs > kMaxOwnerBlocks) return PICASSO_ERR_INVALID_ARG;
@@ -321,6 +322,10 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     ctx->launches_fwd = 0;
     if (ctx->world > 1) {
         if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_fwd
+        if (ctx->opts.exchange == 0 && !ctx->mp.p2p) {
+            ctx->last_msg = "peer-memory exchange: picasso_p2p_handle / picasso_p2p_open not done";
+            return PICASSO_ERR_STATE;
+        }
         return ctx->mp.p2p ? multi_fwd_p2p(ctx, ids, offsets, batch, n_ids, out, s)
                            : multi_fwd_nccl(ctx, ids, offsets, batch, n_ids, out, s);
     }

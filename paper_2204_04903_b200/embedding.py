@@ -38,11 +38,12 @@ class PackedEmbedding:
         self.plan = abi.picasso_pack_plan(self.f2t, self.rows, self.dims, warmup_count, split)
         self.opt = opt
         self.rank, self.world = rank, world
+        self.exchange = exchange or default_exchange()
         self.device = torch.device(device)
         self.ctx = abi.picasso_ctx_create(self.plan, self.f2t, self.rows, self.dims, table_salt, self.field_col,
                                           self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
                                           eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv,
-                                          cache_max_bytes=cache_max_bytes)
+                                          cache_max_bytes=cache_max_bytes, exchange=self.exchange)
         P = self.plan["n_packs"]
         self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
         ws = abi.picasso_workspace_size(self.ctx)
@@ -60,7 +61,6 @@ class PackedEmbedding:
         # world > 1, one process per GPU: the exchange runs over NVLink peer memory ("p2p", the
         # default) or NCCL AllToAllv ("nccl").  all_gather(bytes) -> [bytes] * world shares the
         # windows' IPC handles (default: torch.distributed.all_gather_object).
-        self.exchange = exchange or default_exchange()
         if world > 1 and nccl_uid is not None and self.exchange == "p2p":
             h = abi.picasso_p2p_handle(self.ctx)
             if all_gather is None:
@@ -144,10 +144,10 @@ class LoopbackGroup:
 
     def __init__(self, world, field_to_table, table_rows, table_dim, exchange=None, **kw):
         self.world = world
-        self.ranks = [PackedEmbedding(field_to_table, table_rows, table_dim, rank=r, world=world, **kw)
-                      for r in range(world)]
-        self.group = abi.picasso_group_create([e.ctx for e in self.ranks])
         self.exchange = exchange or default_exchange()
+        self.ranks = [PackedEmbedding(field_to_table, table_rows, table_dim, rank=r, world=world,
+                                      exchange=self.exchange, **kw) for r in range(world)]
+        self.group = abi.picasso_group_create([e.ctx for e in self.ranks])
         if self.exchange == "p2p":  # the peer-memory kernels, windows as plain pointers
             abi.picasso_group_p2p(self.group)
 
