@@ -143,6 +143,7 @@ struct picasso_ctx {
     int32_t *pack_ustart = nullptr;
     Slot *table = nullptr;
     int32_t *slot_of = nullptr, *seg_of = nullptr, *inverse = nullptr;
+    uint8_t *fmask = nullptr;  // first-occurrence flags (k_flag_count -> k_assign)
     int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
     int *err = nullptr;
     unsigned long long *unique_gkey = nullptr;
@@ -232,6 +233,7 @@ struct picasso_ctx {
         pack_ustart = c.take<int32_t>(P + 1);
         table = c.take<Slot>(cap);
         slot_of = c.take<int32_t>(N);
+        fmask = c.take<uint8_t>(NR / 8 + 2);
         seg_of = c.take<int32_t>(N);
         inverse = c.take<int32_t>(N);
         blk_cnt = c.take<int32_t>(nblk);

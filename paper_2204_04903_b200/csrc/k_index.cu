@@ -131,12 +131,20 @@ __global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
     __shared__ typename BlockReduce::TempStorage tmp;
     const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    int32_t slot[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) slot[i] = g0 + i < N ? __ldg(a.slot_of + g0 + i) : 0;
     int32_t c = 0;
+    uint32_t m = 0;  // first-occurrence flags of this thread's 8 positions (k_assign reads them)
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;
-        if (g < N) c += (a.table[a.slot_of[g]].minpos == (unsigned int)g);
+        if (g < N && a.table[slot[i]].minpos == (unsigned int)g) {
+            ++c;
+            m |= 1u << i;
+        }
     }
+    if (g0 < N) a.fmask[g0 / kItems] = (uint8_t)m;
     const int32_t tot = BlockReduce(tmp).Sum(c);
     if (threadIdx.x == 0) a.blk_cnt[blockIdx.x] = tot;
 }
@@ -149,22 +157,15 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
     int32_t slot[kItems];
     bool first[kItems];
     unsigned long long key[kItems];
-    int32_t c = 0;
-    // all table reads before any table write: stores to table[] would otherwise order every
-    // later load behind them (possible aliasing) and serialise the round trips
+    const uint32_t m = g0 < N ? a.fmask[g0 / kItems] : 0u;  // from k_flag_count
+    const int32_t c = __popc(m);
+    // table reads (first occurrences only) before any table write: stores to table[] would
+    // otherwise order every later load behind them (possible aliasing)
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        const int64_t g = g0 + i;
-        first[i] = false;
-        slot[i] = 0;
-        key[i] = 0;
-        if (g < N) {
-            slot[i] = a.slot_of[g];
-            const ulonglong2 sv = *reinterpret_cast<const ulonglong2 *>(&a.table[slot[i]]);  // key | minpos,uid
-            key[i] = sv.x;
-            first[i] = (unsigned int)(sv.y & 0xffffffffull) == (unsigned int)g;
-            c += first[i];
-        }
+        first[i] = (m >> i) & 1u;
+        slot[i] = first[i] ? __ldg(a.slot_of + g0 + i) : 0;
+        key[i] = first[i] ? a.table[slot[i]].key : 0ull;
     }
     int32_t excl;
     BlockScan(tmp).ExclusiveSum(c, excl);

@@ -151,6 +151,32 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter2(const int32_t *kin, c
     }
 }
 
+// Next pass's digit histogram of every 2048-key tile of a pass's output (large sorts: cheaper
+// than the scatter's per-key global atomics once the key count is in the millions).
+__global__ void __launch_bounds__(kTileThreads) k_hist_tiles(const int32_t *keys, int64_t n, int shift, int bits,
+                                                             int32_t *hist, int64_t nblk) {
+    __shared__ int32_t h[kMaxRadix];
+    const int radix = 1 << bits;
+    for (int d = threadIdx.x; d < radix; d += kTileThreads) h[d] = 0;
+    __syncthreads();
+    const unsigned dmask = (unsigned)radix - 1u;
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kTile; i += kTileThreads) {
+        const int64_t g = (int64_t)blockIdx.x * kTile + i;
+        const bool valid = g < n;
+        const int d = valid ? (int)(((unsigned)__ldg(keys + g) >> shift) & dmask) : 0;
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(vm, d);
+            if (lane == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < radix; d += kTileThreads) hist[(int64_t)d * nblk + blockIdx.x] = h[d];
+}
+
+constexpr int64_t kBigSort = (int64_t)1 << 22;  // from here on the next histogram is its own pass
+
 void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, int32_t *v_a, int32_t *k_b,
                        int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
                        int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches) {
@@ -170,12 +196,18 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
         const int rows = radix > next_radix ? radix : next_radix;
         k_scan_rows<<<(rows + 7) / 8, 256, 0, s>>>(hist[p & 1], nblk, rowtot, more ? hist[(p + 1) & 1] : nullptr,
                                                    radix, next_radix);
+        const bool fused_hist = more && n < kBigSort;
         k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
                                                           plan.bits[p], hist[p & 1], rowtot, nblk,
-                                                          more ? hist[(p + 1) & 1] : nullptr,
+                                                          fused_hist ? hist[(p + 1) & 1] : nullptr,
                                                           more ? plan.shift[p + 1] : 0, more ? plan.bits[p + 1] : 0,
                                                           nullptr);
         *launches += 2;
+        if (more && !fused_hist) {
+            k_hist_tiles<<<(unsigned)nblk, kTileThreads, 0, s>>>(bufk[p & 1], n, plan.shift[p + 1], plan.bits[p + 1],
+                                                                 hist[(p + 1) & 1], nblk);
+            *launches += 1;
+        }
         ck = bufk[p & 1];
         cv = bufv[p & 1];
     }

@@ -39,6 +39,7 @@ struct IndexArgs {
     const int32_t *pack_dim;       // [P]
     int64_t *pack_gbase;           // [P+1] out: float offset of each pack's G rows (sum U_p * D_p)
     const int32_t *n_dev;          // if set: the position count lives on the device (N = capacity)
+    uint8_t *fmask;                // [N/8+1] first-occurrence flags, 8 positions per byte
     int32_t sort_bits0;            // digit width of the backward's first radix pass
     int32_t *sort_hist0;           // [radix0, nblk] out: digit-major histogram of that pass
     int *err;

@@ -222,6 +222,7 @@ picasso_status mfwd_c(picasso_ctx *ctx, cudaStream_t s) {
     a.P = P;
     a.table = ctx->table;
     a.slot_of = mp.oslot;
+    a.fmask = ctx->fmask;
     a.blk_cnt = ctx->blk_cnt;
     a.blk_off = ctx->blk_off;
     a.d_total = mp.od_total;

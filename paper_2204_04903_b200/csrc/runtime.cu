@@ -296,6 +296,7 @@ IndexArgs picasso::make_index_args(picasso_ctx *ctx, const int64_t *ids, const i
     a.pack_gstart = ctx->pack_gstart;
     a.table = ctx->table;
     a.slot_of = ctx->slot_of;
+    a.fmask = ctx->fmask;
     a.seg_of = ctx->seg_of;
     a.inverse = ctx->inverse;
     a.blk_cnt = ctx->blk_cnt;
