@@ -317,7 +317,11 @@ def main():
     emb.check()
     ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends))) / args.steps
     t = torch.tensor([ms], device=dev)
+    ms_ranks = [ms]
     if world > 1:
+        allms = [None] * world
+        dist.all_gather_object(allms, ms)
+        ms_ranks = allms
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
@@ -425,6 +429,7 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
                          "peak_source": peak_src},
+            "ms_per_step_by_rank": ms_ranks,
             "phases_ms": per_phase,
             "nvlink": nvlink,
             "cache": ({"bytes_per_gpu": args.cache_bytes, "warmup_iters": args.cache_warmup,
