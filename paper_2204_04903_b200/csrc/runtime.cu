@@ -126,10 +126,15 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     c->seg_cfg = segsum_pipe_cfg();
     if (const char *e = std::getenv("PICASSO_POOL")) c->pipe_pool = std::strcmp(e, "legacy") != 0;
     if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap = std::strcmp(e, "0") != 0;
+    // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
+    // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
+    c->pool_reserve = world == 1 ? 48 : 0;
+    if (const char *e = std::getenv("PICASSO_POOL_RESERVE")) c->pool_reserve = std::atoi(e);
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     c->seg_nt = c->num_sms * segsum_pipe_warps(c->seg_cfg);
+    c->pool_sms = std::max(c->num_sms / 2, c->num_sms - (c->overlap ? c->pool_reserve : 0));
     c->ws_bytes = c->carve(nullptr);
     *out = c;
     return PICASSO_OK;
@@ -264,6 +269,7 @@ int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
 int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
 void transpose_fork(picasso_ctx *ctx, cudaStream_t s);
+void transpose_on(picasso_ctx *ctx, cudaStream_t t);
 void transpose_join(picasso_ctx *ctx, cudaStream_t s);
 }
 picasso_status multi_fwd_nccl(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
@@ -333,17 +339,36 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
     const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
     a.cap_mask = cap_step - 1;
-    ctx->mark(0, true, s);
-    CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
-    launch_field_prep(a, s);
-    launch_dedup_insert(a, s);
-    launch_dedup_assign(a, s);
-    ctx->mark(0, false, s);
-    ctx->launches_fwd += 1 + (n_ids > 0 ? 4 : 0) + 1;  // prep, insert+flag+scan+assign, inverse
     ctx->B = batch;
     ctx->N = n_ids;
     ctx->offsets = offsets;
-    picasso::transpose_fork(ctx, s);
+    if (ctx->overlap && ctx->side) {
+        // At world == 1 the pool needs only the raw IDs (row = h(id)), not the dedup: the index
+        // work (Unique, inverse) and the backward's transpose run on the internal stream while
+        // the pool streams rows on the caller's stream; the forward joins both before returning.
+        launch_field_prep(a, s);
+        launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        cudaStream_t t = ctx->side;
+        ctx->mark(0, true, t);
+        CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, t));
+        launch_dedup_insert(a, t);
+        launch_dedup_assign(a, t);
+        ctx->mark(0, false, t);
+        picasso::transpose_on(ctx, t);
+        CK(cudaEventRecord(ctx->ev_join, t));
+        ctx->launches_fwd += 2 + (n_ids > 0 ? 4 : 0) + 1;  // prep, seg_of, insert+flag+scan+assign, inverse
+    } else {
+        ctx->mark(0, true, s);
+        CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+        launch_field_prep(a, s);
+        launch_dedup_insert(a, s);
+        launch_dedup_assign(a, s);
+        ctx->mark(0, false, s);
+        ctx->launches_fwd += 1 + (n_ids > 0 ? 4 : 0) + 1;  // prep, insert+flag+scan+assign, inverse
+        picasso::transpose_fork(ctx, s);
+    }
     ctx->mark(1, true, s);
     {
         PoolArgs pa{};
@@ -417,6 +442,12 @@ void picasso::transpose_fork(picasso_ctx *ctx, cudaStream_t s) {
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         t = ctx->side;
     }
+    transpose_on(ctx, t);
+    if (t != s) cudaEventRecord(ctx->ev_join, t);
+}
+
+// the transpose itself, on stream t (seg_of and the pass-0 histogram already written)
+void picasso::transpose_on(picasso_ctx *ctx, cudaStream_t t) {
     ctx->mark(2, true, t);
     int32_t *su = nullptr, *sseg = nullptr;
     radix_sort_pairs2(ctx->inverse, ctx->seg_of, ctx->k_a, ctx->v_a, ctx->k_b, ctx->v_b, &su, &sseg, ctx->N,
@@ -426,7 +457,6 @@ void picasso::transpose_fork(picasso_ctx *ctx, cudaStream_t s) {
     ctx->mark(2, false, t);
     ctx->su = su;
     ctx->sseg = sseg;
-    if (t != s) cudaEventRecord(ctx->ev_join, t);
 }
 
 void picasso::transpose_join(picasso_ctx *ctx, cudaStream_t s) {
@@ -463,7 +493,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
         pa.weight = pa.row_off ? ctx->gbuf : ctx->w[p];
         if ((int64_t)pa.Fp * pa.B == 0) continue;
         if (pool_pipe_supported(ctx->pack_dim[p], pa)) {
-            n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->num_sms, s);
+            n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->pool_sms, s);
         } else {
             launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
             ++n;
