@@ -163,6 +163,7 @@ struct picasso_ctx {
     bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
     bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share
+    bool early_pool = false;  // W = 1: pool concurrently with the dedup + transpose chain
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int32_t *su = nullptr, *sseg = nullptr;  // the last forward's transpose (uid-sorted occurrences)

@@ -128,7 +128,10 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap = std::strcmp(e, "0") != 0;
     // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
     // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
-    c->pool_reserve = world == 1 ? 48 : 0;
+    // Off by default: the step is ~7 % faster (C2: 0.327 -> 0.304 ms) but the pool, sharing the
+    // GPU, then runs at ~3.1 TB/s instead of 4.2 (PICASSO_EARLY_POOL=1 turns it on).
+    if (const char *e = std::getenv("PICASSO_EARLY_POOL")) c->early_pool = std::strcmp(e, "0") != 0;
+    c->pool_reserve = (world == 1 && c->early_pool) ? 48 : 0;
     if (const char *e = std::getenv("PICASSO_POOL_RESERVE")) c->pool_reserve = std::atoi(e);
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -342,7 +345,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     ctx->B = batch;
     ctx->N = n_ids;
     ctx->offsets = offsets;
-    if (ctx->overlap && ctx->side) {
+    if (ctx->overlap && ctx->side && ctx->early_pool) {
         // At world == 1 the pool needs only the raw IDs (row = h(id)), not the dedup: the index
         // work (Unique, inverse) and the backward's transpose run on the internal stream while
         // the pool streams rows on the caller's stream; the forward joins both before returning.
