@@ -126,11 +126,31 @@ __global__ void __launch_bounds__(256) k_writeback(MultiArgs m, int pack, const 
 
 // FCounter histogram of the owned rows (counts clamped to kCntBins - 1)
 constexpr int kCntBins = 1 << 16;
-__global__ void k_count_hist(const uint32_t *fcnt, int64_t n, uint32_t *hist) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t c = fcnt[i];
-        if (c) atomicAdd(hist + (c < kCntBins ? c : kCntBins - 1), 1u);
+// Most rows have small counts (Zipf tail): those bins are counted per block in shared memory
+// with warp-aggregated adds, and merged once per block; large counts go straight to global.
+constexpr int kSmallBins = 1024;
+__global__ void __launch_bounds__(256) k_count_hist(const uint32_t *fcnt, int64_t n, uint32_t *hist) {
+    __shared__ uint32_t sh[kSmallBins];
+    for (int i = threadIdx.x; i < kSmallBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < n;
+         b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b0 + lane;
+        const uint32_t c = i < n ? __ldg(fcnt + i) : 0u;
+        const uint32_t bin = c < kCntBins ? c : kCntBins - 1;
+        const unsigned active = __ballot_sync(0xffffffffu, c != 0);
+        if (c) {
+            const unsigned peers = __match_any_sync(active, bin);
+            if (lane == __ffs(peers) - 1) {
+                if (bin < kSmallBins) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+                else atomicAdd(hist + bin, (uint32_t)__popc(peers));
+            }
+        }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSmallBins; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
 // candidates: rows with count > cstar (any order), plus the first m rows with count == cstar in

@@ -106,6 +106,8 @@ bool pool_pipe_supported(int D, const PoolArgs &a);
 int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
                    int32_t *seg_of, cudaStream_t s);
+// k_pool_flat.cu: one thread per 16-B output chunk (every D); returns #launches
+int launch_pool_flat(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 
 // k_update.cu
 struct UpdateArgs {

@@ -124,7 +124,11 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_BWD")) c->split_bwd = std::strcmp(e, "fused") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     c->seg_cfg = segsum_pipe_cfg();
-    if (const char *e = std::getenv("PICASSO_POOL")) c->pipe_pool = std::strcmp(e, "legacy") != 0;
+    if (const char *e = std::getenv("PICASSO_POOL")) {
+        c->pipe_pool = std::strcmp(e, "legacy") != 0;
+        if (!std::strcmp(e, "flat")) c->pool_kind = 2;
+        if (!std::strcmp(e, "pipe")) c->pool_kind = 1;
+    }
     if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap = std::strcmp(e, "0") != 0;
     // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
     // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
@@ -495,7 +499,9 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
         pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
         pa.weight = pa.row_off ? ctx->gbuf : ctx->w[p];
         if ((int64_t)pa.Fp * pa.B == 0) continue;
-        if (pool_pipe_supported(ctx->pack_dim[p], pa)) {
+        if (ctx->pool_kind == 2) {
+            n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
+        } else if (pool_pipe_supported(ctx->pack_dim[p], pa)) {
             n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->pool_sms, s);
         } else {
             launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
