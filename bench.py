@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--cache-warmup", type=int, default=3, help="Alg. 1 warmup_iters")
     ap.add_argument("--cache-flush", type=int, default=10, help="Alg. 1 flush_iters")
     ap.add_argument("--eager", action="store_true", help="N = 1: launch every step eagerly instead of a CUDA graph")
+    ap.add_argument("--kgroups", type=int, default=None,
+                    help="K-Interleaving groups (packs per dim) at N > 1 with the peer-memory exchange "
+                         "(default 1: measured no gain at C2 with 2 groups, DESIGN.md 7b)")
     return ap.parse_args()
 
 
@@ -233,7 +236,9 @@ def main():
         obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    kgroups = args.kgroups if args.kgroups is not None else 1
     emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=B, max_ids=max_ids,
+                             split=kgroups if kgroups >= 2 else False,
                              table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
                              device=dev, rank=rank, world=world, nccl_uid=uid, max_recv=max_ids,
                              cache_max_bytes=args.cache_bytes if world > 1 else 0)
@@ -416,6 +421,7 @@ def main():
                        "alpha": cfg.alpha, "optimizer": "adagrad", "pool": "sum",
                        "parallelism": f"dp{world}+rowshard{world}" if world > 1 else "single",
                        "exchange": emb.exchange if world > 1 else None,
+                       "packs": emb.n_packs, "k_interleave_groups": kgroups if world > 1 else None,
                        "l2": "flushed (256 MiB write, untimed) before every timed step",
                        "launch": "cuda_graph (one captured step, replayed)" if use_graph else "eager",
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},

@@ -60,9 +60,12 @@ typedef struct picasso_ctx picasso_ctx;
  *   Groups tables by embedding dim (ascending dim).  vparam(group) = sum_t dim_t * count_t
  *   (Eq. 1 with ID_freq = count/N, reading O15); count_t = table_warmup_count[t] (ID
  *   occurrences seen in warm-up iterations, L353-354) or, when NULL, the number of fields
- *   that reference t.  split != 0: a group with vparam above the mean is split into
+ *   that reference t.  split == 1: a group with vparam above the mean is split into
  *   min(#tables, ceil(vparam / min_vparam)) shards (reading O14; reproduces the paper's
  *   four-shard example L358-362), members dealt round-robin by descending dim_t*count_t.
+ *   split = k >= 2: every group is dealt the same way into min(#tables, k) packs — the
+ *   K-Interleaving groups of L424-443 (at world > 1 with the peer-memory exchange, pack p's
+ *   exchange then overlaps pack p-1's pool and owner update).
  *   Within a pack tables are ordered by ascending index; table_base[t] = rows of the pack's
  *   earlier tables, so pack key = table_base[t] + row.
  * In : n_fields F >= 1, field_to_table [F] (host), n_tables T >= 1, table_rows [T] (> 0),

@@ -136,7 +136,7 @@ def picasso_pack_plan(field_to_table, table_rows, table_dim, table_warmup_count=
     tb, pd, pr = np.zeros(T, np.int64), np.zeros(T, np.int32), np.zeros(T, np.int64)
     n = C.c_int32()
     st = lib().picasso_pack_plan(F, f2t.ctypes.data, T, rows.ctypes.data, dims.ctypes.data,
-                                 None if wc is None else wc.ctypes.data, int(bool(split)), f2p.ctypes.data,
+                                 None if wc is None else wc.ctypes.data, int(split), f2p.ctypes.data,
                                  t2p.ctypes.data, tb.ctypes.data, pd.ctypes.data, pr.ctypes.data, C.byref(n))
     _chk(st, "picasso_pack_plan")
     P = n.value

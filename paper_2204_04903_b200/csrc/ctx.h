@@ -110,7 +110,7 @@ struct MultiState {
     size_t win_bytes = 0, win_bcount = 0, win_keys = 0, win_gbuf = 0;
     P2PPeers peers{};
     void *peer_base[kP2PMaxW] = {};     // opened IPC mappings (closed at destroy)
-    uint32_t *epoch_d = nullptr;        // [kP2PPhases]
+    uint32_t *epoch_d = nullptr;        // [2 * kP2PFlags] signal / wait counts per barrier slot
     int32_t *R_d = nullptr;             // [1] received keys (device)
     int64_t *gsrc = nullptr;            // [max_recv * W] G-row offsets per (owner-unique, source)
     int64_t *pack_fbase_d = nullptr, *dbase_d = nullptr, *dst_off = nullptr, *row_base_d = nullptr;
@@ -167,6 +167,9 @@ struct picasso_ctx {
     bool early_pool = false;  // W = 1: pool concurrently with the dedup + transpose chain
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side2 = nullptr;  // K-Interleaving: the pools / owner updates beside the exchange
+    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+    int kinterleave = 1;           // PICASSO_KINTERLEAVE=0 turns the per-pack pipelining off
     int32_t *su = nullptr, *sseg = nullptr;  // the last forward's transpose (uid-sorted occurrences)
     std::vector<float *> w, s1, s2;
     // step state
@@ -305,7 +308,7 @@ struct picasso_ctx {
             mp.rsend_off = c.take<int64_t>(RM);
             mp.rows_send = p2p_ex ? nullptr : c.take<float>((size_t)RM * maxD);  // NCCL staging only
             osort_hist = c.take<int32_t>(2 * ((RM + kTile - 1) / kTile) + 2);
-            mp.epoch_d = c.take<uint32_t>(kP2PPhases);
+            mp.epoch_d = c.take<uint32_t>(2 * kP2PFlags);
             mp.R_d = c.take<int32_t>(1);
             if (opts.cache_max_bytes > 0) {  // HybridHash
                 const int64_t K = std::max<int64_t>(mp.k_max, 1);

@@ -35,7 +35,7 @@ UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, i
                             const int32_t *sseg);
 int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
-int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
+int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s, int only_pack = -1);  // #launches
 void transpose_fork(picasso_ctx *ctx, cudaStream_t s);
 void transpose_join(picasso_ctx *ctx, cudaStream_t s);
 }
@@ -273,6 +273,38 @@ picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s) {
 }
 
 // ---- phase E: transpose + segment-sum into the send layout -----------------------------------
+// arguments of the phase-E segment-sum (hot buffers zeroed on s when the cache is on)
+UpdateArgs mbwd_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s) {
+    UpdateArgs u = make_update_args(ctx, grad_out, lr, step, ctx->su, ctx->sseg);
+    MultiState &mp = ctx->mp;
+    if (mp.hot_k > 0) {  // this rank's hot-row gradients and occurrence counts (AllReduced next)
+        cudaMemsetAsync(mp.hot_g, 0, sizeof(float) * mp.hot_g_floats, s);
+        cudaMemsetAsync(mp.hot_touch, 0, sizeof(float) * mp.hot_k, s);
+        u.hslot = mp.hslot;
+        u.hot_g = mp.hot_g;
+        u.hot_g_off = mp.hot_off_d + 3 * ctx->P;
+        u.hot_pslot = mp.hot_pslot_d;
+        u.hot_touch = mp.hot_touch;
+    }
+    u.gbuf = ctx->gbuf;
+    u.row_off = ctx->mp.row_off;
+    if (mp.p2p) {  // G rows straight into the owners' receive buffers (p2p.cu)
+        u.dst_rank = mp.dst_rank;
+        u.dst_off = mp.dst_off;
+        for (int q = 0; q < ctx->world; ++q) u.dst_buf[q] = mp.peers.ogbuf[q];
+    }
+    return u;
+}
+
+// segment-sum of one pack (phase E)
+int mbwd_segsum_pack(picasso_ctx *ctx, UpdateArgs u, int p, cudaStream_t s) {
+    if (ctx->N == 0) return 0;
+    u.pack = p;
+    u.long_cnt = ctx->long_cnt + p;
+    u.pack_key_off = ctx->pack_key_off[p];
+    return launch_segsum_any(ctx, ctx->pack_dim[p], u, s);
+}
+
 picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s) {
     const int64_t N = ctx->N;
     ctx->mark(3, true, s);  // the transpose ran in the forward (transpose_fork)

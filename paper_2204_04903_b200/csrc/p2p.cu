@@ -38,18 +38,23 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 // ------------------------------------------------------------------------------------------
-__global__ void k_p2p_signal(P2PArgs a, int phase) {
+__global__ void k_p2p_signal(P2PArgs a, int slot) {
     if (threadIdx.x != 0) return;
-    const uint32_t e = ++a.epoch[phase];
+    const uint32_t e = ++a.epoch[slot];
     __threadfence_system();
-    for (int q = 0; q < a.W; ++q) st_release_sys(a.peer.flags[q] + phase * kP2PMaxW + a.rank, e);
+    for (int q = 0; q < a.W; ++q) st_release_sys(a.peer.flags[q] + slot * kP2PMaxW + a.rank, e);
 }
 
-__global__ void k_p2p_wait(P2PArgs a, int phase) {
+// The waiter counts its own waits per slot (epoch[kP2PFlags + slot]): its target never depends
+// on whether this rank's own signal of the slot (possibly on another stream) has run yet.
+__global__ void k_p2p_wait(P2PArgs a, int slot) {
+    __shared__ uint32_t s_e;
+    if (threadIdx.x == 0) s_e = ++a.epoch[kP2PFlags + slot];
+    __syncthreads();
     const int q = threadIdx.x;
     if (q < a.W) {
-        const uint32_t e = a.epoch[phase];
-        const uint32_t *f = a.peer.flags[a.rank] + phase * kP2PMaxW + q;
+        const uint32_t e = s_e;
+        const uint32_t *f = a.peer.flags[a.rank] + slot * kP2PMaxW + q;
         const uint64_t t0 = globaltimer();
         while ((int32_t)(ld_acquire_sys(f) - e) < 0) {
             if (globaltimer() - t0 > kP2PTimeoutNs) {  // a peer never arrived: latch, do not hang
@@ -336,8 +341,8 @@ __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *
         default: break;             \
     }
 
-void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s) { k_p2p_signal<<<1, 32, 0, s>>>(a, phase); }
-void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s) { k_p2p_wait<<<1, 32, 0, s>>>(a, phase); }
+void launch_p2p_signal(const P2PArgs &a, int slot, cudaStream_t s) { k_p2p_signal<<<1, 32, 0, s>>>(a, slot); }
+void launch_p2p_wait(const P2PArgs &a, int slot, cudaStream_t s) { k_p2p_wait<<<1, 32, 0, s>>>(a, slot); }
 void launch_p2p_tables(const P2PArgs &a, cudaStream_t s) { k_p2p_tables<<<1, 1024, 0, s>>>(a); }
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_dst_insert<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);

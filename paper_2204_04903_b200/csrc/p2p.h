@@ -7,12 +7,14 @@ namespace picasso {
 
 constexpr int kP2PMaxW = 8;                                 // ranks per node at most
 constexpr int kP2PPhases = 4;                               // barrier phases per step
+constexpr int kP2PMaxGroups = 16;                           // K-Interleaving groups (packs) with own barriers
+constexpr int kP2PFlags = kP2PPhases * kP2PMaxGroups;       // barrier slots: (phase, group)
 constexpr unsigned long long kP2PTimeoutNs = 20000000000ull;  // a peer missing for 20 s latches an error
 enum P2PErrBits : int { ERR_PEER_TIMEOUT = 4 };
 
 // One rank's IPC window, seen by everyone (index = rank; own pointers at [rank]).
 struct P2PPeers {
-    uint32_t *flags[kP2PMaxW];     // [kP2PPhases][kP2PMaxW] epoch written by each source rank
+    uint32_t *flags[kP2PMaxW];     // [kP2PFlags][kP2PMaxW] epoch written by each source rank
     int32_t *bcount[kP2PMaxW];     // [W*P+1] bucket counts (owner-major, pack), hot bucket last
     int32_t *send_keys[kP2PMaxW];  // [max_ids] requested local rows, owner-major send layout
     float *gbuf[kP2PMaxW];         // [max_ids * maxD] rows received (fwd), send layout
@@ -24,7 +26,7 @@ struct P2PArgs {
     int32_t W, P, rank;
     int64_t max_recv;
     P2PPeers peer;
-    uint32_t *epoch;               // [kP2PPhases] this rank's barrier epochs (device)
+    uint32_t *epoch;               // [2 * kP2PFlags] this rank's signal, then wait counts per slot
     int *err;
     const int32_t *pack_dim;       // [P]
     const int64_t *pack_key_off;   // [P+1]
@@ -54,8 +56,9 @@ struct P2PArgs {
     const int64_t *fcnt_off;
 };
 
-void launch_p2p_signal(const P2PArgs &a, int phase, cudaStream_t s);
-void launch_p2p_wait(const P2PArgs &a, int phase, cudaStream_t s);
+// barrier slot = phase * kP2PMaxGroups + group
+void launch_p2p_signal(const P2PArgs &a, int slot, cudaStream_t s);
+void launch_p2p_wait(const P2PArgs &a, int slot, cudaStream_t s);
 void launch_p2p_tables(const P2PArgs &a, cudaStream_t s);
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s);

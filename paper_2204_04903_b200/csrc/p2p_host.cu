@@ -40,6 +40,12 @@ picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s);
 picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
 picasso_status hot_allreduce_group(std::vector<picasso_ctx *> &cs, cudaStream_t s);
 picasso_status hot_update_all(picasso_ctx *ctx, float lr, float ss, cudaStream_t s);
+UpdateArgs mbwd_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
+int mbwd_segsum_pack(picasso_ctx *ctx, UpdateArgs u, int p, cudaStream_t s);
+namespace picasso {
+int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s, int only_pack = -1);  // #launches
+void transpose_join(picasso_ctx *ctx, cudaStream_t s);
+}
 
 namespace {
 
@@ -49,7 +55,7 @@ int max_dim(const picasso_ctx *ctx) {
     return maxD;
 }
 
-constexpr size_t kFlagBytes = sizeof(uint32_t) * kP2PPhases * kP2PMaxW;
+constexpr size_t kFlagBytes = sizeof(uint32_t) * kP2PFlags * kP2PMaxW;
 
 // window: [flags | bcount | send_keys | gbuf | ogbuf], the same layout on every rank (same plan,
 // max_ids, max_recv)
@@ -93,7 +99,7 @@ picasso_status window_alloc(picasso_ctx *ctx) {
     mp.bcount = mp.peers.bcount[ctx->rank];
     mp.send_keys = mp.peers.send_keys[ctx->rank];
     ctx->gbuf = mp.peers.gbuf[ctx->rank];
-    PCK(cudaMemset(mp.epoch_d, 0, sizeof(uint32_t) * kP2PPhases));
+    PCK(cudaMemset(mp.epoch_d, 0, sizeof(uint32_t) * 2 * kP2PFlags));
     return PICASSO_OK;
 }
 
@@ -137,17 +143,31 @@ P2PArgs make_p2p_args(picasso_ctx *ctx) {
 void barrier(picasso_ctx *ctx, int phase, cudaStream_t s) {
     if (ctx->mp.p2p_loop) return;
     const P2PArgs a = make_p2p_args(ctx);
-    launch_p2p_signal(a, phase, s);
-    launch_p2p_wait(a, phase, s);
+    launch_p2p_signal(a, phase * kP2PMaxGroups, s);
+    launch_p2p_wait(a, phase * kP2PMaxGroups, s);
     ctx->launches_fwd += 2;
+}
+// split barrier of one K-Interleaving group: signal where the group's data is produced, wait
+// where it is consumed (another stream)
+void signal_group(picasso_ctx *ctx, int phase, int group, cudaStream_t s) {
+    launch_p2p_signal(make_p2p_args(ctx), phase * kP2PMaxGroups + group, s);
+}
+void wait_group(picasso_ctx *ctx, int phase, int group, cudaStream_t s) {
+    launch_p2p_wait(make_p2p_args(ctx), phase * kP2PMaxGroups + group, s);
+}
+
+// K-Interleaving over the packs: pack p's exchange overlaps pack p-1's pool
+// (forward) and owner update (backward); one barrier per (phase, pack).  Needs >= 2 packs, no
+// HybridHash, one process per GPU.
+bool interleaved(const picasso_ctx *ctx) {
+    return ctx->kinterleave && ctx->P >= 2 && ctx->P <= kP2PMaxGroups && ctx->opts.cache_max_bytes == 0 &&
+           !ctx->mp.p2p_loop && ctx->side2;
 }
 
 // ---- C': owner side --------------------------------------------------------------------------
-picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
-    MultiState &mp = ctx->mp;
+picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
     const int P = ctx->P;
     const P2PArgs a = make_p2p_args(ctx);
-    const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
     ctx->mark(4, true, s);
     launch_p2p_reset(a, ctx->num_sms, s);  // the previous forward's direct-table entries
     launch_p2p_tables(a, s);
@@ -155,25 +175,38 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s) {
     launch_p2p_leaders(a, ctx->num_sms, s);
     static const bool split = std::getenv("PICASSO_PROF_SPLIT") != nullptr;  // measurement aid
     if (split) ctx->mark(4, false, s);
-    for (int p = 0; p < P; ++p) launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
+    if (kil) {  // the pools start on the second stream once the prep is done
+        PCK(cudaEventRecord(ctx->ev_fork2, s));
+        PCK(cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0));
+    }
+    for (int p = 0; p < P; ++p) {
+        launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
+        if (kil) signal_group(ctx, 1, p, s);  // pack p's rows are in every requester's buffer
+    }
     if (!split) ctx->mark(4, false, s);
-    ctx->launches_fwd += 4 + P;
+    ctx->launches_fwd += 4 + P * (kil ? 2 : 1);
     PCK(cudaGetLastError());
     return PICASSO_OK;
 }
 
 // ---- F': owner reduce (pulled G rows, source order) + optimizer -------------------------------
-picasso_status p2p_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) {
-    const P2PArgs a = make_p2p_args(ctx);
+float adam_step(const picasso_ctx *ctx, float lr, int64_t step) {
     const double bc1 = 1.0 - std::pow((double)ctx->opts.beta1, (double)step);
     const double bc2 = 1.0 - std::pow((double)ctx->opts.beta2, (double)step);
-    const float ss = (float)((double)lr * std::sqrt(bc2) / bc1);
+    return (float)((double)lr * std::sqrt(bc2) / bc1);
+}
+
+void p2p_update_pack(picasso_ctx *ctx, const P2PArgs &a, int p, float lr, float ss, cudaStream_t s) {
+    launch_p2p_update(ctx->pack_dim[p], a, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr, ctx->opts.eps,
+                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s);
+    ctx->launches_bwd += 1;
+}
+
+picasso_status p2p_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) {
+    const P2PArgs a = make_p2p_args(ctx);
+    const float ss = adam_step(ctx, lr, step);
     ctx->mark(5, true, s);
-    for (int32_t p = 0; p < ctx->P; ++p) {
-        launch_p2p_update(ctx->pack_dim[p], a, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr,
-                          ctx->opts.eps, ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s);
-        ctx->launches_bwd += 1;
-    }
+    for (int32_t p = 0; p < ctx->P; ++p) p2p_update_pack(ctx, a, p, lr, ss, s);
     picasso_status st = hot_update_all(ctx, lr, ss, s);
     if (st) return st;
     ctx->mark(5, false, s);
@@ -192,14 +225,67 @@ picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t
     picasso_status st;
     if ((st = mfwd_a(ctx, ids, offsets, B, N, s))) return st;
     barrier(ctx, 0, s);
-    if ((st = p2p_c(ctx, s))) return st;
-    barrier(ctx, 1, s);
-    return mfwd_d(ctx, out, s);
+    const bool kil = interleaved(ctx);
+    if ((st = p2p_c(ctx, s, kil))) return st;
+    if (!kil) {
+        barrier(ctx, 1, s);
+        return mfwd_d(ctx, out, s);
+    }
+    // pool of pack p as soon as every owner has stored pack p's rows (gathers of later packs
+    // still running on s)
+    PoolArgs pa{};
+    pa.ids = nullptr;
+    pa.offsets = ctx->offsets;
+    pa.B = ctx->B;
+    pa.row_off = ctx->mp.row_off;
+    pa.inverse = ctx->inverse;
+    cudaStream_t t = ctx->side2;
+    for (int p = 0; p < ctx->P; ++p) {
+        wait_group(ctx, 1, p, t);
+        ctx->mark(1, true, t);
+        ctx->launches_fwd += 1 + launch_pool_all(ctx, pa, out, t, p);
+        ctx->mark(1, false, t);
+    }
+    PCK(cudaEventRecord(ctx->ev_join2, t));
+    PCK(cudaStreamWaitEvent(s, ctx->ev_join2, 0));
+    transpose_join(ctx, s);
+    PCK(cudaGetLastError());
+    ctx->fwd_done = true;
+    ctx->last_stream = s;
+    return PICASSO_OK;
 }
 
 picasso_status multi_bwd_p2p(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s) {
     picasso_status st;
     MultiState &mp = ctx->mp;
+    if (interleaved(ctx)) {  // owner update of pack p once every requester has stored pack p's G
+        UpdateArgs u = mbwd_args(ctx, grad_out, lr, step, s);
+        PCK(cudaEventRecord(ctx->ev_fork2, s));
+        PCK(cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0));
+        ctx->mark(3, true, s);
+        for (int p = 0; p < ctx->P; ++p) {
+            ctx->launches_bwd += mbwd_segsum_pack(ctx, u, p, s);
+            signal_group(ctx, 2, p, s);
+        }
+        ctx->mark(3, false, s);
+        const P2PArgs a = make_p2p_args(ctx);
+        const float ss = adam_step(ctx, lr, step);
+        cudaStream_t t = ctx->side2;
+        for (int p = 0; p < ctx->P; ++p) {
+            wait_group(ctx, 2, p, t);
+            ctx->mark(5, true, t);
+            p2p_update_pack(ctx, a, p, lr, ss, t);
+            ctx->mark(5, false, t);
+        }
+        ctx->launches_bwd += 2 * ctx->P;
+        PCK(cudaEventRecord(ctx->ev_join2, t));
+        PCK(cudaStreamWaitEvent(s, ctx->ev_join2, 0));
+        if (ctx->prof) ++ctx->prof_calls;
+        PCK(cudaGetLastError());
+        ctx->fwd_done = false;
+        ctx->last_stream = s;
+        return PICASSO_OK;
+    }
     if ((st = mbwd_e(ctx, grad_out, lr, step, s))) return st;
     barrier(ctx, 2, s);
     if (mp.hot_k > 0) {  // HybridHash: hot-row gradients and occurrence counts summed over ranks
@@ -218,7 +304,7 @@ picasso_status group_fwd_p2p(picasso_group *g, const int64_t *const *ids, const 
     for (int r = 0; r < W; ++r)
         if ((st = mfwd_a(g->ctx[r], ids[r], offsets[r], batch[r], n_ids[r], s))) return st;
     for (int r = 0; r < W; ++r)
-        if ((st = p2p_c(g->ctx[r], s))) return st;
+        if ((st = p2p_c(g->ctx[r], s, false))) return st;
     for (int r = 0; r < W; ++r)
         if ((st = mfwd_d(g->ctx[r], out[r], s))) return st;
     return PICASSO_OK;

@@ -47,7 +47,9 @@ extern "C" picasso_status picasso_pack_plan(int32_t n_fields, const int32_t *fie
     for (auto &kv : by_dim) {
         std::vector<int32_t> members = kv.second;  // ascending table index
         int32_t shards = 1;
-        if (split && vparam[gi] > mean && unit > 0.0) {
+        if (split >= 2) {  // K-Interleaving groups: every dim group dealt into `split` packs
+            shards = (int32_t)std::min<size_t>(members.size(), (size_t)split);
+        } else if (split && vparam[gi] > mean && unit > 0.0) {
             const double want = std::ceil(vparam[gi] / unit);
             shards = (int32_t)std::max(1.0, std::min((double)members.size(), want));
         }

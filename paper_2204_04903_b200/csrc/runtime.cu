@@ -130,6 +130,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
         if (!std::strcmp(e, "pipe")) c->pool_kind = 1;
     }
     if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap = std::strcmp(e, "0") != 0;
+    if (const char *e = std::getenv("PICASSO_KINTERLEAVE")) c->kinterleave = std::atoi(e);
     // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
     // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
     // Off by default: the step is ~7 % faster (C2: 0.327 -> 0.304 ms) but the pool, sharing the
@@ -238,10 +239,13 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
             CK(cudaStreamSynchronize(0));
         }
     }
-    if (!ctx->side) {  // internal stream of the forward's overlapped transpose
+    if (!ctx->side) {  // internal streams: the forward's overlapped transpose, K-Interleaving
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming));
     }
     ctx->bound = true;
     ctx->fwd_done = false;
@@ -255,6 +259,9 @@ extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
         cudaStreamDestroy(ctx->side);
         cudaEventDestroy(ctx->ev_fork);
         cudaEventDestroy(ctx->ev_join);
+        cudaStreamDestroy(ctx->side2);
+        cudaEventDestroy(ctx->ev_fork2);
+        cudaEventDestroy(ctx->ev_join2);
     }
     if (ctx->mp.comm) ncclCommDestroy(ctx->mp.comm);
     if (ctx->mp.cnt_send_h) {
@@ -274,7 +281,7 @@ UpdateArgs make_update_args(picasso_ctx *ctx, const float *grad_out, float lr, i
                             const int32_t *sseg);
 int launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s);  // returns #launches
 void launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s);
-int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s);  // returns #launches
+int launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s, int only_pack = -1);  // #launches
 void transpose_fork(picasso_ctx *ctx, cudaStream_t s);
 void transpose_on(picasso_ctx *ctx, cudaStream_t t);
 void transpose_join(picasso_ctx *ctx, cudaStream_t s);
@@ -480,7 +487,7 @@ void picasso::launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cud
 
 // Gather + Stitch + pool of every pack (base: ids / offsets / B, plus row_off / inverse at W > 1,
 // where the rows come from the received-rows buffer instead of the local tables).
-int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s) {
+int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStream_t s, int only_pack) {
     int n = 0;
     pa.finfo = ctx->finfo;
     pa.field_gstart = ctx->field_gstart;
@@ -494,6 +501,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
     pa.pack_gstart = ctx->pack_gstart;
     pa.field_k = ctx->pipe_pool ? ctx->field_k_d : nullptr;
     for (int32_t p = 0; p < ctx->P; ++p) {  // seg_of: written by transpose_fork (k_seg_of)
+        if (only_pack >= 0 && p != only_pack) continue;
         pa.pack = p;
         pa.Fp = ctx->pack_first_k[p + 1] - ctx->pack_first_k[p];
         pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];

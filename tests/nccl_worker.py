@@ -32,7 +32,7 @@ def main():
     base = name[:-6] if (cache or graph) else name
     if base == "toy":
         cfg = dc.toy(alpha=1.2)
-    elif base == "criteo":  # D = 128: pipelined kernels, rows spanning tiles, P2P pushes
+    elif base in ("criteo", "criteok2"):  # D = 128: pipelined kernels, rows spanning tiles, P2P pushes
         cfg = dc.scaled(dc.criteo(), batch=2048, rows_div=20000)
     elif base == "uneven":  # per-rank batch sizes differ; the last rank has an empty batch
         cfg = dc.scaled(dc.wdl(), batch=32, rows_div=2000)
@@ -49,7 +49,8 @@ def main():
     e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=max(cfg.batch, 1), max_ids=mi,
                            table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
                            rank=rank, world=world, nccl_uid=obj[0], max_recv=world * mi,
-                           device=torch.device("cuda", local), cache_max_bytes=(1 << 20) if cache else 0)
+                           device=torch.device("cuda", local), cache_max_bytes=(1 << 20) if cache else 0,
+                           split=2 if base == "criteok2" else False)  # k2: two K-Interleaving groups
     init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights, rank=rank,
                            world=world)
     m, tabs = oracle_model(cfg), oracle_tables(cfg)
