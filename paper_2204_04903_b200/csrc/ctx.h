@@ -161,7 +161,10 @@ struct picasso_ctx {
     int32_t seg_nt = 0;       // its tiles per pack
     int32_t *tile_start = nullptr;
     int4 *split = nullptr;
-    bool split_bwd = true;  // PICASSO_BWD=fused selects the fused segsum+update kernel
+    bool split_bwd = true;  // PICASSO_BWD=fused selects the legacy fused segsum+update kernel
+    bool fuse_pipe = false;  // PICASSO_BWD=fusepipe (W = 1, D = 64/128): pipelined segsum with the
+                             // update at each row's flush.  Measured slower (C2: 219 us vs 73 + 71 us
+                             // split) — one deferred row per warp does not hide the state loads.
     bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share
     bool early_pool = false;  // W = 1: pool concurrently with the dedup + transpose chain

@@ -47,7 +47,7 @@ struct BG {
     static constexpr int RS = ROWB >= kStageBytes ? 1 : kStageBytes / ROWB;  // rows per stage (divides 32)
     static constexpr int SB = RS * ROWB;
     static constexpr int EPL = D / 32;                                      // floats per lane
-    static constexpr int META = NW * S * 8 * RS;                            // uid + len per staged row
+    static constexpr int META = NW * S * 16 * RS;                           // uid + len + row per staged row
     static constexpr int RING_OFF = (META + 127) / 128 * 128;
     static constexpr int SMEM = RING_OFF + NW * S * SB;
     static_assert(32 % RS == 0, "a stage must lie inside one 32-position round");
@@ -137,6 +137,52 @@ __device__ __forceinline__ void lane_load_f64(const double *row, int lane, doubl
     }
 }
 
+// lane's elements of a row in global memory (same layout as lane_load)
+template <int D>
+__device__ __forceinline__ void lane_gload(const float *row, int lane, float *v) {
+    constexpr int EPL = D / 32;
+    if constexpr (EPL == 2) {
+        const float2 x = reinterpret_cast<const float2 *>(row)[lane];
+        v[0] = x.x;
+        v[1] = x.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q) {
+            const float4 x = reinterpret_cast<const float4 *>(row)[q * 32 + lane];
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+    }
+}
+template <int D>
+__device__ __forceinline__ void lane_gstore(float *row, int lane, const float *v) {
+    constexpr int EPL = D / 32;
+    if constexpr (EPL == 2) {
+        reinterpret_cast<float2 *>(row)[lane] = make_float2(v[0], v[1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q)
+            reinterpret_cast<float4 *>(row)[q * 32 + lane] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+}
+
+// Adagrad / lazy Adam on one element (north star; reading O10), IEEE round-to-nearest throughout
+__device__ __forceinline__ void opt_step(const UpdateArgs &a, float g, float &w, float &s1, float &s2) {
+    if (a.opt == 0) {
+        s1 = __fadd_rn(s1, __fmul_rn(g, g));
+        w = __fsub_rn(w, __fmul_rn(a.lr, __fdiv_rn(g, __fadd_rn(__fsqrt_rn(s1), a.eps))));
+    } else {
+        const float mo = s1, vo = s2;
+        const float mu = __fmul_rn(__fsub_rn(g, mo), __fsub_rn(1.0f, a.beta1));
+        const float vu = __fmul_rn(__fsub_rn(__fmul_rn(g, g), vo), __fsub_rn(1.0f, a.beta2));
+        s1 = __fadd_rn(mu, mo);
+        s2 = __fadd_rn(vu, vo);
+        w = __fsub_rn(w, __fmul_rn(a.adam_ss, __fdiv_rn(s1, __fadd_rn(__fsqrt_rn(s2), a.eps))));
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Row starts + equal-cost tiles.  Pack p holds sorted positions [G0, G1) = [pack_gstart[p],
 // pack_gstart[p+1]) (uids are pack-major) and rows [U0, U1).  cost(i) = (i - G0) + (su[i] - U0)
@@ -170,12 +216,16 @@ __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const
         for (int64_t kk = k + 1; kk <= nt; ++kk) ts[kk] = (int32_t)G1;
 }
 
-template <int D, int NW, int S>
+// FUSE (world == 1, D <= 128): the optimizer runs at the row's flush instead of writing G —
+// the row's weight / state loads are issued at its flush and consumed at the next flush (one
+// row in flight per warp), so no G buffer round trip and no separate update kernel.
+template <int D, int NW, int S, bool FUSE>
 __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     using G = BG<D, NW, S>;
     constexpr int RS = G::RS, SB = G::SB, ROWB = G::ROWB, EPL = G::EPL;
     extern __shared__ __align__(128) unsigned char smem[];
-    int32_t *s_uid = reinterpret_cast<int32_t *>(smem);
+    int64_t *s_row = reinterpret_cast<int64_t *>(smem);
+    int32_t *s_uid = reinterpret_cast<int32_t *>(smem + (size_t)NW * S * RS * 8);
     int32_t *s_len = s_uid + NW * S * RS;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
@@ -187,6 +237,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     if (pa >= pb) return;
 
     int32_t *wu = s_uid + w * S * RS, *wl = s_len + w * S * RS;
+    int64_t *wrow = s_row + w * S * RS;
     unsigned char *wr = smem + G::RING_OFF + (size_t)w * S * SB;
     float *gp = a.gbuf + a.pack_gbase[a.pack];
     const float4 *dy4 = reinterpret_cast<const float4 *>(a.dy);
@@ -203,7 +254,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     // lane l holds position base + l of a 32-position round: dY row (float4 units), uid, bag length
     uint32_t off_c, off_n;
     int32_t uid_c, uid_n, len_c, len_n;
-    auto resolve = [&](int32_t base, uint32_t &off, int32_t &uid, int32_t &len) {
+    int64_t row_c = 0, row_n = 0;  // FUSE: the table row of the position's unique key
+    auto resolve = [&](int32_t base, uint32_t &off, int32_t &uid, int32_t &len, int64_t &row) {
         const int32_t p = base + lane;
         off = 0;
         uid = -1;
@@ -214,10 +266,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
             const int32_t f = seg / a.B;
             off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col) >> 2);
             if (a.pool_mean) len = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
+            if constexpr (FUSE) row = (int64_t)(__ldg(a.unique_gkey + uid) - (unsigned long long)a.pack_key_off);
         }
     };
-    resolve(pa, off_c, uid_c, len_c);
-    resolve(pa + 32, off_n, uid_n, len_n);
+    resolve(pa, off_c, uid_c, len_c, row_c);
+    resolve(pa + 32, off_n, uid_n, len_n, row_n);
     int32_t round_c = 0;
     auto issue = [&](int32_t k) {  // stage k -> ring slot k % S
         const int slot = k % S;
@@ -226,8 +279,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
             off_c = off_n;
             uid_c = uid_n;
             len_c = len_n;
+            row_c = row_n;
             round_c = r;
-            resolve(pa + (r + 1) * 32, off_n, uid_n, len_n);
+            resolve(pa + (r + 1) * 32, off_n, uid_n, len_n, row_n);
         }
         const int32_t p0 = pa + k * RS;
         const int nrows = pb - p0 < RS ? pb - p0 : RS;
@@ -251,6 +305,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
         if (i >= 0 && i < nrows) {
             wu[slot * RS + i] = uid_c;
             wl[slot * RS + i] = len_c;
+            if constexpr (FUSE) wrow[slot * RS + i] = row_c;
         }
     };
 
@@ -258,12 +313,35 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.0;
     int32_t cur = -1, ncur = 0;  // current row, its occurrences in this tile (= all of them if unsplit)
+    int64_t cur_row = 0;
+    // FUSE: the previous finished row, its G and its weight / state (loads in flight)
+    int64_t pend = -1;
+    float pg[EPL], pw[EPL], ps1[EPL], ps2[EPL];
+    auto finish_pending = [&]() {
+        if constexpr (FUSE) {
+            if (pend < 0) return;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) opt_step(a, pg[e], pw[e], ps1[e], ps2[e]);
+            lane_gstore<D>(a.weight + pend, lane, pw);
+            lane_gstore<D>(a.state1 + pend, lane, ps1);
+            if (a.opt == 1) lane_gstore<D>(a.state2 + pend, lane, ps2);
+            pend = -1;
+        }
+    };
     auto flush = [&](int32_t u) {
         double *part = reinterpret_cast<double *>(a.partial);
         if (u == hp) {
             lane_store_f64<D>(part + (int64_t)(2 * t) * D, lane, acc);
         } else if (u == tp) {
             lane_store_f64<D>(part + (int64_t)(2 * t + 1) * D, lane, acc);
+        } else if constexpr (FUSE) {
+            finish_pending();
+            pend = cur_row * D;
+            lane_gload<D>(a.weight + pend, lane, pw);
+            lane_gload<D>(a.state1 + pend, lane, ps1);
+            if (a.opt == 1) lane_gload<D>(a.state2 + pend, lane, ps2);
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) pg[e] = __double2float_rn(acc[e]);
         } else {
             lane_store_f32<D>(g_dst<D>(a, u, u0, gp, lane, (float)ncur), lane, acc);
         }
@@ -295,6 +373,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
                 if (uid != cur) {
                     if (cur >= 0) flush(cur);
                     cur = uid;
+                    if constexpr (FUSE) cur_row = wrow[slot * RS + i];
                     ncur = 0;
                 }
                 ++ncur;
@@ -312,11 +391,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
         ldgsts_commit();
     }
     if (cur >= 0) flush(cur);
+    finish_pending();
 }
 
 // One CTA per listed split row: its pieces (j = 0: slot 2t+1 of its first tile t; j >= 1: slot
 // 2(t+j)) summed in tile order — warp w takes j = w mod 4, the warps combined in order.
-template <int D>
+template <int D, bool FUSE>
 __global__ void __launch_bounds__(128) k_segsum_fix(UpdateArgs a) {
     constexpr int EPL = D / 32, NWF = 4;
     __shared__ double s_acc[NWF][D];
@@ -363,22 +443,35 @@ __global__ void __launch_bounds__(128) k_segsum_fix(UpdateArgs a) {
 #pragma unroll
             for (int q = 0; q < EPL; ++q) acc[q] = __dadd_rn(acc[q], v[q]);
         }
-        const int32_t u0 = a.pack_ustart[a.pack];
-        float *gp = a.gbuf + a.pack_gbase[a.pack];
-        lane_store_f32<D>(g_dst<D>(a, u, u0, gp, lane, (float)(re - rs)), lane, acc);
+        if constexpr (FUSE) {  // the split row's update
+            const int64_t o = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off) * D;
+            float w4[EPL], s1[EPL], s2[EPL];
+            lane_gload<D>(a.weight + o, lane, w4);
+            lane_gload<D>(a.state1 + o, lane, s1);
+            if (a.opt == 1) lane_gload<D>(a.state2 + o, lane, s2);
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) opt_step(a, __double2float_rn(acc[q]), w4[q], s1[q], s2[q]);
+            lane_gstore<D>(a.weight + o, lane, w4);
+            lane_gstore<D>(a.state1 + o, lane, s1);
+            if (a.opt == 1) lane_gstore<D>(a.state2 + o, lane, s2);
+        } else {
+            const int32_t u0 = a.pack_ustart[a.pack];
+            float *gp = a.gbuf + a.pack_gbase[a.pack];
+            lane_store_f32<D>(g_dst<D>(a, u, u0, gp, lane, (float)(re - rs)), lane, acc);
+        }
     }
 }
 
-template <int D, int NW, int S>
+template <int D, int NW, int S, bool FUSE = false>
 void launch_pipe(const UpdateArgs &a, int num_sms, cudaStream_t s) {
     using G = BG<D, NW, S>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_segsum_pipe<D, NW, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(k_segsum_pipe<D, NW, S, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         attr = true;
     }
-    k_segsum_pipe<D, NW, S><<<(unsigned)num_sms, NW * 32, G::SMEM, s>>>(a);
-    k_segsum_fix<D><<<(unsigned)a.nt, 128, 0, s>>>(a);
+    k_segsum_pipe<D, NW, S, FUSE><<<(unsigned)num_sms, NW * 32, G::SMEM, s>>>(a);
+    k_segsum_fix<D, FUSE><<<(unsigned)a.nt, 128, 0, s>>>(a);
 }
 
 template <int D>
@@ -428,6 +521,17 @@ void launch_csr_tiles(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32
     if (N > 0)
         k_csr_tiles<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(sorted_u, N, ustart, pack_gstart, pack_ustart, P,
                                                                 nt, tile_start);
+}
+
+// segment-sum fused with the optimizer (world == 1, D = 64 / 128); returns #launches (0: n/a)
+int launch_segsum_fused(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    if (!a.tile_start || a.row_off || a.hslot || ((uintptr_t)a.dy & 15) || (a.dy_stride & 3)) return 0;
+    switch (D) {
+        case 64: launch_pipe<64, 16, 3, true>(a, num_sms, s); break;
+        case 128: launch_pipe<128, 16, 3, true>(a, num_sms, s); break;
+        default: return 0;
+    }
+    return 2;
 }
 
 size_t segsum_bulk_partial_doubles(int maxD, int num_sms) { return (size_t)2 * num_sms * kMaxNW * maxD; }
