@@ -134,3 +134,15 @@ def test_pool_pipe_mean_and_all_empty_pack():
     m, tabs = oracle_model(cfg), oracle_tables(cfg)
     ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, None)
     assert np.array_equal(got, oracle.forward(m, ob, tabs, cfg.out_width))
+
+
+# ---- alternative paths behind environment switches (read when the context is created) ---------
+@pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "1"}, {"PICASSO_BWD": "fusepipe"}, {"PICASSO_POOL": "flat"},
+                                 {"PICASSO_OVERLAP": "0"}, {"PICASSO_SEGSUM_CFG": "12x4"}])
+def test_alternative_paths_match_oracle(env, monkeypatch):
+    """Every switchable variant computes the same step: forward bit-exact, update within the
+    north-star tolerance of the oracle (bit-exact under dyadic dY)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    run_step(_cfg(128, batch=1024), steps=2, dyadic=True, check_intermediates=False)
+    run_step(_cfg(64, batch=512, pool=dc.POOL_MEAN), steps=1, dyadic=False, check_intermediates=False)
