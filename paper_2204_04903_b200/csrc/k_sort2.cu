@@ -13,6 +13,9 @@
 // The first pass's histogram comes from k_inverse, so a 2-pass sort is 4 launches.
 #include <cub/block/block_scan.cuh>
 
+#include <cstdlib>
+#include <string>
+
 #include "kernels.h"
 
 namespace picasso {
@@ -151,6 +154,136 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter2(const int32_t *kin, c
     }
 }
 
+// Same pass with coalesced writes: the tile is first sorted by digit in shared memory (stable),
+// then written out in that order, so consecutive threads store consecutive positions of a digit's
+// run instead of scattering one key per digit run per warp.
+__global__ void __launch_bounds__(kTileThreads) k_scatter3(const int32_t *kin, const int32_t *vin, int32_t *kout,
+                                                           int32_t *vout, int64_t n, int shift, int bits,
+                                                           const int32_t *hist_off, const int32_t *rowtot,
+                                                           int64_t nblk, int32_t *hist_next, int next_shift,
+                                                           int next_bits, const int32_t *n_dev) {
+    if (n_dev) n = *n_dev;
+    constexpr int kWarps = kTileThreads / 32;
+    constexpr int kRounds = kTile / kTileThreads;
+    constexpr int PER = kMaxRadix / kTileThreads;
+    extern __shared__ int32_t sm3[];
+    const int radix = 1 << bits;
+    int32_t *wc = sm3;                           // [kWarps][radix]
+    int32_t *gbase = wc + kWarps * radix;        // [radix] global start of this tile's digit run
+    int32_t *tstart = gbase + radix;             // [radix] tile-local start of the digit run
+    int32_t *sk = tstart + radix;                // [kTile] staged keys
+    int32_t *sv = sk + kTile;                    // [kTile] staged values
+    using BlockScan = cub::BlockScan<int32_t, kTileThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    const unsigned dmask = (unsigned)radix - 1u;
+    for (int i = threadIdx.x; i < kWarps * radix; i += kTileThreads) wc[i] = 0;
+    {   // global digit starts: exclusive scan of the digit totals + this tile's offset
+        int32_t v[PER], s = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int d = threadIdx.x * PER + i;
+            v[i] = d < radix ? rowtot[d] : 0;
+            s += v[i];
+        }
+        int32_t e;
+        BlockScan(tmp).ExclusiveSum(s, e);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int d = threadIdx.x * PER + i;
+            if (d < radix) gbase[d] = e + hist_off[(int64_t)d * nblk + blockIdx.x];
+            e += v[i];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+    const int64_t base = tile0 + (int64_t)w * (32 * kRounds);
+    int32_t key[kRounds], val[kRounds], rk[kRounds];
+    int dg[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t g = base + r * 32 + lane;
+        key[r] = g < n ? __ldg(kin + g) : 0;
+        val[r] = g < n ? __ldg(vin + g) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {  // stable rank within the warp's digit run
+        const int64_t g = base + r * 32 + lane;
+        const bool valid = g < n;
+        dg[r] = valid ? (int)(((unsigned)key[r] >> shift) & dmask) : (kMaxRadix + lane);
+        const unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
+        int32_t before = 0;
+        if (valid) before = wc[w * radix + dg[r]];
+        rk[r] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wc[w * radix + dg[r]] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {   // per digit: warp prefixes (in place) and the tile total; then tile-local digit starts
+        int32_t tot[PER], s = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int d = threadIdx.x * PER + i;
+            int32_t run = 0;
+            if (d < radix)
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ++ww) {
+                    const int32_t t = wc[ww * radix + d];
+                    wc[ww * radix + d] = run;
+                    run += t;
+                }
+            tot[i] = run;
+            s += run;
+        }
+        int32_t e;
+        BlockScan(tmp).ExclusiveSum(s, e);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int d = threadIdx.x * PER + i;
+            if (d < radix) tstart[d] = e;
+            e += tot[i];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {  // stage in digit order (stable)
+        const int64_t g = base + r * 32 + lane;
+        if (g < n) {
+            const int lp = tstart[dg[r]] + wc[w * radix + dg[r]] + rk[r];
+            sk[lp] = key[r];
+            sv[lp] = val[r];
+        }
+    }
+    __syncthreads();
+    const int nt = (int)(n - tile0 < kTile ? n - tile0 : kTile);
+    const unsigned nmask = (1u << next_bits) - 1u;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {  // consecutive threads -> consecutive positions of a run
+        const int i = r * kTileThreads + threadIdx.x;
+        const bool valid = i < nt;
+        int32_t pos = 0, k = 0;
+        if (valid) {
+            k = sk[i];
+            const int d = (int)(((unsigned)k >> shift) & dmask);
+            pos = gbase[d] + (i - tstart[d]);
+            kout[pos] = k;
+            vout[pos] = sv[i];
+        }
+        if (hist_next) {
+            const unsigned vm = __ballot_sync(0xffffffffu, valid);
+            if (valid) {
+                const int64_t slot = (int64_t)(((unsigned)k >> next_shift) & nmask) * nblk + pos / kTile;
+                const unsigned peers = __match_any_sync(vm, (unsigned long long)slot);
+                if (lane == __ffs(peers) - 1) atomicAdd(hist_next + slot, (int32_t)__popc(peers));
+            }
+        }
+    }
+}
+
+size_t scatter3_smem(int bits) { return sizeof(int32_t) * ((size_t)(kTileThreads / 32 + 2) * (1u << bits) + 2 * kTile); }
+
 // Next pass's digit histogram of every 2048-key tile of a pass's output (large sorts: cheaper
 // than the scatter's per-key global atomics once the key count is in the millions).
 __global__ void __launch_bounds__(kTileThreads) k_hist_tiles(const int32_t *keys, int64_t n, int shift, int bits,
@@ -197,11 +330,27 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
         k_scan_rows<<<(rows + 7) / 8, 256, 0, s>>>(hist[p & 1], nblk, rowtot, more ? hist[(p + 1) & 1] : nullptr,
                                                    radix, next_radix);
         const bool fused_hist = more && n < kBigSort;
-        k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
-                                                          plan.bits[p], hist[p & 1], rowtot, nblk,
-                                                          fused_hist ? hist[(p + 1) & 1] : nullptr,
-                                                          more ? plan.shift[p + 1] : 0, more ? plan.bits[p + 1] : 0,
-                                                          nullptr);
+        static const bool v3 = !(std::getenv("PICASSO_SORT") && std::string(std::getenv("PICASSO_SORT")) == "2");
+        if (v3) {
+            const size_t sm = scatter3_smem(plan.bits[p]);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_scatter3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)scatter3_smem(kMaxRadixBits));
+                attr = true;
+            }
+            k_scatter3<<<(unsigned)nblk, kTileThreads, sm, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
+                                                                plan.bits[p], hist[p & 1], rowtot, nblk,
+                                                                fused_hist ? hist[(p + 1) & 1] : nullptr,
+                                                                more ? plan.shift[p + 1] : 0,
+                                                                more ? plan.bits[p + 1] : 0, nullptr);
+        } else {
+            k_scatter2<<<(unsigned)nblk, kTileThreads, 0, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
+                                                              plan.bits[p], hist[p & 1], rowtot, nblk,
+                                                              fused_hist ? hist[(p + 1) & 1] : nullptr,
+                                                              more ? plan.shift[p + 1] : 0,
+                                                              more ? plan.bits[p + 1] : 0, nullptr);
+        }
         *launches += 2;
         if (more && !fused_hist) {
             k_hist_tiles<<<(unsigned)nblk, kTileThreads, 0, s>>>(bufk[p & 1], n, plan.shift[p + 1], plan.bits[p + 1],
