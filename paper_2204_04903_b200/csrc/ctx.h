@@ -169,7 +169,7 @@ struct picasso_ctx {
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share
     bool early_pool = false;  // W = 1: pool concurrently with the dedup + transpose chain
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fp = nullptr, ev_seg = nullptr;
     cudaStream_t side2 = nullptr;  // K-Interleaving: the pools / owner updates beside the exchange
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     int kinterleave = 1;           // PICASSO_KINTERLEAVE=0 turns the per-pack pipelining off

@@ -246,6 +246,8 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fp, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_seg, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming));
@@ -262,6 +264,8 @@ extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
         cudaStreamDestroy(ctx->side);
         cudaEventDestroy(ctx->ev_fork);
         cudaEventDestroy(ctx->ev_join);
+        cudaEventDestroy(ctx->ev_fp);
+        cudaEventDestroy(ctx->ev_seg);
         cudaStreamDestroy(ctx->side2);
         cudaEventDestroy(ctx->ev_fork2);
         cudaEventDestroy(ctx->ev_join2);
@@ -376,6 +380,25 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         picasso::transpose_on(ctx, t);
         CK(cudaEventRecord(ctx->ev_join, t));
         ctx->launches_fwd += 2 + (n_ids > 0 ? 4 : 0) + 1;  // prep, seg_of, insert+flag+scan+assign, inverse
+    } else if (ctx->overlap && ctx->side) {
+        // the internal stream takes seg_of (needs only the field layout) beside the dedup chain,
+        // then the transpose beside the pool
+        ctx->mark(0, true, s);
+        CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+        launch_field_prep(a, s);
+        CK(cudaEventRecord(ctx->ev_fp, s));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fp, 0));
+        launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, ctx->side);
+        CK(cudaEventRecord(ctx->ev_seg, ctx->side));
+        launch_dedup_insert(a, s);
+        launch_dedup_assign(a, s);
+        ctx->mark(0, false, s);
+        ctx->launches_fwd += 2 + (n_ids > 0 ? 4 : 0) + 1;  // prep, seg_of, insert+flag+scan+assign, inverse
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        picasso::transpose_on(ctx, ctx->side);
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+        CK(cudaStreamWaitEvent(s, ctx->ev_seg, 0));  // the pool reads seg_of
     } else {
         ctx->mark(0, true, s);
         CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
