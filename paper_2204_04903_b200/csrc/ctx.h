@@ -138,7 +138,8 @@ struct picasso_ctx {
     int32_t *pm_fields_d = nullptr, *pack_first_k_d = nullptr;
     int32_t *field_k_d = nullptr;  // [F] index of each field within its pack
     bool pipe_pool = true;         // PICASSO_POOL=legacy selects the register-staged pool for every D
-    int pool_kind = 1;             // PICASSO_POOL=flat (2) | pipe (1, D >= 64) | legacy
+    int pool_kind = 1;             // PICASSO_POOL=flat (2: k_pool_flat for every D) | default (1: the
+                                   // cp.async ring for D >= 64, k_pool_flat below) | legacy (k_pool)
     int64_t *pack_key_off_d = nullptr;
     int32_t *id_start = nullptr, *gstart_pm = nullptr, *field_gstart = nullptr, *pack_gstart = nullptr;
     int32_t *pack_ustart = nullptr;
