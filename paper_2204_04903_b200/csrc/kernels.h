@@ -72,11 +72,7 @@ void launch_dedup_assign(const IndexArgs &a, cudaStream_t s);  // flag, scan, ui
 void launch_scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *scratch, int32_t *total,
                            cudaStream_t s);
 size_t scan_scratch_ints(int64_t n);
-// Stable LSD radix sort of (key, val) int32 pairs by key < 2^bits.  Result in (k_out, v_out).
-void radix_sort_pairs(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, int32_t *v_a, int32_t *k_b,
-                      int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, int bits, int32_t *hist,
-                      int32_t *scratch, cudaStream_t s, int64_t *launches);
-size_t radix_hist_ints(int64_t n);
+
 
 // k_pool.cu
 struct PoolArgs {
