@@ -146,6 +146,11 @@ struct picasso_ctx {
     Slot *table = nullptr;
     int32_t *slot_of = nullptr, *seg_of = nullptr, *inverse = nullptr;
     uint8_t *fmask = nullptr;  // first-occurrence flags (k_flag_count -> k_assign)
+    int64_t *region_base = nullptr;  // per-table dedup hash regions (k_field_prep)
+    int region_shift = 1;
+    bool use_regions = false;        // max_ids > 2M: one global table would not stay in L2
+    uint32_t *region_mask = nullptr;
+    int32_t *tocc = nullptr;
     int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
     int *err = nullptr;
     unsigned long long *unique_gkey = nullptr;
@@ -242,6 +247,9 @@ struct picasso_ctx {
         pack_gstart = c.take<int32_t>(P + 1);
         pack_ustart = c.take<int32_t>(P + 1);
         table = c.take<Slot>(cap);
+        region_base = c.take<int64_t>(T + 1);
+        region_mask = c.take<uint32_t>(T);
+        tocc = c.take<int32_t>(T);
         slot_of = c.take<int32_t>(N);
         fmask = c.take<uint8_t>(NR / 8 + 2);
         seg_of = c.take<int32_t>(N);

@@ -74,24 +74,85 @@ __global__ void __launch_bounds__(1024) k_field_prep(IndexArgs a) {
     if (tid == 0) a.gstart_pm[a.F] = carry;
     __syncthreads();
     for (int p = tid; p <= a.P; p += 1024) a.pack_gstart[p] = a.gstart_pm[a.pack_first_k[p]];
+    if (!a.region_base) return;
+    // per-table hash regions: pow2 >= 2^region_shift x (occurrences of the table's fields), >= 64
+    // slots, laid out in table order — the positions of one table are contiguous in the packed
+    // stream, so the inserts / flag / assign / inverse passes over a range of positions touch one
+    // region at a time, which stays in L2 even when the whole table is gigabytes
+    for (int t = tid; t < a.T; t += 1024) a.tocc[t] = 0;
+    __syncthreads();
+    for (int f = tid; f < a.F; f += 1024)
+        atomicAdd(a.tocc + a.finfo[f].table,
+                  a.offsets[(int64_t)(f + 1) * a.B] - a.offsets[(int64_t)f * a.B]);
+    __syncthreads();
+    __shared__ int64_t s_carry, wsum64[32];
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int base0 = 0; base0 < a.T; base0 += 1024) {  // block scan of the region sizes
+        const int t = base0 + tid;
+        uint64_t sz = 0;
+        if (t < a.T) {
+            const int32_t occ = __ldcg(a.tocc + t);
+            sz = 64;
+            while (sz < ((uint64_t)occ << a.region_shift)) sz <<= 1;
+            a.region_mask[t] = (uint32_t)(sz - 1);
+        }
+        const int lane = tid & 31, w = tid >> 5;
+        int64_t x = (int64_t)sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum64[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int64_t y = wsum64[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            wsum64[lane] = y;
+        }
+        __syncthreads();
+        if (t < a.T) a.region_base[t] = s_carry + (w ? wsum64[w - 1] : 0) + x - (int64_t)sz;
+        __syncthreads();
+        if (tid == 0) s_carry += wsum64[31];
+        __syncthreads();
+    }
+    if (tid == 0) a.region_base[a.T] = s_carry;
 }
 
-void launch_field_prep(const IndexArgs &a, cudaStream_t s) { k_field_prep<<<1, 1024, 0, s>>>(a); }
+// the dedup table's used part (the regions) back to empty (0xFF), size from the device
+__global__ void k_table_clear(ulonglong2 *table, const int64_t *total) {
+    const int64_t n = *total;
+    const ulonglong2 e = make_ulonglong2(~0ull, ~0ull);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        table[i] = e;
+}
+
+void launch_field_prep(const IndexArgs &a, cudaStream_t s) {
+    k_field_prep<<<1, 1024, 0, s>>>(a);
+    if (a.region_base)
+        k_table_clear<<<1184, 256, 0, s>>>(reinterpret_cast<ulonglong2 *>(a.table), a.region_base + a.T);
+}
 
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_dedup_insert(IndexArgs a) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = g < a.N;
     unsigned long long gkey = 0;
+    int32_t tbl = 0;
     if (valid) {
-        // packed position -> pm field -> field-major index j (segment ids are written by the
-        // pool kernel, which walks segments anyway)
+        // packed position -> pm field -> field-major index j
         const int64_t k = upper_bound_dev(a.gstart_pm, 0, a.F + 1, (int32_t)g) - 1;
         const int f = __ldg(a.pm_fields + k);
         const int64_t j = (int64_t)__ldg(a.id_start + f) + (g - __ldg(a.gstart_pm + k));
         const FieldInfo fi = a.finfo[f];
         const int64_t row = row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
         gkey = (unsigned long long)(__ldg(a.pack_key_off + fi.pack) + fi.base + row);
+        tbl = fi.table;
     }
     // warp pre-dedup: lanes holding the same key elect the lowest lane (= smallest g)
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
@@ -101,13 +162,20 @@ __global__ void __launch_bounds__(256) k_dedup_insert(IndexArgs a) {
     const int leader = __ffs(peers) - 1;
     uint32_t slot = 0;
     if (lane == leader) {
-        slot = slot_hash(gkey) & a.cap_mask;
+        uint32_t rbase = 0, mask = a.cap_mask;
+        if (a.region_base) {  // the table's own region (k_field_prep); equal keys: same table
+            rbase = (uint32_t)__ldg(a.region_base + tbl);
+            mask = __ldg(a.region_mask + tbl);
+        }
+        uint32_t h = slot_hash(gkey) & mask;
+        slot = rbase + h;
         for (uint32_t probe = 0;; ++probe) {
             unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(&a.table[slot].key);
             if (cur == kEmptyKey) cur = atomicCAS(&a.table[slot].key, kEmptyKey, gkey);
             if (cur == kEmptyKey || cur == gkey) break;
-            slot = (slot + 1) & a.cap_mask;
-            if (probe > a.cap_mask) {  // table full: cannot happen with cap >= 2N
+            h = (h + 1) & mask;
+            slot = rbase + h;
+            if (probe > mask) {  // region full: cannot happen with 2x occurrences
                 atomicOr(a.err, ERR_CAPACITY);
                 break;
             }

@@ -40,6 +40,12 @@ struct IndexArgs {
     int64_t *pack_gbase;           // [P+1] out: float offset of each pack's G rows (sum U_p * D_p)
     const int32_t *n_dev;          // if set: the position count lives on the device (N = capacity)
     uint8_t *fmask;                // [N/8+1] first-occurrence flags, 8 positions per byte
+    int32_t T;                     // tables
+    int64_t *region_base;          // [T+1] per-table hash region start (slots); [T] = total (nullptr:
+                                   //   one global table masked by cap_mask)
+    uint32_t *region_mask;         // [T] region size - 1
+    int32_t region_shift;          // region >= occurrences << shift (load factor <= 1/2 or 1/4)
+    int32_t *tocc;                 // [T] scratch: occurrences per table
     int32_t sort_bits0;            // digit width of the backward's first radix pass
     int32_t *sort_hist0;           // [radix0, nblk] out: digit-major histogram of that pass
     int *err;

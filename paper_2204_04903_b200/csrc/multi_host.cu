@@ -122,8 +122,8 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
     const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(N, 1) * 2));
     a.cap_mask = cap_step - 1;
     ctx->mark(0, true, s);
-    MCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
-    launch_field_prep(a, s);
+    if (!a.region_base) MCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+    launch_field_prep(a, s);  // (+ the table regions' clear)
     launch_dedup_insert(a, s);
     launch_dedup_assign(a, s);
     MultiArgs m = multi_args(ctx);

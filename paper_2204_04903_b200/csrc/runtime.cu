@@ -99,7 +99,17 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
             if (c->t2p[c->f2t[f]] == p) c->pm_fields.push_back(f);
     }
     c->pack_first_k[c->P] = c->F;
+    // dedup table: per-table regions (<= 4 x max_ids + 64 per table) for the rank-local dedup, and a
+    // pow2 >= 2 x max_recv global table for the NCCL owner dedup, in the same slots
     c->cap = pow2_at_least((uint64_t)std::max<int64_t>(std::max<int64_t>(opts->max_ids, c->mp.max_recv), 1) * 2);
+    // per-table regions only when one global table would not stay in L2 (2 x max_ids x 16 B > ~64 MB):
+    // below that the global table (load factor <= 1/4 here) has the shorter probe chains
+    c->use_regions = opts->max_ids > ((int64_t)1 << 21);
+    if (const char *e = std::getenv("PICASSO_DEDUP_REGIONS")) c->use_regions = std::atoi(e) != 0;
+    c->region_shift = 1;
+    if (c->use_regions)
+        c->cap = (uint32_t)std::max<uint64_t>(
+            c->cap, ((uint64_t)opts->max_ids << (c->region_shift + 1)) + 64 * (uint64_t)c->T);
     if (world > 1) {  // local rows must fit int32 (received keys are int32 local rows)
         for (int32_t p = 0; p < c->P; ++p)
             if (c->pack_rows[p] / world >= ((int64_t)1 << 31)) {
@@ -324,6 +334,11 @@ IndexArgs picasso::make_index_args(picasso_ctx *ctx, const int64_t *ids, const i
     a.table = ctx->table;
     a.slot_of = ctx->slot_of;
     a.fmask = ctx->fmask;
+    a.T = ctx->T;
+    a.region_base = ctx->use_regions ? ctx->region_base : nullptr;
+    a.region_mask = ctx->region_mask;
+    a.region_shift = ctx->region_shift;
+    a.tocc = ctx->tocc;
     a.seg_of = ctx->seg_of;
     a.inverse = ctx->inverse;
     a.blk_cnt = ctx->blk_cnt;
@@ -367,13 +382,13 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         // At world == 1 the pool needs only the raw IDs (row = h(id)), not the dedup: the index
         // work (Unique, inverse) and the backward's transpose run on the internal stream while
         // the pool streams rows on the caller's stream; the forward joins both before returning.
+        if (!a.region_base) CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
         launch_field_prep(a, s);
         launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
         CK(cudaEventRecord(ctx->ev_fork, s));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
         cudaStream_t t = ctx->side;
         ctx->mark(0, true, t);
-        CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, t));
         launch_dedup_insert(a, t);
         launch_dedup_assign(a, t);
         ctx->mark(0, false, t);
@@ -384,8 +399,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         // the internal stream takes seg_of (needs only the field layout) beside the dedup chain,
         // then the transpose beside the pool
         ctx->mark(0, true, s);
-        CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
-        launch_field_prep(a, s);
+        if (!a.region_base) CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+        launch_field_prep(a, s);  // (+ the table regions' clear)
         CK(cudaEventRecord(ctx->ev_fp, s));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fp, 0));
         launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, ctx->side);
@@ -401,8 +416,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         CK(cudaStreamWaitEvent(s, ctx->ev_seg, 0));  // the pool reads seg_of
     } else {
         ctx->mark(0, true, s);
-        CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
-        launch_field_prep(a, s);
+        if (!a.region_base) CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+        launch_field_prep(a, s);  // (+ the table regions' clear)
         launch_dedup_insert(a, s);
         launch_dedup_assign(a, s);
         ctx->mark(0, false, s);
