@@ -151,6 +151,7 @@ struct picasso_ctx {
     bool use_regions = false;        // max_ids > 2M: one global table would not stay in L2
     uint32_t *region_mask = nullptr;
     int32_t *tocc = nullptr;
+    int32_t *empty_pack = nullptr;  // [P] the pack has an empty segment this step
     int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
     int *err = nullptr;
     unsigned long long *unique_gkey = nullptr;
@@ -250,6 +251,7 @@ struct picasso_ctx {
         region_base = c.take<int64_t>(T + 1);
         region_mask = c.take<uint32_t>(T);
         tocc = c.take<int32_t>(T);
+        empty_pack = c.take<int32_t>(P);
         slot_of = c.take<int32_t>(N);
         fmask = c.take<uint8_t>(NR / 8 + 2);
         seg_of = c.take<int32_t>(N);

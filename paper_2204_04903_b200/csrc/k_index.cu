@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(1024) k_field_prep(IndexArgs a) {
     if (tid == 0) a.gstart_pm[a.F] = carry;
     __syncthreads();
     for (int p = tid; p <= a.P; p += 1024) a.pack_gstart[p] = a.gstart_pm[a.pack_first_k[p]];
+    if (a.empty_pack)
+        for (int p = tid; p < a.P; p += 1024) a.empty_pack[p] = 0;
     if (!a.region_base) return;
     // per-table hash regions: pow2 >= 2^region_shift x (occurrences of the table's fields), >= 64
     // slots, laid out in table order — the positions of one table are contiguous in the packed

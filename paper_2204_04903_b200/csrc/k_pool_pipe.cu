@@ -13,7 +13,9 @@
 //                   issues the LDGSTS copies of its slice of each row into a per-warp
 //                   shared-memory ring.  Landed rows are added in order in fp32; a finished
 //                   segment is written into its column block of the [B, out_width] output
-//                   with streaming stores, and empty segments in between get zeros.
+//                   with streaming stores.  Empty segments (no position to visit) are written by
+//                   k_pool_zero_empty in a pass over the segments' offsets: a warp here would walk
+//                   them one by one (C4's sparse positional fields: 13 ms).
 #include "kernels.h"
 
 namespace picasso {
@@ -76,20 +78,16 @@ __device__ __forceinline__ void lane_store_cs(float *row, int lane, const float 
     }
 }
 
+// (also flags the packs that have an empty segment: k_pool_zero_empty runs only for those)
 __global__ void k_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart,
-                         const int32_t *id_start, int32_t *seg_of) {
+                         const int32_t *id_start, int32_t *seg_of, const FieldInfo *finfo, int32_t *empty_pack) {
     const int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sg >= (int64_t)F * B) return;
     const int32_t f = (int32_t)(sg / B);
     const int32_t o0 = __ldg(offsets + sg), o1 = __ldg(offsets + sg + 1);
     const int32_t gb = __ldg(field_gstart + f) - __ldg(id_start + f);
     for (int32_t j = o0; j < o1; ++j) seg_of[j + gb] = (int32_t)sg;
-}
-
-// output offset of the pack's ps-th segment (ps = k * B + b, k-th field of the pack)
-__device__ __forceinline__ int64_t seg_out(const PoolArgs &a, int32_t ps) {
-    const int32_t k = ps / a.B, b = ps - k * a.B;
-    return (int64_t)b * a.out_stride + a.finfo[__ldg(a.pack_fields + k)].col;
+    if (o1 == o0 && empty_pack) empty_pack[finfo[f].pack] = 1;
 }
 
 template <int D>
@@ -99,7 +97,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int32_t P0 = __ldg(a.pack_gstart + a.pack), P1 = __ldg(a.pack_gstart + a.pack + 1);
-    const int32_t nseg = a.Fp * a.B;
     const int64_t nwarps = (int64_t)gridDim.x * kNW;
     const int64_t t = (int64_t)blockIdx.x * kNW + w;
     const int32_t tile = (int32_t)((P1 - P0 + nwarps - 1) / nwarps);
@@ -124,17 +121,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
     const int32_t pa = seg_start_from(P0 + (int32_t)(na < n ? na : n));
     const int32_t pb = seg_start_from(P0 + (int32_t)(nb < n ? nb : n));
     const int32_t seg_before = pa > P0 && pa < P1 ? pseg(pa - 1) : -1;  // segment of position pa - 1
-    const bool last_tile = pb == P1;
-    if (pa >= pb) {
-        // no positions: a pack whose segments are all empty still needs its zeros (first warp)
-        if (P1 == P0 && t == 0) {
-            float z[EPL];
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) z[e] = 0.f;
-            for (int32_t s = 0; s < nseg; ++s) lane_store_cs<D>(a.out + seg_out(a, s), lane, z);
-        }
-        return;
-    }
+    if (pa >= pb) return;  // empty segments get their zeros from k_pool_zero_empty
     int64_t *s_out = reinterpret_cast<int64_t *>(smem) + (size_t)w * kS * RS;
     int32_t *s_seg = reinterpret_cast<int32_t *>(smem + (size_t)kNW * kS * RS * 8) + (size_t)w * kS * RS;
     unsigned char *wr = smem + G::RING_OFF + (size_t)w * kS * SB;
@@ -203,9 +190,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
     float acc[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
-    float zero[EPL];
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) zero[e] = 0.f;
     int32_t cur = seg_before, ncur = 0;  // current segment (pack order) and its length so far
     int64_t cur_out = 0;
     auto flush = [&]() {
@@ -240,8 +224,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
                 const int32_t sg = s_seg[slot * RS + i];
                 if (sg != cur) {
                     if (ncur > 0) flush();
-#pragma unroll 1
-                    for (int32_t z = cur + 1; z < sg; ++z) lane_store_cs<D>(a.out + seg_out(a, z), lane, zero);
                     cur = sg;
                     cur_out = s_out[slot * RS + i];
                     ncur = 0;
@@ -256,9 +238,6 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
         ldgsts_commit();
     }
     flush();
-    if (last_tile)  // trailing empty segments of the pack
-#pragma unroll 1
-        for (int32_t z = cur + 1; z < nseg; ++z) lane_store_cs<D>(a.out + seg_out(a, z), lane, zero);
 }
 
 template <int D>
@@ -280,9 +259,11 @@ bool pool_pipe_supported(int D, const PoolArgs &a) {
 }
 
 void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
-                   int32_t *seg_of, cudaStream_t s) {
+                   int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo, int32_t *empty_pack) {
     const int64_t n = (int64_t)F * B;
-    if (n > 0) k_seg_of<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(offsets, B, F, field_gstart, id_start, seg_of);
+    if (n > 0)
+        k_seg_of<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(offsets, B, F, field_gstart, id_start, seg_of, finfo,
+                                                            empty_pack);
 }
 
 int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s) {

@@ -338,6 +338,7 @@ IndexArgs picasso::make_index_args(picasso_ctx *ctx, const int64_t *ids, const i
     a.region_base = ctx->use_regions ? ctx->region_base : nullptr;
     a.region_mask = ctx->region_mask;
     a.region_shift = ctx->region_shift;
+    a.empty_pack = ctx->empty_pack;
     a.tocc = ctx->tocc;
     a.seg_of = ctx->seg_of;
     a.inverse = ctx->inverse;
@@ -384,7 +385,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         // the pool streams rows on the caller's stream; the forward joins both before returning.
         if (!a.region_base) CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
         launch_field_prep(a, s);
-        launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
+        launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s, ctx->finfo,
+                      ctx->empty_pack);
         CK(cudaEventRecord(ctx->ev_fork, s));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
         cudaStream_t t = ctx->side;
@@ -403,7 +405,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         launch_field_prep(a, s);  // (+ the table regions' clear)
         CK(cudaEventRecord(ctx->ev_fp, s));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fp, 0));
-        launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, ctx->side);
+        launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, ctx->side, ctx->finfo,
+                      ctx->empty_pack);
         CK(cudaEventRecord(ctx->ev_seg, ctx->side));
         launch_dedup_insert(a, s);
         launch_dedup_assign(a, s);
@@ -493,7 +496,8 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
 // returns (a forward stays self-contained, e.g. inside a CUDA graph capture).  k_seg_of first:
 // segment of every packed position, for the sort and the pool.
 void picasso::transpose_fork(picasso_ctx *ctx, cudaStream_t s) {
-    launch_seg_of(ctx->offsets, ctx->B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s);
+    launch_seg_of(ctx->offsets, ctx->B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s, ctx->finfo,
+                  ctx->empty_pack);
     ctx->launches_fwd += (int64_t)ctx->F * ctx->B > 0 ? 1 : 0;
     cudaStream_t t = s;
     if (ctx->overlap && ctx->side) {
@@ -545,6 +549,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
     pa.err = ctx->err;
     pa.pack_gstart = ctx->pack_gstart;
     pa.field_k = ctx->pipe_pool ? ctx->field_k_d : nullptr;
+    pa.empty_pack = ctx->empty_pack;
     for (int32_t p = 0; p < ctx->P; ++p) {  // seg_of: written by transpose_fork (k_seg_of)
         if (only_pack >= 0 && p != only_pack) continue;
         pa.pack = p;
@@ -556,6 +561,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
             n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else if (pool_pipe_supported(ctx->pack_dim[p], pa)) {  // D >= 64: the cp.async ring
             n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->pool_sms, s);
+            n += launch_pool_zero_empty(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else if (ctx->pipe_pool) {  // narrow rows: one thread per 16-B chunk (C4: 20 -> 6 ms)
             n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else {  // PICASSO_POOL=legacy
