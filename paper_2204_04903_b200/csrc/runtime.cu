@@ -629,6 +629,7 @@ extern "C" picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t
             if (cudaMemcpy(&h, ctx->err, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && h) {
                 if (h & ERR_ID_RANGE) { st = PICASSO_ERR_ID_RANGE; m = "raw ID outside [0, V_t) in ROWS mode"; }
                 else if (h & ERR_CAPACITY) { st = PICASSO_ERR_CAPACITY; m = "device capacity overflow"; }
+                else if (h & ERR_PEER_TIMEOUT) { st = PICASSO_ERR_CUDA; m = "peer timeout: a rank never reached a barrier"; }
                 cudaMemset(ctx->err, 0, sizeof(int));
             }
         }
