@@ -30,6 +30,7 @@ def _nccl_dir():
 NCCL = _nccl_dir()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include")]
+FLAGS += os.environ.get("PICASSO_NVCC_EXTRA", "").split()  # tuning experiments only
 
 
 def _needs(obj, src, deps):

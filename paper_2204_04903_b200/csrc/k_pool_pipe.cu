@@ -25,15 +25,15 @@ __device__ __forceinline__ void ldgsts16(void *smem, const void *gmem) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void ldgsts8(void *smem, const void *gmem) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void ldgsts_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void ldgsts_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int kNW = 16, kS = 3, kStageBytes = 4096;
+#ifndef PICASSO_CONSUME_ROWS
+#define PICASSO_CONSUME_ROWS 4
+#endif
+constexpr int kConsumeRows = PICASSO_CONSUME_ROWS;  // rows per unrolled consume step
 
 template <int D>
 struct PG {
@@ -94,6 +94,7 @@ template <int D>
 __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
     using G = PG<D>;
     constexpr int RS = G::RS, SB = G::SB, ROWB = G::ROWB, EPL = G::EPL;
+    constexpr int CH = RS < kConsumeRows ? RS : kConsumeRows;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int32_t P0 = __ldg(a.pack_gstart + a.pack), P1 = __ldg(a.pack_gstart + a.pack + 1);
@@ -167,14 +168,19 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
         const int nrows = pb - p0 < RS ? pb - p0 : RS;
         const int l0 = (k * RS) & 31;
         unsigned char *dst = wr + slot * SB;
+        if constexpr (EPL == 2) {  // D = 64: two rows per instruction, a half-warp of 16-B copies each
+            const int h = lane >> 4, c = lane & 15;
 #pragma unroll
-        for (int i = 0; i < RS; ++i) {
-            const int64_t row = __shfl_sync(0xffffffffu, row_c, l0 + i);
-            if (i < nrows) {
-                const float *src = a.weight + row;
-                if constexpr (EPL == 2) {
-                    ldgsts8(dst + i * ROWB + lane * 8, src + lane * 2);
-                } else {
+            for (int i = 0; i < RS; i += 2) {
+                const int64_t row = __shfl_sync(0xffffffffu, row_c, l0 + i + h);
+                if (i + h < nrows) ldgsts16(dst + (i + h) * ROWB + c * 16, a.weight + row + c * 4);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < RS; ++i) {
+                const int64_t row = __shfl_sync(0xffffffffu, row_c, l0 + i);
+                if (i < nrows) {
+                    const float *src = a.weight + row;
 #pragma unroll
                     for (int q = 0; q < EPL / 4; ++q) ldgsts16(dst + i * ROWB + q * 512 + lane * 16, src + q * 128 + lane * 4);
                 }
@@ -214,23 +220,29 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
         const int32_t p0 = pa + k * RS;
         const int nrows = pb - p0 < RS ? pb - p0 : RS;
         const float *rows = reinterpret_cast<const float *>(wr + slot * SB);
-        float v[RS][EPL];
+        // CH rows at a time (a fully unrolled stage with its inlined flushes overflows the
+        // instruction cache at D = 64)
+#pragma unroll 1
+        for (int i0 = 0; i0 < nrows; i0 += CH) {
+            float v[CH][EPL];
 #pragma unroll
-        for (int i = 0; i < RS; ++i)
-            if (i < nrows) lane_load<D>(rows + i * D, lane, v[i]);
+            for (int c = 0; c < CH; ++c)
+                if (i0 + c < nrows) lane_load<D>(rows + (i0 + c) * D, lane, v[c]);
 #pragma unroll
-        for (int i = 0; i < RS; ++i) {
-            if (i < nrows) {
-                const int32_t sg = s_seg[slot * RS + i];
-                if (sg != cur) {
-                    if (ncur > 0) flush();
-                    cur = sg;
-                    cur_out = s_out[slot * RS + i];
-                    ncur = 0;
+            for (int c = 0; c < CH; ++c) {
+                const int i = i0 + c;
+                if (i < nrows) {
+                    const int32_t sg = s_seg[slot * RS + i];
+                    if (sg != cur) {
+                        if (ncur > 0) flush();
+                        cur = sg;
+                        cur_out = s_out[slot * RS + i];
+                        ncur = 0;
+                    }
+                    ++ncur;
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) acc[e] = __fadd_rn(acc[e], v[c][e]);
                 }
-                ++ncur;
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) acc[e] = __fadd_rn(acc[e], v[i][e]);
             }
         }
         __syncwarp();

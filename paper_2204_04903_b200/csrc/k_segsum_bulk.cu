@@ -27,12 +27,9 @@
 namespace picasso {
 namespace {
 
-__device__ __forceinline__ void ldgsts(void *smem, const void *gmem, int bytes) {
+__device__ __forceinline__ void ldgsts(void *smem, const void *gmem) {  // 16 bytes, bypassing L1
     const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
-    if (bytes == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void ldgsts_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -40,6 +37,10 @@ __device__ __forceinline__ void ldgsts_wait() { asm volatile("cp.async.wait_grou
 
 constexpr int kStageBytes = 4096;  // target bytes per ring stage
 constexpr int kMaxNW = 16;         // warps per CTA at most (sizes the tile arrays)
+#ifndef PICASSO_CONSUME_ROWS
+#define PICASSO_CONSUME_ROWS 4
+#endif
+constexpr int kConsumeRows = PICASSO_CONSUME_ROWS;  // rows per unrolled consume step
 
 template <int D, int NW, int S>
 struct BG {
@@ -223,6 +224,7 @@ template <int D, int NW, int S, bool FUSE>
 __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     using G = BG<D, NW, S>;
     constexpr int RS = G::RS, SB = G::SB, ROWB = G::ROWB, EPL = G::EPL;
+    constexpr int CH = RS < kConsumeRows ? RS : kConsumeRows;
     extern __shared__ __align__(128) unsigned char smem[];
     int64_t *s_row = reinterpret_cast<int64_t *>(smem);
     int32_t *s_uid = reinterpret_cast<int32_t *>(smem + (size_t)NW * S * RS * 8);
@@ -287,17 +289,22 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
         const int nrows = pb - p0 < RS ? pb - p0 : RS;
         const int l0 = (k * RS) & 31;
         unsigned char *dst = wr + slot * SB;
+        if constexpr (EPL == 2) {  // D = 64: two rows per instruction, a half-warp of 16-B copies each
+            const int h = lane >> 4, c = lane & 15;
 #pragma unroll
-        for (int i = 0; i < RS; ++i) {
-            const uint32_t off = __shfl_sync(0xffffffffu, off_c, l0 + i);
-            if (i < nrows) {
-                const float4 *src = dy4 + off;
-                if constexpr (EPL == 2) {
-                    ldgsts(dst + i * ROWB + lane * 8, reinterpret_cast<const float *>(src) + lane * 2, 8);
-                } else {
+            for (int i = 0; i < RS; i += 2) {
+                const uint32_t off = __shfl_sync(0xffffffffu, off_c, l0 + i + h);
+                if (i + h < nrows) ldgsts(dst + (i + h) * ROWB + c * 16, dy4 + off + c);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < RS; ++i) {
+                const uint32_t off = __shfl_sync(0xffffffffu, off_c, l0 + i);
+                if (i < nrows) {
+                    const float4 *src = dy4 + off;
 #pragma unroll
                     for (int q = 0; q < EPL / 4; ++q)
-                        ldgsts(dst + i * ROWB + q * 512 + lane * 16, src + q * 32 + lane, 16);
+                        ldgsts(dst + i * ROWB + q * 512 + lane * 16, src + q * 32 + lane);
                 }
             }
         }
@@ -362,28 +369,34 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
         const int32_t p0 = pa + k * RS;
         const int nrows = pb - p0 < RS ? pb - p0 : RS;
         const float *rows = reinterpret_cast<const float *>(wr + slot * SB);
-        float v[RS][EPL];
+        // CH rows at a time: the flush is inlined once per row of the unrolled body, and a
+        // fully unrolled stage (16 rows at D = 64) overflows the instruction cache
+#pragma unroll 1
+        for (int i0 = 0; i0 < nrows; i0 += CH) {
+            float v[CH][EPL];
 #pragma unroll
-        for (int i = 0; i < RS; ++i)
-            if (i < nrows) lane_load<D>(rows + i * D, lane, v[i]);
+            for (int c = 0; c < CH; ++c)
+                if (i0 + c < nrows) lane_load<D>(rows + (i0 + c) * D, lane, v[c]);
 #pragma unroll
-        for (int i = 0; i < RS; ++i) {
-            if (i < nrows) {
-                const int32_t uid = wu[slot * RS + i];
-                if (uid != cur) {
-                    if (cur >= 0) flush(cur);
-                    cur = uid;
-                    if constexpr (FUSE) cur_row = wrow[slot * RS + i];
-                    ncur = 0;
+            for (int c = 0; c < CH; ++c) {
+                const int i = i0 + c;
+                if (i < nrows) {
+                    const int32_t uid = wu[slot * RS + i];
+                    if (uid != cur) {
+                        if (cur >= 0) flush(cur);
+                        cur = uid;
+                        if constexpr (FUSE) cur_row = wrow[slot * RS + i];
+                        ncur = 0;
+                    }
+                    ++ncur;
+                    if (a.pool_mean) {
+                        const float len = (float)wl[slot * RS + i];
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) v[c][e] = __fdiv_rn(v[c][e], len);
+                    }
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) acc[e] = __dadd_rn(acc[e], (double)v[c][e]);
                 }
-                ++ncur;
-                if (a.pool_mean) {
-                    const float len = (float)wl[slot * RS + i];
-#pragma unroll
-                    for (int e = 0; e < EPL; ++e) v[i][e] = __fdiv_rn(v[i][e], len);
-                }
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) acc[e] = __dadd_rn(acc[e], (double)v[i][e]);
             }
         }
         __syncwarp();  // the slot's uid / len are rewritten by the next issue
