@@ -164,6 +164,7 @@ struct picasso_ctx {
     int64_t *pack_gbase = nullptr;
     int32_t *pack_dim_d = nullptr;
     bool bulk_segsum = true;  // PICASSO_SEGSUM=legacy selects the register-staged segsum + hot-row path
+    bool flat_small = true;   // D <= 8 segsum: k_segsum_flat (PICASSO_SEGSUM_SMALL=legacy: k_segsum)
     int seg_cfg = 0;          // PICASSO_SEGSUM_CFG (warps x stages of the pipelined segsum)
     int32_t seg_nt = 0;       // its tiles per pack
     int32_t *tile_start = nullptr;

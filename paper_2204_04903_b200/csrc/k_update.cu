@@ -502,6 +502,50 @@ __global__ void __launch_bounds__(256) k_segsum(UpdateArgs a) {
     }
 }
 
+// Narrow rows (D <= 32: one float4 chunk per thread, D/4 threads per row): a thread group per
+// unique row, rows dealt round robin over the whole grid, each thread walking the row's
+// occurrences with two dY chunks in flight.  At these widths a pack's dY block (B x F_p x D)
+// mostly stays in L2, so the warp-cooperative kernel above is bound by its per-occurrence
+// instruction count, not by bytes; this one spends ~10 instructions per occurrence and chunk.
+// It wins at D <= 8 only: wider rows (more threads per row walking the same dependent
+// seg -> dY chain) lose to the warp kernel's broadcast addresses.
+// Rows with > kLongRow occurrences go to the chunked path as above.
+template <int D>
+__global__ void __launch_bounds__(256) k_segsum_flat(UpdateArgs a) {
+    constexpr int LANES = Geo<D>::LANES;
+    static_assert(Geo<D>::VPL == 1, "one float4 chunk per thread");
+    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
+    float *gp = a.gbuf + a.pack_gbase[a.pack];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int li = (int)(t % LANES);
+    const int64_t ng = (int64_t)gridDim.x * blockDim.x / LANES;
+#pragma unroll 1
+    for (int64_t u = u0 + t / LANES; u < u1; u += ng) {
+        const int32_t i0 = __ldg(a.ustart + u), i1 = __ldg(a.ustart + u + 1);
+        if (i1 - i0 > kLongRow) {
+            if (li == 0) a.long_list[atomicAdd(a.long_cnt, 1)] = (int32_t)u;
+            continue;
+        }
+        dbl4 g = zero4d();
+        int32_t i = i0;
+#pragma unroll 1
+        for (; i + 2 <= i1; i += 2) {
+            const int32_t s0 = __ldg(a.sorted_seg + i), s1 = __ldg(a.sorted_seg + i + 1);
+            float4 c0, c1;
+            load_contrib<D>(a, s0, li, &c0);
+            load_contrib<D>(a, s1, li, &c1);
+            g = add4d(add4d(g, c0), c1);
+        }
+        if (i < i1) {
+            float4 c0;
+            load_contrib<D>(a, __ldg(a.sorted_seg + i), li, &c0);
+            g = add4d(g, c0);
+        }
+        float *o = g_row_ptr<D>(a, u, u0, gp, li, (float)(i1 - i0)) + li * 4;
+        *reinterpret_cast<float4 *>(o) = round4(g);
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_update_rows(UpdateArgs a) {
     constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
@@ -710,7 +754,17 @@ void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t 
 #undef CALL
 }
 
-void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
+void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s, bool flat_small) {
+    if (flat_small && D <= 8) {  // measured at C3: D = 8 0.96 -> 0.75 ms; D = 16 / 32 slower (0.99 -> 1.10, 1.18 -> 1.87)
+        const unsigned blocks = (unsigned)num_sms * 8;
+        switch (D) {
+            case 4: k_segsum_flat<4><<<blocks, 256, 0, s>>>(a); return;
+            case 8: k_segsum_flat<8><<<blocks, 256, 0, s>>>(a); return;
+            case 16: k_segsum_flat<16><<<blocks, 256, 0, s>>>(a); return;
+            case 32: k_segsum_flat<32><<<blocks, 256, 0, s>>>(a); return;
+            default: break;
+        }
+    }
     const unsigned blocks = (unsigned)num_sms * 4;
 #define CALL(DD) k_segsum<DD><<<blocks, 256, 0, s>>>(a)
     PICASSO_DISPATCH_D(D, CALL)

@@ -153,7 +153,7 @@ struct UpdateArgs {
     const int64_t *dst_off;      //   [U] float offset of its G row in the owner's receive buffer
     float *dst_buf[8];           //   the ranks' receive buffers (NVLink peer pointers)
 };
-void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
+void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s, bool flat_small = true);
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, int32_t n_cnt,
                        cudaStream_t s);

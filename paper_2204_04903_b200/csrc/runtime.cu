@@ -136,6 +136,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
         c->fuse_pipe = std::strcmp(e, "fusepipe") == 0;
     }
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
+    if (const char *e = std::getenv("PICASSO_SEGSUM_SMALL")) c->flat_small = std::strcmp(e, "legacy") != 0;
     c->seg_cfg = segsum_pipe_cfg();
     if (const char *e = std::getenv("PICASSO_POOL")) {
         c->pipe_pool = std::strcmp(e, "legacy") != 0;
@@ -575,7 +576,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
 int picasso::launch_segsum_any(picasso_ctx *ctx, int D, const UpdateArgs &u, cudaStream_t s) {
     if (ctx->bulk_segsum && segsum_bulk_supported(D, u))
         return launch_segsum_bulk(ctx->seg_cfg, D, u, ctx->num_sms, s);
-    launch_segsum(D, u, ctx->num_sms, s);
+    launch_segsum(D, u, ctx->num_sms, s, ctx->flat_small);
     return 1 + launch_long_update(D, u, ctx->num_sms, s);
 }
 

@@ -37,6 +37,14 @@ def test_pipe_dims_long_rows_dyadic(D):
     run_step(_cfg(D), steps=2, dyadic=True, check_intermediates=False)
 
 
+@pytest.mark.parametrize("D", [4, 8, 16, 32])
+def test_narrow_dims_long_rows(D):
+    """D <= 32 (k_segsum_flat + the chunked long-row path): dyadic bit-exact, then continuous
+    dY with mean pooling."""
+    run_step(_cfg(D), steps=2, dyadic=True, check_intermediates=False)
+    run_step(_cfg(D, batch=512, pool=dc.POOL_MEAN), steps=1, dyadic=False, check_intermediates=False)
+
+
 @pytest.mark.parametrize("D", [64, 128])
 def test_pipe_continuous(D):
     run_step(_cfg(D), steps=2, dyadic=False, check_intermediates=False)
@@ -139,7 +147,7 @@ def test_pool_pipe_mean_and_all_empty_pack():
 # ---- alternative paths behind environment switches (read when the context is created) ---------
 @pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "1"}, {"PICASSO_BWD": "fusepipe"}, {"PICASSO_POOL": "flat"},
                                  {"PICASSO_OVERLAP": "0"}, {"PICASSO_SEGSUM_CFG": "12x4"},
-                                 {"PICASSO_DEDUP_REGIONS": "1"}])
+                                 {"PICASSO_DEDUP_REGIONS": "1"}, {"PICASSO_SEGSUM_SMALL": "legacy"}])
 def test_alternative_paths_match_oracle(env, monkeypatch):
     """Every switchable variant computes the same step: forward bit-exact, update within the
     north-star tolerance of the oracle (bit-exact under dyadic dY)."""
@@ -147,3 +155,4 @@ def test_alternative_paths_match_oracle(env, monkeypatch):
         monkeypatch.setenv(k, v)
     run_step(_cfg(128, batch=1024), steps=2, dyadic=True, check_intermediates=False)
     run_step(_cfg(64, batch=512, pool=dc.POOL_MEAN), steps=1, dyadic=False, check_intermediates=False)
+    run_step(_cfg(16, batch=1024), steps=2, dyadic=True, check_intermediates=False)
