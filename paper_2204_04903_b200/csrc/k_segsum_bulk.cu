@@ -208,9 +208,18 @@ __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const
     const int64_t C = (G1 - G0) + (U1 - U0);
     const int64_t nte = nt < C ? nt : C;
     const int64_t cost = (i - G0) + (u - U0);
-    const int64_t k = cost * nte / C;
+    // floor(c * nte / C) without a 64-bit division: a double estimate, corrected exactly
+    const double r = (double)nte / (double)C;
+    auto tile_of = [&](int64_t c) {
+        int64_t k = (int64_t)((double)c * r);
+        const int64_t x = c * nte;
+        while (k > 0 && k * C > x) --k;
+        while ((k + 1) * C <= x) ++k;
+        return k;
+    };
+    const int64_t k = tile_of(cost);
     int64_t kprev = -1;
-    if (i > G0) kprev = (cost - (row_start ? 2 : 1)) * nte / C;
+    if (i > G0) kprev = tile_of(cost - (row_start ? 2 : 1));
     int32_t *ts = tile_start + (int64_t)lo * (nt + 1);
     for (int64_t kk = kprev + 1; kk <= k; ++kk) ts[kk] = (int32_t)i;
     if (i == G1 - 1)

@@ -20,6 +20,14 @@
 
 namespace picasso {
 
+// owner = key mod W, local row = key div W (reading O3); shifts when W is a power of two
+__device__ __forceinline__ uint64_t key_owner(uint64_t key, int W) {
+    return (W & (W - 1)) == 0 ? (key & (uint64_t)(W - 1)) : key % (uint64_t)W;
+}
+__device__ __forceinline__ uint64_t key_local(uint64_t key, int W) {
+    return (W & (W - 1)) == 0 ? (key >> (__ffs(W) - 1)) : key / (uint64_t)W;
+}
+
 // ------------------------------------------------------------------------------------------
 // bucket of uid u = owner * P + pack; keys/values for one stable radix pass + its histogram
 __global__ void __launch_bounds__(kTileThreads) k_bucket(MultiArgs m) {
@@ -36,7 +44,7 @@ __global__ void __launch_bounds__(kTileThreads) k_bucket(MultiArgs m) {
         if (valid) {
             const int64_t p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
             const uint64_t key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
-            b = (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
+            b = (int32_t)key_owner(key, m.W) * m.P + (int32_t)p;
             if (m.hot_k > 0 && m.hslot[u] >= 0) b = m.W * m.P;  // hot: served by the replica, not sent
             m.bkey[u] = b;
             m.bval[u] = (int32_t)u;
@@ -80,8 +88,8 @@ __global__ void k_send_prep(MultiArgs m) {
                                      m.gbuf_base);
             continue;
         }
-        const int32_t b = (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
-        m.send_keys[i] = (int32_t)(key / (uint64_t)m.W);
+        const int32_t b = (int32_t)key_owner(key, m.W) * m.P + (int32_t)p;
+        m.send_keys[i] = (int32_t)key_local(key, m.W);
         m.row_off[u] = m.sroff[b] + (i - m.bstart[b]) * m.pack_dim[p];
     }
 }
@@ -95,7 +103,7 @@ __device__ __forceinline__ int32_t bucket_of(const MultiArgs &m, int64_t u, int6
     p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
     key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
     if (m.hot_k > 0 && m.hslot[u] >= 0) return m.W * m.P;  // hot: served by the replica
-    return (int32_t)(key % (uint64_t)m.W) * m.P + (int32_t)p;
+    return (int32_t)key_owner(key, m.W) * m.P + (int32_t)p;
 }
 
 // one atomic per (warp, bucket); returns this lane's rank among the lanes of its bucket
@@ -176,7 +184,7 @@ __global__ void k_part_place(MultiArgs m) {
         }
         const int64_t i = s_start[b] + j;
         m.send_pos[u] = (int32_t)i;
-        m.send_keys[i] = (int32_t)(key / (uint64_t)m.W);
+        m.send_keys[i] = (int32_t)key_local(key, m.W);
         m.row_off[u] = s_foff[b] + (int64_t)j * m.pack_dim[p];
     }
 }
