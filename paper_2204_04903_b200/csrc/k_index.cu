@@ -194,10 +194,15 @@ void launch_dedup_insert(const IndexArgs &a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------------
-constexpr int kItems = kTile / kTileThreads;  // 8 consecutive positions per thread
+// 1024 threads x 2 positions per 2048-position tile: at C2 there are only ~208 tiles, and the
+// passes are latency-bound table lookups, so parallelism comes from threads, not from items
+constexpr int kIdxThreads = 1024;
+constexpr int kItems = kTile / kIdxThreads;  // consecutive positions per thread
+constexpr int kTpb = 8 / kItems;             // threads whose flags share one fmask byte
+static_assert(8 % kItems == 0 && 32 % kTpb == 0, "fmask packing");
 
-__global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
-    using BlockReduce = cub::BlockReduce<int32_t, kTileThreads>;
+__global__ void __launch_bounds__(kIdxThreads) k_flag_count(IndexArgs a) {
+    using BlockReduce = cub::BlockReduce<int32_t, kIdxThreads>;
     __shared__ typename BlockReduce::TempStorage tmp;
     const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
 #pragma unroll
     for (int i = 0; i < kItems; ++i) slot[i] = g0 + i < N ? __ldg(a.slot_of + g0 + i) : 0;
     int32_t c = 0;
-    uint32_t m = 0;  // first-occurrence flags of this thread's 8 positions (k_assign reads them)
+    uint32_t m = 0;  // first-occurrence flags of this thread's positions (k_assign reads them)
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;
@@ -214,20 +219,23 @@ __global__ void __launch_bounds__(kTileThreads) k_flag_count(IndexArgs a) {
             m |= 1u << i;
         }
     }
-    if (g0 < N) a.fmask[g0 / kItems] = (uint8_t)m;
+    uint32_t m8 = m;  // 8 positions per byte: kTpb consecutive threads
+#pragma unroll
+    for (int t = 1; t < kTpb; ++t) m8 |= __shfl_down_sync(0xffffffffu, m, t) << (t * kItems);
+    if (threadIdx.x % kTpb == 0 && g0 < N) a.fmask[g0 / 8] = (uint8_t)m8;
     const int32_t tot = BlockReduce(tmp).Sum(c);
     if (threadIdx.x == 0) a.blk_cnt[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
-    using BlockScan = cub::BlockScan<int32_t, kTileThreads>;
+__global__ void __launch_bounds__(kIdxThreads) k_assign(IndexArgs a) {
+    using BlockScan = cub::BlockScan<int32_t, kIdxThreads>;
     __shared__ typename BlockScan::TempStorage tmp;
     const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
     int32_t slot[kItems];
     bool first[kItems];
     unsigned long long key[kItems];
-    const uint32_t m = g0 < N ? a.fmask[g0 / kItems] : 0u;  // from k_flag_count
+    const uint32_t m = g0 < N ? (a.fmask[g0 / 8] >> (g0 % 8)) & ((1u << kItems) - 1u) : 0u;  // k_flag_count's
     const int32_t c = __popc(m);
     // table reads (first occurrences only) before any table write: stores to table[] would
     // otherwise order every later load behind them (possible aliasing)
@@ -256,10 +264,10 @@ __global__ void __launch_bounds__(kTileThreads) k_assign(IndexArgs a) {
 
 // inverse[g] = uid; also the digit histogram of the backward's first radix pass over this
 // 2048-position tile (digit-major, so the sort starts with its scan: one pass over N saved)
-__global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
+__global__ void __launch_bounds__(kIdxThreads) k_inverse(IndexArgs a) {
     __shared__ int32_t h[kMaxRadix];
     const int radix = 1 << a.sort_bits0;
-    for (int d = threadIdx.x; d < radix; d += kTileThreads) h[d] = 0;
+    for (int d = threadIdx.x; d < radix; d += kIdxThreads) h[d] = 0;
     __syncthreads();
     const int64_t N = a.n_dev ? *a.n_dev : a.N;
     const int64_t g0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kTileThreads) k_inverse(IndexArgs a) {
     __syncthreads();
     const int64_t nblk = (N + kTile - 1) / kTile;
     if (N > 0 && blockIdx.x < nblk)
-        for (int d = threadIdx.x; d < radix; d += kTileThreads) a.sort_hist0[(int64_t)d * nblk + blockIdx.x] = h[d];
+        for (int d = threadIdx.x; d < radix; d += kIdxThreads) a.sort_hist0[(int64_t)d * nblk + blockIdx.x] = h[d];
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // uid ranges of empty packs (and the end)
         int32_t next = *a.d_total;
         a.pack_ustart[a.P] = next;
@@ -325,13 +333,13 @@ __global__ void k_scan_blocks(const int32_t *cnt, int32_t *off, int32_t n, int32
 void launch_dedup_assign(const IndexArgs &a, cudaStream_t s) {
     const int64_t nb = (a.N + kTile - 1) / kTile;
     if (nb) {
-        k_flag_count<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
+        k_flag_count<<<(unsigned)nb, kIdxThreads, 0, s>>>(a);
         k_scan_blocks<<<1, 1024, 0, s>>>(a.blk_cnt, a.blk_off, (int32_t)nb, a.d_total, a.n_dev);
-        k_assign<<<(unsigned)nb, kTileThreads, 0, s>>>(a);
+        k_assign<<<(unsigned)nb, kIdxThreads, 0, s>>>(a);
     } else {
         cudaMemsetAsync(a.d_total, 0, sizeof(int32_t), s);
     }
-    k_inverse<<<(unsigned)std::max<int64_t>(1, nb), kTileThreads, 0, s>>>(a);
+    k_inverse<<<(unsigned)std::max<int64_t>(1, nb), kIdxThreads, 0, s>>>(a);
 }
 
 }  // namespace picasso
