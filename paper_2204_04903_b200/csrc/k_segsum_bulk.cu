@@ -208,11 +208,12 @@ __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const
     const int64_t C = (G1 - G0) + (U1 - U0);
     const int64_t nte = nt < C ? nt : C;
     const int64_t cost = (i - G0) + (u - U0);
-    // floor(c * nte / C) without a 64-bit division: a double estimate, corrected exactly
-    const double r = (double)nte / (double)C;
-    auto tile_of = [&](int64_t c) {
-        int64_t k = (int64_t)((double)c * r);
+    // floor(c * nte / C) without a 64-bit division: 32-bit when it fits, else a double
+    // estimate corrected exactly
+    auto tile_of = [&](int64_t c) -> int64_t {
         const int64_t x = c * nte;
+        if (x <= 0xffffffffll && C <= 0xffffffffll) return (int64_t)((uint32_t)x / (uint32_t)C);
+        int64_t k = (int64_t)((double)x / (double)C);
         while (k > 0 && k * C > x) --k;
         while ((k + 1) * C <= x) ++k;
         return k;

@@ -7,7 +7,10 @@
 
 namespace picasso {
 
-constexpr int kTile = 2048;     // keys per block in the index / scan / sort kernels
+#ifndef PICASSO_KTILE
+#define PICASSO_KTILE 2048
+#endif
+constexpr int kTile = PICASSO_KTILE;  // keys per block in the index / scan / sort kernels
 constexpr int kTileThreads = 256;
 constexpr int kLongRow = 256;   // rows with more occurrences take the chunked backward path
 
