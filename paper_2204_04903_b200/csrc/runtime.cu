@@ -147,7 +147,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_KINTERLEAVE")) c->kinterleave = std::atoi(e);
     // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
     // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
-    // Off by default: the step is ~7 % faster (C2: 0.327 -> 0.304 ms) but the pool, sharing the
+    // Off by default: the step is ~8 % faster (C2: 0.294 -> 0.270 ms) but the pool, sharing the
     // GPU, then runs at ~3.1 TB/s instead of 4.2 (PICASSO_EARLY_POOL=1 turns it on).
     if (const char *e = std::getenv("PICASSO_EARLY_POOL")) c->early_pool = std::strcmp(e, "0") != 0;
     c->pool_reserve = (world == 1 && c->early_pool) ? 48 : 0;
