@@ -50,26 +50,6 @@ __global__ void __launch_bounds__(256) k_pool_flat(PoolArgs a) {
 // One thread per segment: reads its two offsets (coalesced), writes a zero row only if the segment is
 // empty — a cheap pass when there are none (one-hot packs), and no per-segment walk when most are
 // (sparse positional fields).
-__global__ void __launch_bounds__(256) k_pool_zero_empty(PoolArgs a, int D) {
-    if (a.empty_pack && !a.empty_pack[a.pack]) return;  // no empty segment in this pack
-    const int64_t S = (int64_t)a.Fp * a.B;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t k = (int32_t)(s / a.B);
-        const int32_t b = (int32_t)(s - (int64_t)k * a.B);
-        const int32_t f = __ldg(a.pack_fields + k);
-        const int64_t sg = (int64_t)f * a.B + b;
-        if (__ldg(a.offsets + sg + 1) > __ldg(a.offsets + sg)) continue;
-        float4 *o = reinterpret_cast<float4 *>(a.out + (int64_t)b * a.out_stride + a.finfo[f].col);
-        for (int c = 0; c < D / 4; ++c) __stcs(o + c, make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-}
-
-int launch_pool_zero_empty(int D, const PoolArgs &a, int num_sms, cudaStream_t s) {
-    if ((int64_t)a.Fp * a.B == 0) return 0;
-    k_pool_zero_empty<<<(unsigned)num_sms * 8, 256, 0, s>>>(a, D);
-    return 1;
-}
-
 int launch_pool_flat(int D, const PoolArgs &a, int num_sms, cudaStream_t s) {
     if ((int64_t)a.Fp * a.B == 0) return 0;
     const unsigned blocks = (unsigned)num_sms * 8;

@@ -13,9 +13,10 @@
 //                   issues the LDGSTS copies of its slice of each row into a per-warp
 //                   shared-memory ring.  Landed rows are added in order in fp32; a finished
 //                   segment is written into its column block of the [B, out_width] output
-//                   with streaming stores.  Empty segments (no position to visit) are written by
-//                   k_pool_zero_empty in a pass over the segments' offsets: a warp here would walk
-//                   them one by one (C4's sparse positional fields: 13 ms).
+//                   with streaming stores.  Empty segments (no position to visit) are zeroed
+//                   after the tiles, by a grid-stride pass over the segments' offsets in packs
+//                   k_seg_of flagged: a warp here would walk them one by one inside its ring
+//                   (C4's sparse positional fields: 13 ms).
 #include "kernels.h"
 
 namespace picasso {
@@ -78,7 +79,7 @@ __device__ __forceinline__ void lane_store_cs(float *row, int lane, const float 
     }
 }
 
-// (also flags the packs that have an empty segment: k_pool_zero_empty runs only for those)
+// (also flags the packs that have an empty segment: k_pool_pipe zeroes them only there)
 __global__ void k_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart,
                          const int32_t *id_start, int32_t *seg_of, const FieldInfo *finfo, int32_t *empty_pack) {
     const int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
     const int32_t pa = seg_start_from(P0 + (int32_t)(na < n ? na : n));
     const int32_t pb = seg_start_from(P0 + (int32_t)(nb < n ? nb : n));
     const int32_t seg_before = pa > P0 && pa < P1 ? pseg(pa - 1) : -1;  // segment of position pa - 1
-    if (pa >= pb) return;  // empty segments get their zeros from k_pool_zero_empty
+    auto tiles = [&]() {  // this warp's tile (empty segments: the zero pass below)
     int64_t *s_out = reinterpret_cast<int64_t *>(smem) + (size_t)w * kS * RS;
     int32_t *s_seg = reinterpret_cast<int32_t *>(smem + (size_t)kNW * kS * RS * 8) + (size_t)w * kS * RS;
     unsigned char *wr = smem + G::RING_OFF + (size_t)w * kS * SB;
@@ -250,6 +251,24 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
         ldgsts_commit();
     }
     flush();
+    };
+    if (pa < pb) tiles();
+
+    // empty segments (no position, so no tile writes them): zeros, only in packs k_seg_of
+    // flagged (a sparse scan inside the ring would stall every warp on them)
+    if (!a.empty_pack || a.empty_pack[a.pack]) {
+        const int64_t S = (int64_t)a.Fp * a.B;
+        for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
+            const int32_t k = (int32_t)(s / a.B);
+            const int32_t b = (int32_t)(s - (int64_t)k * a.B);
+            const int32_t f = __ldg(a.pack_fields + k);
+            const int64_t sg = (int64_t)f * a.B + b;
+            if (__ldg(a.offsets + sg + 1) > __ldg(a.offsets + sg)) continue;
+            float4 *o = reinterpret_cast<float4 *>(a.out + (int64_t)b * a.out_stride + a.finfo[f].col);
+#pragma unroll
+            for (int c = 0; c < D / 4; ++c) __stcs(o + c, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+    }
 }
 
 template <int D>

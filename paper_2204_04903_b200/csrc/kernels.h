@@ -115,7 +115,6 @@ void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *
                    int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo = nullptr, int32_t *empty_pack = nullptr);
 // k_pool_flat.cu: one thread per 16-B output chunk (every D); returns #launches
 int launch_pool_flat(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
-int launch_pool_zero_empty(int D, const PoolArgs &a, int num_sms, cudaStream_t s);  // after k_pool_pipe
 
 // k_update.cu
 struct UpdateArgs {

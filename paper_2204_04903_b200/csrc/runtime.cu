@@ -561,8 +561,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
         if (ctx->pool_kind == 2) {
             n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else if (pool_pipe_supported(ctx->pack_dim[p], pa)) {  // D >= 64: the cp.async ring
-            n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->pool_sms, s);
-            n += launch_pool_zero_empty(ctx->pack_dim[p], pa, ctx->num_sms, s);
+            n += launch_pool_pipe(ctx->pack_dim[p], pa, ctx->pool_sms, s);  // (+ its empty segments)
         } else if (ctx->pipe_pool) {  // narrow rows: one thread per 16-B chunk (C4: 20 -> 6 ms)
             n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else {  // PICASSO_POOL=legacy
