@@ -52,6 +52,7 @@ struct picasso_group;
 
 // Per-rank state of the row-sharded step (world > 1), host side.
 struct MultiState {
+    bool reset_forked = false;  // p2p: this forward's dtab reset runs on side2 (joined in p2p_c)
     ncclComm_t comm = nullptr;       // NCCL mode
     picasso_group *group = nullptr;  // loopback mode (all ranks in one process)
     int64_t max_recv = 0;

@@ -169,7 +169,12 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
     const int P = ctx->P;
     const P2PArgs a = make_p2p_args(ctx);
     ctx->mark(4, true, s);
-    launch_p2p_reset(a, ctx->num_sms, s);  // the previous forward's direct-table entries
+    if (ctx->mp.reset_forked) {  // the reset ran beside unique + partition (multi_fwd_p2p)
+        PCK(cudaStreamWaitEvent(s, ctx->ev_join2, 0));
+        ctx->mp.reset_forked = false;
+    } else {
+        launch_p2p_reset(a, ctx->num_sms, s);  // the previous forward's direct-table entries
+    }
     launch_p2p_tables(a, s);
     launch_p2p_dst_insert(a, ctx->num_sms, s);
     launch_p2p_leaders(a, ctx->num_sms, s);
@@ -223,7 +228,24 @@ picasso_status p2p_f(picasso_ctx *ctx, float lr, int64_t step, cudaStream_t s) {
 picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
                              float *out, cudaStream_t s) {
     picasso_status st;
-    if ((st = mfwd_a(ctx, ids, offsets, B, N, s))) return st;
+    // the previous step's direct-table entries are cleared on the second stream while the
+    // index work runs (it touches none of dtab / lrow / osrc / R); p2p_c joins it before the
+    // tables kernel rewrites R
+    ctx->mp.reset_forked = false;
+    if (ctx->side2) {
+        PCK(cudaEventRecord(ctx->ev_fork2, s));
+        PCK(cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0));
+        launch_p2p_reset(make_p2p_args(ctx), ctx->num_sms, ctx->side2);
+        PCK(cudaEventRecord(ctx->ev_join2, ctx->side2));
+        ctx->mp.reset_forked = true;
+    }
+    if ((st = mfwd_a(ctx, ids, offsets, B, N, s))) {
+        if (ctx->mp.reset_forked) {  // keep the stream joined on the error path
+            cudaStreamWaitEvent(s, ctx->ev_join2, 0);
+            ctx->mp.reset_forked = false;
+        }
+        return st;
+    }
     barrier(ctx, 0, s);
     const bool kil = interleaved(ctx);
     if ((st = p2p_c(ctx, s, kil))) return st;
