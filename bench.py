@@ -313,6 +313,10 @@ def main():
         torch.cuda.synchronize()
         if clk is not None:
             clk.__enter__()
+        if world > 1:
+            # align the ranks' streams on the device: the host barrier above returns at different
+            # times per rank, and a rank that starts early would absorb the skew in its first step
+            dist.all_reduce(align)
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             starts[i].record(stream)
@@ -337,6 +341,7 @@ def main():
             pb.picasso_profile_enable(emb.ctx, False)
         return float(sum(a.elapsed_time(b) for a, b in zip(starts, ends))) / args.steps, phase, calls
 
+    align = torch.zeros(1, device=dev)
     clk = ClockSampler(local)
     ms, _, _ = run_pass(False, clk)
     ms_prof, phase_ms, ncalls = run_pass(True)
