@@ -175,6 +175,7 @@ struct picasso_ctx {
                              // update at each row's flush.  Measured slower (C2: 219 us vs 73 + 71 us
                              // split) — one deferred row per warp does not hide the state loads.
     bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
+    int overlap_env = -1;   // PICASSO_OVERLAP (0 / 1) if set; else chosen per world == 1 forward
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share
     bool early_pool = false;  // W = 1: pool concurrently with the dedup + transpose chain
     cudaStream_t side = nullptr;

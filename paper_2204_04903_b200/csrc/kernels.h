@@ -12,6 +12,7 @@ namespace picasso {
 #endif
 constexpr int kTile = PICASSO_KTILE;  // keys per block in the index / scan / sort kernels
 constexpr int kTileThreads = 256;
+constexpr int64_t kOverlapMinIds = (int64_t)1 << 22;  // world == 1: transpose beside the pool from here on
 constexpr int kLongRow = 256;   // rows with more occurrences take the chunked backward path
 
 struct IndexArgs {

@@ -143,7 +143,8 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
         if (!std::strcmp(e, "flat")) c->pool_kind = 2;
         if (!std::strcmp(e, "pipe")) c->pool_kind = 1;
     }
-    if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap = std::strcmp(e, "0") != 0;
+    if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap_env = std::strcmp(e, "0") != 0;
+    if (c->overlap_env >= 0) c->overlap = c->overlap_env;
     if (const char *e = std::getenv("PICASSO_KINTERLEAVE")) c->kinterleave = std::atoi(e);
     // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
     // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
@@ -380,6 +381,11 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     ctx->B = batch;
     ctx->N = n_ids;
     ctx->offsets = offsets;
+    // world == 1: the transpose beside the pool pays only for large batches.  Below kOverlapMinIds
+    // the persistent pool (one CTA per SM, static tiles) waits for SMs the transpose's blocks
+    // hold, and the serial order is faster (C2: 0.283 vs 0.294 ms; C3, 83.5 M IDs: 26.2 vs
+    // 26.6 ms the other way round).  PICASSO_OVERLAP=0/1 forces either; the early pool needs it.
+    if (ctx->overlap_env < 0) ctx->overlap = ctx->early_pool || n_ids >= kOverlapMinIds;
     if (ctx->overlap && ctx->side && ctx->early_pool) {
         // At world == 1 the pool needs only the raw IDs (row = h(id)), not the dedup: the index
         // work (Unique, inverse) and the backward's transpose run on the internal stream while
