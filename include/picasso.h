@@ -254,6 +254,13 @@ picasso_status picasso_group_bwd_update(picasso_group *group, const float *const
  * host). */
 picasso_status picasso_get_owner_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n);
 picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts);
+/* Partition of the last forward (world > 1; tests, synchronises): the local rows (key div W,
+ * reading O3) this rank requested from `owner` for pack `pack`, in send order — the pack's
+ * unique keys with key mod W == owner in first-occurrence order (PAPER.md L211 Partition,
+ * SPEC.md L113-118; = oracle_partition's list).  Hot keys (HybridHash) are not sent.  dst: host
+ * int64 [cap]; n: the list length. */
+picasso_status picasso_get_send_list(picasso_ctx *ctx, int32_t owner, int32_t pack, int64_t *dst, int64_t cap,
+                                     int64_t *n);
 
 /* 7. Exchange over NVLink peer memory (kernel-initiated Shuffle&Stitch).
  * Replaces the NCCL AllToAllv of section 5 with one shared window per rank (barrier flags,

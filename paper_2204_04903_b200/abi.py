@@ -23,7 +23,7 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_group_create", "picasso_group_destroy", "picasso_group_fwd", "picasso_group_bwd_update",
            "picasso_get_owner_unique", "picasso_get_send_counts", "picasso_hot_cache_refresh",
            "picasso_group_hot_cache_refresh", "picasso_get_hot_keys", "picasso_p2p_handle", "picasso_p2p_open",
-           "picasso_group_p2p"]
+           "picasso_group_p2p", "picasso_get_send_list"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -76,6 +76,7 @@ def lib():
             "picasso_group_bwd_update": [vp, vp, C.c_float, i64, vp],
             "picasso_get_owner_unique": [vp, i32, vp, i64, C.POINTER(i64)],
             "picasso_get_send_counts": [vp, vp],
+            "picasso_get_send_list": [vp, i32, i32, vp, i64, C.POINTER(i64)],
             "picasso_hot_cache_refresh": [vp, C.c_size_t, vp, vp],
             "picasso_group_hot_cache_refresh": [vp, C.c_size_t, vp, vp],
             "picasso_get_hot_keys": [vp, vp, vp, i64, C.POINTER(i64)],
@@ -320,6 +321,16 @@ def picasso_get_send_counts(ctx, world):
     arr = (C.c_int64 * world)()
     _chk(lib().picasso_get_send_counts(ctx, arr), "picasso_get_send_counts", ctx)
     return list(arr)
+
+
+def picasso_get_send_list(ctx, owner, pack):
+    """Local rows this rank requested from `owner` for `pack`, send order (numpy int64)."""
+    n = C.c_int64()
+    _chk(lib().picasso_get_send_list(ctx, int(owner), int(pack), None, 0, C.byref(n)), "picasso_get_send_list", ctx)
+    out = np.zeros(max(n.value, 1), np.int64)
+    _chk(lib().picasso_get_send_list(ctx, int(owner), int(pack), out.ctypes.data, n.value, C.byref(n)),
+         "picasso_get_send_list", ctx)
+    return out[:n.value]
 
 
 def picasso_unique_offsets(ctx, dst, stream=None):

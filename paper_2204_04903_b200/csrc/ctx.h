@@ -291,7 +291,7 @@ struct picasso_ctx {
             const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
             const int WP = world * P;
             int bb = 1;
-            while ((1 << bb) < WP) ++bb;
+            while ((1 << bb) < WP + 1) ++bb;  // + the hot bucket (multi_args' bucket_bits)
             mp.bkey = c.take<int32_t>(N);
             mp.bval = c.take<int32_t>(N);
             mp.bsorted = c.take<int32_t>(N);

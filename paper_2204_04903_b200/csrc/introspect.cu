@@ -33,3 +33,25 @@ extern "C" picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *hos
     for (int r = 0; r < ctx->world; ++r) host_counts[r] = ctx->mp.sk[r];
     return PICASSO_OK;
 }
+
+// Requested local rows of bucket (owner, pack) in send-slot order (both exchanges use the
+// stable layout: owner-major, pack, uid order inside a bucket).
+extern "C" picasso_status picasso_get_send_list(picasso_ctx *ctx, int32_t owner, int32_t pack, int64_t *dst,
+                                                int64_t cap, int64_t *n) {
+    if (!ctx || !n || ctx->world < 2 || !ctx->bound || owner < 0 || owner >= ctx->world || pack < 0 || pack >= ctx->P)
+        return PICASSO_ERR_INVALID_ARG;
+    if (cudaStreamSynchronize(ctx->last_stream) != cudaSuccess) return PICASSO_ERR_CUDA;
+    const int b = owner * ctx->P + pack;
+    int64_t se[2];
+    if (cudaMemcpy(se, ctx->mp.bstart + b, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return PICASSO_ERR_CUDA;
+    *n = se[1] - se[0];
+    if (dst && cap > 0 && *n > 0) {
+        std::vector<int32_t> v(*n);
+        if (cudaMemcpy(v.data(), ctx->mp.send_keys + se[0], sizeof(int32_t) * *n, cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+            return PICASSO_ERR_CUDA;
+        for (int64_t i = 0; i < std::min(*n, cap); ++i) dst[i] = v[i];
+    }
+    return PICASSO_OK;
+}

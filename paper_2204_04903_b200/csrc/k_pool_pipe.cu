@@ -273,11 +273,7 @@ __global__ void __launch_bounds__(kNW * 32, 1) k_pool_pipe(PoolArgs a) {
 
 template <int D>
 void launch_pipe(const PoolArgs &a, int num_sms, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pool_pipe<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, PG<D>::SMEM);
-        attr = true;
-    }
+    ensure_dyn_smem((const void *)k_pool_pipe<D>, PG<D>::SMEM);
     k_pool_pipe<D><<<(unsigned)num_sms, kNW * 32, PG<D>::SMEM, s>>>(a);
 }
 

@@ -488,11 +488,7 @@ __global__ void __launch_bounds__(128) k_segsum_fix(UpdateArgs a) {
 template <int D, int NW, int S, bool FUSE = false>
 void launch_pipe(const UpdateArgs &a, int num_sms, cudaStream_t s) {
     using G = BG<D, NW, S>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_segsum_pipe<D, NW, S, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        attr = true;
-    }
+    ensure_dyn_smem((const void *)k_segsum_pipe<D, NW, S, FUSE>, G::SMEM);
     k_segsum_pipe<D, NW, S, FUSE><<<(unsigned)num_sms, NW * 32, G::SMEM, s>>>(a);
     k_segsum_fix<D, FUSE><<<(unsigned)a.nt, 128, 0, s>>>(a);
 }

@@ -336,12 +336,7 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
         const bool v3 = sort_env ? std::string(sort_env) == "3" : n >= kBigSort;
         if (v3) {
             const size_t sm = scatter3_smem(plan.bits[p]);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_scatter3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)scatter3_smem(kMaxRadixBits));
-                attr = true;
-            }
+            ensure_dyn_smem((const void *)k_scatter3, scatter3_smem(kMaxRadixBits));
             k_scatter3<<<(unsigned)nblk, kTileThreads, sm, s>>>(ck, cv, bufk[p & 1], bufv[p & 1], n, plan.shift[p],
                                                                 plan.bits[p], hist[p & 1], rowtot, nblk,
                                                                 fused_hist ? hist[(p + 1) & 1] : nullptr,
@@ -365,6 +360,12 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
     }
     *k_out = const_cast<int32_t *>(ck);
     *v_out = const_cast<int32_t *>(cv);
+}
+
+// Per-tile bucket offsets (exclusive, in place) and bucket totals of a digit-major histogram
+// (the peer-memory partition's k_bucket output).
+void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s) {
+    if (nblk > 0) k_scan_rows<<<(radix + 7) / 8, 256, 0, s>>>(hist, nblk, rowtot, nullptr, radix, 0);
 }
 
 // One stable pass by a small key (the multi-GPU partition by (owner, pack)); bhist was filled

@@ -743,11 +743,7 @@ void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t 
     const size_t smem = segsum_smem_bytes(D);
 #define CALL(DD)                                                                                        \
     {                                                                                                   \
-        static bool attr = false;                                                                       \
-        if (!attr) {                                                                                    \
-            cudaFuncSetAttribute(k_segsum_update<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            attr = true;                                                                                \
-        }                                                                                               \
+        ensure_dyn_smem((const void *)k_segsum_update<DD>, smem);                                       \
         k_segsum_update<DD><<<blocks, 256, smem, s>>>(a);                                               \
     }
     PICASSO_DISPATCH_D(D, CALL)

@@ -1,11 +1,30 @@
 // kernels.h — host-side launchers of the sm_100a kernels (internal; not part of the C ABI).
 #pragma once
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
 
 namespace picasso {
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device (the attribute is
+// per device: a process driving several GPUs sets it once per (kernel, device)).
+inline cudaError_t ensure_dyn_smem(const void *fn, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    std::lock_guard<std::mutex> g(mu);
+    size_t &v = done[{fn, dev}];
+    if (v >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) v = bytes;
+    return e;
+}
 
 #ifndef PICASSO_KTILE
 #define PICASSO_KTILE 2048
@@ -71,6 +90,7 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
                        int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
                        int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches);
 size_t radix_hist2_ints(int64_t n);
+void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s);
 void bucket_sort_pass(const int32_t *k_in, const int32_t *v_in, int32_t *k_out, int32_t *v_out, int64_t n_max,
                       const int32_t *n_dev, int bits, int32_t *bhist, int32_t *rowtot, cudaStream_t s);
 

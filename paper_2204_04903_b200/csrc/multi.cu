@@ -95,53 +95,22 @@ __global__ void k_send_prep(MultiArgs m) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Partition for the peer-memory exchange.  There the owner reads a requester's bucket (r, p)
-// by slot index and sums contributions in source order, so the order of the slots inside a
-// bucket is free: counts with warp-aggregated atomics, then placement with per-bucket cursors
-// (two passes over the uniques, no sort).  Results do not depend on the slot order.
-__device__ __forceinline__ int32_t bucket_of(const MultiArgs &m, int64_t u, int64_t &p, uint64_t &key) {
-    p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
-    key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
-    if (m.hot_k > 0 && m.hslot[u] >= 0) return m.W * m.P;  // hot: served by the replica
-    return (int32_t)key_owner(key, m.W) * m.P + (int32_t)p;
-}
-
-// one atomic per (warp, bucket); returns this lane's rank among the lanes of its bucket
-__device__ __forceinline__ int32_t warp_agg_add(int32_t *ctr, int32_t b, bool active) {
-    const unsigned am = __ballot_sync(0xffffffffu, active);
-    int32_t r = 0;
-    if (active) {
-        const int lane = threadIdx.x & 31;
-        const unsigned peers = __match_any_sync(am, b);
-        const int first = __ffs(peers) - 1;
-        int32_t base = 0;
-        if (lane == first) base = atomicAdd(ctr + b, __popc(peers));
-        base = __shfl_sync(peers, base, first);
-        r = base + __popc(peers & ((1u << lane) - 1u));
-    }
-    return r;
-}
-
-__global__ void k_part_count(MultiArgs m) {
-    const int32_t U = *m.d_total;
-    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < U;
-         b0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = b0 + (threadIdx.x & 31);
-        int32_t b = 0;
-        if (u < U) {
-            int64_t p;
-            uint64_t key;
-            b = bucket_of(m, u, p, key);
-            m.bkey[u] = b;
-        }
-        warp_agg_add(m.bcount, b, u < U);
-    }
-}
-
-__global__ void k_part_place(MultiArgs m) {
-    __shared__ int64_t s_start[kMaxOwnerBlocks + 1], s_foff[kMaxOwnerBlocks + 1];
-    const int nb = m.W * m.P;
-    if (threadIdx.x == 0) {  // bucket starts (slots) and float offsets (rows buffer), every block
+// Partition for the peer-memory exchange: the same stable layout as the NCCL driver's sort
+// (owner-major, pack, then first-occurrence = uid order inside a bucket, so each bucket is
+// exactly oracle_partition's per-owner list of the pack), placed without the sort's second
+// buffer: k_bucket counts every 2048-uid tile per bucket, k_scan_rows turns the digit-major
+// counts into per-tile bucket offsets, and k_part_place ranks each uid stably inside its tile
+// (warp by warp, __match_any_sync) and writes its send slot, requested local row and row offset.
+__global__ void __launch_bounds__(kTileThreads) k_part_place(MultiArgs m) {
+    constexpr int kWarps = kTileThreads / 32;
+    constexpr int kRounds = kTile / kTileThreads;  // 8 rounds of 32 uids per warp
+    const int nb = m.W * m.P;  // bucket nb = hot (not sent)
+    extern __shared__ int64_t smp[];
+    int64_t *s_start = smp, *s_foff = smp + nb + 1;              // [nb+1] each
+    int32_t *wcf = reinterpret_cast<int32_t *>(smp + 2 * (nb + 1));  // [kWarps][nb+1]
+    auto wc = [&](int ww, int b) -> int32_t & { return wcf[ww * (nb + 1) + b]; };
+    for (int i = threadIdx.x; i < kWarps * (nb + 1); i += kTileThreads) wcf[i] = 0;
+    if (threadIdx.x == 0) {  // bucket starts (slots) and float offsets (rows buffer)
         int64_t e = 0, f = 0;
         for (int b = 0; b < nb; ++b) {
             s_start[b] = e;
@@ -155,33 +124,57 @@ __global__ void k_part_place(MultiArgs m) {
     }
     __syncthreads();
     if (blockIdx.x == 0)
-        for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        for (int b = threadIdx.x; b <= nb; b += kTileThreads) {
             m.bstart[b] = s_start[b];
             m.sroff[b] = s_foff[b];
         }
     const int32_t U = *m.d_total;
-    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < U;
-         b0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = b0 + (threadIdx.x & 31);
-        const bool valid = u < U;
-        int32_t b = nb;
-        int64_t p = 0;
-        uint64_t key = 0;
-        if (valid) {
-            b = m.bkey[u];
-            p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
-            key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)w * (32 * kRounds);
+    int32_t bk[kRounds], rk[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t u = base + r * 32 + lane;
+        bk[r] = u < U ? __ldg(m.bkey + u) : nb + 1 + lane;  // invalid lanes never match a bucket
+    }
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {  // stable rank inside the warp's 256 uids
+        const bool valid = base + r * 32 + lane < U;
+        const unsigned peers = __match_any_sync(0xffffffffu, bk[r]);
+        int32_t before = 0;
+        if (valid) before = wc(w, bk[r]);
+        rk[r] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wc(w, bk[r]) = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += kTileThreads) {  // warp prefixes + this tile's bucket offset
+        int32_t run = m.bhist[(int64_t)b * m.nblk + blockIdx.x];
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ++ww) {
+            const int32_t t = wc(ww, b);
+            wc(ww, b) = run;
+            run += t;
         }
-        const bool cold = valid && b < nb;
-        const int32_t j = warp_agg_add(m.cursor, b, cold);
-        if (!valid) continue;
-        if (!cold) {  // hot: row of the local replica (offset relative to the rows buffer)
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t u = base + r * 32 + lane;
+        if (u >= U) continue;
+        const int32_t b = bk[r];
+        const int64_t p = upper_bound_dev(m.pack_ustart, 0, m.P + 1, (int32_t)u) - 1;
+        if (b >= nb) {  // hot: row of the local replica (offset relative to the rows buffer)
             const int32_t hs = m.hslot[u];
             m.send_pos[u] = -1;
             m.row_off[u] = (int64_t)((m.hot_arena + m.hot_w_off[p] + (int64_t)(hs - m.hot_pslot[p]) * m.pack_dim[p]) -
                                      m.gbuf_base);
             continue;
         }
+        const uint64_t key = m.unique_gkey[u] - (unsigned long long)m.pack_key_off[p];
+        const int32_t j = wc(w, b) + rk[r];  // rank of u inside its bucket (uid order)
         const int64_t i = s_start[b] + j;
         m.send_pos[u] = (int32_t)i;
         m.send_keys[i] = (int32_t)key_local(key, m.W);
@@ -381,10 +374,13 @@ void launch_send_prep(const MultiArgs &m, int num_sms, cudaStream_t s) {
     k_send_prep<<<(unsigned)num_sms * 4, 256, 0, s>>>(m);
 }
 void launch_partition_p2p(const MultiArgs &m, int num_sms, cudaStream_t s) {
-    cudaMemsetAsync(m.bcount, 0, sizeof(int32_t) * (m.W * m.P + 1), s);
-    cudaMemsetAsync(m.cursor, 0, sizeof(int32_t) * (m.W * m.P + 1), s);
-    k_part_count<<<(unsigned)num_sms * 4, 256, 0, s>>>(m);
-    k_part_place<<<(unsigned)num_sms * 4, 256, 0, s>>>(m);
+    (void)num_sms;
+    k_bucket<<<(unsigned)m.nblk, kTileThreads, 0, s>>>(m);
+    bucket_scan(m.bhist, m.nblk, m.bcount, 1 << m.bucket_bits, s);
+    const int nb = m.W * m.P;
+    const size_t sm = sizeof(int64_t) * 2 * (nb + 1) + sizeof(int32_t) * (kTileThreads / 32) * (nb + 1);
+    ensure_dyn_smem((const void *)k_part_place, sm);
+    k_part_place<<<(unsigned)m.nblk, kTileThreads, sm, s>>>(m);
 }
 void launch_owner_insert(const MultiArgs &m, Slot *table, uint32_t cap_mask, int *err, cudaStream_t s) {
     if (m.R > 0) k_owner_insert<<<(unsigned)((m.R + 255) / 256), 256, 0, s>>>(m, table, cap_mask, err);

@@ -31,7 +31,6 @@ struct MultiArgs {
     int32_t *bkey, *bval;            // [U] bucket, uid (pass input)
     int32_t *bhist;                  // [2^bits, nblk] bucket histogram (digit-major)
     int32_t *bcount;                 // [W*P+1] bucket counts (radix row totals; hot bucket last)
-    int32_t *cursor;                 // [W*P] placement cursors (peer-memory partition)
     int64_t *bstart;                 // [W*P+1] first send slot of each bucket
     int64_t *sroff;                  // [W*P+1] float offset of each bucket in the rows buffer
     const int32_t *send_uid;         // [U] uid of each send slot (bucket-sorted)
@@ -72,7 +71,7 @@ struct MultiArgs {
 void launch_bucket(const MultiArgs &m, cudaStream_t s);
 void launch_bucket_prefix(const MultiArgs &m, cudaStream_t s);
 void launch_send_prep(const MultiArgs &m, int num_sms, cudaStream_t s);
-// Partition without the sort (peer-memory exchange: slot order inside a bucket is free)
+// Partition of the peer-memory exchange: stable (uid order inside a bucket), placed without a sort
 void launch_partition_p2p(const MultiArgs &m, int num_sms, cudaStream_t s);
 void launch_owner_insert(const MultiArgs &m, Slot *table, uint32_t cap_mask, int *err, cudaStream_t s);
 void launch_contrib(const MultiArgs &m, cudaStream_t s);

@@ -63,7 +63,6 @@ static MultiArgs multi_args(picasso_ctx *ctx) {
     m.bval = mp.bval;
     m.bhist = mp.bhist;
     m.bcount = mp.bcount;
-    m.cursor = mp.bhist;  // scratch: the peer-memory partition does not use the bucket histogram
     m.bstart = mp.bstart;
     m.sroff = mp.sroff;
     m.send_uid = mp.send_uid;

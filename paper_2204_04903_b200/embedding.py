@@ -121,6 +121,10 @@ class PackedEmbedding:
     def hot_keys(self):
         return abi.picasso_get_hot_keys(self.ctx)
 
+    def send_list(self, owner, pack):
+        """Local rows this rank requested from `owner` for `pack` in the last forward (send order)."""
+        return abi.picasso_get_send_list(self.ctx, owner, pack)
+
     def send_counts(self):
         return abi.picasso_get_send_counts(self.ctx, self.world)
 

@@ -102,6 +102,9 @@ def run(cfg, W, steps=1, opt=0, dyadic=True, lr=0.05):
                     s = 0
                     for o in range(W):
                         recv.setdefault((o, p), []).append(plr[s:s + cnt[o]])
+                        # partition lists bit-exact (both exchanges: stable, uid order per bucket)
+                        got = g.ranks[r].send_list(o, p)
+                        assert np.array_equal(got, plr[s:s + cnt[o]]), f"send list r{r} owner {o} p{p}"
                         s += cnt[o]
                 assert g.ranks[r].send_counts() == sent.tolist(), f"send counts r{r}"
             for (o, p), lists in recv.items():

@@ -464,3 +464,84 @@ def test_batches_deterministic():
     assert (a.lengths == 0).any()  # toy has empty bags
     dy = make_dy(cfg, 0, 0)
     assert (dy * 256 == np.round(dy * 256)).all()
+
+
+# ---------------------------------------------------------------- reading O2: the pack key stream order
+def _o2_model_batch():
+    g = GOLD["key_stream_o2"]
+    F = len(g["field_to_table"])
+    dims = np.array(g["table_dim"], np.int64)
+    col = np.concatenate([[0], np.cumsum(dims[g["field_to_table"]])[:-1]])
+    m = oracle.OracleModel(g["field_to_table"], g["table_rows"], g["table_dim"], col, id_mode=dc.IDS_ROWS,
+                           pool=dc.POOL_SUM)
+    ob = oracle.OracleBatch(g["batch"], np.array(g["ids"], np.int64), np.array(g["offsets"], np.int32))
+    assert len(g["offsets"]) == F * g["batch"] + 1
+    return g, m, ob
+
+
+def test_o2_key_stream_golden():
+    """Hand-derived key stream / unique / inverse of a 2-pack, 4-field batch (fields sharing a
+    table dedupe together, fields of another pack are skipped, an empty bag).  Swapping the
+    stream to sample-major, or the fields' order, changes the unique order and fails here."""
+    g, m, ob = _o2_model_batch()
+    for p, exp in enumerate(g["packs"]):
+        keys = oracle.pack_key_stream(m, g["field_to_pack"], g["table_base"], ob, p)
+        assert keys.tolist() == exp["key_stream"]
+        u, inv = oracle.unique(keys)
+        assert u.tolist() == exp["unique"] and inv.tolist() == exp["inverse"]
+        k, lrow, cnt = oracle.partition(u, 2)
+        ex = exp["partition_W2"]
+        assert k.tolist() == ex["owner_keys"][0] + ex["owner_keys"][1]
+        assert lrow.tolist() == ex["local_rows"][0] + ex["local_rows"][1]
+        assert cnt.tolist() == ex["counts"]
+
+
+def test_o2_plan_reproduces_golden_layout():
+    """The oracle planner gives the golden's pack / table_base layout (one pack per dim)."""
+    g, m, ob = _o2_model_batch()
+    p = oracle.pack_plan(g["field_to_table"], g["table_rows"], g["table_dim"])
+    assert p["field_to_pack"].tolist() == g["field_to_pack"]
+    assert p["table_base"].tolist() == g["table_base"]
+
+
+# ---------------------------------------------------------------- reading O12: hot-set tie-break
+def test_hot_select_tie_golden():
+    g = GOLD["hot_select_ties"]
+    pk, ky, ct = np.array(g["pack"]), np.array(g["key"]), np.array(g["count"], np.uint64)
+    for c in g["cases"]:
+        sel = oracle.hot_select(pk, ky, ct, g["row_cost_bytes"], c["capacity"])
+        assert [[int(pk[i]), int(ky[i])] for i in sel] == c["hot"], c
+
+
+# ---------------------------------------------------------------- reading O6: fp64 accumulation
+def test_near_cancelling_gradient_is_the_rounded_exact_sum():
+    """A hot row whose gradient nearly cancels: 4001 occurrences of +1 / -1 (+ 2^-20 perturbations)
+    and one tiny term.  A fp32 running sum loses the tiny term (and its sign); the oracle's G must be
+    fp32(exact rational sum) — reading O6 (fp64 accumulation, rounded once), computed here with
+    Python Fractions, independently of the oracle."""
+    from fractions import Fraction
+
+    rng = np.random.default_rng(5)
+    n = 4001
+    vals = rng.uniform(-1, 1, n).astype(np.float32)
+    vals[0], vals[1] = np.float32(1e4), np.float32(-1e4)  # a large partial sum early on
+    vals[2:2000:2] += np.float32(3e3)
+    vals[3:2000:2] -= np.float32(3e3)
+    rest = float(sum(Fraction(float(v)) for v in vals[:-1]))
+    vals[-1] = np.float32(-rest)  # total = the rounding residue of the last term: tiny
+    # one table, one row, one field: sample b holds the row once with dY[b] = vals[b]
+    D = 4
+    m = oracle.OracleModel([0], [3], [D], [0], id_mode=dc.IDS_ROWS, pool=dc.POOL_SUM)
+    ids = np.ones(n, np.int64)
+    off = np.arange(n + 1, dtype=np.int32)
+    dy = np.repeat(vals[:, None], D, axis=1).astype(np.float32)
+    ob = oracle.OracleBatch(n, ids, off, dy)
+    G, cnt = oracle.table_grad(m, [ob], 0)
+    exact = sum((Fraction(float(v)) for v in vals), Fraction(0))
+    ref = np.float32(float(exact))  # float(Fraction) is correctly rounded; the sum is far inside fp64
+    assert cnt[1] == n and cnt[0] == 0 and cnt[2] == 0
+    assert (G[1] == ref).all(), (G[1], ref)
+    run = np.float32(0)
+    for v in vals:
+        run = np.float32(run + v)
+    assert run != ref  # the plain fp32 running sum misses it: the case reading O6 fixes
