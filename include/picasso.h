@@ -270,7 +270,10 @@ picasso_status picasso_get_send_list(picasso_ctx *ctx, int32_t owner, int32_t pa
  * the backward pull the requesters' G rows into the reduce + optimizer kernel.  Sizes stay on
  * the device (no host synchronisation inside a step: a step can be captured in a CUDA graph);
  * ranks meet at three device-side barriers per step (system-scope release/acquire flags; a
- * peer missing for 20 s latches PICASSO_ERR_CUDA "peer timeout" instead of hanging).  Results are
+ * peer missing for 20 s latches a sticky "peer timeout" instead of hanging: from then on the owner
+ * update kernels leave the tables and optimizer state untouched, and picasso_last_error — which
+ * every caller must check after a step in this mode — returns PICASSO_ERR_STATE until the
+ * context is destroyed).  Results are
  * bit-identical to section 5 (same layouts, same source-ordered sums).  HybridHash hot rows
  * keep their NCCL AllReduce.  Requirements: every rank built with the same plan and max_ids,
  * one GPU per rank, peer access between the GPUs (NVLink / NVSwitch).

@@ -205,12 +205,63 @@ def picasso_ctx_destroy(ctx):
     lib().picasso_ctx_destroy(ctx)
 
 
-def picasso_packed_lookup_fwd(ctx, ids, offsets, batch, out, stream=None):
+def _same_device(a, b):
+    import torch
+
+    b = torch.device(b)
+    if b.index is None:
+        b = torch.device(b.type, torch.cuda.current_device())
+    return a == b
+
+
+def _check(t, name, dtype, numel=None, shape=None, device=None):
+    """Host-side argument checks (the C ABI takes raw pointers and cannot see them): dtype,
+    contiguity, device and size of a tensor argument.  Raises PicassoError(INVALID_ARG)."""
+    import torch
+
+    if t is None:
+        return
+    bad = None
+    if t.dtype != dtype:
+        bad = f"dtype {t.dtype}, expected {dtype}"
+    elif not t.is_contiguous():
+        bad = "not contiguous"
+    elif not t.is_cuda:
+        bad = "not a CUDA tensor"
+    elif device is not None and not _same_device(t.device, device):
+        bad = f"on {t.device}, expected {device}"
+    elif not t.is_cuda:
+        bad = "not a CUDA tensor"
+    elif numel is not None and t.numel() != numel:
+        bad = f"{t.numel()} elements, expected {numel}"
+    elif shape is not None and tuple(t.shape) != tuple(shape):
+        bad = f"shape {tuple(t.shape)}, expected {tuple(shape)}"
+    if bad:
+        raise PicassoError(-1, "argument check", f"{name}: {bad}")
+
+
+def picasso_packed_lookup_fwd(ctx, ids, offsets, batch, out, stream=None, n_fields=None, out_width=None,
+                              device=None):
+    """ids int64 [N], offsets int32 [F*B+1] (CSR over the N ids, field-major), out fp32 [B, out_width]:
+    all contiguous CUDA tensors on the ctx's device.  n_fields / out_width (known to PackedEmbedding)
+    enable the size checks; offsets[F*B] == N is checked on the device (latched, picasso_last_error)."""
+    import torch
+
+    _check(ids, "ids", torch.int64, device=device)
+    _check(offsets, "offsets", torch.int32, numel=None if n_fields is None else int(n_fields) * int(batch) + 1,
+           device=device)
+    _check(out, "out", torch.float32, shape=None if out_width is None else (int(batch), int(out_width)),
+           device=device)
     _chk(lib().picasso_packed_lookup_fwd(ctx, _ptr(ids), _ptr(offsets), int(batch), int(ids.numel()), _ptr(out),
                                          _stream(stream)), "picasso_packed_lookup_fwd", ctx)
 
 
-def picasso_packed_lookup_bwd_update(ctx, grad_out, lr, step, stream=None):
+def picasso_packed_lookup_bwd_update(ctx, grad_out, lr, step, stream=None, batch=None, out_width=None, device=None):
+    """grad_out fp32 [B, out_width] contiguous, the forward's output layout."""
+    import torch
+
+    _check(grad_out, "grad_out", torch.float32,
+           shape=None if (batch is None or out_width is None) else (int(batch), int(out_width)), device=device)
     _chk(lib().picasso_packed_lookup_bwd_update(ctx, _ptr(grad_out), float(lr), int(step), _stream(stream)),
          "picasso_packed_lookup_bwd_update", ctx)
 

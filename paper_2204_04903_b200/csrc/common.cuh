@@ -24,7 +24,7 @@ struct Slot {
     int uid;                 // global unique index (first-occurrence order)
 };
 
-enum ErrBits : int { ERR_ID_RANGE = 1, ERR_CAPACITY = 2 };
+enum ErrBits : int { ERR_ID_RANGE = 1, ERR_CAPACITY = 2, ERR_OFFSETS = 8 };  // (4: ERR_PEER_TIMEOUT, p2p.h)
 
 // fp64 accumulator of four columns (gradient sums, reading O6)
 struct alignas(16) dbl4 {

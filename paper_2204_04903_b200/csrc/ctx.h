@@ -33,10 +33,10 @@ struct Carver {
     }
 };
 
-inline uint32_t pow2_at_least(uint64_t x) {
+inline uint64_t pow2_at_least(uint64_t x) {
     uint64_t p = 1024;
     while (p < x) p <<= 1;
-    return (uint32_t)p;
+    return p;
 }
 
 inline int bits_for(int64_t maxval) {
@@ -155,6 +155,7 @@ struct picasso_ctx {
     int32_t *empty_pack = nullptr;  // [P] the pack has an empty segment this step
     int32_t *blk_cnt = nullptr, *blk_off = nullptr, *d_total = nullptr, *long_cnt = nullptr;
     int *err = nullptr;
+    int32_t *seg_limit = nullptr;  // [1] k_field_prep -> k_seg_of (0 after an offsets error)
     unsigned long long *unique_gkey = nullptr;
     int32_t *k_a = nullptr, *v_a = nullptr, *k_b = nullptr, *v_b = nullptr, *hist = nullptr, *scratch = nullptr;
     int32_t *hist0 = nullptr, *hist1 = nullptr, *rowtot = nullptr;
@@ -264,6 +265,7 @@ struct picasso_ctx {
         d_total = c.take<int32_t>(1);
         long_cnt = c.take<int32_t>(P);
         err = c.take<int>(1);
+        seg_limit = c.take<int32_t>(1);
         unique_gkey = c.take<unsigned long long>(N);
         k_a = c.take<int32_t>(N);
         v_a = c.take<int32_t>(N);

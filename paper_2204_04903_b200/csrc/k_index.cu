@@ -71,6 +71,34 @@ __global__ void __launch_bounds__(1024) k_field_prep(IndexArgs a) {
         if (tid == 0) carry += warp_sums[31];
         __syncthreads();
     }
+    // offsets must be a CSR over the n_ids IDs (offsets[0] = 0, non-decreasing, offsets[F*B] =
+    // n_ids).  Checked at the field boundaries, the layout's only inputs; on a violation the
+    // error latches (PICASSO_ERR_INVALID_ARG) and the step runs on a substitute layout whose
+    // every position and segment is in range, so no later kernel indexes past the ID, position,
+    // output or dY buffers (per-segment kernels also clamp their ranges to [0, n_ids)).  The
+    // step's results are then meaningless: the caller must check picasso_last_error.
+    __shared__ int bad;
+    if (tid == 0) bad = (carry != a.N) || (a.F > 0 && a.offsets[0] != 0);
+    __syncthreads();
+    for (int f = tid; f < a.F; f += 1024)
+        if (a.offsets[(int64_t)(f + 1) * a.B] < a.offsets[(int64_t)f * a.B]) bad = 1;
+    __syncthreads();
+    if (bad) {  // substitute layout: the first field of the first pack holds all n_ids IDs in one bag
+        if (tid == 0) atomicOr(a.err, ERR_OFFSETS);
+        for (int k = tid; k < a.F; k += 1024) {
+            const int32_t gs = k == 0 ? 0 : (int32_t)a.N;
+            a.gstart_pm[k] = gs;
+            a.field_gstart[a.pm_fields[k]] = gs;
+            a.id_start[a.pm_fields[k]] = 0;
+        }
+        if (a.F > 0) {
+            const int32_t sg0 = a.pm_fields[0] * a.B;
+            for (int64_t g = tid; g < a.N; g += 1024) a.seg_of[g] = sg0;
+        }
+        if (tid == 0) carry = (int32_t)a.N;
+        __syncthreads();
+    }
+    if (tid == 0 && a.seg_limit) *a.seg_limit = bad ? 0 : (int32_t)a.N;  // k_seg_of: nothing to place
     if (tid == 0) a.gstart_pm[a.F] = carry;
     __syncthreads();
     for (int p = tid; p <= a.P; p += 1024) a.pack_gstart[p] = a.gstart_pm[a.pack_first_k[p]];
@@ -83,9 +111,10 @@ __global__ void __launch_bounds__(1024) k_field_prep(IndexArgs a) {
     // region at a time, which stays in L2 even when the whole table is gigabytes
     for (int t = tid; t < a.T; t += 1024) a.tocc[t] = 0;
     __syncthreads();
-    for (int f = tid; f < a.F; f += 1024)
-        atomicAdd(a.tocc + a.finfo[f].table,
-                  a.offsets[(int64_t)(f + 1) * a.B] - a.offsets[(int64_t)f * a.B]);
+    if (!bad)
+        for (int f = tid; f < a.F; f += 1024)
+            atomicAdd(a.tocc + a.finfo[f].table,
+                      a.offsets[(int64_t)(f + 1) * a.B] - a.offsets[(int64_t)f * a.B]);
     __syncthreads();
     __shared__ int64_t s_carry, wsum64[32];
     if (tid == 0) s_carry = 0;
@@ -146,19 +175,26 @@ __global__ void __launch_bounds__(256) k_dedup_insert(IndexArgs a) {
     const bool valid = g < a.N;
     unsigned long long gkey = 0;
     int32_t tbl = 0;
+    bool ok = false;
     if (valid) {
-        // packed position -> pm field -> field-major index j
+        // packed position -> pm field -> field-major index j (k == F only after an offsets error:
+        // k_field_prep then laid every field out empty)
         const int64_t k = upper_bound_dev(a.gstart_pm, 0, a.F + 1, (int32_t)g) - 1;
-        const int f = __ldg(a.pm_fields + k);
-        const int64_t j = (int64_t)__ldg(a.id_start + f) + (g - __ldg(a.gstart_pm + k));
-        const FieldInfo fi = a.finfo[f];
-        const int64_t row = row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
-        gkey = (unsigned long long)(__ldg(a.pack_key_off + fi.pack) + fi.base + row);
-        tbl = fi.table;
+        if (k < a.F) {
+            const int f = __ldg(a.pm_fields + k);
+            const int64_t j = (int64_t)__ldg(a.id_start + f) + (g - __ldg(a.gstart_pm + k));
+            const FieldInfo fi = a.finfo[f];
+            const int64_t row = row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
+            gkey = (unsigned long long)(__ldg(a.pack_key_off + fi.pack) + fi.base + row);
+            tbl = fi.table;
+            ok = true;
+        } else {
+            a.slot_of[g] = 0;
+        }
     }
     // warp pre-dedup: lanes holding the same key elect the lowest lane (= smallest g)
-    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-    if (!valid) return;
+    const unsigned vmask = __ballot_sync(0xffffffffu, ok);
+    if (!ok) return;
     const int lane = threadIdx.x & 31;
     const unsigned peers = __match_any_sync(vmask, gkey);
     const int leader = __ffs(peers) - 1;
@@ -277,6 +313,12 @@ __global__ void __launch_bounds__(kIdxThreads) k_inverse(IndexArgs a) {
     for (int i = 0; i < kItems; ++i) uids[i] = g0 + i < N ? __ldg(a.slot_of + g0 + i) : 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) uids[i] = g0 + i < N ? a.table[uids[i]].uid : 0;  // all lookups in flight
+    // a position left out of the dedup (only after an offsets error: k_field_prep) has no uid;
+    // 0 keeps the transpose's digits and row starts in range
+    const uint32_t U = (uint32_t)*a.d_total;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+        if ((uint32_t)uids[i] >= U) uids[i] = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int64_t g = g0 + i;

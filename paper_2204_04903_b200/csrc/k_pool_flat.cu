@@ -28,14 +28,18 @@ __global__ void __launch_bounds__(256) k_pool_flat(PoolArgs a) {
         const int32_t j0 = __ldg(a.offsets + sg), j1 = __ldg(a.offsets + sg + 1);
         const FieldInfo fi = a.finfo[f];
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int32_t gb = __ldg(a.field_gstart + f) - __ldg(a.id_start + f);
+        // IDs [lo, hi): the segment's range clamped so that j and its packed position j + gb stay
+        // inside [0, n_ids) whatever the offsets hold (an offsets error latches in k_field_prep)
+        const int64_t lo = max(max((int64_t)j0, (int64_t)0), -(int64_t)gb);
+        const int64_t hi = min(min((int64_t)j1, a.n_ids), a.n_ids - gb);
         if (a.row_off) {  // W > 1: the rows received for the position's unique key
-            const int32_t gb = __ldg(a.field_gstart + f) - __ldg(a.id_start + f);
 #pragma unroll 4
-            for (int32_t j = j0; j < j1; ++j)
+            for (int64_t j = lo; j < hi; ++j)
                 acc = add4(acc, ldg_f4(a.weight + a.row_off[__ldg(a.inverse + j + gb)] + c * 4));
         } else {
 #pragma unroll 4
-            for (int32_t j = j0; j < j1; ++j) {
+            for (int64_t j = lo; j < hi; ++j) {
                 const int64_t row = fi.base + row_of(a.id_mode, __ldg(a.ids + j), fi, a.err);
                 acc = add4(acc, ldg_f4(a.weight + row * D + c * 4));
             }

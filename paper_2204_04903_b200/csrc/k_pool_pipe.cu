@@ -81,13 +81,19 @@ __device__ __forceinline__ void lane_store_cs(float *row, int lane, const float 
 
 // (also flags the packs that have an empty segment: k_pool_pipe zeroes them only there)
 __global__ void k_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart,
-                         const int32_t *id_start, int32_t *seg_of, const FieldInfo *finfo, int32_t *empty_pack) {
+                         const int32_t *id_start, int32_t *seg_of, const FieldInfo *finfo, int32_t *empty_pack,
+                         const int32_t *gtotal, int *err) {
     const int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sg >= (int64_t)F * B) return;
     const int32_t f = (int32_t)(sg / B);
-    const int32_t o0 = __ldg(offsets + sg), o1 = __ldg(offsets + sg + 1);
+    int32_t o0 = __ldg(offsets + sg), o1 = __ldg(offsets + sg + 1);
     const int32_t gb = __ldg(field_gstart + f) - __ldg(id_start + f);
-    for (int32_t j = o0; j < o1; ++j) seg_of[j + gb] = (int32_t)sg;
+    // positions stay inside [0, total) whatever the offsets hold (total = 0 after an offsets
+    // error: k_field_prep filled seg_of itself); a decreasing pair inside a field latches it
+    const int64_t total = __ldg(gtotal);
+    if (o1 < o0 && err) atomicOr(err, ERR_OFFSETS);
+    const int64_t lo = max((int64_t)o0, -(int64_t)gb), hi = min((int64_t)o1, total - gb);
+    for (int64_t j = lo; j < hi; ++j) seg_of[j + gb] = (int32_t)sg;
     if (o1 == o0 && empty_pack) empty_pack[finfo[f].pack] = 1;
 }
 
@@ -286,11 +292,12 @@ bool pool_pipe_supported(int D, const PoolArgs &a) {
 }
 
 void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
-                   int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo, int32_t *empty_pack) {
+                   int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo, int32_t *empty_pack, const int32_t *gtotal,
+                   int *err) {
     const int64_t n = (int64_t)F * B;
     if (n > 0)
         k_seg_of<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(offsets, B, F, field_gstart, id_start, seg_of, finfo,
-                                                            empty_pack);
+                                                            empty_pack, gtotal, err);
 }
 
 int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s) {

@@ -70,6 +70,7 @@ struct IndexArgs {
     int32_t region_shift;          // region >= occurrences << shift (load factor <= 1/2 or 1/4)
     int32_t *tocc;                 // [T] scratch: occurrences per table
     int32_t *empty_pack;           // [P] zeroed here, set by k_seg_of
+    int32_t *seg_limit;            // [1] out: positions k_seg_of may place (n_ids; 0 after an offsets error)
     int32_t sort_bits0;            // digit width of the backward's first radix pass
     int32_t *sort_hist0;           // [radix0, nblk] out: digit-major histogram of that pass
     int *err;
@@ -127,13 +128,16 @@ struct PoolArgs {
     const int32_t *pack_gstart;  //   [P+1] its packed positions,
     const int32_t *field_k;      //   [F] index of each field within its pack
     const int32_t *empty_pack;   //   [P] 1 if the pack has an empty segment this step (k_seg_of)
+    int64_t n_ids;               // IDs of the step: per-segment ranges are clamped to [0, n_ids)
 };
 void launch_pool(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 // k_pool_pipe.cu: pipelined pool for D >= 64 (needs seg_of from launch_seg_of); returns #launches
 bool pool_pipe_supported(int D, const PoolArgs &a);
 int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
+// gtotal: [1] positions k_seg_of may place (k_field_prep: n_ids, 0 after an offsets error); err: latch
 void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
-                   int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo = nullptr, int32_t *empty_pack = nullptr);
+                   int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo, int32_t *empty_pack, const int32_t *gtotal,
+                   int *err);
 // k_pool_flat.cu: one thread per 16-B output chunk (every D); returns #launches
 int launch_pool_flat(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 

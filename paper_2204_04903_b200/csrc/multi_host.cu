@@ -118,7 +118,7 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
     ctx->B = B;
     ctx->offsets = offsets;
     IndexArgs a = make_index_args(ctx, ids, offsets, B, N);
-    const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(N, 1) * 2));
+    const uint32_t cap_step = (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(N, 1) * 2));
     a.cap_mask = cap_step - 1;
     ctx->mark(0, true, s);
     if (!a.region_base) MCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
@@ -236,7 +236,7 @@ picasso_status mfwd_c(picasso_ctx *ctx, cudaStream_t s) {
     a.err = ctx->err;
     for (int p = 0; p <= P; ++p) mp.og_h[p] = (int32_t)mp.opack_ostart[p];
     MCK(cudaMemcpyAsync(mp.opack_gstart, mp.og_h, sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice, s));
-    const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(R, 1) * 2));
+    const uint32_t cap_step = (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(R, 1) * 2));
     ctx->mark(4, true, s);
     MCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
     launch_owner_insert(m, ctx->table, cap_step - 1, ctx->err, s);

@@ -271,6 +271,9 @@ __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *
                                                     float *state2, int opt, float lr, float eps, float beta1,
                                                     float beta2, float adam_ss) {
     constexpr int V4 = D / 4;
+    // a barrier of this or an earlier step timed out (sticky until the context is destroyed): the
+    // pushed G rows may be stale or partial, so the tables and optimizer state are left untouched
+    if (__ldcg(a.err) & ERR_PEER_TIMEOUT) return;
     const int64_t o0 = a.pack_ostart[pack];
     const int64_t n = (int64_t)a.ocount[pack] * V4;
     const int64_t rb = a.row_base[pack];

@@ -101,15 +101,21 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     c->pack_first_k[c->P] = c->F;
     // dedup table: per-table regions (<= 4 x max_ids + 64 per table) for the rank-local dedup, and a
     // pow2 >= 2 x max_recv global table for the NCCL owner dedup, in the same slots
-    c->cap = pow2_at_least((uint64_t)std::max<int64_t>(std::max<int64_t>(opts->max_ids, c->mp.max_recv), 1) * 2);
     // per-table regions only when one global table would not stay in L2 (2 x max_ids x 16 B > ~64 MB):
     // below that the global table (load factor <= 1/4 here) has the shorter probe chains
     c->use_regions = opts->max_ids > ((int64_t)1 << 21);
     if (const char *e = std::getenv("PICASSO_DEDUP_REGIONS")) c->use_regions = std::atoi(e) != 0;
     c->region_shift = 1;
+    uint64_t cap64 = pow2_at_least((uint64_t)std::max<int64_t>(std::max<int64_t>(opts->max_ids, c->mp.max_recv), 1) * 2);
     if (c->use_regions)
-        c->cap = (uint32_t)std::max<uint64_t>(
-            c->cap, ((uint64_t)opts->max_ids << (c->region_shift + 1)) + 64 * (uint64_t)c->T);
+        cap64 = std::max<uint64_t>(cap64, ((uint64_t)opts->max_ids << (c->region_shift + 1)) + 64 * (uint64_t)c->T);
+    // hash slots are int32 (slot_of, the device-side region bases): a table that would need more
+    // than 2^31 - 1 slots (max_ids above ~2^28 with per-table regions) is refused up front
+    if (cap64 > (uint64_t)INT32_MAX) {
+        delete c;
+        return PICASSO_ERR_CAPACITY;
+    }
+    c->cap = (uint32_t)cap64;
     if (world > 1) {  // local rows must fit int32 (received keys are int32 local rows)
         for (int32_t p = 0; p < c->P; ++p)
             if (c->pack_rows[p] / world >= ((int64_t)1 << 31)) {
@@ -128,7 +134,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
             for (int32_t p = 0; p < c->P; ++p) minD = std::min(minD, c->pack_dim[p]);
             const int nst = opts->opt == PICASSO_OPT_ADAM_LAZY ? 2 : 1;
             c->mp.k_max = opts->cache_max_bytes / ((int64_t)4 * minD * (1 + nst));
-            c->mp.hot_mask = pow2_at_least((uint64_t)std::max<int64_t>(c->mp.k_max, 1) * 2) - 1;
+            c->mp.hot_mask = (uint32_t)(pow2_at_least((uint64_t)std::max<int64_t>(c->mp.k_max, 1) * 2) - 1);
         }
     }
     if (const char *e = std::getenv("PICASSO_BWD")) {
@@ -341,6 +347,7 @@ IndexArgs picasso::make_index_args(picasso_ctx *ctx, const int64_t *ids, const i
     a.region_mask = ctx->region_mask;
     a.region_shift = ctx->region_shift;
     a.empty_pack = ctx->empty_pack;
+    a.seg_limit = ctx->seg_limit;
     a.tocc = ctx->tocc;
     a.seg_of = ctx->seg_of;
     a.inverse = ctx->inverse;
@@ -367,7 +374,10 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ctx->launches_fwd = 0;
     if (ctx->world > 1) {
-        if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_fwd
+        // loopback groups step through picasso_group_fwd; the NCCL exchange and the HybridHash
+        // AllReduce need the communicator; the peer-memory exchange alone needs only the windows
+        if (ctx->mp.group) return PICASSO_ERR_STATE;
+        if (!ctx->mp.comm && (!ctx->mp.p2p || ctx->opts.cache_max_bytes > 0)) return PICASSO_ERR_STATE;
         if (ctx->opts.exchange == 0 && !ctx->mp.p2p) {
             ctx->last_msg = "peer-memory exchange: picasso_p2p_handle / picasso_p2p_open not done";
             return PICASSO_ERR_STATE;
@@ -376,7 +386,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
                            : multi_fwd_nccl(ctx, ids, offsets, batch, n_ids, out, s);
     }
     IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
-    const uint32_t cap_step = std::min<uint32_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
+    const uint32_t cap_step =
+        (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
     a.cap_mask = cap_step - 1;
     ctx->B = batch;
     ctx->N = n_ids;
@@ -393,7 +404,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         if (!a.region_base) CK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
         launch_field_prep(a, s);
         launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s, ctx->finfo,
-                      ctx->empty_pack);
+                      ctx->empty_pack, ctx->seg_limit, ctx->err);
         CK(cudaEventRecord(ctx->ev_fork, s));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
         cudaStream_t t = ctx->side;
@@ -413,7 +424,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         CK(cudaEventRecord(ctx->ev_fp, s));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fp, 0));
         launch_seg_of(offsets, batch, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, ctx->side, ctx->finfo,
-                      ctx->empty_pack);
+                      ctx->empty_pack, ctx->seg_limit, ctx->err);
         CK(cudaEventRecord(ctx->ev_seg, ctx->side));
         launch_dedup_insert(a, s);
         launch_dedup_assign(a, s);
@@ -458,7 +469,8 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ctx->launches_bwd = 0;
     if (ctx->world > 1) {
-        if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;  // loopback: picasso_group_bwd_update
+        if (ctx->mp.group) return PICASSO_ERR_STATE;  // loopback: picasso_group_bwd_update
+        if (!ctx->mp.comm && (!ctx->mp.p2p || ctx->opts.cache_max_bytes > 0)) return PICASSO_ERR_STATE;
         return ctx->mp.p2p ? multi_bwd_p2p(ctx, grad_out, lr, step, s) : multi_bwd_nccl(ctx, grad_out, lr, step, s);
     }
     const int64_t N = ctx->N;
@@ -504,7 +516,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
 // segment of every packed position, for the sort and the pool.
 void picasso::transpose_fork(picasso_ctx *ctx, cudaStream_t s) {
     launch_seg_of(ctx->offsets, ctx->B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s, ctx->finfo,
-                  ctx->empty_pack);
+                  ctx->empty_pack, ctx->seg_limit, ctx->err);
     ctx->launches_fwd += (int64_t)ctx->F * ctx->B > 0 ? 1 : 0;
     cudaStream_t t = s;
     if (ctx->overlap && ctx->side) {
@@ -557,6 +569,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
     pa.pack_gstart = ctx->pack_gstart;
     pa.field_k = ctx->pipe_pool ? ctx->field_k_d : nullptr;
     pa.empty_pack = ctx->empty_pack;
+    pa.n_ids = ctx->N;
     for (int32_t p = 0; p < ctx->P; ++p) {  // seg_of: written by transpose_fork (k_seg_of)
         if (only_pack >= 0 && p != only_pack) continue;
         pa.pack = p;
@@ -633,10 +646,17 @@ extern "C" picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t
         } else {
             int h = 0;
             if (cudaMemcpy(&h, ctx->err, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && h) {
-                if (h & ERR_ID_RANGE) { st = PICASSO_ERR_ID_RANGE; m = "raw ID outside [0, V_t) in ROWS mode"; }
+                if (h & ERR_PEER_TIMEOUT) { st = PICASSO_ERR_STATE; m = "peer timeout: a rank never reached a barrier (sticky: destroy the context)"; }
+                else if (h & ERR_ID_RANGE) { st = PICASSO_ERR_ID_RANGE; m = "raw ID outside [0, V_t) in ROWS mode"; }
+                else if (h & ERR_OFFSETS) { st = PICASSO_ERR_INVALID_ARG; m = "offsets are not a CSR over n_ids IDs"; }
                 else if (h & ERR_CAPACITY) { st = PICASSO_ERR_CAPACITY; m = "device capacity overflow"; }
-                else if (h & ERR_PEER_TIMEOUT) { st = PICASSO_ERR_CUDA; m = "peer timeout: a rank never reached a barrier"; }
+                // ID-range / capacity / offsets errors belong to the step that raised them; a peer
+                // timeout is sticky (the ranks' barrier epochs no longer agree: destroy the context)
                 cudaMemset(ctx->err, 0, sizeof(int));
+                if (h & ERR_PEER_TIMEOUT) {
+                    const int keep = ERR_PEER_TIMEOUT;
+                    cudaMemcpy(ctx->err, &keep, sizeof(int), cudaMemcpyHostToDevice);
+                }
             }
         }
     }

@@ -61,7 +61,10 @@ class PackedEmbedding:
         # world > 1, one process per GPU: the exchange runs over NVLink peer memory ("p2p", the
         # default) or NCCL AllToAllv ("nccl").  all_gather(bytes) -> [bytes] * world shares the
         # windows' IPC handles (default: torch.distributed.all_gather_object).
-        if world > 1 and nccl_uid is not None and self.exchange == "p2p":
+        # Without a NCCL id (nccl_uid None) the peer-memory exchange still runs when all_gather is
+        # given and the cache is off: e.g. several processes sharing one GPU, where NCCL refuses
+        # duplicate devices (tests/test_xproc_gpu.py).
+        if world > 1 and self.exchange == "p2p" and (nccl_uid is not None or all_gather is not None):
             h = abi.picasso_p2p_handle(self.ctx)
             if all_gather is None:
                 import torch.distributed as dist
@@ -80,12 +83,16 @@ class PackedEmbedding:
                 stream=None):
         if out is None:
             out = torch.empty(batch, self.out_width, dtype=torch.float32, device=self.device)
-        abi.picasso_packed_lookup_fwd(self.ctx, ids, offsets, batch, out, stream)
+        abi.picasso_packed_lookup_fwd(self.ctx, ids, offsets, batch, out, stream, n_fields=len(self.f2t),
+                                      out_width=self.out_width, device=self.device)
+        self._batch = batch
         return out
 
     def backward_update(self, grad_out: torch.Tensor, lr: float, step: int | None = None, stream=None):
         self.step = self.step + 1 if step is None else step
-        abi.picasso_packed_lookup_bwd_update(self.ctx, grad_out, lr, self.step, stream)
+        abi.picasso_packed_lookup_bwd_update(self.ctx, grad_out, lr, self.step, stream,
+                                             batch=getattr(self, "_batch", None), out_width=self.out_width,
+                                             device=self.device)
 
     def check(self):
         st, msg = abi.picasso_last_error(self.ctx)

@@ -16,9 +16,16 @@ import torch.distributed as dist  # noqa: E402
 
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # PICASSO_XPROC_SAMEDEV=1: every rank on cuda:0, no NCCL communicator (NCCL refuses two ranks
+    # on one device): the peer-memory exchange between processes — IPC windows opened by another
+    # process, system-scope device barriers — is then testable on a one-GPU box
+    samedev = os.environ.get("PICASSO_XPROC_SAMEDEV") == "1"
+    local = 0 if samedev else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if samedev:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import oracle
     import paper_2204_04903_b200 as pb
     from datagen import configs as dc
@@ -45,12 +52,22 @@ def main():
     cfgs = [cfg.replace(batch=b) for b in bsz]
     obj = [pb.picasso_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
+    all_gather = None
+    if samedev:
+        assert not cache, "HybridHash needs the NCCL AllReduce"
+        obj = [None]
+
+        def all_gather(x):
+            out = [None] * world
+            dist.all_gather_object(out, x)
+            return out
     mi = cfg.batch * cfg.F * 60
     e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=max(cfg.batch, 1), max_ids=mi,
                            table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
                            rank=rank, world=world, nccl_uid=obj[0], max_recv=world * mi,
                            device=torch.device("cuda", local), cache_max_bytes=(1 << 20) if cache else 0,
-                           split=2 if base == "criteok2" else False)  # k2: two K-Interleaving groups
+                           split=2 if base == "criteok2" else False,  # k2: two K-Interleaving groups
+                           all_gather=all_gather)
     init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights, rank=rank,
                            world=world)
     m, tabs = oracle_model(cfg), oracle_tables(cfg)
@@ -101,7 +118,8 @@ def main():
             assert_close(e.state1[p][:len(exp)].cpu().numpy(), exp, what=f"state p{p}")
     report["ok"] = True
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"nccl_{name}_rank{rank}.json"), "w") as f:
+    tag = "xproc" if samedev else "nccl"
+    with open(os.path.join(ROOT, "gpurun_out", f"{tag}_{name}_rank{rank}.json"), "w") as f:
         json.dump(report, f)
     e.close()
     dist.destroy_process_group()

@@ -274,6 +274,62 @@ def test_rows_mode_out_of_range_is_latched():
         emb.check()
 
 
+@pytest.mark.parametrize("kind", ["short", "long", "decreasing", "start"])
+def test_bad_offsets_are_latched(kind):
+    """offsets that are not a CSR over the ids (total != n_ids, a decreasing field boundary, a
+    non-zero start) latch INVALID_ARG in k_field_prep, which then lays the step out on a
+    substitute layout: no kernel reads or writes past its buffers (no illegal access, which would
+    surface as PICASSO_ERR_CUDA), and the error belongs to that step only."""
+    import paper_2204_04903_b200 as pb
+
+    for cfg in (dc.scaled(dc.criteo(), batch=256, rows_div=20000), dc.toy(), dc.scaled(dc.wdl(), batch=16, rows_div=1000)):
+        emb = gpu_embedding(cfg)
+        b = make_batch(cfg, 0, 0)
+        off = b.offsets.copy()
+        if kind == "short":
+            off[-1] -= 3
+        elif kind == "long":
+            off[-1] += 1000
+        elif kind == "decreasing":
+            off[cfg.batch] = off[2 * cfg.batch] + 5
+        else:
+            off[0] = 2
+        ids = torch.from_numpy(b.ids).cuda()
+        emb.forward(ids, torch.from_numpy(off).cuda(), cfg.batch)
+        emb.backward_update(torch.ones(cfg.batch, cfg.out_width, device="cuda"), lr=0.1, step=1)
+        with pytest.raises(pb.PicassoError) as ei:
+            emb.check()
+        assert ei.value.status == -1 and "CSR" in str(ei.value), str(ei.value)
+        # a valid step afterwards runs clean and its forward is the oracle's on the current tables
+        b2 = make_batch(cfg, 0, 1)
+        i2, o2 = to_dev(b2)
+        out = emb.forward(i2, o2, cfg.batch)
+        emb.check()
+        tabs = [gpu_table_rows(emb, cfg, t) for t in range(cfg.T)]
+        ref = oracle.forward(oracle_model(cfg), oracle.OracleBatch(cfg.batch, b2.ids, b2.offsets), tabs, cfg.out_width)
+        assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_host_side_argument_checks():
+    import paper_2204_04903_b200 as pb
+
+    cfg = dc.toy()
+    emb = gpu_embedding(cfg)
+    b = make_batch(cfg, 0, 0)
+    ids, off = to_dev(b)
+    with pytest.raises(pb.PicassoError, match="ids: dtype"):
+        emb.forward(ids.to(torch.int32), off, cfg.batch)
+    with pytest.raises(pb.PicassoError, match="offsets: .* elements"):
+        emb.forward(ids, off[:-1], cfg.batch)
+    with pytest.raises(pb.PicassoError, match="not contiguous"):
+        emb.forward(torch.stack([ids, ids], 1)[:, 0], off, cfg.batch)
+    with pytest.raises(pb.PicassoError, match="not a CUDA tensor"):
+        emb.forward(ids.cpu(), off, cfg.batch)
+    emb.forward(ids, off, cfg.batch)
+    with pytest.raises(pb.PicassoError, match="grad_out: shape"):
+        emb.backward_update(torch.zeros(cfg.batch, cfg.out_width + 4, device="cuda"), lr=0.1, step=1)
+
+
 def test_deterministic_rerun():
     cfg = dc.scaled(dc.wdl(), batch=64, rows_div=5000).replace(alpha=1.3)
     res = []
