@@ -22,8 +22,9 @@
  *    synchronise the host when world == 1 or with the peer-memory exchange at world > 1
  *    (the step is CUDA-graph capturable).
  *  - Argument / plan errors are synchronous return codes.  Device-detected errors (ID out
- *    of range in ROWS mode, capacity overflow) are latched in a device word and reported by
- *    picasso_last_error (which synchronises the stream it last used).
+ *    of range in ROWS mode, capacity overflow, offsets that are not a CSR over the IDs, a peer
+ *    timeout) are latched in a device word and reported by picasso_last_error (which
+ *    synchronises the stream it last used).
  *  - One ctx per rank; a ctx is not thread-safe.
  */
 #ifndef PICASSO_H_
@@ -110,6 +111,13 @@ typedef struct {
     int32_t exchange;        /* world > 1: 0 = NVLink peer memory (section 7; the rows / G buffers
                               live in the IPC window, not the workspace), 1 = NCCL AllToAllv
                               (section 5; loopback: device copies) */
+    int64_t max_step_unique; /* world == 1: D-Interleaving (section 8) — distinct keys one step's
+                              micro-batches may touch together (sizes the step accumulator:
+                              16 B index slots x 2, max_step_unique x max dim fp64); 0 = off */
+    int32_t cold_tier;       /* world == 1: 1 = HybridHash with a host-DRAM cold tier (section 9):
+                              the packs' weights / state passed to picasso_bind live in pinned,
+                              device-mapped host memory and up to cache_max_bytes of their
+                              hottest rows are cached in HBM; 0 = tables in device memory */
 } picasso_ctx_opts;
 
 /* NCCL unique id (128 bytes, host) for picasso_ctx_create; rank 0 calls it and broadcasts
@@ -147,7 +155,10 @@ picasso_status picasso_ctx_destroy(picasso_ctx *ctx);
  *           offsets[0] == 0, non-decreasing, offsets[F*B] == n_ids.
  * out     : device fp32 [batch, out_width], fully overwritten.
  * Keeps the per-step state (unique keys, inverse, segment map) in the workspace for the
- * next picasso_packed_lookup_bwd_update.
+ * next picasso_packed_lookup_bwd_update, and reads `offsets` again there (mean combiner: bag
+ * lengths): offsets must stay valid and unchanged until that backward has been enqueued.
+ * offsets that are not such a CSR latch INVALID_ARG (picasso_last_error); the step then runs
+ * on a substitute layout that keeps every access in bounds, and its results are meaningless.
  * Errors: CAPACITY if batch > max_batch or n_ids > max_ids; STATE if not bound. */
 picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets,
                                          int32_t batch, int64_t n_ids, float *out, void *stream);
@@ -261,6 +272,34 @@ picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts);
  * int64 [cap]; n: the list length. */
 picasso_status picasso_get_send_list(picasso_ctx *ctx, int32_t owner, int32_t pack, int64_t *dst, int64_t cap,
                                      int64_t *n);
+
+/* 8. D-Interleaving (Eq. 2), world == 1, opts.max_step_unique > 0.
+ * A step's batch is sliced into micro-batches (per field, samples [b0, b1): the caller slices
+ * ids / offsets) that flow through the layer one after another, so every batch-proportional
+ * buffer — out, dY, and the ctx's per-ID / per-unique scratch (max_batch, max_ids) — is sized
+ * for one micro-batch; the update is applied once, with the whole batch's gradient:
+ *   picasso_micro_batch_size : Eq. 2, BS_micro = min over ops of rbound[i] / rinstance[i]
+ *                              (host arrays [n_ops]; e.g. bytes of device memory an op may use /
+ *                              its bytes per sample measured in warm-up, L416-421), clamped to
+ *                              batch, then the batch evenly divided: n_micro = ceil(batch /
+ *                              BS_micro), bs_micro = ceil(batch / n_micro).  CAPACITY if a bound
+ *                              admits no sample at all.
+ *   picasso_dinterleave_begin : starts a step (clears the step accumulator).
+ *   then per micro-batch: picasso_packed_lookup_fwd (unchanged: its output rows are the whole
+ *      batch's rows of those samples, bit-exact — the tables are not updated until apply), and
+ *   picasso_packed_lookup_bwd_accumulate(grad_out = that micro-batch's dY, out's layout): its
+ *      per-unique G rows (rounded once from fp64) added in fp64 to the step accumulator;
+ *   picasso_dinterleave_apply : G = fp32(accumulated sum) of every row any micro-batch touched,
+ *      and the optimizer step (as picasso_packed_lookup_bwd_update; step is 1-based).
+ * Results equal the whole batch's step (bit-exact under dyadic dY; otherwise within 1 ulp of G:
+ * reading O6').  More distinct keys than max_step_unique latch CAPACITY (the step's
+ * update is then incomplete).  picasso_packed_lookup_bwd_update is refused (STATE) between begin
+ * and apply. */
+picasso_status picasso_micro_batch_size(int32_t n_ops, const double *rbound, const double *rinstance, int32_t batch,
+                                        int32_t *bs_micro, int32_t *n_micro);
+picasso_status picasso_dinterleave_begin(picasso_ctx *ctx, void *stream);
+picasso_status picasso_packed_lookup_bwd_accumulate(picasso_ctx *ctx, const float *grad_out, void *stream);
+picasso_status picasso_dinterleave_apply(picasso_ctx *ctx, float lr, int64_t step, void *stream);
 
 /* 7. Exchange over NVLink peer memory (kernel-initiated Shuffle&Stitch).
  * Replaces the NCCL AllToAllv of section 5 with one shared window per rank (barrier flags,

@@ -34,6 +34,12 @@ from .abi import (  # noqa: F401
     picasso_hot_cache_refresh,
     picasso_group_hot_cache_refresh,
     picasso_get_hot_keys,
+    picasso_get_send_list,
+    picasso_micro_batch_size,
+    picasso_dinterleave_begin,
+    picasso_packed_lookup_bwd_accumulate,
+    picasso_dinterleave_apply,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
 from .embedding import LoopbackGroup, PackedEmbedding  # noqa: F401
+from . import dinterleave  # noqa: F401

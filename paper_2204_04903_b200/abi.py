@@ -23,7 +23,8 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_group_create", "picasso_group_destroy", "picasso_group_fwd", "picasso_group_bwd_update",
            "picasso_get_owner_unique", "picasso_get_send_counts", "picasso_hot_cache_refresh",
            "picasso_group_hot_cache_refresh", "picasso_get_hot_keys", "picasso_p2p_handle", "picasso_p2p_open",
-           "picasso_group_p2p", "picasso_get_send_list"]
+           "picasso_group_p2p", "picasso_get_send_list", "picasso_micro_batch_size", "picasso_dinterleave_begin",
+           "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -43,7 +44,8 @@ class PlanView(C.Structure):
 class CtxOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_ids", C.c_int64), ("pool", C.c_int32), ("id_mode", C.c_int32),
                 ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
-                ("max_recv", C.c_int64), ("cache_max_bytes", C.c_int64), ("exchange", C.c_int32)]
+                ("max_recv", C.c_int64), ("cache_max_bytes", C.c_int64), ("exchange", C.c_int32),
+                ("max_step_unique", C.c_int64), ("cold_tier", C.c_int32)]
 
 
 class CacheStats(C.Structure):
@@ -93,6 +95,10 @@ def lib():
             "picasso_profile_enable": [vp, i32],
             "picasso_profile_read": [vp, vp, C.POINTER(i64)],
             "picasso_unique_offsets": [vp, vp, vp],
+            "picasso_micro_batch_size": [i32, vp, vp, i32, C.POINTER(i32), C.POINTER(i32)],
+            "picasso_dinterleave_begin": [vp, vp],
+            "picasso_packed_lookup_bwd_accumulate": [vp, vp, vp],
+            "picasso_dinterleave_apply": [vp, C.c_float, i64, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -157,7 +163,8 @@ def picasso_nccl_unique_id():
 
 def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, field_col, out_width, rank, world,
                        max_batch, max_ids, pool=POOL_SUM, id_mode=IDS_HASH, opt=OPT_ADAGRAD, eps=None, beta1=0.9,
-                       beta2=0.999, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange="p2p"):
+                       beta2=0.999, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange="p2p", max_step_unique=0,
+                       cold_tier=0):
     k = _Keep()
     k.f2t = _np(field_to_table, np.int32)
     k.t2p = _np(plan["table_to_pack"], np.int32)
@@ -172,7 +179,8 @@ def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, 
     if eps is None:
         eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
     o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),
-                float(beta2), int(max_recv), int(cache_max_bytes), 0 if exchange == "p2p" else 1)
+                float(beta2), int(max_recv), int(cache_max_bytes), 0 if exchange == "p2p" else 1, int(max_step_unique),
+                int(cold_tier))
     ctx = C.c_void_p()
     uid = None if nccl_uid is None else (C.c_uint8 * 128)(*nccl_uid)
     _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), uid, C.byref(o), C.byref(ctx)),
@@ -414,3 +422,31 @@ def picasso_get_hot_keys(ctx):
     _chk(lib().picasso_get_hot_keys(ctx, pk.ctypes.data, ky.ctypes.data, n.value, C.byref(n)), "picasso_get_hot_keys",
          ctx)
     return pk[:n.value], ky[:n.value]
+
+
+# ---- D-Interleaving (include/picasso.h section 8) -----------------------------------------
+def picasso_micro_batch_size(rbound, rinstance, batch):
+    """Eq. 2: (bs_micro, n_micro) from per-op bounds and per-instance costs (sequences of floats)."""
+    rb = _np(rbound, np.float64)
+    ri = _np(rinstance, np.float64)
+    bs, n = C.c_int32(), C.c_int32()
+    _chk(lib().picasso_micro_batch_size(len(rb), rb.ctypes.data, ri.ctypes.data, int(batch), C.byref(bs), C.byref(n)),
+         "picasso_micro_batch_size")
+    return bs.value, n.value
+
+
+def picasso_dinterleave_begin(ctx, stream=None):
+    _chk(lib().picasso_dinterleave_begin(ctx, _stream(stream)), "picasso_dinterleave_begin", ctx)
+
+
+def picasso_packed_lookup_bwd_accumulate(ctx, grad_out, stream=None, batch=None, out_width=None, device=None):
+    import torch
+
+    _check(grad_out, "grad_out", torch.float32,
+           shape=None if (batch is None or out_width is None) else (int(batch), int(out_width)), device=device)
+    _chk(lib().picasso_packed_lookup_bwd_accumulate(ctx, _ptr(grad_out), _stream(stream)),
+         "picasso_packed_lookup_bwd_accumulate", ctx)
+
+
+def picasso_dinterleave_apply(ctx, lr, step, stream=None):
+    _chk(lib().picasso_dinterleave_apply(ctx, float(lr), int(step), _stream(stream)), "picasso_dinterleave_apply", ctx)

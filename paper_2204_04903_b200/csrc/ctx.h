@@ -233,6 +233,18 @@ struct picasso_ctx {
             }
     }
 
+    // D-Interleaving (dinterleave.cu): step accumulator over the micro-batches
+    Slot *di_table = nullptr;              // key -> arena offset (dbl4 units, in the uid field)
+    uint64_t di_cap = 0;                   // index slots (pow2)
+    double *di_acc = nullptr;              // fp64 arena
+    int64_t di_acc_cap4 = 0;               // arena capacity, dbl4 units
+    int64_t *di_off = nullptr;             // [max_ids] arena offset of each uid of the micro-batch
+    int32_t *di_list = nullptr;            // [max_step_unique] index slot of every accumulated row
+    unsigned long long *di_counters = nullptr;  // [2] rows, arena used
+    float **di_w = nullptr, **di_s1 = nullptr, **di_s2 = nullptr;  // [P] device copies of the pointers
+    bool di_active = false;
+    int64_t di_micro = 0;
+
     int32_t *osort_hist = nullptr;  // k_inverse's pass-0 histogram output when run on the owner stream
     int32_t *hot_scan_scratch = nullptr;
 
@@ -286,6 +298,18 @@ struct picasso_ctx {
         chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
         pack_gbase = c.take<int64_t>(P + 1);
         pack_dim_d = c.take<int32_t>(P);
+        if (world == 1 && opts.max_step_unique > 0) {  // D-Interleaving step accumulator
+            di_cap = pow2_at_least((uint64_t)opts.max_step_unique * 2);
+            di_table = c.take<Slot>(di_cap);
+            di_acc_cap4 = opts.max_step_unique * (maxD / 4);
+            di_acc = c.take<double>((size_t)di_acc_cap4 * 4);
+            di_off = c.take<int64_t>(N);
+            di_list = c.take<int32_t>(opts.max_step_unique);
+            di_counters = c.take<unsigned long long>(2);
+            di_w = c.take<float *>(P);
+            di_s1 = c.take<float *>(P);
+            di_s2 = c.take<float *>(P);
+        }
         // rows / G buffer: the IPC window holds it with the peer-memory exchange
         const bool p2p_ex = world > 1 && opts.exchange == 0;
         gbuf = ((split_bwd && world == 1) || (world > 1 && !p2p_ex)) ? c.take<float>((size_t)N * maxD) : nullptr;

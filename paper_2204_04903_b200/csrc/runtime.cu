@@ -41,6 +41,10 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (world < 1 || world > 8 || rank < 0 || rank >= world) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_batch <= 0 || opts->max_ids < 0 || opts->max_ids >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_recv < 0 || opts->max_recv >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
+    if (opts->max_step_unique < 0 || opts->max_step_unique >= (int64_t)1 << 31 ||
+        (opts->max_step_unique > 0 && world != 1))
+        return PICASSO_ERR_INVALID_ARG;
+    if (opts->cold_tier < 0 || opts->cold_tier > 1 || (opts->cold_tier && world != 1)) return PICASSO_ERR_INVALID_ARG;
     if (opts->pool < 0 || opts->pool > 1 || opts->id_mode < 0 || opts->id_mode > 1 || opts->opt < 0 || opts->opt > 1 ||
         opts->exchange < 0 || opts->exchange > 1)
         return PICASSO_ERR_INVALID_ARG;
@@ -225,6 +229,11 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_dim_d, ctx->pack_dim.data(), sizeof(int32_t) * ctx->P, cudaMemcpyHostToDevice));
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
+    if (ctx->di_w) {  // D-Interleaving: the apply kernel reaches every pack's rows
+        CK(cudaMemcpy(ctx->di_w, ctx->w.data(), sizeof(float *) * ctx->P, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->di_s1, ctx->s1.data(), sizeof(float *) * ctx->P, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->di_s2, ctx->s2.data(), sizeof(float *) * ctx->P, cudaMemcpyHostToDevice));
+    }
     if (ctx->world > 1 && !ctx->mp.cnt_send_h) {
         const int WP = ctx->world * ctx->P;
         CK(cudaMallocHost(&ctx->mp.cnt_send_h, sizeof(int32_t) * (WP + 1)));
@@ -464,7 +473,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
 extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, const float *grad_out, float lr,
                                                            int64_t step, void *stream) {
     if (!ctx || step < 1) return PICASSO_ERR_INVALID_ARG;
-    if (!ctx->bound || !ctx->fwd_done) return PICASSO_ERR_STATE;
+    if (!ctx->bound || !ctx->fwd_done || ctx->di_active) return PICASSO_ERR_STATE;
     if (!grad_out && ctx->B > 0) return PICASSO_ERR_INVALID_ARG;  // an empty batch has no dY
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ctx->launches_bwd = 0;

@@ -26,7 +26,8 @@ class PackedEmbedding:
     def __init__(self, field_to_table, table_rows, table_dim, *, max_batch, max_ids, table_salt=None,
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
-                 init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange=None, all_gather=None):
+                 init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange=None, all_gather=None,
+                 max_step_unique=0):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -43,7 +44,8 @@ class PackedEmbedding:
         self.ctx = abi.picasso_ctx_create(self.plan, self.f2t, self.rows, self.dims, table_salt, self.field_col,
                                           self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
                                           eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv,
-                                          cache_max_bytes=cache_max_bytes, exchange=self.exchange)
+                                          cache_max_bytes=cache_max_bytes, exchange=self.exchange,
+                                          max_step_unique=max_step_unique)
         P = self.plan["n_packs"]
         self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
         ws = abi.picasso_workspace_size(self.ctx)
@@ -93,6 +95,19 @@ class PackedEmbedding:
         abi.picasso_packed_lookup_bwd_update(self.ctx, grad_out, lr, self.step, stream,
                                              batch=getattr(self, "_batch", None), out_width=self.out_width,
                                              device=self.device)
+
+    # ---- D-Interleaving (include/picasso.h section 8)
+    def dinterleave_begin(self, stream=None):
+        abi.picasso_dinterleave_begin(self.ctx, stream)
+
+    def backward_accumulate(self, grad_out: torch.Tensor, stream=None):
+        """The last forward's micro-batch: its G rows added to the step accumulator."""
+        abi.picasso_packed_lookup_bwd_accumulate(self.ctx, grad_out, stream, batch=getattr(self, "_batch", None),
+                                                 out_width=self.out_width, device=self.device)
+
+    def dinterleave_apply(self, lr: float, step: int | None = None, stream=None):
+        self.step = self.step + 1 if step is None else step
+        abi.picasso_dinterleave_apply(self.ctx, lr, self.step, stream)
 
     def check(self):
         st, msg = abi.picasso_last_error(self.ctx)
