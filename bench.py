@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--config", default="criteo")
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--rows-div", type=int, default=1, help="tables at 1/rows_div of their rows (fit one GPU)")
     ap.add_argument("--nbatches", type=int, default=4, help="distinct pre-generated batches, used round robin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -46,6 +47,11 @@ def parse():
     ap.add_argument("--cache-warmup", type=int, default=3, help="Alg. 1 warmup_iters")
     ap.add_argument("--cache-flush", type=int, default=10, help="Alg. 1 flush_iters")
     ap.add_argument("--eager", action="store_true", help="N = 1: launch every step eagerly instead of a CUDA graph")
+    ap.add_argument("--micro", default=None,
+                    help="N = 1: D-Interleaving with this many micro-batches per step, or 'auto' (Eq. 2 "
+                         "from --micro-budget-gb); prints its own JSON line")
+    ap.add_argument("--micro-budget-gb", type=float, default=16.0,
+                    help="device-memory budget (GB) of the batch-proportional buffers for --micro auto")
     ap.add_argument("--kgroups", type=int, default=None,
                     help="K-Interleaving groups (packs per dim) at N > 1 with the peer-memory exchange "
                          "(default 1: measured no gain at C2 with 2 groups, DESIGN.md 7b)")
@@ -60,6 +66,8 @@ def get_cfg(args):
         cfg = cfg.replace(alpha=args.alpha)
     if args.batch is not None:
         cfg = cfg.replace(batch=args.batch)
+    if args.rows_div > 1:
+        cfg = dc.scaled(cfg, rows_div=args.rows_div)
     return cfg
 
 
@@ -117,56 +125,85 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_oracle_baseline(cfg, seconds):
-    """The oracle (oracle/picasso_oracle.cpp, single thread, as it stands) on a bounded sample
-    of the same workload: whole batches of this config, one rank; forward over every segment
+def host_cpu():
+    """Cores this process may use and the CPU model (/proc/cpuinfo) of the box."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return cores, model
+
+
+def cpu_oracle_baseline(cfg, seconds, openmp=False, max_steps=50):
+    """The oracle (oracle/picasso_oracle.cpp as it stands) on a bounded sample of the same
+    workload: whole batches of this config, one rank; forward over every segment
     (oracle_forward_sampled), gradients of every touched row (oracle_row_grads) and the
     Adagrad update (oracle_apply_update).  Table rows the sample touches are materialised
-    from the same generator beforehand (not timed)."""
+    from the same generator beforehand (not timed).  openmp=True: the -fopenmp build on every
+    host core (the same loops split over threads, results bitwise the plain build's)."""
     import oracle
     from datagen import make_batch, make_dy, table_values_np
 
-    m = oracle.OracleModel(cfg.field_to_table, cfg.table_rows, cfg.table_dim, cfg.field_col, id_mode=cfg.id_mode,
-                           pool=cfg.pool, table_salt=cfg.table_salt)
-    B = cfg.batch
-    ld = int(cfg.table_dim.max())
-    spent, samples, steps = 0.0, 0, 0
-    while steps == 0 or (spent < seconds and steps < 50):
-        b = make_batch(cfg, 0, 1000 + steps)
-        dy = make_dy(cfg, 0, 1000 + steps, dyadic=False)
-        ob = oracle.OracleBatch(B, b.ids, b.offsets, dy)
-        qf = np.repeat(np.arange(cfg.F, dtype=np.int32), B)
-        qs = np.tile(np.arange(B, dtype=np.int32), cfg.F)
-        rt, rr = oracle.segment_rows(m, ob, qf, qs)
-        key = np.unique(rt.astype(np.int64) * (1 << 40) + rr)
-        ut, ur = (key >> 40).astype(np.int32), key & ((1 << 40) - 1)
-        vals = np.zeros((len(key), ld), np.float32)
-        for t in np.unique(ut):
-            sel = ut == t
-            D = int(cfg.table_dim[t])
-            vals[sel, :D] = table_values_np(cfg.seed, int(t), ur[sel], D)
-        acc = np.full_like(vals, 0.1)
-        t0 = time.perf_counter()
-        oracle.forward_sampled(m, ob, ut, ur, vals, qf, qs)
-        G, cnt = oracle.row_grads(m, [ob], ut, ur, ld)
-        oracle.apply_update(G, cnt, vals, acc, lr=0.01, D=ld)
-        spent += time.perf_counter() - t0
-        samples += B
-        steps += 1
-    return {"value": samples / spent, "unit": UNIT, "cores": 1, "kind": "oracle",
+    oracle.use_openmp(openmp)
+    try:
+        m = oracle.OracleModel(cfg.field_to_table, cfg.table_rows, cfg.table_dim, cfg.field_col,
+                               id_mode=cfg.id_mode, pool=cfg.pool, table_salt=cfg.table_salt)
+        B = cfg.batch
+        ld = int(cfg.table_dim.max())
+        spent, samples, steps = 0.0, 0, 0
+        while steps == 0 or (spent < seconds and steps < max_steps):
+            b = make_batch(cfg, 0, 1000 + steps)
+            dy = make_dy(cfg, 0, 1000 + steps, dyadic=False)
+            ob = oracle.OracleBatch(B, b.ids, b.offsets, dy)
+            qf = np.repeat(np.arange(cfg.F, dtype=np.int32), B)
+            qs = np.tile(np.arange(B, dtype=np.int32), cfg.F)
+            rt, rr = oracle.segment_rows(m, ob, qf, qs)
+            key = np.unique(rt.astype(np.int64) * (1 << 40) + rr)
+            ut, ur = (key >> 40).astype(np.int32), key & ((1 << 40) - 1)
+            vals = np.zeros((len(key), ld), np.float32)
+            for t in np.unique(ut):
+                sel = ut == t
+                D = int(cfg.table_dim[t])
+                vals[sel, :D] = table_values_np(cfg.seed, int(t), ur[sel], D)
+            acc = np.full_like(vals, 0.1)
+            t0 = time.perf_counter()
+            oracle.forward_sampled(m, ob, ut, ur, vals, qf, qs)
+            G, cnt = oracle.row_grads(m, [ob], ut, ur, ld)
+            oracle.apply_update(G, cnt, vals, acc, lr=0.01, D=ld)
+            spent += time.perf_counter() - t0
+            samples += B
+            steps += 1
+    finally:
+        oracle.use_openmp(False)
+    cores, model = host_cpu()
+    used = cores if openmp else 1
+    how = f"OpenMP build on all {cores} host cores" if openmp else "single-threaded"
+    return {"value": samples / spent, "unit": UNIT, "cores": used, "kind": "oracle", "cpu_model": model,
+            "host_cores": cores,
             "sample": f"{steps} full batch(es) of {cfg.name} (B={B}, {cfg.F} fields): fwd over all segments, "
-                      f"grads + Adagrad over all touched rows; {spent:.1f} s single-threaded C++ (-O2)"}
+                      f"grads + Adagrad over all touched rows; {spent:.1f} s, {how} C++ (-O2)"}
 
 
 def run_reference(args):
+    """The reference arm: the oracle (the paper has no code) on every host core, one whole batch
+    of the same workload per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = get_cfg(args)
     per = []
-    # bounded: one batch per step; warmup steps untimed
+    cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_oracle_baseline(cfg, seconds=0.0)  # exactly one batch per call
+        cb = cpu_oracle_baseline(cfg, seconds=0.0, openmp=True)  # exactly one batch per call
         if i >= args.warmup:
             per.append(cfg.batch / cb["value"])
     tot = float(np.sum(per))
@@ -176,8 +213,10 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "global_batch": cfg.batch, "fields": cfg.F,
                        "dims": sorted(set(cfg.table_dim.tolist())), "alpha": cfg.alpha},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{len(per)} full batches of {cfg.name}, single thread"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
+                             "cpu_model": cb["cpu_model"],
+                             "sample": f"{len(per)} full batches of {cfg.name}, OpenMP oracle build on all "
+                                       f"{cb['cores']} host cores"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -204,10 +243,124 @@ def algorithmic_bytes(cfg, B, N, U_by_pack, plan, world=1):
     }
 
 
+def run_micro(args):
+    """D-Interleaving: the step's batch in micro-batches (Eq. 2 or a fixed
+    count), each forwarded + accumulated, one update per step; the whole micro-batched step is
+    one CUDA graph.  Reports the step time of the whole batch and the device memory of the
+    batch-proportional buffers (ctx workspace + out + dY) against the one-shot step's."""
+    import torch
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2204_04903_b200 as pb
+    from paper_2204_04903_b200 import dinterleave as di
+    from datagen import init_pack_tables_torch, make_batch, make_dy
+
+    cfg = get_cfg(args)
+    B = cfg.batch
+    batches = [make_batch(cfg, 0, s) for s in range(args.nbatches)]
+    max_ids = max(b.n_ids for b in batches)
+    kw = dict(pool=cfg.pool, id_mode=cfg.id_mode, table_salt=cfg.table_salt, field_col=cfg.field_col)
+    if args.micro == "auto":
+        plan = pb.picasso_pack_plan(cfg.field_to_table, cfg.table_rows, cfg.table_dim)
+        ctx_kw = dict(plan=plan, field_to_table=cfg.field_to_table, table_rows=cfg.table_rows,
+                      table_dim=cfg.table_dim, table_salt=cfg.table_salt, field_col=cfg.field_col,
+                      out_width=cfg.out_width, rank=0, world=1, max_batch=B, max_ids=max_ids)
+        ws_id = di.workspace_bytes_per_id(ctx_kw)
+        ids_ps = max_ids / B  # warm-up measurement: IDs per sample (the largest of the batches)
+        bs, n_micro, ops = di.micro_batch_plan(B, cfg.out_width, cfg.F, ids_ps, ws_id, args.micro_budget_gb * 1e9)
+    else:
+        n_micro, ops = int(args.micro), None
+    sl = di.even_slices(B, n_micro)
+    mb = max(b1 - b0 for b0, b1 in sl)
+    mbs = []  # per batch: per micro-batch (ids, offsets, dY) on the device
+    mb_ids = 0
+    for k, b in enumerate(batches):
+        dy = make_dy(cfg, 0, k, dyadic=False)
+        parts = []
+        for b0, b1 in sl:
+            ids, off = di.slice_batch(b.ids, b.offsets, cfg.F, B, b0, b1)
+            mb_ids = max(mb_ids, len(ids))
+            parts.append((torch.from_numpy(ids).to(dev), torch.from_numpy(off).to(dev),
+                          torch.from_numpy(np.ascontiguousarray(dy[b0:b1])).to(dev), b1 - b0))
+        mbs.append(parts)
+    emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=mb, max_ids=mb_ids,
+                             device=dev, max_step_unique=max_ids, **kw)
+    init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights)
+    outs = [torch.empty(n, emb.out_width, device=dev) for (_, _, _, n) in mbs[0]]
+    lr = 0.01
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k, s, stepno):
+        emb.dinterleave_begin(stream=s)
+        for (ids, off, dy, n), o in zip(mbs[k], outs):
+            emb.forward(ids, off, n, o, stream=s)
+            emb.backward_accumulate(dy, stream=s)
+        emb.dinterleave_apply(lr, step=stepno, stream=s)
+
+    for i in range(max(args.warmup, 1)):
+        step(i % args.nbatches, stream, i + 1)
+    emb.check()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(stream)
+    graphs = []
+    for k in range(args.nbatches):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            step(k, cap, args.warmup + 1)
+        graphs.append(g)
+    stream.wait_stream(cap)
+    for g in graphs:
+        g.replay()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = ClockSampler(0)
+    with clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            st[i].record(stream)
+            graphs[i % args.nbatches].replay()
+            en[i].record(stream)
+        torch.cuda.synchronize()
+    emb.check()
+    ms = float(sum(a.elapsed_time(b) for a, b in zip(st, en))) / args.steps
+    ws_micro = pb.picasso_workspace_size(emb.ctx)
+    io_micro = 2 * 4 * mb * emb.out_width
+    # the one-shot step's batch-proportional buffers (not allocated: workspace size only)
+    c1 = pb.picasso_ctx_create(emb.plan, cfg.field_to_table, cfg.table_rows, cfg.table_dim, cfg.table_salt,
+                               cfg.field_col, emb.out_width, 0, 1, B, max_ids)
+    ws_full = pb.picasso_workspace_size(c1)
+    pb.picasso_ctx_destroy(c1)
+    line = {"metric": METRIC, "value": B / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": B, "fields": cfg.F, "rows": int(cfg.table_rows.sum()),
+                       "alpha": cfg.alpha, "optimizer": "adagrad", "parallelism": "single",
+                       "l2": "flushed (256 MiB write, untimed) before every timed step",
+                       "launch": "cuda_graph (one captured micro-batched step per batch)"},
+            "dinterleave": {"n_micro": n_micro, "bs_micro": mb, "micro_batch_ids_max": mb_ids,
+                            "eq2_ops": ops, "budget_gb": args.micro_budget_gb if args.micro == "auto" else None,
+                            "batch_buffers_bytes": {"micro": int(ws_micro + io_micro),
+                                                    "one_shot": int(ws_full + 2 * 4 * B * emb.out_width)},
+                            "note": "batch-proportional device memory = ctx workspace (incl. the step "
+                                    "accumulator in micro mode) + out + dY"},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.micro:
+        run_micro(args)
         return
     import torch
     import torch.distributed as dist
@@ -280,21 +433,31 @@ def main():
     # steps records them (same graph without vs with the event nodes; eager: profiling on), and
     # its step time is reported beside the timed one.
     use_graph = not args.eager and (world == 1 or (emb.exchange == "p2p" and not args.cache_bytes))
-    graphs = {}
+    graphs, graphs_t = {}, []
     if use_graph:
-        ids0, off0 = dev_in[0]
+        # timed pass: one captured step per pre-generated batch (--nbatches), replayed round robin;
+        # profiled pass: batch 0's step with the phase-event nodes
         cap = torch.cuda.Stream(dev)
         cap.wait_stream(stream)
-        for prof in (0, 2):
-            pb.picasso_profile_enable(emb.ctx, prof)
+        for k in range(args.nbatches):
+            ids_k, off_k = dev_in[k]
+            pb.picasso_profile_enable(emb.ctx, 0)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=cap):
-                emb.forward(ids0, off0, B, out, stream=cap)
-                emb.backward_update(dys[0], lr, step=args.warmup + 1, stream=cap)
-            graphs[prof] = g
+                emb.forward(ids_k, off_k, B, out, stream=cap)
+                emb.backward_update(dys[k], lr, step=args.warmup + 1, stream=cap)
+            graphs_t.append(g)
+        ids0, off0 = dev_in[0]
+        pb.picasso_profile_enable(emb.ctx, 2)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            emb.forward(ids0, off0, B, out, stream=cap)
+            emb.backward_update(dys[0], lr, step=args.warmup + 1, stream=cap)
+        graphs[2] = g
         stream.wait_stream(cap)  # profiling stays in graph mode (2): phase events read after replays
         for _ in range(2):  # warm replays
-            graphs[0].replay()
+            for gt in graphs_t:
+                gt.replay()
             graphs[2].replay()
         torch.cuda.synchronize()
         pb.picasso_profile_read(emb.ctx)
@@ -321,7 +484,7 @@ def main():
             flush.fill_(i & 0xFF)
             starts[i].record(stream)
             if use_graph:
-                graphs[2 if profiled else 0].replay()
+                (graphs[2] if profiled else graphs_t[i % len(graphs_t)]).replay()
             else:
                 step(next_i[0], stream)
                 next_i[0] += 1
@@ -439,7 +602,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_baseline(cfg, args.cpu_seconds)
+        # all host cores (the OpenMP build), and the plain single-threaded oracle beside it
+        cpu = cpu_oracle_baseline(cfg, args.cpu_seconds / 2, openmp=True)
+        one = cpu_oracle_baseline(cfg, args.cpu_seconds / 2, openmp=False)
+        cpu["single_thread"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
 
     if rank == 0:
         line = {
@@ -453,7 +619,9 @@ def main():
                        "exchange": emb.exchange if world > 1 else None,
                        "packs": emb.n_packs, "k_interleave_groups": kgroups if world > 1 else None,
                        "l2": "flushed (256 MiB write, untimed) before every timed step",
-                       "launch": "cuda_graph (one captured step, replayed)" if use_graph else "eager",
+                       "launch": (f"cuda_graph (one captured step per batch, {args.nbatches} distinct batches "
+                                  "replayed round robin)") if use_graph else "eager",
+                       "nbatches": args.nbatches,
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

@@ -25,14 +25,31 @@ POOL_SUM, POOL_MEAN = 0, 1
 OPT_ADAGRAD, OPT_ADAM = 0, 1
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle with g++ (-O2, no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
+def build(force: bool = False, openmp: bool = False) -> str:
+    """Compile the oracle with g++ (-O2, no FMA contraction, no fast-math).  openmp=True builds
+    the same source with -fopenmp (liboracle_omp.so): the loops bench.py's all-cores CPU
+    baseline times are split over threads with every per-row / per-segment sum in the same
+    sequential order, so its results are bitwise those of the plain build (pinned in
+    tests/test_oracle_pins.py).  Tests use the plain build."""
+    lib_path = _LIB_OMP if openmp else _LIB
+    if force or not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(_SRC):
         cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-               "-shared", "-Wall", "-o", _LIB + ".tmp", _SRC]
+               "-shared", "-Wall", *(["-fopenmp"] if openmp else []), "-o", lib_path + ".tmp", _SRC]
         subprocess.check_call(cmd)
-        os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+        os.replace(lib_path + ".tmp", lib_path)
+    return lib_path
+
+
+_use_openmp = False
+
+
+def use_openmp(on: bool = True):
+    """Route the wrappers below to the -fopenmp build (bench.py's all-cores baseline) or back."""
+    global _use_openmp
+    _use_openmp = bool(on)
 
 
 class Model(C.Structure):
@@ -52,14 +69,12 @@ class Opt(C.Structure):
                 ("beta1", C.c_float), ("beta2", C.c_float)]
 
 
-_lib = None
+_libs = {}
 
 
 def lib():
-    global _lib
-    if _lib is None:
-        _lib = C.CDLL(build())
-        L = _lib
+    if _use_openmp not in _libs:
+        _libs[_use_openmp] = L = C.CDLL(build(openmp=_use_openmp))
         L.oracle_mix64.restype = C.c_uint64
         L.oracle_mix64.argtypes = [C.c_uint64]
         L.oracle_row_of.restype = C.c_int32
@@ -103,7 +118,7 @@ def lib():
                                         C.c_uint64, C.c_void_p]
         L.oracle_fcounter_add.restype = C.c_int32
         L.oracle_fcounter_add.argtypes = [C.c_int64, C.c_void_p, C.c_void_p]
-    return _lib
+    return _libs[_use_openmp]
 
 
 def _p(a):

@@ -29,6 +29,9 @@
  * torch.nn.functional.embedding_bag, torch.optim.Adagrad / SparseAdam sparse paths,
  * SplitMix64 published known-answer vectors, the paper's four-shard example.
  */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -266,6 +269,10 @@ int32_t oracle_forward_sampled(const oracle_model *m, const oracle_batch *bt, in
     where.reserve((size_t)n_rows * 2 + 1);
     for (int64_t i = 0; i < n_rows; ++i) where[((uint64_t)r_table[i] << 48) ^ (uint64_t)r_row[i]] = i;
     const int32_t B = bt->batch;
+    int32_t status = OR_OK;
+    /* the segments are independent: the all-cores baseline build (-fopenmp, bench.py) splits them
+     * over threads; every segment's sum is the same sequential loop either way */
+#pragma omp parallel for schedule(dynamic, 64)
     for (int64_t q = 0; q < n_q; ++q) {
         const int32_t f = q_field[q], b = q_sample[q], t = m->field_to_table[f];
         const int32_t D = m->table_dim[t];
@@ -274,10 +281,15 @@ int32_t oracle_forward_sampled(const oracle_model *m, const oracle_batch *bt, in
             float acc = 0.0f;
             for (int32_t j = s0; j < s1; ++j) {
                 int64_t row;
-                if (oracle_row_of(m->id_mode, bt->ids[j], m->table_salt ? m->table_salt[t] : 0, m->table_rows[t], &row))
-                    return OR_ID_RANGE;
+                if (oracle_row_of(m->id_mode, bt->ids[j], m->table_salt ? m->table_salt[t] : 0, m->table_rows[t], &row)) {
+                    status = OR_ID_RANGE;
+                    break;
+                }
                 auto it = where.find(((uint64_t)t << 48) ^ (uint64_t)row);
-                if (it == where.end()) return OR_MISMATCH;
+                if (it == where.end()) {
+                    status = OR_MISMATCH;
+                    break;
+                }
                 acc = acc + r_val[it->second * ld + d];
             }
             const int32_t len = s1 - s0;
@@ -285,7 +297,7 @@ int32_t oracle_forward_sampled(const oracle_model *m, const oracle_batch *bt, in
             out_q[q * ld + d] = acc;
         }
     }
-    return OR_OK;
+    return status;
 }
 
 /* ------------------------------------------------------------------------------------ */
@@ -493,34 +505,49 @@ int32_t oracle_row_grads(const oracle_model *m, int32_t R, const oracle_batch *b
         where[((uint64_t)q_table[q] << 48) ^ (uint64_t)q_row[q]] = q;
         count[q] = 0;
     }
-    for (int32_t r = 0; r < R; ++r) {
-        const oracle_batch *bt = &batches[r];
-        const int32_t B = bt->batch;
-        for (int32_t f = 0; f < m->n_fields; ++f) {
-            const int32_t t = m->field_to_table[f];
-            const int32_t D = m->table_dim[t];
-            for (int32_t b = 0; b < B; ++b) {
-                const int32_t s0 = bt->offsets[(int64_t)f * B + b], s1 = bt->offsets[(int64_t)f * B + b + 1];
-                const int32_t len = s1 - s0;
-                for (int32_t j = s0; j < s1; ++j) {
-                    int64_t row;
-                    if (oracle_row_of(m->id_mode, bt->ids[j], m->table_salt ? m->table_salt[t] : 0,
-                                      m->table_rows[t], &row))
-                        return OR_ID_RANGE;
-                    auto it = where.find(((uint64_t)t << 48) ^ (uint64_t)row);
-                    if (it == where.end()) continue;
-                    const float *dy = bt->dy + (int64_t)b * bt->dy_stride + m->field_col[f];
-                    double *g = G64.data() + it->second * ld;
-                    for (int32_t d = 0; d < D; ++d) {
-                        float c = dy[d];
-                        if (m->pool == OR_POOL_MEAN) c = c / (float)len;
-                        g[d] = g[d] + (double)c;
+    int32_t status = OR_OK;
+    /* the all-cores baseline build (-fopenmp, bench.py): every thread scans all occurrences in
+     * the order above but accumulates only the queried rows it owns (q mod threads), so each
+     * row's sum keeps the sequential order; without OpenMP this is the plain loop (1 thread) */
+#pragma omp parallel
+    {
+        int nth = 1, tid = 0;
+#ifdef _OPENMP
+        nth = omp_get_num_threads();
+        tid = omp_get_thread_num();
+#endif
+        for (int32_t r = 0; r < R; ++r) {
+            const oracle_batch *bt = &batches[r];
+            const int32_t B = bt->batch;
+            for (int32_t f = 0; f < m->n_fields; ++f) {
+                const int32_t t = m->field_to_table[f];
+                const int32_t D = m->table_dim[t];
+                for (int32_t b = 0; b < B; ++b) {
+                    const int32_t s0 = bt->offsets[(int64_t)f * B + b], s1 = bt->offsets[(int64_t)f * B + b + 1];
+                    const int32_t len = s1 - s0;
+                    for (int32_t j = s0; j < s1; ++j) {
+                        int64_t row;
+                        if (oracle_row_of(m->id_mode, bt->ids[j], m->table_salt ? m->table_salt[t] : 0,
+                                          m->table_rows[t], &row)) {
+                            status = OR_ID_RANGE;
+                            continue;
+                        }
+                        auto it = where.find(((uint64_t)t << 48) ^ (uint64_t)row);
+                        if (it == where.end() || it->second % nth != tid) continue;
+                        const float *dy = bt->dy + (int64_t)b * bt->dy_stride + m->field_col[f];
+                        double *g = G64.data() + it->second * ld;
+                        for (int32_t d = 0; d < D; ++d) {
+                            float c = dy[d];
+                            if (m->pool == OR_POOL_MEAN) c = c / (float)len;
+                            g[d] = g[d] + (double)c;
+                        }
+                        count[it->second] += 1;
                     }
-                    count[it->second] += 1;
                 }
             }
         }
     }
+    if (status != OR_OK) return status;
     for (size_t i = 0; i < G64.size(); ++i) G[i] = (float)G64[i];
     return OR_OK;
 }
@@ -528,7 +555,8 @@ int32_t oracle_row_grads(const oracle_model *m, int32_t R, const oracle_batch *b
 /* Apply the optimizer to n rows given G (rows with count 0 are left untouched). */
 int32_t oracle_apply_update(const oracle_opt *opt, int64_t step, int64_t n, int32_t D, int64_t ld,
                             const float *G, const int64_t *count, float *w, float *s1, float *s2) {
-    for (int64_t i = 0; i < n; ++i) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {  /* rows are independent (all-cores build: split over threads) */
         if (count && count[i] == 0) continue;
         update_row(opt, step, D, G + i * ld, w + i * ld, s1 + i * ld, s2 ? s2 + i * ld : nullptr);
     }

@@ -545,3 +545,37 @@ def test_near_cancelling_gradient_is_the_rounded_exact_sum():
     for v in vals:
         run = np.float32(run + v)
     assert run != ref  # the plain fp32 running sum misses it: the case reading O6 fixes
+
+
+# ---------------------------------------------------------------- the all-cores baseline build
+def test_openmp_build_is_bitwise_the_plain_oracle():
+    """bench.py's all-cores CPU baseline runs the oracle built with -fopenmp; its sampled forward,
+    row gradients and update must be bitwise those of the plain build (same per-row order)."""
+    cfg = dc.scaled(dc.wdl(), batch=64, rows_div=2000)
+    b, dy = make_batch(cfg, 0, 0), make_dy(cfg, 0, 0, dyadic=False)
+    res = []
+    for omp in (False, True):
+        oracle.use_openmp(omp)
+        try:
+            m = oracle.OracleModel(cfg.field_to_table, cfg.table_rows, cfg.table_dim, cfg.field_col,
+                                   id_mode=cfg.id_mode, pool=cfg.pool, table_salt=cfg.table_salt)
+            ob = oracle.OracleBatch(cfg.batch, b.ids, b.offsets, dy)
+            qf = np.repeat(np.arange(cfg.F, dtype=np.int32), cfg.batch)
+            qs = np.tile(np.arange(cfg.batch, dtype=np.int32), cfg.F)
+            rt, rr = oracle.segment_rows(m, ob, qf, qs)
+            key = np.unique(rt.astype(np.int64) * (1 << 40) + rr)
+            ut, ur = (key >> 40).astype(np.int32), key & ((1 << 40) - 1)
+            ld = int(cfg.table_dim.max())
+            vals = np.zeros((len(key), ld), np.float32)
+            for t in np.unique(ut):
+                sel = ut == t
+                vals[sel, :cfg.table_dim[t]] = table_values_np(cfg.seed, int(t), ur[sel], int(cfg.table_dim[t]))
+            out = oracle.forward_sampled(m, ob, ut, ur, vals, qf, qs)
+            G, cnt = oracle.row_grads(m, [ob], ut, ur, ld)
+            acc = np.full_like(vals, 0.1)
+            oracle.apply_update(G, cnt, vals, acc, lr=0.01, D=ld)
+            res.append((out, G, cnt, vals, acc))
+        finally:
+            oracle.use_openmp(False)
+    for a, c in zip(*res):
+        assert np.array_equal(a, c)
