@@ -287,20 +287,40 @@ def run_micro(args):
             parts.append((torch.from_numpy(ids).to(dev), torch.from_numpy(off).to(dev),
                           torch.from_numpy(np.ascontiguousarray(dy[b0:b1])).to(dev), b1 - b0))
         mbs.append(parts)
-    emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=mb, max_ids=mb_ids,
-                             device=dev, max_step_unique=max_ids, **kw)
-    init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights)
-    outs = [torch.empty(n, emb.out_width, device=dev) for (_, _, _, n) in mbs[0]]
     lr = 0.01
     stream = torch.cuda.current_stream(dev)
+    state = {}
 
     def step(k, s, stepno):
+        emb = state["emb"]
         emb.dinterleave_begin(stream=s)
-        for (ids, off, dy, n), o in zip(mbs[k], outs):
+        for (ids, off, dy, n), o in zip(mbs[k], state["outs"]):
             emb.forward(ids, off, n, o, stream=s)
             emb.backward_accumulate(dy, stream=s)
         emb.dinterleave_apply(lr, step=stepno, stream=s)
 
+    def make(msu, msf):
+        e = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=mb, max_ids=mb_ids,
+                               device=dev, max_step_unique=msu, max_step_floats=msf, **kw)
+        init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights)
+        state["emb"] = e
+        state["outs"] = [torch.empty(n, e.out_width, device=dev) for (_, _, _, n) in mbs[0]]
+        return e
+
+    # warm-up measurement of the step accumulator (L419-421): one step per batch with a generous
+    # accumulator, then the layer is rebuilt with the measured distinct keys / values (+ 15 %)
+    emb = make(max_ids, 0)
+    rows = floats = 0
+    for k in range(args.nbatches):
+        step(k, stream, k + 1)
+        r, f = emb.dinterleave_stats()
+        rows, floats = max(rows, r), max(floats, f)
+    emb.check()
+    emb.close()
+    del emb, state["emb"]
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    emb = make(int(rows * 1.15) + 64, int(floats * 1.15) + 256)
     for i in range(max(args.warmup, 1)):
         step(i % args.nbatches, stream, i + 1)
     emb.check()
@@ -345,6 +365,7 @@ def run_micro(args):
                        "l2": "flushed (256 MiB write, untimed) before every timed step",
                        "launch": "cuda_graph (one captured micro-batched step per batch)"},
             "dinterleave": {"n_micro": n_micro, "bs_micro": mb, "micro_batch_ids_max": mb_ids,
+                            "step_distinct_keys": int(rows), "step_accumulator_values": int(floats),
                             "eq2_ops": ops, "budget_gb": args.micro_budget_gb if args.micro == "auto" else None,
                             "batch_buffers_bytes": {"micro": int(ws_micro + io_micro),
                                                     "one_shot": int(ws_full + 2 * 4 * B * emb.out_width)},

@@ -112,8 +112,10 @@ typedef struct {
                               live in the IPC window, not the workspace), 1 = NCCL AllToAllv
                               (section 5; loopback: device copies) */
     int64_t max_step_unique; /* world == 1: D-Interleaving (section 8) — distinct keys one step's
-                              micro-batches may touch together (sizes the step accumulator:
-                              16 B index slots x 2, max_step_unique x max dim fp64); 0 = off */
+                              micro-batches may touch together (sizes the step accumulator's
+                              index: 2 x 16 B per key); 0 = off */
+    int64_t max_step_floats; /* D-Interleaving: fp64 accumulator values (sum of D over the step's
+                              distinct keys); 0 = max_step_unique x the largest pack dim */
     int32_t cold_tier;       /* world == 1: 1 = HybridHash with a host-DRAM cold tier (section 9):
                               the packs' weights / state passed to picasso_bind live in pinned,
                               device-mapped host memory and up to cache_max_bytes of their
@@ -300,6 +302,9 @@ picasso_status picasso_micro_batch_size(int32_t n_ops, const double *rbound, con
 picasso_status picasso_dinterleave_begin(picasso_ctx *ctx, void *stream);
 picasso_status picasso_packed_lookup_bwd_accumulate(picasso_ctx *ctx, const float *grad_out, void *stream);
 picasso_status picasso_dinterleave_apply(picasso_ctx *ctx, float lr, int64_t step, void *stream);
+/* The last D-Interleaving step's accumulator use (synchronises): distinct keys and fp64 values
+ * (host int64) — the warm-up measurement that sizes max_step_unique / max_step_floats. */
+picasso_status picasso_dinterleave_stats(picasso_ctx *ctx, int64_t *rows, int64_t *floats);
 
 /* 7. Exchange over NVLink peer memory (kernel-initiated Shuffle&Stitch).
  * Replaces the NCCL AllToAllv of section 5 with one shared window per rank (barrier flags,

@@ -24,7 +24,7 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_get_owner_unique", "picasso_get_send_counts", "picasso_hot_cache_refresh",
            "picasso_group_hot_cache_refresh", "picasso_get_hot_keys", "picasso_p2p_handle", "picasso_p2p_open",
            "picasso_group_p2p", "picasso_get_send_list", "picasso_micro_batch_size", "picasso_dinterleave_begin",
-           "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply"]
+           "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply", "picasso_dinterleave_stats"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -45,7 +45,7 @@ class CtxOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_ids", C.c_int64), ("pool", C.c_int32), ("id_mode", C.c_int32),
                 ("opt", C.c_int32), ("eps", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("max_recv", C.c_int64), ("cache_max_bytes", C.c_int64), ("exchange", C.c_int32),
-                ("max_step_unique", C.c_int64), ("cold_tier", C.c_int32)]
+                ("max_step_unique", C.c_int64), ("max_step_floats", C.c_int64), ("cold_tier", C.c_int32)]
 
 
 class CacheStats(C.Structure):
@@ -99,6 +99,7 @@ def lib():
             "picasso_dinterleave_begin": [vp, vp],
             "picasso_packed_lookup_bwd_accumulate": [vp, vp, vp],
             "picasso_dinterleave_apply": [vp, C.c_float, i64, vp],
+            "picasso_dinterleave_stats": [vp, C.POINTER(i64), C.POINTER(i64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -164,7 +165,7 @@ def picasso_nccl_unique_id():
 def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, field_col, out_width, rank, world,
                        max_batch, max_ids, pool=POOL_SUM, id_mode=IDS_HASH, opt=OPT_ADAGRAD, eps=None, beta1=0.9,
                        beta2=0.999, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange="p2p", max_step_unique=0,
-                       cold_tier=0):
+                       max_step_floats=0, cold_tier=0):
     k = _Keep()
     k.f2t = _np(field_to_table, np.int32)
     k.t2p = _np(plan["table_to_pack"], np.int32)
@@ -180,7 +181,7 @@ def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, 
         eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
     o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),
                 float(beta2), int(max_recv), int(cache_max_bytes), 0 if exchange == "p2p" else 1, int(max_step_unique),
-                int(cold_tier))
+                int(max_step_floats), int(cold_tier))
     ctx = C.c_void_p()
     uid = None if nccl_uid is None else (C.c_uint8 * 128)(*nccl_uid)
     _chk(lib().picasso_ctx_create(C.byref(pv), int(rank), int(world), uid, C.byref(o), C.byref(ctx)),
@@ -450,3 +451,10 @@ def picasso_packed_lookup_bwd_accumulate(ctx, grad_out, stream=None, batch=None,
 
 def picasso_dinterleave_apply(ctx, lr, step, stream=None):
     _chk(lib().picasso_dinterleave_apply(ctx, float(lr), int(step), _stream(stream)), "picasso_dinterleave_apply", ctx)
+
+
+def picasso_dinterleave_stats(ctx):
+    """(distinct keys, fp64 values) the last D-Interleaving step accumulated."""
+    r, f = C.c_int64(), C.c_int64()
+    _chk(lib().picasso_dinterleave_stats(ctx, C.byref(r), C.byref(f)), "picasso_dinterleave_stats", ctx)
+    return r.value, f.value

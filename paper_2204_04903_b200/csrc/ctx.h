@@ -178,7 +178,8 @@ struct picasso_ctx {
     bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
     int overlap_env = -1;   // PICASSO_OVERLAP (0 / 1) if set; else chosen per world == 1 forward
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share
-    bool early_pool = false;  // W = 1: pool concurrently with the dedup + transpose chain
+    bool early_pool = false;  // W = 1: this forward pools concurrently with the dedup + transpose chain
+    int early_env = -1;       // PICASSO_EARLY_POOL (0 / 1) if set; else on below kOverlapMinIds IDs
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fp = nullptr, ev_seg = nullptr;
     cudaStream_t side2 = nullptr;  // K-Interleaving: the pools / owner updates beside the exchange
@@ -301,7 +302,7 @@ struct picasso_ctx {
         if (world == 1 && opts.max_step_unique > 0) {  // D-Interleaving step accumulator
             di_cap = pow2_at_least((uint64_t)opts.max_step_unique * 2);
             di_table = c.take<Slot>(di_cap);
-            di_acc_cap4 = opts.max_step_unique * (maxD / 4);
+            di_acc_cap4 = opts.max_step_floats > 0 ? (opts.max_step_floats + 3) / 4 : opts.max_step_unique * (maxD / 4);
             di_acc = c.take<double>((size_t)di_acc_cap4 * 4);
             di_off = c.take<int64_t>(N);
             di_list = c.take<int32_t>(opts.max_step_unique);

@@ -300,3 +300,14 @@ extern "C" picasso_status picasso_dinterleave_apply(picasso_ctx *ctx, float lr, 
     ctx->last_stream = s;
     return PICASSO_OK;
 }
+
+extern "C" picasso_status picasso_dinterleave_stats(picasso_ctx *ctx, int64_t *rows, int64_t *floats) {
+    if (!ctx || !rows || !floats) return PICASSO_ERR_INVALID_ARG;
+    if (!ctx->bound || !ctx->di_counters) return PICASSO_ERR_STATE;
+    DCK(cudaStreamSynchronize(ctx->last_stream));
+    unsigned long long c[2];
+    DCK(cudaMemcpy(c, ctx->di_counters, sizeof(c), cudaMemcpyDeviceToHost));
+    *rows = (int64_t)c[0];
+    *floats = (int64_t)c[1] * 4;
+    return PICASSO_OK;
+}

@@ -41,6 +41,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (world < 1 || world > 8 || rank < 0 || rank >= world) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_batch <= 0 || opts->max_ids < 0 || opts->max_ids >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_recv < 0 || opts->max_recv >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
+    if (opts->max_step_floats < 0 || opts->max_step_floats / 4 >= (int64_t)1 << 31) return PICASSO_ERR_INVALID_ARG;
     if (opts->max_step_unique < 0 || opts->max_step_unique >= (int64_t)1 << 31 ||
         (opts->max_step_unique > 0 && world != 1))
         return PICASSO_ERR_INVALID_ARG;
@@ -156,18 +157,22 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_OVERLAP")) c->overlap_env = std::strcmp(e, "0") != 0;
     if (c->overlap_env >= 0) c->overlap = c->overlap_env;
     if (const char *e = std::getenv("PICASSO_KINTERLEAVE")) c->kinterleave = std::atoi(e);
-    // SMs the world == 1 pool leaves to the index + transpose chain running beside it on the
-    // internal stream (measured best on B200 at C2: 48 of 148; PICASSO_POOL_RESERVE overrides)
-    // Off by default: the step is ~8 % faster (C2: 0.294 -> 0.270 ms) but the pool, sharing the
-    // GPU, then runs at ~3.1 TB/s instead of 4.2 (PICASSO_EARLY_POOL=1 turns it on).
-    if (const char *e = std::getenv("PICASSO_EARLY_POOL")) c->early_pool = std::strcmp(e, "0") != 0;
-    c->pool_reserve = (world == 1 && c->early_pool) ? 48 : 0;
+    // World == 1: the pool needs only the raw IDs (row = h(id)), so by default it starts at once
+    // and streams rows on the caller's stream while the Unique chain and the backward's transpose
+    // run beside it on the internal stream (C2: 0.291 -> 0.271 ms / step, round-2 measurement;
+    // the pool alone then runs slower, ~3.1 TB/s, sharing the SMs).  The pool leaves 48 of 148
+    // SMs to that chain (measured best at C2; PICASSO_POOL_RESERVE overrides).
+    // PICASSO_EARLY_POOL=0: the serial order (dedup, then pool).
+    // Chosen per forward (below kOverlapMinIds IDs; at C3's 83.5 M IDs the early pool measured
+    // slower, 26.3 vs 25.6 ms, and the transpose alone goes beside the pool instead).
+    if (const char *e = std::getenv("PICASSO_EARLY_POOL")) c->early_env = std::strcmp(e, "0") != 0;
+    c->pool_reserve = 48;
     if (const char *e = std::getenv("PICASSO_POOL_RESERVE")) c->pool_reserve = std::atoi(e);
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     c->seg_nt = c->num_sms * segsum_pipe_warps(c->seg_cfg);
-    c->pool_sms = std::max(c->num_sms / 2, c->num_sms - (c->overlap ? c->pool_reserve : 0));
+    c->pool_sms = c->num_sms;
     c->ws_bytes = c->carve(nullptr);
     *out = c;
     return PICASSO_OK;
@@ -405,7 +410,11 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     // the persistent pool (one CTA per SM, static tiles) waits for SMs the transpose's blocks
     // hold, and the serial order is faster (C2: 0.283 vs 0.294 ms; C3, 83.5 M IDs: 26.2 vs
     // 26.6 ms the other way round).  PICASSO_OVERLAP=0/1 forces either; the early pool needs it.
+    ctx->early_pool = ctx->early_env >= 0 ? ctx->early_env != 0 : n_ids < kOverlapMinIds;
     if (ctx->overlap_env < 0) ctx->overlap = ctx->early_pool || n_ids >= kOverlapMinIds;
+    ctx->pool_sms = (ctx->early_pool && ctx->overlap && ctx->side)
+                        ? std::max(ctx->num_sms / 2, ctx->num_sms - ctx->pool_reserve)
+                        : ctx->num_sms;
     if (ctx->overlap && ctx->side && ctx->early_pool) {
         // At world == 1 the pool needs only the raw IDs (row = h(id)), not the dedup: the index
         // work (Unique, inverse) and the backward's transpose run on the internal stream while

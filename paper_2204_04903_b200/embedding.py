@@ -27,7 +27,7 @@ class PackedEmbedding:
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
                  init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange=None, all_gather=None,
-                 max_step_unique=0):
+                 max_step_unique=0, max_step_floats=0):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -45,7 +45,7 @@ class PackedEmbedding:
                                           self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
                                           eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv,
                                           cache_max_bytes=cache_max_bytes, exchange=self.exchange,
-                                          max_step_unique=max_step_unique)
+                                          max_step_unique=max_step_unique, max_step_floats=max_step_floats)
         P = self.plan["n_packs"]
         self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
         ws = abi.picasso_workspace_size(self.ctx)
@@ -108,6 +108,9 @@ class PackedEmbedding:
     def dinterleave_apply(self, lr: float, step: int | None = None, stream=None):
         self.step = self.step + 1 if step is None else step
         abi.picasso_dinterleave_apply(self.ctx, lr, self.step, stream)
+
+    def dinterleave_stats(self):
+        return abi.picasso_dinterleave_stats(self.ctx)
 
     def check(self):
         st, msg = abi.picasso_last_error(self.ctx)
