@@ -69,15 +69,16 @@ def init_pack_tables_torch(cfg, table_to_pack, table_base, n_packs, weights, ran
     tb = np.asarray(table_base)
     for p in range(n_packs):
         W = weights[p]
+        dev = W.device if W.is_cuda else torch.device("cuda", torch.cuda.current_device())  # host tables: made on the GPU
         tabs = np.nonzero(t2p == p)[0]
         tabs = tabs[np.argsort(tb[tabs], kind="stable")]
-        bases = torch.tensor(tb[tabs], dtype=torch.int64, device=W.device)
-        tids = torch.tensor(tabs, dtype=torch.int64, device=W.device)
+        bases = torch.tensor(tb[tabs], dtype=torch.int64, device=dev)
+        tids = torch.tensor(tabs, dtype=torch.int64, device=dev)
         n, D = W.shape
         for s in range(0, n, chunk_rows):
             e = min(n, s + chunk_rows)
-            lr = torch.arange(s, e, device=W.device, dtype=torch.int64)
+            lr = torch.arange(s, e, device=dev, dtype=torch.int64)
             key = lr * world + rank
             ti = torch.searchsorted(bases, key, right=True) - 1
             row = key - bases[ti]
-            W[s:e] = table_values_torch(cfg.seed, tids[ti], row, D)
+            W[s:e] = table_values_torch(cfg.seed, tids[ti], row, D).to(W.device)

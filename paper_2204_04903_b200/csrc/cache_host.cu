@@ -253,12 +253,16 @@ int64_t kc_for(picasso_ctx *ctx, size_t capacity) {
 }  // namespace
 
 // ---- NCCL: one rank per process -----------------------------------------------------------
+picasso_status ct_refresh(picasso_ctx *ctx, size_t capacity, cudaStream_t s, picasso_cache_stats *stats);  // coldtier.cu
+picasso_status ct_hot_keys(picasso_ctx *ctx, int32_t *pack, int64_t *key, int64_t cap, int64_t *n);
+
 extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t capacity_bytes, void *stream,
                                                     picasso_cache_stats *stats) {
     if (!ctx) return PICASSO_ERR_INVALID_ARG;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     picasso_status st = check_refresh_args(ctx, capacity_bytes);
     if (st) return st;
+    if (ctx->world == 1 && ctx->opts.cold_tier) return ct_refresh(ctx, capacity_bytes, s, stats);  // host-DRAM tier
     if (ctx->world == 1 || ctx->opts.cache_max_bytes <= 0) {  // no shard to skip: the table is the hot storage
         if (stats) *stats = picasso_cache_stats{0, 0, 0, 0, 0.0};
         return PICASSO_OK;
@@ -370,6 +374,7 @@ extern "C" picasso_status picasso_group_hot_cache_refresh(picasso_group *g, size
 extern "C" picasso_status picasso_get_hot_keys(picasso_ctx *ctx, int32_t *pack, int64_t *key, int64_t cap,
                                                int64_t *n) {
     if (!ctx || !n) return PICASSO_ERR_INVALID_ARG;
+    if (ctx->opts.cold_tier) return ct_hot_keys(ctx, pack, key, cap, n);
     MultiState &mp = ctx->mp;
     *n = mp.hot_k;
     if (mp.hot_k == 0 || !pack || !key) return PICASSO_OK;

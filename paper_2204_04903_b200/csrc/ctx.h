@@ -242,7 +242,23 @@ struct picasso_ctx {
     int64_t *di_off = nullptr;             // [max_ids] arena offset of each uid of the micro-batch
     int32_t *di_list = nullptr;            // [max_step_unique] index slot of every accumulated row
     unsigned long long *di_counters = nullptr;  // [2] rows, arena used
-    float **di_w = nullptr, **di_s1 = nullptr, **di_s2 = nullptr;  // [P] device copies of the pointers
+    float **di_w = nullptr, **di_s1 = nullptr, **di_s2 = nullptr;  // [P] device copies of the pack pointers
+                                                                    // (D-Interleaving and the cold tier)
+    // HybridHash with a host-DRAM cold tier (coldtier.cu), world == 1
+    uint32_t *ct_fcnt = nullptr;           // [ct_rows_total] FCounter by global key
+    Slot *ct_index = nullptr;              // HStore index: key -> slot
+    uint32_t ct_mask = 0;
+    unsigned long long *ct_keys = nullptr; // [ct_kmax] global key of each hot slot (pack-major)
+    float *ct_arena = nullptr;             // HStore rows: w of every pack, then s1, then s2
+    int32_t *ct_pslot_d = nullptr;         // [P+1]
+    int64_t *ct_arena_off_d = nullptr;     // [3P]
+    int32_t *ct_hslot = nullptr;           // [max_ids]
+    int64_t *ct_row_off = nullptr;         // [max_ids]
+    unsigned long long *ct_hits = nullptr, *ct_hist = nullptr, *ct_bsum = nullptr, *ct_sel = nullptr,
+                       *ct_nsel = nullptr;
+    int64_t ct_kmax = 0, ct_rows_total = 0;
+    int32_t ct_k = 0;
+    std::vector<int32_t> ct_pslot;
     bool di_active = false;
     int64_t di_micro = 0;
 
@@ -307,9 +323,32 @@ struct picasso_ctx {
             di_off = c.take<int64_t>(N);
             di_list = c.take<int32_t>(opts.max_step_unique);
             di_counters = c.take<unsigned long long>(2);
+        }
+        if (world == 1 && (opts.max_step_unique > 0 || opts.cold_tier)) {
             di_w = c.take<float *>(P);
             di_s1 = c.take<float *>(P);
             di_s2 = c.take<float *>(P);
+        }
+        if (world == 1 && opts.cold_tier) {  // HStore + FCounter of the host-DRAM cold tier
+            int minD = 1 << 30;
+            for (int32_t d : pack_dim) minD = std::min(minD, d);
+            const int nst = opts.opt == PICASSO_OPT_ADAM_LAZY ? 2 : 1;
+            ct_kmax = std::max<int64_t>(opts.cache_max_bytes / ((int64_t)4 * minD * (1 + nst)), 1);
+            ct_rows_total = pack_key_off.empty() ? 0 : pack_key_off[P];
+            ct_mask = (uint32_t)(pow2_at_least((uint64_t)ct_kmax * 2) - 1);
+            ct_fcnt = c.take<uint32_t>(std::max<int64_t>(ct_rows_total, 1));
+            ct_index = c.take<Slot>((size_t)ct_mask + 1);
+            ct_keys = c.take<unsigned long long>(ct_kmax);
+            ct_arena = c.take<float>(opts.cache_max_bytes / 4 + 4 * P);
+            ct_pslot_d = c.take<int32_t>(P + 1);
+            ct_arena_off_d = c.take<int64_t>(3 * P);
+            ct_hslot = c.take<int32_t>(N);
+            ct_row_off = c.take<int64_t>(N);
+            ct_hits = c.take<unsigned long long>(1);
+            ct_hist = c.take<unsigned long long>(1 << 16);
+            ct_bsum = c.take<unsigned long long>((ct_rows_total + 1023) / 1024 + 1);
+            ct_sel = c.take<unsigned long long>(ct_kmax);
+            ct_nsel = c.take<unsigned long long>(1);
         }
         // rows / G buffer: the IPC window holds it with the peer-memory exchange
         const bool p2p_ex = world > 1 && opts.exchange == 0;

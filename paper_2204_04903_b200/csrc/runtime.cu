@@ -46,6 +46,8 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
         (opts->max_step_unique > 0 && world != 1))
         return PICASSO_ERR_INVALID_ARG;
     if (opts->cold_tier < 0 || opts->cold_tier > 1 || (opts->cold_tier && world != 1)) return PICASSO_ERR_INVALID_ARG;
+    if (opts->cold_tier && opts->max_step_unique > 0) return PICASSO_ERR_INVALID_ARG;  // not combined (yet)
+    if (opts->cache_max_bytes < 0) return PICASSO_ERR_INVALID_ARG;
     if (opts->pool < 0 || opts->pool > 1 || opts->id_mode < 0 || opts->id_mode > 1 || opts->opt < 0 || opts->opt > 1 ||
         opts->exchange < 0 || opts->exchange > 1)
         return PICASSO_ERR_INVALID_ARG;
@@ -234,7 +236,15 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_dim_d, ctx->pack_dim.data(), sizeof(int32_t) * ctx->P, cudaMemcpyHostToDevice));
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
-    if (ctx->di_w) {  // D-Interleaving: the apply kernel reaches every pack's rows
+    if (ctx->ct_fcnt) {  // cold tier: FCounter zero, HStore empty
+        CK(cudaMemset(ctx->ct_fcnt, 0, sizeof(uint32_t) * std::max<int64_t>(ctx->ct_rows_total, 1)));
+        CK(cudaMemset(ctx->ct_index, 0xFF, sizeof(Slot) * ((size_t)ctx->ct_mask + 1)));
+        CK(cudaMemset(ctx->ct_pslot_d, 0, sizeof(int32_t) * (ctx->P + 1)));
+        CK(cudaMemset(ctx->ct_arena_off_d, 0, sizeof(int64_t) * 3 * ctx->P));
+        ctx->ct_k = 0;
+        ctx->ct_pslot.assign(ctx->P + 1, 0);
+    }
+    if (ctx->di_w) {  // D-Interleaving / cold tier: kernels reach every pack's rows
         CK(cudaMemcpy(ctx->di_w, ctx->w.data(), sizeof(float *) * ctx->P, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->di_s1, ctx->s1.data(), sizeof(float *) * ctx->P, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->di_s2, ctx->s2.data(), sizeof(float *) * ctx->P, cudaMemcpyHostToDevice));
@@ -331,6 +341,9 @@ picasso_status multi_bwd_nccl(picasso_ctx *ctx, const float *grad_out, float lr,
 picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
                              float *out, cudaStream_t s);
 picasso_status multi_bwd_p2p(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
+picasso_status ct_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t batch, int64_t n_ids,
+                      float *out, cudaStream_t s);  // coldtier.cu
+picasso_status ct_bwd(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
 
 static IndexArgs index_args(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N) {
     return picasso::make_index_args(ctx, ids, offsets, B, N);
@@ -399,6 +412,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
         return ctx->mp.p2p ? multi_fwd_p2p(ctx, ids, offsets, batch, n_ids, out, s)
                            : multi_fwd_nccl(ctx, ids, offsets, batch, n_ids, out, s);
     }
+    if (ctx->opts.cold_tier) return ct_fwd(ctx, ids, offsets, batch, n_ids, out, s);
     IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
     const uint32_t cap_step =
         (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
@@ -491,6 +505,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
         if (!ctx->mp.comm && (!ctx->mp.p2p || ctx->opts.cache_max_bytes > 0)) return PICASSO_ERR_STATE;
         return ctx->mp.p2p ? multi_bwd_p2p(ctx, grad_out, lr, step, s) : multi_bwd_nccl(ctx, grad_out, lr, step, s);
     }
+    if (ctx->opts.cold_tier) return ct_bwd(ctx, grad_out, lr, step, s);
     const int64_t N = ctx->N;
     ctx->mark(3, true, s);  // the transpose ran in the forward (transpose_fork)
     UpdateArgs u = picasso::make_update_args(ctx, grad_out, lr, step, ctx->su, ctx->sseg);

@@ -27,7 +27,7 @@ class PackedEmbedding:
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
                  init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange=None, all_gather=None,
-                 max_step_unique=0, max_step_floats=0):
+                 max_step_unique=0, max_step_floats=0, cold_tier=False):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -45,19 +45,25 @@ class PackedEmbedding:
                                           self.out_width, rank, world, max_batch, max_ids, pool, id_mode, opt,
                                           eps, beta1, beta2, nccl_uid=nccl_uid, max_recv=max_recv,
                                           cache_max_bytes=cache_max_bytes, exchange=self.exchange,
-                                          max_step_unique=max_step_unique, max_step_floats=max_step_floats)
+                                          max_step_unique=max_step_unique, max_step_floats=max_step_floats,
+                                          cold_tier=int(bool(cold_tier)))
+        self.cold_tier = bool(cold_tier)
         P = self.plan["n_packs"]
         self.local_rows = [abi.picasso_pack_local_rows(self.ctx, p) for p in range(P)]
         ws = abi.picasso_workspace_size(self.ctx)
         self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=self.device)
-        self.weights = [torch.zeros(max(r, 1), int(self.plan["pack_dim"][p]), dtype=torch.float32,
-                                    device=self.device) for p, r in enumerate(self.local_rows)]
-        if opt == abi.OPT_ADAGRAD:
-            self.state1 = [torch.full_like(w, init_acc) for w in self.weights]
-            self.state2 = None
-        else:
-            self.state1 = [torch.zeros_like(w) for w in self.weights]
-            self.state2 = [torch.zeros_like(w) for w in self.weights]
+        # cold tier (HybridHash with host-DRAM Cold-storage): the tables and their
+        # optimizer state live in pinned host memory the GPU maps; HBM holds only the hot rows
+        def table(p, r, fill):
+            shape = (max(r, 1), int(self.plan["pack_dim"][p]))
+            if self.cold_tier:
+                return torch.empty(shape, dtype=torch.float32, pin_memory=True).fill_(fill)
+            return torch.full(shape, fill, dtype=torch.float32, device=self.device)
+
+        rows = list(enumerate(self.local_rows))
+        self.weights = [table(p, r, 0.0) for p, r in rows]
+        self.state1 = [table(p, r, init_acc if opt == abi.OPT_ADAGRAD else 0.0) for p, r in rows]
+        self.state2 = None if opt == abi.OPT_ADAGRAD else [table(p, r, 0.0) for p, r in rows]
         abi.picasso_bind(self.ctx, self.workspace, self.weights, self.state1, self.state2)
         self.step = 0
         # world > 1, one process per GPU: the exchange runs over NVLink peer memory ("p2p", the
