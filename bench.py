@@ -43,10 +43,15 @@ def parse():
     ap.add_argument("--nbatches", type=int, default=4, help="distinct pre-generated batches, used round robin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--cache-bytes", type=int, default=0, help="HybridHash hot storage per GPU (N > 1)")
+    ap.add_argument("--cache-bytes", type=int, default=0,
+                    help="HybridHash hot storage per GPU (N > 1, or N = 1 with --cold-tier)")
     ap.add_argument("--cache-warmup", type=int, default=3, help="Alg. 1 warmup_iters")
     ap.add_argument("--cache-flush", type=int, default=10, help="Alg. 1 flush_iters")
     ap.add_argument("--eager", action="store_true", help="N = 1: launch every step eagerly instead of a CUDA graph")
+    ap.add_argument("--cold-tier", action="store_true",
+                    help="N = 1: HybridHash with a host-DRAM cold tier (tables in pinned host memory, "
+                         "--cache-bytes of hot rows in HBM, Alg. 1 with --cache-warmup / --cache-flush); "
+                         "prints its own JSON line")
     ap.add_argument("--micro", default=None,
                     help="N = 1: D-Interleaving with this many micro-batches per step, or 'auto' (Eq. 2 "
                          "from --micro-budget-gb); prints its own JSON line")
@@ -375,10 +380,103 @@ def run_micro(args):
     print(json.dumps(line), flush=True)
 
 
+def run_coldtier(args):
+    """HybridHash with DRAM as Cold-storage: the tables and Adagrad state in
+    pinned host memory, --cache-bytes of the hottest rows (FCounter top-k) in HBM.  Alg. 1 schedule:
+    FCounter from the first iteration, refresh after the backward of every itr >= warmup with
+    itr % flush == 0 (reading O13).  Eager launches (a refresh changes the hot set the kernels are
+    launched with); the timed K steps include their refreshes."""
+    import torch
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2204_04903_b200 as pb
+    from datagen import init_pack_tables_torch, make_batch, make_dy
+
+    cfg = get_cfg(args)
+    B = cfg.batch
+    batches = [make_batch(cfg, 0, s) for s in range(args.nbatches)]
+    max_ids = max(b.n_ids for b in batches)
+    t0 = time.time()
+    emb = pb.PackedEmbedding(cfg.field_to_table, cfg.table_rows, cfg.table_dim, max_batch=B, max_ids=max_ids,
+                             table_salt=cfg.table_salt, field_col=cfg.field_col, pool=cfg.pool, id_mode=cfg.id_mode,
+                             device=dev, cold_tier=True, cache_max_bytes=max(args.cache_bytes, 1024))
+    init_pack_tables_torch(cfg, emb.plan["table_to_pack"], emb.plan["table_base"], emb.n_packs, emb.weights)
+    setup_s = time.time() - t0
+    dev_in = [(torch.from_numpy(b.ids).to(dev), torch.from_numpy(b.offsets).to(dev)) for b in batches]
+    dys = [torch.from_numpy(make_dy(cfg, 0, s, dyadic=False)).to(dev) for s in range(args.nbatches)]
+    out = torch.empty(B, emb.out_width, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    stats = {}
+    refresh_ms = []
+
+    def step(itr):
+        ids, off = dev_in[itr % args.nbatches]
+        emb.forward(ids, off, B, out, stream=stream)
+        emb.backward_update(dys[itr % args.nbatches], 0.01, step=itr + 1, stream=stream)
+        if args.cache_bytes > 0 and itr >= args.cache_warmup and itr % args.cache_flush == 0:
+            st = emb.hot_cache_refresh(args.cache_bytes, stream=stream)
+            stats.update(st)
+            refresh_ms.append(st["refresh_ms"])
+
+    itr = 0
+    warm = max(args.warmup, args.cache_warmup + args.cache_flush + 1) if args.cache_bytes else args.warmup
+    for _ in range(warm):
+        step(itr)
+        itr += 1
+    emb.check()
+    torch.cuda.synchronize()
+    refresh_ms.clear()
+    st_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    en_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    hot_hits = []
+    clk = ClockSampler(0)
+    with clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            st_ev[i].record(stream)
+            step(itr)
+            itr += 1
+            en_ev[i].record(stream)
+        torch.cuda.synchronize()
+    emb.check()
+    ms = float(sum(a.elapsed_time(b) for a, b in zip(st_ev, en_ev))) / args.steps
+    U = int(np.diff(np.array(emb.unique_offsets_host(), np.int64)).sum())
+    nst = 1
+    row_b = [4 * int(d) for d in emb.plan["pack_dim"]]
+    hit = stats.get("hit_ratio_unique", 0.0)
+    line = {"metric": METRIC, "value": B / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": B, "fields": cfg.F, "rows": int(cfg.table_rows.sum()),
+                       "alpha": cfg.alpha, "optimizer": "adagrad", "parallelism": "single",
+                       "tables": "pinned host memory (Cold-storage), device-mapped",
+                       "l2": "flushed (256 MiB write, untimed) before every timed step", "launch": "eager"},
+            "cold_tier": {"cache_bytes": args.cache_bytes, "warmup_iters": args.cache_warmup,
+                          "flush_iters": args.cache_flush, "hot_rows": stats.get("k", 0),
+                          "hit_ratio_unique": hit, "unique_per_step": U,
+                          "refresh_ms_mean": float(np.mean(refresh_ms)) if refresh_ms else None,
+                          "refreshes_in_timed_steps": len(refresh_ms),
+                          "pcie_bytes_per_step_est": int(U * (1 - hit) * row_b[0] * (3 + 2 * nst))
+                          if len(row_b) == 1 else None,
+                          "note": "PCIe estimate: per cold unique row one row read (stage) + w and state read "
+                                  "+ written (update)",
+                          "setup_s": setup_s},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.cold_tier:
+        run_coldtier(args)
         return
     if args.micro:
         run_micro(args)

@@ -94,6 +94,9 @@ typedef struct {
     const int64_t *field_col;      /* [F] first column of field f in the [B, out_width] output
                                       (a multiple of 4) */
     int64_t out_width;             /* row stride of out / dY in floats (multiple of 4) */
+    const int32_t *pack_group;     /* [P] K-Interleaving group of each pack (picasso_pack_plan_kinterleave;
+                                      -1 = preset excluded, ahead of the groups), or NULL: one group per
+                                      pack.  Groups must be contiguous and ascending in pack order. */
 } picasso_plan_view;
 
 typedef struct {
@@ -121,6 +124,32 @@ typedef struct {
                               device-mapped host memory and up to cache_max_bytes of their
                               hottest rows are cached in HBM; 0 = tables in device memory */
 } picasso_ctx_opts;
+
+/* 1b. K-Interleaving plan (Eq. 3).
+ *   picasso_interleave_capacity : Eq. 3, Capacity_g = min over ops of rbound[i] / rparam[i] in
+ *     parameters per step ("we simply treat the parameter volume as the cost in embedding lookup
+ *     and exchange", L437-438): e.g. rbound = bytes an op's dominant resource (HBM, NVLink) moves
+ *     in one interleaving slot at its measured rate, rparam = its bytes per parameter.  Ops with
+ *     rparam 0 never bind; none binding gives +inf.
+ *   picasso_pack_plan_kinterleave : D-Packing (as picasso_pack_plan, split 0) where (1) the tables
+ *     flagged in `excluded` ([T] or NULL) — the paper's "preset excluded embedding", L444-447 —
+ *     form one pack per dim placed first, outside the chain (pack_group -1); (2) every other dim
+ *     group of volume V = sum_t dim_t * count_t (Eq. 1) is cut into min(#tables, ceil(V /
+ *     capacity_g)) packs, tables dealt round-robin by descending dim_t * count_t; (3) those packs
+ *     are joined, in order, into interleaving groups of at most capacity_g parameters (a pack above
+ *     it stays alone).  capacity_g <= 0 or +inf: one pack per dim, one group.  With the peer-memory
+ *     exchange at world > 1 each group has its own barrier: group g's pool (forward) and owner
+ *     update (backward) run beside group g+1's exchange; excluded packs run first and wait on
+ *     no group.  Out: as picasso_pack_plan, plus pack_group [<=T], *n_groups (excluded packs
+ *     not counted). */
+picasso_status picasso_interleave_capacity(int32_t n_ops, const double *rbound, const double *rparam,
+                                           double *capacity);
+picasso_status picasso_pack_plan_kinterleave(int32_t n_fields, const int32_t *field_to_table, int32_t n_tables,
+                                             const int64_t *table_rows, const int32_t *table_dim,
+                                             const uint64_t *table_warmup_count, double capacity_g,
+                                             const uint8_t *excluded, int32_t *field_to_pack, int32_t *table_to_pack,
+                                             int64_t *table_base, int32_t *pack_dim, int64_t *pack_rows,
+                                             int32_t *pack_group, int32_t *n_packs, int32_t *n_groups);
 
 /* NCCL unique id (128 bytes, host) for picasso_ctx_create; rank 0 calls it and broadcasts
  * the bytes to the other ranks (e.g. over torch.distributed). */

@@ -116,6 +116,12 @@ def lib():
         L.oracle_hot_select.restype = C.c_int64
         L.oracle_hot_select.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_uint64, C.c_void_p]
+        L.oracle_interleave_capacity.restype = C.c_double
+        L.oracle_interleave_capacity.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
+        L.oracle_kinterleave_plan.restype = C.c_int32
+        L.oracle_kinterleave_plan.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]
         L.oracle_fcounter_add.restype = C.c_int32
         L.oracle_fcounter_add.argtypes = [C.c_int64, C.c_void_p, C.c_void_p]
     return _libs[_use_openmp]
@@ -321,3 +327,22 @@ def fcounter_add(keys, counts):
     k = _arr(keys, np.int64)
     assert counts.dtype == np.uint64
     _ok(lib().oracle_fcounter_add(len(k), _p(k), _p(counts)))
+
+
+def interleave_capacity(rbound, rparam):
+    rb, rp = _arr(rbound, np.float64), _arr(rparam, np.float64)
+    return lib().oracle_interleave_capacity(len(rb), _p(rb), _p(rp))
+
+
+def kinterleave_plan(field_to_table, table_rows, table_dim, capacity, excluded=None, warmup_count=None):
+    f2t, rows, dims = _arr(field_to_table, np.int32), _arr(table_rows, np.int64), _arr(table_dim, np.int32)
+    T = len(rows)
+    wc = None if warmup_count is None else _arr(warmup_count, np.uint64)
+    ex = None if excluded is None else _arr(excluded, np.uint8)
+    t2p, tb = np.zeros(T, np.int32), np.zeros(T, np.int64)
+    pd, pr, pg = np.zeros(T, np.int32), np.zeros(T, np.int64), np.zeros(T, np.int32)
+    ng = C.c_int32()
+    P = lib().oracle_kinterleave_plan(len(f2t), _p(f2t), T, _p(rows), _p(dims), _p(wc), float(capacity), _p(ex),
+                                      _p(t2p), _p(tb), _p(pd), _p(pr), _p(pg), C.byref(ng))
+    return dict(table_to_pack=t2p, table_base=tb, pack_dim=pd[:P].copy(), pack_rows=pr[:P].copy(), n_packs=P,
+                pack_group=pg[:P].copy(), n_groups=ng.value, field_to_pack=t2p[f2t])

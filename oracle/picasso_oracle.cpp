@@ -301,6 +301,114 @@ int32_t oracle_forward_sampled(const oracle_model *m, const oracle_batch *bt, in
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* K-Interleaving.
+ * Eq. 3 (L433-436): Capacity_g = min_{op in layer} RBound_op / RParam_op, "the parameter volume
+ * as the cost in embedding lookup and exchange" (L437-438): ops with RParam 0 do not bind.  */
+double oracle_interleave_capacity(int32_t n_ops, const double *rbound, const double *rparam) {
+    double c = INFINITY;
+    for (int32_t i = 0; i < n_ops; ++i)
+        if (rparam[i] > 0.0 && rbound[i] / rparam[i] < c) c = rbound[i] / rparam[i];
+    return c;
+}
+
+/* The interleaving plan (reading O22), written out step by step:
+ *  1. the "preset excluded embedding" tables (L444-447) form one pack per dim (ascending dim),
+ *     numbered first, group -1 (no control dependencies on the other groups);
+ *  2. every other dim group (ascending dim) has parameter volume V = sum_t dim_t * count_t (Eq. 1,
+ *     count_t as in oracle_pack_plan); it becomes min(#tables, ceil(V / Capacity_g)) packs (1 if
+ *     Capacity_g is not a positive finite number), tables dealt round-robin in descending
+ *     dim_t * count_t (ties: ascending index) — each pack a packed operation within the capacity;
+ *  3. groups of packed operations (L427-432): the packs, in order, are joined into a group while
+ *     its volume stays <= Capacity_g; a pack that does not fit starts the next group;
+ *  4. table_base: running row sum in ascending table index within each pack.
+ * Returns the number of packs; *n_groups receives the number of groups (excluded packs not
+ * counted). */
+int32_t oracle_kinterleave_plan(int32_t n_fields, const int32_t *field_to_table, int32_t n_tables,
+                                const int64_t *table_rows, const int32_t *table_dim,
+                                const uint64_t *warmup_count, double capacity, const uint8_t *excluded,
+                                int32_t *table_to_pack, int64_t *table_base, int32_t *pack_dim,
+                                int64_t *pack_rows, int32_t *pack_group, int32_t *n_groups) {
+    std::vector<double> cnt(n_tables, 0.0);
+    for (int32_t f = 0; f < n_fields; ++f) cnt[field_to_table[f]] += 1.0;
+    if (warmup_count)
+        for (int32_t t = 0; t < n_tables; ++t) cnt[t] = (double)warmup_count[t];
+    std::vector<int32_t> dims;
+    for (int32_t t = 0; t < n_tables; ++t) dims.push_back(table_dim[t]);
+    std::sort(dims.begin(), dims.end());
+    dims.erase(std::unique(dims.begin(), dims.end()), dims.end());
+    std::vector<double> pvol;
+    int32_t P = 0;
+    /* step 1 */
+    for (int32_t d : dims) {
+        bool any = false;
+        double v = 0.0;
+        for (int32_t t = 0; t < n_tables; ++t)
+            if (excluded && excluded[t] && table_dim[t] == d) {
+                table_to_pack[t] = P;
+                v += (double)table_dim[t] * cnt[t];
+                any = true;
+            }
+        if (any) {
+            pack_dim[P] = d;
+            pack_group[P] = -1;
+            pvol.push_back(v);
+            ++P;
+        }
+    }
+    const int32_t n_ex = P;
+    /* step 2 */
+    for (int32_t d : dims) {
+        std::vector<int32_t> ord;
+        double V = 0.0;
+        for (int32_t t = 0; t < n_tables; ++t)
+            if (!(excluded && excluded[t]) && table_dim[t] == d) {
+                ord.push_back(t);
+                V += (double)table_dim[t] * cnt[t];
+            }
+        if (ord.empty()) continue;
+        int32_t shards = 1;
+        if (capacity > 0.0 && std::isfinite(capacity)) {
+            double q = std::ceil(V / capacity);
+            shards = (int32_t)std::min<double>((double)ord.size(), q);
+            if (shards < 1) shards = 1;
+        }
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+            double va = (double)table_dim[a] * cnt[a], vb = (double)table_dim[b] * cnt[b];
+            if (va != vb) return va > vb;
+            return a < b;
+        });
+        for (int32_t s = 0; s < shards; ++s) {
+            pack_dim[P + s] = d;
+            pvol.push_back(0.0);
+        }
+        for (size_t i = 0; i < ord.size(); ++i) {
+            table_to_pack[ord[i]] = P + (int32_t)(i % shards);
+            pvol[P + (int32_t)(i % shards)] += (double)table_dim[ord[i]] * cnt[ord[i]];
+        }
+        P += shards;
+    }
+    /* step 3 */
+    int32_t g = -1;
+    double in_group = 0.0;
+    for (int32_t p = n_ex; p < P; ++p) {
+        if (g == -1 || (in_group > 0.0 && in_group + pvol[p] > capacity)) {
+            g += 1;
+            in_group = 0.0;
+        }
+        pack_group[p] = g;
+        in_group += pvol[p];
+    }
+    *n_groups = g + 1;
+    /* step 4 */
+    for (int32_t p = 0; p < P; ++p) pack_rows[p] = 0;
+    for (int32_t t = 0; t < n_tables; ++t) {
+        table_base[t] = pack_rows[table_to_pack[t]];
+        pack_rows[table_to_pack[t]] += table_rows[t];
+    }
+    return P;
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* Intermediates of the packed operation (bit-exact targets).
  * Key stream of pack p on one rank (reading O2): the pack's fields in ascending field
  * index, then sample b, then j; key = table_base[t] + row. */

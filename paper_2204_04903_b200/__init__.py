@@ -40,6 +40,8 @@ from .abi import (  # noqa: F401
     picasso_packed_lookup_bwd_accumulate,
     picasso_dinterleave_apply,
     picasso_dinterleave_stats,
+    picasso_interleave_capacity,
+    picasso_pack_plan_kinterleave,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
 from .embedding import LoopbackGroup, PackedEmbedding  # noqa: F401

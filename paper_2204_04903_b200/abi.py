@@ -24,7 +24,8 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_get_owner_unique", "picasso_get_send_counts", "picasso_hot_cache_refresh",
            "picasso_group_hot_cache_refresh", "picasso_get_hot_keys", "picasso_p2p_handle", "picasso_p2p_open",
            "picasso_group_p2p", "picasso_get_send_list", "picasso_micro_batch_size", "picasso_dinterleave_begin",
-           "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply", "picasso_dinterleave_stats"]
+           "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply", "picasso_dinterleave_stats",
+           "picasso_interleave_capacity", "picasso_pack_plan_kinterleave"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -38,7 +39,7 @@ class PlanView(C.Structure):
     _fields_ = [("n_fields", C.c_int32), ("n_tables", C.c_int32), ("n_packs", C.c_int32),
                 ("field_to_table", C.c_void_p), ("table_to_pack", C.c_void_p), ("table_base", C.c_void_p),
                 ("table_rows", C.c_void_p), ("table_dim", C.c_void_p), ("table_salt", C.c_void_p),
-                ("field_col", C.c_void_p), ("out_width", C.c_int64)]
+                ("field_col", C.c_void_p), ("out_width", C.c_int64), ("pack_group", C.c_void_p)]
 
 
 class CtxOpts(C.Structure):
@@ -100,6 +101,9 @@ def lib():
             "picasso_packed_lookup_bwd_accumulate": [vp, vp, vp],
             "picasso_dinterleave_apply": [vp, C.c_float, i64, vp],
             "picasso_dinterleave_stats": [vp, C.POINTER(i64), C.POINTER(i64)],
+            "picasso_interleave_capacity": [i32, vp, vp, C.POINTER(C.c_double)],
+            "picasso_pack_plan_kinterleave": [i32, vp, i32, vp, vp, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp,
+                                              C.POINTER(i32), C.POINTER(i32)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -152,6 +156,37 @@ def picasso_pack_plan(field_to_table, table_rows, table_dim, table_warmup_count=
                 pack_rows=pr[:P].copy(), n_packs=P)
 
 
+def picasso_interleave_capacity(rbound, rparam):
+    """Eq. 3: Capacity_g = min over ops of rbound / rparam (parameters per step)."""
+    rb, rp = _np(rbound, np.float64), _np(rparam, np.float64)
+    c = C.c_double()
+    _chk(lib().picasso_interleave_capacity(len(rb), rb.ctypes.data, rp.ctypes.data, C.byref(c)),
+         "picasso_interleave_capacity")
+    return c.value
+
+
+def picasso_pack_plan_kinterleave(field_to_table, table_rows, table_dim, capacity_g, excluded=None,
+                                  table_warmup_count=None):
+    """The K-Interleaving plan (include/picasso.h 1b): picasso_pack_plan's dict plus pack_group
+    (-1 = preset excluded) and n_groups."""
+    f2t, rows, dims = _np(field_to_table, np.int32), _np(table_rows, np.int64), _np(table_dim, np.int32)
+    wc = None if table_warmup_count is None else _np(table_warmup_count, np.uint64)
+    ex = None if excluded is None else _np(excluded, np.uint8)
+    F, T = len(f2t), len(rows)
+    f2p, t2p = np.zeros(F, np.int32), np.zeros(T, np.int32)
+    tb, pd, pr, pg = np.zeros(T, np.int64), np.zeros(T, np.int32), np.zeros(T, np.int64), np.zeros(T, np.int32)
+    n, g = C.c_int32(), C.c_int32()
+    st = lib().picasso_pack_plan_kinterleave(F, f2t.ctypes.data, T, rows.ctypes.data, dims.ctypes.data,
+                                             None if wc is None else wc.ctypes.data, float(capacity_g),
+                                             None if ex is None else ex.ctypes.data, f2p.ctypes.data,
+                                             t2p.ctypes.data, tb.ctypes.data, pd.ctypes.data, pr.ctypes.data,
+                                             pg.ctypes.data, C.byref(n), C.byref(g))
+    _chk(st, "picasso_pack_plan_kinterleave")
+    P = n.value
+    return dict(field_to_pack=f2p, table_to_pack=t2p, table_base=tb, pack_dim=pd[:P].copy(),
+                pack_rows=pr[:P].copy(), n_packs=P, pack_group=pg[:P].copy(), n_groups=g.value)
+
+
 class _Keep:
     """Keeps numpy arrays referenced by a C struct alive."""
 
@@ -174,9 +209,10 @@ def picasso_ctx_create(plan, field_to_table, table_rows, table_dim, table_salt, 
     k.dims = _np(table_dim, np.int32)
     k.salt = _np(np.zeros(len(k.rows)) if table_salt is None else table_salt, np.uint64)
     k.col = _np(field_col, np.int64)
+    k.pg = None if plan.get("pack_group") is None else _np(plan["pack_group"], np.int32)
     pv = PlanView(len(k.f2t), len(k.rows), int(plan["n_packs"]), k.f2t.ctypes.data, k.t2p.ctypes.data,
                   k.tb.ctypes.data, k.rows.ctypes.data, k.dims.ctypes.data, k.salt.ctypes.data, k.col.ctypes.data,
-                  int(out_width))
+                  int(out_width), None if k.pg is None else k.pg.ctypes.data)
     if eps is None:
         eps = 1e-10 if opt == OPT_ADAGRAD else 1e-8
     o = CtxOpts(int(max_batch), int(max_ids), int(pool), int(id_mode), int(opt), float(eps), float(beta1),

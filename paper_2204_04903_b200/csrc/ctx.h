@@ -131,6 +131,8 @@ struct picasso_ctx {
     std::vector<uint64_t> tsalt;
     int64_t out_width = 0;
     std::vector<int32_t> pm_fields, pack_first_k;
+    std::vector<int32_t> pack_slot;  // [P] K-Interleaving barrier slot (excluded packs, then groups)
+    int32_t n_slots = 0;
     // workspace layout
     size_t ws_bytes = 0;
     uint32_t cap = 0;

@@ -160,9 +160,11 @@ void wait_group(picasso_ctx *ctx, int phase, int group, cudaStream_t s) {
 // (forward) and owner update (backward); one barrier per (phase, pack).  Needs >= 2 packs, no
 // HybridHash, one process per GPU.
 bool interleaved(const picasso_ctx *ctx) {
-    return ctx->kinterleave && ctx->P >= 2 && ctx->P <= kP2PMaxGroups && ctx->opts.cache_max_bytes == 0 &&
+    return ctx->kinterleave && ctx->n_slots >= 2 && ctx->n_slots <= kP2PMaxGroups && ctx->opts.cache_max_bytes == 0 &&
            !ctx->mp.p2p_loop && ctx->side2;
 }
+// last pack of its barrier slot (a group's packs are contiguous)
+bool slot_end(const picasso_ctx *ctx, int p) { return p + 1 == ctx->P || ctx->pack_slot[p + 1] != ctx->pack_slot[p]; }
 
 // ---- C': owner side --------------------------------------------------------------------------
 picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
@@ -184,12 +186,16 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
         PCK(cudaEventRecord(ctx->ev_fork2, s));
         PCK(cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0));
     }
+    int nsig = 0;
     for (int p = 0; p < P; ++p) {
         launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
-        if (kil) signal_group(ctx, 1, p, s);  // pack p's rows are in every requester's buffer
+        if (kil && slot_end(ctx, p)) {  // the slot's rows are in every requester's buffer
+            signal_group(ctx, 1, ctx->pack_slot[p], s);
+            ++nsig;
+        }
     }
     if (!split) ctx->mark(4, false, s);
-    ctx->launches_fwd += 4 + P * (kil ? 2 : 1);
+    ctx->launches_fwd += 4 + P + nsig;
     PCK(cudaGetLastError());
     return PICASSO_OK;
 }
@@ -263,9 +269,12 @@ picasso_status multi_fwd_p2p(picasso_ctx *ctx, const int64_t *ids, const int32_t
     pa.inverse = ctx->inverse;
     cudaStream_t t = ctx->side2;
     for (int p = 0; p < ctx->P; ++p) {
-        wait_group(ctx, 1, p, t);
+        if (p == 0 || ctx->pack_slot[p] != ctx->pack_slot[p - 1]) {  // the slot's first pack
+            wait_group(ctx, 1, ctx->pack_slot[p], t);
+            ctx->launches_fwd += 1;
+        }
         ctx->mark(1, true, t);
-        ctx->launches_fwd += 1 + launch_pool_all(ctx, pa, out, t, p);
+        ctx->launches_fwd += launch_pool_all(ctx, pa, out, t, p);
         ctx->mark(1, false, t);
     }
     PCK(cudaEventRecord(ctx->ev_join2, t));
@@ -287,19 +296,24 @@ picasso_status multi_bwd_p2p(picasso_ctx *ctx, const float *grad_out, float lr, 
         ctx->mark(3, true, s);
         for (int p = 0; p < ctx->P; ++p) {
             ctx->launches_bwd += mbwd_segsum_pack(ctx, u, p, s);
-            signal_group(ctx, 2, p, s);
+            if (slot_end(ctx, p)) {
+                signal_group(ctx, 2, ctx->pack_slot[p], s);
+                ctx->launches_bwd += 1;
+            }
         }
         ctx->mark(3, false, s);
         const P2PArgs a = make_p2p_args(ctx);
         const float ss = adam_step(ctx, lr, step);
         cudaStream_t t = ctx->side2;
         for (int p = 0; p < ctx->P; ++p) {
-            wait_group(ctx, 2, p, t);
+            if (p == 0 || ctx->pack_slot[p] != ctx->pack_slot[p - 1]) {
+                wait_group(ctx, 2, ctx->pack_slot[p], t);
+                ctx->launches_bwd += 1;
+            }
             ctx->mark(5, true, t);
             p2p_update_pack(ctx, a, p, lr, ss, t);
             ctx->mark(5, false, t);
         }
-        ctx->launches_bwd += 2 * ctx->P;
         PCK(cudaEventRecord(ctx->ev_join2, t));
         PCK(cudaStreamWaitEvent(s, ctx->ev_join2, 0));
         if (ctx->prof) ++ctx->prof_calls;

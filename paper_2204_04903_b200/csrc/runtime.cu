@@ -76,6 +76,28 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (plan->table_salt) c->tsalt.assign(plan->table_salt, plan->table_salt + c->T);
     c->fcol.assign(plan->field_col, plan->field_col + c->F);
     c->out_width = plan->out_width;
+    // K-Interleaving barrier slots: every preset-excluded pack (-1) its own slot, first; then one slot
+    // per group, groups contiguous and ascending in pack order
+    c->pack_slot.assign(c->P, 0);
+    {
+        int32_t nex = 0, last = -1;
+        bool grouped = false;
+        for (int32_t p = 0; p < c->P; ++p) {
+            const int32_t g = plan->pack_group ? plan->pack_group[p] : p;
+            if (g < 0) {
+                if (grouped) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }  // excluded packs come first
+                c->pack_slot[p] = nex++;
+                continue;
+            }
+            if (g != last && g != last + 1) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
+            grouped = true;
+            last = g;
+            c->pack_slot[p] = g;  // + nex below
+        }
+        for (int32_t p = 0; p < c->P; ++p)
+            if (!plan->pack_group || plan->pack_group[p] >= 0) c->pack_slot[p] += nex;
+        c->n_slots = c->P ? c->pack_slot[c->P - 1] + 1 : 0;
+    }
     // validate plan: tables tile each pack's key range, dims agree, columns fit
     c->pack_dim.assign(c->P, -1);
     c->pack_rows.assign(c->P, 0);

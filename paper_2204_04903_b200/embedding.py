@@ -27,7 +27,7 @@ class PackedEmbedding:
                  field_col=None, pool=abi.POOL_SUM, id_mode=abi.IDS_HASH, opt=abi.OPT_ADAGRAD, eps=None,
                  beta1=0.9, beta2=0.999, split=False, warmup_count=None, rank=0, world=1, device="cuda",
                  init_acc=0.1, nccl_uid=None, max_recv=0, cache_max_bytes=0, exchange=None, all_gather=None,
-                 max_step_unique=0, max_step_floats=0, cold_tier=False):
+                 max_step_unique=0, max_step_floats=0, cold_tier=False, plan=None):
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
@@ -36,7 +36,9 @@ class PackedEmbedding:
                           else np.asarray(field_col, np.int64))
         self.out_width = int(max(self.field_col + fd)) if len(fd) else 0
         self.out_width = (self.out_width + 3) // 4 * 4
-        self.plan = abi.picasso_pack_plan(self.f2t, self.rows, self.dims, warmup_count, split)
+        # plan: a precomputed plan dict (e.g. picasso_pack_plan_kinterleave's, with pack_group)
+        self.plan = plan if plan is not None else abi.picasso_pack_plan(self.f2t, self.rows, self.dims,
+                                                                        warmup_count, split)
         self.opt = opt
         self.rank, self.world = rank, world
         self.exchange = exchange or default_exchange()

@@ -45,6 +45,14 @@ def main():
         cfg = dc.scaled(dc.wdl(), batch=32, rows_div=2000)
     else:
         cfg = dc.scaled(dc.wdl(), batch=32, rows_div=2000)
+    kplan = None
+    if base == "wdlk":  # K-Interleaving plan (Eq. 3): groups of several packs + preset-excluded packs first
+        ex = np.zeros(cfg.T, np.uint8)
+        ex[::9] = 1
+        vol = float((cfg.table_dim.astype(np.float64) * np.bincount(cfg.field_to_table, minlength=cfg.T)).sum())
+        kplan = pb.picasso_pack_plan_kinterleave(cfg.field_to_table, cfg.table_rows, cfg.table_dim, vol / 4, ex)
+        assert kplan["n_groups"] >= 3 and (kplan["pack_group"] == -1).sum() >= 2
+        assert np.bincount(kplan["pack_group"][kplan["pack_group"] >= 0]).max() >= 2  # a group of >= 2 packs
     bsz = [cfg.batch] * world
     if base == "uneven":
         bsz = [max(cfg.batch - 11 * r, 1) for r in range(world)]
@@ -67,7 +75,7 @@ def main():
                            rank=rank, world=world, nccl_uid=obj[0], max_recv=world * mi,
                            device=torch.device("cuda", local), cache_max_bytes=(1 << 20) if cache else 0,
                            split=2 if base == "criteok2" else False,  # k2: two K-Interleaving groups
-                           all_gather=all_gather)
+                           all_gather=all_gather, plan=kplan)
     init_pack_tables_torch(cfg, e.plan["table_to_pack"], e.plan["table_base"], e.n_packs, e.weights, rank=rank,
                            world=world)
     m, tabs = oracle_model(cfg), oracle_tables(cfg)

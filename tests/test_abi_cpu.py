@@ -93,3 +93,31 @@ def test_ctx_create_validation(pb):
     with pytest.raises(pb.PicassoError):
         pb.picasso_ctx_create(p, cfg.field_to_table, cfg.table_rows, cfg.table_dim, None, cfg.field_col,
                               cfg.out_width, 0, 1, 0, 100)
+
+
+def test_kinterleave_plan_matches_oracle(pb):
+    """picasso_pack_plan_kinterleave (host C++ of the product) == the oracle's plan, bit-exact,
+    on the golden example and on random industrial-shaped configurations."""
+    import json
+
+    import numpy as np
+
+    import oracle
+    from datagen import configs as dc
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "worked_examples.json")))["kinterleave_plan"]
+    assert pb.picasso_interleave_capacity(g["rbound"], g["rparam"]) == g["capacity"]
+    cases = [(g["field_to_table"], g["table_rows"], g["table_dim"], g["capacity"], g["excluded"], None)]
+    cfg = dc.scaled(dc.industrial(), batch=8, rows_div=10**4)
+    rng = np.random.default_rng(11)
+    for _ in range(6):
+        cnt = rng.integers(1, 5000, cfg.T).astype(np.uint64)
+        ex = (rng.random(cfg.T) < 0.15).astype(np.uint8)
+        cap = float(rng.uniform(0.02, 0.6) * (cfg.table_dim * cnt).sum())
+        cases.append((cfg.field_to_table, cfg.table_rows, cfg.table_dim, cap, ex, cnt))
+    for f2t, rows, dims, cap, ex, cnt in cases:
+        a = pb.picasso_pack_plan_kinterleave(f2t, rows, dims, cap, ex, cnt)
+        b = oracle.kinterleave_plan(f2t, rows, dims, cap, ex, cnt)
+        for k in ("table_to_pack", "table_base", "pack_dim", "pack_rows", "pack_group", "field_to_pack"):
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+        assert a["n_groups"] == b["n_groups"] and a["n_packs"] == b["n_packs"]

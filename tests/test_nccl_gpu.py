@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("name", ["toy", "wdl", "toy_cache", "wdl_cache", "criteo", "uneven", "toy_graph",
-                                  "criteo_graph", "criteok2", "criteok2_graph"])
+                                  "criteo_graph", "criteok2", "criteok2_graph", "wdlk", "wdlk_graph"])
 def test_nccl_sharded_parity(name, exchange):
     n = torch.cuda.device_count()
     if n < 2:

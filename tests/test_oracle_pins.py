@@ -579,3 +579,45 @@ def test_openmp_build_is_bitwise_the_plain_oracle():
             oracle.use_openmp(False)
     for a, c in zip(*res):
         assert np.array_equal(a, c)
+
+
+# ---------------------------------------------------------------- K-Interleaving (Eq. 3, reading O22)
+def test_eq3_capacity_and_kinterleave_plan_golden():
+    g = GOLD["kinterleave_plan"]
+    assert oracle.interleave_capacity(g["rbound"], g["rparam"]) == g["capacity"]
+    assert oracle.interleave_capacity([5.0, 7.0], [0.0, 0.0]) == float("inf")  # nothing binds
+    p = oracle.kinterleave_plan(g["field_to_table"], g["table_rows"], g["table_dim"], g["capacity"], g["excluded"])
+    for k in ("table_to_pack", "table_base", "pack_dim", "pack_rows", "pack_group"):
+        assert p[k].tolist() == g[k], k
+    assert p["n_groups"] == g["n_groups"]
+    p40 = oracle.kinterleave_plan(g["field_to_table"], g["table_rows"], g["table_dim"], 40.0, g["excluded"])
+    assert p40["table_to_pack"].tolist() == g["capacity_40"]["table_to_pack"]
+    assert p40["pack_group"].tolist() == g["capacity_40"]["pack_group"]
+
+
+def test_kinterleave_plan_invariants():
+    """Every pack's volume and every group's volume stay within the capacity unless a single table
+    (resp. pack) exceeds it; excluded tables never share a pack with others; no capacity = D-Packing."""
+    cfg = dc.scaled(dc.industrial(), batch=8, rows_div=10**4)
+    rng = np.random.default_rng(3)
+    cnt = rng.integers(1, 1000, cfg.T).astype(np.uint64)
+    vol = cfg.table_dim.astype(float) * cnt
+    ex = (rng.random(cfg.T) < 0.1).astype(np.uint8)
+    for cap in (vol.max() * 0.5, vol.sum() / 7, vol.sum() / 3, float("inf")):
+        p = oracle.kinterleave_plan(cfg.field_to_table, cfg.table_rows, cfg.table_dim, cap, ex, cnt)
+        pv = np.bincount(p["table_to_pack"], weights=vol, minlength=p["n_packs"])
+        ntab = np.bincount(p["table_to_pack"], minlength=p["n_packs"])
+        pg = p["pack_group"]
+        assert (pg[:ex.any() and len(set(cfg.table_dim[ex == 1]))] == -1).all()
+        for q in range(p["n_packs"]):
+            members = np.nonzero(p["table_to_pack"] == q)[0]
+            assert len(set(ex[members])) == 1 and len(set(cfg.table_dim[members])) == 1
+            if pg[q] >= 0 and np.isfinite(cap):  # within capacity, or as small as the dealing allows
+                assert pv[q] <= cap or ntab[q] == 1 or pv[q] <= np.ceil(vol[members].sum() / cap) * cap
+        gv = np.bincount(pg[pg >= 0], weights=pv[pg >= 0])
+        gn = np.bincount(pg[pg >= 0])
+        assert ((gv <= cap) | (gn == 1)).all()
+        assert list(pg[pg >= 0]) == sorted(pg[pg >= 0])  # contiguous, ascending
+    pinf = oracle.kinterleave_plan(cfg.field_to_table, cfg.table_rows, cfg.table_dim, float("inf"), None, cnt)
+    p0 = oracle.pack_plan(cfg.field_to_table, cfg.table_rows, cfg.table_dim, warmup_count=cnt)
+    assert pinf["table_to_pack"].tolist() == p0["table_to_pack"].tolist() and pinf["n_groups"] == 1

@@ -17,9 +17,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("W", [2, 3])
-@pytest.mark.parametrize("name", ["toy", "wdl", "criteo", "uneven", "toy_graph", "criteok2", "criteok2_graph"])
+@pytest.mark.parametrize("name", ["toy", "wdl", "criteo", "uneven", "toy_graph", "criteok2", "criteok2_graph", "wdlk",
+                                  "wdlk_graph"])
 def test_xproc_same_gpu_parity(name, W):
-    if W == 3 and name not in ("toy", "criteok2"):
+    if W == 3 and name not in ("toy", "criteok2", "wdlk"):
         pytest.skip("W = 3 (non-power-of-two owner arithmetic): two cases suffice")
     import __graft_entry__
 
