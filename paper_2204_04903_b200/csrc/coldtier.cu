@@ -16,15 +16,18 @@
 //                  (cold: read-modify-write over PCIe)
 //   refresh (Alg. 1, called by the caller after bwd when itr >= warmup and
 //   itr % flush == 0, reading O13):
-//     k_ct_writeback : HStore rows back to CStore (the host tables are then authoritative)
 //     k_ct_hist      : capacity cost of the rows at each FCounter value
 //     (host)         : the count c* where the prefix of (count desc, pack asc, key asc) — the
 //                      order of oracle_hot_select, reading O12 — stops fitting
 //     k_ct_tiesum / k_ct_scan / k_ct_select : every row above c*, plus the rows at c* in
-//                      ascending global key (= pack asc, key asc) while their cost prefix fits
-//     k_ct_index / k_ct_load : the new HStore index and rows (host -> HBM)
+//                      ascending global key (= pack asc, key asc) while their cost prefix fits,
+//                      compacted in that order (= the new slot order, pack-major)
+//     k_ct_layout / k_ct_index : the new HStore layout and index (a second buffer)
+//     k_ct_merge     : rows staying hot move HBM -> HBM to their new slots, rows entering are
+//                      loaded from CStore, rows leaving are written back to it
 // Results equal the uncached step's ("tier transparency"): a row is updated in exactly one
-// tier, the same arithmetic (optim.cuh), and written back before the hot set changes.
+// tier, with the same arithmetic (optim.cuh), and written back when it leaves HStore (capacity
+// 0 writes every hot row back: the host tables are then authoritative).
 #include <algorithm>
 #include <chrono>
 #include <cstring>
@@ -157,29 +160,6 @@ __global__ void __launch_bounds__(256) k_ct_update(CtArgs a, OptParams o) {
     }
 }
 
-// HStore rows <-> CStore rows, one thread per 4-float chunk of a hot row and state array.
-// dir 0: write back (arena -> host), dir 1: load (host -> arena)
-__global__ void __launch_bounds__(256) k_ct_move(CtArgs a, const unsigned long long *keys, int32_t k, int nst,
-                                                 int maxD, int dir) {
-    const int V4 = maxD / 4;
-    const int64_t n = (int64_t)k * V4 * (1 + nst);
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int arr = (int)(e / ((int64_t)k * V4));
-        const int64_t r = e - (int64_t)arr * k * V4;
-        const int32_t slot = (int32_t)(r / V4);
-        const int c = (int)(r % V4) * 4;
-        const unsigned long long key = keys[slot];
-        const int p = pack_of_gkey(a.pack_key_off, a.P, key);
-        const int D = __ldg(a.pack_dim + p);
-        if (c >= D) continue;
-        const int64_t row = (int64_t)(key - (unsigned long long)__ldg(a.pack_key_off + p));
-        float *host = (arr == 0 ? a.w[p] : arr == 1 ? a.s1[p] : a.s2[p]) + row * D + c;
-        float *hot = a.arena + a.arena_off[arr * a.P + p] + (int64_t)(slot - a.pslot[p]) * D + c;
-        if (dir == 0) *reinterpret_cast<float4 *>(host) = *reinterpret_cast<const float4 *>(hot);
-        else *reinterpret_cast<float4 *>(hot) = *reinterpret_cast<const float4 *>(host);
-    }
-}
-
 // capacity cost of the rows at each FCounter value (bucket kCountBuckets-1 collects the rest)
 __global__ void __launch_bounds__(256) k_ct_hist(const uint32_t *fcnt, int64_t n, const int64_t *pack_key_off, int P,
                                                  const int32_t *pack_dim, int nst, unsigned long long *hist) {
@@ -248,20 +228,20 @@ __global__ void __launch_bounds__(1024) k_ct_scan(unsigned long long *v, int64_t
 }
 
 // the new hot set: every row above c*, and the rows at c* whose cost prefix (ascending global
-// key) fits `rem`; appended in any order (the host sorts them)
+// key) fits `rem`.  Pass 0 counts the taken rows per block; pass 1 (after a scan of the counts)
+// writes them in ascending global key order — the slot order, pack-major.
 __global__ void __launch_bounds__(kTieBlock) k_ct_select(const uint32_t *fcnt, int64_t n, const int64_t *pack_key_off,
                                                          int P, const int32_t *pack_dim, int nst, uint32_t cstar,
                                                          unsigned long long rem, const unsigned long long *boff,
-                                                         unsigned long long *out, unsigned long long *nout,
-                                                         int64_t cap) {
-    __shared__ unsigned long long ws[32];
+                                                         unsigned long long *bcnt, unsigned long long *out,
+                                                         int64_t cap, int pass) {
+    __shared__ unsigned long long ws[32], wt[32];
     const int64_t g = (int64_t)blockIdx.x * kTieBlock + threadIdx.x;
     const uint32_t c = g < n ? fcnt[g] : 0u;
     const uint32_t cb = min(c, (uint32_t)kCountBuckets - 1u);
-    unsigned long long cost = 0;
-    if (c && cb >= cstar) cost = (unsigned long long)(4 * __ldg(pack_dim + pack_of_gkey(pack_key_off, P, g)) * (1 + nst));
     // inclusive prefix of the tie costs inside the block (key order)
-    unsigned long long x = (c && cb == cstar) ? cost : 0ull;
+    unsigned long long x = 0;
+    if (c && cb == cstar) x = (unsigned long long)(4 * __ldg(pack_dim + pack_of_gkey(pack_key_off, P, g)) * (1 + nst));
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -282,9 +262,95 @@ __global__ void __launch_bounds__(kTieBlock) k_ct_select(const uint32_t *fcnt, i
     __syncthreads();
     const unsigned long long incl = boff[blockIdx.x] + (w ? ws[w - 1] : 0ull) + x;
     const bool take = c && (cb > cstar || (cb == cstar && incl <= rem));
-    if (take) {
-        const unsigned long long i = atomicAdd(nout, 1ull);
+    // rank of this row among the block's taken rows
+    const unsigned tm = __ballot_sync(0xffffffffu, take);
+    if (lane == 0) wt[w] = __popc(tm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int k = 0; k < kTieBlock / 32; ++k) {
+            const unsigned long long t = wt[k];
+            wt[k] = run;
+            run += t;
+        }
+        if (pass == 0) bcnt[blockIdx.x] = run;
+    }
+    __syncthreads();
+    if (pass == 1 && take) {
+        const unsigned long long i = bcnt[blockIdx.x] + wt[w] + __popc(tm & ((1u << lane) - 1u));
         if ((int64_t)i < cap) out[i] = (unsigned long long)g;
+    }
+}
+
+// slots of each pack in the new (sorted) hot set, and the arena layout [w | s1 | s2], pack-major
+__global__ void k_ct_layout(const unsigned long long *keys, const unsigned long long *nkeys, const int64_t *pack_key_off,
+                            const int32_t *pack_dim, int P, int nst, int32_t *pslot, int64_t *arena_off) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t k = (int64_t)*nkeys;
+    for (int p = 0; p <= P; ++p) {  // first slot whose key >= pack_key_off[p]
+        const unsigned long long b = p == P ? ~0ull : (unsigned long long)pack_key_off[p];
+        int64_t lo = 0, hi = k;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < b) lo = mid + 1; else hi = mid;
+        }
+        pslot[p] = (int32_t)(p == P ? k : lo);
+    }
+    int64_t off = 0;
+    for (int arr = 0; arr < 3; ++arr)
+        for (int p = 0; p < P; ++p) {
+            arena_off[arr * P + p] = off;
+            if (arr <= nst) off += (int64_t)(pslot[p + 1] - pslot[p]) * pack_dim[p];
+        }
+}
+
+__device__ __forceinline__ int32_t ct_lookup(const Slot *index, uint32_t mask, unsigned long long key) {
+    uint32_t s = slot_hash(key) & mask;
+    for (uint32_t probe = 0; probe <= mask; ++probe) {
+        const unsigned long long k = index[s].key;
+        if (k == key) return (int32_t)index[s].minpos;
+        if (k == kEmptyKey) return -1;
+        s = (s + 1) & mask;
+    }
+    return -1;
+}
+
+// New HStore from the old one (rows staying hot: HBM -> HBM) and from CStore (rows entering:
+// host -> HBM); dir 0 instead writes back the old rows that leave (HBM -> host).  One thread per
+// 4-float chunk of a slot's row in one of the 1 + nst arrays.
+struct CtMerge {
+    const unsigned long long *keys;        // the slots walked (new set for dir 1, old set for dir 0)
+    int32_t k;
+    const Slot *other_index;               // the other set's index (old for dir 1, new for dir 0)
+    uint32_t other_mask;
+    const int32_t *pslot, *other_pslot;
+    const int64_t *aoff, *other_aoff;
+    float *arena, *other_arena;
+};
+__global__ void __launch_bounds__(256) k_ct_merge(CtArgs a, CtMerge m, int nst, int maxD, int dir) {
+    const int V4 = maxD / 4;
+    const int64_t n = (int64_t)m.k * V4 * (1 + nst);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int arr = (int)(e / ((int64_t)m.k * V4));
+        const int64_t r = e - (int64_t)arr * m.k * V4;
+        const int32_t slot = (int32_t)(r / V4);
+        const int c = (int)(r % V4) * 4;
+        const unsigned long long key = m.keys[slot];
+        const int p = pack_of_gkey(a.pack_key_off, a.P, key);
+        const int D = __ldg(a.pack_dim + p);
+        if (c >= D) continue;
+        const int32_t os = ct_lookup(m.other_index, m.other_mask, key);
+        float *mine = m.arena + m.aoff[arr * a.P + p] + (int64_t)(slot - m.pslot[p]) * D + c;
+        const int64_t row = (int64_t)(key - (unsigned long long)__ldg(a.pack_key_off + p));
+        float *host = (arr == 0 ? a.w[p] : arr == 1 ? a.s1[p] : a.s2[p]) + row * D + c;
+        if (dir == 1) {  // fill the new slot
+            const float *src = os >= 0
+                ? m.other_arena + m.other_aoff[arr * a.P + p] + (int64_t)(os - m.other_pslot[p]) * D + c
+                : host;
+            *reinterpret_cast<float4 *>(mine) = *reinterpret_cast<const float4 *>(src);
+        } else if (os < 0) {  // an old slot whose row leaves the hot set
+            *reinterpret_cast<float4 *>(host) = *reinterpret_cast<const float4 *>(mine);
+        }
     }
 }
 
@@ -419,21 +485,22 @@ picasso_status ct_bwd(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
     return PICASSO_OK;
 }
 
-// Alg. 1: write back, top-k(FCounter) within capacity_bytes, load the new rows.
+// Alg. 1: hot_ids = top-k(FCounter) within capacity_bytes; HStore <- CStore(hot_ids).
+// Incremental: rows that stay hot move HBM -> HBM into their new slots (double-buffered HStore),
+// rows that leave are written back to CStore, rows that enter are loaded from it.
 picasso_status ct_refresh(picasso_ctx *ctx, size_t capacity, cudaStream_t s, picasso_cache_stats *stats) {
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     const int nst = ct_nst(ctx);
     int maxD = 4;
     for (int32_t d : ctx->pack_dim) maxD = std::max(maxD, d);
-    CtArgs a = ct_args(ctx);
     unsigned long long hits = 0;
     TCK(cudaMemcpyAsync(&hits, ctx->ct_hits, sizeof(hits), cudaMemcpyDeviceToHost, s));
-    if (ctx->ct_k > 0)  // HStore -> CStore
-        k_ct_move<<<(unsigned)ctx->num_sms * 8, 256, 0, s>>>(a, ctx->ct_keys, ctx->ct_k, nst, maxD, 0);
     const int64_t n = ctx->ct_rows_total;
-    std::vector<unsigned long long> keys;
-    const auto t1 = clk::now();
+    const int b = ctx->ct_buf ^ 1;  // the new HStore's buffers
+    unsigned long long *nkeys = ctx->ct_keys_b[b];
+    int64_t knew = 0;
+    TCK(cudaMemsetAsync(ctx->ct_nsel, 0, sizeof(unsigned long long), s));
     if (capacity > 0 && n > 0) {
         TCK(cudaMemsetAsync(ctx->ct_hist, 0, sizeof(unsigned long long) * kCountBuckets, s));
         k_ct_hist<<<(unsigned)ctx->num_sms * 8, 256, 0, s>>>(ctx->ct_fcnt, n, ctx->pack_key_off_d, ctx->P,
@@ -452,7 +519,7 @@ picasso_status ct_refresh(picasso_ctx *ctx, size_t capacity, cudaStream_t s, pic
             }
             above += h[c];
         }
-        const unsigned long long rem = capacity - above;  // room for rows tied at c* (0: none)
+        const unsigned long long rem = capacity - above;  // room for rows tied at c* (cstar 0: no ties)
         const int64_t nb = (n + kTieBlock - 1) / kTieBlock;
         if (cstar > 0) {
             k_ct_tiesum<<<(unsigned)nb, kTieBlock, 0, s>>>(ctx->ct_fcnt, n, ctx->pack_key_off_d, ctx->P,
@@ -461,51 +528,55 @@ picasso_status ct_refresh(picasso_ctx *ctx, size_t capacity, cudaStream_t s, pic
         } else {
             TCK(cudaMemsetAsync(ctx->ct_bsum, 0, sizeof(unsigned long long) * nb, s));
         }
-        TCK(cudaMemsetAsync(ctx->ct_nsel, 0, sizeof(unsigned long long), s));
-        // cstar == 0: every counted row fits (rows above 0 are all taken, no ties to cut)
         k_ct_select<<<(unsigned)nb, kTieBlock, 0, s>>>(ctx->ct_fcnt, n, ctx->pack_key_off_d, ctx->P, ctx->pack_dim_d,
-                                                       nst, cstar, rem,
-                                                       ctx->ct_bsum, ctx->ct_sel, ctx->ct_nsel, ctx->ct_kmax);
+                                                       nst, cstar, rem, ctx->ct_bsum, ctx->ct_bcnt, nullptr, 0, 0);
+        TCK(cudaMemsetAsync(ctx->ct_bcnt + nb, 0, sizeof(unsigned long long), s));
+        k_ct_scan<<<1, 1024, 0, s>>>(ctx->ct_bcnt, nb + 1);  // [nb] = the number taken
+        k_ct_select<<<(unsigned)nb, kTieBlock, 0, s>>>(ctx->ct_fcnt, n, ctx->pack_key_off_d, ctx->P, ctx->pack_dim_d,
+                                                       nst, cstar, rem, ctx->ct_bsum, ctx->ct_bcnt, nkeys,
+                                                       ctx->ct_kmax, 1);
         unsigned long long ns = 0;
-        TCK(cudaMemcpyAsync(&ns, ctx->ct_nsel, sizeof(ns), cudaMemcpyDeviceToHost, s));
+        TCK(cudaMemcpyAsync(&ns, ctx->ct_bcnt + nb, sizeof(ns), cudaMemcpyDeviceToHost, s));
         TCK(cudaStreamSynchronize(s));
         if ((int64_t)ns > ctx->ct_kmax) {
             ctx->last_msg = "hot set larger than the workspace's HStore (cache_max_bytes)";
             return PICASSO_ERR_CAPACITY;
         }
-        keys.resize(ns);
-        TCK(cudaMemcpy(keys.data(), ctx->ct_sel, sizeof(unsigned long long) * ns, cudaMemcpyDeviceToHost));
-        std::sort(keys.begin(), keys.end());  // pack-major (global key order): slots grouped by pack
+        knew = (int64_t)ns;
+        TCK(cudaMemcpyAsync(ctx->ct_nsel, ctx->ct_bcnt + nb, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
     }
-    const auto t2 = clk::now();
-    // slots per pack and the arena layout [w of every pack | s1 ... | s2 ...]
-    std::vector<int32_t> pslot(ctx->P + 1, 0);
-    for (unsigned long long k : keys) {
-        int p = (int)(std::upper_bound(ctx->pack_key_off.begin(), ctx->pack_key_off.begin() + ctx->P,
-                                       (int64_t)k) - ctx->pack_key_off.begin()) - 1;
-        ++pslot[p + 1];
+    const auto t1 = clk::now();
+    // the new layout, index and rows
+    k_ct_layout<<<1, 32, 0, s>>>(nkeys, ctx->ct_nsel, ctx->pack_key_off_d, ctx->pack_dim_d, ctx->P, nst,
+                                 ctx->ct_pslot_b[b], ctx->ct_aoff_b[b]);
+    TCK(cudaMemsetAsync(ctx->ct_index_b[b], 0xFF, sizeof(Slot) * ((size_t)ctx->ct_mask + 1), s));
+    if (knew > 0)
+        k_ct_index<<<(unsigned)ctx->num_sms * 2, 256, 0, s>>>(ctx->ct_index_b[b], ctx->ct_mask, nkeys, (int32_t)knew);
+    const int o = ctx->ct_buf;
+    CtArgs a = ct_args(ctx);
+    if (knew > 0) {  // fill: staying rows from the old HStore, entering rows from CStore
+        CtMerge m{nkeys, (int32_t)knew, ctx->ct_index_b[o], ctx->ct_mask, ctx->ct_pslot_b[b], ctx->ct_pslot_b[o],
+                  ctx->ct_aoff_b[b], ctx->ct_aoff_b[o], ctx->ct_arena_b[b], ctx->ct_arena_b[o]};
+        if (ctx->ct_k == 0) m.other_index = ctx->ct_index_b[o];  // empty (all 0xFF): every row loads
+        k_ct_merge<<<(unsigned)ctx->num_sms * 8, 256, 0, s>>>(a, m, nst, maxD, 1);
     }
-    for (int p = 0; p < ctx->P; ++p) pslot[p + 1] += pslot[p];
-    std::vector<int64_t> aoff(3 * ctx->P, 0);
-    int64_t off = 0;
-    for (int arr = 0; arr < 3; ++arr)
-        for (int p = 0; p < ctx->P; ++p) {
-            aoff[arr * ctx->P + p] = off;
-            if (arr <= nst) off += (int64_t)(pslot[p + 1] - pslot[p]) * ctx->pack_dim[p];
-        }
-    ctx->ct_k = (int32_t)keys.size();
-    TCK(cudaMemcpyAsync(ctx->ct_pslot_d, pslot.data(), sizeof(int32_t) * (ctx->P + 1), cudaMemcpyHostToDevice, s));
-    TCK(cudaMemcpyAsync(ctx->ct_arena_off_d, aoff.data(), sizeof(int64_t) * 3 * ctx->P, cudaMemcpyHostToDevice, s));
-    TCK(cudaMemsetAsync(ctx->ct_index, 0xFF, sizeof(Slot) * ((size_t)ctx->ct_mask + 1), s));
-    if (ctx->ct_k > 0) {
-        TCK(cudaMemcpyAsync(ctx->ct_keys, keys.data(), sizeof(unsigned long long) * keys.size(),
-                            cudaMemcpyHostToDevice, s));
-        k_ct_index<<<(unsigned)ctx->num_sms * 2, 256, 0, s>>>(ctx->ct_index, ctx->ct_mask, ctx->ct_keys, ctx->ct_k);
-        a = ct_args(ctx);
-        k_ct_move<<<(unsigned)ctx->num_sms * 8, 256, 0, s>>>(a, ctx->ct_keys, ctx->ct_k, nst, maxD, 1);  // load
+    if (ctx->ct_k > 0) {  // write back the old rows that leave
+        CtMerge m{ctx->ct_keys_b[o], ctx->ct_k, ctx->ct_index_b[b], ctx->ct_mask, ctx->ct_pslot_b[o], ctx->ct_pslot_b[b],
+                  ctx->ct_aoff_b[o], ctx->ct_aoff_b[b], ctx->ct_arena_b[o], ctx->ct_arena_b[b]};
+        k_ct_merge<<<(unsigned)ctx->num_sms * 8, 256, 0, s>>>(a, m, nst, maxD, 0);
     }
+    std::vector<int32_t> pslot(ctx->P + 1);
+    TCK(cudaMemcpyAsync(pslot.data(), ctx->ct_pslot_b[b], sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost, s));
     TCK(cudaStreamSynchronize(s));
+    // swap: the new buffers become the current HStore
+    ctx->ct_buf = b;
+    ctx->ct_k = (int32_t)knew;
     ctx->ct_pslot = pslot;
+    ctx->ct_keys = ctx->ct_keys_b[b];
+    ctx->ct_index = ctx->ct_index_b[b];
+    ctx->ct_arena = ctx->ct_arena_b[b];
+    ctx->ct_pslot_d = ctx->ct_pslot_b[b];
+    ctx->ct_arena_off_d = ctx->ct_aoff_b[b];
     if (stats) {
         int64_t bytes = 0;
         for (int p = 0; p < ctx->P; ++p) bytes += (int64_t)(pslot[p + 1] - pslot[p]) * 4 * ctx->pack_dim[p] * (1 + nst);
@@ -514,15 +585,15 @@ picasso_status ct_refresh(picasso_ctx *ctx, size_t capacity, cudaStream_t s, pic
         if (cudaMemcpy(us.data(), ctx->pack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost) ==
             cudaSuccess)
             U = us[ctx->P];
-        const auto t3 = clk::now();
+        const auto t2 = clk::now();
         stats->k = ctx->ct_k;
         stats->bytes = bytes;
         stats->hot_uniques = (int64_t)hits;
         stats->uniques = U;
         stats->hit_ratio_unique = U ? (double)hits / (double)U : 0.0;
-        stats->refresh_ms = std::chrono::duration<double, std::milli>(t3 - t0).count();
-        stats->propose_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
-        stats->select_ms = 0.0;
+        stats->refresh_ms = std::chrono::duration<double, std::milli>(t2 - t0).count();
+        stats->propose_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();  // top-k selection
+        stats->select_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();   // index + row moves
     }
     ctx->last_stream = s;
     return PICASSO_OK;

@@ -256,8 +256,15 @@ struct picasso_ctx {
     int64_t *ct_arena_off_d = nullptr;     // [3P]
     int32_t *ct_hslot = nullptr;           // [max_ids]
     int64_t *ct_row_off = nullptr;         // [max_ids]
-    unsigned long long *ct_hits = nullptr, *ct_hist = nullptr, *ct_bsum = nullptr, *ct_sel = nullptr,
+    unsigned long long *ct_hits = nullptr, *ct_hist = nullptr, *ct_bsum = nullptr, *ct_bcnt = nullptr,
                        *ct_nsel = nullptr;
+    // double-buffered HStore (current = index ct_buf; the refresh builds the other one)
+    int ct_buf = 0;
+    Slot *ct_index_b[2] = {nullptr, nullptr};
+    unsigned long long *ct_keys_b[2] = {nullptr, nullptr};
+    float *ct_arena_b[2] = {nullptr, nullptr};
+    int32_t *ct_pslot_b[2] = {nullptr, nullptr};
+    int64_t *ct_aoff_b[2] = {nullptr, nullptr};
     int64_t ct_kmax = 0, ct_rows_total = 0;
     int32_t ct_k = 0;
     std::vector<int32_t> ct_pslot;
@@ -339,17 +346,24 @@ struct picasso_ctx {
             ct_rows_total = pack_key_off.empty() ? 0 : pack_key_off[P];
             ct_mask = (uint32_t)(pow2_at_least((uint64_t)ct_kmax * 2) - 1);
             ct_fcnt = c.take<uint32_t>(std::max<int64_t>(ct_rows_total, 1));
-            ct_index = c.take<Slot>((size_t)ct_mask + 1);
-            ct_keys = c.take<unsigned long long>(ct_kmax);
-            ct_arena = c.take<float>(opts.cache_max_bytes / 4 + 4 * P);
-            ct_pslot_d = c.take<int32_t>(P + 1);
-            ct_arena_off_d = c.take<int64_t>(3 * P);
+            for (int b = 0; b < 2; ++b) {
+                ct_index_b[b] = c.take<Slot>((size_t)ct_mask + 1);
+                ct_keys_b[b] = c.take<unsigned long long>(ct_kmax);
+                ct_arena_b[b] = c.take<float>(opts.cache_max_bytes / 4 + 4 * P);
+                ct_pslot_b[b] = c.take<int32_t>(P + 1);
+                ct_aoff_b[b] = c.take<int64_t>(3 * P);
+            }
+            ct_index = ct_index_b[ct_buf];
+            ct_keys = ct_keys_b[ct_buf];
+            ct_arena = ct_arena_b[ct_buf];
+            ct_pslot_d = ct_pslot_b[ct_buf];
+            ct_arena_off_d = ct_aoff_b[ct_buf];
             ct_hslot = c.take<int32_t>(N);
             ct_row_off = c.take<int64_t>(N);
             ct_hits = c.take<unsigned long long>(1);
             ct_hist = c.take<unsigned long long>(1 << 16);
             ct_bsum = c.take<unsigned long long>((ct_rows_total + 1023) / 1024 + 1);
-            ct_sel = c.take<unsigned long long>(ct_kmax);
+            ct_bcnt = c.take<unsigned long long>((ct_rows_total + 1023) / 1024 + 2);
             ct_nsel = c.take<unsigned long long>(1);
         }
         // rows / G buffer: the IPC window holds it with the peer-memory exchange

@@ -260,9 +260,11 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
     CK(cudaMemset(ctx->err, 0, sizeof(int)));
     if (ctx->ct_fcnt) {  // cold tier: FCounter zero, HStore empty
         CK(cudaMemset(ctx->ct_fcnt, 0, sizeof(uint32_t) * std::max<int64_t>(ctx->ct_rows_total, 1)));
-        CK(cudaMemset(ctx->ct_index, 0xFF, sizeof(Slot) * ((size_t)ctx->ct_mask + 1)));
-        CK(cudaMemset(ctx->ct_pslot_d, 0, sizeof(int32_t) * (ctx->P + 1)));
-        CK(cudaMemset(ctx->ct_arena_off_d, 0, sizeof(int64_t) * 3 * ctx->P));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMemset(ctx->ct_index_b[b], 0xFF, sizeof(Slot) * ((size_t)ctx->ct_mask + 1)));
+            CK(cudaMemset(ctx->ct_pslot_b[b], 0, sizeof(int32_t) * (ctx->P + 1)));
+            CK(cudaMemset(ctx->ct_aoff_b[b], 0, sizeof(int64_t) * 3 * ctx->P));
+        }
         ctx->ct_k = 0;
         ctx->ct_pslot.assign(ctx->P + 1, 0);
     }
