@@ -169,6 +169,8 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_BWD")) {
         c->split_bwd = std::strcmp(e, "fused") != 0;
         c->fuse_pipe = std::strcmp(e, "fusepipe") == 0;
+        if (!std::strcmp(e, "flat")) c->flat_bwd = 1;       // flat segment-sum + k_update_rows
+        if (!std::strcmp(e, "flatfused")) c->flat_bwd = 2;  // flat segment-sum fused with the update
     }
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM_SMALL")) c->flat_small = std::strcmp(e, "legacy") != 0;
@@ -542,6 +544,14 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
             u.state1 = ctx->s1[p];
             u.state2 = ctx->s2[p];
             int fl = 0;
+            if (ctx->flat_bwd) {  // flat backward: segment-sum (+ optimizer in the same pass when fused)
+                ctx->launches_bwd += launch_bwd_flat(ctx->pack_dim[p], u, ctx->flat_bwd == 2, ctx->num_sms, s);
+                if (ctx->flat_bwd == 1) {
+                    launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
+                    ++ctx->launches_bwd;
+                }
+                continue;
+            }
             if (ctx->fuse_pipe && ctx->bulk_segsum) fl = launch_segsum_fused(ctx->pack_dim[p], u, ctx->num_sms, s);
             if (fl) {  // segment-sum and optimizer in one pass over the rows
                 ctx->launches_bwd += fl;
