@@ -177,7 +177,6 @@ struct picasso_ctx {
     bool fuse_pipe = false;  // PICASSO_BWD=fusepipe (W = 1, D = 64/128): pipelined segsum with the
                              // update at each row's flush.  Measured slower (C2: 219 us vs 73 + 71 us
                              // split) — one deferred row per warp does not hide the state loads.
-    int flat_bwd = 0;       // W = 1 backward: 1 flat segment-sum + update, 2 flat fused (PICASSO_BWD=flat|flatfused)
     bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
     int overlap_env = -1;   // PICASSO_OVERLAP (0 / 1) if set; else chosen per world == 1 forward
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share

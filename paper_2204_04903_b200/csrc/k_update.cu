@@ -107,15 +107,6 @@ __device__ __forceinline__ void load_contrib(const UpdateArgs &a, int32_t seg, i
     }
 }
 
-// 16-byte chunk c of an occurrence's contribution (dY row of its segment, / len for mean)
-__device__ __forceinline__ float4 load_chunk(const UpdateArgs &a, int32_t seg, int c) {
-    const int32_t f = seg / a.B;
-    const int32_t b = seg - f * a.B;
-    float4 v = ldg_f4(a.dy + (int64_t)b * a.dy_stride + a.finfo[f].col + c * 4);
-    if (a.pool_mean) v = div4(v, (float)(__ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg)));
-    return v;
-}
-
 // Weight / state row registers of one update.
 template <int VPL>
 struct RowRegs {
@@ -131,24 +122,6 @@ __device__ __forceinline__ void load_row(const UpdateArgs &a, int64_t row, int l
         r.w[q] = *reinterpret_cast<const float4 *>(a.weight + o + q * LANES * 4);
         r.s1[q] = *reinterpret_cast<const float4 *>(a.state1 + o + q * LANES * 4);
         if (a.opt == 1) r.s2[q] = *reinterpret_cast<const float4 *>(a.state2 + o + q * LANES * 4);
-    }
-}
-
-// the optimizer on one element (reading O10), the arithmetic of update_row32
-__device__ __forceinline__ void opt_elem(const UpdateArgs &a, float g, float &w, float &s1, float &s2) {
-    if (a.opt == 0) {
-        const float acc = __fadd_rn(s1, __fmul_rn(g, g));
-        s1 = acc;
-        w = __fsub_rn(w, __fmul_rn(a.lr, __fdiv_rn(g, __fadd_rn(__fsqrt_rn(acc), a.eps))));
-    } else {
-        const float omb1 = __fsub_rn(1.0f, a.beta1), omb2 = __fsub_rn(1.0f, a.beta2);
-        const float mo = s1, vo = s2;
-        const float mu = __fmul_rn(__fsub_rn(g, mo), omb1);
-        const float vu = __fmul_rn(__fsub_rn(__fmul_rn(g, g), vo), omb2);
-        const float mn = __fadd_rn(mu, mo), vn = __fadd_rn(vu, vo);
-        s1 = mn;
-        s2 = vn;
-        w = __fsub_rn(w, __fmul_rn(a.adam_ss, __fdiv_rn(mn, __fadd_rn(__fsqrt_rn(vn), a.eps))));
     }
 }
 
@@ -575,148 +548,6 @@ __global__ void __launch_bounds__(256) k_segsum_flat(UpdateArgs a) {
     }
 }
 
-// Flat backward: one thread per 16-byte chunk of a unique row (D/4 consecutive threads per row,
-// so every occurrence is one coalesced row read per row group), the row's occurrences summed in
-// ascending order in fp64 (reading O6) with 4 dY loads in flight per thread, and — FUSE — the
-// optimizer applied right there: the row's weight / state chunks are loaded before the dY walk,
-// so the update needs no G round trip through HBM and no second pass over the rows.  Rows with
-// more than kLongRow occurrences go to the chunked path (k_long_*), which then updates them.
-// Without FUSE the rounded G chunk is written instead (k_update_rows applies the optimizer).
-template <int D, bool FUSE>
-__global__ void __launch_bounds__(256) k_bwd_flat(UpdateArgs a) {
-    constexpr int V4 = D / 4;
-    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
-    float *gp = a.gbuf ? a.gbuf + a.pack_gbase[a.pack] : nullptr;
-    const int64_t n = (int64_t)(u1 - u0) * V4;
-#pragma unroll 1
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = u0 + e / V4;
-        const int c = (int)(e % V4);
-        const int32_t i0 = __ldg(a.ustart + u), i1 = __ldg(a.ustart + u + 1);
-        if (i1 - i0 > kLongRow) {  // Zipf head: the chunked path
-            if (c == 0) a.long_list[atomicAdd(a.long_cnt, 1)] = (int32_t)u;
-            continue;
-        }
-        float4 w4, s14, s24 = make_float4(0.f, 0.f, 0.f, 0.f);
-        int64_t o = 0;
-        if constexpr (FUSE) {  // weight / state in flight during the dY walk
-            o = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off) * D + c * 4;
-            w4 = *reinterpret_cast<const float4 *>(a.weight + o);
-            s14 = *reinterpret_cast<const float4 *>(a.state1 + o);
-            if (a.opt == 1) s24 = *reinterpret_cast<const float4 *>(a.state2 + o);
-        }
-        dbl4 g = zero4d();
-        int32_t i = i0;
-#pragma unroll 1
-        for (; i + 4 <= i1; i += 4) {
-            float4 v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = load_chunk(a, __ldg(a.sorted_seg + i + k), c);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) g = add4d(g, v[k]);
-        }
-        if (i < i1) {
-            float4 v[3];
-            const int r = i1 - i;
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                if (k < r) v[k] = load_chunk(a, __ldg(a.sorted_seg + i + k), c);
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                if (k < r) g = add4d(g, v[k]);
-        }
-        const float4 g4 = round4(g);
-        if constexpr (FUSE) {
-            const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
-            float ww[4] = {w4.x, w4.y, w4.z, w4.w}, s1[4] = {s14.x, s14.y, s14.z, s14.w};
-            float s2[4] = {s24.x, s24.y, s24.z, s24.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) opt_elem(a, gg[k], ww[k], s1[k], s2[k]);
-            *reinterpret_cast<float4 *>(a.weight + o) = make_float4(ww[0], ww[1], ww[2], ww[3]);
-            *reinterpret_cast<float4 *>(a.state1 + o) = make_float4(s1[0], s1[1], s1[2], s1[3]);
-            if (a.opt == 1) *reinterpret_cast<float4 *>(a.state2 + o) = make_float4(s2[0], s2[1], s2[2], s2[3]);
-        } else {
-            *reinterpret_cast<float4 *>(g_row_ptr<D>(a, u, u0, gp, c, (float)(i1 - i0)) + c * 4) = g4;
-        }
-    }
-}
-
-// The flat backward with 32-byte chunks (D % 8 == 0): D/8 threads per row, 256-bit loads / stores.
-template <int D, bool FUSE>
-__global__ void __launch_bounds__(256) k_bwd_flat8(UpdateArgs a) {
-    constexpr int V8 = D / 8;
-    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
-    float *gp = a.gbuf ? a.gbuf + a.pack_gbase[a.pack] : nullptr;
-    const int64_t n = (int64_t)(u1 - u0) * V8;
-#pragma unroll 1
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = u0 + e / V8;
-        const int c = (int)(e % V8);
-        const int32_t i0 = __ldg(a.ustart + u), i1 = __ldg(a.ustart + u + 1);
-        if (i1 - i0 > kLongRow) {
-            if (c == 0) a.long_list[atomicAdd(a.long_cnt, 1)] = (int32_t)u;
-            continue;
-        }
-        f8 w8, s18, s28;
-        int64_t o = 0;
-        if constexpr (FUSE) {
-            o = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off) * D + c * 8;
-            w8 = ld_f8(a.weight + o);
-            s18 = ld_f8(a.state1 + o);
-            if (a.opt == 1) s28 = ld_f8(a.state2 + o);
-        }
-        double g[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) g[k] = 0.0;
-        auto contrib = [&](int32_t seg) -> f8 {
-            const int32_t f = seg / a.B;
-            const int32_t b = seg - f * a.B;
-            f8 v = ldg_f8(a.dy + (int64_t)b * a.dy_stride + a.finfo[f].col + c * 8);
-            if (a.pool_mean) {
-                const float len = (float)(__ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg));
-#pragma unroll
-                for (int k = 0; k < 8; ++k) v.v[k] = __fdiv_rn(v.v[k], len);
-            }
-            return v;
-        };
-        int32_t i = i0;
-#pragma unroll 1
-        for (; i + 4 <= i1; i += 4) {
-            f8 v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = contrib(__ldg(a.sorted_seg + i + k));
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int q = 0; q < 8; ++q) g[q] = __dadd_rn(g[q], (double)v[k].v[q]);
-        }
-        if (i < i1) {
-            f8 v[3];
-            const int r = i1 - i;
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                if (k < r) v[k] = contrib(__ldg(a.sorted_seg + i + k));
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                if (k < r)
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) g[q] = __dadd_rn(g[q], (double)v[k].v[q]);
-        }
-        if constexpr (FUSE) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) opt_elem(a, __double2float_rn(g[q]), w8.v[q], s18.v[q], s28.v[q]);
-            st_f8(a.weight + o, w8);
-            st_f8(a.state1 + o, s18);
-            if (a.opt == 1) st_f8(a.state2 + o, s28);
-        } else {
-            f8 g8;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) g8.v[q] = __double2float_rn(g[q]);
-            st_f8(g_row_ptr<D>(a, u, u0, gp, c * 2, (float)(i1 - i0)) + c * 8, g8);
-        }
-    }
-}
-
 template <int D>
 __global__ void __launch_bounds__(256) k_update_rows(UpdateArgs a) {
     constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
@@ -943,35 +774,6 @@ void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s)
 #define CALL(DD) k_update_rows<DD><<<blocks, 256, 0, s>>>(a)
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
-}
-
-// flat backward of one pack (+ the chunked path of its long rows); fuse: the optimizer in the
-// same pass (a.gbuf unused, the long rows' finish updates too).  Returns #launches.
-int launch_bwd_flat(int D, const UpdateArgs &a0, bool fuse, int num_sms, cudaStream_t s) {
-    UpdateArgs a = a0;
-    if (fuse) a.gbuf = nullptr;
-    const unsigned blocks = (unsigned)num_sms * 8;
-    static const bool w16 = std::getenv("PICASSO_FLAT_W16") != nullptr;  // 16-byte chunks (A/B)
-    if (D >= 8 && !w16) {
-#define CALL(DD)                                                      \
-    {                                                                 \
-        if constexpr (DD >= 8) {                                      \
-            if (fuse) k_bwd_flat8<DD, true><<<blocks, 256, 0, s>>>(a); \
-            else k_bwd_flat8<DD, false><<<blocks, 256, 0, s>>>(a);    \
-        }                                                             \
-    }
-        PICASSO_DISPATCH_D(D, CALL)
-#undef CALL
-    } else {
-#define CALL(DD)                                                      \
-    {                                                                 \
-        if (fuse) k_bwd_flat<DD, true><<<blocks, 256, 0, s>>>(a);     \
-        else k_bwd_flat<DD, false><<<blocks, 256, 0, s>>>(a);         \
-    }
-        PICASSO_DISPATCH_D(D, CALL)
-#undef CALL
-    }
-    return 1 + launch_long_update(D, a, num_sms, s);
 }
 
 int launch_long_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {

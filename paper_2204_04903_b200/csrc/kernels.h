@@ -182,7 +182,6 @@ struct UpdateArgs {
 };
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s, bool flat_small = true);
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
-int launch_bwd_flat(int D, const UpdateArgs &a, bool fuse, int num_sms, cudaStream_t s);  // returns #launches
 void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, int32_t n_cnt,
                        cudaStream_t s);
 void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);

@@ -169,8 +169,6 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_BWD")) {
         c->split_bwd = std::strcmp(e, "fused") != 0;
         c->fuse_pipe = std::strcmp(e, "fusepipe") == 0;
-        if (!std::strcmp(e, "flat")) c->flat_bwd = 1;       // flat segment-sum + k_update_rows
-        if (!std::strcmp(e, "flatfused")) c->flat_bwd = 2;  // flat segment-sum fused with the update
     }
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM_SMALL")) c->flat_small = std::strcmp(e, "legacy") != 0;
@@ -185,14 +183,14 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_KINTERLEAVE")) c->kinterleave = std::atoi(e);
     // World == 1: the pool needs only the raw IDs (row = h(id)), so by default it starts at once
     // and streams rows on the caller's stream while the Unique chain and the backward's transpose
-    // run beside it on the internal stream (C2: 0.291 -> 0.271 ms / step, round-2 measurement;
-    // the pool alone then runs slower, ~3.1 TB/s, sharing the SMs).  The pool leaves 48 of 148
-    // SMs to that chain (measured best at C2; PICASSO_POOL_RESERVE overrides).
+    // run beside it on the internal stream (C2: 0.291 -> 0.258 ms / step, round-2 measurement;
+    // the pool alone then runs slower, sharing the SMs).  The pool leaves 74 of 148 SMs to that
+    // chain (measured best at C2; PICASSO_POOL_RESERVE overrides).
     // PICASSO_EARLY_POOL=0: the serial order (dedup, then pool).
     // Chosen per forward (below kOverlapMinIds IDs; at C3's 83.5 M IDs the early pool measured
     // slower, 26.3 vs 25.6 ms, and the transpose alone goes beside the pool instead).
     if (const char *e = std::getenv("PICASSO_EARLY_POOL")) c->early_env = std::strcmp(e, "0") != 0;
-    c->pool_reserve = 48;
+    c->pool_reserve = 74;  // C2 sweep (round 2): 24 -> 0.283, 48 -> 0.270, 74 -> 0.258, 84 -> 0.267 ms / step
     if (const char *e = std::getenv("PICASSO_POOL_RESERVE")) c->pool_reserve = std::atoi(e);
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -311,7 +309,15 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
         }
     }
     if (!ctx->side) {  // internal streams: the forward's overlapped transpose, K-Interleaving
-        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        // the internal stream carries the latency-bound Unique / transpose chain beside the pool:
+        // highest priority, so its blocks are scheduled first whenever SMs free up
+        int lo_prio = 0, hi_prio = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        static const char *pe = std::getenv("PICASSO_SIDE_PRIO");
+        if (pe && std::atoi(pe) == 0)
+            CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        else
+            CK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi_prio));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_fp, cudaEventDisableTiming));
@@ -453,7 +459,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     ctx->early_pool = ctx->early_env >= 0 ? ctx->early_env != 0 : n_ids < kOverlapMinIds;
     if (ctx->overlap_env < 0) ctx->overlap = ctx->early_pool || n_ids >= kOverlapMinIds;
     ctx->pool_sms = (ctx->early_pool && ctx->overlap && ctx->side)
-                        ? std::max(ctx->num_sms / 2, ctx->num_sms - ctx->pool_reserve)
+                        ? std::max(ctx->num_sms / 4, ctx->num_sms - ctx->pool_reserve)
                         : ctx->num_sms;
     if (ctx->overlap && ctx->side && ctx->early_pool) {
         // At world == 1 the pool needs only the raw IDs (row = h(id)), not the dedup: the index
@@ -544,14 +550,6 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
             u.state1 = ctx->s1[p];
             u.state2 = ctx->s2[p];
             int fl = 0;
-            if (ctx->flat_bwd) {  // flat backward: segment-sum (+ optimizer in the same pass when fused)
-                ctx->launches_bwd += launch_bwd_flat(ctx->pack_dim[p], u, ctx->flat_bwd == 2, ctx->num_sms, s);
-                if (ctx->flat_bwd == 1) {
-                    launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
-                    ++ctx->launches_bwd;
-                }
-                continue;
-            }
             if (ctx->fuse_pipe && ctx->bulk_segsum) fl = launch_segsum_fused(ctx->pack_dim[p], u, ctx->num_sms, s);
             if (fl) {  // segment-sum and optimizer in one pass over the rows
                 ctx->launches_bwd += fl;

@@ -148,8 +148,7 @@ def test_pool_pipe_mean_and_all_empty_pack():
 @pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "0"}, {"PICASSO_BWD": "fusepipe"}, {"PICASSO_POOL": "flat"},
                                  {"PICASSO_OVERLAP": "0"}, {"PICASSO_OVERLAP": "1"}, {"PICASSO_SEGSUM_CFG": "12x4"},
                                  {"PICASSO_DEDUP_REGIONS": "1"}, {"PICASSO_SEGSUM_SMALL": "legacy"},
-                                 {"PICASSO_SORT": "3"}, {"PICASSO_SORT": "2"}, {"PICASSO_BWD": "flat"},
-                                 {"PICASSO_BWD": "flatfused"}])
+                                 {"PICASSO_SORT": "3"}, {"PICASSO_SORT": "2"}])
 def test_alternative_paths_match_oracle(env, monkeypatch):
     """Every switchable variant computes the same step: forward bit-exact, update within the
     north-star tolerance of the oracle (bit-exact under dyadic dY)."""
