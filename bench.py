@@ -243,6 +243,9 @@ def algorithmic_bytes(cfg, B, N, U_by_pack, plan, world=1):
         "segsum": out_bytes + 4 * N + 4 * (U + 1) + rows_bytes,
         # G rows in + row keys + weight and accumulator read + written (W = 1: this rank's uniques)
         "update": rows_bytes + 8 * U + 4 * rows_bytes if world == 1 else None,
+        # fused segment-sum + Adagrad (W = 1 default, k_segsum_upd): dY rows + sorted segment list + row
+        # bounds + row keys + weight and accumulator read + written — no G row in either direction
+        "segsum_update": out_bytes + 4 * N + 4 * (U + 1) + 8 * U + 4 * rows_bytes if world == 1 else None,
         # whole step, fused definition of SURVEY §8(d) (fwd + bwd + Adagrad)
         "step": 8 * N + 4 * (S + 1) + 4 * N + 8 * U + rows_bytes + out_bytes + out_bytes + 4 * N + 4 * rows_bytes,
     }
@@ -657,7 +660,11 @@ def main():
     # longest of the kernels that run alone.
     early = (world == 1 and last_b.n_ids < (1 << 22) and os.environ.get("PICASSO_EARLY_POOL", "1") != "0"
              and not args.eager)
-    cand = [k for k in ("pool", "segsum", "update") if k in per_phase and k in alg and not (early and k == "pool")]
+    fused = world == 1 and "segsum" in per_phase and "update" not in per_phase  # k_segsum_upd: one kernel
+    if fused:
+        per_phase["segsum_update"] = per_phase.pop("segsum")
+    cand = [k for k in ("pool", "segsum", "update", "segsum_update") if k in per_phase and k in alg
+            and not (early and k == "pool")]
     dom = max(cand, key=lambda k: per_phase[k])
     peak = None
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -755,7 +762,8 @@ def main():
             "gpu_launches": int((lf + lb) * args.steps),
             "roofline": {"bound": "hbm", "kernel": {"pool": "k_pool_pipe (+ k_seg_of)",
                                                      "segsum": "k_segsum_pipe (+ k_segsum_fix)",
-                                                     "update": "k_update_rows"}[dom],
+                                                     "update": "k_update_rows",
+                                                     "segsum_update": "k_segsum_upd (+ k_segsum_fix)"}[dom],
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
                          "peak_source": peak_src},

@@ -174,9 +174,11 @@ struct picasso_ctx {
     int32_t *tile_start = nullptr;
     int4 *split = nullptr;
     bool split_bwd = true;  // PICASSO_BWD=fused selects the legacy fused segsum+update kernel
-    bool fuse_pipe = false;  // PICASSO_BWD=fusepipe (W = 1, D = 64/128): pipelined segsum with the
-                             // update at each row's flush.  Measured slower (C2: 219 us vs 73 + 71 us
-                             // split) — one deferred row per warp does not hide the state loads.
+    int fuse_rw = 3;        // fused backward: tile cost of a row in occurrences (PICASSO_FUSE_RW; C2 sweep)
+    bool fuse_pipe = true;   // W = 1, tiled packs of D = 64 / 128: k_segsum_upd, the pipelined segment-sum
+                             // with each row's weight / state prefetched into a shared-memory ring and
+                             // the optimizer applied at its flush (C2: 116 us vs 74 + 71 us split);
+                             // PICASSO_BWD=split: segment-sum + k_update_rows
     bool overlap = true;    // PICASSO_OVERLAP=0: the transpose runs on the caller's stream
     int overlap_env = -1;   // PICASSO_OVERLAP (0 / 1) if set; else chosen per world == 1 forward
     int pool_reserve = 0, pool_sms = 148;  // pipelined pool grid = SMs minus the transpose's share

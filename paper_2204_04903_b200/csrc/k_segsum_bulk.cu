@@ -36,7 +36,7 @@ template <int N>
 __device__ __forceinline__ void ldgsts_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int kStageBytes = 4096;  // target bytes per ring stage
-constexpr int kMaxNW = 16;         // warps per CTA at most (sizes the tile arrays)
+constexpr int kMaxNW = 24;         // warps per CTA at most (sizes the tile arrays)
 #ifndef PICASSO_CONSUME_ROWS
 #define PICASSO_CONSUME_ROWS 4
 #endif
@@ -191,7 +191,7 @@ __device__ __forceinline__ void opt_step(const UpdateArgs &a, float g, float &w,
 // nte = min(nt, C), position i belongs to tile floor(cost(i) * nte / C): tiles never come out
 // empty inside a row, and tiles >= nte are empty at the pack's end.
 __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const int32_t *pack_gstart,
-                            const int32_t *pack_ustart, int32_t P, int32_t nt, int32_t *tile_start) {
+                            const int32_t *pack_ustart, int32_t P, int32_t nt, int32_t *tile_start, int32_t rw) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int32_t u = su[i];
@@ -205,9 +205,11 @@ __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const
     }
     const int64_t G0 = __ldg(pack_gstart + lo), G1 = __ldg(pack_gstart + lo + 1);
     const int64_t U0 = __ldg(pack_ustart + lo), U1 = __ldg(pack_ustart + lo + 1);
-    const int64_t C = (G1 - G0) + (U1 - U0);
+    // rw: cost of a row relative to an occurrence (1: G row write vs dY row read; the fused kernel
+    // also reads and writes the row's weight and state, rw = 4)
+    const int64_t C = (G1 - G0) + rw * (U1 - U0);
     const int64_t nte = nt < C ? nt : C;
-    const int64_t cost = (i - G0) + (u - U0);
+    const int64_t cost = (i - G0) + rw * (u - U0);
     // floor(c * nte / C) without a 64-bit division: 32-bit when it fits, else a double
     // estimate corrected exactly
     auto tile_of = [&](int64_t c) -> int64_t {
@@ -220,7 +222,7 @@ __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const
     };
     const int64_t k = tile_of(cost);
     int64_t kprev = -1;
-    if (i > G0) kprev = tile_of(cost - (row_start ? 2 : 1));
+    if (i > G0) kprev = tile_of(cost - (row_start ? 1 + rw : 1));
     int32_t *ts = tile_start + (int64_t)lo * (nt + 1);
     for (int64_t kk = kprev + 1; kk <= k; ++kk) ts[kk] = (int32_t)i;
     if (i == G1 - 1)
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     if (u1 <= u0) return;
     const int32_t *ts = a.tile_start + (int64_t)a.pack * (a.nt + 1);
     const int32_t t = blockIdx.x * NW + w;
+    if (t >= a.nt) return;
     const int32_t pa = __ldg(ts + t), pb = __ldg(ts + t + 1);
     if (pa >= pb) return;
 
@@ -417,6 +420,220 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     finish_pending();
 }
 
+// ------------------------------------------------------------------------------------------
+// Segment-sum fused with the optimizer (world == 1, D = 64 / 128).  The pipe above, plus a
+// second cp.async stream per warp: when a stage is issued, the weight and optimizer-state rows of
+// every row that starts in it are copied into a ring of row slots (slot = row sequence number in
+// the tile mod RR), in the same commit group as the stage's dY rows.  A row's flush therefore finds
+// its G in registers and its weight / state in shared memory: the optimizer runs there and the
+// rows are stored straight back — no G round trip through HBM and no second pass over the rows.
+// Rows cut by a tile edge keep the fp64-partial path; k_segsum_fix<D, true> updates them.
+// Ring bound: when stage k + S is issued (after stage k is consumed) at most 1 + S*RS rows of the
+// tile are unflushed, so RR = S*RS + 2 slots never overwrite a row still to be read.
+template <int D, int RS, int S, int NST>
+struct FG {
+    static constexpr int ROWB = D * 4;
+    static constexpr int SB = RS * ROWB;             // dY bytes per stage
+    static constexpr int RR = S * RS + 2;            // row slots
+    static constexpr int SLOTB = (1 + NST) * ROWB;   // weight + state rows of one slot
+    static constexpr int WARPB = S * SB + RR * SLOTB;
+    static constexpr int META = S * RS * 8;          // uid + len per staged row
+    static constexpr int EPL = D / 32;
+    static_assert(32 % RS == 0, "a stage lies inside one 32-position round");
+};
+
+template <int D, int NW, int RS, int S, int NST>
+__global__ void __launch_bounds__(NW * 32, 1) k_segsum_upd(UpdateArgs a) {
+    using G = FG<D, RS, S, NST>;
+    constexpr int ROWB = G::ROWB, SB = G::SB, RR = G::RR, SLOTB = G::SLOTB, EPL = G::EPL;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t *wu = reinterpret_cast<int32_t *>(smem) + w * (G::META / 4);
+    int32_t *wl = wu + S * RS;
+    unsigned char *wr = smem + NW * G::META + (size_t)w * G::WARPB;  // [S stages of dY | RR row slots]
+    unsigned char *wslot = wr + S * SB;
+
+    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
+    if (u1 <= u0) return;
+    const int32_t *ts = a.tile_start + (int64_t)a.pack * (a.nt + 1);
+    const int32_t t = blockIdx.x * NW + w;
+    if (t >= a.nt) return;
+    const int32_t pa = __ldg(ts + t), pb = __ldg(ts + t + 1);
+    if (pa >= pb) return;
+    const float4 *dy4 = reinterpret_cast<const float4 *>(a.dy);
+
+    const int32_t u_first = __ldg(a.sorted_u + pa), u_last = __ldg(a.sorted_u + pb - 1);
+    const int32_t last_end = __ldg(a.ustart + u_last + 1);
+    const int32_t hp = __ldg(a.ustart + u_first) < pa ? u_first : -1;
+    const int32_t tp = (last_end > pb && u_last != hp) ? u_last : -1;
+    if (lane == 0 && tp >= 0) a.split[atomicAdd(a.long_cnt, 1)] = make_int4(t, tp, __ldg(a.ustart + tp), last_end);
+    const int32_t nst = (pb - pa + RS - 1) / RS;
+
+    uint32_t off_c, off_n;
+    int32_t uid_c, uid_n, len_c, len_n;
+    int64_t row_c = 0, row_n = 0;
+    auto resolve = [&](int32_t base, uint32_t &off, int32_t &uid, int32_t &len, int64_t &row) {
+        const int32_t p = base + lane;
+        off = 0;
+        uid = -1;
+        len = 1;
+        row = 0;
+        if (p < pb) {
+            const int32_t seg = __ldg(a.sorted_seg + p);
+            uid = __ldg(a.sorted_u + p);
+            const int32_t f = seg / a.B;
+            off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col) >> 2);
+            if (a.pool_mean) len = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
+            row = (int64_t)(__ldg(a.unique_gkey + uid) - (unsigned long long)a.pack_key_off);
+        }
+    };
+    resolve(pa, off_c, uid_c, len_c, row_c);
+    resolve(pa + 32, off_n, uid_n, len_n, row_n);
+    int32_t round_c = 0, prev_last = -1, rseq_issue = 0;
+    auto issue = [&](int32_t k) {
+        const int slot = k % S;
+        const int32_t r = (k * RS) >> 5;
+        if (r != round_c) {
+            prev_last = __shfl_sync(0xffffffffu, uid_c, 31);
+            off_c = off_n;
+            uid_c = uid_n;
+            len_c = len_n;
+            row_c = row_n;
+            round_c = r;
+            resolve(pa + (r + 1) * 32, off_n, uid_n, len_n, row_n);
+        }
+        const int32_t p0 = pa + k * RS;
+        const int nrows = pb - p0 < RS ? pb - p0 : RS;
+        const int l0 = (k * RS) & 31;
+        unsigned char *dst = wr + slot * SB;
+        if constexpr (EPL == 2) {
+            const int h = lane >> 4, c = lane & 15;
+#pragma unroll
+            for (int i = 0; i < RS; i += 2) {
+                const uint32_t off = __shfl_sync(0xffffffffu, off_c, l0 + i + h);
+                if (i + h < nrows) ldgsts(dst + (i + h) * ROWB + c * 16, dy4 + off + c);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < RS; ++i) {
+                const uint32_t off = __shfl_sync(0xffffffffu, off_c, l0 + i);
+                if (i < nrows) {
+#pragma unroll
+                    for (int q = 0; q < EPL / 4; ++q)
+                        ldgsts(dst + i * ROWB + q * 512 + lane * 16, dy4 + off + q * 32 + lane);
+                }
+            }
+        }
+        const int i = lane - l0;
+        if (i >= 0 && i < nrows) {
+            wu[slot * RS + i] = uid_c;
+            wl[slot * RS + i] = len_c;
+        }
+        // the weight / state rows of the rows starting in this stage
+        const int32_t up = __shfl_up_sync(0xffffffffu, uid_c, 1);
+        const bool start = i >= 0 && i < nrows && (p0 + i == pa || uid_c != (lane == 0 ? prev_last : up));
+        unsigned m = __ballot_sync(0xffffffffu, start);
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const int32_t uid = __shfl_sync(0xffffffffu, uid_c, b);
+            const int64_t row = __shfl_sync(0xffffffffu, row_c, b);
+            unsigned char *sl = wslot + (rseq_issue % RR) * SLOTB;
+            ++rseq_issue;
+            if (uid == hp || uid == tp) continue;  // split rows: partials, updated by k_segsum_fix
+            const float4 *src[1 + NST];
+            src[0] = reinterpret_cast<const float4 *>(a.weight + row * D);
+            src[1] = reinterpret_cast<const float4 *>(a.state1 + row * D);
+            if constexpr (NST == 2) src[2] = reinterpret_cast<const float4 *>(a.state2 + row * D);
+            if constexpr (EPL == 2) {  // 256-B rows: lanes 0-15 and 16-31 copy two arrays per instruction
+                const int h = lane >> 4, c = lane & 15;
+#pragma unroll
+                for (int arr = 0; arr < 1 + NST; arr += 2)
+                    if (arr + h < 1 + NST) ldgsts(sl + (arr + h) * ROWB + c * 16, src[arr + h] + c);
+            } else {
+#pragma unroll
+                for (int arr = 0; arr < 1 + NST; ++arr)
+#pragma unroll
+                    for (int q = 0; q < EPL / 4; ++q)
+                        ldgsts(sl + arr * ROWB + q * 512 + lane * 16, src[arr] + q * 32 + lane);
+            }
+        }
+    };
+
+    double acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.0;
+    int32_t cur = -1, rseq_cons = 0;
+    int64_t cur_row = 0;
+    auto flush = [&](int32_t u) {
+        double *part = reinterpret_cast<double *>(a.partial);
+        const unsigned char *sl = wslot + (rseq_cons % RR) * SLOTB;
+        ++rseq_cons;
+        if (u == hp) {
+            lane_store_f64<D>(part + (int64_t)(2 * t) * D, lane, acc);
+        } else if (u == tp) {
+            lane_store_f64<D>(part + (int64_t)(2 * t + 1) * D, lane, acc);
+        } else {
+            float wv[EPL], s1[EPL], s2[EPL];
+            lane_load<D>(reinterpret_cast<const float *>(sl), lane, wv);
+            lane_load<D>(reinterpret_cast<const float *>(sl + ROWB), lane, s1);
+            if constexpr (NST == 2) lane_load<D>(reinterpret_cast<const float *>(sl + 2 * ROWB), lane, s2);
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) opt_step(a, __double2float_rn(acc[e]), wv[e], s1[e], s2[e]);
+            lane_gstore<D>(a.weight + cur_row * D, lane, wv);
+            lane_gstore<D>(a.state1 + cur_row * D, lane, s1);
+            if constexpr (NST == 2) lane_gstore<D>(a.state2 + cur_row * D, lane, s2);
+        }
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = 0.0;
+    };
+
+    for (int32_t k = 0; k < S; ++k) {
+        if (k < nst) issue(k);
+        ldgsts_commit();
+    }
+    constexpr int CH = RS < kConsumeRows ? RS : kConsumeRows;
+#pragma unroll 1
+    for (int32_t k = 0; k < nst; ++k) {
+        const int slot = k % S;
+        ldgsts_wait<S - 1>();
+        __syncwarp();
+        const int32_t p0 = pa + k * RS;
+        const int nrows = pb - p0 < RS ? pb - p0 : RS;
+        const float *rows = reinterpret_cast<const float *>(wr + slot * SB);
+#pragma unroll 1
+        for (int i0 = 0; i0 < nrows; i0 += CH) {
+            float v[CH][EPL];
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+                if (i0 + c < nrows) lane_load<D>(rows + (i0 + c) * D, lane, v[c]);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int i = i0 + c;
+                if (i < nrows) {
+                    const int32_t uid = wu[slot * RS + i];
+                    if (uid != cur) {
+                        if (cur >= 0) flush(cur);
+                        cur = uid;
+                        cur_row = (int64_t)(__ldg(a.unique_gkey + uid) - (unsigned long long)a.pack_key_off);
+                    }
+                    if (a.pool_mean) {
+                        const float len = (float)wl[slot * RS + i];
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) v[c][e] = __fdiv_rn(v[c][e], len);
+                    }
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) acc[e] = __dadd_rn(acc[e], (double)v[c][e]);
+                }
+            }
+        }
+        __syncwarp();
+        if (k + S < nst) issue(k + S);
+        ldgsts_commit();
+    }
+    if (cur >= 0) flush(cur);
+}
+
 // One CTA per listed split row: its pieces (j = 0: slot 2t+1 of its first tile t; j >= 1: slot
 // 2(t+j)) summed in tile order — warp w takes j = w mod 4, the warps combined in order.
 template <int D, bool FUSE>
@@ -489,7 +706,8 @@ template <int D, int NW, int S, bool FUSE = false>
 void launch_pipe(const UpdateArgs &a, int num_sms, cudaStream_t s) {
     using G = BG<D, NW, S>;
     ensure_dyn_smem((const void *)k_segsum_pipe<D, NW, S, FUSE>, G::SMEM);
-    k_segsum_pipe<D, NW, S, FUSE><<<(unsigned)num_sms, NW * 32, G::SMEM, s>>>(a);
+    (void)num_sms;  // one warp per tile: the grid covers the ctx's nt tiles
+    k_segsum_pipe<D, NW, S, FUSE><<<(unsigned)((a.nt + NW - 1) / NW), NW * 32, G::SMEM, s>>>(a);
     k_segsum_fix<D, FUSE><<<(unsigned)a.nt, 128, 0, s>>>(a);
 }
 
@@ -535,19 +753,85 @@ int launch_segsum_bulk(int cfg, int D, const UpdateArgs &a, int num_sms, cudaStr
 
 void launch_csr_tiles(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt,
                       const int32_t *pack_gstart, const int32_t *pack_ustart, int32_t P, int32_t nt,
-                      int32_t *tile_start, cudaStream_t s) {
+                      int32_t *tile_start, cudaStream_t s, int32_t row_weight) {
     cudaMemsetAsync(long_cnt, 0, sizeof(int32_t) * P, s);
     if (N > 0)
         k_csr_tiles<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(sorted_u, N, ustart, pack_gstart, pack_ustart, P,
-                                                                nt, tile_start);
+                                                                nt, tile_start, row_weight);
 }
 
 // segment-sum fused with the optimizer (world == 1, D = 64 / 128); returns #launches (0: n/a)
+template <int D, int NW, int RS, int S, int NST>
+void launch_upd(const UpdateArgs &a, int num_sms, cudaStream_t s) {
+    using G = FG<D, RS, S, NST>;
+    const size_t smem = (size_t)NW * (G::META + G::WARPB);
+    ensure_dyn_smem((const void *)k_segsum_upd<D, NW, RS, S, NST>, smem);
+    (void)num_sms;
+    k_segsum_upd<D, NW, RS, S, NST><<<(unsigned)((a.nt + NW - 1) / NW), NW * 32, smem, s>>>(a);
+    k_segsum_fix<D, true><<<(unsigned)a.nt, 128, 0, s>>>(a);
+}
+
+// fused-kernel configuration (D = 128 Adagrad; PICASSO_FUSE_CFG for A/B): rows per stage x stages x warps
+static int fuse_cfg() {
+    static const int c = [] {
+        const char *e = std::getenv("PICASSO_FUSE_CFG");
+        if (!e) return 0;
+        if (!std::strcmp(e, "2x3x16")) return 1;
+        if (!std::strcmp(e, "4x3x11")) return 2;
+        if (!std::strcmp(e, "8x2x8")) return 3;
+        if (!std::strcmp(e, "2x2x16")) return 4;
+        if (!std::strcmp(e, "2x3x20")) return 0;
+        if (!std::strcmp(e, "4x2x14")) return 9;
+        if (!std::strcmp(e, "2x2x24")) return 6;
+        if (!std::strcmp(e, "1x4x24")) return 7;
+        if (!std::strcmp(e, "2x4x16")) return 8;
+        return 0;
+    }();
+    return c;
+}
+int segsum_upd_warps(int opt) {  // warps per CTA of the fused kernel (= its tiles per SM)
+    if (opt == 1) return 10;
+    switch (fuse_cfg()) {
+        case 1: return 16;
+        case 2: return 11;
+        case 3: return 8;
+        case 4: return 16;
+        case 6: return 24;
+        case 7: return 24;
+        case 8: return 16;
+        case 9: return 14;
+        default: return 20;  // 2 rows x 3 stages x 20 warps: the C2 sweep's best (0.239 ms / step)
+    }
+}
+
 int launch_segsum_fused(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
-    if (!a.tile_start || a.row_off || a.hslot || ((uintptr_t)a.dy & 15) || (a.dy_stride & 3)) return 0;
+    if (!a.tile_start || a.row_off || a.hslot || a.dst_off || ((uintptr_t)a.dy & 15) || (a.dy_stride & 3)) return 0;
+    if (a.nt != num_sms * segsum_upd_warps(a.opt)) return 0;  // tiles were cut for this kernel's warps
+    const bool adam = a.opt == 1;
     switch (D) {
-        case 64: launch_pipe<64, 16, 3, true>(a, num_sms, s); break;
-        case 128: launch_pipe<128, 16, 3, true>(a, num_sms, s); break;
+        case 64:
+            if (adam) launch_upd<64, 10, 8, 2, 2>(a, num_sms, s);
+            else if (segsum_upd_warps(0) == 20) launch_upd<64, 20, 4, 3, 1>(a, num_sms, s);
+            else if (segsum_upd_warps(0) == 14) launch_upd<64, 14, 8, 2, 1>(a, num_sms, s);
+            else return 0;
+            break;
+        case 128:
+            if (adam) {
+                launch_upd<128, 10, 4, 2, 2>(a, num_sms, s);
+            } else {
+                switch (fuse_cfg()) {
+                    case 1: launch_upd<128, 16, 2, 3, 1>(a, num_sms, s); break;
+                    case 2: launch_upd<128, 11, 4, 3, 1>(a, num_sms, s); break;
+                    case 3: launch_upd<128, 8, 8, 2, 1>(a, num_sms, s); break;
+                    case 4: launch_upd<128, 16, 2, 2, 1>(a, num_sms, s); break;
+                    case 6: launch_upd<128, 24, 2, 2, 1>(a, num_sms, s); break;
+                    case 7: launch_upd<128, 24, 1, 4, 1>(a, num_sms, s); break;
+                    case 8: launch_upd<128, 16, 2, 4, 1>(a, num_sms, s); break;
+                    case 9: launch_upd<128, 14, 4, 2, 1>(a, num_sms, s); break;
+                    default: launch_upd<128, 20, 2, 3, 1>(a, num_sms, s); break;
+                }
+            }
+            break;
         default: return 0;
     }
     return 2;

@@ -194,9 +194,10 @@ bool segsum_bulk_supported(int D, const UpdateArgs &a);
 int launch_segsum_bulk(int cfg, int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_csr_tiles(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt,
                       const int32_t *pack_gstart, const int32_t *pack_ustart, int32_t P, int32_t nt,
-                      int32_t *tile_start, cudaStream_t s);
+                      int32_t *tile_start, cudaStream_t s, int32_t row_weight = 1);
 size_t segsum_bulk_partial_doubles(int maxD, int num_sms);
 int launch_segsum_fused(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);  // 0: not applicable
+int segsum_upd_warps(int opt);  // warps per CTA (= tiles per SM) of the fused segment-sum + update
 size_t segsum_tile_ints(int P, int num_sms);
 size_t segsum_split_entries(int num_sms);
 

@@ -168,7 +168,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     }
     if (const char *e = std::getenv("PICASSO_BWD")) {
         c->split_bwd = std::strcmp(e, "fused") != 0;
-        c->fuse_pipe = std::strcmp(e, "fusepipe") == 0;
+        c->fuse_pipe = std::strcmp(e, "split") != 0 && std::strcmp(e, "fused") != 0;
     }
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM_SMALL")) c->flat_small = std::strcmp(e, "legacy") != 0;
@@ -195,7 +195,16 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
-    c->seg_nt = c->num_sms * segsum_pipe_warps(c->seg_cfg);
+    // fused segment-sum + optimizer (k_segsum_upd): world == 1, every tiled (D >= 64) pack of dim 64
+    // or 128 — the tiles are then cut for its warps per CTA
+    if (c->fuse_pipe) {
+        bool ok = world == 1;
+        for (int32_t d : c->pack_dim)
+            if (d >= 64 && d != 64 && d != 128) ok = false;
+        c->fuse_pipe = ok;
+    }
+    c->seg_nt = c->num_sms * (c->fuse_pipe ? segsum_upd_warps(opts->opt) : segsum_pipe_warps(c->seg_cfg));
+    if (const char *e = std::getenv("PICASSO_FUSE_RW")) c->fuse_rw = std::max(1, std::atoi(e));
     c->pool_sms = c->num_sms;
     c->ws_bytes = c->carve(nullptr);
     *out = c;
@@ -613,7 +622,7 @@ void picasso::transpose_join(picasso_ctx *ctx, cudaStream_t s) {
 void picasso::launch_csr_any(picasso_ctx *ctx, const int32_t *su, int64_t N, cudaStream_t s) {
     if (ctx->bulk_segsum)
         launch_csr_tiles(su, N, ctx->ustart, ctx->long_cnt, ctx->pack_gstart, ctx->pack_ustart, ctx->P, ctx->seg_nt,
-                         ctx->tile_start, s);
+                         ctx->tile_start, s, ctx->fuse_pipe ? ctx->fuse_rw : 1);
     else
         launch_csr_bounds(su, N, ctx->ustart, ctx->long_cnt, ctx->P, s);
 }

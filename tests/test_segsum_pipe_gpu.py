@@ -145,7 +145,7 @@ def test_pool_pipe_mean_and_all_empty_pack():
 
 
 # ---- alternative paths behind environment switches (read when the context is created) ---------
-@pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "0"}, {"PICASSO_BWD": "fusepipe"}, {"PICASSO_POOL": "flat"},
+@pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "0"}, {"PICASSO_BWD": "split"}, {"PICASSO_POOL": "flat"},
                                  {"PICASSO_OVERLAP": "0"}, {"PICASSO_OVERLAP": "1"}, {"PICASSO_SEGSUM_CFG": "12x4"},
                                  {"PICASSO_DEDUP_REGIONS": "1"}, {"PICASSO_SEGSUM_SMALL": "legacy"},
                                  {"PICASSO_SORT": "3"}, {"PICASSO_SORT": "2"}])
