@@ -42,6 +42,9 @@ from .abi import (  # noqa: F401
     picasso_dinterleave_stats,
     picasso_interleave_capacity,
     picasso_pack_plan_kinterleave,
+    picasso_nvls_create,
+    picasso_nvls_open,
+    picasso_nvls_bind,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
 from .embedding import LoopbackGroup, PackedEmbedding  # noqa: F401

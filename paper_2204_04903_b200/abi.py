@@ -25,7 +25,8 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_group_hot_cache_refresh", "picasso_get_hot_keys", "picasso_p2p_handle", "picasso_p2p_open",
            "picasso_group_p2p", "picasso_get_send_list", "picasso_micro_batch_size", "picasso_dinterleave_begin",
            "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply", "picasso_dinterleave_stats",
-           "picasso_interleave_capacity", "picasso_pack_plan_kinterleave"]
+           "picasso_interleave_capacity", "picasso_pack_plan_kinterleave", "picasso_nvls_create", "picasso_nvls_open",
+           "picasso_nvls_bind"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -102,6 +103,9 @@ def lib():
             "picasso_dinterleave_apply": [vp, C.c_float, i64, vp],
             "picasso_dinterleave_stats": [vp, C.POINTER(i64), C.POINTER(i64)],
             "picasso_interleave_capacity": [i32, vp, vp, C.POINTER(C.c_double)],
+            "picasso_nvls_create": [vp, vp],
+            "picasso_nvls_open": [vp, vp],
+            "picasso_nvls_bind": [vp],
             "picasso_pack_plan_kinterleave": [i32, vp, i32, vp, vp, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp,
                                               C.POINTER(i32), C.POINTER(i32)],
         }
@@ -494,3 +498,19 @@ def picasso_dinterleave_stats(ctx):
     r, f = C.c_int64(), C.c_int64()
     _chk(lib().picasso_dinterleave_stats(ctx, C.byref(r), C.byref(f)), "picasso_dinterleave_stats", ctx)
     return r.value, f.value
+
+
+# ---- NVLS multicast of the hot-row gradients (include/picasso.h 7b) -----------------------
+def picasso_nvls_create(ctx):
+    buf = (C.c_uint8 * 64)()
+    _chk(lib().picasso_nvls_create(ctx, buf), "picasso_nvls_create", ctx)
+    return bytes(buf)
+
+
+def picasso_nvls_open(ctx, handle):
+    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+    _chk(lib().picasso_nvls_open(ctx, buf), "picasso_nvls_open", ctx)
+
+
+def picasso_nvls_bind(ctx):
+    _chk(lib().picasso_nvls_bind(ctx), "picasso_nvls_bind", ctx)

@@ -119,6 +119,10 @@ struct MultiState {
     int32_t *dtab = nullptr;            // [rows_total * W] owner position of (owned row, source), or -1
     int32_t *dst_rank = nullptr;
     size_t win_ogbuf = 0;
+    // ---- NVLS multicast of the hot-row gradients (nvls.cu)
+    bool nvls = false;
+    unsigned long long nvls_mc = 0, nvls_uc = 0, nvls_uva = 0, nvls_mva = 0;  // driver handles / VAs
+    size_t nvls_bytes = 0, nvls_touch_off = 0;
 };
 
 struct picasso_ctx {

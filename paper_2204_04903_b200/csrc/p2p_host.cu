@@ -40,6 +40,7 @@ picasso_status mfwd_d(picasso_ctx *ctx, float *out, cudaStream_t s);
 picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
 picasso_status hot_allreduce_group(std::vector<picasso_ctx *> &cs, cudaStream_t s);
 picasso_status hot_update_all(picasso_ctx *ctx, float lr, float ss, cudaStream_t s);
+picasso_status nvls_allreduce(picasso_ctx *ctx, cudaStream_t s);  // nvls.cu
 UpdateArgs mbwd_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t step, cudaStream_t s);
 int mbwd_segsum_pack(picasso_ctx *ctx, UpdateArgs u, int p, cudaStream_t s);
 namespace picasso {
@@ -324,7 +325,10 @@ picasso_status multi_bwd_p2p(picasso_ctx *ctx, const float *grad_out, float lr, 
     }
     if ((st = mbwd_e(ctx, grad_out, lr, step, s))) return st;
     barrier(ctx, 2, s);
-    if (mp.hot_k > 0) {  // HybridHash: hot-row gradients and occurrence counts summed over ranks
+    if (mp.hot_k > 0 && mp.nvls) {  // HybridHash over NVLS: in-switch reduce + multicast broadcast
+        if ((st = nvls_allreduce(ctx, s))) return st;
+        barrier(ctx, 3, s);  // every rank's broadcast landed before any hot-row update reads it
+    } else if (mp.hot_k > 0) {  // HybridHash: hot-row gradients and occurrence counts summed over ranks
         PNCK(ncclGroupStart());
         PNCK(ncclAllReduce(mp.hot_g, mp.hot_g, mp.hot_g_floats, ncclFloat32, ncclSum, mp.comm, s));
         PNCK(ncclAllReduce(mp.hot_touch, mp.hot_touch, mp.hot_k, ncclFloat32, ncclSum, mp.comm, s));

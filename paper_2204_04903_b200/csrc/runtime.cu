@@ -10,6 +10,7 @@
 #include "ctx.h"
 
 void p2p_release(picasso_ctx *ctx);  // p2p_host.cu
+void nvls_release(picasso_ctx *ctx);  // nvls.cu
 
 #define CK(x)                                                             \
     do {                                                                  \
@@ -342,6 +343,7 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
 
 extern "C" picasso_status picasso_ctx_destroy(picasso_ctx *ctx) {
     if (!ctx) return PICASSO_OK;
+    if (ctx->mp.nvls_mc) nvls_release(ctx);
     p2p_release(ctx);
     if (ctx->side) {
         cudaStreamDestroy(ctx->side);

@@ -2,6 +2,8 @@
 rank's context and forwards to the C ABI.  Plumbing only — every step runs in libpicasso."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -84,6 +86,33 @@ class PackedEmbedding:
                     dist.all_gather_object(out, x)
                     return out
             abi.picasso_p2p_open(self.ctx, all_gather(h))
+            # HybridHash hot-row gradients over NVLS multicast (PICASSO_NVLS=0: keep NCCL's AllReduce)
+            self.nvls = False
+            if cache_max_bytes > 0 and nccl_uid is not None and os.environ.get("PICASSO_NVLS", "1") != "0":
+                self.nvls = self._nvls_setup(all_gather)
+
+    def _nvls_setup(self, all_gather):
+        """Collective: every rank runs the same calls; any failure on any rank leaves all ranks on the
+        NCCL AllReduce (the agreement goes through all_gather)."""
+        ok, h = True, b"\0" * 64
+        try:
+            h = abi.picasso_nvls_create(self.ctx)
+        except abi.PicassoError:
+            ok = False
+        res = all_gather((ok, h))
+        if not all(r[0] for r in res):
+            return False
+        try:
+            abi.picasso_nvls_open(self.ctx, res[0][1])
+        except abi.PicassoError:
+            ok = False
+        if not all(all_gather(ok)):  # also the barrier between every rank's open and any bind
+            return False
+        try:
+            abi.picasso_nvls_bind(self.ctx)
+        except abi.PicassoError:
+            ok = False
+        return all(all_gather(ok))
 
     @property
     def n_packs(self):

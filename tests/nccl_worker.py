@@ -80,7 +80,11 @@ def main():
                            world=world)
     m, tabs = oracle_model(cfg), oracle_tables(cfg)
     acc = [np.full_like(t, 0.1) for t in tabs]
-    report = {"rank": rank, "world": world, "ok": False}
+    report = {"rank": rank, "world": world, "ok": False, "nvls": bool(getattr(e, "nvls", False))}
+    if cache and e.exchange == "p2p" and os.environ.get("PICASSO_NVLS", "1") != "0":
+        # the hot-row gradients must go through the NVLS multicast reduce (B200 NVSwitch), not NCCL
+        assert e.nvls, "NVLS multicast setup failed on a multicast-capable box"
+
     gr = None
     for step in (1, 2, 3):
         bstep = 1 if graph else step

@@ -27,5 +27,7 @@ def test_nccl_sharded_parity(name, exchange):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "nccl_worker.py"), name]
     env = {**os.environ, "PICASSO_EXCHANGE": exchange}
+    if name.endswith("_cache") and exchange == "nccl":
+        env["PICASSO_NVLS"] = "0"
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
