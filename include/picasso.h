@@ -362,16 +362,18 @@ picasso_status picasso_dinterleave_stats(picasso_ctx *ctx, int64_t *rows, int64_
  * multicast-bound buffer; after the backward barrier every rank reduces 1/W of it inside the
  * NVSwitch (multimem.ld_reduce) and broadcasts the sums to all ranks (multimem.st), then a second
  * barrier.  Collective setup, in this order on every rank (after picasso_p2p_open):
- *   picasso_nvls_create : rank 0 creates the multicast object and writes its 64-byte fabric handle
- *                         to handle_out (other ranks: zeros); every rank sizes the buffer.
- *   picasso_nvls_open   : handle = rank 0's bytes; imports it and adds this rank's device.
+ *   picasso_nvls_create : rank 0 creates the multicast object and exports it as a POSIX file
+ *                         descriptor (*fd_out; other ranks: -1); every rank sizes the buffer.
+ *   (the caller passes rank 0's descriptor to the other processes, e.g. SCM_RIGHTS)
+ *   picasso_nvls_open   : fd = that descriptor in this process (ignored on rank 0); imports the
+ *                         object and adds this rank's device.
  *   (a host barrier: every rank has opened)
  *   picasso_nvls_bind   : binds this rank's device memory, maps the unicast and multicast views,
  *                         and routes the hot-row gradients there.
  * PICASSO_ERR_CUDA when the GPUs / driver lack multicast or fabric handles: the step then keeps
  * the NCCL AllReduce. */
-picasso_status picasso_nvls_create(picasso_ctx *ctx, void *handle_out);
-picasso_status picasso_nvls_open(picasso_ctx *ctx, const void *handle);
+picasso_status picasso_nvls_create(picasso_ctx *ctx, int32_t *fd_out);
+picasso_status picasso_nvls_open(picasso_ctx *ctx, int32_t fd);
 picasso_status picasso_nvls_bind(picasso_ctx *ctx);
 picasso_status picasso_p2p_handle(picasso_ctx *ctx, void *handle_out);
 picasso_status picasso_p2p_open(picasso_ctx *ctx, const void *handles);

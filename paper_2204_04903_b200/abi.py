@@ -103,8 +103,8 @@ def lib():
             "picasso_dinterleave_apply": [vp, C.c_float, i64, vp],
             "picasso_dinterleave_stats": [vp, C.POINTER(i64), C.POINTER(i64)],
             "picasso_interleave_capacity": [i32, vp, vp, C.POINTER(C.c_double)],
-            "picasso_nvls_create": [vp, vp],
-            "picasso_nvls_open": [vp, vp],
+            "picasso_nvls_create": [vp, C.POINTER(i32)],
+            "picasso_nvls_open": [vp, i32],
             "picasso_nvls_bind": [vp],
             "picasso_pack_plan_kinterleave": [i32, vp, i32, vp, vp, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp,
                                               C.POINTER(i32), C.POINTER(i32)],
@@ -502,14 +502,14 @@ def picasso_dinterleave_stats(ctx):
 
 # ---- NVLS multicast of the hot-row gradients (include/picasso.h 7b) -----------------------
 def picasso_nvls_create(ctx):
-    buf = (C.c_uint8 * 64)()
-    _chk(lib().picasso_nvls_create(ctx, buf), "picasso_nvls_create", ctx)
-    return bytes(buf)
+    """Rank 0: the multicast object's POSIX file descriptor; other ranks: -1."""
+    fd = C.c_int32(-1)
+    _chk(lib().picasso_nvls_create(ctx, C.byref(fd)), "picasso_nvls_create", ctx)
+    return fd.value
 
 
-def picasso_nvls_open(ctx, handle):
-    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
-    _chk(lib().picasso_nvls_open(ctx, buf), "picasso_nvls_open", ctx)
+def picasso_nvls_open(ctx, fd):
+    _chk(lib().picasso_nvls_open(ctx, int(fd)), "picasso_nvls_open", ctx)
 
 
 def picasso_nvls_bind(ctx):

@@ -13,11 +13,12 @@
 // rank's hot-row update reads them.
 //
 // Setup (host, once, collective over the ranks): rank 0 creates the multicast object and exports
-// a fabric handle (picasso_nvls_create); every rank imports it and adds its device
-// (picasso_nvls_open); after all ranks have opened, each binds its own device memory and maps the
-// unicast and multicast views (picasso_nvls_bind).  Requires multicast-capable NVSwitch GPUs
-// (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED) and fabric handles; the caller falls back to the
-// NCCL AllReduce when any call fails.
+// it as a POSIX file descriptor (picasso_nvls_create); the caller passes the descriptor to the other
+// ranks' processes (SCM_RIGHTS over a Unix socket, embedding.py); every rank imports it and adds its
+// device (picasso_nvls_open); after all ranks have opened, each binds its own device memory and
+// maps the unicast and multicast views (picasso_nvls_bind).  Requires multicast-capable NVSwitch
+// GPUs (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED); the caller falls back to the NCCL AllReduce when
+// any call fails.
 #include <cuda.h>
 
 #include <cstring>
@@ -147,40 +148,48 @@ static void nvls_sizes(picasso_ctx *ctx, size_t gran) {
     mp.nvls_bytes = (raw + gran - 1) / gran * gran;
 }
 
-extern "C" picasso_status picasso_nvls_create(picasso_ctx *ctx, void *handle_out) {
+extern "C" picasso_status picasso_nvls_create(picasso_ctx *ctx, int32_t *fd_out) {
     picasso_status st = nvls_check(ctx);
     if (st) return st;
-    if (!handle_out) return PICASSO_ERR_INVALID_ARG;
-    std::memset(handle_out, 0, sizeof(CUmemFabricHandle));
+    if (!fd_out) return PICASSO_ERR_INVALID_ARG;
+    *fd_out = -1;
     MultiState &mp = ctx->mp;
     CUmulticastObjectProp prop{};
     prop.numDevices = (unsigned)ctx->world;
-    prop.handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+    prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     prop.size = 1;
-    size_t gran = 0;
-    DRV(MulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-    nvls_sizes(ctx, gran);
-    if (ctx->rank != 0) return PICASSO_OK;  // rank 0 creates; the others import its handle
+    // one size for the multicast object and every rank's bound allocation: a multiple of both the
+    // multicast and the device-allocation granularity
+    size_t gran = 0, agran = 0;
+    DRV(MulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_MINIMUM));
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return PICASSO_ERR_CUDA;
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = dev;
+    DRV(MemGetAllocationGranularity(&agran, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+    nvls_sizes(ctx, std::max(gran, agran));
+    if (ctx->rank != 0) return PICASSO_OK;  // rank 0 creates; the others import its descriptor
     prop.size = mp.nvls_bytes;
     CUmemGenericAllocationHandle mc;
     DRV(MulticastCreate(&mc, &prop));
     mp.nvls_mc = (unsigned long long)mc;
-    CUmemFabricHandle fh;
-    DRV(MemExportToShareableHandle(&fh, mc, CU_MEM_HANDLE_TYPE_FABRIC, 0));
-    std::memcpy(handle_out, &fh, sizeof(fh));
+    int fd = -1;
+    DRV(MemExportToShareableHandle(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    *fd_out = fd;
     return PICASSO_OK;
 }
 
-extern "C" picasso_status picasso_nvls_open(picasso_ctx *ctx, const void *handle) {
+extern "C" picasso_status picasso_nvls_open(picasso_ctx *ctx, int32_t fd) {
     picasso_status st = nvls_check(ctx);
     if (st) return st;
-    if (!handle) return PICASSO_ERR_INVALID_ARG;
     MultiState &mp = ctx->mp;
     if (ctx->rank != 0) {
-        CUmemFabricHandle fh;
-        std::memcpy(&fh, handle, sizeof(fh));
+        if (fd < 0) return PICASSO_ERR_INVALID_ARG;
         CUmemGenericAllocationHandle mc;
-        DRV(MemImportFromShareableHandle(&mc, &fh, CU_MEM_HANDLE_TYPE_FABRIC));
+        DRV(MemImportFromShareableHandle(&mc, reinterpret_cast<void *>((uintptr_t)fd),
+                                         CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
         mp.nvls_mc = (unsigned long long)mc;
     }
     int dev = 0;
@@ -200,13 +209,20 @@ extern "C" picasso_status picasso_nvls_bind(picasso_ctx *ctx) {
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = dev;
-    size_t agran = 0;
-    DRV(MemGetAllocationGranularity(&agran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
-    mp.nvls_bytes = (mp.nvls_bytes + agran - 1) / agran * agran;
-    CUmemGenericAllocationHandle uc;
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // as the multicast object
+    CUmemGenericAllocationHandle uc;  // nvls_bytes: the multicast object's size (picasso_nvls_create)
     DRV(MemCreate(&uc, mp.nvls_bytes, &ap, 0));
     mp.nvls_uc = (unsigned long long)uc;
-    DRV(MulticastBindMem((CUmemGenericAllocationHandle)mp.nvls_mc, 0, uc, 0, mp.nvls_bytes, 0));
+    {
+        const CUresult r = drv().MulticastBindMem((CUmemGenericAllocationHandle)mp.nvls_mc, 0, uc, 0, mp.nvls_bytes, 0);
+        if (r != CUDA_SUCCESS) {
+            const char *m = nullptr;
+            drv().GetErrorString(r, &m);
+            ctx->last_msg = std::string("cuMulticastBindMem: ") + (m ? m : "?") + " (bytes " +
+                            std::to_string(mp.nvls_bytes) + ")";
+            return PICASSO_ERR_CUDA;
+        }
+    }
     CUdeviceptr uva = 0, mva = 0;
     DRV(MemAddressReserve(&uva, mp.nvls_bytes, 0, 0, 0));
     DRV(MemMap(uva, mp.nvls_bytes, 0, uc, 0));

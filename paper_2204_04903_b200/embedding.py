@@ -93,25 +93,57 @@ class PackedEmbedding:
 
     def _nvls_setup(self, all_gather):
         """Collective: every rank runs the same calls; any failure on any rank leaves all ranks on the
-        NCCL AllReduce (the agreement goes through all_gather)."""
-        ok, h = True, b"\0" * 64
-        try:
-            h = abi.picasso_nvls_create(self.ctx)
-        except abi.PicassoError:
-            ok = False
-        res = all_gather((ok, h))
+        NCCL AllReduce (the agreement goes through all_gather).  Rank 0's multicast descriptor reaches
+        the other processes over an abstract Unix socket (SCM_RIGHTS)."""
+        import secrets
+        import socket
+        import sys
+
+        def attempt(fn, *args):
+            try:
+                return True, fn(self.ctx, *args)
+            except abi.PicassoError as err:
+                print(f"[picasso] rank {self.rank}: NVLS off ({err}); hot rows use the NCCL AllReduce",
+                      file=sys.stderr)
+                return False, None
+
+        ok, fd = attempt(abi.picasso_nvls_create)
+        srv, name = None, b""
+        if ok and self.rank == 0:
+            name = b"\0picasso-nvls-" + secrets.token_hex(8).encode()
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(name)
+            srv.listen(self.world)
+        res = all_gather((ok, name))
         if not all(r[0] for r in res):
+            if srv:
+                srv.close()
             return False
         try:
-            abi.picasso_nvls_open(self.ctx, res[0][1])
-        except abi.PicassoError:
+            if self.rank == 0:
+                for _ in range(self.world - 1):
+                    conn, _ = srv.accept()
+                    socket.send_fds(conn, [b"f"], [fd])
+                    conn.close()
+                srv.close()
+                myfd = fd
+            else:
+                cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                cli.connect(res[0][1])
+                _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+                cli.close()
+                myfd = fds[0]
+        except OSError as err:
+            print(f"[picasso] rank {self.rank}: NVLS off (descriptor exchange: {err})", file=sys.stderr)
             ok = False
+        if not all(all_gather(ok)):
+            return False
+        ok, _ = attempt(abi.picasso_nvls_open, myfd)
+        if self.rank != 0:
+            os.close(myfd)  # the driver holds its own reference after the import
         if not all(all_gather(ok)):  # also the barrier between every rank's open and any bind
             return False
-        try:
-            abi.picasso_nvls_bind(self.ctx)
-        except abi.PicassoError:
-            ok = False
+        ok, _ = attempt(abi.picasso_nvls_bind)
         return all(all_gather(ok))
 
     @property
