@@ -535,11 +535,14 @@ def main():
         emb.forward(ids, off, B, out, stream=s)
         emb.backward_update(dys[i % args.nbatches], lr, step=i + 1, stream=s)
         itr = i + 1  # Alg. 1 schedule (reading O13): refresh after bwd when itr >= warmup, itr % flush == 0
-        if world > 1 and args.cache_bytes > 0 and itr >= args.cache_warmup and itr % args.cache_flush == 0:
+        # (--cache-flush 0: one refresh, at itr == warmup — the steady state of a hot set, no refresh cost)
+        due = (itr % args.cache_flush == 0) if args.cache_flush > 0 else itr == args.cache_warmup
+        if world > 1 and args.cache_bytes > 0 and itr >= args.cache_warmup and due:
             cache_stats.update(emb.hot_cache_refresh(args.cache_bytes, stream=s))
 
     if world > 1 and args.cache_bytes > 0:  # the first refresh and a hot step happen before timing
         args.warmup = max(args.warmup, max(args.cache_flush, args.cache_warmup) + 1)
+    hot_refresh_off = world > 1 and args.cache_bytes > 0 and args.cache_flush == 0
     for i in range(args.warmup):
         step(i, stream)
     emb.check()
@@ -554,7 +557,8 @@ def main():
     # they cost ~26 us per step of inter-node gaps at C2 (0.320 vs 0.293 ms).  A second pass of K
     # steps records them (same graph without vs with the event nodes; eager: profiling on), and
     # its step time is reported beside the timed one.
-    use_graph = not args.eager and (world == 1 or (emb.exchange == "p2p" and not args.cache_bytes))
+    # (a hot set that no longer changes — --cache-flush 0 — keeps the step capturable)
+    use_graph = not args.eager and (world == 1 or (emb.exchange == "p2p" and (not args.cache_bytes or hot_refresh_off)))
     graphs, graphs_t = {}, []
     if use_graph:
         # timed pass: one captured step per pre-generated batch (--nbatches), replayed round robin;

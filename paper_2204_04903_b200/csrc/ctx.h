@@ -177,7 +177,7 @@ struct picasso_ctx {
     int32_t seg_nt = 0;       // its tiles per pack
     int32_t *tile_start = nullptr;
     int4 *split = nullptr;
-    bool split_bwd = true;  // PICASSO_BWD=fused selects the legacy fused segsum+update kernel
+    bool split_bwd = true;  // the backward keeps a G buffer (k_segsum* -> k_update_rows, the long rows, D-Interleaving)
     int fuse_rw = 3;        // fused backward: tile cost of a row in occurrences (PICASSO_FUSE_RW; C2 sweep)
     bool fuse_pipe = true;   // W = 1, tiled packs of D = 64 / 128: k_segsum_upd, the pipelined segment-sum
                              // with each row's weight / state prefetched into a shared-memory ring and

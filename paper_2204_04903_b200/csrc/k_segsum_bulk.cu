@@ -229,17 +229,13 @@ __global__ void k_csr_tiles(const int32_t *su, int64_t N, int32_t *ustart, const
         for (int64_t kk = k + 1; kk <= nt; ++kk) ts[kk] = (int32_t)G1;
 }
 
-// FUSE (world == 1, D <= 128): the optimizer runs at the row's flush instead of writing G —
-// the row's weight / state loads are issued at its flush and consumed at the next flush (one
-// row in flight per warp), so no G buffer round trip and no separate update kernel.
-template <int D, int NW, int S, bool FUSE>
+template <int D, int NW, int S>
 __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     using G = BG<D, NW, S>;
     constexpr int RS = G::RS, SB = G::SB, ROWB = G::ROWB, EPL = G::EPL;
     constexpr int CH = RS < kConsumeRows ? RS : kConsumeRows;
     extern __shared__ __align__(128) unsigned char smem[];
-    int64_t *s_row = reinterpret_cast<int64_t *>(smem);
-    int32_t *s_uid = reinterpret_cast<int32_t *>(smem + (size_t)NW * S * RS * 8);
+    int32_t *s_uid = reinterpret_cast<int32_t *>(smem + (size_t)NW * S * RS * 8);  // (after an unused 8-B slot per row)
     int32_t *s_len = s_uid + NW * S * RS;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
@@ -252,7 +248,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     if (pa >= pb) return;
 
     int32_t *wu = s_uid + w * S * RS, *wl = s_len + w * S * RS;
-    int64_t *wrow = s_row + w * S * RS;
     unsigned char *wr = smem + G::RING_OFF + (size_t)w * S * SB;
     float *gp = a.gbuf + a.pack_gbase[a.pack];
     const float4 *dy4 = reinterpret_cast<const float4 *>(a.dy);
@@ -269,8 +264,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
     // lane l holds position base + l of a 32-position round: dY row (float4 units), uid, bag length
     uint32_t off_c, off_n;
     int32_t uid_c, uid_n, len_c, len_n;
-    int64_t row_c = 0, row_n = 0;  // FUSE: the table row of the position's unique key
-    auto resolve = [&](int32_t base, uint32_t &off, int32_t &uid, int32_t &len, int64_t &row) {
+    auto resolve = [&](int32_t base, uint32_t &off, int32_t &uid, int32_t &len) {
         const int32_t p = base + lane;
         off = 0;
         uid = -1;
@@ -281,11 +275,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
             const int32_t f = seg / a.B;
             off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col) >> 2);
             if (a.pool_mean) len = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
-            if constexpr (FUSE) row = (int64_t)(__ldg(a.unique_gkey + uid) - (unsigned long long)a.pack_key_off);
         }
     };
-    resolve(pa, off_c, uid_c, len_c, row_c);
-    resolve(pa + 32, off_n, uid_n, len_n, row_n);
+    resolve(pa, off_c, uid_c, len_c);
+    resolve(pa + 32, off_n, uid_n, len_n);
     int32_t round_c = 0;
     auto issue = [&](int32_t k) {  // stage k -> ring slot k % S
         const int slot = k % S;
@@ -294,9 +287,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
             off_c = off_n;
             uid_c = uid_n;
             len_c = len_n;
-            row_c = row_n;
             round_c = r;
-            resolve(pa + (r + 1) * 32, off_n, uid_n, len_n, row_n);
+            resolve(pa + (r + 1) * 32, off_n, uid_n, len_n);
         }
         const int32_t p0 = pa + k * RS;
         const int nrows = pb - p0 < RS ? pb - p0 : RS;
@@ -325,7 +317,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
         if (i >= 0 && i < nrows) {
             wu[slot * RS + i] = uid_c;
             wl[slot * RS + i] = len_c;
-            if constexpr (FUSE) wrow[slot * RS + i] = row_c;
         }
     };
 
@@ -333,35 +324,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.0;
     int32_t cur = -1, ncur = 0;  // current row, its occurrences in this tile (= all of them if unsplit)
-    int64_t cur_row = 0;
-    // FUSE: the previous finished row, its G and its weight / state (loads in flight)
-    int64_t pend = -1;
-    float pg[EPL], pw[EPL], ps1[EPL], ps2[EPL];
-    auto finish_pending = [&]() {
-        if constexpr (FUSE) {
-            if (pend < 0) return;
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) opt_step(a, pg[e], pw[e], ps1[e], ps2[e]);
-            lane_gstore<D>(a.weight + pend, lane, pw);
-            lane_gstore<D>(a.state1 + pend, lane, ps1);
-            if (a.opt == 1) lane_gstore<D>(a.state2 + pend, lane, ps2);
-            pend = -1;
-        }
-    };
     auto flush = [&](int32_t u) {
         double *part = reinterpret_cast<double *>(a.partial);
         if (u == hp) {
             lane_store_f64<D>(part + (int64_t)(2 * t) * D, lane, acc);
         } else if (u == tp) {
             lane_store_f64<D>(part + (int64_t)(2 * t + 1) * D, lane, acc);
-        } else if constexpr (FUSE) {
-            finish_pending();
-            pend = cur_row * D;
-            lane_gload<D>(a.weight + pend, lane, pw);
-            lane_gload<D>(a.state1 + pend, lane, ps1);
-            if (a.opt == 1) lane_gload<D>(a.state2 + pend, lane, ps2);
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) pg[e] = __double2float_rn(acc[e]);
         } else {
             lane_store_f32<D>(g_dst<D>(a, u, u0, gp, lane, (float)ncur), lane, acc);
         }
@@ -398,7 +366,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
                     if (uid != cur) {
                         if (cur >= 0) flush(cur);
                         cur = uid;
-                        if constexpr (FUSE) cur_row = wrow[slot * RS + i];
                         ncur = 0;
                     }
                     ++ncur;
@@ -417,7 +384,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
         ldgsts_commit();
     }
     if (cur >= 0) flush(cur);
-    finish_pending();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -702,13 +668,13 @@ __global__ void __launch_bounds__(128) k_segsum_fix(UpdateArgs a) {
     }
 }
 
-template <int D, int NW, int S, bool FUSE = false>
+template <int D, int NW, int S>
 void launch_pipe(const UpdateArgs &a, int num_sms, cudaStream_t s) {
     using G = BG<D, NW, S>;
-    ensure_dyn_smem((const void *)k_segsum_pipe<D, NW, S, FUSE>, G::SMEM);
+    ensure_dyn_smem((const void *)k_segsum_pipe<D, NW, S>, G::SMEM);
     (void)num_sms;  // one warp per tile: the grid covers the ctx's nt tiles
-    k_segsum_pipe<D, NW, S, FUSE><<<(unsigned)((a.nt + NW - 1) / NW), NW * 32, G::SMEM, s>>>(a);
-    k_segsum_fix<D, FUSE><<<(unsigned)a.nt, 128, 0, s>>>(a);
+    k_segsum_pipe<D, NW, S><<<(unsigned)((a.nt + NW - 1) / NW), NW * 32, G::SMEM, s>>>(a);
+    k_segsum_fix<D, false><<<(unsigned)a.nt, 128, 0, s>>>(a);
 }
 
 template <int D>

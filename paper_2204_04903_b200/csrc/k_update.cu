@@ -6,21 +6,15 @@
 // The optimizer (north star; readings O9/O10) then updates each touched row once:
 //   Adagrad   acc += G*G;  w -= lr * (G / (sqrt(acc) + eps))
 //   lazy Adam m += (G-m)(1-b1); v += (G*G-v)(1-b2); w -= ss * (m / (sqrt(v) + eps))
-// Fusing the two keeps G in registers: per touched row the kernel reads its dY rows once and
-// the weight/state rows once, and writes weight/state once (no G round trip through HBM).
 // Each contribution is formed in fp32 (dY, dY/len), accumulated in fp64 and rounded once
 // (reading O6): G = fp32(exact sum) whatever the summation order, so the chunked hot-row
 // path and the oracle agree even when G nearly cancels.
 //
 //   k_csr_bounds     : row boundaries in the uid-sorted occurrence list (ustart)
-//   k_segsum_update  : a warp owns the rows that start in its tile of occurrence positions
-//                      (one tile per warp: balanced under Zipf skew); each LANES-wide row group
-//                      takes RT rows at a time: their weight/state rows are staged in shared
-//                      memory with cp.async while the group walks their occurrences as one
-//                      flattened stream (dY addresses resolved one per lane and broadcast, U dY
-//                      rows in flight); a row's optimizer step runs from shared memory the
-//                      moment its occurrences end.  Rows with > kLongRow occurrences are
-//                      deferred to the chunked path.
+//   k_segsum         : (narrow packs, D < 64) a warp walks the rows that start in its tile of
+//                      occurrence positions and writes their rounded G (the fused / pipelined
+//                      backward of D >= 64 lives in k_segsum_bulk.cu); rows with > kLongRow
+//                      occurrences are deferred to the chunked path.
 //   k_long_plan      : chunk counts (kChunk occurrences per chunk) of the deferred rows + scan
 //   k_long_partial   : one row group per chunk -> fp64 partial sums (all chunks in parallel:
 //                      a Zipf head with 1e5 occurrences is spread over the whole GPU)
@@ -181,207 +175,12 @@ __device__ __forceinline__ int32_t row_at_or_after(const int32_t *su, int32_t p,
     return (p == P0 || __ldg(su + p - 1) != u) ? u : u + 1;
 }
 
-template <int D>
-struct SegGeo {
-    static constexpr int RT = D <= 128 ? 4 : 2;                  // rows per group per sub-tile
-    static constexpr int ROWS = Geo<D>::R * RT;                  // rows per warp sub-tile
-    static constexpr int NST = 4;                                // staged: w, s1, s2, G
-    // shared bytes per warp: descriptors + staged weight/state rows of one sub-tile
-    static constexpr int STAGE_F4 = ROWS * NST * (D / 4);
-};
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-template <int D>
-__global__ void __launch_bounds__(256, 2) k_segsum_update(UpdateArgs a) {
-    using Gm = Geo<D>;
-    constexpr int LANES = Gm::LANES, VPL = Gm::VPL, R = Gm::R, U = Gm::U;
-    constexpr int RT = SegGeo<D>::RT, ROWS = SegGeo<D>::ROWS, V4 = D / 4;
-    constexpr int PPL = U > LANES ? U / LANES : 1, RND = LANES * PPL;
-    __shared__ int32_t s_i0[8][ROWS], s_n[8][ROWS], s_cum[8][R][RT + 1];
-    __shared__ int64_t s_row[8][ROWS];
-    extern __shared__ float4 s_stage[];  // [8 warps][ROWS][3][V4]: staged w, s1, s2 rows
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int li = lane % LANES, grp = lane / LANES;
-    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
-    float4 *stage = s_stage + (size_t)w * SegGeo<D>::STAGE_F4;
-    const int32_t u0 = a.pack_ustart[a.pack], u1 = a.pack_ustart[a.pack + 1];
-    if (u1 <= u0) return;
-    const int32_t P0 = __ldg(a.ustart + u0), P1 = __ldg(a.ustart + u1);
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int nst = a.opt == 1 ? 3 : 2;
-    // a warp owns the rows that START inside its tile of occurrence positions (tiles sized so
-    // every warp gets one); rows have <= kLongRow occurrences here, so the work is balanced
-    int64_t tile = ((int64_t)(P1 - P0) + nwarps - 1) / nwarps;
-    tile = tile < 128 ? 128 : tile;
-    for (int64_t pa = P0 + ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * tile; pa < P1; pa += nwarps * tile) {
-        const int64_t pb = pa + tile < P1 ? pa + tile : P1;
-        const int32_t ua = row_at_or_after(a.sorted_u, (int32_t)pa, P0);
-        const int32_t ub = pb == P1 ? u1 : row_at_or_after(a.sorted_u, (int32_t)pb, P0);
-        for (int32_t t0 = ua; t0 < ub; t0 += ROWS) {
-            // ---- sub-tile rows: ranges (long rows -> empty, deferred), group-local prefix
-            for (int x = lane; x < ROWS; x += 32) {
-                const int32_t u = t0 + x;
-                int32_t i0 = 0, n = 0;
-                int64_t row = -1;
-                if (u < ub) {
-                    i0 = __ldg(a.ustart + u);
-                    n = __ldg(a.ustart + u + 1) - i0;
-                    if (n > kLongRow) {  // Zipf head: chunked path
-                        a.long_list[atomicAdd(a.long_cnt, 1)] = u;
-                        n = 0;
-                    } else {
-                        row = (int64_t)(a.unique_gkey[u] - (unsigned long long)a.pack_key_off);
-                    }
-                }
-                s_i0[w][x] = i0;
-                s_n[w][x] = n;
-                s_row[w][x] = row;
-            }
-            __syncwarp();
-            const int rbase = grp * RT;
-            // ---- stage the group's RT weight/state rows in shared memory (cp.async, 16 B per
-            // lane per row per array; each lane copies exactly the columns it will update, so it
-            // only waits for its own copies) — overlaps with the dY walk below
-#pragma unroll
-            for (int r = 0; r < RT; ++r) {
-                const int64_t row = s_row[w][rbase + r];
-                if (row >= 0) {
-                    const int64_t o = row * D + li * 4;
-                    float4 *st = stage + (size_t)(rbase + r) * SegGeo<D>::NST * V4 + li;
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) {
-                        cp_async16(st + q * LANES, a.weight + o + q * LANES * 4);
-                        cp_async16(st + V4 + q * LANES, a.state1 + o + q * LANES * 4);
-                        if (nst == 3) cp_async16(st + 2 * V4 + q * LANES, a.state2 + o + q * LANES * 4);
-                    }
-                }
-            }
-            cp_async_commit();
-            if (li == 0) {
-                int32_t c = 0;
-                s_cum[w][grp][0] = 0;
-#pragma unroll
-                for (int r = 0; r < RT; ++r) {
-                    c += s_n[w][rbase + r];
-                    s_cum[w][grp][r + 1] = c;
-                }
-            }
-            __syncwarp();
-            const int32_t *cum = s_cum[w][grp];
-            const int32_t total = cum[RT];
-            dbl4 g[VPL];
-#pragma unroll
-            for (int q = 0; q < VPL; ++q) g[q] = zero4d();
-            int cur = 0;
-            // row `cur` complete: its rounded G goes to the row's 4th staging slot
-            auto finish = [&](int r) {
-                float4 *st = stage + (size_t)(rbase + r) * SegGeo<D>::NST * V4 + 3 * V4 + li;
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) {
-                    st[q * LANES] = round4(g[q]);
-                    g[q] = zero4d();
-                }
-            };
-#pragma unroll 1
-            for (int32_t q0 = 0; q0 < total; q0 += RND) {
-                int64_t myoff[PPL];
-                int32_t myc[PPL], mylen[PPL];
-#pragma unroll
-                for (int p = 0; p < PPL; ++p) {
-                    const int32_t q = q0 + p * LANES + li;
-                    myc[p] = RT;
-                    myoff[p] = 0;
-                    mylen[p] = 0;
-                    if (q < total) {
-                        int lo = 0;
-#pragma unroll
-                        for (int r = 1; r < RT; ++r) lo += (cum[r] <= q);
-                        const int32_t seg = __ldg(a.sorted_seg + s_i0[w][rbase + lo] + (q - cum[lo]));
-                        const int32_t f = seg / a.B;
-                        myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
-                        if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
-                        myc[p] = lo;
-                    }
-                }
-                const int32_t nround = min(RND, total - q0);
-#pragma unroll 1
-                for (int k0 = 0; k0 < nround; k0 += U) {
-                    float4 c4[U][VPL];
-                    int ck[U];
-#pragma unroll
-                    for (int k = 0; k < U; ++k) {
-                        // PPL > 1 only when RND == U (k0 == 0): the slot index stays static
-                        const int src = (k0 + k) % LANES, slot = PPL > 1 ? k / LANES : 0;
-                        const int64_t off = __shfl_sync(gmask, myoff[slot], src, LANES);
-                        const int32_t len = __shfl_sync(gmask, mylen[slot], src, LANES);
-                        ck[k] = __shfl_sync(gmask, myc[slot], src, LANES);
-                        if (k0 + k < nround) {
-                            const float *p = a.dy + off + li * 4;
-#pragma unroll
-                            for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = ldg_f4(p + qq * LANES * 4);
-                            if (a.pool_mean) {
-#pragma unroll
-                                for (int qq = 0; qq < VPL; ++qq) c4[k][qq] = div4(c4[k][qq], (float)len);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < U; ++k) {
-                        if (k0 + k < nround) {
-                            while (cur < ck[k]) finish(cur++);
-#pragma unroll
-                            for (int qq = 0; qq < VPL; ++qq) g[qq] = add4d(g[qq], c4[k][qq]);
-                        }
-                    }
-                }
-            }
-            while (cur < RT) finish(cur++);
-            // ---- optimizer on the group's RT rows from shared memory, results to global (one
-            // copy of the update code: keeps the kernel inside the instruction cache)
-            cp_async_wait_all();
-#pragma unroll 1
-            for (int r = 0; r < RT; ++r) {
-                const int64_t row = s_row[w][rbase + r];
-                if (row < 0) continue;
-                const float4 *st = stage + (size_t)(rbase + r) * SegGeo<D>::NST * V4 + li;
-                RowRegs<VPL> rr;
-                float4 g32[VPL];
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) {
-                    rr.w[q] = st[q * LANES];
-                    rr.s1[q] = st[V4 + q * LANES];
-                    if (nst == 3) rr.s2[q] = st[2 * V4 + q * LANES];
-                    g32[q] = st[3 * V4 + q * LANES];
-                }
-                update_row32<D>(a, row, li, rr, g32);
-            }
-            __syncwarp();
-        }
-    }
-}
-
-size_t segsum_smem_bytes(int D) {
-    switch (D) {
-#define SB(DD) case DD: return (size_t)8 * SegGeo<DD>::STAGE_F4 * sizeof(float4);
-        SB(4) SB(8) SB(16) SB(32) SB(64) SB(128) SB(256) SB(384) SB(512)
-#undef SB
-        default: return 0;
-    }
-}
-
 // ------------------------------------------------------------------------------------------
-// Split backward (PICASSO_BWD=split, the default): k_segsum writes the rounded G of every
+// Split backward: k_segsum writes the rounded G of every
 // unique row of the pack into a G buffer (rows in uid order: coalesced), k_update_rows then
 // applies the optimizer row by row with two rows' weight/state loads in flight per group.
-// Costs one extra G write + read (4·D bytes per unique row each way) but both kernels are
-// short, register-light and run at high occupancy; the fused kernel above is kept as an
-// alternative (PICASSO_BWD=fused).
+// Costs one extra G write + read (4·D bytes per unique row each way); used for the packs the fused
+// k_segsum_upd (k_segsum_bulk.cu) does not take.
 template <int D>
 __global__ void __launch_bounds__(256) k_segsum(UpdateArgs a) {
     using Gm = Geo<D>;
@@ -739,18 +538,6 @@ __global__ void __launch_bounds__(256) k_long_finish(UpdateArgs a) {
         case 512: CALL(512); break; \
         default: break;             \
     }
-
-void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
-    const unsigned blocks = (unsigned)num_sms * 2;  // one resident wave (2 blocks / SM)
-    const size_t smem = segsum_smem_bytes(D);
-#define CALL(DD)                                                                                        \
-    {                                                                                                   \
-        ensure_dyn_smem((const void *)k_segsum_update<DD>, smem);                                       \
-        k_segsum_update<DD><<<blocks, 256, smem, s>>>(a);                                               \
-    }
-    PICASSO_DISPATCH_D(D, CALL)
-#undef CALL
-}
 
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s, bool flat_small) {
     if (flat_small && D <= 8) {  // measured at C3: D = 8 0.96 -> 0.75 ms; D = 16 / 32 slower (0.99 -> 1.10, 1.18 -> 1.87)

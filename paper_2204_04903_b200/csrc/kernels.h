@@ -184,7 +184,6 @@ void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s, bool
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, int32_t n_cnt,
                        cudaStream_t s);
-void launch_segsum_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 int launch_long_update(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);  // returns #launches
 size_t long_partial_doubles(int64_t N, int maxD);
 // k_segsum_bulk.cu: bulk-copy pipelined segsum (+ split-row fix-up); returns #launches

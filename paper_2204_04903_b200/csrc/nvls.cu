@@ -49,9 +49,20 @@ __global__ void __launch_bounds__(256) k_nvls_allreduce(float *mc, int64_t n4_g,
     asm volatile("fence.proxy.alias;" ::: "memory");  // unicast writes (segment-sum) before multicast reads
     const int64_t total = n4_g + n4_t;
     const int64_t lo = total * rank / W, hi = total * (rank + 1) / W;
-    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = i < n4_g ? i : t_off4 + (i - n4_g);
-        mm_st(mc + 4 * c, mm_ld_reduce_add(mc + 4 * c));
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    // 4 reductions in flight per thread: the switch round trip is long
+    for (int64_t i0 = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < hi; i0 += 4 * nth) {
+        float4 v[4];
+        int64_t c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = i0 + k * nth;
+            c[k] = i < n4_g ? i : t_off4 + (i - n4_g);
+            if (i < hi) v[k] = mm_ld_reduce_add(mc + 4 * c[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (i0 + k * nth < hi) mm_st(mc + 4 * c[k], v[k]);
     }
     asm volatile("fence.proxy.alias;" ::: "memory");
 }

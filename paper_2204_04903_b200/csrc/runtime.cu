@@ -167,10 +167,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
             c->mp.hot_mask = (uint32_t)(pow2_at_least((uint64_t)std::max<int64_t>(c->mp.k_max, 1) * 2) - 1);
         }
     }
-    if (const char *e = std::getenv("PICASSO_BWD")) {
-        c->split_bwd = std::strcmp(e, "fused") != 0;
-        c->fuse_pipe = std::strcmp(e, "split") != 0 && std::strcmp(e, "fused") != 0;
-    }
+    if (const char *e = std::getenv("PICASSO_BWD")) c->fuse_pipe = std::strcmp(e, "split") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM")) c->bulk_segsum = std::strcmp(e, "legacy") != 0;
     if (const char *e = std::getenv("PICASSO_SEGSUM_SMALL")) c->flat_small = std::strcmp(e, "legacy") != 0;
     c->seg_cfg = segsum_pipe_cfg();
@@ -564,16 +561,13 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
             if (ctx->fuse_pipe && ctx->bulk_segsum) fl = launch_segsum_fused(ctx->pack_dim[p], u, ctx->num_sms, s);
             if (fl) {  // segment-sum and optimizer in one pass over the rows
                 ctx->launches_bwd += fl;
-            } else if (ctx->split_bwd) {
+            } else {
                 ctx->launches_bwd += 1 + launch_segsum_any(ctx, ctx->pack_dim[p], u, s);
                 ctx->mark(3, false, s);
                 ctx->mark(5, true, s);
                 launch_update_rows(ctx->pack_dim[p], u, ctx->num_sms, s);
                 ctx->mark(5, false, s);
                 ctx->mark(3, true, s);
-            } else {
-                launch_segsum_update(ctx->pack_dim[p], u, ctx->num_sms, s);
-                ctx->launches_bwd += 1 + launch_long_update(ctx->pack_dim[p], u, ctx->num_sms, s);
             }
         }
     }
