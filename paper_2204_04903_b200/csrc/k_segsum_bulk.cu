@@ -737,38 +737,11 @@ void launch_upd(const UpdateArgs &a, int num_sms, cudaStream_t s) {
     k_segsum_fix<D, true><<<(unsigned)a.nt, 128, 0, s>>>(a);
 }
 
-// fused-kernel configuration (D = 128 Adagrad; PICASSO_FUSE_CFG for A/B): rows per stage x stages x warps
-static int fuse_cfg() {
-    static const int c = [] {
-        const char *e = std::getenv("PICASSO_FUSE_CFG");
-        if (!e) return 0;
-        if (!std::strcmp(e, "2x3x16")) return 1;
-        if (!std::strcmp(e, "4x3x11")) return 2;
-        if (!std::strcmp(e, "8x2x8")) return 3;
-        if (!std::strcmp(e, "2x2x16")) return 4;
-        if (!std::strcmp(e, "2x3x20")) return 0;
-        if (!std::strcmp(e, "4x2x14")) return 9;
-        if (!std::strcmp(e, "2x2x24")) return 6;
-        if (!std::strcmp(e, "1x4x24")) return 7;
-        if (!std::strcmp(e, "2x4x16")) return 8;
-        return 0;
-    }();
-    return c;
-}
-int segsum_upd_warps(int opt) {  // warps per CTA of the fused kernel (= its tiles per SM)
-    if (opt == 1) return 10;
-    switch (fuse_cfg()) {
-        case 1: return 16;
-        case 2: return 11;
-        case 3: return 8;
-        case 4: return 16;
-        case 6: return 24;
-        case 7: return 24;
-        case 8: return 16;
-        case 9: return 14;
-        default: return 20;  // 2 rows x 3 stages x 20 warps: the C2 sweep's best (0.239 ms / step)
-    }
-}
+// Warps per CTA (= tiles per SM) of the fused kernel.  Adagrad, D = 128: 2 rows x 3 stages x 20 warps
+// won the C2 sweep of rows / stage x stages x warps (0.2390 ms / step; 4 x 2 x 14: 0.2508, 2 x 2 x 24:
+// 0.2399, 2 x 4 x 16: 0.2460, 4 x 3 x 11: 0.2728, 8 x 2 x 8: 0.3008); Adam stages a
+// third row per slot and fits 10 warps.
+int segsum_upd_warps(int opt) { return opt == 1 ? 10 : 20; }
 
 int launch_segsum_fused(int D, const UpdateArgs &a, int num_sms, cudaStream_t s) {
     if (!a.tile_start || a.row_off || a.hslot || a.dst_off || ((uintptr_t)a.dy & 15) || (a.dy_stride & 3)) return 0;
@@ -777,26 +750,11 @@ int launch_segsum_fused(int D, const UpdateArgs &a, int num_sms, cudaStream_t s)
     switch (D) {
         case 64:
             if (adam) launch_upd<64, 10, 8, 2, 2>(a, num_sms, s);
-            else if (segsum_upd_warps(0) == 20) launch_upd<64, 20, 4, 3, 1>(a, num_sms, s);
-            else if (segsum_upd_warps(0) == 14) launch_upd<64, 14, 8, 2, 1>(a, num_sms, s);
-            else return 0;
+            else launch_upd<64, 20, 4, 3, 1>(a, num_sms, s);
             break;
         case 128:
-            if (adam) {
-                launch_upd<128, 10, 4, 2, 2>(a, num_sms, s);
-            } else {
-                switch (fuse_cfg()) {
-                    case 1: launch_upd<128, 16, 2, 3, 1>(a, num_sms, s); break;
-                    case 2: launch_upd<128, 11, 4, 3, 1>(a, num_sms, s); break;
-                    case 3: launch_upd<128, 8, 8, 2, 1>(a, num_sms, s); break;
-                    case 4: launch_upd<128, 16, 2, 2, 1>(a, num_sms, s); break;
-                    case 6: launch_upd<128, 24, 2, 2, 1>(a, num_sms, s); break;
-                    case 7: launch_upd<128, 24, 1, 4, 1>(a, num_sms, s); break;
-                    case 8: launch_upd<128, 16, 2, 4, 1>(a, num_sms, s); break;
-                    case 9: launch_upd<128, 14, 4, 2, 1>(a, num_sms, s); break;
-                    default: launch_upd<128, 20, 2, 3, 1>(a, num_sms, s); break;
-                }
-            }
+            if (adam) launch_upd<128, 10, 4, 2, 2>(a, num_sms, s);
+            else launch_upd<128, 20, 2, 3, 1>(a, num_sms, s);
             break;
         default: return 0;
     }

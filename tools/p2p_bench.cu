@@ -38,6 +38,55 @@ __global__ void k_pull(const float4 *const *src, float4 *__restrict__ dst, int n
     }
 }
 
+// push with 32-byte (256-bit) stores: half the store instructions / transactions of 16-B stores
+__global__ void k_push8(const float *__restrict__ src, float *const *dst, int npeer, int64_t n, int d) {
+    const int v8 = d / 8;
+    const int64_t per = n * v8, tot = per * npeer;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e / per);
+        const int64_t w = e - k * per;
+        const float *s = src + e * 8;
+        float *o = dst[k] + w * 8;
+        float v[8];
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                     : "l"(s));
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                     "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                     : "memory");
+    }
+}
+// push through the TMA unit: each block stages 8-KB tiles in shared memory (double buffered) and
+// issues one cp.async.bulk shared -> peer global per tile
+__global__ void __launch_bounds__(256) k_push_tma(const float4 *__restrict__ src, float4 *const *dst, int npeer,
+                                                  int64_t n, int v4) {
+    constexpr int TB = 8192, TV = TB / 16;
+    __shared__ __align__(128) float4 buf[2][TV];
+    const int64_t per = n * v4;  // float4 per peer
+    const int64_t ntile = (per + TV - 1) / TV;
+    int b = 0;
+    for (int64_t t = blockIdx.x; t < ntile * npeer; t += gridDim.x) {
+        const int k = (int)(t / ntile);
+        const int64_t t0 = (t - (int64_t)k * ntile) * TV;
+        const int cnt = (int)(per - t0 < TV ? per - t0 : TV);
+        if (threadIdx.x == 0)  // the buffer of two tiles ago has been read by the bulk copy
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) buf[b][i] = __ldg(src + (int64_t)k * per + t0 + i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[b][0]);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[k] + t0), "r"(sa),
+                         "r"(cnt * 16)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        b ^= 1;
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main(int argc, char **argv) {
     const double mb = argc > 1 ? atof(argv[1]) : 20.0;
     const int D = argc > 2 ? atoi(argv[2]) : 128;
@@ -99,6 +148,11 @@ int main(int argc, char **argv) {
                 if (mode == 0) k_push<<<sms * 8, 256, 0, st[g]>>>(src[g], pdst[g], G - 1, nullptr, rows, v4);
                 if (mode == 1) k_push<<<sms * 8, 256, 0, st[g]>>>(src[g], pdst[g], G - 1, perm[g], rows, v4);
                 if (mode == 3) k_pull<<<sms * 8, 256, 0, st[g]>>>(psrc[g], dst[g], G - 1, perm[g], rows, v4);
+                if (mode == 4)
+                    k_push8<<<sms * 8, 256, 0, st[g]>>>(reinterpret_cast<const float *>(src[g]),
+                                                        reinterpret_cast<float *const *>(pdst[g]), G - 1, rows, D);
+                if (mode == 5) k_push_tma<<<sms * 2, 256, 0, st[g]>>>(src[g], pdst[g], G - 1, rows, v4);
+                if (mode == 6) k_push_tma<<<sms * 4, 256, 0, st[g]>>>(src[g], pdst[g], G - 1, rows, v4);
                 if (mode == 2)
                     for (int q = 0; q < G; ++q)
                         if (q != g)
@@ -126,5 +180,8 @@ int main(int argc, char **argv) {
     run("push, random row slots (16-B stores)", 1);
     run("cudaMemcpyPeerAsync", 2);
     run("pull, random rows (16-B loads)", 3);
+    run("push, contiguous (32-B stores)", 4);
+    run("push, TMA bulk 8-KB tiles (2 CTA/SM)", 5);
+    run("push, TMA bulk 8-KB tiles (4 CTA/SM)", 6);
     return 0;
 }
