@@ -74,11 +74,17 @@ def init_pack_tables_torch(cfg, table_to_pack, table_base, n_packs, weights, ran
         tabs = tabs[np.argsort(tb[tabs], kind="stable")]
         bases = torch.tensor(tb[tabs], dtype=torch.int64, device=dev)
         tids = torch.tensor(tabs, dtype=torch.int64, device=dev)
-        n, D = W.shape
+        n, KD = W.shape
+        D = int(cfg.table_dim[tabs[0]])  # the tables' own dim; columns D..KD are the kernel-dim padding
         for s in range(0, n, chunk_rows):
             e = min(n, s + chunk_rows)
             lr = torch.arange(s, e, device=dev, dtype=torch.int64)
             key = lr * world + rank
             ti = torch.searchsorted(bases, key, right=True) - 1
             row = key - bases[ti]
-            W[s:e] = table_values_torch(cfg.seed, tids[ti], row, D).to(W.device)
+            vals = table_values_torch(cfg.seed, tids[ti], row, D).to(W.device)
+            if D == KD:
+                W[s:e] = vals
+            else:
+                W[s:e, :D] = vals
+                W[s:e, D:] = 0.0

@@ -89,7 +89,10 @@ typedef struct {
     const int32_t *table_to_pack;  /* [T] */
     const int64_t *table_base;     /* [T] */
     const int64_t *table_rows;     /* [T] */
-    const int32_t *table_dim;      /* [T]; every dim a multiple of 4, <= 512 */
+    const int32_t *table_dim;      /* [T]; 1 <= dim <= 512.  Stored at the kernel dim (picasso_kernel_dim:
+                                      the next of 4, 8, 16, 32, 64, 128, 256, 384, 512): weights, state,
+                                      and the field's out / dY column block are kernel-dim wide, the
+                                      padding columns are 0 in out and must be 0 in dY and the tables */
     const uint64_t *table_salt;    /* [T] HASH-mode salts (NULL = all 0) */
     const int64_t *field_col;      /* [F] first column of field f in the [B, out_width] output
                                       (a multiple of 4) */
@@ -150,6 +153,10 @@ picasso_status picasso_pack_plan_kinterleave(int32_t n_fields, const int32_t *fi
                                              const uint8_t *excluded, int32_t *field_to_pack, int32_t *table_to_pack,
                                              int64_t *table_base, int32_t *pack_dim, int64_t *pack_rows,
                                              int32_t *pack_group, int32_t *n_packs, int32_t *n_groups);
+
+/* Row width the kernels store a table of embedding dim `dim` at (1 <= dim <= 512): the next of 4, 8,
+ * 16, 32, 64, 128, 256, 384, 512.  INVALID_ARG outside that range. */
+picasso_status picasso_kernel_dim(int32_t dim, int32_t *kdim);
 
 /* NCCL unique id (128 bytes, host) for picasso_ctx_create; rank 0 calls it and broadcasts
  * the bytes to the other ranks (e.g. over torch.distributed). */

@@ -45,6 +45,7 @@ from .abi import (  # noqa: F401
     picasso_nvls_create,
     picasso_nvls_open,
     picasso_nvls_bind,
+    picasso_kernel_dim,
     POOL_SUM, POOL_MEAN, OPT_ADAGRAD, OPT_ADAM_LAZY, IDS_ROWS, IDS_HASH,
 )
 from .embedding import LoopbackGroup, PackedEmbedding  # noqa: F401

@@ -26,7 +26,7 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_group_p2p", "picasso_get_send_list", "picasso_micro_batch_size", "picasso_dinterleave_begin",
            "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply", "picasso_dinterleave_stats",
            "picasso_interleave_capacity", "picasso_pack_plan_kinterleave", "picasso_nvls_create", "picasso_nvls_open",
-           "picasso_nvls_bind"]
+           "picasso_nvls_bind", "picasso_kernel_dim"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -106,6 +106,7 @@ def lib():
             "picasso_nvls_create": [vp, C.POINTER(i32)],
             "picasso_nvls_open": [vp, i32],
             "picasso_nvls_bind": [vp],
+            "picasso_kernel_dim": [i32, C.POINTER(i32)],
             "picasso_pack_plan_kinterleave": [i32, vp, i32, vp, vp, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp,
                                               C.POINTER(i32), C.POINTER(i32)],
         }
@@ -189,6 +190,13 @@ def picasso_pack_plan_kinterleave(field_to_table, table_rows, table_dim, capacit
     P = n.value
     return dict(field_to_pack=f2p, table_to_pack=t2p, table_base=tb, pack_dim=pd[:P].copy(),
                 pack_rows=pr[:P].copy(), n_packs=P, pack_group=pg[:P].copy(), n_groups=g.value)
+
+
+def picasso_kernel_dim(dim):
+    """The padded row width a table of embedding dim `dim` is stored at."""
+    k = C.c_int32()
+    _chk(lib().picasso_kernel_dim(int(dim), C.byref(k)), "picasso_kernel_dim")
+    return k.value
 
 
 class _Keep:

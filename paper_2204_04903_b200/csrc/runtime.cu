@@ -21,8 +21,20 @@ void nvls_release(picasso_ctx *ctx);  // nvls.cu
         }                                                                 \
     } while (0)
 
-static bool dim_ok(int32_t d) {
-    return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 384 || d == 512;
+// The kernels are instantiated for these row widths; any other embedding dim (1..512: CAN's 8~200,
+// MMoE's 12~128) is stored zero-padded to the next one — its rows, optimizer state,
+// output / dY column block are kernel-dim wide, the padding stays 0 (its gradient is 0).
+static int32_t kernel_dim(int32_t d) {
+    static const int32_t ks[] = {4, 8, 16, 32, 64, 128, 256, 384, 512};
+    for (int32_t k : ks)
+        if (d >= 1 && d <= k) return k;
+    return 0;
+}
+
+extern "C" picasso_status picasso_kernel_dim(int32_t dim, int32_t *kdim) {
+    if (!kdim) return PICASSO_ERR_INVALID_ARG;
+    *kdim = kernel_dim(dim);
+    return *kdim ? PICASSO_OK : PICASSO_ERR_INVALID_ARG;
 }
 
 extern "C" picasso_status picasso_nccl_unique_id(uint8_t *out) {
@@ -73,6 +85,14 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     c->tbase.assign(plan->table_base, plan->table_base + c->T);
     c->trows.assign(plan->table_rows, plan->table_rows + c->T);
     c->tdim.assign(plan->table_dim, plan->table_dim + c->T);
+    for (int32_t t = 0; t < c->T; ++t) {  // the kernel (padded) dim: the layout of rows and columns
+        const int32_t k = kernel_dim(c->tdim[t]);
+        if (!k) {
+            delete c;
+            return PICASSO_ERR_PLAN_MISMATCH;
+        }
+        c->tdim[t] = k;
+    }
     c->tsalt.assign(c->T, 0);
     if (plan->table_salt) c->tsalt.assign(plan->table_salt, plan->table_salt + c->T);
     c->fcol.assign(plan->field_col, plan->field_col + c->F);
@@ -104,7 +124,7 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     c->pack_rows.assign(c->P, 0);
     for (int32_t t = 0; t < c->T; ++t) {
         const int32_t p = c->t2p[t];
-        if (p < 0 || p >= c->P || !dim_ok(c->tdim[t]) || c->trows[t] <= 0) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
+        if (p < 0 || p >= c->P || c->trows[t] <= 0) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
         if (c->pack_dim[p] != -1 && c->pack_dim[p] != c->tdim[t]) { delete c; return PICASSO_ERR_PLAN_MISMATCH; }
         c->pack_dim[p] = c->tdim[t];
         c->pack_rows[p] = std::max(c->pack_rows[p], c->tbase[t] + c->trows[t]);

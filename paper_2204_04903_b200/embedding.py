@@ -33,7 +33,10 @@ class PackedEmbedding:
         self.f2t = np.asarray(field_to_table, np.int32)
         self.rows = np.asarray(table_rows, np.int64)
         self.dims = np.asarray(table_dim, np.int32)
-        fd = self.dims[self.f2t].astype(np.int64)
+        # every table is stored at its kernel dim (picasso_kernel_dim: dims other than 4, 8, 16, ... 512 are
+        # zero-padded); the output column block of a field is that wide, the padding columns stay 0
+        self.kdims = np.array([abi.picasso_kernel_dim(int(d)) for d in self.dims], np.int32)
+        fd = self.kdims[self.f2t].astype(np.int64)
         self.field_col = (np.concatenate([[0], np.cumsum(fd)[:-1]]) if field_col is None
                           else np.asarray(field_col, np.int64))
         self.out_width = int(max(self.field_col + fd)) if len(fd) else 0
@@ -59,7 +62,7 @@ class PackedEmbedding:
         # cold tier (HybridHash with host-DRAM Cold-storage): the tables and their
         # optimizer state live in pinned host memory the GPU maps; HBM holds only the hot rows
         def table(p, r, fill):
-            shape = (max(r, 1), int(self.plan["pack_dim"][p]))
+            shape = (max(r, 1), abi.picasso_kernel_dim(int(self.plan["pack_dim"][p])))
             if self.cold_tier:
                 return torch.empty(shape, dtype=torch.float32, pin_memory=True).fill_(fill)
             return torch.full(shape, fill, dtype=torch.float32, device=self.device)
