@@ -589,6 +589,8 @@ def main():
         pb.picasso_profile_read(emb.ctx)
     next_i = [args.warmup]
 
+    pack_ms = [[0.0] * emb.n_packs, [0.0] * emb.n_packs]  # per pack: pool ms, backward ms (profiled pass)
+
     def run_pass(profiled, clk=None):
         """K steps, L2 flushed before each; returns (ms per step, phase ms summed, #calls)."""
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -616,6 +618,9 @@ def main():
                 next_i[0] += 1
             ends[i].record(stream)
             if use_graph and profiled:  # this replay's phase times (the sync is outside the start/end events)
+                pp, pw = pb.picasso_profile_read_packs(emb.ctx, emb.n_packs)
+                pack_ms[0] = [a + b for a, b in zip(pack_ms[0], pp)]
+                pack_ms[1] = [a + b for a, b in zip(pack_ms[1], pw)]
                 ph, _ = pb.picasso_profile_read(emb.ctx)
                 phase = {k: phase.get(k, 0.0) + v for k, v in ph.items()}
                 calls += 1
@@ -625,6 +630,7 @@ def main():
         if world > 1:
             dist.barrier()
         if not use_graph and profiled:
+            pack_ms[0], pack_ms[1] = pb.picasso_profile_read_packs(emb.ctx, emb.n_packs)
             phase, calls = pb.picasso_profile_read(emb.ctx)
         if profiled:
             pb.picasso_profile_enable(emb.ctx, False)
@@ -655,6 +661,21 @@ def main():
     last_b = batches[0 if use_graph else (next_i[0] - 1) % args.nbatches]
     alg = algorithmic_bytes(cfg, B, last_b.n_ids, U_by_pack, emb.plan, world)
     alg = {k: v for k, v in alg.items() if v is not None}
+    # the gather (pool) GB/s per pack dim — algorithmic bytes of pack p's pool (its IDs,
+    # offsets, distinct rows, pooled output) over its own CUDA-event time
+    gather_by_pack = []
+    f2p = np.asarray(emb.plan["field_to_pack"])
+    seg_len = np.diff(last_b.offsets.astype(np.int64)).reshape(cfg.F, B)
+    for p in range(emb.n_packs):
+        fields = np.nonzero(f2p == p)[0]
+        Dp = int(emb.plan["pack_dim"][p])
+        Np, Sp = int(seg_len[fields].sum()), int(len(fields) * B)
+        bytes_p = 8 * Np + 4 * (Sp + 1) + 4 * Dp * U_by_pack[p] + 4 * B * int(cfg.field_dim[fields].sum())
+        t_ms = pack_ms[0][p] / max(ncalls, 1)
+        gather_by_pack.append({"pack": p, "dim": int(emb.plan["pack_dim"][p]), "fields": int(len(fields)),
+                               "pool_ms": t_ms, "alg_bytes": bytes_p,
+                               "gbs": bytes_p / (t_ms * 1e-3) / 1e9 if t_ms > 0 else None,
+                               "backward_ms": pack_ms[1][p] / max(ncalls, 1) if world == 1 else None})
     per_phase = {k: v / max(ncalls, 1) for k, v in phase_ms.items()}
     per_phase = {k: v for k, v in per_phase.items() if v > 0}
     # The dominant kernel = the longest row kernel on the step's serial path.  At world == 1 below
@@ -771,6 +792,7 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
                          "peak_source": peak_src},
+            "gather_by_pack": gather_by_pack,
             "pool_concurrent": ({"achieved": alg["pool"] / (per_phase["pool"] * 1e-3) / 1e9, "unit": "GB/s",
                                  "frac_of_peak": alg["pool"] / (per_phase["pool"] * 1e-3) / 1e9 / peak,
                                  "sms": "148 - 74 reserved for the Unique / transpose chain",

@@ -247,6 +247,10 @@ picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int64_t *calls)
  * pack p = [u[p], u[p+1])), copied asynchronously on `stream` into dst (device memory or
  * pinned host memory).  Enqueue-only; the caller synchronises. */
 picasso_status picasso_unique_offsets(picasso_ctx *ctx, int32_t *dst, void *stream);
+/* Per pack (the first 64): ms of its pool (Gather + Stitch + SegmentReduction) and of its backward kernels
+ * (segment-sum and update) in the profiled steps since the last picasso_profile_read (host arrays
+ * [cap]; call before picasso_profile_read, which resets them; world == 1 backward only). */
+picasso_status picasso_profile_read_packs(picasso_ctx *ctx, float *pool_ms, float *bwd_ms, int32_t cap);
 
 /* ------------------------------------------------------------------------------------ */
 /* 5. Row-sharded step at world > 1 (PAPER.md L192-195 MP strategy, L209-215 operators).

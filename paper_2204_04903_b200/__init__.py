@@ -23,6 +23,7 @@ from .abi import (  # noqa: F401
     picasso_workspace_size,
     picasso_profile_enable,
     picasso_profile_read,
+    picasso_profile_read_packs,
     picasso_unique_offsets,
     picasso_nccl_unique_id,
     picasso_group_create,

@@ -26,7 +26,7 @@ EXPORTS = ["picasso_pack_plan", "picasso_ctx_create", "picasso_workspace_size", 
            "picasso_group_p2p", "picasso_get_send_list", "picasso_micro_batch_size", "picasso_dinterleave_begin",
            "picasso_packed_lookup_bwd_accumulate", "picasso_dinterleave_apply", "picasso_dinterleave_stats",
            "picasso_interleave_capacity", "picasso_pack_plan_kinterleave", "picasso_nvls_create", "picasso_nvls_open",
-           "picasso_nvls_bind", "picasso_kernel_dim"]
+           "picasso_nvls_bind", "picasso_kernel_dim", "picasso_profile_read_packs"]
 PHASES = ["unique", "pool", "transpose", "segsum", "owner_gather", "update"]
 
 
@@ -107,6 +107,7 @@ def lib():
             "picasso_nvls_open": [vp, i32],
             "picasso_nvls_bind": [vp],
             "picasso_kernel_dim": [i32, C.POINTER(i32)],
+            "picasso_profile_read_packs": [vp, vp, vp, i32],
             "picasso_pack_plan_kinterleave": [i32, vp, i32, vp, vp, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp,
                                               C.POINTER(i32), C.POINTER(i32)],
         }
@@ -367,6 +368,14 @@ def picasso_profile_read(ctx):
     n = C.c_int64()
     _chk(lib().picasso_profile_read(ctx, ms, C.byref(n)), "picasso_profile_read", ctx)
     return {PHASES[i]: float(ms[i]) for i in range(len(PHASES))}, n.value
+
+
+def picasso_profile_read_packs(ctx, n_packs):
+    """Per pack: (pool ms, backward ms) summed since the last picasso_profile_read (call before it)."""
+    pool = (C.c_float * n_packs)()
+    bwd = (C.c_float * n_packs)()
+    _chk(lib().picasso_profile_read_packs(ctx, pool, bwd, int(n_packs)), "picasso_profile_read_packs", ctx)
+    return list(pool), list(bwd)
 
 
 # ---- world > 1 ---------------------------------------------------------------------------

@@ -206,11 +206,12 @@ struct picasso_ctx {
     std::string last_msg;
     // phase profiling (events on the caller's stream)
     // 0 unique(+partition) 1 pool 2 transpose 3 segsum(+update at W=1) 4 owner dedup+gather 5 owner update
-    static constexpr int kPhases = 6;
+    // then per pack (first kPackPhases packs): kPhases + p its pool, kPhases + kPackPhases + p its backward
+    static constexpr int kPhases = 6, kPackPhases = 64, kAllPhases = kPhases + 2 * kPackPhases;
     bool prof = false;
     bool prof_graph = false;  // events were captured into a CUDA graph: reads do not reset them
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
-    size_t ev_used[kPhases] = {0, 0, 0, 0, 0, 0};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kAllPhases];
+    size_t ev_used[kAllPhases] = {};
     int64_t prof_calls = 0;
 
     // inside a capture, an external record becomes a graph node that re-records on every replay
@@ -218,8 +219,11 @@ struct picasso_ctx {
         if (prof_graph) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
         else cudaEventRecord(e, s);
     }
+    void mark_pack(int which, int p, bool begin, cudaStream_t s) {  // which: 0 pool, 1 backward
+        if (p < kPackPhases) mark(kPhases + which * kPackPhases + p, begin, s);
+    }
     void mark(int ph, bool begin, cudaStream_t s) {
-        if (!prof) return;
+        if (!prof || ph >= kAllPhases) return;
         auto &v = ev[ph];
         if (begin) {
             if (ev_used[ph] == v.size()) {

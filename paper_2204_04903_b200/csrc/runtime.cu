@@ -571,6 +571,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     UpdateArgs u = picasso::make_update_args(ctx, grad_out, lr, step, ctx->su, ctx->sseg);
     if (N > 0) {
         for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
+            ctx->mark_pack(1, p, true, s);
             u.pack = p;
             u.long_cnt = ctx->long_cnt + p;
             u.pack_key_off = ctx->pack_key_off[p];
@@ -589,6 +590,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
                 ctx->mark(5, false, s);
                 ctx->mark(3, true, s);
             }
+            ctx->mark_pack(1, p, false, s);
         }
     }
     ctx->mark(3, false, s);
@@ -667,6 +669,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
         pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
         pa.weight = pa.row_off ? ctx->gbuf : ctx->w[p];
         if ((int64_t)pa.Fp * pa.B == 0) continue;
+        ctx->mark_pack(0, p, true, s);
         if (ctx->pool_kind == 2) {
             n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
         } else if (pool_pipe_supported(ctx->pack_dim[p], pa)) {  // D >= 64: the cp.async ring
@@ -677,6 +680,7 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
             launch_pool(ctx->pack_dim[p], pa, ctx->num_sms, s);
             ++n;
         }
+        ctx->mark_pack(0, p, false, s);
     }
     return n;
 }
@@ -793,7 +797,7 @@ extern "C" picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, in
 extern "C" picasso_status picasso_profile_enable(picasso_ctx *ctx, int32_t on) {
     if (!ctx) return PICASSO_ERR_INVALID_ARG;
     if (on == 2 && !ctx->prof_graph) {  // start of a graph capture: fresh event list, kept afterwards
-        for (int ph = 0; ph < picasso_ctx::kPhases; ++ph) ctx->ev_used[ph] = 0;
+        for (int ph = 0; ph < picasso_ctx::kAllPhases; ++ph) ctx->ev_used[ph] = 0;
         ctx->prof_calls = 0;
     }
     ctx->prof = on != 0;
@@ -814,8 +818,32 @@ extern "C" picasso_status picasso_profile_read(picasso_ctx *ctx, float *ms, int6
         ms[ph] = tot;
         if (!ctx->prof_graph) ctx->ev_used[ph] = 0;  // graph mode: the replayed nodes re-record them
     }
+    if (!ctx->prof_graph)
+        for (int ph = picasso_ctx::kPhases; ph < picasso_ctx::kAllPhases; ++ph) ctx->ev_used[ph] = 0;
     if (calls) *calls = ctx->prof_graph ? 1 : ctx->prof_calls;
     if (!ctx->prof_graph) ctx->prof_calls = 0;
+    return PICASSO_OK;
+}
+
+// per pack (first kPackPhases packs): its pool and its backward kernels since the last read; call
+// before picasso_profile_read, which resets them
+extern "C" picasso_status picasso_profile_read_packs(picasso_ctx *ctx, float *pool_ms, float *bwd_ms, int32_t cap) {
+    if (!ctx || !pool_ms || !bwd_ms || cap < 0) return PICASSO_ERR_INVALID_ARG;
+    for (int32_t p = 0; p < cap; ++p) {
+        for (int which = 0; which < 2; ++which) {
+            float tot = 0.f;
+            if (p < picasso_ctx::kPackPhases) {
+                const int ph = picasso_ctx::kPhases + which * picasso_ctx::kPackPhases + p;
+                for (size_t i = 0; i < ctx->ev_used[ph]; ++i) {
+                    CK(cudaEventSynchronize(ctx->ev[ph][i].second));
+                    float t = 0.f;
+                    CK(cudaEventElapsedTime(&t, ctx->ev[ph][i].first, ctx->ev[ph][i].second));
+                    tot += t;
+                }
+            }
+            (which ? bwd_ms : pool_ms)[p] = tot;
+        }
+    }
     return PICASSO_OK;
 }
 

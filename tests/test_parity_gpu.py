@@ -348,3 +348,30 @@ def test_deterministic_rerun():
 def test_criteo_small_shape():
     cfg = dc.scaled(dc.criteo(), batch=2048, rows_div=1000)
     run_step(cfg, steps=2, check_intermediates=True)
+
+
+def test_profile_per_pack():
+    """picasso_profile_read_packs: each pack's pool and backward carry their own event time, the
+    per-pack pool times sum to no more than the pool phase (they partition it), and the read
+    resets with picasso_profile_read."""
+    import paper_2204_04903_b200 as pb
+
+    cfg = dc.scaled(dc.wdl(), batch=64, rows_div=1000)
+    emb = gpu_embedding(cfg)
+    b = make_batch(cfg, 0, 1)
+    ids, off = to_dev(b)
+    dy = torch.from_numpy(make_dy(cfg, 0, 1)).cuda()
+    pb.picasso_profile_enable(emb.ctx, 1)
+    pb.picasso_profile_read(emb.ctx)
+    emb.forward(ids, off, cfg.batch)
+    emb.backward_update(dy, lr=0.05, step=1)
+    torch.cuda.synchronize()
+    pool, bwd = pb.picasso_profile_read_packs(emb.ctx, emb.n_packs)
+    phase, calls = pb.picasso_profile_read(emb.ctx)
+    pb.picasso_profile_enable(emb.ctx, 0)
+    emb.check()
+    assert emb.n_packs > 1 and calls == 1
+    assert all(t > 0 for t in pool) and all(t > 0 for t in bwd), (pool, bwd)
+    assert sum(pool) <= phase["pool"] * 1.05 + 1e-3, (pool, phase)
+    pool2, _ = pb.picasso_profile_read_packs(emb.ctx, emb.n_packs)
+    assert all(t == 0 for t in pool2)
