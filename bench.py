@@ -678,13 +678,16 @@ def main():
                                "backward_ms": pack_ms[1][p] / max(ncalls, 1) if world == 1 else None})
     per_phase = {k: v / max(ncalls, 1) for k, v in phase_ms.items()}
     per_phase = {k: v for k, v in per_phase.items() if v > 0}
-    # The dominant kernel = the longest row kernel on the step's serial path.  At world == 1 below
-    # 4M IDs the library runs the pool beside the Unique / transpose chain on half the SMs
-    # (runtime.cu, early pool): its event time then spans the overlap and it is off the serial
-    # path, so it is reported separately ("pool_concurrent") and the roofline object takes the
-    # longest of the kernels that run alone.
-    early = (world == 1 and last_b.n_ids < (1 << 22) and os.environ.get("PICASSO_EARLY_POOL", "1") != "0"
-             and not args.eager)
+    # The dominant kernel = the longest row kernel on the step's serial path.  At world == 1 the
+    # library runs the pool beside the sort-based index chain (runtime.cu fwd_sorted; with the
+    # hash index: beside its Unique / transpose chain below 4M IDs): its event time then spans the
+    # overlap and it is off the serial path, so it is reported separately ("pool_concurrent") and
+    # the roofline object takes the longest of the kernels that run alone.
+    env = os.environ.get
+    sort_idx = env("PICASSO_INDEX", "sort") != "hash"
+    early = world == 1 and not args.eager and (
+        env("PICASSO_SORT_OVERLAP", "1") != "0" if sort_idx
+        else last_b.n_ids < (1 << 22) and env("PICASSO_EARLY_POOL", "1") != "0")
     fused = world == 1 and "segsum" in per_phase and "update" not in per_phase  # k_segsum_upd: one kernel
     if fused:
         per_phase["segsum_update"] = per_phase.pop("segsum")
@@ -704,6 +707,36 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(cfg.name, {}).get(dom)
+    kernel_name = {"pool": "k_pool_pipe (+ k_seg_of)", "segsum": "k_segsum_pipe (+ k_segsum_fix)",
+                   "update": "k_update_rows", "segsum_update": "k_segsum_upd (+ k_segsum_fix)"}[dom]
+    dom_bytes, dom_ms = alg[dom], per_phase[dom]
+    # Several packs (world == 1): the phases mix kernels of different packs, so the dominant kernel
+    # is taken per pack — each pack's pool and backward with its own algorithmic bytes (SURVEY
+    # §8(d) per-unit figures x that pack's IDs / rows / segments) over its own event time.
+    if world == 1 and emb.n_packs > 1 and ncalls > 0:
+        fused_ok = env("PICASSO_BWD", "") != "split" and all(
+            int(d) in (64, 128) for d in emb.plan["pack_dim"] if int(d) >= 64)
+        items = []
+        for e in gather_by_pack:
+            D, p = e["dim"], e["pack"]
+            fields = np.nonzero(f2p == p)[0]
+            Np, Up = int(seg_len[fields].sum()), U_by_pack[p]
+            out_p, rows_p = 4 * B * int(cfg.field_dim[fields].sum()), 4 * D * Up
+            if fused_ok and D in (64, 128):
+                e["backward_alg_bytes"] = out_p + 4 * Np + 4 * (Up + 1) + 8 * Up + 4 * rows_p
+                blabel = f"k_segsum_upd<{D}> (+ k_segsum_fix), pack {p}"
+            else:  # split: segment-sum writes G, the update reads it back
+                e["backward_alg_bytes"] = (out_p + 4 * Np + 4 * (Up + 1) + rows_p) + (rows_p + 8 * Up + 4 * rows_p)
+                blabel = f"k_segsum<{D}> + k_update_rows<{D}> (+ long rows), pack {p}"
+            bms = e["backward_ms"] or 0.0
+            e["backward_gbs"] = e["backward_alg_bytes"] / (bms * 1e-3) / 1e9 if bms > 0 else None
+            items.append((blabel, bms, e["backward_alg_bytes"]))
+            if not early:
+                items.append((f"{'k_pool_pipe' if D >= 64 else 'k_pool_flat'}<{D}>, pack {p}", e["pool_ms"],
+                              e["alg_bytes"]))
+        kernel_name, dom_ms, dom_bytes = max(items, key=lambda x: x[1])
+        achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+        traffic = None
 
     # ---------------- NVLink traffic of the exchange (W > 1): bytes this rank pushed per step
     nvlink = None
@@ -780,22 +813,22 @@ def main():
                        "launch": (f"cuda_graph (one captured step per batch, {args.nbatches} distinct batches "
                                   "replayed round robin)") if use_graph else "eager",
                        "nbatches": args.nbatches,
+                       "index": ("sort" if sort_idx else "hash") if world == 1 else "hash (row-sharded)",
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "note": "H2D of ids+offsets+dY from pinned host memory, D2H of the per-pack unique counts"},
             "gpu_launches": int((lf + lb) * args.steps),
-            "roofline": {"bound": "hbm", "kernel": {"pool": "k_pool_pipe (+ k_seg_of)",
-                                                     "segsum": "k_segsum_pipe (+ k_segsum_fix)",
-                                                     "update": "k_update_rows",
-                                                     "segsum_update": "k_segsum_upd (+ k_segsum_fix)"}[dom],
+            "roofline": {"bound": "hbm", "kernel": kernel_name,
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "algorithmic_bytes_per_launch": alg[dom],
+                         "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
                          "peak_source": peak_src},
             "gather_by_pack": gather_by_pack,
             "pool_concurrent": ({"achieved": alg["pool"] / (per_phase["pool"] * 1e-3) / 1e9, "unit": "GB/s",
                                  "frac_of_peak": alg["pool"] / (per_phase["pool"] * 1e-3) / 1e9 / peak,
-                                 "sms": "148 - 74 reserved for the Unique / transpose chain",
+                                 "sms": (f"148 - {env('PICASSO_SORT_RESERVE', '52')} reserved for the sort-based index"
+                                         if sort_idx else f"148 - {env('PICASSO_POOL_RESERVE', '74')} reserved for "
+                                         "the Unique / transpose chain"),
                                  "note": "k_pool_pipe runs beside the index chain (off the serial path); its "
                                          "event time includes the overlap"}
                                 if early and "pool" in per_phase else None),

@@ -194,6 +194,20 @@ struct picasso_ctx {
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     int kinterleave = 1;           // PICASSO_KINTERLEAVE=0 turns the per-pack pipelining off
     int32_t *su = nullptr, *sseg = nullptr;  // the last forward's transpose (uid-sorted occurrences)
+    // sort-based index (k_sortidx.cu): world == 1, pack keys < 2^32, the tiled backward; used from
+    // sort_min_ids IDs on (PICASSO_INDEX=hash / sort forces either; PICASSO_SORT_MIN_IDS).  A sorted step numbers the
+    // backward's rows in run order and keeps their keys in run_keys() (the dedup table's memory).
+    bool sort_idx = false;
+    bool sort_step = false;       // the last forward indexed by sort
+    bool views_ready = false;     // its reading-O1 views (inverse, Unique) materialised
+    const uint64_t *sorted_items = nullptr;  // its sorted (key << 32 | position) items
+    bool sort_overlap = true;     // PICASSO_SORT_OVERLAP=0: index chain and pool on the caller's stream
+    int sort_key_bits = 32;
+    int64_t sort_min_ids = 0;     // (every world == 1 step: C2 0.2411 -> 0.2202 ms, C3 25.3 -> 18.3 ms)
+    int sort_reserve = 52;        // SMs the pool leaves to the sort chain beside it (PICASSO_SORT_RESERVE;
+                                  // C2 sweep 24 / 32 / 40 / 48 / 56 / 64: 0.2286 / 0.2223 / 0.2185 / 0.2178 / 0.2172 / 0.2185 ms)
+    unsigned long long *run_keys() const { return reinterpret_cast<unsigned long long *>(table); }
+    unsigned long long *row_keys() const { return sort_step ? run_keys() : unique_gkey; }
     std::vector<float *> w, s1, s2;
     // step state
     bool fwd_done = false;
@@ -305,7 +319,7 @@ struct picasso_ctx {
         tocc = c.take<int32_t>(T);
         empty_pack = c.take<int32_t>(P);
         slot_of = c.take<int32_t>(N);
-        fmask = c.take<uint8_t>(NR / 8 + 2);
+        fmask = c.take<uint8_t>(4 * (size_t)(NR / 32 + 2));  // (also the sort index's 32-bit bitmap words)
         seg_of = c.take<int32_t>(N);
         inverse = c.take<int32_t>(N);
         blk_cnt = c.take<int32_t>(nblk);
@@ -315,10 +329,10 @@ struct picasso_ctx {
         err = c.take<int>(1);
         seg_limit = c.take<int32_t>(1);
         unique_gkey = c.take<unsigned long long>(N);
-        k_a = c.take<int32_t>(N);
-        v_a = c.take<int32_t>(N);
-        k_b = c.take<int32_t>(N);
-        v_b = c.take<int32_t>(N);
+        k_a = c.take<int32_t>(2 * (size_t)N);  // (k_a, v_a) / (k_b, v_b) adjacent: the sort-based
+        v_a = k_a ? k_a + N : nullptr;          //  index's 8-byte items use each pair as one buffer
+        k_b = c.take<int32_t>(2 * (size_t)N);
+        v_b = k_b ? k_b + N : nullptr;
         hist0 = c.take<int32_t>(radix_hist2_ints(N));
         hist1 = c.take<int32_t>(radix_hist2_ints(N));
         rowtot = c.take<int32_t>(kMaxRadix);

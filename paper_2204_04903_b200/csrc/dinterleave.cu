@@ -248,7 +248,7 @@ extern "C" picasso_status picasso_packed_lookup_bwd_accumulate(picasso_ctx *ctx,
         DiArgs a{};
         a.P = ctx->P;
         a.pack_ustart = ctx->pack_ustart;
-        a.unique_gkey = ctx->unique_gkey;
+        a.unique_gkey = ctx->row_keys();  // the rows of the segment-sum's G (run order after a sorted index)
         a.pack_key_off = ctx->pack_key_off_d;
         a.pack_dim = ctx->pack_dim_d;
         a.pack_gbase = ctx->pack_gbase;

@@ -94,6 +94,11 @@ __global__ void __launch_bounds__(1024) k_field_prep(IndexArgs a) {
         if (a.F > 0) {
             const int32_t sg0 = a.pm_fields[0] * a.B;
             for (int64_t g = tid; g < a.N; g += 1024) a.seg_of[g] = sg0;
+            if (a.keys) {  // every position keys row 0 of that field's table: in range, meaningless
+                const FieldInfo fi = a.finfo[a.pm_fields[0]];
+                const uint32_t k0 = (uint32_t)(a.pack_key_off[fi.pack] + fi.base);
+                for (int64_t g = tid; g < a.N; g += 1024) a.keys[g] = k0;
+            }
         }
         if (tid == 0) carry = (int32_t)a.N;
         __syncthreads();

@@ -80,21 +80,61 @@ __device__ __forceinline__ void lane_store_cs(float *row, int lane, const float 
 }
 
 // (also flags the packs that have an empty segment: k_pool_pipe zeroes them only there)
-__global__ void k_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart,
-                         const int32_t *id_start, int32_t *seg_of, const FieldInfo *finfo, int32_t *empty_pack,
-                         const int32_t *gtotal, int *err) {
-    const int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (sg >= (int64_t)F * B) return;
-    const int32_t f = (int32_t)(sg / B);
-    int32_t o0 = __ldg(offsets + sg), o1 = __ldg(offsets + sg + 1);
-    const int32_t gb = __ldg(field_gstart + f) - __ldg(id_start + f);
+// One warp per 32 consecutive segments: the lanes read the 33 offsets, then walk the warp's
+// positions j (consecutive lanes, consecutive j: coalesced ID reads and seg_of / key writes), each
+// finding its segment by a 5-step search over the lanes' starts.  Offsets that decrease inside
+// the warp (an invalid CSR: latched) fall back to one lane per segment.  ka (sort-based index):
+// also the pack key of every position.
+__global__ void __launch_bounds__(256) k_seg_of(const int32_t *offsets, int32_t B, int32_t F,
+                                                const int32_t *field_gstart, const int32_t *id_start, int32_t *seg_of,
+                                                const FieldInfo *finfo, int32_t *empty_pack, const int32_t *gtotal,
+                                                int *err, SegKeyArgs ka) {
+    const int64_t S = (int64_t)F * B;
+    const int64_t sg0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32 * 32;
+    if (sg0 >= S) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t sg = sg0 + lane;
+    const bool valid = sg < S;
+    const int32_t f = valid ? (int32_t)(sg / B) : 0;
+    const int32_t o0 = valid ? __ldg(offsets + sg) : INT32_MAX;
+    const int32_t o1 = valid ? __ldg(offsets + sg + 1) : INT32_MAX;
+    const int32_t gb = valid ? __ldg(field_gstart + f) - __ldg(id_start + f) : 0;
     // positions stay inside [0, total) whatever the offsets hold (total = 0 after an offsets
-    // error: k_field_prep filled seg_of itself); a decreasing pair inside a field latches it
+    // error: k_field_prep filled seg_of itself)
     const int64_t total = __ldg(gtotal);
-    if (o1 < o0 && err) atomicOr(err, ERR_OFFSETS);
-    const int64_t lo = max((int64_t)o0, -(int64_t)gb), hi = min((int64_t)o1, total - gb);
-    for (int64_t j = lo; j < hi; ++j) seg_of[j + gb] = (int32_t)sg;
-    if (o1 == o0 && empty_pack) empty_pack[finfo[f].pack] = 1;
+    const bool bad = valid && o1 < o0;
+    if (bad && err) atomicOr(err, ERR_OFFSETS);
+    if (valid && o1 == o0 && empty_pack) empty_pack[finfo[f].pack] = 1;
+    auto put = [&](int64_t j, int32_t s, int32_t ff, int32_t gbo) {
+        const int64_t g = j + gbo;
+        if (g < 0 || g >= total) return;
+        seg_of[g] = s;
+        if (ka.keys) {
+            const FieldInfo fi = finfo[ff];
+            const int64_t row = row_of(ka.id_mode, __ldg(ka.ids + j), fi, err);
+            ka.keys[g] = (uint32_t)(__ldg(ka.pack_key_off + fi.pack) + fi.base + row);
+        }
+    };
+    if (__any_sync(0xffffffffu, bad)) {  // not a CSR here: one lane per segment, ranges clamped
+        if (valid) {
+            const int64_t lo = max((int64_t)o0, -(int64_t)gb), hi = min((int64_t)o1, total - gb);
+            for (int64_t j = lo; j < hi; ++j) put(j, (int32_t)sg, f, gb);
+        }
+        return;
+    }
+    const int nv = S - sg0 < 32 ? (int)(S - sg0) : 32;
+    const int32_t J0 = __shfl_sync(0xffffffffu, o0, 0), J1 = __shfl_sync(0xffffffffu, o1, nv - 1);
+    for (int64_t jb = J0; jb < J1; jb += 32) {
+        const int64_t j = jb + lane;
+        int o = 0;  // the last lane whose segment starts at or before j (non-empty when j < J1)
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+            const int32_t v = __shfl_sync(0xffffffffu, o0, o + step);
+            if (v <= j) o += step;
+        }
+        const int32_t fo = __shfl_sync(0xffffffffu, f, o), gbo = __shfl_sync(0xffffffffu, gb, o);
+        if (j < J1) put(j, (int32_t)(sg0 + o), fo, gbo);
+    }
 }
 
 template <int D>
@@ -293,11 +333,11 @@ bool pool_pipe_supported(int D, const PoolArgs &a) {
 
 void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
                    int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo, int32_t *empty_pack, const int32_t *gtotal,
-                   int *err) {
+                   int *err, const SegKeyArgs *ka) {
     const int64_t n = (int64_t)F * B;
     if (n > 0)
         k_seg_of<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(offsets, B, F, field_gstart, id_start, seg_of, finfo,
-                                                            empty_pack, gtotal, err);
+                                                            empty_pack, gtotal, err, ka ? *ka : SegKeyArgs{});
 }
 
 int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s) {

@@ -71,6 +71,8 @@ struct IndexArgs {
     int32_t *tocc;                 // [T] scratch: occurrences per table
     int32_t *empty_pack;           // [P] zeroed here, set by k_seg_of
     int32_t *seg_limit;            // [1] out: positions k_seg_of may place (n_ids; 0 after an offsets error)
+    uint32_t *keys;                // [N] sort-based index: k_field_prep's substitute layout also keys every
+                                   //   position (row 0 of the first field's table) after an offsets error
     int32_t sort_bits0;            // digit width of the backward's first radix pass
     int32_t *sort_hist0;           // [radix0, nblk] out: digit-major histogram of that pass
     int *err;
@@ -94,6 +96,57 @@ size_t radix_hist2_ints(int64_t n);
 void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s);
 void bucket_sort_pass(const int32_t *k_in, const int32_t *v_in, int32_t *k_out, int32_t *v_out, int64_t n_max,
                       const int32_t *n_dev, int bits, int32_t *bhist, int32_t *rowtot, cudaStream_t s);
+
+// k_sortidx.cu: the index phase of a large world == 1 step as one stable LSD sort of
+// (pack key << 32 | position); rows come out in run (ascending key) order
+struct SortIdxArgs {
+    const int64_t *ids;            // first up-sweep: keys from the IDs
+    const int32_t *seg_of;         //   [N] segment f * B + b of each packed position
+    int32_t B;
+    int64_t N;
+    int32_t id_mode;
+    const FieldInfo *finfo;
+    const int32_t *id_start, *field_gstart;
+    const int64_t *pack_key_off;
+    int *err;
+    uint32_t *keys;                // [N] pack key of each position (first pass)
+    int32_t *hist, *rowtot;        // LSD passes: [radix, nc] chunk counts, [radix] digit totals
+    int32_t nc;
+    int64_t chunk;
+    int32_t *tile_heads, *tile_last, *run_base, *carry;  // [nblk] each
+    int32_t *pack_hb;              // [P+1] heads before each pack's first item, in its tile
+    int32_t *d_total;              // [1] U
+    int32_t *su, *sseg;            // [N] row (run index) and segment of each sorted occurrence
+    int32_t *ustart;               // [U+1] first sorted occurrence of each row (run order)
+    unsigned long long *run_key;   // [U] pack key of each row (run order: the backward's rows)
+    int32_t P;
+    const int32_t *pack_gstart;
+    int32_t *pack_ustart;
+    int64_t *pack_gbase;
+    const int32_t *pack_dim;
+    int32_t nt, rw;                // equal-cost tiles of the backward (k_csr_tiles partition)
+    int32_t *tile_start;           //   [P, nt+1] (nullptr: none)
+    int32_t *long_cnt;             // [P] zeroed
+    // reading-O1 views (launch_sort_views)
+    uint32_t *bm;                  // [N/32] first-occurrence bitmap over positions
+    int32_t *wpref;                // [N/32] first occurrences before each bitmap word
+    int32_t *view_scratch;         // [2 nblk]
+    int32_t *inverse;              // [N] uid of each position
+    unsigned long long *unique_gkey;  // [U] key of each uid (first-occurrence order)
+};
+struct SortIdxPlan {
+    int passes;
+    int bits[4];
+    int shift[4];
+    int64_t chunk;  // items per CTA (a multiple of kTile)
+    int32_t nc;     // CTAs
+};
+SortIdxPlan make_sortidx_plan(int64_t n, int key_bits, int num_sms);
+size_t sortidx_scratch_ints(int64_t n, int32_t P);  // tile arrays + views scratch + word ranks
+// returns #launches; *sorted: the sorted items, *other: the buffer holding su / sseg
+int launch_sort_index(SortIdxArgs a, const SortIdxPlan &plan, uint64_t *buf_a, uint64_t *buf_b, uint64_t **sorted,
+                      uint64_t **other, cudaStream_t s);
+int launch_sort_views(SortIdxArgs a, const uint64_t *sorted, cudaStream_t s);  // inverse + Unique (reading O1)
 
 // k_index.cu
 void launch_field_prep(const IndexArgs &a, cudaStream_t s);
@@ -134,10 +187,17 @@ void launch_pool(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 // k_pool_pipe.cu: pipelined pool for D >= 64 (needs seg_of from launch_seg_of); returns #launches
 bool pool_pipe_supported(int D, const PoolArgs &a);
 int launch_pool_pipe(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
-// gtotal: [1] positions k_seg_of may place (k_field_prep: n_ids, 0 after an offsets error); err: latch
+// gtotal: [1] positions k_seg_of may place (k_field_prep: n_ids, 0 after an offsets error); err: latch;
+// ka (optional): also the pack key of every position (the sort-based index's first pass)
+struct SegKeyArgs {
+    const int64_t *ids;
+    const int64_t *pack_key_off;
+    int32_t id_mode;
+    uint32_t *keys;  // [N] out (nullptr: seg_of only)
+};
 void launch_seg_of(const int32_t *offsets, int32_t B, int32_t F, const int32_t *field_gstart, const int32_t *id_start,
                    int32_t *seg_of, cudaStream_t s, const FieldInfo *finfo, int32_t *empty_pack, const int32_t *gtotal,
-                   int *err);
+                   int *err, const SegKeyArgs *ka = nullptr);
 // k_pool_flat.cu: one thread per 16-B output chunk (every D); returns #launches
 int launch_pool_flat(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 

@@ -223,6 +223,18 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     }
     c->seg_nt = c->num_sms * (c->fuse_pipe ? segsum_upd_warps(opts->opt) : segsum_pipe_warps(c->seg_cfg));
     if (const char *e = std::getenv("PICASSO_FUSE_RW")) c->fuse_rw = std::max(1, std::atoi(e));
+    // sort-based index: the backward must be the tiled one (the sort emits its tiles)
+    c->sort_idx = world == 1 && !opts->cold_tier && c->bulk_segsum && c->pack_key_off[c->P] <= ((int64_t)1 << 32) &&
+                  sortidx_scratch_ints(std::max<int64_t>(opts->max_ids, 1), c->P) <=
+                      radix_hist2_ints(std::max<int64_t>(opts->max_ids, 1));
+    c->sort_key_bits = c->pack_key_off[c->P] > 1 ? 64 - __builtin_clzll((unsigned long long)(c->pack_key_off[c->P] - 1)) : 1;
+    if (const char *e = std::getenv("PICASSO_INDEX")) {
+        if (!std::strcmp(e, "hash")) c->sort_idx = false;
+        if (!std::strcmp(e, "sort")) c->sort_min_ids = 0;
+    }
+    if (const char *e = std::getenv("PICASSO_SORT_MIN_IDS")) c->sort_min_ids = std::atoll(e);
+    if (const char *e = std::getenv("PICASSO_SORT_OVERLAP")) c->sort_overlap = std::strcmp(e, "0") != 0;
+    if (const char *e = std::getenv("PICASSO_SORT_RESERVE")) c->sort_reserve = std::atoi(e);
     c->pool_sms = c->num_sms;
     c->ws_bytes = c->carve(nullptr);
     *out = c;
@@ -452,6 +464,108 @@ IndexArgs picasso::make_index_args(picasso_ctx *ctx, const int64_t *ids, const i
     return a;
 }
 
+static SortIdxArgs sort_idx_args(picasso_ctx *ctx, const int64_t *ids, int32_t B, int64_t N) {
+    SortIdxArgs x{};
+    x.ids = ids;
+    x.seg_of = ctx->seg_of;
+    x.B = B;
+    x.N = N;
+    x.id_mode = ctx->opts.id_mode;
+    x.finfo = ctx->finfo;
+    x.id_start = ctx->id_start;
+    x.field_gstart = ctx->field_gstart;
+    x.pack_key_off = ctx->pack_key_off_d;
+    x.err = ctx->err;
+    x.keys = reinterpret_cast<uint32_t *>(ctx->slot_of);
+    x.hist = ctx->hist0;
+    x.rowtot = ctx->rowtot;
+    const int64_t nb1 = (N + kTile - 1) / kTile + 1;  // scratch (hist1): tile arrays, views, word ranks
+    x.tile_heads = ctx->blk_cnt;
+    x.run_base = ctx->blk_off;
+    x.tile_last = ctx->hist1;
+    x.carry = ctx->hist1 + nb1;
+    x.pack_hb = ctx->hist1 + 2 * nb1;
+    x.view_scratch = x.pack_hb + ctx->P + 1;
+    x.wpref = x.view_scratch + 2 * nb1;
+    x.bm = reinterpret_cast<uint32_t *>(ctx->fmask);
+    x.d_total = ctx->d_total;
+    x.inverse = ctx->inverse;
+    x.ustart = ctx->ustart;
+    x.run_key = ctx->run_keys();
+    x.unique_gkey = ctx->unique_gkey;
+    x.P = ctx->P;
+    x.pack_gstart = ctx->pack_gstart;
+    x.pack_ustart = ctx->pack_ustart;
+    x.pack_gbase = ctx->pack_gbase;
+    x.pack_dim = ctx->pack_dim_d;
+    x.nt = ctx->seg_nt;
+    x.rw = ctx->fuse_pipe ? ctx->fuse_rw : 1;
+    x.tile_start = ctx->tile_start;
+    x.long_cnt = ctx->long_cnt;
+    return x;
+}
+
+// the reading-O1 views of a sorted step (Unique in first-occurrence order, inverse), on request
+static picasso_status ensure_views(picasso_ctx *ctx) {
+    if (!ctx->sort_step || ctx->views_ready) return PICASSO_OK;
+    const SortIdxArgs x = sort_idx_args(ctx, nullptr, ctx->B, ctx->N);
+    launch_sort_views(x, ctx->sorted_items, ctx->last_stream);
+    CK(cudaGetLastError());
+    ctx->views_ready = true;
+    return PICASSO_OK;
+}
+
+// World == 1, sort-based index (k_sortidx.cu): field layout + segment of every position, then the
+// sort chain on the internal stream beside the pool (which needs only the IDs and seg_of); the
+// forward joins both.  The chain emits Unique / inverse (reading O1) and the backward's CSR + tiles.
+static picasso_status fwd_sorted(picasso_ctx *ctx, IndexArgs a, float *out, cudaStream_t s) {
+    const int64_t N = a.N;
+    ctx->B = a.B;
+    ctx->N = N;
+    ctx->offsets = a.offsets;
+    a.region_base = nullptr;  // no dedup table
+    a.keys = reinterpret_cast<uint32_t *>(ctx->slot_of);
+    launch_field_prep(a, s);
+    const SegKeyArgs ka{a.ids, ctx->pack_key_off_d, ctx->opts.id_mode, a.keys};
+    launch_seg_of(a.offsets, a.B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s, ctx->finfo,
+                  ctx->empty_pack, ctx->seg_limit, ctx->err, &ka);
+    ctx->launches_fwd += 2;
+    cudaStream_t t = s;
+    if (ctx->sort_overlap && ctx->side) {
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        t = ctx->side;
+    }
+    SortIdxArgs x = sort_idx_args(ctx, a.ids, a.B, N);
+    const SortIdxPlan plan = make_sortidx_plan(N, ctx->sort_key_bits, ctx->num_sms);
+    uint64_t *sorted = nullptr, *other = nullptr;
+    ctx->mark(0, true, t);
+    ctx->launches_fwd += launch_sort_index(x, plan, reinterpret_cast<uint64_t *>(ctx->k_a),
+                                           reinterpret_cast<uint64_t *>(ctx->k_b), &sorted, &other, t);
+    ctx->mark(0, false, t);
+    ctx->su = reinterpret_cast<int32_t *>(other);
+    ctx->sseg = ctx->su + N;
+    ctx->sorted_items = sorted;
+    ctx->views_ready = false;
+    if (t != s) CK(cudaEventRecord(ctx->ev_join, t));
+    // the pool leaves sort_reserve SMs to the sort chain running beside it (C2 sweep)
+    ctx->pool_sms = t != s ? std::max(ctx->num_sms / 4, ctx->num_sms - ctx->sort_reserve) : ctx->num_sms;
+    ctx->mark(1, true, s);
+    {
+        PoolArgs pa{};
+        pa.ids = a.ids;
+        pa.offsets = a.offsets;
+        pa.B = a.B;
+        ctx->launches_fwd += launch_pool_all(ctx, pa, out, s);
+    }
+    ctx->mark(1, false, s);
+    if (t != s) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    CK(cudaGetLastError());
+    ctx->fwd_done = true;
+    ctx->last_stream = s;
+    return PICASSO_OK;
+}
+
 extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets,
                                                     int32_t batch, int64_t n_ids, float *out, void *stream) {
     if (!ctx || !offsets || (!out && batch > 0) || batch < 0 || n_ids < 0 || (n_ids > 0 && !ids))
@@ -474,6 +588,8 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
     }
     if (ctx->opts.cold_tier) return ct_fwd(ctx, ids, offsets, batch, n_ids, out, s);
     IndexArgs a = index_args(ctx, ids, offsets, batch, n_ids);
+    ctx->sort_step = ctx->sort_idx && batch > 0 && n_ids >= ctx->sort_min_ids;
+    if (ctx->sort_step) return fwd_sorted(ctx, a, out, s);
     const uint32_t cap_step =
         (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(n_ids, 1) * 2));
     a.cap_mask = cap_step - 1;
@@ -699,7 +815,7 @@ UpdateArgs picasso::make_update_args(picasso_ctx *ctx, const float *grad_out, fl
     u.sorted_seg = sseg;
     u.ustart = ctx->ustart;
     u.pack_ustart = ctx->pack_ustart;
-    u.unique_gkey = ctx->unique_gkey;
+    u.unique_gkey = ctx->row_keys();
     u.offsets = ctx->offsets;
     u.B = ctx->B;
     u.finfo = ctx->finfo;
@@ -762,6 +878,7 @@ extern "C" picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t
 
 extern "C" picasso_status picasso_get_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n) {
     if (!ctx || !n || pack < 0 || pack >= ctx->P || !ctx->bound) return PICASSO_ERR_INVALID_ARG;
+    if (picasso_status st = ensure_views(ctx)) return st;
     CK(cudaStreamSynchronize(ctx->last_stream));
     std::vector<int32_t> us(ctx->P + 1);
     CK(cudaMemcpy(us.data(), ctx->pack_ustart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost));
@@ -779,6 +896,7 @@ extern "C" picasso_status picasso_get_unique(picasso_ctx *ctx, int32_t pack, int
 
 extern "C" picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, int32_t *dst, int64_t cap, int64_t *n) {
     if (!ctx || !n || pack < 0 || pack >= ctx->P || !ctx->bound) return PICASSO_ERR_INVALID_ARG;
+    if (picasso_status st = ensure_views(ctx)) return st;
     CK(cudaStreamSynchronize(ctx->last_stream));
     std::vector<int32_t> gs(ctx->P + 1), us(ctx->P + 1);
     CK(cudaMemcpy(gs.data(), ctx->pack_gstart, sizeof(int32_t) * (ctx->P + 1), cudaMemcpyDeviceToHost));

@@ -131,6 +131,7 @@ def test_dedup_per_table_regions(monkeypatch):
     """The per-table hash regions of large batches (forced on a small one): same unique / inverse
     (bit-exact, checked per pack) and the same step."""
     monkeypatch.setenv("PICASSO_DEDUP_REGIONS", "1")
+    monkeypatch.setenv("PICASSO_INDEX", "hash")
     cfg = dc.scaled(dc.wdl(), batch=40, rows_div=1000)
     run_step(cfg, steps=2)
     run_step(dc.toy(), steps=2)

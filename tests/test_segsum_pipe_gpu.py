@@ -145,10 +145,15 @@ def test_pool_pipe_mean_and_all_empty_pack():
 
 
 # ---- alternative paths behind environment switches (read when the context is created) ---------
-@pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "0"}, {"PICASSO_BWD": "split"}, {"PICASSO_POOL": "flat"},
-                                 {"PICASSO_OVERLAP": "0"}, {"PICASSO_OVERLAP": "1"}, {"PICASSO_SEGSUM_CFG": "12x4"},
-                                 {"PICASSO_DEDUP_REGIONS": "1"}, {"PICASSO_SEGSUM_SMALL": "legacy"},
-                                 {"PICASSO_SORT": "3"}, {"PICASSO_SORT": "2"}])
+_H = {"PICASSO_INDEX": "hash"}  # the hash-table index path's own switches
+
+
+@pytest.mark.parametrize("env", [{"PICASSO_EARLY_POOL": "0", **_H}, {"PICASSO_BWD": "split"}, {"PICASSO_POOL": "flat"},
+                                 {"PICASSO_OVERLAP": "0", **_H}, {"PICASSO_OVERLAP": "1", **_H},
+                                 {"PICASSO_SEGSUM_CFG": "12x4"}, {"PICASSO_DEDUP_REGIONS": "1", **_H},
+                                 {"PICASSO_SEGSUM_SMALL": "legacy"}, _H, {"PICASSO_SORT_OVERLAP": "0"},
+                                 {"PICASSO_SORT_RESERVE": "100"}, {"PICASSO_BWD": "split", **_H},
+                                 {"PICASSO_SORT": "3", **_H}, {"PICASSO_SORT": "2", **_H}])
 def test_alternative_paths_match_oracle(env, monkeypatch):
     """Every switchable variant computes the same step: forward bit-exact, update within the
     north-star tolerance of the oracle (bit-exact under dyadic dY)."""
