@@ -195,6 +195,10 @@ picasso_status picasso_ctx_destroy(picasso_ctx *ctx);
  * Keeps the per-step state (unique keys, inverse, segment map) in the workspace for the
  * next picasso_packed_lookup_bwd_update, and reads `offsets` again there (mean combiner: bag
  * lengths): offsets must stay valid and unchanged until that backward has been enqueued.
+ * Index path: at world == 1 the Unique of every pack comes from one stable LSD sort of the
+ * step's (pack key, position) items, which also yields the backward's rows in ascending-key
+ * order (PICASSO_INDEX=hash selects the hash-table Unique + uid transpose, which the
+ * row-sharded step always uses); both give the same forward and the same updates.
  * offsets that are not such a CSR latch INVALID_ARG (picasso_last_error); the step then runs
  * on a substitute layout that keeps every access in bounds, and its results are meaningless.
  * Errors: CAPACITY if batch > max_batch or n_ids > max_ids; STATE if not bound. */
@@ -223,7 +227,10 @@ picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t len);
  * Copies into caller device buffers; *n receives the element count (copy truncated at cap).
  *   picasso_get_unique : pack keys of pack p in first-occurrence order (int64 [U_p])
  *   picasso_get_inverse: per occurrence of pack p's key stream (pack fields in ascending
- *                        field order, then b, then j) its index into unique (int32 [N_p]) */
+ *                        field order, then b, then j) its index into unique (int32 [N_p])
+ * After a sort-indexed forward (world == 1) the step itself numbers rows by key; these two
+ * first-occurrence views (reading O1) are built from the sorted items on the first call after
+ * the forward (a few extra kernels on the ctx's last stream), valid until the next forward. */
 picasso_status picasso_get_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n);
 picasso_status picasso_get_inverse(picasso_ctx *ctx, int32_t pack, int32_t *dst, int64_t cap, int64_t *n);
 
