@@ -156,8 +156,22 @@ __global__ void __launch_bounds__(kSiThreads, 3) k_si_down(SortIdxArgs a, const 
 #pragma unroll
         for (int r = 0; r < kSiItems; ++r) {  // stable rank inside the warp's run of each digit
             const bool valid = wb + r * 32 + lane < nt;
-            dg[r] = valid ? (int)((uint32_t)(it[r] >> dshift) & dm) : kSiRadix + lane;
-            const unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
+            dg[r] = valid ? (int)((uint32_t)(it[r] >> dshift) & dm) : 0;
+            // lanes holding the same digit: MATCH.ANY for half the rounds, one ballot per digit bit
+            // for the other half — MATCH alone kept the ADU pipe 88 % busy, the ballots alone the
+            // ALU pipe 65 % (C3 ncu); alternating splits the work between the two pipes
+            unsigned peers;
+            if (r & 1) {
+                peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+                for (int b = 0; b < kSiBits; ++b) {
+                    const bool bit = (dg[r] >> b) & 1;
+                    const unsigned m = __ballot_sync(0xffffffffu, bit);
+                    peers &= bit ? m : ~m;
+                }
+            } else {
+                peers = __match_any_sync(0xffffffffu, valid ? dg[r] : kSiRadix + lane);
+            }
             const int before = valid ? wc[w][dg[r]] : 0;
             rk[r] = before + __popc(peers & lt);
             __syncwarp();
@@ -288,72 +302,93 @@ __device__ __forceinline__ int64_t si_tile_of(int64_t c, double scale, int64_t n
 __global__ void __launch_bounds__(kSiThreads, 3) k_si_final(SortIdxArgs a, const uint64_t *s) {
     using BS = cub::BlockScan<int32_t, kSiThreads>;
     __shared__ typename BS::TempStorage tmp;
-    const int64_t i0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kSiItems;
+    // the tile's outputs staged in shared memory, then stored with consecutive threads on
+    // consecutive addresses (per-thread scattered stores of the row starts / keys and half-used
+    // 32-B sectors of su / sseg made k_si_final L2-store bound: 247 M sectors per launch at C3)
+    __shared__ __align__(16) int32_t s_su[kTile], s_seg[kTile], s_us[kTile];
+    __shared__ __align__(16) unsigned long long s_key[kTile];
+    __shared__ int32_t s_nh;
+    const int64_t t0 = (int64_t)blockIdx.x * kTile;
+    const int64_t i0 = t0 + (int64_t)threadIdx.x * kSiItems;
     uint64_t x[kSiItems];
     load8(s, i0, a.N, x);
     const unsigned hm = heads8(s, i0, a.N, x);
-    int32_t hb;
-    BS(tmp).ExclusiveSum(__popc(hm), hb);
-    if (i0 >= a.N) return;
-    int32_t r = __ldg(a.run_base + blockIdx.x) + hb - 1;  // the row the thread's first items continue
+    int32_t hb, nh;
+    BS(tmp).ExclusiveSum(__popc(hm), hb, nh);
+    if (threadIdx.x == 0) s_nh = nh;
     int32_t out_r[kSiItems], out_s[kSiItems];
-    int lo = -1;
-    int64_t G0 = 0, G1 = 0, U0 = 0, nte = 0;
-    double scale = 0.0;
-    int32_t *ts = nullptr;
-    const int64_t rw = a.rw;
+#pragma unroll
+    for (int k = 0; k < kSiItems; ++k)  // segments first: eight independent gathers in flight
+        out_s[k] = i0 + k < a.N ? __ldg(a.seg_of + (uint32_t)x[k]) : 0;
+    const int32_t rb = __ldg(a.run_base + blockIdx.x);
+    int32_t r = rb + hb - 1;  // the row the thread's first items continue
+    int hl = hb;              // tile-local index of the thread's next head
 #pragma unroll
     for (int k = 0; k < kSiItems; ++k) {
-        const int64_t i = i0 + k;
-        out_r[k] = 0;
-        out_s[k] = 0;
-        if (i >= a.N) continue;
-        const uint64_t xi = x[k];
-        const bool head = (hm >> k) & 1u;
-        if (head) {
+        if (i0 + k < a.N && ((hm >> k) & 1u)) {
             ++r;
-            a.ustart[r] = (int32_t)i;
-            a.run_key[r] = xi >> 32;
+            s_us[hl] = (int32_t)(i0 + k);
+            s_key[hl] = x[k] >> 32;
+            ++hl;
         }
         out_r[k] = r;
-        out_s[k] = __ldg(a.seg_of + (uint32_t)xi);
-        if (a.tile_start) {  // the backward's equal-cost tiles (k_csr_tiles)
-            if (lo < 0 || i >= G1) {  // the last pack starting at or before i (skips empty packs)
+    }
+    const int lt = threadIdx.x * kSiItems;
+#pragma unroll
+    for (int k = 0; k < kSiItems; ++k) {
+        s_su[lt + k] = out_r[k];
+        s_seg[lt + k] = out_s[k];
+    }
+    if (a.tile_start && i0 < a.N) {  // the backward's equal-cost tiles (k_csr_tiles): tile of each item's cost
+        const int64_t rw = a.rw;
+        int64_t G0 = 0, G1 = -1, U0 = 0, nte = 1, kp = -1;
+        double scale = 0.0;
+        int32_t *ts = nullptr;
+#pragma unroll
+        for (int k = 0; k < kSiItems; ++k) {
+            const int64_t i = i0 + k;
+            if (i >= a.N) continue;
+            const bool head = (hm >> k) & 1u;
+            if (i >= G1) {  // (re)locate: the last pack starting at or before i (skips empty packs)
                 int l = 0, h = a.P;
                 while (h - l > 1) {
                     const int mid = (l + h) >> 1;
                     if (__ldg(a.pack_gstart + mid) <= i) l = mid; else h = mid;
                 }
-                lo = l;
-                G0 = __ldg(a.pack_gstart + lo);
-                G1 = __ldg(a.pack_gstart + lo + 1);
-                U0 = __ldg(a.pack_ustart + lo);
-                const int64_t C = (G1 - G0) + rw * (__ldg(a.pack_ustart + lo + 1) - U0);
+                G0 = __ldg(a.pack_gstart + l);
+                G1 = __ldg(a.pack_gstart + l + 1);
+                U0 = __ldg(a.pack_ustart + l);
+                const int64_t C = (G1 - G0) + rw * (__ldg(a.pack_ustart + l + 1) - U0);
                 nte = a.nt < C ? a.nt : C;
                 scale = (double)nte / (double)C;
-                ts = a.tile_start + (int64_t)lo * (a.nt + 1);
+                ts = a.tile_start + (int64_t)l * (a.nt + 1);
+                const int64_t c0 = (i - G0) + rw * (out_r[k] - U0);  // the previous item's tile
+                kp = i > G0 ? si_tile_of(c0 - (head ? 1 + rw : 1), scale, nte) : -1;
             }
-            const int64_t cost = (i - G0) + rw * (r - U0);
-            const int64_t kt = si_tile_of(cost, scale, nte);
-            int64_t kp = -1;
-            if (i > G0) kp = si_tile_of(cost - (head ? 1 + rw : 1), scale, nte);
+            const int64_t kt = si_tile_of((i - G0) + rw * (out_r[k] - U0), scale, nte);
             for (int64_t kk = kp + 1; kk <= kt; ++kk) ts[kk] = (int32_t)i;
             if (i == G1 - 1)
                 for (int64_t kk = kt + 1; kk <= a.nt; ++kk) ts[kk] = (int32_t)G1;
+            kp = kt;
         }
     }
-    if (i0 + kSiItems <= a.N && ((uintptr_t)(a.su + i0) & 15) == 0 && ((uintptr_t)(a.sseg + i0) & 15) == 0) {
-        reinterpret_cast<int4 *>(a.su + i0)[0] = make_int4(out_r[0], out_r[1], out_r[2], out_r[3]);
-        reinterpret_cast<int4 *>(a.su + i0)[1] = make_int4(out_r[4], out_r[5], out_r[6], out_r[7]);
-        reinterpret_cast<int4 *>(a.sseg + i0)[0] = make_int4(out_s[0], out_s[1], out_s[2], out_s[3]);
-        reinterpret_cast<int4 *>(a.sseg + i0)[1] = make_int4(out_s[4], out_s[5], out_s[6], out_s[7]);
+    __syncthreads();
+    const int nt = (int)(a.N - t0 < kTile ? a.N - t0 : kTile);
+    nh = s_nh;
+    if (nt == kTile && ((uintptr_t)(a.su + t0) & 15) == 0 && ((uintptr_t)(a.sseg + t0) & 15) == 0) {
+        for (int q = threadIdx.x; q < kTile / 4; q += kSiThreads) {
+            reinterpret_cast<int4 *>(a.su + t0)[q] = reinterpret_cast<const int4 *>(s_su)[q];
+            reinterpret_cast<int4 *>(a.sseg + t0)[q] = reinterpret_cast<const int4 *>(s_seg)[q];
+        }
     } else {
-#pragma unroll
-        for (int k = 0; k < kSiItems; ++k)
-            if (i0 + k < a.N) {
-                a.su[i0 + k] = out_r[k];
-                a.sseg[i0 + k] = out_s[k];
-            }
+        for (int q = threadIdx.x; q < nt; q += kSiThreads) {
+            a.su[t0 + q] = s_su[q];
+            a.sseg[t0 + q] = s_seg[q];
+        }
+    }
+    for (int q = threadIdx.x; q < nh; q += kSiThreads) {  // rows starting in this tile: rb .. rb + nh
+        a.ustart[rb + q] = s_us[q];
+        a.run_key[rb + q] = s_key[q];
     }
 }
 
