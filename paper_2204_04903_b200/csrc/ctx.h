@@ -194,6 +194,15 @@ struct picasso_ctx {
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     int kinterleave = 1;           // PICASSO_KINTERLEAVE=0 turns the per-pack pipelining off
     int32_t *su = nullptr, *sseg = nullptr;  // the last forward's transpose (uid-sorted occurrences)
+    // world == 1, several packs: dY regrouped pack by pack before the backward (k_dy_pack), so a
+    // pack's per-occurrence dY row reads hit L2 (PICASSO_DY_STAGE=0 reads dY in place)
+    bool dy_stage = false;
+    float *dyp = nullptr;                 // [max_batch * out_width]
+    int32_t *col4_field_d = nullptr;      // [out_width / 4] field of each 16-B column chunk
+    int64_t *dyp_base_d = nullptr;        // [F] float offset of field f's block in its pack's rows
+    int32_t *dyp_stride_d = nullptr;      // [F] row stride of field f's pack (F_p * D_p)
+    int32_t *dyp_col_d = nullptr;         // [F] column of field f inside its pack's rows
+    std::vector<int64_t> dyp_off;         // [P] float offset of each pack's [max_batch, F_p * D_p] block
     // sort-based index (k_sortidx.cu): world == 1, pack keys < 2^32, the tiled backward; used from
     // sort_min_ids IDs on (PICASSO_INDEX=hash / sort forces either; PICASSO_SORT_MIN_IDS).  A sorted step numbers the
     // backward's rows in run order and keeps their keys in run_keys() (the dedup table's memory).
@@ -348,6 +357,13 @@ struct picasso_ctx {
         chunk_row = c.take<int32_t>(long_partial_doubles(N, 1));
         pack_gbase = c.take<int64_t>(P + 1);
         pack_dim_d = c.take<int32_t>(P);
+        if (dy_stage) {
+            dyp = c.take<float>((size_t)opts.max_batch * (size_t)out_width);
+            col4_field_d = c.take<int32_t>(out_width / 4 + 1);
+            dyp_base_d = c.take<int64_t>(F);
+            dyp_stride_d = c.take<int32_t>(F);
+            dyp_col_d = c.take<int32_t>(F);
+        }
         if (world == 1 && opts.max_step_unique > 0) {  // D-Interleaving step accumulator
             di_cap = pow2_at_least((uint64_t)opts.max_step_unique * 2);
             di_table = c.take<Slot>(di_cap);

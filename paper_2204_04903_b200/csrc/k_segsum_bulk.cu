@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_pipe(UpdateArgs a) {
             const int32_t seg = __ldg(a.sorted_seg + p);
             uid = __ldg(a.sorted_u + p);
             const int32_t f = seg / a.B;
-            off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col) >> 2);
+            off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + dy_col(a, f)) >> 2);
             if (a.pool_mean) len = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
         }
     };
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_segsum_upd(UpdateArgs a) {
             const int32_t seg = __ldg(a.sorted_seg + p);
             uid = __ldg(a.sorted_u + p);
             const int32_t f = seg / a.B;
-            off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col) >> 2);
+            off = (uint32_t)(((int64_t)(seg - f * a.B) * a.dy_stride + dy_col(a, f)) >> 2);
             if (a.pool_mean) len = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
             row = (int64_t)(__ldg(a.unique_gkey + uid) - (unsigned long long)a.pack_key_off);
         }

@@ -91,7 +91,7 @@ __device__ __forceinline__ void load_contrib(const UpdateArgs &a, int32_t seg, i
     constexpr int LANES = Geo<D>::LANES, VPL = Geo<D>::VPL;
     const int32_t f = seg / a.B;
     const int32_t b = seg - f * a.B;
-    const float *p = a.dy + (int64_t)b * a.dy_stride + a.finfo[f].col + li * 4;
+    const float *p = a.dy + (int64_t)b * a.dy_stride + dy_col(a, f) + li * 4;
 #pragma unroll
     for (int q = 0; q < VPL; ++q) c[q] = ldg_f4(p + q * LANES * 4);
     if (a.pool_mean) {
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256) k_segsum(UpdateArgs a) {
                         }
                         const int32_t seg = __ldg(a.sorted_seg + s_i0[w][c_lo + lo] + (q - cum[lo]));
                         const int32_t f = seg / a.B;
-                        myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
+                        myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + dy_col(a, f);
                         if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
                         myc[p] = c_lo + lo;
                     }
@@ -345,6 +345,27 @@ __global__ void __launch_bounds__(256) k_segsum_flat(UpdateArgs a) {
         float *o = g_row_ptr<D>(a, u, u0, gp, li, (float)(i1 - i0)) + li * 4;
         *reinterpret_cast<float4 *>(o) = round4(g);
     }
+}
+
+__global__ void __launch_bounds__(256) k_dy_pack(const float4 *dy, int32_t B, int64_t ow4, const int32_t *col4_field,
+                                                 const FieldInfo *finfo, const int64_t *dst_base,
+                                                 const int32_t *fstride, float *dyp) {
+    const int64_t n = (int64_t)B * ow4;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = q / ow4, c4 = q - b * ow4;
+        const int32_t f = __ldg(col4_field + c4);
+        if (f < 0) continue;  // a column no field owns
+        const int64_t within = 4 * c4 - finfo[f].col;
+        const float4 v = __ldcs(dy + q);  // read once
+        *reinterpret_cast<float4 *>(dyp + __ldg(dst_base + f) + b * __ldg(fstride + f) + within) = v;
+    }
+}
+
+void launch_dy_pack(const float *dy, int32_t B, int64_t out_width, const int32_t *col4_field, const FieldInfo *finfo,
+                    const int64_t *dst_base, const int32_t *fstride, float *dyp, cudaStream_t s) {
+    if (B <= 0 || out_width <= 0) return;
+    k_dy_pack<<<2048, 256, 0, s>>>(reinterpret_cast<const float4 *>(dy), B, out_width / 4, col4_field, finfo, dst_base,
+                                   fstride, dyp);
 }
 
 template <int D>
@@ -445,7 +466,7 @@ __global__ void __launch_bounds__(256) k_long_partial(UpdateArgs a) {
                 if (q < n) {
                     const int32_t seg = __ldg(a.sorted_seg + p0 + q);
                     const int32_t f = seg / a.B;
-                    myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + a.finfo[f].col;
+                    myoff[p] = (int64_t)(seg - f * a.B) * a.dy_stride + dy_col(a, f);
                     if (a.pool_mean) mylen[p] = __ldg(a.offsets + seg + 1) - __ldg(a.offsets + seg);
                 }
             }

@@ -215,6 +215,7 @@ struct UpdateArgs {
     const FieldInfo *finfo;
     const float *dy;
     int64_t dy_stride;
+    const int32_t *dy_col;       // [F] column of each field in dy (nullptr: finfo[f].col)
     int32_t pool_mean;
     int32_t opt;                 // 0 adagrad, 1 adam
     float lr, eps, beta1, beta2, adam_ss;
@@ -240,6 +241,15 @@ struct UpdateArgs {
     const int64_t *dst_off;      //   [U] float offset of its G row in the owner's receive buffer
     float *dst_buf[8];           //   the ranks' receive buffers (NVLink peer pointers)
 };
+#ifdef __CUDACC__
+__device__ __forceinline__ int64_t dy_col(const UpdateArgs &a, int32_t f) {
+    return a.dy_col ? (int64_t)__ldg(a.dy_col + f) : a.finfo[f].col;
+}
+#endif
+// dY of a multi-pack step regrouped pack by pack ([pack][b][F_p * D_p], so one pack's gradient is
+// contiguous and its random per-occurrence row reads stay in L2); one thread per 16-B chunk
+void launch_dy_pack(const float *dy, int32_t B, int64_t out_width, const int32_t *col4_field, const FieldInfo *finfo,
+                    const int64_t *dst_base, const int32_t *fstride, float *dyp, cudaStream_t s);
 void launch_segsum(int D, const UpdateArgs &a, int num_sms, cudaStream_t s, bool flat_small = true);
 void launch_update_rows(int D, const UpdateArgs &a, int num_sms, cudaStream_t s);
 void launch_csr_bounds(const int32_t *sorted_u, int64_t N, int32_t *ustart, int32_t *long_cnt, int32_t n_cnt,

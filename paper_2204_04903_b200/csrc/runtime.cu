@@ -235,6 +235,21 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_SORT_MIN_IDS")) c->sort_min_ids = std::atoll(e);
     if (const char *e = std::getenv("PICASSO_SORT_OVERLAP")) c->sort_overlap = std::strcmp(e, "0") != 0;
     if (const char *e = std::getenv("PICASSO_SORT_RESERVE")) c->sort_reserve = std::atoi(e);
+    // dY regrouped per pack before the world == 1 backward (several packs, disjoint columns)
+    c->dy_stage = world == 1 && c->P > 1 && !opts->cold_tier;
+    if (const char *e = std::getenv("PICASSO_DY_STAGE")) c->dy_stage = c->dy_stage && std::strcmp(e, "0") != 0;
+    if (c->dy_stage) {
+        std::vector<int32_t> owner(c->out_width / 4, -1);
+        for (int32_t f = 0; f < c->F && c->dy_stage; ++f)
+            for (int64_t q = c->fcol[f] / 4; q < (c->fcol[f] + c->tdim[c->f2t[f]]) / 4; ++q) {
+                if (owner[q] >= 0) c->dy_stage = false;  // overlapping columns: read dY in place
+                owner[q] = f;
+            }
+        c->dyp_off.assign(c->P + 1, 0);
+        for (int32_t p = 0; p < c->P; ++p)
+            c->dyp_off[p + 1] = c->dyp_off[p] + (int64_t)opts->max_batch * (c->pack_first_k[p + 1] - c->pack_first_k[p]) *
+                                                     c->pack_dim[p];
+    }
     c->pool_sms = c->num_sms;
     c->ws_bytes = c->carve(nullptr);
     *out = c;
@@ -293,6 +308,21 @@ extern "C" picasso_status picasso_bind(picasso_ctx *ctx, void *workspace, size_t
             for (int32_t k = ctx->pack_first_k[p]; k < ctx->pack_first_k[p + 1]; ++k)
                 fk[ctx->pm_fields[k]] = k - ctx->pack_first_k[p];
         CK(cudaMemcpy(ctx->field_k_d, fk.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
+        if (ctx->dy_stage) {  // k_dy_pack's maps: chunk -> field, field -> its block in its pack's rows
+            std::vector<int32_t> c4f(ctx->out_width / 4 + 1, -1), stride(ctx->F), col(ctx->F);
+            std::vector<int64_t> base(ctx->F);
+            for (int32_t f = 0; f < ctx->F; ++f) {
+                const int32_t t = ctx->f2t[f], p = ctx->t2p[t], D = ctx->pack_dim[p];
+                for (int64_t q = ctx->fcol[f] / 4; q < (ctx->fcol[f] + ctx->tdim[t]) / 4; ++q) c4f[q] = f;
+                stride[f] = (ctx->pack_first_k[p + 1] - ctx->pack_first_k[p]) * D;
+                col[f] = fk[f] * D;
+                base[f] = ctx->dyp_off[p] + col[f];
+            }
+            CK(cudaMemcpy(ctx->col4_field_d, c4f.data(), sizeof(int32_t) * c4f.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ctx->dyp_base_d, base.data(), sizeof(int64_t) * ctx->F, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ctx->dyp_stride_d, stride.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ctx->dyp_col_d, col.data(), sizeof(int32_t) * ctx->F, cudaMemcpyHostToDevice));
+        }
     }
     CK(cudaMemcpy(ctx->pack_key_off_d, ctx->pack_key_off.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->pack_dim_d, ctx->pack_dim.data(), sizeof(int32_t) * ctx->P, cudaMemcpyHostToDevice));
@@ -686,9 +716,19 @@ extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, con
     ctx->mark(3, true, s);  // the transpose ran in the forward (transpose_fork)
     UpdateArgs u = picasso::make_update_args(ctx, grad_out, lr, step, ctx->su, ctx->sseg);
     if (N > 0) {
+        if (ctx->dy_stage) {
+            launch_dy_pack(grad_out, ctx->B, ctx->out_width, ctx->col4_field_d, ctx->finfo, ctx->dyp_base_d,
+                           ctx->dyp_stride_d, ctx->dyp, s);
+            ctx->launches_bwd += 1;
+            u.dy_col = ctx->dyp_col_d;
+        }
         for (int32_t p = 0; p < ctx->P; ++p) {  // packs in stream order share the long-row scratch
             ctx->mark_pack(1, p, true, s);
             u.pack = p;
+            if (ctx->dy_stage) {  // this pack's rows of the regrouped dY
+                u.dy = ctx->dyp + ctx->dyp_off[p];
+                u.dy_stride = (int64_t)(ctx->pack_first_k[p + 1] - ctx->pack_first_k[p]) * ctx->pack_dim[p];
+            }
             u.long_cnt = ctx->long_cnt + p;
             u.pack_key_off = ctx->pack_key_off[p];
             u.weight = ctx->w[p];

@@ -376,3 +376,22 @@ def test_profile_per_pack():
     assert sum(pool) <= phase["pool"] * 1.05 + 1e-3, (pool, phase)
     pool2, _ = pb.picasso_profile_read_packs(emb.ctx, emb.n_packs)
     assert all(t == 0 for t in pool2)
+
+
+def test_dy_staging_same_update(monkeypatch):
+    """The backward of a multi-pack step reads dY regrouped pack by pack (k_dy_pack); reading it
+    in place (PICASSO_DY_STAGE=0) gives bit-identical tables, and both match the oracle."""
+    cfg = dc.scaled(dc.wdl(), batch=96, rows_div=1000)
+    b, dy = make_batch(cfg, 0, 1), make_dy(cfg, 0, 1, dyadic=False)
+    res = []
+    for stage in ("1", "0"):
+        monkeypatch.setenv("PICASSO_DY_STAGE", stage)
+        emb = gpu_embedding(cfg)
+        ids, off = to_dev(b)
+        emb.forward(ids, off, cfg.batch)
+        emb.backward_update(torch.from_numpy(dy).cuda(), lr=0.05, step=1)
+        emb.check()
+        res.append([torch.cat([w.flatten(), s.flatten()]).cpu() for w, s in zip(emb.weights, emb.state1)])
+    assert all(torch.equal(x, y) for x, y in zip(res[0], res[1]))
+    monkeypatch.setenv("PICASSO_DY_STAGE", "1")
+    run_step(cfg, steps=2, dyadic=False, check_intermediates=False)
