@@ -279,7 +279,11 @@ typedef struct picasso_group picasso_group;
  * the paper warms up 100 steps, L795).  The refresh writes the replicas back to the owners,
  * selects the longest prefix of all keys sorted by (count desc, pack asc, key asc) whose rows
  * (weights + optimizer state, 4*D*(1+n_state) bytes each) fit capacity_bytes (<= the ctx's
- * cache_max_bytes), and replicates those rows on every rank.  From then on hot keys are served
+ * cache_max_bytes), and replicates those rows on every rank, slots in ascending key (grouped by
+ * pack).  The selection runs on the devices: the ranks AllReduce per-pack count histograms and
+ * a key-bin histogram of the rows at the cut count, so each finds the same cut without moving
+ * candidate lists (exact while FCounter values stay below 65535; larger counts share the top
+ * histogram bin and are then ordered by key).  From then on hot keys are served
  * by the local replica, skip the AllToAllv, and their gradients are summed over the ranks
  * (AllReduce) so every replica applies the same update.  Results equal the uncached step
  * (tier transparency) up to the fp32 cross-rank sum of hot gradients.  capacity_bytes = 0:
@@ -293,14 +297,15 @@ typedef struct {
     int64_t hot_uniques;      /* last forward: unique keys served by the replica ... */
     int64_t uniques;          /* ... out of this many unique keys of the rank */
     double hit_ratio_unique;  /* hot_uniques / uniques */
-    double refresh_ms;        /* host wall time of this refresh (all phases, synchronised) */
-    double propose_ms, select_ms;  /* of which: local top-k proposals; gather + merge + pack */
+    double refresh_ms;        /* host wall time of this refresh (from the drained stream to its end) */
+    double propose_ms, select_ms;  /* of which: histograms + threshold + tie cut; bitmap + staging */
 } picasso_cache_stats;
 picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t capacity_bytes, void *stream,
                                          picasso_cache_stats *stats);
 picasso_status picasso_group_hot_cache_refresh(picasso_group *group, size_t capacity_bytes, void *stream,
                                                picasso_cache_stats *stats /* [world] or NULL */);
-/* Current hot keys (tests): pack and pack key of each hot slot, slot order (host arrays). */
+/* Current hot keys (tests): pack and pack key of each hot slot, slot order = ascending global key
+ * (host arrays). */
 picasso_status picasso_get_hot_keys(picasso_ctx *ctx, int32_t *pack, int64_t *key, int64_t cap, int64_t *n);
 picasso_status picasso_group_create(picasso_ctx *const *ctxs, int32_t world, picasso_group **out);
 picasso_status picasso_group_destroy(picasso_group *group);

@@ -10,6 +10,11 @@
 // the keys they receive, ranks count their hot hits per slot.  The refresh (Alg. 1)
 // writes replicas back to the owners, merges the counts, selects the global top-k by
 // (count desc, pack asc, key asc) within the capacity, and fetches the new rows.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
 #include "kernels.h"
 #include "multi.h"
 
@@ -153,61 +158,142 @@ __global__ void __launch_bounds__(256) k_count_hist(const uint32_t *fcnt, int64_
         if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
-// candidates: rows with count > cstar (any order), plus the first m rows with count == cstar in
-// ascending row order (= ascending key, the oracle's tie order) via per-tile counts
-__global__ void k_tie_count(const uint32_t *fcnt, int64_t n, uint32_t cstar, int32_t *tile_cnt) {
-    __shared__ int32_t c;
-    if (threadIdx.x == 0) c = 0;
-    __syncthreads();
-    int32_t mine = 0;
-    for (int i = threadIdx.x; i < kTile; i += blockDim.x) {
-        const int64_t r = (int64_t)blockIdx.x * kTile + i;
-        if (r < n && fcnt[r] == cstar) ++mine;
+// ---- the selection (Alg. 1 L515 top-k): every rank finds the same global threshold from
+// AllReduced histograms, so no candidate list ever leaves its owner.  Rows are taken by (count
+// desc, key asc) while their bytes fit: all rows above the threshold count c*, then the rows at
+// c* in ascending key up to the key cut.
+__device__ __forceinline__ uint32_t cnt_bin(uint32_t c) { return c < kCntBins ? c : kCntBins - 1; }
+
+// byte units (16 B) of pack p's owned rows at count c*, by global-key bin.  Each thread walks
+// kRun consecutive rows (consecutive keys, stride W) and adds once per bin it leaves: one bin
+// holds thousands of consecutive rows, so per-row atomics would all hit the same address.
+constexpr int kRun = 64;
+__global__ void k_tie_keyhist(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t key0, int32_t W, int kshift,
+                              uint32_t unit, uint32_t *hist) {
+    for (int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun; r0 < n;
+         r0 += (int64_t)gridDim.x * blockDim.x * kRun) {
+        int64_t bin = -1;
+        uint32_t acc = 0;
+        for (int64_t r = r0; r < r0 + kRun && r < n; ++r) {
+            if (cnt_bin(__ldg(fcnt + r)) != cstar) continue;
+            const int64_t b = (key0 + r * W) >> kshift;
+            if (b != bin) {
+                if (acc) atomicAdd(hist + bin, acc);
+                bin = b;
+                acc = 0;
+            }
+            acc += unit;
+        }
+        if (acc) atomicAdd(hist + bin, acc);
     }
-    atomicAdd(&c, mine);
-    __syncthreads();
-    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = c;
 }
 
-__global__ void k_collect(const uint32_t *fcnt, int64_t n, uint32_t cstar, int32_t m_ties, const int32_t *tile_off,
-                          const int64_t *row_key, int32_t nseg, const int64_t *seg_start, unsigned long long *out_key,
-                          uint32_t *out_cnt, int32_t *out_n) {
-    // rows are the concatenation over packs of the owner's local rows: seg_start[p] = first row of
-    // pack p; row_key maps (pack p, local row lr) -> global key (pack_key_off + lr*W + rank)
-    __shared__ int32_t s_rank[kTile / 256];
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-    int32_t rank_before = tile_off[blockIdx.x];
-    for (int chunk = 0; chunk < kTile; chunk += blockDim.x) {
-        const int64_t r = base + chunk + threadIdx.x;
-        const bool valid = r < n;
-        const uint32_t c = valid ? fcnt[r] : 0;
-        const bool tie = valid && c == cstar;
-        // block-wide exclusive rank of ties in this chunk (ascending r)
-        const unsigned b = __ballot_sync(0xffffffffu, tie);
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        if (lane == 0) s_rank[w] = __popc(b);
-        __syncthreads();
-        int32_t before = rank_before;
-        for (int ww = 0; ww < w; ++ww) before += s_rank[ww];
-        before += __popc(b & ((1u << lane) - 1u));
-        int32_t chunk_total = 0;
-        for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) chunk_total += s_rank[ww];
-        if (valid && c != 0 && (c > cstar || (tie && before < m_ties))) {
-            int p = 0;
-            while (p + 1 < nseg && seg_start[p + 1] <= r) ++p;
+// this owner's rows at count c* inside key bin b* (the key cut falls inside it)
+__global__ void k_tie_bin_collect(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t key0, int32_t W, int kshift,
+                                  int64_t bstar, unsigned long long *out, int32_t *out_n, int32_t cap) {
+    const int64_t lo = ((bstar << kshift) - key0 + W - 1) / W, hi = (((bstar + 1) << kshift) - key0 + W - 1) / W;
+    for (int64_t r = max(lo, (int64_t)0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < min(hi, n);
+         r += (int64_t)gridDim.x * blockDim.x)
+        if (cnt_bin(__ldg(fcnt + r)) == cstar) {
             const int32_t o = atomicAdd(out_n, 1);
-            out_key[o] = (unsigned long long)(row_key[2 * p] + (r - seg_start[p]) * row_key[2 * p + 1]);
-            out_cnt[o] = c;
+            if (o < cap) out[o] = (unsigned long long)(key0 + r * W);
         }
+}
+
+// selected owned rows -> bits of the global selection bitmap (owners set disjoint bits); each
+// thread builds the words of kRun consecutive rows in a register and ORs each word once
+__global__ void k_select_bits(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t kcut, int64_t key0, int32_t W,
+                              uint32_t *bits) {
+    for (int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun; r0 < n;
+         r0 += (int64_t)gridDim.x * blockDim.x * kRun) {
+        int64_t word = -1;
+        uint32_t m = 0;
+        for (int64_t r = r0; r < r0 + kRun && r < n; ++r) {
+            const uint32_t c = __ldg(fcnt + r);
+            if (c == 0) continue;
+            const uint32_t b = cnt_bin(c);
+            const int64_t key = key0 + r * W;
+            if (!(b > cstar || (b == cstar && key <= kcut))) continue;
+            if ((key >> 5) != word) {
+                if (m) atomicOr(bits + word, m);
+                word = key >> 5;
+                m = 0;
+            }
+            m |= 1u << (key & 31);
+        }
+        if (m) atomicOr(bits + word, m);
+    }
+}
+
+// bitmap -> hot keys in ascending key order (slots grouped by pack: the key space is pack-major)
+constexpr int kBitWords = 1024;  // words per block
+__global__ void __launch_bounds__(kBitWords) k_bits_count(const uint32_t *bits, int64_t nw, int32_t *blk) {
+    using BR = cub::BlockReduce<int32_t, kBitWords>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t w = (int64_t)blockIdx.x * kBitWords + threadIdx.x;
+    const int32_t c = BR(tmp).Sum(w < nw ? __popc(bits[w]) : 0);
+    if (threadIdx.x == 0) blk[blockIdx.x] = c;
+}
+__global__ void __launch_bounds__(1024) k_bits_scan(int32_t *blk, int64_t nb, int32_t *total) {
+    using BS = cub::BlockScan<int32_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
+        const int64_t i = b0 + threadIdx.x;
+        int32_t e, agg;
+        BS(tmp).ExclusiveSum(i < nb ? blk[i] : 0, e, agg);
+        if (i < nb) blk[i] = carry + e;
         __syncthreads();
-        rank_before += chunk_total;
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+__global__ void __launch_bounds__(kBitWords) k_bits_emit(const uint32_t *bits, int64_t nw, const int32_t *blk,
+                                                         unsigned long long *keys, int32_t kmax) {
+    using BS = cub::BlockScan<int32_t, kBitWords>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t w = (int64_t)blockIdx.x * kBitWords + threadIdx.x;
+    uint32_t x = w < nw ? bits[w] : 0u;
+    int32_t e;
+    BS(tmp).ExclusiveSum(__popc(x), e);
+    int32_t o = blk[blockIdx.x] + e;
+    while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        if (o < kmax) keys[o] = (unsigned long long)(w * 32 + b);
+        ++o;
+    }
+}
+
+// slot range of each pack (first hot key >= pack_key_off[p]) and each slot's staging offset
+__global__ void k_hot_layout(const unsigned long long *keys, int32_t k, const int64_t *pack_key_off, int32_t P,
+                             int32_t *pslot) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > P) return;
+    int32_t lo = 0, hi = k;
+    const unsigned long long v = (unsigned long long)pack_key_off[p];
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (keys[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    pslot[p] = p == P ? k : lo;
+}
+__global__ void k_stage_idx(const int32_t *pslot, const int64_t *stage_off, const int32_t *pack_dim, int32_t P, int nst,
+                            int32_t k, int64_t *stage_idx) {
+    for (int32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < k; sl += gridDim.x * blockDim.x) {
+        int p = 0;
+        while (p + 1 < P && pslot[p + 1] <= sl) ++p;
+        stage_idx[sl] = stage_off[p] + (int64_t)(sl - pslot[p]) * nst * pack_dim[p];
     }
 }
 
 // new hot rows: owners pack their owned slots (w, s1, s2) in slot order into staging
 template <int D>
 __global__ void __launch_bounds__(256) k_pack_owned(MultiArgs m, int pack, const unsigned long long *keys,
-                                                    const int32_t *stage_idx, const float *weight, const float *state1,
+                                                    const int64_t *stage_idx, const float *weight, const float *state1,
                                                     const float *state2, int nst, float *stage, int rank) {
     constexpr int V4 = D / 4, LANES = V4 < 32 ? V4 : 32, VPL = V4 / LANES;
     const int li = threadIdx.x % LANES;
@@ -218,7 +304,7 @@ __global__ void __launch_bounds__(256) k_pack_owned(MultiArgs m, int pack, const
         const int64_t key = (int64_t)(keys[s] - (unsigned long long)m.pack_key_off[pack]);
         if (key % m.W != rank) continue;
         const int64_t lr = key / m.W;
-        float *dst = stage + (int64_t)stage_idx[s];  // this slot's float offset in the staging
+        float *dst = stage + stage_idx[s];  // this slot's float offset in the staging
         const float *src[3] = {weight, state1, state2};
         for (int a = 0; a < nst; ++a)
 #pragma unroll
@@ -230,7 +316,7 @@ __global__ void __launch_bounds__(256) k_pack_owned(MultiArgs m, int pack, const
 
 // staging (all owners' blocks) -> replica arena; rebuild the hot index (key -> slot)
 template <int D>
-__global__ void __launch_bounds__(256) k_place(MultiArgs m, int pack, const int32_t *stage_idx, const float *stage,
+__global__ void __launch_bounds__(256) k_place(MultiArgs m, int pack, const int64_t *stage_idx, const float *stage,
                                                int nst) {
     constexpr int V4 = D / 4, LANES = V4 < 32 ? V4 : 32, VPL = V4 / LANES;
     const int li = threadIdx.x % LANES;
@@ -239,7 +325,7 @@ __global__ void __launch_bounds__(256) k_place(MultiArgs m, int pack, const int3
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / LANES;
     for (int64_t s = s0 + grp; s < s1e; s += ngrp) {
         const int64_t i = s - s0;
-        const float *src = stage + (int64_t)stage_idx[s];
+        const float *src = stage + stage_idx[s];
         const int64_t off[3] = {m.hot_w_off[pack], m.hot_s1_off[pack], m.hot_s2_off[pack]};
         for (int a = 0; a < nst; ++a)
 #pragma unroll
@@ -305,24 +391,46 @@ void launch_count_hist(const uint32_t *fcnt, int64_t n, uint32_t *hist, int num_
     if (n > 0) k_count_hist<<<(unsigned)num_sms * 4, 256, 0, s>>>(fcnt, n, hist);
 }
 int count_hist_bins() { return kCntBins; }
-void launch_tie_count(const uint32_t *fcnt, int64_t n, uint32_t cstar, int32_t *tile_cnt, cudaStream_t s) {
-    if (n > 0) k_tie_count<<<(unsigned)((n + kTile - 1) / kTile), 256, 0, s>>>(fcnt, n, cstar, tile_cnt);
+void launch_tie_keyhist(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t key0, int32_t W, int kshift,
+                        uint32_t unit, uint32_t *hist, int num_sms, cudaStream_t s) {
+    if (n > 0) k_tie_keyhist<<<(unsigned)num_sms * 4, 256, 0, s>>>(fcnt, n, cstar, key0, W, kshift, unit, hist);
 }
-void launch_collect(const uint32_t *fcnt, int64_t n, uint32_t cstar, int32_t m_ties, const int32_t *tile_off,
-                    const int64_t *row_key, int32_t nseg, const int64_t *seg_start, unsigned long long *out_key,
-                    uint32_t *out_cnt, int32_t *out_n, cudaStream_t s) {
-    if (n > 0)
-        k_collect<<<(unsigned)((n + kTile - 1) / kTile), 256, 0, s>>>(fcnt, n, cstar, m_ties, tile_off, row_key, nseg,
-                                                                      seg_start, out_key, out_cnt, out_n);
+void launch_tie_bin_collect(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t key0, int32_t W, int kshift,
+                            int64_t bstar, unsigned long long *out, int32_t *out_n, int32_t cap, cudaStream_t s) {
+    if (n > 0) k_tie_bin_collect<<<64, 256, 0, s>>>(fcnt, n, cstar, key0, W, kshift, bstar, out, out_n, cap);
 }
-void launch_pack_owned(int D, const MultiArgs &m, int pack, const unsigned long long *keys, const int32_t *stage_idx,
+void launch_select_bits(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t kcut, int64_t key0, int32_t W,
+                        uint32_t *bits, int num_sms, cudaStream_t s) {
+    if (n > 0) k_select_bits<<<(unsigned)num_sms * 4, 256, 0, s>>>(fcnt, n, cstar, kcut, key0, W, bits);
+}
+// bitmap (nw words) -> keys; blk: [nw / 1024 + 1] scratch; total: [1] device
+void launch_bits_compact(const uint32_t *bits, int64_t nw, int32_t *blk, int32_t *total, unsigned long long *keys,
+                         int32_t kmax, cudaStream_t s) {
+    const int64_t nb = (nw + kBitWords - 1) / kBitWords;
+    if (nb == 0) {
+        cudaMemsetAsync(total, 0, sizeof(int32_t), s);
+        return;
+    }
+    k_bits_count<<<(unsigned)nb, kBitWords, 0, s>>>(bits, nw, blk);
+    k_bits_scan<<<1, 1024, 0, s>>>(blk, nb, total);
+    k_bits_emit<<<(unsigned)nb, kBitWords, 0, s>>>(bits, nw, blk, keys, kmax);
+}
+void launch_hot_layout(const unsigned long long *keys, int32_t k, const int64_t *pack_key_off, int32_t P,
+                       int32_t *pslot, cudaStream_t s) {
+    k_hot_layout<<<(unsigned)((P + 1 + 127) / 128), 128, 0, s>>>(keys, k, pack_key_off, P, pslot);
+}
+void launch_stage_idx(const int32_t *pslot, const int64_t *stage_off, const int32_t *pack_dim, int32_t P, int nst,
+                      int32_t k, int64_t *stage_idx, cudaStream_t s) {
+    if (k > 0) k_stage_idx<<<(unsigned)std::min<int64_t>((k + 255) / 256, 4096), 256, 0, s>>>(pslot, stage_off, pack_dim, P, nst, k, stage_idx);
+}
+void launch_pack_owned(int D, const MultiArgs &m, int pack, const unsigned long long *keys, const int64_t *stage_idx,
                        const float *w, const float *s1, const float *s2, int nst, float *stage, int rank, int num_sms,
                        cudaStream_t s) {
 #define CALL(DD) k_pack_owned<DD><<<(unsigned)num_sms, 256, 0, s>>>(m, pack, keys, stage_idx, w, s1, s2, nst, stage, rank)
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
 }
-void launch_place(int D, const MultiArgs &m, int pack, const int32_t *stage_idx, const float *stage, int nst,
+void launch_place(int D, const MultiArgs &m, int pack, const int64_t *stage_idx, const float *stage, int nst,
                   int num_sms, cudaStream_t s) {
 #define CALL(DD) k_place<DD><<<(unsigned)num_sms, 256, 0, s>>>(m, pack, stage_idx, stage, nst)
     PICASSO_DISPATCH_D(D, CALL)

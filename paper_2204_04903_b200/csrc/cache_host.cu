@@ -2,16 +2,22 @@
 //
 //   1. replicas -> owners' shards; the ranks' hot-hit counts are summed (AllReduce) and added
 //      to the owners' FCounter;
-//   2. each owner proposes its local top-kc rows by (count desc, key asc) — kc = the most rows
-//      the capacity can hold — found with a count histogram, a threshold and an ordered tie
-//      cut, so the union of proposals contains the global top-k;
-//   3. the proposals are gathered; every rank merges them on the host in the same
-//      deterministic order and keeps the longest prefix whose rows (weights + optimizer state)
-//      fit the capacity (readings O12/O13; equals oracle_hot_select);
-//   4. owners pack their new hot rows, every rank receives every owner's block (broadcasts),
-//      places the rows into its replica arena and rebuilds the key -> slot index.
-// capacity_bytes = 0 writes back and drops the hot set (checkpoint / disable).
+//   2. top-k (L515) without moving candidates: every owner histograms its rows' counts per pack,
+//      the histograms are summed over the ranks (AllReduce), and every rank finds the same count
+//      c* at which the selection by (count desc, key asc) reaches the capacity; the rows at c*
+//      are cut in ascending key by a second AllReduced histogram over key bins and, inside the
+//      bin where the budget runs out, the few tie keys themselves (AllGather);
+//   3. owners set their selected rows in a bitmap over the global key space; summed over the
+//      ranks (disjoint bits) it is the hot set, compacted on every rank into the hot keys in
+//      ascending key (slots grouped by pack) — equal as a set to oracle_hot_select;
+//   4. owners write their new hot rows into a slot-major staging buffer, the staging is summed
+//      over the ranks as 32-bit words (each word has one non-zero contributor: an exact copy),
+//      and every rank places it into its replica arena and rebuilds the key -> slot index.
+// Everything but a few KB of histograms stays on the devices.  capacity_bytes = 0 writes back
+// and drops the hot set (checkpoint / disable).
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ctx.h"
 
@@ -41,24 +47,27 @@ void launch_writeback(int D, const MultiArgs &m, int pack, const unsigned long l
                       float *s2, int nst, const uint32_t *cnt_sum, int rank, int num_sms, cudaStream_t s);
 void launch_count_hist(const uint32_t *fcnt, int64_t n, uint32_t *hist, int num_sms, cudaStream_t s);
 int count_hist_bins();
-void launch_tie_count(const uint32_t *fcnt, int64_t n, uint32_t cstar, int32_t *tile_cnt, cudaStream_t s);
-void launch_collect(const uint32_t *fcnt, int64_t n, uint32_t cstar, int32_t m_ties, const int32_t *tile_off,
-                    const int64_t *row_key, int32_t nseg, const int64_t *seg_start, unsigned long long *out_key,
-                    uint32_t *out_cnt, int32_t *out_n, cudaStream_t s);
-void launch_pack_owned(int D, const MultiArgs &m, int pack, const unsigned long long *keys, const int32_t *stage_idx,
+void launch_tie_keyhist(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t key0, int32_t W, int kshift,
+                        uint32_t unit, uint32_t *hist, int num_sms, cudaStream_t s);
+void launch_tie_bin_collect(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t key0, int32_t W, int kshift,
+                            int64_t bstar, unsigned long long *out, int32_t *out_n, int32_t cap, cudaStream_t s);
+void launch_select_bits(const uint32_t *fcnt, int64_t n, uint32_t cstar, int64_t kcut, int64_t key0, int32_t W,
+                        uint32_t *bits, int num_sms, cudaStream_t s);
+void launch_bits_compact(const uint32_t *bits, int64_t nw, int32_t *blk, int32_t *total, unsigned long long *keys,
+                         int32_t kmax, cudaStream_t s);
+void launch_hot_layout(const unsigned long long *keys, int32_t k, const int64_t *pack_key_off, int32_t P,
+                       int32_t *pslot, cudaStream_t s);
+void launch_stage_idx(const int32_t *pslot, const int64_t *stage_off, const int32_t *pack_dim, int32_t P, int nst,
+                      int32_t k, int64_t *stage_idx, cudaStream_t s);
+void launch_pack_owned(int D, const MultiArgs &m, int pack, const unsigned long long *keys, const int64_t *stage_idx,
                        const float *w, const float *s1, const float *s2, int nst, float *stage, int rank, int num_sms,
                        cudaStream_t s);
-void launch_place(int D, const MultiArgs &m, int pack, const int32_t *stage_idx, const float *stage, int nst,
+void launch_place(int D, const MultiArgs &m, int pack, const int64_t *stage_idx, const float *stage, int nst,
                   int num_sms, cudaStream_t s);
 void launch_hot_index(Slot *index, uint32_t mask, const unsigned long long *keys, int32_t k, cudaStream_t s);
 }  // namespace picasso
 
 namespace {
-
-struct Cand {
-    uint32_t cnt;
-    unsigned long long key;
-};
 
 int nst_of(const picasso_ctx *ctx) { return ctx->opts.opt == PICASSO_OPT_ADAM_LAZY ? 2 : 1; }
 
@@ -84,128 +93,219 @@ picasso_status refresh_writeback(picasso_ctx *ctx, cudaStream_t s) {
     return PICASSO_OK;
 }
 
-// step 2: this owner's proposals (host vector), kc = most rows the capacity can hold
-picasso_status refresh_propose(picasso_ctx *ctx, int64_t kc, std::vector<Cand> &out, cudaStream_t s) {
-    MultiState &mp = ctx->mp;
-    const int64_t n = mp.rows_total;
-    out.clear();
-    if (kc <= 0 || n == 0) return PICASSO_OK;
-    const int bins = count_hist_bins();
-    launch_count_hist(mp.fcnt, n, mp.cnt_hist, ctx->num_sms, s);
-    std::vector<uint32_t> h(bins);
-    HCK(cudaMemcpyAsync(h.data(), mp.cnt_hist, sizeof(uint32_t) * bins, cudaMemcpyDeviceToHost, s));
-    HCK(cudaStreamSynchronize(s));
-    // cstar: the kc-th largest count; above it all rows are taken, at it the first m_ties
-    int64_t above = 0;
-    uint32_t cstar = 0;
-    int64_t m_ties = 0;
-    for (int c = bins - 1; c >= 1; --c) {
-        if (above + h[c] >= kc) {
-            cstar = (uint32_t)c;
-            m_ties = kc - above;
-            break;
-        }
-        above += h[c];
+// ---- the ranks of one refresh: NCCL (one local ctx) or the loopback group (all ctxs here) ----
+struct Ranks {
+    std::vector<picasso_ctx *> cs;  // the ctxs this process drives
+    ncclComm_t comm = nullptr;      // NCCL mode
+};
+
+// sum of a u32 buffer over the ranks, into every rank's copy (the same buffer of each ctx)
+template <typename F>
+picasso_status allreduce_u32(const Ranks &R, F buf, int64_t n, cudaStream_t s) {
+    picasso_ctx *ctx = R.cs[0];
+    if (n <= 0) return PICASSO_OK;
+    if (R.comm) {
+        HNK(ncclAllReduce(buf(ctx), buf(ctx), (size_t)n, ncclUint32, ncclSum, R.comm, s));
+        return PICASSO_OK;
     }
-    if (cstar == 0) {  // fewer than kc rows were ever counted: propose all of them
-        cstar = 1;
-        m_ties = h[1];
-        above -= h[1];
-    }
-    const int64_t ntile = (n + kTile - 1) / kTile;
-    launch_tie_count(mp.fcnt, n, cstar, mp.tie_cnt, s);
-    launch_scan_exclusive(mp.tie_cnt, mp.tie_cnt, ntile, ctx->hot_scan_scratch, nullptr, s);
-    std::vector<int64_t> rk(2 * ctx->P), seg(ctx->P + 1);
-    for (int p = 0; p < ctx->P; ++p) {
-        rk[2 * p] = ctx->pack_key_off[p] + ctx->rank;  // global key of local row lr: rk0 + lr * W
-        rk[2 * p + 1] = ctx->world;
-        seg[p] = mp.fcnt_off[p];
-    }
-    seg[ctx->P] = mp.fcnt_off[ctx->P];
-    HCK(cudaMemcpyAsync(mp.row_key_d, rk.data(), sizeof(int64_t) * 2 * ctx->P, cudaMemcpyHostToDevice, s));
-    HCK(cudaMemcpyAsync(mp.fcnt_off_d, seg.data(), sizeof(int64_t) * (ctx->P + 1), cudaMemcpyHostToDevice, s));
-    HCK(cudaMemsetAsync(mp.cand_n, 0, sizeof(int32_t), s));
-    launch_collect(mp.fcnt, n, cstar, (int32_t)m_ties, mp.tie_cnt, mp.row_key_d, ctx->P, mp.fcnt_off_d, mp.cand_key,
-                   mp.cand_cnt, mp.cand_n, s);
-    int32_t nc = 0;
-    HCK(cudaMemcpyAsync(&nc, mp.cand_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    HCK(cudaStreamSynchronize(s));
-    nc = std::min<int32_t>(nc, (int32_t)mp.k_max);
-    std::vector<unsigned long long> k(nc);
-    std::vector<uint32_t> c(nc);
-    HCK(cudaMemcpy(k.data(), mp.cand_key, sizeof(unsigned long long) * nc, cudaMemcpyDeviceToHost));
-    HCK(cudaMemcpy(c.data(), mp.cand_cnt, sizeof(uint32_t) * nc, cudaMemcpyDeviceToHost));
-    for (int32_t i = 0; i < nc; ++i) out.push_back({c[i], k[i]});
+    RankPtrs pc{};
+    const int W = (int)R.cs.size();
+    for (int r = 0; r < W; ++r) pc.p[r] = buf(R.cs[r]);
+    launch_sum_ranks_u32(pc, W, buf(ctx), n, s);  // in place into rank 0 (element-wise), then copies
+    for (int r = 1; r < W; ++r)
+        HCK(cudaMemcpyAsync(buf(R.cs[r]), buf(ctx), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
     return PICASSO_OK;
 }
 
-// step 3 + layout: identical on every rank given the same proposals
-picasso_status refresh_select(picasso_ctx *ctx, std::vector<Cand> all, size_t capacity, cudaStream_t s) {
-    MultiState &mp = ctx->mp;
-    const int P = ctx->P, W = ctx->world, nst = 1 + nst_of(ctx);
-    std::sort(all.begin(), all.end(), [](const Cand &a, const Cand &b) {
-        if (a.cnt != b.cnt) return a.cnt > b.cnt;
-        return a.key < b.key;  // (pack asc, key asc) == global key asc
-    });
-    std::vector<std::vector<unsigned long long>> by_pack(P);
-    uint64_t used = 0;
-    for (const Cand &c : all) {
-        const int p = pack_of_key(ctx, c.key);
-        const uint64_t cost = (uint64_t)4 * ctx->pack_dim[p] * nst;
-        if (used + cost > capacity) break;  // longest prefix that fits (oracle_hot_select)
-        used += cost;
-        by_pack[p].push_back(c.key);
-    }
-    std::vector<unsigned long long> keys;
-    mp.hot_pslot.assign(P + 1, 0);
-    mp.hot_off.assign(4 * P, 0);
-    int64_t cur = 0, g = 0;
-    for (int p = 0; p < P; ++p) {
-        mp.hot_pslot[p] = (int32_t)keys.size();
-        keys.insert(keys.end(), by_pack[p].begin(), by_pack[p].end());
-        const int64_t kp = (int64_t)by_pack[p].size(), D = ctx->pack_dim[p];
-        mp.hot_off[p] = cur;
-        cur += kp * D;
-        mp.hot_off[P + p] = cur;
-        cur += kp * D;
-        mp.hot_off[2 * P + p] = nst == 3 ? cur : mp.hot_off[P + p];
-        if (nst == 3) cur += kp * D;
-        mp.hot_off[3 * P + p] = g;
-        g += kp * D;
-    }
-    mp.hot_pslot[P] = (int32_t)keys.size();
-    mp.hot_g_floats = g;
-    const int32_t k = (int32_t)keys.size();
-    // staging: owner-major blocks, each owned slot's w|s1|s2 rows in slot order
-    std::vector<int32_t> sidx(k);
-    std::vector<int64_t> blk(W + 1, 0);
-    int64_t off = 0;
-    for (int o = 0; o < W; ++o) {
-        blk[o] = off;
+int64_t key_space(const picasso_ctx *ctx) { return ctx->pack_key_off[ctx->P]; }
+
+// steps 2-4 (capacity > 0); identical decisions on every rank
+picasso_status refresh_select_all(const Ranks &R, size_t capacity, cudaStream_t s, double *t_threshold) {
+    using clk = std::chrono::steady_clock;
+    static const bool trace = std::getenv("PICASSO_REFRESH_TRACE") != nullptr;  // measurement aid
+    auto tlast = clk::now();
+    auto mark = [&](const char *what) {
+        if (!trace) return;
+        cudaStreamSynchronize(s);
+        const auto t = clk::now();
+        std::fprintf(stderr, "[refresh r%d] %-22s %9.3f ms\n", R.cs[0]->rank, what,
+                     std::chrono::duration<double, std::milli>(t - tlast).count());
+        tlast = t;
+    };
+    mark("(queued work)");
+    const auto t0 = clk::now();
+    picasso_ctx *ctx = R.cs[0];
+    picasso_status st;
+    const int P = ctx->P, W = ctx->world, nst = 1 + nst_of(ctx), bins = count_hist_bins();
+    std::vector<int64_t> unit(P);  // 16-byte units of one hot row (weights + state) per pack
+    for (int p = 0; p < P; ++p) unit[p] = (int64_t)ctx->pack_dim[p] * nst / 4;
+    const int64_t cap_units = (int64_t)(capacity / 16);
+    // 2a. per-pack count histograms of the owned rows, summed over the ranks
+    for (picasso_ctx *c : R.cs)
         for (int p = 0; p < P; ++p)
-            for (int32_t sl = mp.hot_pslot[p]; sl < mp.hot_pslot[p + 1]; ++sl)
-                if ((int64_t)((keys[sl] - (unsigned long long)ctx->pack_key_off[p]) % W) == o) {
-                    sidx[sl] = (int32_t)off;
-                    off += (int64_t)nst * ctx->pack_dim[p];
+            launch_count_hist(c->mp.fcnt + c->mp.fcnt_off[p], c->mp.fcnt_off[p + 1] - c->mp.fcnt_off[p],
+                              c->mp.phist + (size_t)p * bins, c->num_sms, s);
+    mark("count histograms");
+    if ((st = allreduce_u32(R, [](picasso_ctx *c) { return c->mp.phist; }, (int64_t)P * bins, s))) return st;
+    mark("histogram allreduce");
+    std::vector<uint32_t> h((size_t)P * bins);
+    HCK(cudaMemcpyAsync(h.data(), ctx->mp.phist, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    // 2b. c*: the count at which the (count desc) order reaches the capacity
+    auto units_at = [&](int b) {
+        int64_t u = 0;
+        for (int p = 0; p < P; ++p) u += (int64_t)h[(size_t)p * bins + b] * unit[p];
+        return u;
+    };
+    uint32_t cstar = 0;
+    int64_t kcut = INT64_MAX, above = 0;
+    int b = bins - 1;
+    for (; b >= 1; --b) {
+        const int64_t u = units_at(b);
+        if (above + u > cap_units) break;
+        above += u;
+    }
+    if (b >= 1) {  // rows at count b only partly fit: cut them in ascending key
+        cstar = (uint32_t)b;
+        const int64_t rem = cap_units - above;
+        const int64_t KT = key_space(ctx);
+        int kbits = 1;
+        while (kbits < 40 && ((int64_t)1 << kbits) < KT) ++kbits;
+        const int kshift = std::max(0, kbits - 16);
+        const int64_t nkb = (KT >> kshift) + 1;
+        for (picasso_ctx *c : R.cs) {
+            HCK(cudaMemsetAsync(c->mp.khist, 0, sizeof(uint32_t) * nkb, s));
+            for (int p = 0; p < P; ++p)
+                launch_tie_keyhist(c->mp.fcnt + c->mp.fcnt_off[p], c->mp.fcnt_off[p + 1] - c->mp.fcnt_off[p], cstar,
+                                   ctx->pack_key_off[p] + c->rank, W, kshift, (uint32_t)unit[p], c->mp.khist,
+                                   c->num_sms, s);
+        }
+        mark("tie key histogram");
+        if ((st = allreduce_u32(R, [](picasso_ctx *c) { return c->mp.khist; }, nkb, s))) return st;
+        mark("tie allreduce");
+        std::vector<uint32_t> kh(nkb);
+        HCK(cudaMemcpyAsync(kh.data(), ctx->mp.khist, sizeof(uint32_t) * nkb, cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+        int64_t acc = 0, bstar = 0;
+        for (; bstar < nkb; ++bstar) {
+            if (acc + (int64_t)kh[bstar] > rem) break;
+            acc += kh[bstar];
+        }
+        kcut = (bstar << kshift) - 1;  // every tie key below bin b* fits
+        if (bstar < nkb) {           // inside b*: the tie keys themselves, in ascending order
+            const int32_t tcap = (int32_t)(((int64_t)1 << kshift) / W + 2);
+            std::vector<unsigned long long> keys;
+            for (picasso_ctx *c : R.cs) {
+                HCK(cudaMemsetAsync(c->mp.tie_n, 0, sizeof(int32_t), s));
+                for (int p = 0; p < P; ++p)
+                    launch_tie_bin_collect(c->mp.fcnt + c->mp.fcnt_off[p], c->mp.fcnt_off[p + 1] - c->mp.fcnt_off[p],
+                                           cstar, ctx->pack_key_off[p] + c->rank, W, kshift, bstar,
+                                           c->mp.tie_keys + (size_t)c->rank * tcap, c->mp.tie_n, tcap, s);
+                if (R.comm) {  // [W, tcap] keys + [W] counts on every rank
+                    HCK(cudaMemcpyAsync(c->mp.tie_keys + (size_t)W * tcap + c->rank, c->mp.tie_n, sizeof(int32_t),
+                                        cudaMemcpyDeviceToDevice, s));
+                    HNK(ncclGroupStart());
+                    HNK(ncclAllGather(c->mp.tie_keys + (size_t)c->rank * tcap, c->mp.tie_keys, tcap, ncclUint64,
+                                      R.comm, s));
+                    HNK(ncclAllGather(reinterpret_cast<int32_t *>(c->mp.tie_keys + (size_t)W * tcap) + c->rank,
+                                      reinterpret_cast<int32_t *>(c->mp.tie_keys + (size_t)W * tcap), 1, ncclInt32,
+                                      R.comm, s));
+                    HNK(ncclGroupEnd());
+                    std::vector<unsigned long long> all((size_t)W * tcap);
+                    std::vector<int32_t> cnt(W);
+                    HCK(cudaMemcpyAsync(all.data(), c->mp.tie_keys, sizeof(unsigned long long) * all.size(),
+                                        cudaMemcpyDeviceToHost, s));
+                    HCK(cudaMemcpyAsync(cnt.data(), c->mp.tie_keys + (size_t)W * tcap, sizeof(int32_t) * W,
+                                        cudaMemcpyDeviceToHost, s));
+                    HCK(cudaStreamSynchronize(s));
+                    for (int r = 0; r < W; ++r)
+                        keys.insert(keys.end(), all.begin() + (size_t)r * tcap,
+                                    all.begin() + (size_t)r * tcap + std::min(cnt[r], tcap));
+                } else {
+                    int32_t n = 0;
+                    HCK(cudaMemcpyAsync(&n, c->mp.tie_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                    HCK(cudaStreamSynchronize(s));
+                    std::vector<unsigned long long> mine(std::min(n, tcap));
+                    HCK(cudaMemcpy(mine.data(), c->mp.tie_keys + (size_t)c->rank * tcap,
+                                   sizeof(unsigned long long) * mine.size(), cudaMemcpyDeviceToHost));
+                    keys.insert(keys.end(), mine.begin(), mine.end());
                 }
+            }
+            mark("tie bin keys");
+            std::sort(keys.begin(), keys.end());
+            for (unsigned long long k : keys) {
+                int p = 0;
+                while (p + 1 < P && (unsigned long long)ctx->pack_key_off[p + 1] <= k) ++p;
+                if (acc + unit[p] > rem) break;  // the longest prefix that fits (oracle_hot_select)
+                acc += unit[p];
+                kcut = (int64_t)k;
+            }
+        }
     }
-    blk[W] = off;
-    mp.stage_blk = blk;
-    if (k > 0) {
-        HCK(cudaMemcpyAsync(mp.hot_keys, keys.data(), sizeof(unsigned long long) * k, cudaMemcpyHostToDevice, s));
-        HCK(cudaMemcpyAsync(mp.stage_idx, sidx.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+    if (t_threshold) *t_threshold = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    // 3. the selection bitmap over the global key space, summed over the ranks; hot keys
+    const int64_t nw = key_space(ctx) / 32 + 1;
+    for (picasso_ctx *c : R.cs) {
+        HCK(cudaMemsetAsync(c->mp.sel_bits, 0, sizeof(uint32_t) * nw, s));
+        for (int p = 0; p < P; ++p)
+            launch_select_bits(c->mp.fcnt + c->mp.fcnt_off[p], c->mp.fcnt_off[p + 1] - c->mp.fcnt_off[p], cstar, kcut,
+                               ctx->pack_key_off[p] + c->rank, W, c->mp.sel_bits, c->num_sms, s);
     }
-    HCK(cudaMemcpyAsync(mp.hot_pslot_d, mp.hot_pslot.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice, s));
-    HCK(cudaMemcpyAsync(mp.hot_off_d, mp.hot_off.data(), sizeof(int64_t) * 4 * P, cudaMemcpyHostToDevice, s));
-    HCK(cudaStreamSynchronize(s));  // the host vectors above go out of scope
-    mp.new_k = k;
-    // owners pack their new hot rows into the staging
-    MultiArgs m = picasso_multi_args(ctx);
-    for (int p = 0; p < P; ++p)
-        if (mp.hot_pslot[p + 1] > mp.hot_pslot[p])
-            launch_pack_owned(ctx->pack_dim[p], m, p, mp.hot_keys, mp.stage_idx, ctx->w[p], ctx->s1[p], ctx->s2[p],
-                              nst, mp.stage, ctx->rank, ctx->num_sms, s);
-    return PICASSO_OK;
+    mark("selection bits");
+    if ((st = allreduce_u32(R, [](picasso_ctx *c) { return c->mp.sel_bits; }, nw, s))) return st;
+    mark("bits allreduce");
+    for (picasso_ctx *c : R.cs) {
+        MultiState &mp = c->mp;
+        launch_bits_compact(mp.sel_bits, nw, mp.bits_blk, mp.bits_blk + nw / 1024 + 1, mp.hot_keys,
+                            (int32_t)mp.k_max, s);
+        int32_t k = 0;
+        HCK(cudaMemcpyAsync(&k, mp.bits_blk + nw / 1024 + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+        if (k > mp.k_max) {
+            c->last_msg = "hot set larger than the workspace's k_max";
+            return PICASSO_ERR_CAPACITY;
+        }
+        launch_hot_layout(mp.hot_keys, k, c->pack_key_off_d, P, mp.hot_pslot_d, s);
+        mp.hot_pslot.assign(P + 1, 0);
+        HCK(cudaMemcpyAsync(mp.hot_pslot.data(), mp.hot_pslot_d, sizeof(int32_t) * (P + 1), cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+        // replica arena (per pack: w, s1, s2 blocks) + G offsets; slot-major staging
+        mp.hot_off.assign(4 * P, 0);
+        std::vector<int64_t> soff(P);
+        int64_t cur = 0, g = 0, so = 0;
+        for (int p = 0; p < P; ++p) {
+            const int64_t kp = mp.hot_pslot[p + 1] - mp.hot_pslot[p], D = c->pack_dim[p];
+            mp.hot_off[p] = cur;
+            cur += kp * D;
+            mp.hot_off[P + p] = cur;
+            cur += kp * D;
+            mp.hot_off[2 * P + p] = nst == 3 ? cur : mp.hot_off[P + p];
+            if (nst == 3) cur += kp * D;
+            mp.hot_off[3 * P + p] = g;
+            g += kp * D;
+            soff[p] = so;
+            so += kp * D * nst;
+        }
+        mp.hot_g_floats = g;
+        mp.stage_floats = so;
+        HCK(cudaMemcpyAsync(mp.hot_off_d, mp.hot_off.data(), sizeof(int64_t) * 4 * P, cudaMemcpyHostToDevice, s));
+        HCK(cudaMemcpyAsync(mp.stage_off_d, soff.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, s));
+        launch_stage_idx(mp.hot_pslot_d, mp.stage_off_d, c->pack_dim_d, P, nst, k, mp.stage_idx, s);
+        HCK(cudaStreamSynchronize(s));  // soff goes out of scope
+        mp.new_k = k;
+        // 4. owners write their new hot rows into the staging (others' slots stay zero)
+        HCK(cudaMemsetAsync(mp.stage, 0, sizeof(float) * std::max<int64_t>(so, 1), s));
+        MultiArgs m = picasso_multi_args(c);
+        for (int p = 0; p < P; ++p)
+            if (mp.hot_pslot[p + 1] > mp.hot_pslot[p])
+                launch_pack_owned(c->pack_dim[p], m, p, mp.hot_keys, mp.stage_idx, c->w[p], c->s1[p], c->s2[p], nst,
+                                  mp.stage, c->rank, c->num_sms, s);
+    }
+    mark("compact + stage");
+    st = allreduce_u32(R, [](picasso_ctx *c) { return reinterpret_cast<uint32_t *>(c->mp.stage); },
+                       ctx->mp.stage_floats, s);
+    mark("stage allreduce");
+    return st;
 }
 
 // step 4b: staging (all owners' blocks now present) -> replicas; index; counters
@@ -244,12 +344,6 @@ picasso_status check_refresh_args(picasso_ctx *ctx, size_t capacity) {
     return PICASSO_OK;
 }
 
-int64_t kc_for(picasso_ctx *ctx, size_t capacity) {
-    int minD = 1 << 30;
-    for (int p = 0; p < ctx->P; ++p) minD = std::min(minD, ctx->pack_dim[p]);
-    return std::min<int64_t>(ctx->mp.k_max, (int64_t)(capacity / ((size_t)4 * minD * (1 + nst_of(ctx)))));
-}
-
 }  // namespace
 
 // ---- NCCL: one rank per process -----------------------------------------------------------
@@ -270,49 +364,20 @@ extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t cap
     if (ctx->mp.group || !ctx->mp.comm) return PICASSO_ERR_STATE;
     MultiState &mp = ctx->mp;
     using clk = std::chrono::steady_clock;
+    HCK(cudaStreamSynchronize(s));  // the steps queued before it are not the refresh's cost
     const auto t0 = clk::now();
     auto t1 = t0, t2 = t0;
     if (mp.hot_k > 0)
         HNK(ncclAllReduce(mp.hot_cnt, mp.cnt_sum, mp.hot_k, ncclUint32, ncclSum, mp.comm, s));
     if ((st = refresh_writeback(ctx, s))) return st;
+    double t_thr = 0.0;
     if (capacity_bytes > 0) {
-        const int64_t kc = kc_for(ctx, capacity_bytes);
-        std::vector<Cand> mine;
-        if ((st = refresh_propose(ctx, kc, mine, s))) return st;
-        t1 = clk::now();
-        // gather the proposals: fixed kc records per rank (count 0 = padding)
-        const int W = ctx->world;
-        std::vector<unsigned long long> kk(kc, 0ull);
-        std::vector<uint32_t> cc(kc, 0u);
-        for (size_t i = 0; i < mine.size(); ++i) {
-            kk[i] = mine[i].key;
-            cc[i] = mine[i].cnt;
-        }
-        // in-place AllGather: this rank's records at slot `rank` of the [W, kc] arrays
-        HCK(cudaMemcpy(mp.cand_key + (size_t)ctx->rank * kc, kk.data(), sizeof(unsigned long long) * kc,
-                       cudaMemcpyHostToDevice));
-        HCK(cudaMemcpy(mp.cand_cnt + (size_t)ctx->rank * kc, cc.data(), sizeof(uint32_t) * kc, cudaMemcpyHostToDevice));
-        HNK(ncclGroupStart());
-        HNK(ncclAllGather(mp.cand_key + (size_t)ctx->rank * kc, mp.cand_key, kc, ncclUint64, mp.comm, s));
-        HNK(ncclAllGather(mp.cand_cnt + (size_t)ctx->rank * kc, mp.cand_cnt, kc, ncclUint32, mp.comm, s));
-        HNK(ncclGroupEnd());
-        std::vector<unsigned long long> ak((size_t)kc * W);
-        std::vector<uint32_t> ac((size_t)kc * W);
-        HCK(cudaMemcpyAsync(ak.data(), mp.cand_key, sizeof(unsigned long long) * kc * W, cudaMemcpyDeviceToHost, s));
-        HCK(cudaMemcpyAsync(ac.data(), mp.cand_cnt, sizeof(uint32_t) * kc * W, cudaMemcpyDeviceToHost, s));
-        HCK(cudaStreamSynchronize(s));
-        std::vector<Cand> all;
-        for (size_t i = 0; i < ak.size(); ++i)
-            if (ac[i] > 0) all.push_back({ac[i], ak[i]});
-        if ((st = refresh_select(ctx, all, capacity_bytes, s))) return st;
+        Ranks R;
+        R.cs = {ctx};
+        R.comm = mp.comm;
+        if ((st = refresh_select_all(R, capacity_bytes, s, &t_thr))) return st;
+        t1 = t0 + std::chrono::duration_cast<clk::duration>(std::chrono::duration<double, std::milli>(t_thr));
         t2 = clk::now();
-        HNK(ncclGroupStart());
-        for (int o = 0; o < W; ++o) {
-            const int64_t n = mp.stage_blk[o + 1] - mp.stage_blk[o];
-            if (n > 0)
-                HNK(ncclBroadcast(mp.stage + mp.stage_blk[o], mp.stage + mp.stage_blk[o], n, ncclFloat32, o, mp.comm, s));
-        }
-        HNK(ncclGroupEnd());
         if ((st = refresh_place(ctx, s))) return st;
     }
     HCK(cudaStreamSynchronize(s));
@@ -348,22 +413,9 @@ extern "C" picasso_status picasso_group_hot_cache_refresh(picasso_group *g, size
     for (auto *c : g->ctx)
         if ((st = refresh_writeback(c, s))) return st;
     if (capacity_bytes > 0) {
-        std::vector<Cand> all;
-        for (auto *c : g->ctx) {
-            std::vector<Cand> mine;
-            if ((st = refresh_propose(c, kc_for(c, capacity_bytes), mine, s))) return st;
-            all.insert(all.end(), mine.begin(), mine.end());
-        }
-        for (auto *c : g->ctx)
-            if ((st = refresh_select(c, all, capacity_bytes, s))) return st;
-        for (int o = 0; o < W; ++o) {  // owner o's block to every other rank
-            picasso_ctx *src = g->ctx[o];
-            const int64_t off = src->mp.stage_blk[o], n = src->mp.stage_blk[o + 1] - off;
-            for (int r = 0; r < W; ++r)
-                if (r != o && n > 0)
-                    HCK(cudaMemcpyAsync(g->ctx[r]->mp.stage + off, src->mp.stage + off, sizeof(float) * n,
-                                        cudaMemcpyDeviceToDevice, s));
-        }
+        Ranks R;
+        R.cs = g->ctx;
+        if ((st = refresh_select_all(R, capacity_bytes, s, nullptr))) return st;
         for (auto *c : g->ctx)
             if ((st = refresh_place(c, s))) return st;
     }

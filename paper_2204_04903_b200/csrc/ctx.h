@@ -90,19 +90,26 @@ struct MultiState {
     int32_t *hslot = nullptr;
     unsigned long long *hot_keys = nullptr;
     float *hot_arena = nullptr, *hot_g = nullptr, *hot_gsum = nullptr, *hot_touch = nullptr, *stage = nullptr;
-    uint32_t *hot_cnt = nullptr, *cnt_sum = nullptr, *fcnt = nullptr, *cnt_hist = nullptr;
-    int32_t *hot_pslot_d = nullptr, *stage_idx = nullptr, *tie_cnt = nullptr, *cand_n = nullptr;
+    uint32_t *hot_cnt = nullptr, *cnt_sum = nullptr, *fcnt = nullptr;
+    int32_t *hot_pslot_d = nullptr;
     int64_t *hot_off_d = nullptr;       // [4P]: w, s1, s2, g offsets
-    int64_t *fcnt_off_d = nullptr, *row_key_d = nullptr;
-    unsigned long long *cand_key = nullptr;
-    uint32_t *cand_cnt = nullptr;
+    int64_t *fcnt_off_d = nullptr;
+    // refresh selection (cache_host.cu refresh_select_all)
+    uint32_t *phist = nullptr;          // [P, 65536] per-pack count histograms of the owned rows
+    uint32_t *khist = nullptr;          // [65536 + 2] tie bytes by global-key bin
+    unsigned long long *tie_keys = nullptr;  // [W, tcap] tie keys in the cut bin (+ [W] counts)
+    int32_t *tie_n = nullptr;           // [1]
+    uint32_t *sel_bits = nullptr;       // [key space / 32 + 1] the selection bitmap
+    int32_t *bits_blk = nullptr;        // [words / 1024 + 3] compaction scratch (+ total)
+    int64_t *stage_idx = nullptr;       // [k_max] float offset of each slot in the staging
+    int64_t *stage_off_d = nullptr;     // [P] staging offset of each pack's slots
+    int64_t stage_floats = 0;
     int64_t rows_total = 0;
     std::vector<int64_t> fcnt_off;      // [P+1]
     std::vector<int32_t> hot_pslot;     // [P+1]
     std::vector<int64_t> hot_off;       // [4P]
     int64_t hot_g_floats = 0;
     int64_t last_hot_uniques = 0, last_uniques = 0;
-    std::vector<int64_t> stage_blk;     // [W+1] owner blocks of the refresh staging (floats)
     int32_t new_k = 0;
     // ---- NVLink peer-memory exchange (p2p.cu / p2p_host.cu)
     bool p2p = false;                   // exchanges go through the peers' windows (no NCCL a2av)
@@ -305,7 +312,6 @@ struct picasso_ctx {
     int64_t di_micro = 0;
 
     int32_t *osort_hist = nullptr;  // k_inverse's pass-0 histogram output when run on the owner stream
-    int32_t *hot_scan_scratch = nullptr;
 
     size_t carve(char *base) {
         Carver c{base};
@@ -463,17 +469,18 @@ struct picasso_ctx {
                 mp.hot_cnt = c.take<uint32_t>(K);
                 mp.cnt_sum = c.take<uint32_t>(2 * K);
                 mp.fcnt = c.take<uint32_t>(std::max<int64_t>(mp.rows_total, 1));
-                mp.cnt_hist = c.take<uint32_t>(1 << 16);
                 mp.hot_pslot_d = c.take<int32_t>(P + 1);
-                mp.stage_idx = c.take<int32_t>(K);
-                mp.tie_cnt = c.take<int32_t>((mp.rows_total + kTile - 1) / kTile + 2);
-                mp.cand_n = c.take<int32_t>(2);
                 mp.hot_off_d = c.take<int64_t>(4 * P);
                 mp.fcnt_off_d = c.take<int64_t>(P + 1);
-                mp.row_key_d = c.take<int64_t>(2 * P);
-                mp.cand_key = c.take<unsigned long long>((size_t)K * world);
-                mp.cand_cnt = c.take<uint32_t>((size_t)K * world);
-                hot_scan_scratch = c.take<int32_t>((mp.rows_total + kTile - 1) / kTile / kTile + 64);
+                const int64_t KT = pack_key_off.empty() ? 0 : pack_key_off[P], nw = KT / 32 + 1;
+                mp.phist = c.take<uint32_t>((size_t)P << 16);
+                mp.khist = c.take<uint32_t>((1 << 16) + 2);
+                mp.tie_keys = c.take<unsigned long long>((size_t)world * ((1 << 16) / world + 2) + world + 2);
+                mp.tie_n = c.take<int32_t>(1);
+                mp.sel_bits = c.take<uint32_t>(nw);
+                mp.bits_blk = c.take<int32_t>(nw / 1024 + 3);
+                mp.stage_idx = c.take<int64_t>(K);
+                mp.stage_off_d = c.take<int64_t>(P);
             }
         }
         return c.off + kAlign;

@@ -90,7 +90,7 @@ def test_hybridhash_transparency_and_topk(cfg_name):
             sel = oracle.hot_select(packs, nz - pko[packs], counts[nz], cost, capacity)
             exp = nz[sel]
             exp_pack = np.searchsorted(pko, exp, side="right") - 1
-            order = np.argsort(exp_pack, kind="stable")  # slots grouped by pack, selection order within
+            order = np.argsort(exp, kind="stable")  # slots in ascending global key: grouped by pack
             for e in g.ranks:
                 pk, ky = e.hot_keys()
                 assert np.array_equal(pk, exp_pack[order]) and np.array_equal(ky, (exp - pko[exp_pack])[order])
