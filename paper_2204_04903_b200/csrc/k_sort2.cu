@@ -43,7 +43,31 @@ __global__ void __launch_bounds__(256) k_scan_rows(int32_t *hist, int64_t nblk, 
                                                    int radix, int next_radix) {
     const int lane = threadIdx.x & 31;
     const int d = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (d < radix) {
+    constexpr int kRegRow = 16;  // rows up to 32 x 16 entries: every load issued at once
+    if (d < radix && nblk <= 32 * kRegRow) {
+        int32_t *row = hist + (int64_t)d * nblk;
+        const int64_t k0 = (int64_t)lane * kRegRow;  // this lane's consecutive entries
+        int32_t v[kRegRow], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kRegRow; ++j) {
+            v[j] = k0 + j < nblk ? row[k0 + j] : 0;
+            sum += v[j];
+        }
+        int32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int32_t run = x - sum;
+#pragma unroll
+        for (int j = 0; j < kRegRow; ++j)
+            if (k0 + j < nblk) {
+                row[k0 + j] = run;
+                run += v[j];
+            }
+        if (lane == 31) rowtot[d] = x;
+    } else if (d < radix) {
         int32_t *row = hist + (int64_t)d * nblk;
         int32_t carry = 0;
         for (int64_t base = 0; base < nblk; base += 32) {
@@ -364,8 +388,10 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
 
 // Per-tile bucket offsets (exclusive, in place) and bucket totals of a digit-major histogram
 // (the peer-memory partition's k_bucket output).
-void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s) {
-    if (nblk > 0) k_scan_rows<<<(radix + 7) / 8, 256, 0, s>>>(hist, nblk, rowtot, nullptr, radix, 0);
+void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s, int32_t *zero_next,
+                 int next_radix) {
+    const int rows = radix > next_radix ? radix : next_radix;
+    if (nblk > 0) k_scan_rows<<<(rows + 7) / 8, 256, 0, s>>>(hist, nblk, rowtot, zero_next, radix, next_radix);
 }
 
 // One stable pass by a small key (the multi-GPU partition by (owner, pack)); bhist was filled

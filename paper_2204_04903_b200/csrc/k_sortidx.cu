@@ -34,6 +34,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 

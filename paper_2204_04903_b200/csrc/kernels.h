@@ -93,7 +93,10 @@ void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, i
                        int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
                        int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches);
 size_t radix_hist2_ints(int64_t n);
-void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s);
+// per-digit exclusive scan of a digit-major [radix, nblk] histogram (+ digit totals); zero_next:
+// also zeroes the [next_radix, nblk] rows of that buffer (the next pass's counts)
+void bucket_scan(int32_t *hist, int64_t nblk, int32_t *rowtot, int radix, cudaStream_t s, int32_t *zero_next = nullptr,
+                 int next_radix = 0);
 void bucket_sort_pass(const int32_t *k_in, const int32_t *v_in, int32_t *k_out, int32_t *v_out, int64_t n_max,
                       const int32_t *n_dev, int bits, int32_t *bhist, int32_t *rowtot, cudaStream_t s);
 
