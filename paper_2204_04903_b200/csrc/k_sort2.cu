@@ -333,11 +333,28 @@ __global__ void __launch_bounds__(kTileThreads) k_hist_tiles(const int32_t *keys
 }
 
 constexpr int64_t kBigSort = (int64_t)1 << 22;  // from here on the next histogram is its own pass
+constexpr int64_t kChunkedSort = (int64_t)1 << 20;  // from here on: the chunked passes (k_sortidx.cu)
 
 void radix_sort_pairs2(const int32_t *k_in, const int32_t *v_in, int32_t *k_a, int32_t *v_a, int32_t *k_b,
                        int32_t *v_b, int32_t **k_out, int32_t **v_out, int64_t n, const SortPlan &plan,
                        int32_t *hist0, int32_t *hist1, int32_t *rowtot, cudaStream_t s, int64_t *launches) {
     const int64_t nblk = (n + kTile - 1) / kTile;
+    // large sorts: the chunked LSD passes of k_sortidx.cu ((k_a, v_a) and (k_b, v_b) are adjacent:
+    // 8-byte item buffers); PICASSO_SORT=2 / 3 keep these passes
+    static const char *sort_env0 = std::getenv("PICASSO_SORT");
+    if (n >= kChunkedSort && !sort_env0 && v_a == k_a + n && v_b == k_b + n) {
+        static int num_sms = [] {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            return sms;
+        }();
+        int bits = 0;
+        for (int i = 0; i < plan.passes; ++i) bits += plan.bits[i];
+        *launches += sort_pairs_chunked(k_in, v_in, reinterpret_cast<uint64_t *>(k_a), reinterpret_cast<uint64_t *>(k_b),
+                                        k_out, v_out, n, bits, hist0, rowtot, num_sms, s);
+        return;
+    }
     const int32_t *ck = k_in, *cv = v_in;
     int32_t *bufk[2] = {k_a, k_b}, *bufv[2] = {v_a, v_b};
     int32_t *hist[2] = {hist0, hist1};

@@ -114,7 +114,7 @@ __device__ __forceinline__ void si_load_tile(const SortIdxArgs &a, const uint64_
         const int li = wb + r * 32 + lane;
         if (li < nt) {
             const int64_t g = t0 + li;
-            if (FIRST) it[r] = ((uint64_t)__ldg(a.keys + g) << 32) | (uint32_t)g;
+            if (FIRST) it[r] = ((uint64_t)__ldg(a.keys + g) << 32) | (a.vals ? (uint32_t)__ldg(a.vals + g) : (uint32_t)g);
             else it[r] = ld_item(in, g);
         } else {
             it[r] = 0ull;
@@ -493,7 +493,50 @@ __global__ void __launch_bounds__(kSiThreads) k_sv_final(SortIdxArgs a, const ui
     }
 }
 
+__global__ void k_unpack_pairs(const uint64_t *items, int64_t n, int32_t *k_out, int32_t *v_out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = ld_item(items, i);
+        k_out[i] = (int32_t)(x >> 32);
+        v_out[i] = (int32_t)(uint32_t)x;
+    }
+}
+
 }  // namespace
+
+// The hash index's transpose (stable sort of (uid, segment) pairs by uid) through the same chunked
+// LSD passes: for large sorts they beat the per-tile-histogram passes of k_sort2.cu, whose digit-
+// major [1024, N / 2048] histograms and their scans are re-read every pass.
+int sort_pairs_chunked(const int32_t *k_in, const int32_t *v_in, uint64_t *buf_a, uint64_t *buf_b, int32_t **k_out,
+                       int32_t **v_out, int64_t n, int key_bits, int32_t *hist, int32_t *rowtot, int num_sms,
+                       cudaStream_t s) {
+    SortIdxArgs a{};
+    a.N = n;
+    a.keys = reinterpret_cast<uint32_t *>(const_cast<int32_t *>(k_in));
+    a.vals = v_in;
+    a.hist = hist;
+    a.rowtot = rowtot;
+    const SortIdxPlan plan = make_sortidx_plan(n, key_bits, num_sms);
+    a.chunk = plan.chunk;
+    a.nc = plan.nc;
+    uint64_t *bufs[2] = {buf_a, buf_b};
+    const uint64_t *cur = nullptr;
+    int launches = 0;
+    for (int p = 0; p < plan.passes; ++p) {
+        uint64_t *out = bufs[p & 1];
+        if (p == 0) k_si_up<true><<<(unsigned)a.nc, kSiThreads, 0, s>>>(a, nullptr, plan.shift[p], plan.bits[p]);
+        else k_si_up<false><<<(unsigned)a.nc, kSiThreads, 0, s>>>(a, cur, plan.shift[p], plan.bits[p]);
+        bucket_scan(a.hist, a.nc, a.rowtot, 1 << plan.bits[p], s);
+        if (p == 0) k_si_down<true><<<(unsigned)a.nc, kSiThreads, 0, s>>>(a, nullptr, out, plan.shift[p], plan.bits[p]);
+        else k_si_down<false><<<(unsigned)a.nc, kSiThreads, 0, s>>>(a, cur, out, plan.shift[p], plan.bits[p]);
+        cur = out;
+        launches += 3;
+    }
+    int32_t *ko = reinterpret_cast<int32_t *>(cur == buf_a ? buf_b : buf_a);
+    *k_out = ko;
+    *v_out = ko + n;
+    k_unpack_pairs<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 16), 256, 0, s>>>(cur, n, ko, ko + n);
+    return launches + 1;
+}
 
 SortIdxPlan make_sortidx_plan(int64_t n, int key_bits, int num_sms) {
     SortIdxPlan p{};

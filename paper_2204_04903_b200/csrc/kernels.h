@@ -113,6 +113,7 @@ struct SortIdxArgs {
     const int64_t *pack_key_off;
     int *err;
     uint32_t *keys;                // [N] pack key of each position (first pass)
+    const int32_t *vals;           // [N] first pass's item values (nullptr: the position itself)
     int32_t *hist, *rowtot;        // LSD passes: [radix, nc] chunk counts, [radix] digit totals
     int32_t nc;
     int64_t chunk;
@@ -150,6 +151,11 @@ size_t sortidx_scratch_ints(int64_t n, int32_t P);  // tile arrays + views scrat
 int launch_sort_index(SortIdxArgs a, const SortIdxPlan &plan, uint64_t *buf_a, uint64_t *buf_b, uint64_t **sorted,
                       uint64_t **other, cudaStream_t s);
 int launch_sort_views(SortIdxArgs a, const uint64_t *sorted, cudaStream_t s);  // inverse + Unique (reading O1)
+// stable sort of int32 (key, val) pairs by key < 2^key_bits through the chunked passes; the sorted
+// pairs land in the buffer the last pass did not write (*k_out, *v_out = *k_out + n); #launches
+int sort_pairs_chunked(const int32_t *k_in, const int32_t *v_in, uint64_t *buf_a, uint64_t *buf_b, int32_t **k_out,
+                       int32_t **v_out, int64_t n, int key_bits, int32_t *hist, int32_t *rowtot, int num_sms,
+                       cudaStream_t s);
 
 // k_index.cu
 void launch_field_prep(const IndexArgs &a, cudaStream_t s);
