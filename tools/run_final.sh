@@ -10,7 +10,8 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --mast
 CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --config wdl --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/final_wdl.jsonl 2> gpurun_out/final_wdl.err; echo wdl=$?
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29613 bench.py --gpus 4 --config industrial --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/final_c4.jsonl 2> gpurun_out/final_c4.err; echo c4=$?
 CUDA_VISIBLE_DEVICES=0 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/final_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/final_list.log 2>&1; echo list=$?
-CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_segsum_upd|k_pool_pipe|k_si_down|k_si_final" --launch-skip 20 --launch-count 4 -o gpurun_out/final_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --eager > gpurun_out/final_full.log 2>&1; echo full=$?
-ncu -i gpurun_out/final_full.ncu-rep --page raw --csv > gpurun_out/final_full_raw.csv 2>/dev/null
-ncu -i gpurun_out/final_full.ncu-rep --page details --csv > gpurun_out/final_full_details.csv 2>/dev/null
+for k in k_segsum_upd k_pool_pipe k_si_down k_si_final; do
+  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" --launch-skip 5 --launch-count 1 -o gpurun_out/final_full_$k python bench.py --steps 1 --warmup 3 --no-cpu-baseline --eager > gpurun_out/final_full_$k.log 2>&1; echo full_$k=$?
+  ncu -i gpurun_out/final_full_$k.ncu-rep --page raw --csv > gpurun_out/final_full_${k}_raw.csv 2>/dev/null
+done
 echo done
