@@ -223,6 +223,14 @@ struct picasso_ctx {
     int sort_reserve = 52;        // SMs the pool leaves to the sort chain beside it (PICASSO_SORT_RESERVE;
                                   // C2 sweep 24 / 32 / 40 / 48 / 56 / 64: 0.2286 / 0.2223 / 0.2185 / 0.2178 / 0.2172 / 0.2185 ms)
     unsigned long long *run_keys() const { return reinterpret_cast<unsigned long long *>(table); }
+    // the row-sharded step indexed by sort (world > 1, from sort_min_ids_w IDs on): Unique / inverse
+    // from the sort's views (the exchange's uid order), the backward in run order with its per-row
+    // arrays gathered through run_uid — no uid transpose (PICASSO_INDEX=hash: off)
+    bool sort_w = false;
+    bool w_runorder = false;      // the last row-sharded forward indexed by sort
+    int64_t sort_min_ids_w = (int64_t)1 << 20;
+    int32_t *run_uid = nullptr, *hs_run = nullptr, *dr_run = nullptr;  // [N]
+    int64_t *ro_run = nullptr, *do_run = nullptr;                        // [N]
     unsigned long long *row_keys() const { return sort_step ? run_keys() : unique_gkey; }
     std::vector<float *> w, s1, s2;
     // step state
@@ -415,6 +423,13 @@ struct picasso_ctx {
         // rows / G buffer: the IPC window holds it with the peer-memory exchange
         const bool p2p_ex = world > 1 && opts.exchange == 0;
         gbuf = ((split_bwd && world == 1) || (world > 1 && !p2p_ex)) ? c.take<float>((size_t)N * maxD) : nullptr;
+        if (world > 1 && sort_w) {
+            run_uid = c.take<int32_t>(N);
+            hs_run = c.take<int32_t>(N);
+            dr_run = c.take<int32_t>(N);
+            ro_run = c.take<int64_t>(N);
+            do_run = c.take<int64_t>(N);
+        }
         if (world > 1) {
             const int64_t RM = std::max<int64_t>(mp.max_recv, 1);
             const int WP = world * P;

@@ -493,6 +493,26 @@ __global__ void __launch_bounds__(kSiThreads) k_sv_final(SortIdxArgs a, const ui
     }
 }
 
+// uid of each row (run order): the rank of its head's first position
+__global__ void k_sv_run_uid(SortIdxArgs a, const uint64_t *s) {
+    const int32_t U = *a.d_total;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < U; r += (int64_t)gridDim.x * blockDim.x)
+        a.run_uid[r] = sv_rank(a, (uint32_t)ld_item(s, __ldg(a.ustart + r)));
+}
+
+__global__ void k_run_gather(const int32_t *run_uid, const int32_t *d_total, const int32_t *hslot, int32_t *hs_run,
+                             const int64_t *row_off, int64_t *ro_run, const int32_t *dst_rank, int32_t *dr_run,
+                             const int64_t *dst_off, int64_t *do_run) {
+    const int32_t U = *d_total;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < U; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = __ldg(run_uid + r);
+        if (hslot) hs_run[r] = hslot[u];
+        if (row_off) ro_run[r] = row_off[u];
+        if (dst_rank) dr_run[r] = dst_rank[u];
+        if (dst_off) do_run[r] = dst_off[u];
+    }
+}
+
 __global__ void k_unpack_pairs(const uint64_t *items, int64_t n, int32_t *k_out, int32_t *v_out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t x = ld_item(items, i);
@@ -609,7 +629,16 @@ int launch_sort_views(SortIdxArgs a, const uint64_t *sorted, cudaStream_t s) {
     k_bm_scan<<<1, 1024, 0, s>>>(bm_cnt, bm_pref, nblk);
     k_bm_prefix<<<(unsigned)((nblk + 7) / 8), 256, 0, s>>>(a.bm, nwords, bm_pref, a.wpref, nblk);
     k_sv_final<<<(unsigned)nblk, kSiThreads, 0, s>>>(a, sorted);
-    return 6;
+    if (a.run_uid) k_sv_run_uid<<<(unsigned)std::min<int64_t>((a.N + 255) / 256, 4096), 256, 0, s>>>(a, sorted);
+    return a.run_uid ? 7 : 6;
+}
+
+void launch_run_gather(const int32_t *run_uid, const int32_t *d_total, int64_t n_max, const int32_t *hslot,
+                       int32_t *hs_run, const int64_t *row_off, int64_t *ro_run, const int32_t *dst_rank,
+                       int32_t *dr_run, const int64_t *dst_off, int64_t *do_run, int num_sms, cudaStream_t s) {
+    if (n_max <= 0) return;
+    k_run_gather<<<(unsigned)std::min<int64_t>((n_max + 255) / 256, (int64_t)num_sms * 8), 256, 0, s>>>(
+        run_uid, d_total, hslot, hs_run, row_off, ro_run, dst_rank, dr_run, dst_off, do_run);
 }
 
 }  // namespace picasso

@@ -137,6 +137,7 @@ struct SortIdxArgs {
     int32_t *view_scratch;         // [2 nblk]
     int32_t *inverse;              // [N] uid of each position
     unsigned long long *unique_gkey;  // [U] key of each uid (first-occurrence order)
+    int32_t *run_uid;              // [U] (optional) uid of each row in run order
 };
 struct SortIdxPlan {
     int passes;
@@ -151,6 +152,11 @@ size_t sortidx_scratch_ints(int64_t n, int32_t P);  // tile arrays + views scrat
 int launch_sort_index(SortIdxArgs a, const SortIdxPlan &plan, uint64_t *buf_a, uint64_t *buf_b, uint64_t **sorted,
                       uint64_t **other, cudaStream_t s);
 int launch_sort_views(SortIdxArgs a, const uint64_t *sorted, cudaStream_t s);  // inverse + Unique (reading O1)
+// row-sharded step indexed by sort: the backward's per-row arrays in run order (row r = uid run_uid[r]);
+// any source may be nullptr (its destination is then left alone)
+void launch_run_gather(const int32_t *run_uid, const int32_t *d_total, int64_t n_max, const int32_t *hslot,
+                       int32_t *hs_run, const int64_t *row_off, int64_t *ro_run, const int32_t *dst_rank,
+                       int32_t *dr_run, const int64_t *dst_off, int64_t *do_run, int num_sms, cudaStream_t s);
 // stable sort of int32 (key, val) pairs by key < 2^key_bits through the chunked passes; the sorted
 // pairs land in the buffer the last pass did not write (*k_out, *v_out = *k_out + n); #launches
 int sort_pairs_chunked(const int32_t *k_in, const int32_t *v_in, uint64_t *buf_a, uint64_t *buf_b, int32_t **k_out,

@@ -111,20 +111,30 @@ void launch_sum_ranks(const RankPtrs &src, int W, float *dst, int64_t n, cudaStr
 }  // namespace picasso
 
 // ---- phase A: dedup (as at W = 1) + Partition into the owner-major send layout -------------
+picasso_status w_sorted_index(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
+                              cudaStream_t s);  // runtime.cu
+
 picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
                       cudaStream_t s) {
     MultiState &mp = ctx->mp;
     ctx->N = N;
     ctx->B = B;
     ctx->offsets = offsets;
-    IndexArgs a = make_index_args(ctx, ids, offsets, B, N);
-    const uint32_t cap_step = (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(N, 1) * 2));
-    a.cap_mask = cap_step - 1;
+    ctx->w_runorder = ctx->sort_w && B > 0 && N >= ctx->sort_min_ids_w;
     ctx->mark(0, true, s);
-    if (!a.region_base) MCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
-    launch_field_prep(a, s);  // (+ the table regions' clear)
-    launch_dedup_insert(a, s);
-    launch_dedup_assign(a, s);
+    if (ctx->w_runorder) {  // sort-based index: no dedup table, no uid transpose later
+        picasso_status st = w_sorted_index(ctx, ids, offsets, B, N, s);
+        if (st) return st;
+    } else {
+        IndexArgs a = make_index_args(ctx, ids, offsets, B, N);
+        const uint32_t cap_step =
+            (uint32_t)std::min<uint64_t>(ctx->cap, pow2_at_least((uint64_t)std::max<int64_t>(N, 1) * 2));
+        a.cap_mask = cap_step - 1;
+        if (!a.region_base) MCK(cudaMemsetAsync(ctx->table, 0xFF, sizeof(Slot) * cap_step, s));
+        launch_field_prep(a, s);  // (+ the table regions' clear)
+        launch_dedup_insert(a, s);
+        launch_dedup_assign(a, s);
+    }
     MultiArgs m = multi_args(ctx);
     if (mp.hot_k > 0) launch_hot_probe(m, ctx->num_sms, s);  // hot keys skip the exchange
     if (mp.p2p) {  // slot order inside a bucket is free: counts + placement, no sort
@@ -143,8 +153,22 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
                             cudaMemcpyDeviceToHost, s));
     ctx->mark(0, false, s);
     ctx->launches_fwd += 1 + (N > 0 ? 4 : 0) + 1 + 5;
-    transpose_fork(ctx, s);
+    if (!ctx->w_runorder) transpose_fork(ctx, s);  // (the sort already gave the backward's rows)
     return PICASSO_OK;
+}
+
+// run-order backward of a sort-indexed row-sharded step: the per-row destination arrays the
+// segment-sum indexes by row, gathered from their uid-indexed originals
+static void run_order_args(picasso_ctx *ctx, UpdateArgs &u, cudaStream_t s) {
+    if (!ctx->w_runorder) return;
+    launch_run_gather(ctx->run_uid, ctx->d_total, ctx->N, u.hslot, ctx->hs_run, u.row_off, ctx->ro_run, u.dst_rank,
+                      ctx->dr_run, u.dst_off, ctx->do_run, ctx->num_sms, s);
+    ctx->launches_bwd += 1;
+    if (u.hslot) u.hslot = ctx->hs_run;
+    if (u.row_off) u.row_off = ctx->ro_run;
+    if (u.dst_rank) u.dst_rank = ctx->dr_run;
+    if (u.dst_off) u.dst_off = ctx->do_run;
+    u.unique_gkey = ctx->run_keys();
 }
 
 // ---- phase B: counts known -> offsets, capacity check, owner block table ------------------
@@ -292,6 +316,7 @@ UpdateArgs mbwd_args(picasso_ctx *ctx, const float *grad_out, float lr, int64_t 
         u.dst_off = mp.dst_off;
         for (int q = 0; q < ctx->world; ++q) u.dst_buf[q] = mp.peers.ogbuf[q];
     }
+    run_order_args(ctx, u, s);
     return u;
 }
 
@@ -325,6 +350,7 @@ picasso_status mbwd_e(picasso_ctx *ctx, const float *grad_out, float lr, int64_t
         u.dst_off = mp.dst_off;
         for (int q = 0; q < ctx->world; ++q) u.dst_buf[q] = mp.peers.ogbuf[q];
     }
+    run_order_args(ctx, u, s);
     if (N > 0) {
         for (int32_t p = 0; p < ctx->P; ++p) {
             u.pack = p;

@@ -235,6 +235,12 @@ extern "C" picasso_status picasso_ctx_create(const picasso_plan_view *plan, int3
     if (const char *e = std::getenv("PICASSO_SORT_MIN_IDS")) c->sort_min_ids = std::atoll(e);
     if (const char *e = std::getenv("PICASSO_SORT_OVERLAP")) c->sort_overlap = std::strcmp(e, "0") != 0;
     if (const char *e = std::getenv("PICASSO_SORT_RESERVE")) c->sort_reserve = std::atoi(e);
+    c->sort_w = world > 1 && !opts->cold_tier && c->bulk_segsum && c->pack_key_off[c->P] <= ((int64_t)1 << 32) &&
+                sortidx_scratch_ints(std::max<int64_t>(opts->max_ids, 1), c->P) <=
+                    radix_hist2_ints(std::max<int64_t>(opts->max_ids, 1));
+    if (const char *e = std::getenv("PICASSO_INDEX"))
+        if (!std::strcmp(e, "hash")) c->sort_w = false;
+    if (const char *e = std::getenv("PICASSO_SORT_MIN_IDS_W")) c->sort_min_ids_w = std::atoll(e);
     // dY regrouped per pack before the world == 1 backward (several packs, disjoint columns)
     c->dy_stage = world == 1 && c->P > 1 && !opts->cold_tier;
     if (const char *e = std::getenv("PICASSO_DY_STAGE")) c->dy_stage = c->dy_stage && std::strcmp(e, "0") != 0;
@@ -535,6 +541,32 @@ static SortIdxArgs sort_idx_args(picasso_ctx *ctx, const int64_t *ids, int32_t B
     return x;
 }
 
+// Row-sharded step (world > 1) indexed by sort: field layout, segment map + keys, the sort (the
+// backward's run-order rows and tiles), and at once the reading-O1 views the exchange works in
+// (Unique in first-occurrence order, inverse, per-pack uid ranges) plus run -> uid.  multi_host.cu.
+picasso_status w_sorted_index(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets, int32_t B, int64_t N,
+                              cudaStream_t s) {
+    IndexArgs a = index_args(ctx, ids, offsets, B, N);
+    a.region_base = nullptr;
+    a.keys = reinterpret_cast<uint32_t *>(ctx->slot_of);
+    launch_field_prep(a, s);
+    const SegKeyArgs ka{ids, ctx->pack_key_off_d, ctx->opts.id_mode, a.keys};
+    launch_seg_of(offsets, B, ctx->F, ctx->field_gstart, ctx->id_start, ctx->seg_of, s, ctx->finfo, ctx->empty_pack,
+                  ctx->seg_limit, ctx->err, &ka);
+    SortIdxArgs x = sort_idx_args(ctx, ids, B, N);
+    x.run_uid = ctx->run_uid;
+    const SortIdxPlan plan = make_sortidx_plan(N, ctx->sort_key_bits, ctx->num_sms);
+    uint64_t *sorted = nullptr, *other = nullptr;
+    ctx->launches_fwd += 2 + launch_sort_index(x, plan, reinterpret_cast<uint64_t *>(ctx->k_a),
+                                               reinterpret_cast<uint64_t *>(ctx->k_b), &sorted, &other, s);
+    ctx->launches_fwd += launch_sort_views(x, sorted, s);
+    ctx->su = reinterpret_cast<int32_t *>(other);
+    ctx->sseg = ctx->su + N;
+    ctx->sorted_items = sorted;
+    CK(cudaGetLastError());
+    return PICASSO_OK;
+}
+
 // the reading-O1 views of a sorted step (Unique in first-occurrence order, inverse), on request
 static picasso_status ensure_views(picasso_ctx *ctx) {
     if (!ctx->sort_step || ctx->views_ready) return PICASSO_OK;
@@ -790,6 +822,7 @@ void picasso::transpose_on(picasso_ctx *ctx, cudaStream_t t) {
 }
 
 void picasso::transpose_join(picasso_ctx *ctx, cudaStream_t s) {
+    if (ctx->world > 1 && ctx->w_runorder) return;  // no transpose was forked (sort-indexed step)
     if (ctx->overlap && ctx->side) cudaStreamWaitEvent(s, ctx->ev_join, 0);
 }
 
