@@ -197,8 +197,9 @@ picasso_status picasso_ctx_destroy(picasso_ctx *ctx);
  * lengths): offsets must stay valid and unchanged until that backward has been enqueued.
  * Index path: at world == 1 the Unique of every pack comes from one stable LSD sort of the
  * step's (pack key, position) items, which also yields the backward's rows in ascending-key
- * order (PICASSO_INDEX=hash selects the hash-table Unique + uid transpose, which the
- * row-sharded step always uses); both give the same forward and the same updates.
+ * order; the row-sharded step does the same from 2^20 IDs per rank on (its exchange then reads
+ * the sort's first-occurrence views) and below that uses the hash-table Unique + uid transpose
+ * (PICASSO_INDEX=hash everywhere); all give the same forward and the same updates.
  * offsets that are not such a CSR latch INVALID_ARG (picasso_last_error); the step then runs
  * on a substitute layout that keeps every access in bounds, and its results are meaningless.
  * Errors: CAPACITY if batch > max_batch or n_ids > max_ids; STATE if not bound. */
