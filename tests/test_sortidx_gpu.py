@@ -119,3 +119,22 @@ def test_sort_step_then_hash_step_same_ctx(monkeypatch):
         oracle.backward_update(m, [ob], tabs, s1, None, kind=oracle.OPT_ADAGRAD, lr=0.05, step=step)
         for t in range(0, cfg.T, 7):
             assert np.array_equal(gpu_table_rows(emb, cfg, t), tabs[t]), f"step {step} table {t}"
+
+
+@pytest.mark.parametrize("mode", ["sort", "hash"])
+@pytest.mark.parametrize("seed", range(8))
+def test_sort_index_random_shapes(seed, mode, monkeypatch):
+    """Random small layouts (1-12 fields sharing 1-6 tables, dims 4-64, 1-5000 rows, batch 1-300,
+    bags of 0-6 IDs, some fields always empty): both index paths bit-exact against the oracle
+    (forward, Unique / inverse, dyadic updates), two steps each."""
+    monkeypatch.setenv("PICASSO_INDEX", mode)
+    rng = np.random.default_rng(1000 + seed)
+    T = int(rng.integers(1, 7))
+    F = int(rng.integers(1, 13))
+    dims = rng.choice([4, 8, 16, 32, 64], size=T).astype(np.int32)
+    rows = rng.integers(1, 5001, size=T).astype(np.int64)
+    f2t = rng.integers(0, T, size=F).astype(np.int32)
+    bags = [("uniform", 0, int(rng.integers(0, 7))) for _ in range(F)]
+    cfg = dc.toy(batch=int(rng.integers(1, 301))).replace(
+        field_to_table=f2t, table_rows=rows, table_dim=dims, bags=bags, alpha=float(rng.uniform(0.6, 1.4)))
+    run_step(cfg, steps=2)

@@ -20,6 +20,9 @@ for cfg in (dc.toy(), dc.scaled(dc.wdl(), batch=16, rows_div=2000), dc.scaled(dc
         b, dy = make_batch(cfg, 0, step), make_dy(cfg, 0, step)
         ids, off = to_dev(b)
         emb.forward(ids, off, cfg.batch)
+        for p in range(emb.n_packs):  # (the sort index's reading-O1 views)
+            emb.unique(p)
+            emb.inverse(p)
         emb.backward_update(torch.from_numpy(dy).cuda(), lr=0.05, step=step)
         emb.check()
     torch.cuda.synchronize()
