@@ -159,6 +159,8 @@ def cpu_oracle_baseline(cfg, seconds, openmp=False, max_steps=50):
     from datagen import make_batch, make_dy, table_values_np
 
     oracle.use_openmp(openmp)
+    # every host core this process may use (torchrun pins its workers' OMP_NUM_THREADS to 1)
+    used = oracle.set_threads(host_cpu()[0]) if openmp else 1
     try:
         m = oracle.OracleModel(cfg.field_to_table, cfg.table_rows, cfg.table_dim, cfg.field_col,
                                id_mode=cfg.id_mode, pool=cfg.pool, table_salt=cfg.table_salt)
@@ -190,8 +192,7 @@ def cpu_oracle_baseline(cfg, seconds, openmp=False, max_steps=50):
     finally:
         oracle.use_openmp(False)
     cores, model = host_cpu()
-    used = cores if openmp else 1
-    how = f"OpenMP build on all {cores} host cores" if openmp else "single-threaded"
+    how = f"OpenMP build on {used} threads ({cores} host cores)" if openmp else "single-threaded"
     return {"value": samples / spent, "unit": UNIT, "cores": used, "kind": "oracle", "cpu_model": model,
             "host_cores": cores,
             "sample": f"{steps} full batch(es) of {cfg.name} (B={B}, {cfg.F} fields): fwd over all segments, "
@@ -220,8 +221,8 @@ def run_reference(args):
                        "dims": sorted(set(cfg.table_dim.tolist())), "alpha": cfg.alpha},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
                              "cpu_model": cb["cpu_model"],
-                             "sample": f"{len(per)} full batches of {cfg.name}, OpenMP oracle build on all "
-                                       f"{cb['cores']} host cores"},
+                             "sample": f"{len(per)} full batches of {cfg.name}, OpenMP oracle build on "
+                                       f"{cb['cores']} threads ({cb['host_cores']} host cores)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

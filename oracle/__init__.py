@@ -52,6 +52,14 @@ def use_openmp(on: bool = True):
     _use_openmp = bool(on)
 
 
+def set_threads(n: int) -> int:
+    """Threads of the OpenMP build's loops (torchrun sets OMP_NUM_THREADS=1 for its workers); returns
+    the count the build will use.  The plain build: always 1."""
+    L = lib()
+    L.oracle_set_threads(int(n))
+    return int(L.oracle_get_threads())
+
+
 class Model(C.Structure):
     _fields_ = [("n_fields", C.c_int32), ("n_tables", C.c_int32),
                 ("field_to_table", C.c_void_p), ("table_rows", C.c_void_p),
@@ -75,6 +83,8 @@ _libs = {}
 def lib():
     if _use_openmp not in _libs:
         _libs[_use_openmp] = L = C.CDLL(build(openmp=_use_openmp))
+        L.oracle_set_threads.argtypes = [C.c_int32]
+        L.oracle_get_threads.restype = C.c_int32
         L.oracle_mix64.restype = C.c_uint64
         L.oracle_mix64.argtypes = [C.c_uint64]
         L.oracle_row_of.restype = C.c_int32

@@ -709,4 +709,21 @@ int32_t oracle_fcounter_add(int64_t n, const int64_t *keys, uint64_t *counts) {
     return OR_OK;
 }
 
+/* threads of the OpenMP build's parallel loops (the all-cores baseline): set / read; the plain build
+ * always runs on 1 (no arithmetic here: the loops' results do not depend on the thread count) */
+void oracle_set_threads(int32_t n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+int32_t oracle_get_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
 } /* extern "C" */
