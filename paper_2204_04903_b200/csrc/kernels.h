@@ -197,6 +197,7 @@ struct PoolArgs {
     const int32_t *field_k;      //   [F] index of each field within its pack
     const int32_t *empty_pack;   //   [P] 1 if the pack has an empty segment this step (k_seg_of)
     int64_t n_ids;               // IDs of the step: per-segment ranges are clamped to [0, n_ids)
+    int32_t vec8;                // k_pool_flat: 32-B chunks allowed (rows, output columns 32-B aligned)
 };
 void launch_pool(int D, const PoolArgs &a, int num_sms, cudaStream_t s);
 // k_pool_pipe.cu: pipelined pool for D >= 64 (needs seg_of from launch_seg_of); returns #launches

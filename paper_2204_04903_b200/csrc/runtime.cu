@@ -858,6 +858,13 @@ int picasso::launch_pool_all(picasso_ctx *ctx, PoolArgs pa, float *out, cudaStre
         pa.pack_fields = ctx->pm_fields_d + ctx->pack_first_k[p];
         pa.weight = pa.row_off ? ctx->gbuf : ctx->w[p];
         if ((int64_t)pa.Fp * pa.B == 0) continue;
+        {   // 32-B row / output chunks (k_pool_flat8): local rows, 32-B aligned columns and table
+            bool ok = !pa.row_off && ctx->out_width % 8 == 0 && ((uintptr_t)pa.weight & 31) == 0 &&
+                      ((uintptr_t)out & 31) == 0;
+            for (int32_t k = ctx->pack_first_k[p]; ok && k < ctx->pack_first_k[p + 1]; ++k)
+                ok = ctx->fcol[ctx->pm_fields[k]] % 8 == 0;
+            pa.vec8 = ok;
+        }
         ctx->mark_pack(0, p, true, s);
         if (ctx->pool_kind == 2) {
             n += launch_pool_flat(ctx->pack_dim[p], pa, ctx->num_sms, s);
