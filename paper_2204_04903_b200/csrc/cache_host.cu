@@ -352,6 +352,7 @@ picasso_status ct_hot_keys(picasso_ctx *ctx, int32_t *pack, int64_t *key, int64_
 
 extern "C" picasso_status picasso_hot_cache_refresh(picasso_ctx *ctx, size_t capacity_bytes, void *stream,
                                                     picasso_cache_stats *stats) {
+    NvtxRange nvtx("picasso_hot_cache_refresh");
     if (!ctx) return PICASSO_ERR_INVALID_ARG;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     picasso_status st = check_refresh_args(ctx, capacity_bytes);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool is attached
 
 #include "kernels.h"
 #include "multi.h"
@@ -47,6 +48,14 @@ inline int bits_for(int64_t maxval) {
 
 }  // namespace ctxutil
 using namespace ctxutil;
+
+// NVTX range over one ABI call (Nsight timelines: picasso_fwd / picasso_bwd_update / picasso_refresh)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct picasso_group;
 

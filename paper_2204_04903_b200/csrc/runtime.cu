@@ -630,6 +630,7 @@ static picasso_status fwd_sorted(picasso_ctx *ctx, IndexArgs a, float *out, cuda
 
 extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int64_t *ids, const int32_t *offsets,
                                                     int32_t batch, int64_t n_ids, float *out, void *stream) {
+    NvtxRange nvtx("picasso_fwd");
     if (!ctx || !offsets || (!out && batch > 0) || batch < 0 || n_ids < 0 || (n_ids > 0 && !ids))
         return PICASSO_ERR_INVALID_ARG;
     if (!ctx->bound) return PICASSO_ERR_STATE;
@@ -733,6 +734,7 @@ extern "C" picasso_status picasso_packed_lookup_fwd(picasso_ctx *ctx, const int6
 
 extern "C" picasso_status picasso_packed_lookup_bwd_update(picasso_ctx *ctx, const float *grad_out, float lr,
                                                            int64_t step, void *stream) {
+    NvtxRange nvtx("picasso_bwd_update");
     if (!ctx || step < 1) return PICASSO_ERR_INVALID_ARG;
     if (!ctx->bound || !ctx->fwd_done || ctx->di_active) return PICASSO_ERR_STATE;
     if (!grad_out && ctx->B > 0) return PICASSO_ERR_INVALID_ARG;  // an empty batch has no dY
