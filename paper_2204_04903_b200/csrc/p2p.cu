@@ -7,14 +7,15 @@
 //                  side sizes: no host synchronisation, so a step can be captured in a CUDA graph)
 //   k_p2p_dst_insert : requester side, each unique row's G slot at its owner; owner side, each
 //                  requested key read straight from the requester's send list (NVLink loads)
-//                  into a direct (row, source) table (k_p2p_leaders lists each row once)
+//                  into a direct (row, source) table
 //   k_p2p_gather : gathers the owner's rows and stores them straight into each requester's rows
 //                  buffer at the slot its send layout reserved (NVLink stores): Gather + Shuffle
 //                  + Stitch in one kernel, the transfer overlapping the gather row by row
 //   (segment-sum) : stores each G row at its slot in the owner's memory (NVLink stores:
 //                  segment-sum + gradient Shuffle in one kernel)
-//   k_p2p_update : per owner-unique row, the <= W pushed G rows summed in source-rank order
-//                  (fp64, reading O6') and the optimizer applied
+//   k_p2p_update : per owner position whose source is the row's lowest requesting source (each
+//                  row once), the <= W pushed G rows summed in source-rank order (fp64,
+//                  reading O6') and the optimizer applied
 //   k_p2p_signal / k_p2p_wait : epoch flags in the peers' windows (system-scope release /
 //                  acquire), with a timeout that latches an error instead of hanging
 #include "kernels.h"
@@ -151,7 +152,6 @@ __global__ void __launch_bounds__(1024) k_p2p_tables(P2PArgs a) {
         if (over) atomicOr(a.err, ERR_CAPACITY);
     }
     __syncthreads();
-    if (t < a.P) a.ocount[t] = 0;
     if (t == 0) {  // float layout of the received G rows: pack-major, D_p floats per position
         int64_t f = 0;
         for (int q = 0; q < a.P; ++q) {
@@ -204,38 +204,6 @@ __global__ void __launch_bounds__(256) k_p2p_dst_insert(P2PArgs a) {
     }
 }
 
-// rows requested this step, listed once each (by the lowest requesting source), per pack:
-// olist[pack_ostart[p] + i], i < ocount[p] (order irrelevant: each row's update is independent)
-__global__ void k_p2p_leaders(P2PArgs a) {
-    const int64_t R = *a.R;
-    const int lane = threadIdx.x & 31;
-    // warp-uniform trip count; one atomic per (warp, pack) instead of one per row
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < R;
-         base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t opos = base + lane;
-        int p = 0;
-        int32_t row = 0;
-        bool leader = false;
-        if (opos < R) {
-            while (p + 1 < a.P && a.pack_ostart[p + 1] <= opos) ++p;
-            row = a.lrow[opos];
-            const int32_t src = a.osrc[opos];
-            const int32_t *dt = a.dtab + (a.row_base[p] + row) * a.W;
-            leader = true;
-            for (int s = 0; s < src; ++s) leader = leader && dt[s] < 0;
-        }
-        const unsigned lm = __ballot_sync(0xffffffffu, leader);
-        if (leader) {
-            const unsigned peers = __match_any_sync(lm, p);
-            const int first = __ffs(peers) - 1;
-            int32_t b = 0;
-            if (lane == first) b = atomicAdd(a.ocount + p, __popc(peers));
-            b = __shfl_sync(peers, b, first);
-            a.olist[a.pack_ostart[p] + b + __popc(peers & ((1u << lane) - 1u))] = row;
-        }
-    }
-}
-
 // clears the previous step's direct-table entries (positions of the last forward)
 __global__ void k_p2p_reset(P2PArgs a) {
     const int64_t R = *a.R;
@@ -263,9 +231,13 @@ __global__ void __launch_bounds__(256) k_p2p_gather(P2PArgs a, const float *weig
     }
 }
 
-// Per owned row requested this step (olist), the <= W pushed G rows (in this owner's receive
-// buffer) summed in source-rank order in fp64 (reading O6'), rounded once, Adagrad / lazy Adam.
-// One thread per 16-B chunk of a row; the <= NFW contributions of a chunk are loaded together.
+// Per owner position of the pack (one G row pushed by one source), the row's update is done by
+// the position of its lowest requesting source ("leader"; the others return after reading the
+// row's W table entries): the <= W pushed G rows (in this owner's receive buffer) summed in
+// source-rank order in fp64 (reading O6'), rounded once, Adagrad / lazy Adam.  Walking the
+// positions directly replaces a separate leader-listing pass (one random table read per
+// position fewer, no row list).  One thread per 16-B chunk of a row; the <= NFW table entries
+// and contributions of a chunk are loaded together.
 template <int D, int NFW>
 __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *weight, float *state1,
                                                     float *state2, int opt, float lr, float eps, float beta1,
@@ -275,21 +247,27 @@ __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *
     // pushed G rows may be stale or partial, so the tables and optimizer state are left untouched
     if (__ldcg(a.err) & ERR_PEER_TIMEOUT) return;
     const int64_t o0 = a.pack_ostart[pack];
-    const int64_t n = (int64_t)a.ocount[pack] * V4;
+    const int64_t n = (a.pack_ostart[pack + 1] - o0) * V4;
     const int64_t rb = a.row_base[pack];
     const float *gin = a.peer.ogbuf[a.rank] + a.pack_fbase[pack];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t row = __ldg(a.olist + o0 + e / V4);
+        const int64_t opos = o0 + e / V4;
+        const int32_t row = __ldg(a.lrow + opos);
+        const int32_t src = __ldg(a.osrc + opos);
         const int c = (int)(e % V4);
         const int32_t *dt = a.dtab + (rb + row) * a.W;
-        const int64_t o = (int64_t)row * D + c * 4;
-        float4 x[NFW];
         int32_t op[NFW];
 #pragma unroll
-        for (int s = 0; s < NFW; ++s) {
-            op[s] = s < a.W ? __ldg(dt + s) : -1;
+        for (int s = 0; s < NFW; ++s) op[s] = s < a.W ? __ldcg(dt + s) : -1;
+        bool leader = true;
+#pragma unroll
+        for (int s = 0; s < NFW; ++s) leader = leader && !(s < src && op[s] >= 0);
+        if (!leader) continue;
+        const int64_t o = (int64_t)row * D + c * 4;
+        float4 x[NFW];
+#pragma unroll
+        for (int s = 0; s < NFW; ++s)
             if (op[s] >= 0) x[s] = __ldcg(reinterpret_cast<const float4 *>(gin + (op[s] - o0) * D + c * 4));
-        }
         const float4 w4 = *reinterpret_cast<const float4 *>(weight + o);
         const float4 a4 = *reinterpret_cast<const float4 *>(state1 + o);
         float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -349,9 +327,6 @@ void launch_p2p_wait(const P2PArgs &a, int slot, cudaStream_t s) { k_p2p_wait<<<
 void launch_p2p_tables(const P2PArgs &a, cudaStream_t s) { k_p2p_tables<<<1, 1024, 0, s>>>(a); }
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_dst_insert<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
-}
-void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s) {
-    k_p2p_leaders<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_reset<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);

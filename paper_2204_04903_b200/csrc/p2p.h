@@ -41,8 +41,6 @@ struct P2PArgs {
     int64_t *roff;                 // [max_recv] float offset of the row slot in the source's gbuf
     int32_t *dtab;                 // [rows_total * W] owner position of (owned row, source), or -1
     const int64_t *row_base;       // [P+1] owned rows per pack, prefix
-    int32_t *olist;                // [max_recv] rows requested this step, once each, per pack block
-    int32_t *ocount;               // [P] rows listed per pack
     int64_t *pack_fbase;           // [P+1] float offset of pack p's G rows in this rank's ogbuf
     // requester side (push destinations of its G rows)
     const int32_t *d_total;        // [1] U
@@ -62,7 +60,6 @@ void launch_p2p_wait(const P2PArgs &a, int slot, cudaStream_t s);
 void launch_p2p_tables(const P2PArgs &a, cudaStream_t s);
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s);
-void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s);
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
                        float b1, float b2, float ss, int num_sms, cudaStream_t s);

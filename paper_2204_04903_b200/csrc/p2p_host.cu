@@ -125,8 +125,6 @@ P2PArgs make_p2p_args(picasso_ctx *ctx) {
     a.osrc = mp.opos_map;
     a.roff = mp.rsend_off;
     a.dtab = mp.dtab;
-    a.olist = mp.oslot;     // the hash-dedup scratch of the NCCL driver, unused here
-    a.ocount = mp.od_total;
     a.row_base = mp.row_base_d;
     a.pack_fbase = mp.pack_fbase_d;
     a.d_total = ctx->d_total;
@@ -180,7 +178,6 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
     }
     launch_p2p_tables(a, s);
     launch_p2p_dst_insert(a, ctx->num_sms, s);
-    launch_p2p_leaders(a, ctx->num_sms, s);
     static const bool split = std::getenv("PICASSO_PROF_SPLIT") != nullptr;  // measurement aid
     if (split) ctx->mark(4, false, s);
     if (kil) {  // the pools start on the second stream once the prep is done
@@ -196,7 +193,7 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
         }
     }
     if (!split) ctx->mark(4, false, s);
-    ctx->launches_fwd += 4 + P + nsig;
+    ctx->launches_fwd += 3 + P + nsig;
     PCK(cudaGetLastError());
     return PICASSO_OK;
 }
