@@ -1,3 +1,4 @@
+#include <cstdlib>
 // p2p_host.cu — host orchestration of the row-sharded step over NVLink peer memory.
 //
 //   fwd:  A  dedup + Partition (multi_host.cu)                 -> barrier 0 (send lists ready)
@@ -205,9 +206,19 @@ float adam_step(const picasso_ctx *ctx, float lr, int64_t step) {
     return (float)((double)lr * std::sqrt(bc2) / bc1);
 }
 
+// 32-B chunks when every pack's rows are (the receive buffer's pack blocks then start on 32 B too)
+static bool update_vec8(const picasso_ctx *ctx, int p) {
+    static const bool off = std::getenv("PICASSO_P2P_VEC4") != nullptr;  // measurement aid
+    if (off) return false;
+    for (int32_t d : ctx->pack_dim)
+        if (d % 8) return false;
+    auto al = [](const float *q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 31) == 0; };
+    return al(ctx->w[p]) && al(ctx->s1[p]) && (ctx->opts.opt != 1 || al(ctx->s2[p]));
+}
+
 void p2p_update_pack(picasso_ctx *ctx, const P2PArgs &a, int p, float lr, float ss, cudaStream_t s) {
     launch_p2p_update(ctx->pack_dim[p], a, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr, ctx->opts.eps,
-                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s);
+                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s, update_vec8(ctx, p));
     ctx->launches_bwd += 1;
 }
 

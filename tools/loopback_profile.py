@@ -19,9 +19,9 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="skew")
-    ap.add_argument("--alpha", type=float, default=0.8)
+    ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--world", type=int, default=2)
-    ap.add_argument("--rows-div", type=int, default=4)
+    ap.add_argument("--rows-div", type=int, default=1)
     ap.add_argument("--batch", type=int, default=None)
     args = ap.parse_args()
     import __graft_entry__
@@ -31,7 +31,9 @@ def main():
     from datagen import configs as dc
     from datagen import init_pack_tables_torch, make_batch, make_dy
 
-    cfg = dc.get_config(args.config).replace(alpha=args.alpha)
+    cfg = dc.get_config(args.config)
+    if args.alpha is not None:
+        cfg = cfg.replace(alpha=args.alpha)
     cfg = dc.scaled(cfg, batch=args.batch or cfg.batch, rows_div=args.rows_div)
     W = args.world
     bs = [make_batch(cfg, r, 0) for r in range(W)]
