@@ -231,6 +231,24 @@ __global__ void __launch_bounds__(256) k_p2p_gather(P2PArgs a, const float *weig
     }
 }
 
+// k_p2p_gather with one thread per 32-B chunk (D >= 16, D % 8 == 0, 32-B aligned rows and
+// buffers): 256-bit loads of the owner's row, 256-bit peer stores
+template <int D>
+__global__ void __launch_bounds__(256) k_p2p_gather8(P2PArgs a, const float *weight, int pack) {
+    constexpr int V8 = D / 8;
+    const int64_t o0 = a.pack_ostart[pack], o1 = a.pack_ostart[pack + 1];
+    const int64_t n = (o1 - o0) * V8;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t opos = o0 + e / V8;
+        const int c = (int)(e % V8);
+        const f8 v = ldg_f8(weight + (int64_t)__ldg(a.lrow + opos) * D + c * 8);
+        float *dst = a.peer.gbuf[__ldg(a.osrc + opos)] + __ldg(a.roff + opos) + c * 8;
+        asm volatile("st.global.cg.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "f"(v.v[0]), "f"(v.v[1]),
+                     "f"(v.v[2]), "f"(v.v[3]), "f"(v.v[4]), "f"(v.v[5]), "f"(v.v[6]), "f"(v.v[7])
+                     : "memory");
+    }
+}
+
 // Per owner position of the pack (one G row pushed by one source), the row's update is done by
 // the position of its lowest requesting source ("leader"; the others return after reading the
 // row's W table entries): the <= W pushed G rows (in this owner's receive buffer) summed in
@@ -401,7 +419,20 @@ void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_reset<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
-void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s) {
+void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s,
+                       bool vec8) {
+    if (vec8 && D % 8 == 0 && D >= 16) {
+        switch (D) {
+            case 16: k_p2p_gather8<16><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            case 32: k_p2p_gather8<32><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            case 64: k_p2p_gather8<64><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            case 128: k_p2p_gather8<128><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            case 256: k_p2p_gather8<256><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            case 384: k_p2p_gather8<384><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            case 512: k_p2p_gather8<512><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack); return;
+            default: break;
+        }
+    }
 #define CALL(DD) k_p2p_gather<DD><<<(unsigned)num_sms * 16, 256, 0, s>>>(a, weight, pack)
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL

@@ -60,7 +60,8 @@ void launch_p2p_wait(const P2PArgs &a, int slot, cudaStream_t s);
 void launch_p2p_tables(const P2PArgs &a, cudaStream_t s);
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s);
-void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s);
+void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s,
+                       bool vec8 = false);
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
                        float b1, float b2, float ss, int num_sms, cudaStream_t s, bool vec8 = false);
 

@@ -167,6 +167,16 @@ bool interleaved(const picasso_ctx *ctx) {
 bool slot_end(const picasso_ctx *ctx, int p) { return p + 1 == ctx->P || ctx->pack_slot[p + 1] != ctx->pack_slot[p]; }
 
 // ---- C': owner side --------------------------------------------------------------------------
+// 32-B chunks when every pack's rows are (the receive buffer's pack blocks then start on 32 B too)
+static bool rows_vec8(const picasso_ctx *ctx, int p) {
+    static const bool off = std::getenv("PICASSO_P2P_VEC4") != nullptr;  // measurement aid
+    if (off) return false;
+    for (int32_t d : ctx->pack_dim)
+        if (d % 8) return false;
+    auto al = [](const float *q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 31) == 0; };
+    return al(ctx->w[p]) && al(ctx->s1[p]) && (ctx->opts.opt != 1 || al(ctx->s2[p]));
+}
+
 picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
     const int P = ctx->P;
     const P2PArgs a = make_p2p_args(ctx);
@@ -187,7 +197,7 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
     }
     int nsig = 0;
     for (int p = 0; p < P; ++p) {
-        launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s);
+        launch_p2p_gather(ctx->pack_dim[p], a, ctx->w[p], p, ctx->num_sms, s, rows_vec8(ctx, p));
         if (kil && slot_end(ctx, p)) {  // the slot's rows are in every requester's buffer
             signal_group(ctx, 1, ctx->pack_slot[p], s);
             ++nsig;
@@ -206,19 +216,9 @@ float adam_step(const picasso_ctx *ctx, float lr, int64_t step) {
     return (float)((double)lr * std::sqrt(bc2) / bc1);
 }
 
-// 32-B chunks when every pack's rows are (the receive buffer's pack blocks then start on 32 B too)
-static bool update_vec8(const picasso_ctx *ctx, int p) {
-    static const bool off = std::getenv("PICASSO_P2P_VEC4") != nullptr;  // measurement aid
-    if (off) return false;
-    for (int32_t d : ctx->pack_dim)
-        if (d % 8) return false;
-    auto al = [](const float *q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 31) == 0; };
-    return al(ctx->w[p]) && al(ctx->s1[p]) && (ctx->opts.opt != 1 || al(ctx->s2[p]));
-}
-
 void p2p_update_pack(picasso_ctx *ctx, const P2PArgs &a, int p, float lr, float ss, cudaStream_t s) {
     launch_p2p_update(ctx->pack_dim[p], a, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr, ctx->opts.eps,
-                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s, update_vec8(ctx, p));
+                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s, rows_vec8(ctx, p));
     ctx->launches_bwd += 1;
 }
 
