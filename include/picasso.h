@@ -229,7 +229,8 @@ picasso_status picasso_last_error(picasso_ctx *ctx, char *msg, size_t len);
  *   picasso_get_unique : pack keys of pack p in first-occurrence order (int64 [U_p])
  *   picasso_get_inverse: per occurrence of pack p's key stream (pack fields in ascending
  *                        field order, then b, then j) its index into unique (int32 [N_p])
- * After a sort-indexed forward (world == 1) the step itself numbers rows by key; these two
+ * After a sort-indexed forward (world == 1, or world > 1 with the peer-memory exchange) the
+ * step itself numbers rows by key; these two
  * first-occurrence views (reading O1) are built from the sorted items on the first call after
  * the forward (a few extra kernels on the ctx's last stream), valid until the next forward. */
 picasso_status picasso_get_unique(picasso_ctx *ctx, int32_t pack, int64_t *dst, int64_t cap, int64_t *n);
@@ -323,7 +324,8 @@ picasso_status picasso_get_send_counts(picasso_ctx *ctx, int64_t *host_counts);
 /* Partition of the last forward (world > 1; tests, synchronises): the local rows (key div W,
  * reading O3) this rank requested from `owner` for pack `pack`, in send order — the pack's
  * unique keys with key mod W == owner in first-occurrence order (PAPER.md L211 Partition,
- * SPEC.md L113-118; = oracle_partition's list).  Hot keys (HybridHash) are not sent.  dst: host
+ * SPEC.md L113-118; = oracle_partition's list; after a sort-indexed step with the peer-memory
+ * exchange the same rows in ascending order).  Hot keys (HybridHash) are not sent.  dst: host
  * int64 [cap]; n: the list length. */
 picasso_status picasso_get_send_list(picasso_ctx *ctx, int32_t owner, int32_t pack, int64_t *dst, int64_t cap,
                                      int64_t *n);

@@ -237,6 +237,10 @@ struct picasso_ctx {
     // arrays gathered through run_uid — no uid transpose (PICASSO_INDEX=hash: off)
     bool sort_w = false;
     bool w_runorder = false;      // the last row-sharded forward indexed by sort
+    // ... and exchanged in run order (peer-memory exchange: the order inside a bucket is free, so
+    // uid = run index, the inverse comes from k_si_final, no views / run_uid / run gather; the
+    // reading-O1 views only on request).  The NCCL exchange keeps first-occurrence order (O2).
+    bool w_runx = false;
     int64_t sort_min_ids_w = (int64_t)1 << 20;
     int32_t *run_uid = nullptr, *hs_run = nullptr, *dr_run = nullptr;  // [N]
     int64_t *ro_run = nullptr, *do_run = nullptr;                        // [N]

@@ -334,6 +334,11 @@ __global__ void __launch_bounds__(kSiThreads, 3) k_si_final(SortIdxArgs a, const
         }
         out_r[k] = r;
     }
+    if (a.inv_run) {  // the run-order inverse (row-sharded peer-memory steps): position -> row
+#pragma unroll
+        for (int k = 0; k < kSiItems; ++k)
+            if (i0 + k < a.N) a.inv_run[(uint32_t)x[k]] = out_r[k];
+    }
     const int lt = threadIdx.x * kSiItems;
 #pragma unroll
     for (int k = 0; k < kSiItems; ++k) {

@@ -138,6 +138,7 @@ struct SortIdxArgs {
     int32_t *inverse;              // [N] uid of each position
     unsigned long long *unique_gkey;  // [U] key of each uid (first-occurrence order)
     int32_t *run_uid;              // [U] (optional) uid of each row in run order
+    int32_t *inv_run;              // [N] (optional) k_si_final: row (run index) of each position
 };
 struct SortIdxPlan {
     int passes;

@@ -58,7 +58,7 @@ static MultiArgs multi_args(picasso_ctx *ctx) {
     m.pack_key_off = ctx->pack_key_off_d;
     m.d_total = ctx->d_total;
     m.pack_ustart = ctx->pack_ustart;
-    m.unique_gkey = ctx->unique_gkey;
+    m.unique_gkey = ctx->w_runorder && ctx->w_runx ? ctx->run_keys() : ctx->unique_gkey;  // (uid = run index)
     m.bkey = mp.bkey;
     m.bval = mp.bval;
     m.bhist = mp.bhist;
@@ -161,6 +161,8 @@ picasso_status mfwd_a(picasso_ctx *ctx, const int64_t *ids, const int32_t *offse
 // segment-sum indexes by row, gathered from their uid-indexed originals
 static void run_order_args(picasso_ctx *ctx, UpdateArgs &u, cudaStream_t s) {
     if (!ctx->w_runorder) return;
+    u.unique_gkey = ctx->run_keys();
+    if (ctx->w_runx) return;  // rows were numbered in run order from the start
     launch_run_gather(ctx->run_uid, ctx->d_total, ctx->N, u.hslot, ctx->hs_run, u.row_off, ctx->ro_run, u.dst_rank,
                       ctx->dr_run, u.dst_off, ctx->do_run, ctx->num_sms, s);
     ctx->launches_bwd += 1;

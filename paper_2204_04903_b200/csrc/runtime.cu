@@ -555,11 +555,17 @@ picasso_status w_sorted_index(picasso_ctx *ctx, const int64_t *ids, const int32_
                   ctx->seg_limit, ctx->err, &ka);
     SortIdxArgs x = sort_idx_args(ctx, ids, B, N);
     x.run_uid = ctx->run_uid;
+    ctx->w_runx = ctx->mp.p2p && std::getenv("PICASSO_W_UIDORDER") == nullptr;  // (measurement aid)
+    if (ctx->w_runx) x.inv_run = ctx->inverse;
     const SortIdxPlan plan = make_sortidx_plan(N, ctx->sort_key_bits, ctx->num_sms);
     uint64_t *sorted = nullptr, *other = nullptr;
     ctx->launches_fwd += 2 + launch_sort_index(x, plan, reinterpret_cast<uint64_t *>(ctx->k_a),
                                                reinterpret_cast<uint64_t *>(ctx->k_b), &sorted, &other, s);
-    ctx->launches_fwd += launch_sort_views(x, sorted, s);
+    ctx->views_ready = false;
+    if (!ctx->w_runx) {
+        ctx->launches_fwd += launch_sort_views(x, sorted, s);
+        ctx->views_ready = true;
+    }
     ctx->su = reinterpret_cast<int32_t *>(other);
     ctx->sseg = ctx->su + N;
     ctx->sorted_items = sorted;
@@ -569,7 +575,8 @@ picasso_status w_sorted_index(picasso_ctx *ctx, const int64_t *ids, const int32_
 
 // the reading-O1 views of a sorted step (Unique in first-occurrence order, inverse), on request
 static picasso_status ensure_views(picasso_ctx *ctx) {
-    if (!ctx->sort_step || ctx->views_ready) return PICASSO_OK;
+    const bool sorted = ctx->world > 1 ? ctx->w_runorder : ctx->sort_step;
+    if (!sorted || ctx->views_ready) return PICASSO_OK;
     const SortIdxArgs x = sort_idx_args(ctx, nullptr, ctx->B, ctx->N);
     launch_sort_views(x, ctx->sorted_items, ctx->last_stream);
     CK(cudaGetLastError());

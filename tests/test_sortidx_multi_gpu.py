@@ -1,6 +1,7 @@
-"""The row-sharded step indexed by sort (world > 1; csrc/k_sortidx.cu through mfwd_a): Unique /
-inverse from the sort's reading-O1 views, the backward in run order with its per-row destinations
-gathered through run -> uid, no uid transpose.  The loopback parity cases of test_multi_gpu.py and
+"""The row-sharded step indexed by sort (world > 1; csrc/k_sortidx.cu through mfwd_a), no uid
+transpose: with the peer-memory exchange the whole step in run order (send lists in ascending local
+row, Unique / inverse views built on request); with the NCCL exchange Unique / inverse from the
+sort's reading-O1 views and the backward's per-row destinations gathered through run -> uid.  The loopback parity cases of test_multi_gpu.py and
 test_hot_cache_gpu.py re-run with every step sort-indexed (PICASSO_SORT_MIN_IDS_W=0): forward,
 Unique, send lists, owner uniques and shards against the oracle, as on the hash path."""
 import pytest
