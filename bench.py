@@ -814,7 +814,9 @@ def main():
                        "launch": (f"cuda_graph (one captured step per batch, {args.nbatches} distinct batches "
                                   "replayed round robin)") if use_graph else "eager",
                        "nbatches": args.nbatches,
-                       "index": ("sort" if sort_idx else "hash") if world == 1 else "hash (row-sharded)",
+                       "index": ("sort" if sort_idx else "hash") if world == 1 else (
+                           ("sort (row-sharded, run order)" if emb.exchange == "p2p" else "sort (row-sharded)") if sort_idx and last_b.n_ids >= int(
+                               env("PICASSO_SORT_MIN_IDS_W", str(1 << 20))) else "hash (row-sharded)"),
                        "ids_per_step": int(last_b.n_ids), "unique_per_step": int(sum(U_by_pack))},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
