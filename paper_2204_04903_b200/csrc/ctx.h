@@ -361,7 +361,7 @@ struct picasso_ctx {
         blk_cnt = c.take<int32_t>(nblk);
         blk_off = c.take<int32_t>(nblk);
         d_total = c.take<int32_t>(1);
-        long_cnt = c.take<int32_t>(P);
+        long_cnt = c.take<int32_t>(P + 1);  // (+ the k_si_heads ticket)
         err = c.take<int>(1);
         seg_limit = c.take<int32_t>(1);
         unique_gkey = c.take<unsigned long long>(N);

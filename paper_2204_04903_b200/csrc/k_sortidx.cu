@@ -18,8 +18,8 @@
 //        k_seg_of derived from the IDs (position -> field -> table row -> pack key).
 //   k_si_heads   : run heads (first item of each key): per tile head count, last head, and the
 //                  heads before each pack's first item
-//   k_si_scan    : one block: run index base per tile, last head before each tile (runs that
-//                  cross tiles), U, per-pack row ranges, the split backward's G layout
+//   (scan)       : in k_si_heads' last CTA: run index base per tile, last head before each tile
+//                  (runs that cross tiles), U, per-pack row ranges, the split backward's G layout
 //   k_si_final   : per sorted item: its row (run index) and segment, row starts and keys, and the
 //                  backward's equal-cost tiles (the k_csr_tiles partition)
 //
@@ -212,7 +212,56 @@ __global__ void __launch_bounds__(kSiThreads, 3) k_si_down(SortIdxArgs a, const 
     }
 }
 
-// run heads per sorted tile: head count, last head, heads before each pack's first item
+// one block of NT threads: run bases, carries, U, pack row ranges, G layout (the tile arrays are
+// read through L2: the last k_si_heads CTA runs this on the other CTAs' stores)
+template <int NT>
+__device__ __forceinline__ void si_scan_body(const SortIdxArgs &a, int64_t nblk,
+                                             typename cub::BlockScan<int32_t, NT>::TempStorage &tmp) {
+    using BS = cub::BlockScan<int32_t, NT>;
+    __shared__ int32_t c_run, c_last;
+    if (threadIdx.x == 0) {
+        c_run = 0;
+        c_last = -1;
+    }
+    __syncthreads();
+    for (int64_t base = 0; base < nblk; base += NT) {
+        const int64_t i = base + threadIdx.x;
+        const bool v = i < nblk;
+        int32_t e, agg;
+        BS(tmp).ExclusiveSum(v ? __ldcg(a.tile_heads + i) : 0, e, agg);
+        if (v) a.run_base[i] = c_run + e;
+        __syncthreads();
+        if (threadIdx.x == 0) c_run += agg;
+        // last head before each tile (head indices rise with the tile: a running max)
+        BS(tmp).ExclusiveScan(v ? __ldcg(a.tile_last + i) : -1, e, cub::Max(), agg);
+        if (v) a.carry[i] = threadIdx.x == 0 ? c_last : max(c_last, e);
+        __syncthreads();
+        if (threadIdx.x == 0) c_last = max(c_last, agg);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int32_t U = c_run;
+        *a.d_total = U;
+        int64_t gb = 0;
+        int32_t prev = 0;
+        for (int p = 0; p <= a.P; ++p) {  // a pack's first row: run base of its first item's tile + heads before it
+            const int32_t G0 = a.pack_gstart[p];
+            const int32_t u = G0 < a.N ? a.run_base[G0 / kTile] + __ldcg(a.pack_hb + p) : U;
+            a.pack_ustart[p] = u;
+            if (p > 0) {
+                a.pack_gbase[p - 1] = gb;
+                gb += (int64_t)(u - prev) * a.pack_dim[p - 1];
+            }
+            prev = u;
+        }
+        a.pack_gbase[a.P] = gb;
+        a.ustart[U] = (int32_t)a.N;
+    }
+}
+
+// run heads per sorted tile: head count, last head, heads before each pack's first item; the
+// last CTA to finish (ticket a.long_cnt[P], zeroed with the step's counters) then scans the tile
+// arrays (si_scan_body) — no separate single-block launch on the chain
 __global__ void __launch_bounds__(kSiThreads) k_si_heads(SortIdxArgs a, const uint64_t *s) {
     using BS = cub::BlockScan<int32_t, kSiThreads>;
     using BR = cub::BlockReduce<int32_t, kSiThreads>;
@@ -220,6 +269,7 @@ __global__ void __launch_bounds__(kSiThreads) k_si_heads(SortIdxArgs a, const ui
         typename BS::TempStorage scan;
         typename BR::TempStorage red;
     } tmp;
+    __shared__ bool s_last;
     const int64_t i0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kSiItems;
     uint64_t x[kSiItems];
     load8(s, i0, a.N, x);
@@ -234,63 +284,32 @@ __global__ void __launch_bounds__(kSiThreads) k_si_heads(SortIdxArgs a, const ui
         a.tile_heads[blockIdx.x] = tot;
         a.tile_last[blockIdx.x] = last;
     }
-    if (i0 >= a.N) return;
-    // packs whose first item falls in [i0, i0 + 8): their first row = heads before it
-    int lo = 0, hi = a.P + 1;  // first p with pack_gstart[p] >= i0
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a.pack_gstart + mid) < i0) lo = mid + 1; else hi = mid;
+    if (i0 < a.N) {
+        // packs whose first item falls in [i0, i0 + 8): their first row = heads before it
+        int lo = 0, hi = a.P + 1;  // first p with pack_gstart[p] >= i0
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(a.pack_gstart + mid) < i0) lo = mid + 1; else hi = mid;
+        }
+        for (int p = lo; p <= a.P; ++p) {
+            const int64_t G0 = __ldg(a.pack_gstart + p);
+            if (G0 >= i0 + kSiItems || G0 >= a.N) break;
+            a.pack_hb[p] = hb + __popc(hm & ((1u << (int)(G0 - i0)) - 1u));
+        }
     }
-    for (int p = lo; p <= a.P; ++p) {
-        const int64_t G0 = __ldg(a.pack_gstart + p);
-        if (G0 >= i0 + kSiItems || G0 >= a.N) break;
-        a.pack_hb[p] = hb + __popc(hm & ((1u << (int)(G0 - i0)) - 1u));
-    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.long_cnt + a.P, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    si_scan_body<kSiThreads>(a, gridDim.x, tmp.scan);
 }
 
-// one block: run bases, carries, U, pack row ranges, G layout
+// one block: the same scan for an empty step (no k_si_heads)
 __global__ void __launch_bounds__(1024) k_si_scan(SortIdxArgs a, int64_t nblk) {
-    using BS = cub::BlockScan<int32_t, 1024>;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ int32_t c_run, c_last;
-    if (threadIdx.x == 0) {
-        c_run = 0;
-        c_last = -1;
-    }
-    __syncthreads();
-    for (int64_t base = 0; base < nblk; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        const bool v = i < nblk;
-        int32_t e, agg;
-        BS(tmp).ExclusiveSum(v ? a.tile_heads[i] : 0, e, agg);
-        if (v) a.run_base[i] = c_run + e;
-        __syncthreads();
-        if (threadIdx.x == 0) c_run += agg;
-        // last head before each tile (head indices rise with the tile: a running max)
-        BS(tmp).ExclusiveScan(v ? a.tile_last[i] : -1, e, cub::Max(), agg);
-        if (v) a.carry[i] = threadIdx.x == 0 ? c_last : max(c_last, e);
-        __syncthreads();
-        if (threadIdx.x == 0) c_last = max(c_last, agg);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const int32_t U = c_run;
-        *a.d_total = U;
-        int64_t gb = 0;
-        int32_t prev = 0;
-        for (int p = 0; p <= a.P; ++p) {  // a pack's first row: run base of its first item's tile + heads before it
-            const int32_t G0 = a.pack_gstart[p];
-            const int32_t u = G0 < a.N ? a.run_base[G0 / kTile] + a.pack_hb[p] : U;
-            a.pack_ustart[p] = u;
-            if (p > 0) {
-                a.pack_gbase[p - 1] = gb;
-                gb += (int64_t)(u - prev) * a.pack_dim[p - 1];
-            }
-            prev = u;
-        }
-        a.pack_gbase[a.P] = gb;
-        a.ustart[U] = (int32_t)a.N;
-    }
+    __shared__ typename cub::BlockScan<int32_t, 1024>::TempStorage tmp;
+    si_scan_body<1024>(a, nblk, tmp);
 }
 
 // tile of cost c in [0, C): floor(c * nte / C) in double (monotone in c; nte <= C, so consecutive
@@ -594,7 +613,7 @@ int launch_sort_index(SortIdxArgs a, const SortIdxPlan &plan, uint64_t *buf_a, u
     const int64_t nblk = (a.N + kTile - 1) / kTile;
     uint64_t *bufs[2] = {buf_a, buf_b};
     const uint64_t *cur = nullptr;
-    cudaMemsetAsync(a.long_cnt, 0, sizeof(int32_t) * a.P, s);
+    cudaMemsetAsync(a.long_cnt, 0, sizeof(int32_t) * (a.P + 1), s);  // (+ the k_si_heads ticket)
     if (a.N > 0) {
         for (int p = 0; p < plan.passes; ++p) {
             uint64_t *out = bufs[p & 1];
@@ -609,10 +628,9 @@ int launch_sort_index(SortIdxArgs a, const SortIdxPlan &plan, uint64_t *buf_a, u
         int32_t *su = reinterpret_cast<int32_t *>(cur == buf_a ? buf_b : buf_a);
         a.su = su;
         a.sseg = su + a.N;
-        k_si_heads<<<(unsigned)nblk, kSiThreads, 0, s>>>(a, cur);
-        k_si_scan<<<1, 1024, 0, s>>>(a, nblk);
+        k_si_heads<<<(unsigned)nblk, kSiThreads, 0, s>>>(a, cur);  // (+ the scan, in its last CTA)
         k_si_final<<<(unsigned)nblk, kSiThreads, 0, s>>>(a, cur);
-        launches += 3;
+        launches += 2;
     } else {
         cudaMemsetAsync(a.d_total, 0, sizeof(int32_t), s);
         k_si_scan<<<1, 1024, 0, s>>>(a, 0);  // empty packs, ustart[0] = 0

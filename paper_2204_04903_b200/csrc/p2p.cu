@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(1024) k_p2p_tables(P2PArgs a) {
         if (over) atomicOr(a.err, ERR_CAPACITY);
     }
     __syncthreads();
+    if (t < a.P) a.ocount[t] = 0;
     if (t == 0) {  // float layout of the received G rows: pack-major, D_p floats per position
         int64_t f = 0;
         for (int q = 0; q < a.P; ++q) {
@@ -201,6 +202,44 @@ __global__ void __launch_bounds__(256) k_p2p_dst_insert(P2PArgs a) {
         a.roff[opos] = sb[k].rroff + j * __ldg(a.pack_dim + p);
         a.dtab[(a.row_base[p] + lr) * a.W + src] = (int32_t)opos;
         if (a.fcnt) atomicAdd(a.fcnt + a.fcnt_off[p] + lr, 1u);  // FCounter (Alg. 1)
+    }
+}
+
+// W > 2: rows requested this step, listed once each (by the lowest requesting source), per pack:
+// olist[pack_ostart[p] + i], i < ocount[p] (order irrelevant: each row's update is independent).
+// With more sources per row the update then walks rows, not positions (at W = 2 the update's own
+// leader test is cheaper than this pass: see k_p2p_update)
+__global__ void k_p2p_leaders(P2PArgs a) {
+    const int64_t R = *a.R;
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count; one atomic per (warp, pack) instead of one per row
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < R;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t opos = base + lane;
+        int p = 0;
+        int32_t row = 0;
+        bool leader = false;
+        if (opos < R) {
+            while (p + 1 < a.P && a.pack_ostart[p + 1] <= opos) ++p;
+            row = a.lrow[opos];
+            const int32_t src = a.osrc[opos];
+            const int32_t *dt = a.dtab + (a.row_base[p] + row) * a.W;
+            int32_t op[kP2PMaxW];
+#pragma unroll
+            for (int s = 0; s < kP2PMaxW; ++s) op[s] = s < src ? __ldcg(dt + s) : -1;  // independent loads
+            leader = true;
+#pragma unroll
+            for (int s = 0; s < kP2PMaxW; ++s) leader = leader & (op[s] < 0);
+        }
+        const unsigned lm = __ballot_sync(0xffffffffu, leader);
+        if (leader) {
+            const unsigned peers = __match_any_sync(lm, p);
+            const int first = __ffs(peers) - 1;
+            int32_t b = 0;
+            if (lane == first) b = atomicAdd(a.ocount + p, __popc(peers));
+            b = __shfl_sync(peers, b, first);
+            a.olist[a.pack_ostart[p] + b + __popc(peers & ((1u << lane) - 1u))] = row;
+        }
     }
 }
 
@@ -256,7 +295,7 @@ __global__ void __launch_bounds__(256) k_p2p_gather8(P2PArgs a, const float *wei
 // positions directly replaces a separate leader-listing pass (one random table read per
 // position fewer, no row list).  One thread per 16-B chunk of a row; the <= NFW table entries
 // and contributions of a chunk are loaded together.
-template <int D, int NFW>
+template <int D, int NFW, bool LIST>
 __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *weight, float *state1,
                                                     float *state2, int opt, float lr, float eps, float beta1,
                                                     float beta2, float adam_ss) {
@@ -265,13 +304,13 @@ __global__ void __launch_bounds__(256) k_p2p_update(P2PArgs a, int pack, float *
     // pushed G rows may be stale or partial, so the tables and optimizer state are left untouched
     if (__ldcg(a.err) & ERR_PEER_TIMEOUT) return;
     const int64_t o0 = a.pack_ostart[pack];
-    const int64_t n = (a.pack_ostart[pack + 1] - o0) * V4;
+    const int64_t n = (LIST ? (int64_t)a.ocount[pack] : a.pack_ostart[pack + 1] - o0) * V4;
     const int64_t rb = a.row_base[pack];
     const float *gin = a.peer.ogbuf[a.rank] + a.pack_fbase[pack];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t opos = o0 + e / V4;
-        const int32_t row = __ldg(a.lrow + opos);
-        const int32_t src = __ldg(a.osrc + opos);
+        const int32_t row = LIST ? __ldg(a.olist + opos) : __ldg(a.lrow + opos);
+        const int32_t src = LIST ? 0 : __ldg(a.osrc + opos);  // (LIST: every listed row is updated)
         const int c = (int)(e % V4);
         const int32_t *dt = a.dtab + (rb + row) * a.W;
         int32_t op[NFW];
@@ -338,20 +377,20 @@ __device__ __forceinline__ f8 ldcg_f8(const float *p) {
 // k_p2p_update with one thread per 32-B chunk (D % 8 == 0, every pack's rows and the receive
 // buffer 32-B aligned): 256-bit loads and stores, half the memory instructions of the 16-B form
 // for the same bytes in flight.  Same arithmetic, same order.
-template <int D, int NFW>
+template <int D, int NFW, bool LIST>
 __global__ void __launch_bounds__(256) k_p2p_update8(P2PArgs a, int pack, float *weight, float *state1,
                                                      float *state2, int opt, float lr, float eps, float beta1,
                                                      float beta2, float adam_ss) {
     constexpr int V8 = D / 8;
     if (__ldcg(a.err) & ERR_PEER_TIMEOUT) return;
     const int64_t o0 = a.pack_ostart[pack];
-    const int64_t n = (a.pack_ostart[pack + 1] - o0) * V8;
+    const int64_t n = (LIST ? (int64_t)a.ocount[pack] : a.pack_ostart[pack + 1] - o0) * V8;
     const int64_t rb = a.row_base[pack];
     const float *gin = a.peer.ogbuf[a.rank] + a.pack_fbase[pack];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t opos = o0 + e / V8;
-        const int32_t row = __ldg(a.lrow + opos);
-        const int32_t src = __ldg(a.osrc + opos);
+        const int32_t row = LIST ? __ldg(a.olist + opos) : __ldg(a.lrow + opos);
+        const int32_t src = LIST ? 0 : __ldg(a.osrc + opos);  // (LIST: every listed row is updated)
         const int c = (int)(e % V8);
         const int32_t *dt = a.dtab + (rb + row) * a.W;
         int32_t op[NFW];
@@ -416,6 +455,9 @@ void launch_p2p_tables(const P2PArgs &a, cudaStream_t s) { k_p2p_tables<<<1, 102
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_dst_insert<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
+void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s) {
+    k_p2p_leaders<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
+}
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s) {
     k_p2p_reset<<<(unsigned)num_sms * 4, 256, 0, s>>>(a);
 }
@@ -437,8 +479,9 @@ void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, i
     PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
 }
-void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
-                       float b1, float b2, float ss, int num_sms, cudaStream_t s, bool vec8) {
+template <bool L>
+static void update_dispatch(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr,
+                            float eps, float b1, float b2, float ss, int num_sms, cudaStream_t s, bool vec8) {
     const unsigned grid = (unsigned)num_sms * 16;
     if (vec8 && D % 8 == 0 && D >= 16) {  // (D = 8: one thread per row measured slower than two)
 #define DISPATCH8(D, CALL)          \
@@ -453,15 +496,15 @@ void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, f
         default: break;             \
     }
         if (a.W <= 2) {
-#define CALL(DD) k_p2p_update8<DD, 2><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update8<DD, 2, L><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
             DISPATCH8(D, CALL)
 #undef CALL
         } else if (a.W <= 4) {
-#define CALL(DD) k_p2p_update8<DD, 4><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update8<DD, 4, L><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
             DISPATCH8(D, CALL)
 #undef CALL
         } else {
-#define CALL(DD) k_p2p_update8<DD, 8><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update8<DD, 8, L><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
             DISPATCH8(D, CALL)
 #undef CALL
         }
@@ -469,18 +512,24 @@ void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, f
         return;
     }
     if (a.W <= 2) {
-#define CALL(DD) k_p2p_update<DD, 2><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update<DD, 2, L><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
         PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
     } else if (a.W <= 4) {
-#define CALL(DD) k_p2p_update<DD, 4><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update<DD, 4, L><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
         PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
     } else {
-#define CALL(DD) k_p2p_update<DD, 8><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
+#define CALL(DD) k_p2p_update<DD, 8, L><<<grid, 256, 0, s>>>(a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss)
         PICASSO_DISPATCH_D(D, CALL)
 #undef CALL
     }
+}
+
+void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
+                       float b1, float b2, float ss, int num_sms, cudaStream_t s, bool vec8, bool list) {
+    if (list) update_dispatch<true>(D, a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss, num_sms, s, vec8);
+    else update_dispatch<false>(D, a, pack, w, s1, s2, opt, lr, eps, b1, b2, ss, num_sms, s, vec8);
 }
 
 }  // namespace picasso

@@ -40,6 +40,8 @@ struct P2PArgs {
     int32_t *osrc;                 // [max_recv] source rank per owner position
     int64_t *roff;                 // [max_recv] float offset of the row slot in the source's gbuf
     int32_t *dtab;                 // [rows_total * W] owner position of (owned row, source), or -1
+    int32_t *olist;                // [max_recv] (W > 2) rows requested this step, once each, per pack block
+    int32_t *ocount;               // [P] (W > 2) rows listed per pack
     const int64_t *row_base;       // [P+1] owned rows per pack, prefix
     int64_t *pack_fbase;           // [P+1] float offset of pack p's G rows in this rank's ogbuf
     // requester side (push destinations of its G rows)
@@ -59,10 +61,12 @@ void launch_p2p_signal(const P2PArgs &a, int slot, cudaStream_t s);
 void launch_p2p_wait(const P2PArgs &a, int slot, cudaStream_t s);
 void launch_p2p_tables(const P2PArgs &a, cudaStream_t s);
 void launch_p2p_dst_insert(const P2PArgs &a, int num_sms, cudaStream_t s);
+void launch_p2p_leaders(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_reset(const P2PArgs &a, int num_sms, cudaStream_t s);
 void launch_p2p_gather(int D, const P2PArgs &a, const float *weight, int pack, int num_sms, cudaStream_t s,
                        bool vec8 = false);
 void launch_p2p_update(int D, const P2PArgs &a, int pack, float *w, float *s1, float *s2, int opt, float lr, float eps,
-                       float b1, float b2, float ss, int num_sms, cudaStream_t s, bool vec8 = false);
+                       float b1, float b2, float ss, int num_sms, cudaStream_t s, bool vec8 = false,
+                       bool list = false);
 
 }  // namespace picasso

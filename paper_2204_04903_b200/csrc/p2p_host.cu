@@ -126,6 +126,8 @@ P2PArgs make_p2p_args(picasso_ctx *ctx) {
     a.osrc = mp.opos_map;
     a.roff = mp.rsend_off;
     a.dtab = mp.dtab;
+    a.olist = mp.oslot;     // (W > 2) the hash-dedup scratch of the NCCL driver, unused here
+    a.ocount = mp.od_total;
     a.row_base = mp.row_base_d;
     a.pack_fbase = mp.pack_fbase_d;
     a.d_total = ctx->d_total;
@@ -167,6 +169,16 @@ bool interleaved(const picasso_ctx *ctx) {
 bool slot_end(const picasso_ctx *ctx, int p) { return p + 1 == ctx->P || ctx->pack_slot[p + 1] != ctx->pack_slot[p]; }
 
 // ---- C': owner side --------------------------------------------------------------------------
+// W > 2: a leader-listing pass, then the update walks the listed rows; at W = 2 the update walks
+// the owner positions and elects each row's leader itself (C2 loopback: the listing pass cost more
+// than the update's extra lanes at W = 2; at N = 4 the fused form's idle lanes cost more: update
+// 0.074 -> 0.096 ms vs owner phase 0.132 -> 0.120 ms)
+static bool owner_list(const picasso_ctx *ctx) {
+    static const char *e = std::getenv("PICASSO_P2P_LIST");  // measurement aid: 0 / 1 forces
+    if (e) return e[0] == '1';
+    return ctx->world > 2;
+}
+
 // 32-B chunks when every pack's rows are (the receive buffer's pack blocks then start on 32 B too)
 static bool rows_vec8(const picasso_ctx *ctx, int p) {
     static const bool off = std::getenv("PICASSO_P2P_VEC4") != nullptr;  // measurement aid
@@ -189,6 +201,7 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
     }
     launch_p2p_tables(a, s);
     launch_p2p_dst_insert(a, ctx->num_sms, s);
+    if (owner_list(ctx)) launch_p2p_leaders(a, ctx->num_sms, s);
     static const bool split = std::getenv("PICASSO_PROF_SPLIT") != nullptr;  // measurement aid
     if (split) ctx->mark(4, false, s);
     if (kil) {  // the pools start on the second stream once the prep is done
@@ -204,7 +217,7 @@ picasso_status p2p_c(picasso_ctx *ctx, cudaStream_t s, bool kil) {
         }
     }
     if (!split) ctx->mark(4, false, s);
-    ctx->launches_fwd += 3 + P + nsig;
+    ctx->launches_fwd += 3 + (owner_list(ctx) ? 1 : 0) + P + nsig;
     PCK(cudaGetLastError());
     return PICASSO_OK;
 }
@@ -218,7 +231,7 @@ float adam_step(const picasso_ctx *ctx, float lr, int64_t step) {
 
 void p2p_update_pack(picasso_ctx *ctx, const P2PArgs &a, int p, float lr, float ss, cudaStream_t s) {
     launch_p2p_update(ctx->pack_dim[p], a, p, ctx->w[p], ctx->s1[p], ctx->s2[p], ctx->opts.opt, lr, ctx->opts.eps,
-                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s, rows_vec8(ctx, p));
+                      ctx->opts.beta1, ctx->opts.beta2, ss, ctx->num_sms, s, rows_vec8(ctx, p), owner_list(ctx));
     ctx->launches_bwd += 1;
 }
 
